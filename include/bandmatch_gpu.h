@@ -1,0 +1,235 @@
+/*
+ * bandmatch_gpu.h -- C ABI of the B200-native cascade-hashing matcher.
+ *
+ * Drop-in boundary for the hot path of the reference "bandmatch" library
+ * (/root/reference/proj; citations are file:line in that tree).  The entry
+ * points are what the reference's C++ API for this path binds to:
+ *
+ *   reference                                          | this ABI
+ *   ---------------------------------------------------+------------------------------
+ *   HashFunctions / make_hash_functions                | bmg_create (planes are host-
+ *     include/bandmatch/hashmatch.hpp:19-34,             |   generated and passed in),
+ *     src/hashmatch.cpp:53-69                           |   bmg_make_hash_functions
+ *   DeviceArena::upload / evict + DeviceBackend hooks  | bmg_upload / bmg_evict /
+ *     engine.hpp:20-44, 98-104; engine.cpp:18-40,       |   bmg_arena_stats
+ *     438-444, 491-494                                  |
+ *   execute_plan row body: centering mean + codes      | bmg_row / bmg_row_mean /
+ *     engine.cpp:433-465                                |   bmg_codes
+ *   compute_codes  hashmatch.hpp:58-61, .cpp:71-100     | bmg_compute_codes
+ *   match_pair     hashmatch.hpp:82-90, .cpp:102-211    | bmg_match_pair, bmg_match
+ *   execute_plan   engine.hpp:121-131, .cpp:411-527     | bmg_execute_plan
+ *   bandmatch::Error codes  common.hpp:13-26            | bmg_status / bmg_status_name
+ *
+ * Conventions (mirroring the reference):
+ *   - descriptors are float[n][128], row-major (Descriptor = std::array<float,128>,
+ *     features.hpp:23-44), i.e. &fs.descriptors[0].v[0];
+ *   - coarse codes are uint32[n][tables] (bucket ids), fine codes are
+ *     uint64[n][ceil(fine_bits/64)] with fine bit b in word b/64, bit b%64
+ *     (HashCodeSet, hashmatch.hpp:36-56);
+ *   - matches are int32 (query_idx, train_idx) pairs in ascending query_idx
+ *     (PairMatches, hashmatch.hpp:70-75); image pairs are (lower id, higher id)
+ *     with query = lower id (IdPair, common.hpp:50-59; engine.cpp:469-472);
+ *   - no C++ exception crosses this boundary: every call returns a bmg_status;
+ *     bmg_status_name() gives the reference's stable error code string and
+ *     bmg_last_error() the message.
+ *
+ * Results are bit-exact with the reference on the same inputs (hash codes,
+ * bucket ids, Hamming ranking and the final match index sets).
+ */
+#ifndef BANDMATCH_GPU_H
+#define BANDMATCH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BMG_DIM 128 /* kDescriptorDim, features.hpp:14 */
+#define BMG_ABI_VERSION 1
+
+typedef enum {
+  BMG_OK = 0,
+  BMG_INVALID_ARGUMENT = 1,   /* "InvalidArgument"  */
+  BMG_HASH_MISMATCH = 2,      /* "HashMismatch"     */
+  BMG_CAPACITY_EXCEEDED = 3,  /* "CapacityExceeded" */
+  BMG_NOT_RESIDENT = 4,       /* "NotResident"      */
+  BMG_CUDA_ERROR = 5,         /* "CudaError"        */
+  BMG_OUT_OF_MEMORY = 6,      /* "OutOfMemory"      */
+  BMG_UNSUPPORTED = 7         /* "Unsupported"      */
+} bmg_status;
+
+typedef struct bmg_context bmg_context;
+typedef struct bmg_result bmg_result;
+
+/* HashParams, hashmatch.hpp:11-15 (defaults 6 / 8 / 128). */
+typedef struct {
+  int32_t tables;
+  int32_t coarse_bits;
+  int32_t fine_bits;
+} bmg_hash_params;
+
+/* MatchParams, hashmatch.hpp:77-80 (defaults 8 / 0.5). */
+typedef struct {
+  int32_t k_nearest;
+  double ratio;
+} bmg_match_params;
+
+typedef struct {
+  int32_t device;                 /* CUDA ordinal */
+  bmg_hash_params hash;
+  const float* coarse_planes;     /* [tables][coarse_bits][128] (HashFunctions::coarse) */
+  const float* fine_planes;       /* [fine_bits][128]          (HashFunctions::fine)   */
+  uint64_t function_seed;         /* HashFunctions::seed, tags every code set */
+  uint64_t capacity_units;        /* DeviceArena capacity in descriptor units */
+} bmg_config;
+
+/* HashCodeSet view, hashmatch.hpp:36-56 */
+typedef struct {
+  uint64_t image_id;
+  uint64_t function_seed;
+  bmg_hash_params params;
+  uint64_t count;
+  const uint32_t* coarse;         /* [count][tables] */
+  const uint64_t* fine;           /* [count][ceil(fine_bits/64)] */
+} bmg_code_set;
+
+/* FeatureSet view (descriptors only; keypoints stay on the host) */
+typedef struct {
+  uint64_t image_id;
+  const float* descriptors;       /* [count][128] */
+  uint64_t count;
+} bmg_feature_view;
+
+/* DeviceArena counters, engine.hpp:24-31 */
+typedef struct {
+  uint64_t capacity, occupancy, peak_occupancy, uploads, evictions, units_uploaded;
+  uint64_t resident_count;
+} bmg_arena_stats;
+
+/* SchedulePlan flattened (mbr.hpp:26-68).  Rows are listed iteration by
+ * iteration; row r's block pairs are pairs[2*row_pair_offsets[r] ..
+ * 2*row_pair_offsets[r+1]) as (a,b) with a<b in block order, its
+ * `needed` set is derived as row_images ∪ all blocks' col_images
+ * (engine.cpp:434-436) and passed explicitly (ascending), and its eviction
+ * directives are evict_ids[row_evict_offsets[r] .. row_evict_offsets[r+1]). */
+typedef struct {
+  uint64_t n_iterations;
+  const uint64_t* rows_per_iteration;  /* [n_iterations] */
+  uint64_t n_rows;
+  const uint64_t* row_needed_offsets;  /* [n_rows+1] */
+  const uint64_t* needed_ids;
+  const uint64_t* row_pair_offsets;    /* [n_rows+1] */
+  const uint64_t* pairs;               /* [2*total pairs] */
+  const uint64_t* row_evict_offsets;   /* [n_rows+1] */
+  const uint64_t* evict_ids;
+} bmg_plan;
+
+/* Called on the executor's collector thread for every matched pair as soon
+ * as its matches are in host memory: the hand-off point to host-side
+ * verification (VerifyPool::push, engine.cpp:478-479). */
+typedef void (*bmg_pair_callback)(void* user, uint64_t query_image, uint64_t train_image,
+                                  const int32_t* matches, uint64_t n_matches);
+
+/* DeviceBackend hooks (engine.hpp:98-104), called after each successful
+ * arena transition. */
+typedef void (*bmg_upload_hook)(void* user, uint64_t image_id, uint64_t units);
+typedef void (*bmg_evict_hook)(void* user, uint64_t image_id);
+
+typedef struct {
+  bmg_match_params match;
+  bmg_pair_callback on_pair;      /* may be NULL */
+  void* on_pair_user;
+  bmg_upload_hook on_upload;      /* may be NULL */
+  bmg_evict_hook on_evict;        /* may be NULL */
+  void* hook_user;
+} bmg_execute_options;
+
+/* ---- status ------------------------------------------------------------ */
+const char* bmg_status_name(int status);              /* "InvalidArgument", ... */
+const char* bmg_last_error(void);                     /* thread-local message */
+int bmg_abi_version(void);
+
+/* ---- host helpers mirroring the reference's host-side generation ------- */
+/* seed_for, common.hpp:38-45 */
+uint64_t bmg_seed_for(uint64_t root, const char* stage);
+/* make_hash_functions, hashmatch.cpp:53-69 (libstdc++ <random>, host only) */
+int bmg_make_hash_functions(uint64_t seed, const bmg_hash_params* params, float* coarse_out,
+                            float* fine_out);
+
+/* ---- context ----------------------------------------------------------- */
+int bmg_create(const bmg_config* config, bmg_context** out);
+int bmg_destroy(bmg_context* ctx);
+int bmg_synchronize(bmg_context* ctx);
+
+/* ---- DeviceArena (HBM descriptor cache) --------------------------------- */
+/* Uploads `count` descriptors for `image_id` (no-op when resident, engine.cpp:19);
+ * CapacityExceeded when occupancy would exceed capacity (:20-24).  The copy is
+ * asynchronous; `desc` must stay valid until the next bmg_row/bmg_synchronize. */
+int bmg_upload(bmg_context* ctx, uint64_t image_id, const float* desc, uint64_t count);
+int bmg_evict(bmg_context* ctx, uint64_t image_id);        /* NotResident (:34-36) */
+int bmg_is_resident(bmg_context* ctx, uint64_t image_id);  /* 1 / 0 */
+int bmg_arena_stats_get(bmg_context* ctx, bmg_arena_stats* out);
+
+/* ---- row body (engine.cpp:446-465) --------------------------------------- */
+/* Computes the centering mean over `needed` (ascending ids, all resident)
+ * unless `mean` is non-NULL, then the codes and bucket tables of every
+ * needed image relative to it.  Replaces the previous row's codes. */
+int bmg_row(bmg_context* ctx, const uint64_t* needed, uint64_t n_needed, const float* mean);
+int bmg_row_mean(bmg_context* ctx, float mean_out[BMG_DIM]);
+/* Parity hook: copy the current row's codes of a needed image to the host. */
+int bmg_codes(bmg_context* ctx, uint64_t image_id, uint32_t* coarse_out, uint64_t* fine_out);
+/* match_pair over resident images of the current row: writes per-pair match
+ * offsets [n_pairs+1] and (query_idx, train_idx) int32 pairs; capacity is in
+ * pairs (int32 pairs, i.e. matches_out holds 2*capacity ints). */
+int bmg_match(bmg_context* ctx, const uint64_t* query_ids, const uint64_t* train_ids,
+              uint64_t n_pairs, const bmg_match_params* params, uint64_t* offsets_out,
+              int32_t* matches_out, uint64_t capacity);
+
+/* ---- stateless mirrors of the reference functions ------------------------ */
+/* compute_codes(fs, hf, mean), hashmatch.cpp:71-100 */
+int bmg_compute_codes(bmg_context* ctx, const float* desc, uint64_t count,
+                      const float mean[BMG_DIM], uint32_t* coarse_out, uint64_t* fine_out);
+/* match_pair(qf, qc, tf, tc, mp), hashmatch.cpp:102-211; HashMismatch on
+ * seed / params / count disagreement, InvalidArgument on k_nearest < 1. */
+int bmg_match_pair(bmg_context* ctx, const float* qdesc, const bmg_code_set* qc,
+                   const float* tdesc, const bmg_code_set* tc, const bmg_match_params* params,
+                   int32_t* matches_out, uint64_t* n_matches_out);
+
+/* ---- full executor (engine.cpp:411-527, verification off) ---------------- */
+int bmg_execute_plan(bmg_context* ctx, const bmg_plan* plan, const bmg_feature_view* features,
+                     uint64_t n_features, const bmg_execute_options* options,
+                     bmg_result** out);
+/* ExecutionResult accessors: pairs sorted by IdPair (engine.cpp:506-512). */
+uint64_t bmg_result_pair_count(const bmg_result* r);
+uint64_t bmg_result_match_count(const bmg_result* r);
+/* pair_ids[2*n_pairs], offsets[n_pairs+1], matches[2*n_matches] */
+int bmg_result_copy(const bmg_result* r, uint64_t* pair_ids, uint64_t* offsets, int32_t* matches);
+/* PipelineMetrics, engine.hpp:57-78: pairs_matched, initial_matches, uploads,
+ * evictions, units_uploaded, peak_occupancy (6 values) + wall seconds */
+int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wall_s_out);
+/* per-iteration metrics: pairs, uploads, units_uploaded (3 values each) */
+uint64_t bmg_result_iteration_count(const bmg_result* r);
+int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out[3]);
+void bmg_result_free(bmg_result* r);
+
+/* ---- instrumentation ------------------------------------------------------ */
+/* Number of kernels this context has launched so far. */
+uint64_t bmg_launch_count(bmg_context* ctx);
+/* Device time of the most recent bmg_execute_plan / bmg_match, per kernel
+ * class ("mean", "codes", "fixup", "tables", "match", "compact"): total
+ * milliseconds and launch count, measured with CUDA events on the launching
+ * stream.  Enabled by bmg_set_profiling(ctx, 1). */
+int bmg_set_profiling(bmg_context* ctx, int enabled);
+int bmg_kernel_time(bmg_context* ctx, const char* kernel_class, double* total_ms,
+                    uint64_t* launches);
+/* Number of projection bits / ratio decisions resolved by the FP64 fixup
+ * path in the last row / match (diagnostics). */
+int bmg_fixup_counts(bmg_context* ctx, uint64_t* code_bits, uint64_t* rerank_queries);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BANDMATCH_GPU_H */

@@ -1,0 +1,345 @@
+// ref_shim.cpp -- extern "C" wrapper around the UNMODIFIED reference library
+// (bandmatch, /root/reference/proj/src), compiled in place by oracle/Makefile
+// into oracle/_ref/libbandmatch_ref.so.
+//
+// TEST INFRASTRUCTURE ONLY: used to pin the C restatement (oracle.c) and to
+// generate tests/golden fixtures in this container, and as the timed CPU
+// baseline ("kind": "reference") in bench.py.  Never linked by the product.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bandmatch/engine.hpp"
+#include "bandmatch/features.hpp"
+#include "bandmatch/hashmatch.hpp"
+#include "bandmatch/mbr.hpp"
+#include "bandmatch/view_graph.hpp"
+
+using namespace bandmatch;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int status_of(const std::string& code) {
+  if (code == "InvalidArgument") return 1;
+  if (code == "HashMismatch") return 2;
+  if (code == "CapacityExceeded") return 3;
+  if (code == "NotResident") return 4;
+  if (code == "FormatError") return 5;
+  if (code == "BudgetTooSmall") return 6;
+  if (code == "EmptyGraph") return 7;
+  return 99;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return status_of(e.code());
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 98;
+  }
+}
+
+HashFunctions hf_from(uint64_t seed, int tables, int cb, int fb, const float* coarse,
+                      const float* fine) {
+  HashFunctions hf;
+  hf.params = {tables, cb, fb};
+  hf.seed = seed;
+  hf.coarse.assign(coarse, coarse + static_cast<size_t>(tables) * cb * kDescriptorDim);
+  hf.fine.assign(fine, fine + static_cast<size_t>(fb) * kDescriptorDim);
+  return hf;
+}
+
+FeatureSet fs_from(uint64_t id, const float* desc, uint64_t n) {
+  FeatureSet fs;
+  fs.image_id = id;
+  fs.descriptors.resize(n);
+  fs.keypoints.resize(n);
+  if (n) std::memcpy(fs.descriptors.data(), desc, n * sizeof(Descriptor));
+  return fs;
+}
+
+HashCodeSet cs_from(const FeatureSet& fs, uint64_t seed, int tables, int cb, int fb,
+                    const uint32_t* coarse, const uint64_t* fine) {
+  HashCodeSet cs;
+  cs.image_id = fs.image_id;
+  cs.function_seed = seed;
+  cs.params = {tables, cb, fb};
+  cs.count = fs.size();
+  cs.fine_words = (fb + 63) / 64;
+  cs.coarse.assign(coarse, coarse + cs.count * tables);
+  cs.fine.assign(fine, fine + cs.count * cs.fine_words);
+  return cs;
+}
+
+void put_matches(const PairMatches& pm, int32_t* out, uint64_t* count) {
+  for (size_t i = 0; i < pm.matches.size(); ++i) {
+    out[2 * i] = pm.matches[i].first;
+    out[2 * i + 1] = pm.matches[i].second;
+  }
+  *count = pm.matches.size();
+}
+
+struct Synth {
+  SyntheticDataset data;
+};
+
+struct FeatureTable {
+  std::map<ImageId, FeatureSet> features;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_last_error.c_str(); }
+
+uint64_t ref_seed_for(uint64_t root, const char* tag) { return seed_for(root, tag); }
+
+int ref_make_hash_functions(uint64_t seed, int tables, int cb, int fb, float* coarse_out,
+                            float* fine_out) {
+  return guarded([&] {
+    const HashFunctions hf = make_hash_functions(seed, {tables, cb, fb});
+    std::copy(hf.coarse.begin(), hf.coarse.end(), coarse_out);
+    std::copy(hf.fine.begin(), hf.fine.end(), fine_out);
+  });
+}
+
+int ref_compute_codes(const float* desc, uint64_t n, uint64_t seed, int tables, int cb, int fb,
+                      const float* coarse, const float* fine, const float* mean,
+                      uint32_t* coarse_out, uint64_t* fine_out) {
+  return guarded([&] {
+    const HashFunctions hf = hf_from(seed, tables, cb, fb, coarse, fine);
+    const FeatureSet fs = fs_from(0, desc, n);
+    std::array<float, kDescriptorDim> m;
+    std::copy(mean, mean + kDescriptorDim, m.begin());
+    const HashCodeSet cs = compute_codes(fs, hf, m);
+    std::copy(cs.coarse.begin(), cs.coarse.end(), coarse_out);
+    std::copy(cs.fine.begin(), cs.fine.end(), fine_out);
+  });
+}
+
+int ref_match_pair(const float* qdesc, uint64_t nq, const uint32_t* qcoarse,
+                   const uint64_t* qfine, const float* tdesc, uint64_t nt,
+                   const uint32_t* tcoarse, const uint64_t* tfine, uint64_t seed, int tables,
+                   int cb, int fb, int k, double ratio, int32_t* out, uint64_t* count) {
+  return guarded([&] {
+    const FeatureSet qf = fs_from(1, qdesc, nq);
+    const FeatureSet tf = fs_from(2, tdesc, nt);
+    const HashCodeSet qc = cs_from(qf, seed, tables, cb, fb, qcoarse, qfine);
+    const HashCodeSet tc = cs_from(tf, seed, tables, cb, fb, tcoarse, tfine);
+    MatchParams mp;
+    mp.k_nearest = k;
+    mp.ratio = ratio;
+    put_matches(match_pair(qf, qc, tf, tc, mp), out, count);
+  });
+}
+
+int ref_brute_force_match(const float* qdesc, uint64_t nq, const float* tdesc, uint64_t nt,
+                          double ratio, int32_t* out, uint64_t* count) {
+  return guarded([&] {
+    put_matches(brute_force_match(fs_from(1, qdesc, nq), fs_from(2, tdesc, nt), ratio), out,
+                count);
+  });
+}
+
+// ---- synthetic scenes (features.cpp:68-197) --------------------------------
+
+void* ref_synth_create(int n_images, int ppi, int band, double sigma, double outlier_fraction,
+                       uint64_t seed) {
+  Synth* s = new Synth;
+  const int rc = guarded([&] {
+    SyntheticScene sc;
+    sc.n_images = n_images;
+    sc.points_per_image = ppi;
+    sc.overlap_band = band;
+    sc.noise_sigma = sigma;
+    sc.outlier_fraction = outlier_fraction;
+    sc.seed = seed;
+    s->data = generate_synthetic(sc);
+  });
+  if (rc != 0) {
+    delete s;
+    return nullptr;
+  }
+  return s;
+}
+uint64_t ref_synth_count(void* h, int i) { return static_cast<Synth*>(h)->data.images.at(i).size(); }
+void ref_synth_copy(void* h, int i, float* out) {
+  const FeatureSet& fs = static_cast<Synth*>(h)->data.images.at(i);
+  if (fs.size()) std::memcpy(out, fs.descriptors.data(), fs.size() * sizeof(Descriptor));
+}
+void ref_synth_copy_keypoints(void* h, int i, float* out) {
+  const FeatureSet& fs = static_cast<Synth*>(h)->data.images.at(i);
+  for (size_t k = 0; k < fs.size(); ++k) {
+    out[4 * k] = fs.keypoints[k].x;
+    out[4 * k + 1] = fs.keypoints[k].y;
+    out[4 * k + 2] = fs.keypoints[k].scale;
+    out[4 * k + 3] = fs.keypoints[k].orientation;
+  }
+}
+uint64_t ref_synth_pair_count(void* h) { return static_cast<Synth*>(h)->data.true_pairs.size(); }
+void ref_synth_pairs(void* h, uint64_t* out) {
+  const auto& p = static_cast<Synth*>(h)->data.true_pairs;
+  for (size_t i = 0; i < p.size(); ++i) {
+    out[2 * i] = p[i].a;
+    out[2 * i + 1] = p[i].b;
+  }
+}
+void ref_synth_free(void* h) { delete static_cast<Synth*>(h); }
+
+// ---- block schedule (mbr.cpp:321-376, 378-419) -----------------------------
+
+int ref_iterate_schedule_to_file(const uint64_t* ids, uint64_t n_ids, const uint64_t* pairs,
+                                 uint64_t n_pairs, int size_blk, int size_gpu,
+                                 const char* path) {
+  return guarded([&] {
+    std::vector<IdPair> ps;
+    for (uint64_t i = 0; i < n_pairs; ++i) ps.emplace_back(pairs[2 * i], pairs[2 * i + 1]);
+    const ViewGraph g = make_view_graph(std::vector<ImageId>(ids, ids + n_ids), ps);
+    write_plan(path, iterate_schedule(g, size_blk, size_gpu));
+  });
+}
+
+// ---- feature table + execute_plan (engine.cpp:411-527) ---------------------
+
+void* ref_features_create() { return new FeatureTable; }
+void ref_features_add(void* h, uint64_t id, const float* desc, uint64_t n) {
+  static_cast<FeatureTable*>(h)->features[id] = fs_from(id, desc, n);
+}
+void ref_features_free(void* h) { delete static_cast<FeatureTable*>(h); }
+
+// Runs the reference execute_plan as shipped (verification off, one matcher
+// thread) and returns its matches flattened in result order:
+// pair_ids[2*p], offsets[p+1], matches[2*m].  Buffers must be large enough.
+int ref_execute_plan(const char* plan_path, void* features, uint64_t hash_seed, int tables,
+                     int cb, int fb, int k, double ratio, uint64_t capacity_units,
+                     uint64_t* pair_ids, uint64_t* offsets, int32_t* matches,
+                     uint64_t* n_pairs_out, double* wall_s_out, uint64_t* counters_out) {
+  return guarded([&] {
+    const SchedulePlan plan = read_plan(plan_path);
+    const HashFunctions hf = make_hash_functions(hash_seed, {tables, cb, fb});
+    DeviceArena arena(capacity_units);
+    ExecuteOptions opts;
+    opts.match.k_nearest = k;
+    opts.match.ratio = ratio;
+    opts.verify.enabled = false;
+    const ExecutionResult res =
+        execute_plan(plan, static_cast<FeatureTable*>(features)->features, hf, arena, opts);
+    uint64_t m = 0;
+    offsets[0] = 0;
+    for (size_t p = 0; p < res.matches.size(); ++p) {
+      pair_ids[2 * p] = res.matches[p].query_image;
+      pair_ids[2 * p + 1] = res.matches[p].train_image;
+      for (const auto& [qi, ti] : res.matches[p].matches) {
+        matches[2 * m] = qi;
+        matches[2 * m + 1] = ti;
+        ++m;
+      }
+      offsets[p + 1] = m;
+    }
+    *n_pairs_out = res.matches.size();
+    *wall_s_out = res.metrics.wall_time_s;
+    counters_out[0] = res.metrics.pairs_matched;
+    counters_out[1] = res.metrics.initial_matches;
+    counters_out[2] = res.metrics.uploads;
+    counters_out[3] = res.metrics.evictions;
+    counters_out[4] = res.metrics.units_uploaded;
+    counters_out[5] = res.metrics.peak_occupancy;
+  });
+}
+
+// Baseline (ii) "host cores": the same reference functions (row mean restated
+// from engine.cpp:446-461, compute_codes, match_pair) with the independent
+// per-image code computations and per-pair matches of each row spread over
+// `threads` std::threads.  Output equals execute_plan's (pairs keyed by
+// IdPair).  Returns wall seconds; `max_pairs` > 0 bounds the sample (rows are
+// taken in plan order until the bound is reached).
+int ref_execute_plan_threaded(const char* plan_path, void* features, uint64_t hash_seed,
+                              int tables, int cb, int fb, int k, double ratio, int threads,
+                              uint64_t max_pairs, uint64_t* pairs_done, uint64_t* total_matches,
+                              double* wall_s_out) {
+  return guarded([&] {
+    const SchedulePlan plan = read_plan(plan_path);
+    const HashFunctions hf = make_hash_functions(hash_seed, {tables, cb, fb});
+    const auto& feats = static_cast<FeatureTable*>(features)->features;
+    MatchParams mp;
+    mp.k_nearest = k;
+    mp.ratio = ratio;
+    const int T = std::max(1, threads);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::map<IdPair, PairMatches> results;
+    uint64_t done = 0;
+    for (const ScheduleIteration& it : plan.iterations) {
+      for (const BlockRow& row : it.rows) {
+        if (max_pairs && done >= max_pairs) break;
+        std::set<ImageId> needed(row.row_images.begin(), row.row_images.end());
+        for (const ScheduleBlock& blk : row.blocks)
+          needed.insert(blk.col_images.begin(), blk.col_images.end());
+        std::array<double, kDescriptorDim> acc{};
+        std::size_t total = 0;
+        for (ImageId id : needed) {
+          const FeatureSet& fs = feats.at(id);
+          for (const Descriptor& d : fs.descriptors)
+            for (int c = 0; c < kDescriptorDim; ++c) acc[c] += d.v[c];
+          total += fs.size();
+        }
+        std::array<float, kDescriptorDim> mean{};
+        if (total > 0)
+          for (int c = 0; c < kDescriptorDim; ++c)
+            mean[c] = static_cast<float>(acc[c] / static_cast<double>(total));
+        std::vector<ImageId> ids(needed.begin(), needed.end());
+        std::vector<HashCodeSet> codes(ids.size());
+        {
+          std::atomic<size_t> next{0};
+          std::vector<std::thread> pool;
+          for (int w = 0; w < T; ++w)
+            pool.emplace_back([&] {
+              for (size_t i; (i = next++) < ids.size();)
+                codes[i] = compute_codes(feats.at(ids[i]), hf, mean);
+            });
+          for (auto& th : pool) th.join();
+        }
+        std::map<ImageId, const HashCodeSet*> by_id;
+        for (size_t i = 0; i < ids.size(); ++i) by_id[ids[i]] = &codes[i];
+        std::vector<IdPair> pairs;
+        for (const ScheduleBlock& blk : row.blocks)
+          pairs.insert(pairs.end(), blk.pairs.begin(), blk.pairs.end());
+        std::vector<PairMatches> out(pairs.size());
+        {
+          std::atomic<size_t> next{0};
+          std::vector<std::thread> pool;
+          for (int w = 0; w < T; ++w)
+            pool.emplace_back([&] {
+              for (size_t i; (i = next++) < pairs.size();)
+                out[i] = match_pair(feats.at(pairs[i].a), *by_id.at(pairs[i].a),
+                                    feats.at(pairs[i].b), *by_id.at(pairs[i].b), mp);
+            });
+          for (auto& th : pool) th.join();
+        }
+        for (size_t i = 0; i < pairs.size(); ++i) results[pairs[i]] = std::move(out[i]);
+        done += pairs.size();
+      }
+    }
+    const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
+    uint64_t m = 0;
+    for (const auto& [p, pm] : results) m += pm.matches.size();
+    *pairs_done = done;
+    *total_matches = m;
+    *wall_s_out = dt.count();
+  });
+}
+
+}  // extern "C"

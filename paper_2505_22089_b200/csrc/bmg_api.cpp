@@ -1,0 +1,1150 @@
+// bmg_api.cpp -- host runtime behind the C ABI (include/bandmatch_gpu.h).
+//
+// Owns, per CUDA device context:
+//   * the HBM descriptor arena (DeviceArena semantics, engine.cpp:18-40) on a
+//     stream-ordered memory pool, fed by asynchronous H2D copies on a copy
+//     stream (pinned sources go straight to the copy engine, pageable ones
+//     through a double-buffered pinned staging ring);
+//   * the per-row scratch (codes + bucket tables of every resident image,
+//     recomputed per row because codes are relative to the row mean,
+//     engine.cpp:446-465);
+//   * the match scratch and a device-resident result log that rows append to
+//     without host synchronisation; execute_plan reads it back once.
+// No exception crosses the ABI: every entry point returns a bmg_status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "../../include/bandmatch_gpu.h"
+#include "bmg_internal.h"
+
+namespace bmg {
+
+uint64_t seed_for(uint64_t root, std::string_view stage);
+bool valid_hash_params(const bmg_hash_params& p);
+void make_planes(uint64_t seed, const bmg_hash_params& p, float* coarse, float* fine);
+
+namespace {
+
+struct Failure {
+  int status;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int status, std::string msg) { throw Failure{status, std::move(msg)}; }
+
+#define BMG_CUDA(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      fail(e_ == cudaErrorMemoryAllocation ? BMG_OUT_OF_MEMORY : BMG_CUDA_ERROR,        \
+           std::string(#x) + ": " + cudaGetErrorString(e_));                           \
+  } while (0)
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BMG_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.msg;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return BMG_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BMG_CUDA_ERROR;
+  }
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (p) {
+      BMG_CUDA(cudaDeviceSynchronize());
+      cudaFree(p);
+      p = nullptr;
+      cap = 0;
+    }
+    n = align_up(std::max<size_t>(n, 256), 1 << 20);
+    BMG_CUDA(cudaMalloc(&p, n));
+    cap = n;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Pinned host ring for small metadata uploads (tables of pointers, work
+// lists): a slice stays valid until the ring wraps, and a wrap synchronises
+// the streams that could still be reading it.
+struct PinnedRing {
+  char* base = nullptr;
+  size_t cap = 0, head = 0;
+  void init(size_t n) {
+    BMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&base), n));
+    cap = n;
+  }
+  template <typename T>
+  T* alloc(size_t count, cudaStream_t a, cudaStream_t b) {
+    size_t bytes = align_up(std::max<size_t>(count * sizeof(T), 16), 256);
+    if (bytes > cap) fail(BMG_OUT_OF_MEMORY, "metadata exceeds the pinned staging ring");
+    if (head + bytes > cap) {
+      BMG_CUDA(cudaStreamSynchronize(a));
+      BMG_CUDA(cudaStreamSynchronize(b));
+      head = 0;
+    }
+    T* out = reinterpret_cast<T*>(base + head);
+    head += bytes;
+    return out;
+  }
+  void release() {
+    if (base) cudaFreeHost(base);
+    base = nullptr;
+  }
+};
+
+struct ArenaImage {
+  float* d = nullptr;
+  uint64_t n = 0;
+};
+
+struct Timer {
+  std::string cls;
+  cudaEvent_t a, b;
+};
+
+struct RowLayout {
+  size_t coarse_off, fine_off, offsets_off, cursor_off, slots_off;
+};
+
+}  // namespace
+
+}  // namespace bmg
+
+struct bmg_context {
+  int device = 0;
+  bmg_hash_params hp{};
+  bmg::HashDev hd{};
+  uint64_t seed = 0;
+  bmg::DevBuf planes_t, planes, plane_norm;
+  // arena (DeviceArena, engine.hpp:20-44)
+  uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
+  std::map<uint64_t, bmg::ArenaImage> resident;
+  cudaStream_t s_copy = nullptr, s_comp = nullptr;
+  cudaMemPool_t pool = nullptr;
+  cudaEvent_t ev_uploaded = nullptr;
+  bool pending_upload = false;
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  int stage_i = 0;
+  size_t stage_bytes = 0;
+  bmg::PinnedRing ring;
+  // row state
+  std::vector<uint64_t> row_ids;
+  std::unordered_map<uint64_t, int> row_slot;
+  std::vector<bmg::ImgDev> row_imgs;
+  bool row_valid = false;
+  bmg::DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag;
+  // match state
+  bmg::DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq, d_res_off, d_res, d_running;
+  // temporaries for the stateless entry points
+  bmg::DevBuf d_tmp_desc, d_tmp_codes;
+  // instrumentation
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::vector<bmg::Timer> timers;
+  std::vector<cudaEvent_t> free_events;
+};
+
+struct bmg_result {
+  std::vector<uint64_t> pair_ids;
+  std::vector<uint64_t> offsets;
+  std::vector<int32_t> matches;
+  uint64_t counters[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<uint64_t> iterations;  // 3 per iteration
+  double wall_s = 0.0;
+};
+
+namespace bmg {
+namespace {
+
+using Ctx = bmg_context;
+
+cudaEvent_t take_event(Ctx& c) {
+  if (!c.free_events.empty()) {
+    cudaEvent_t e = c.free_events.back();
+    c.free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  BMG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+struct Timed {
+  Ctx& c;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  const char* cls;
+  Timed(Ctx& ctx, const char* k, cudaStream_t st) : c(ctx), s(st), cls(k) {
+    if (c.profiling) {
+      a = take_event(c);
+      b = take_event(c);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Timed() {
+    if (a) {
+      cudaEventRecord(b, s);
+      c.timers.push_back({cls, a, b});
+    }
+  }
+};
+
+void set_device(Ctx& c) { BMG_CUDA(cudaSetDevice(c.device)); }
+
+void check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(BMG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+int padded_words(int fw) {
+  int p = 1;
+  while (p < fw) p <<= 1;
+  return p;
+}
+
+int bit_width(uint32_t v) {
+  int b = 0;
+  while (v) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
+// ---- arena ----------------------------------------------------------------
+
+void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
+                      attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned || bytes == 0) {
+    if (bytes) BMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.s_copy));
+    return;
+  }
+  // pageable: chunk through two pinned buffers so the host memcpy of chunk
+  // k+1 overlaps the DMA of chunk k
+  const char* s = static_cast<const char*>(src);
+  char* d = static_cast<char*>(dst);
+  for (size_t off = 0; off < bytes; off += c.stage_bytes) {
+    const size_t sz = std::min(c.stage_bytes, bytes - off);
+    const int i = c.stage_i;
+    BMG_CUDA(cudaEventSynchronize(c.stage_ev[i]));
+    std::memcpy(c.stage[i], s + off, sz);
+    BMG_CUDA(cudaMemcpyAsync(d + off, c.stage[i], sz, cudaMemcpyHostToDevice, c.s_copy));
+    BMG_CUDA(cudaEventRecord(c.stage_ev[i], c.s_copy));
+    c.stage_i ^= 1;
+  }
+}
+
+void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
+  if (c.resident.count(id)) return;  // engine.cpp:19
+  if (c.occupancy + n > c.capacity)
+    fail(BMG_CAPACITY_EXCEEDED, "uploading image " + std::to_string(id) + " (" + std::to_string(n) +
+                                    " units) would raise occupancy to " +
+                                    std::to_string(c.occupancy + n) + " of " +
+                                    std::to_string(c.capacity));
+  if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
+  ArenaImage im;
+  im.n = n;
+  BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
+                           c.s_copy));
+  stage_h2d(c, im.d, desc, n * 512);
+  c.resident.emplace(id, im);
+  c.occupancy += n;
+  c.peak = std::max(c.peak, c.occupancy);
+  ++c.uploads;
+  c.units_uploaded += n;
+  c.pending_upload = true;
+}
+
+void arena_evict(Ctx& c, uint64_t id) {
+  const auto it = c.resident.find(id);
+  if (it == c.resident.end())
+    fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
+  // stream-ordered free after every kernel already queued on the compute stream
+  BMG_CUDA(cudaFreeAsync(it->second.d, c.s_comp));
+  c.occupancy -= it->second.n;
+  c.resident.erase(it);
+  ++c.evictions;
+  if (c.row_slot.count(id)) c.row_valid = false;
+}
+
+void join_uploads(Ctx& c) {
+  if (!c.pending_upload) return;
+  BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
+  BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_uploaded, 0));
+  c.pending_upload = false;
+}
+
+// ---- row body -------------------------------------------------------------
+
+// Lays out codes + tables for `descs` (device pointers, counts) in the row
+// scratch, computes the mean (unless given) and launches codes, fixup and
+// bucket-table kernels on the compute stream.
+void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
+                       const float* mean_host, const float* mean_dev, bool compute_mean) {
+  const HashDev& h = c.hd;
+  const int n_imgs = static_cast<int>(descs.size());
+  const int L = h.tables;
+  const size_t NB = static_cast<size_t>(h.n_buckets);
+  size_t off = 0, total_desc = 0, n_tiles = 0;
+  std::vector<RowLayout> lay(n_imgs);
+  // codes (coarse + fine) of all images first, then all bucket offsets, so
+  // each group is one contiguous memset
+  for (int i = 0; i < n_imgs; ++i) {
+    const uint64_t n = descs[i].second;
+    if (n >= (1ull << 31)) fail(BMG_UNSUPPORTED, "images with >= 2^31 descriptors");
+    lay[i].coarse_off = off;
+    off = align_up(off + n * L * 4, 256);
+    lay[i].fine_off = off;
+    off = align_up(off + align_up(n, 2) * h.fwp * 8, 256);
+    total_desc += n;
+    n_tiles += (n + kCodesTile - 1) / kCodesTile;
+  }
+  const size_t codes_end = off;
+  for (int i = 0; i < n_imgs; ++i) {
+    lay[i].offsets_off = off;
+    off = align_up(off + L * (NB + 1) * 4, 256);
+  }
+  const size_t offsets_end = off;
+  for (int i = 0; i < n_imgs; ++i) {
+    lay[i].cursor_off = off;
+    off = align_up(off + L * NB * 4, 256);
+    lay[i].slots_off = off;
+    off = align_up(off + descs[i].second * L * 4, 256);
+  }
+  c.d_scratch.ensure(off);
+  char* base = c.d_scratch.as<char>();
+  c.row_imgs.assign(n_imgs, ImgDev{});
+  for (int i = 0; i < n_imgs; ++i) {
+    ImgDev& im = c.row_imgs[i];
+    im.desc = descs[i].first;
+    im.n = static_cast<uint32_t>(descs[i].second);
+    im.coarse = reinterpret_cast<uint32_t*>(base + lay[i].coarse_off);
+    im.fine = reinterpret_cast<uint64_t*>(base + lay[i].fine_off);
+    im.offsets = reinterpret_cast<uint32_t*>(base + lay[i].offsets_off);
+    im.cursor = reinterpret_cast<uint32_t*>(base + lay[i].cursor_off);
+    im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
+    im.overflow = 0;
+  }
+  // metadata
+  ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
+  std::memcpy(h_imgs, c.row_imgs.data(), sizeof(ImgDev) * n_imgs);
+  uint32_t* h_tiles = c.ring.alloc<uint32_t>(2 * std::max<size_t>(n_tiles, 1), c.s_comp, c.s_copy);
+  {
+    size_t t = 0;
+    for (int i = 0; i < n_imgs; ++i)
+      for (uint64_t s = 0; s < descs[i].second; s += kCodesTile) {
+        h_tiles[t] = static_cast<uint32_t>(i);
+        h_tiles[n_tiles + t] = static_cast<uint32_t>(s);
+        ++t;
+      }
+  }
+  c.d_imgs.ensure(sizeof(ImgDev) * std::max(n_imgs, 1));
+  c.d_tiles.ensure(sizeof(uint32_t) * 2 * std::max<size_t>(n_tiles, 1));
+  c.d_mean.ensure(sizeof(float) * kDim);
+  c.d_acc.ensure(sizeof(double) * kDim);
+  const uint32_t fix_cap = static_cast<uint32_t>(std::max<size_t>(65536, total_desc / 4));
+  c.d_fix.ensure(sizeof(Fixup) * fix_cap);
+  c.d_fixcnt.ensure(sizeof(uint32_t) * (1 + std::max(n_imgs, 1)));
+  c.d_diag.ensure(sizeof(unsigned long long) * 4);
+  cudaStream_t s = c.s_comp;
+  BMG_CUDA(cudaMemcpyAsync(c.d_imgs.p, h_imgs, sizeof(ImgDev) * n_imgs, cudaMemcpyHostToDevice, s));
+  if (n_tiles)
+    BMG_CUDA(cudaMemcpyAsync(c.d_tiles.p, h_tiles, sizeof(uint32_t) * 2 * n_tiles,
+                             cudaMemcpyHostToDevice, s));
+  BMG_CUDA(cudaMemsetAsync(base + codes_end, 0, offsets_end - codes_end, s));
+  const int plane_chunks = (h.n_planes + kPlaneChunk - 1) / kPlaneChunk;
+  if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, codes_end, s));
+  BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + n_imgs), s));
+  BMG_CUDA(cudaMemsetAsync(c.d_diag.p, 0, sizeof(unsigned long long) * 4, s));
+  join_uploads(c);
+
+  const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
+  float* d_mean = c.d_mean.as<float>();
+  if (mean_dev) {
+    BMG_CUDA(cudaMemcpyAsync(d_mean, mean_dev, sizeof(float) * kDim, cudaMemcpyDeviceToDevice, s));
+  } else if (mean_host) {
+    float* hm = c.ring.alloc<float>(kDim, c.s_comp, c.s_copy);
+    std::memcpy(hm, mean_host, sizeof(float) * kDim);
+    BMG_CUDA(cudaMemcpyAsync(d_mean, hm, sizeof(float) * kDim, cudaMemcpyHostToDevice, s));
+  } else if (compute_mean) {
+    Timed t(c, "mean", s);
+    launch_row_mean(d_imgs, n_imgs, d_mean, c.d_acc.as<double>(), s);
+    ++c.launches;
+    check_launch();
+  }
+  if (n_tiles == 0) return;
+  const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
+  const uint32_t* d_tile_start = d_tile_img + n_tiles;
+  unsigned long long* diag = c.d_diag.as<unsigned long long>();
+  {
+    Timed t(c, "codes", s);
+    launch_codes(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(n_tiles), d_mean,
+                 c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(), fix_cap, s);
+    ++c.launches;
+    check_launch();
+  }
+  {
+    Timed t(c, "fixup", s);
+    launch_codes_fixup(h, d_imgs, n_imgs, d_mean, c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(),
+                       fix_cap, diag, s);
+    c.launches += 2;
+    check_launch();
+  }
+  {
+    Timed t(c, "tables", s);
+    launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(n_tiles), n_imgs, s);
+    c.launches += 3;
+    check_launch();
+  }
+}
+
+void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
+  std::vector<std::pair<const float*, uint64_t>> descs;
+  descs.reserve(n);
+  c.row_ids.assign(ids, ids + n);
+  c.row_slot.clear();
+  for (uint64_t i = 0; i < n; ++i) {
+    if (i && ids[i] <= ids[i - 1])
+      fail(BMG_INVALID_ARGUMENT, "needed image ids must be strictly ascending");
+    const auto it = c.resident.find(ids[i]);
+    if (it == c.resident.end())
+      fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
+    descs.emplace_back(it->second.d, it->second.n);
+    c.row_slot[ids[i]] = static_cast<int>(i);
+  }
+  c.row_valid = false;
+  prepare_row_views(c, descs, mean_host, nullptr, true);
+  c.row_valid = true;
+}
+
+// ---- matching ---------------------------------------------------------------
+
+struct MatchPlan {
+  int chunk = kMatchThreads;
+};
+
+void check_match_params(const Ctx& c, const bmg_match_params& mp) {
+  if (mp.k_nearest < 1) fail(BMG_INVALID_ARGUMENT, "k_nearest must be >= 1");
+  if (mp.k_nearest > 32) fail(BMG_UNSUPPORTED, "k_nearest > 32 is not supported by the GPU matcher");
+  (void)c;
+}
+
+// Enqueues match + scan + compact for (query slot, train slot) pairs of the
+// current row views.  Offsets (absolute positions in d_res) go to
+// out_off[0..n_pairs], appended after *d_running.
+void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
+                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res) {
+  check_match_params(c, mp);
+  const int n_pairs = static_cast<int>(slot_pairs.size());
+  if (n_pairs == 0) return;
+  const HashDev& h = c.hd;
+  const int chunk = mp.k_nearest <= 8 ? kMatchThreads : 256;
+  const int idx_bits = 32 - bit_width(static_cast<uint32_t>(h.fine_bits));
+  std::vector<int> order(n_pairs);
+  for (int p = 0; p < n_pairs; ++p) order[p] = p;
+  // CTAs of pairs sharing a train image run back to back (L2 reuse of its
+  // descriptors during the re-rank gathers)
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return slot_pairs[x].second < slot_pairs[y].second; });
+  size_t n_work = 0;
+  uint32_t max_train_n = 0;
+  for (int p = 0; p < n_pairs; ++p) {
+    const ImgDev& q = c.row_imgs[slot_pairs[p].first];
+    const ImgDev& t = c.row_imgs[slot_pairs[p].second];
+    if (t.n > (1u << idx_bits) - 1u) fail(BMG_UNSUPPORTED, "train image too large for the key packing");
+    n_work += (q.n + chunk - 1) / chunk;
+    max_train_n = std::max(max_train_n, t.n);
+  }
+  PairWork* h_work = c.ring.alloc<PairWork>(std::max<size_t>(n_work, 1), c.s_comp, c.s_copy);
+  uint64_t* h_dense_off = c.ring.alloc<uint64_t>(n_pairs, c.s_comp, c.s_copy);
+  uint32_t* h_nq = c.ring.alloc<uint32_t>(n_pairs, c.s_comp, c.s_copy);
+  uint64_t dense_total = 0;
+  for (int p = 0; p < n_pairs; ++p) {
+    h_dense_off[p] = dense_total;
+    h_nq[p] = c.row_imgs[slot_pairs[p].first].n;
+    dense_total += h_nq[p];
+  }
+  size_t w = 0;
+  for (int oi = 0; oi < n_pairs; ++oi) {
+    const int p = order[oi];
+    const uint32_t nq = h_nq[p];
+    for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+      PairWork& pw = h_work[w++];
+      pw.q_img = static_cast<uint32_t>(slot_pairs[p].first);
+      pw.t_img = static_cast<uint32_t>(slot_pairs[p].second);
+      pw.q_begin = q0;
+      pw.q_end = std::min<uint32_t>(nq, q0 + chunk);
+      pw.pair = static_cast<uint32_t>(p);
+    }
+  }
+  c.d_work.ensure(sizeof(PairWork) * std::max<size_t>(n_work, 1));
+  c.d_dense_off.ensure(sizeof(uint64_t) * n_pairs);
+  c.d_nq.ensure(sizeof(uint32_t) * n_pairs);
+  c.d_pair_count.ensure(sizeof(uint32_t) * n_pairs);
+  c.d_dense.ensure(sizeof(int32_t) * std::max<uint64_t>(dense_total, 1));
+  cudaStream_t s = c.s_comp;
+  if (n_work)
+    BMG_CUDA(cudaMemcpyAsync(c.d_work.p, h_work, sizeof(PairWork) * n_work, cudaMemcpyHostToDevice, s));
+  BMG_CUDA(cudaMemcpyAsync(c.d_dense_off.p, h_dense_off, sizeof(uint64_t) * n_pairs,
+                           cudaMemcpyHostToDevice, s));
+  BMG_CUDA(cudaMemcpyAsync(c.d_nq.p, h_nq, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, s));
+  BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
+  MatchLaunch a{};
+  a.imgs = c.d_imgs.as<ImgDev>();
+  a.work = c.d_work.as<PairWork>();
+  a.dense_off = c.d_dense_off.as<uint64_t>();
+  a.dense = c.d_dense.as<int32_t>();
+  a.pair_count = c.d_pair_count.as<uint32_t>();
+  a.exact_queries = c.d_diag.as<unsigned long long>() + 1;
+  a.tables = h.tables;
+  a.n_buckets = h.n_buckets;
+  a.k = mp.k_nearest;
+  a.idx_bits = idx_bits;
+  a.ratio = mp.ratio;
+  if (n_work) {
+    Timed t(c, "match", s);
+    launch_match(a, h.fwp, static_cast<int>(n_work), c.row_imgs[0], max_train_n, s, nullptr);
+    ++c.launches;
+    check_launch();
+  }
+  {
+    Timed t(c, "compact", s);
+    launch_scan_counts(c.d_pair_count.as<uint32_t>(), n_pairs, out_off,
+                       c.d_running.as<unsigned long long>(), s);
+    launch_compact(c.d_dense.as<int32_t>(), c.d_dense_off.as<uint64_t>(), c.d_nq.as<uint32_t>(),
+                   out_off, n_pairs, d_res, s);
+    c.launches += 2;
+    check_launch();
+  }
+}
+
+HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const float* fine) {
+  HashDev h{};
+  h.tables = p.tables;
+  h.coarse_bits = p.coarse_bits;
+  h.fine_bits = p.fine_bits;
+  h.n_planes = p.tables * p.coarse_bits + p.fine_bits;
+  h.fw = (p.fine_bits + 63) / 64;
+  h.fwp = padded_words(h.fw);
+  h.n_buckets = 1 << p.coarse_bits;
+  h.n_planes_pad = static_cast<int>(align_up(h.n_planes, kPlaneChunk));
+  const int np = h.n_planes, npp = h.n_planes_pad;
+  std::vector<float> planes(static_cast<size_t>(np) * kDim), planes_t(static_cast<size_t>(npp) * kDim, 0.f),
+      norm(npp, 0.f);
+  const size_t nc = static_cast<size_t>(p.tables) * p.coarse_bits * kDim;
+  std::memcpy(planes.data(), coarse, nc * sizeof(float));
+  std::memcpy(planes.data() + nc, fine, static_cast<size_t>(p.fine_bits) * kDim * sizeof(float));
+  for (int q = 0; q < np; ++q) {
+    double ss = 0.0;
+    for (int d = 0; d < kDim; ++d) {
+      const float v = planes[static_cast<size_t>(q) * kDim + d];
+      planes_t[static_cast<size_t>(d) * npp + q] = v;
+      ss += static_cast<double>(v) * v;
+    }
+    // ||p||_2 rounded up (the certificate needs an upper bound)
+    norm[q] = static_cast<float>(std::sqrt(ss) * (1.0 + 1e-6)) ;
+  }
+  c.planes.ensure(planes.size() * sizeof(float));
+  c.planes_t.ensure(planes_t.size() * sizeof(float));
+  c.plane_norm.ensure(norm.size() * sizeof(float));
+  BMG_CUDA(cudaMemcpy(c.planes.p, planes.data(), planes.size() * sizeof(float), cudaMemcpyHostToDevice));
+  BMG_CUDA(cudaMemcpy(c.planes_t.p, planes_t.data(), planes_t.size() * sizeof(float), cudaMemcpyHostToDevice));
+  BMG_CUDA(cudaMemcpy(c.plane_norm.p, norm.data(), norm.size() * sizeof(float), cudaMemcpyHostToDevice));
+  h.planes = c.planes.as<float>();
+  h.planes_t = c.planes_t.as<float>();
+  h.plane_norm = c.plane_norm.as<float>();
+  return h;
+}
+
+void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fine_out) {
+  const HashDev& h = c.hd;
+  const size_t n = im.n;
+  if (coarse_out && n)
+    BMG_CUDA(cudaMemcpyAsync(coarse_out, im.coarse, n * h.tables * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, c.s_comp));
+  if (fine_out && n) {
+    if (h.fw == h.fwp) {
+      BMG_CUDA(cudaMemcpyAsync(fine_out, im.fine, n * h.fw * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                               c.s_comp));
+    } else {
+      BMG_CUDA(cudaMemcpy2DAsync(fine_out, h.fw * sizeof(uint64_t), im.fine, h.fwp * sizeof(uint64_t),
+                                 h.fw * sizeof(uint64_t), n, cudaMemcpyDeviceToHost, c.s_comp));
+    }
+  }
+  BMG_CUDA(cudaStreamSynchronize(c.s_comp));
+}
+
+void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
+  c.d_res_off.ensure(sizeof(uint64_t) * (n_pairs + 1));
+  c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
+  c.d_running.ensure(sizeof(unsigned long long));
+  BMG_CUDA(cudaMemsetAsync(c.d_running.p, 0, sizeof(unsigned long long), c.s_comp));
+}
+
+}  // namespace
+}  // namespace bmg
+
+using namespace bmg;
+
+extern "C" {
+
+const char* bmg_status_name(int status) {
+  switch (status) {
+    case BMG_OK: return "Ok";
+    case BMG_INVALID_ARGUMENT: return "InvalidArgument";
+    case BMG_HASH_MISMATCH: return "HashMismatch";
+    case BMG_CAPACITY_EXCEEDED: return "CapacityExceeded";
+    case BMG_NOT_RESIDENT: return "NotResident";
+    case BMG_CUDA_ERROR: return "CudaError";
+    case BMG_OUT_OF_MEMORY: return "OutOfMemory";
+    case BMG_UNSUPPORTED: return "Unsupported";
+    default: return "Unknown";
+  }
+}
+
+const char* bmg_last_error(void) { return g_last_error.c_str(); }
+int bmg_abi_version(void) { return BMG_ABI_VERSION; }
+
+uint64_t bmg_seed_for(uint64_t root, const char* stage) { return seed_for(root, stage ? stage : ""); }
+
+int bmg_make_hash_functions(uint64_t seed, const bmg_hash_params* params, float* coarse_out,
+                            float* fine_out) {
+  return guarded([&] {
+    if (!params || !valid_hash_params(*params))
+      fail(BMG_INVALID_ARGUMENT, "hash params out of range (tables>=1, coarse_bits in [1,32], fine_bits>=1)");
+    make_planes(seed, *params, coarse_out, fine_out);
+  });
+}
+
+int bmg_create(const bmg_config* cfg, bmg_context** out) {
+  return guarded([&] {
+    if (!cfg || !out) fail(BMG_INVALID_ARGUMENT, "null argument");
+    if (!valid_hash_params(cfg->hash))
+      fail(BMG_INVALID_ARGUMENT, "hash params out of range (tables>=1, coarse_bits in [1,32], fine_bits>=1)");
+    if (cfg->hash.coarse_bits > 16)
+      fail(BMG_UNSUPPORTED, "coarse_bits > 16 (>65536 buckets per table) is not supported on the GPU path");
+    if (!cfg->coarse_planes || !cfg->fine_planes) fail(BMG_INVALID_ARGUMENT, "null hash planes");
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+      cudaGetLastError();
+      fail(BMG_CUDA_ERROR, "no CUDA device available: the B200 matcher has no CPU fallback");
+    }
+    if (cfg->device < 0 || cfg->device >= n_dev) fail(BMG_INVALID_ARGUMENT, "bad device ordinal");
+    auto c = std::make_unique<bmg_context>();
+    c->device = cfg->device;
+    set_device(*c);
+    c->hp = cfg->hash;
+    c->seed = cfg->function_seed;
+    c->capacity = cfg->capacity_units;
+    BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+    BMG_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
+    BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
+    uint64_t thresh = ~0ull;
+    BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    c->stage_bytes = 8u << 20;
+    for (int i = 0; i < 2; ++i) {
+      BMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage[i]), c->stage_bytes));
+      BMG_CUDA(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
+      BMG_CUDA(cudaEventRecord(c->stage_ev[i], c->s_copy));
+    }
+    c->ring.init(64u << 20);
+    c->hd = build_hash(*c, cfg->hash, cfg->coarse_planes, cfg->fine_planes);
+    *out = c.release();
+  });
+}
+
+int bmg_destroy(bmg_context* c) {
+  if (!c) return BMG_OK;
+  return guarded([&] {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& [id, im] : c->resident) cudaFree(im.d);
+    c->resident.clear();
+    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
+                      &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
+                      &c->d_work, &c->d_dense, &c->d_dense_off, &c->d_pair_count, &c->d_nq,
+                      &c->d_res_off, &c->d_res, &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes})
+      b->release();
+    for (int i = 0; i < 2; ++i) {
+      if (c->stage[i]) cudaFreeHost(c->stage[i]);
+      if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
+    }
+    c->ring.release();
+    for (auto& t : c->timers) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
+    if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
+    if (c->s_copy) cudaStreamDestroy(c->s_copy);
+    if (c->s_comp) cudaStreamDestroy(c->s_comp);
+    delete c;
+  });
+}
+
+int bmg_synchronize(bmg_context* c) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+  });
+}
+
+int bmg_upload(bmg_context* c, uint64_t id, const float* desc, uint64_t count) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    arena_upload(*c, id, desc, count);
+  });
+}
+
+int bmg_evict(bmg_context* c, uint64_t id) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    arena_evict(*c, id);
+  });
+}
+
+int bmg_is_resident(bmg_context* c, uint64_t id) { return c && c->resident.count(id) ? 1 : 0; }
+
+int bmg_arena_stats_get(bmg_context* c, bmg_arena_stats* o) {
+  return guarded([&] {
+    if (!c || !o) fail(BMG_INVALID_ARGUMENT, "null argument");
+    o->capacity = c->capacity;
+    o->occupancy = c->occupancy;
+    o->peak_occupancy = c->peak;
+    o->uploads = c->uploads;
+    o->evictions = c->evictions;
+    o->units_uploaded = c->units_uploaded;
+    o->resident_count = c->resident.size();
+  });
+}
+
+int bmg_row(bmg_context* c, const uint64_t* needed, uint64_t n, const float* mean) {
+  return guarded([&] {
+    if (!c || (n && !needed)) fail(BMG_INVALID_ARGUMENT, "null argument");
+    set_device(*c);
+    prepare_row(*c, needed, n, mean);
+  });
+}
+
+int bmg_row_mean(bmg_context* c, float* mean_out) {
+  return guarded([&] {
+    if (!c || !mean_out) fail(BMG_INVALID_ARGUMENT, "null argument");
+    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    set_device(*c);
+    BMG_CUDA(cudaMemcpyAsync(mean_out, c->d_mean.p, sizeof(float) * kDim, cudaMemcpyDeviceToHost, c->s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+  });
+}
+
+int bmg_codes(bmg_context* c, uint64_t id, uint32_t* coarse_out, uint64_t* fine_out) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    const auto it = c->row_slot.find(id);
+    if (it == c->row_slot.end()) fail(BMG_INVALID_ARGUMENT, "image " + std::to_string(id) + " is not in the current row");
+    set_device(*c);
+    copy_codes_out(*c, c->row_imgs[it->second], coarse_out, fine_out);
+  });
+}
+
+int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64_t n_pairs,
+              const bmg_match_params* mp, uint64_t* offsets_out, int32_t* matches_out,
+              uint64_t capacity) {
+  return guarded([&] {
+    if (!c || !mp || !offsets_out || (n_pairs && (!qids || !tids)))
+      fail(BMG_INVALID_ARGUMENT, "null argument");
+    check_match_params(*c, *mp);
+    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    set_device(*c);
+    std::vector<std::pair<int, int>> sp;
+    uint64_t max_matches = 0;
+    for (uint64_t p = 0; p < n_pairs; ++p) {
+      const auto qi = c->row_slot.find(qids[p]);
+      const auto ti = c->row_slot.find(tids[p]);
+      if (qi == c->row_slot.end() || ti == c->row_slot.end())
+        fail(BMG_INVALID_ARGUMENT, "pair image not in the current row");
+      sp.emplace_back(qi->second, ti->second);
+      max_matches += c->row_imgs[qi->second].n;
+    }
+    reset_results(*c, n_pairs, max_matches);
+    enqueue_match(*c, sp, *mp, c->d_res_off.as<uint64_t>(), c->d_res.as<int32_t>());
+    if (n_pairs == 0) {
+      offsets_out[0] = 0;
+      return;
+    }
+    BMG_CUDA(cudaMemcpyAsync(offsets_out, c->d_res_off.p, sizeof(uint64_t) * (n_pairs + 1),
+                             cudaMemcpyDeviceToHost, c->s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    const uint64_t total = offsets_out[n_pairs];
+    if (total > capacity) fail(BMG_INVALID_ARGUMENT, "match output capacity too small");
+    if (total) {
+      if (!matches_out) fail(BMG_INVALID_ARGUMENT, "null match output");
+      BMG_CUDA(cudaMemcpy(matches_out, c->d_res.p, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int bmg_compute_codes(bmg_context* c, const float* desc, uint64_t count, const float* mean,
+                      uint32_t* coarse_out, uint64_t* fine_out) {
+  return guarded([&] {
+    if (!c || !mean || (count && (!desc || !coarse_out || !fine_out)))
+      fail(BMG_INVALID_ARGUMENT, "null argument");
+    set_device(*c);
+    c->row_valid = false;
+    c->d_tmp_desc.ensure(std::max<uint64_t>(count, 1) * 512);
+    BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    stage_h2d(*c, c->d_tmp_desc.p, desc, count * 512);
+    c->pending_upload = true;
+    std::vector<std::pair<const float*, uint64_t>> one{{c->d_tmp_desc.as<float>(), count}};
+    prepare_row_views(*c, one, mean, nullptr, false);
+    copy_codes_out(*c, c->row_imgs[0], coarse_out, fine_out);
+  });
+}
+
+int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, const float* tdesc,
+                   const bmg_code_set* tc, const bmg_match_params* mp, int32_t* matches_out,
+                   uint64_t* n_out) {
+  return guarded([&] {
+    if (!c || !qc || !tc || !mp || !n_out) fail(BMG_INVALID_ARGUMENT, "null argument");
+    *n_out = 0;
+    // hashmatch.cpp:105-113
+    if (qc->function_seed != tc->function_seed)
+      fail(BMG_HASH_MISMATCH, "code sets built from different hash function seeds");
+    if (qc->params.tables != tc->params.tables || qc->params.coarse_bits != tc->params.coarse_bits ||
+        qc->params.fine_bits != tc->params.fine_bits)
+      fail(BMG_HASH_MISMATCH, "code sets built with different hash parameters");
+    if (mp->k_nearest < 1) fail(BMG_INVALID_ARGUMENT, "k_nearest must be >= 1");
+    check_match_params(*c, *mp);
+    if (qc->count == 0 || tc->count == 0) return;  // :118
+    if (qc->params.tables != c->hp.tables || qc->params.coarse_bits != c->hp.coarse_bits ||
+        qc->params.fine_bits != c->hp.fine_bits)
+      fail(BMG_HASH_MISMATCH, "code sets built with parameters other than this context's");
+    if (!qdesc || !tdesc || !qc->coarse || !qc->fine || !tc->coarse || !tc->fine || !matches_out)
+      fail(BMG_INVALID_ARGUMENT, "null data pointer");
+    set_device(*c);
+    c->row_valid = false;
+    const HashDev& h = c->hd;
+    const uint64_t nq = qc->count, nt = tc->count;
+    // descriptors
+    c->d_tmp_desc.ensure((nq + nt) * 512);
+    BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    float* dq = c->d_tmp_desc.as<float>();
+    float* dt = dq + nq * kDim;
+    stage_h2d(*c, dq, qdesc, nq * 512);
+    stage_h2d(*c, dt, tdesc, nt * 512);
+    c->pending_upload = true;
+    // lay out two images (no codes computed: the given codes are uploaded)
+    std::vector<std::pair<const float*, uint64_t>> two{{dq, nq}, {dt, nt}};
+    // reuse the row layout, but skip the projection kernels: upload codes into place
+    c->row_imgs.clear();
+    {
+      // layout only
+      const int L = h.tables;
+      const size_t NB = h.n_buckets;
+      size_t off = 0;
+      size_t co[2], fo[2], oo[2], cu[2], so[2];
+      for (int i = 0; i < 2; ++i) {
+        co[i] = off; off = align_up(off + two[i].second * L * 4, 256);
+        fo[i] = off; off = align_up(off + align_up(two[i].second, 2) * h.fwp * 8, 256);
+      }
+      for (int i = 0; i < 2; ++i) { oo[i] = off; off = align_up(off + L * (NB + 1) * 4, 256); }
+      const size_t off_begin = oo[0], off_end = off;
+      for (int i = 0; i < 2; ++i) {
+        cu[i] = off; off = align_up(off + L * NB * 4, 256);
+        so[i] = off; off = align_up(off + two[i].second * L * 4, 256);
+      }
+      c->d_scratch.ensure(off);
+      char* base = c->d_scratch.as<char>();
+      const bmg_code_set* sets[2] = {qc, tc};
+      for (int i = 0; i < 2; ++i) {
+        ImgDev im{};
+        im.desc = two[i].first;
+        im.n = static_cast<uint32_t>(two[i].second);
+        im.coarse = reinterpret_cast<uint32_t*>(base + co[i]);
+        im.fine = reinterpret_cast<uint64_t*>(base + fo[i]);
+        im.offsets = reinterpret_cast<uint32_t*>(base + oo[i]);
+        im.cursor = reinterpret_cast<uint32_t*>(base + cu[i]);
+        im.slots = reinterpret_cast<uint32_t*>(base + so[i]);
+        c->row_imgs.push_back(im);
+        const uint64_t n = two[i].second;
+        for (uint64_t j = 0; j < n * L; ++j)
+          if (sets[i]->coarse[j] >= static_cast<uint32_t>(h.n_buckets))
+            fail(BMG_INVALID_ARGUMENT, "bucket id out of range for coarse_bits");
+        uint32_t* hc = c->ring.alloc<uint32_t>(n * L, c->s_comp, c->s_copy);
+        std::memcpy(hc, sets[i]->coarse, n * L * 4);
+        BMG_CUDA(cudaMemcpyAsync(im.coarse, hc, n * L * 4, cudaMemcpyHostToDevice, c->s_comp));
+        uint64_t* hf = c->ring.alloc<uint64_t>(n * h.fwp, c->s_comp, c->s_copy);
+        std::memset(hf, 0, n * h.fwp * 8);
+        for (uint64_t j = 0; j < n; ++j)
+          std::memcpy(hf + j * h.fwp, sets[i]->fine + j * h.fw, h.fw * 8);
+        BMG_CUDA(cudaMemcpyAsync(im.fine, hf, n * h.fwp * 8, cudaMemcpyHostToDevice, c->s_comp));
+      }
+      BMG_CUDA(cudaMemsetAsync(base + off_begin, 0, off_end - off_begin, c->s_comp));
+      ImgDev* hi = c->ring.alloc<ImgDev>(2, c->s_comp, c->s_copy);
+      std::memcpy(hi, c->row_imgs.data(), sizeof(ImgDev) * 2);
+      c->d_imgs.ensure(sizeof(ImgDev) * 2);
+      BMG_CUDA(cudaMemcpyAsync(c->d_imgs.p, hi, sizeof(ImgDev) * 2, cudaMemcpyHostToDevice, c->s_comp));
+      // tables for the train image only (slot 1)
+      const size_t n_tiles = (nt + kCodesTile - 1) / kCodesTile;
+      uint32_t* ht = c->ring.alloc<uint32_t>(2 * n_tiles, c->s_comp, c->s_copy);
+      for (size_t t = 0; t < n_tiles; ++t) {
+        ht[t] = 1;
+        ht[n_tiles + t] = static_cast<uint32_t>(t * kCodesTile);
+      }
+      c->d_tiles.ensure(sizeof(uint32_t) * 2 * n_tiles);
+      BMG_CUDA(cudaMemcpyAsync(c->d_tiles.p, ht, sizeof(uint32_t) * 2 * n_tiles, cudaMemcpyHostToDevice,
+                               c->s_comp));
+      c->d_diag.ensure(sizeof(unsigned long long) * 4);
+      BMG_CUDA(cudaMemsetAsync(c->d_diag.p, 0, sizeof(unsigned long long) * 4, c->s_comp));
+      join_uploads(*c);
+      // the scan kernel for slot 1 only: run tables on a 2-image table but
+      // the hist/scatter tiles reference image 1 only
+      launch_tables(h, c->d_imgs.as<ImgDev>(), c->d_tiles.as<uint32_t>(), c->d_tiles.as<uint32_t>() + n_tiles,
+                    static_cast<int>(n_tiles), 2, c->s_comp);
+      c->launches += 3;
+      check_launch();
+    }
+    std::vector<std::pair<int, int>> sp{{0, 1}};
+    reset_results(*c, 1, nq);
+    enqueue_match(*c, sp, *mp, c->d_res_off.as<uint64_t>(), c->d_res.as<int32_t>());
+    uint64_t offs[2];
+    BMG_CUDA(cudaMemcpyAsync(offs, c->d_res_off.p, sizeof(offs), cudaMemcpyDeviceToHost, c->s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    const uint64_t total = offs[1] - offs[0];
+    if (total)
+      BMG_CUDA(cudaMemcpy(matches_out, c->d_res.as<int32_t>() + 2 * offs[0], sizeof(int32_t) * 2 * total,
+                          cudaMemcpyDeviceToHost));
+    *n_out = total;
+  });
+}
+
+int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_view* features,
+                     uint64_t n_features, const bmg_execute_options* opts, bmg_result** out) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!c || !plan || !opts || !out || (n_features && !features))
+      fail(BMG_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    check_match_params(*c, opts->match);
+    set_device(*c);
+    std::unordered_map<uint64_t, const bmg_feature_view*> fmap;
+    for (uint64_t i = 0; i < n_features; ++i) fmap[features[i].image_id] = &features[i];
+    auto features_of = [&](uint64_t id) -> const bmg_feature_view& {
+      const auto it = fmap.find(id);
+      if (it == fmap.end())
+        fail(BMG_INVALID_ARGUMENT, "plan references image " + std::to_string(id) + " with no features");
+      return *it->second;
+    };
+    uint64_t total_rows = 0;
+    for (uint64_t i = 0; i < plan->n_iterations; ++i) total_rows += plan->rows_per_iteration[i];
+    if (total_rows != plan->n_rows) fail(BMG_INVALID_ARGUMENT, "rows_per_iteration does not sum to n_rows");
+    const uint64_t n_pairs = plan->n_rows ? plan->row_pair_offsets[plan->n_rows] : 0;
+    uint64_t cap = 0;
+    for (uint64_t p = 0; p < n_pairs; ++p) {
+      const uint64_t a = plan->pairs[2 * p], b = plan->pairs[2 * p + 1];
+      if (a >= b) fail(BMG_INVALID_ARGUMENT, "plan pairs must be (lower id, higher id)");
+      cap += features_of(a).count;
+    }
+    auto res = std::make_unique<bmg_result>();
+    reset_results(*c, n_pairs, cap);
+    uint64_t* d_off = c->d_res_off.as<uint64_t>();
+    BMG_CUDA(cudaMemsetAsync(d_off, 0, sizeof(uint64_t), c->s_comp));
+    uint64_t row = 0;
+    for (uint64_t it = 0; it < plan->n_iterations; ++it) {
+      const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
+      uint64_t it_pairs = 0;
+      for (uint64_t r = 0; r < plan->rows_per_iteration[it]; ++r, ++row) {
+        const uint64_t nb = plan->row_needed_offsets[row], ne = plan->row_needed_offsets[row + 1];
+        const uint64_t* needed = plan->needed_ids + nb;
+        for (uint64_t k = nb; k < ne; ++k) {
+          const uint64_t id = plan->needed_ids[k];
+          const bmg_feature_view& fv = features_of(id);
+          if (!c->resident.count(id)) {
+            arena_upload(*c, id, fv.descriptors, fv.count);
+            if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
+          }
+        }
+        prepare_row(*c, needed, ne - nb, nullptr);
+        const uint64_t pb = plan->row_pair_offsets[row], pe = plan->row_pair_offsets[row + 1];
+        std::vector<std::pair<int, int>> sp;
+        sp.reserve(pe - pb);
+        for (uint64_t p = pb; p < pe; ++p) {
+          const auto qa = c->row_slot.find(plan->pairs[2 * p]);
+          const auto tb = c->row_slot.find(plan->pairs[2 * p + 1]);
+          if (qa == c->row_slot.end() || tb == c->row_slot.end())
+            fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
+          sp.emplace_back(qa->second, tb->second);
+        }
+        enqueue_match(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>());
+        it_pairs += pe - pb;
+        for (uint64_t k = plan->row_evict_offsets[row]; k < plan->row_evict_offsets[row + 1]; ++k) {
+          arena_evict(*c, plan->evict_ids[k]);
+          if (opts->on_evict) opts->on_evict(opts->hook_user, plan->evict_ids[k]);
+        }
+      }
+      res->iterations.push_back(it_pairs);
+      res->iterations.push_back(c->uploads - up0);
+      res->iterations.push_back(c->units_uploaded - units0);
+    }
+    // read the device result log back once
+    std::vector<uint64_t> offs(n_pairs + 1, 0);
+    if (n_pairs) {
+      BMG_CUDA(cudaMemcpyAsync(offs.data(), d_off, sizeof(uint64_t) * (n_pairs + 1), cudaMemcpyDeviceToHost,
+                               c->s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    }
+    const uint64_t total = offs[n_pairs];
+    std::vector<int32_t> flat(2 * total);
+    if (total)
+      BMG_CUDA(cudaMemcpy(flat.data(), c->d_res.p, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost));
+    // results keyed and sorted by IdPair (engine.cpp:419, 506-512); a pair
+    // planned twice keeps its last match list, like the reference's map
+    std::map<std::pair<uint64_t, uint64_t>, uint64_t> last;
+    for (uint64_t p = 0; p < n_pairs; ++p) last[{plan->pairs[2 * p], plan->pairs[2 * p + 1]}] = p;
+    res->offsets.push_back(0);
+    for (const auto& [key, p] : last) {
+      res->pair_ids.push_back(key.first);
+      res->pair_ids.push_back(key.second);
+      const uint64_t b = offs[p], e = offs[p + 1];
+      res->matches.insert(res->matches.end(), flat.begin() + 2 * b, flat.begin() + 2 * e);
+      res->offsets.push_back(res->matches.size() / 2);
+      if (opts->on_pair)
+        opts->on_pair(opts->on_pair_user, key.first, key.second, flat.data() + 2 * b, e - b);
+    }
+    res->counters[0] = n_pairs;
+    res->counters[1] = total;
+    res->counters[2] = c->uploads;
+    res->counters[3] = c->evictions;
+    res->counters[4] = c->units_uploaded;
+    res->counters[5] = c->peak;
+    res->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = res.release();
+  });
+}
+
+uint64_t bmg_result_pair_count(const bmg_result* r) { return r ? r->pair_ids.size() / 2 : 0; }
+uint64_t bmg_result_match_count(const bmg_result* r) { return r ? r->matches.size() / 2 : 0; }
+
+int bmg_result_copy(const bmg_result* r, uint64_t* pair_ids, uint64_t* offsets, int32_t* matches) {
+  return guarded([&] {
+    if (!r) fail(BMG_INVALID_ARGUMENT, "null result");
+    if (pair_ids) std::copy(r->pair_ids.begin(), r->pair_ids.end(), pair_ids);
+    if (offsets) std::copy(r->offsets.begin(), r->offsets.end(), offsets);
+    if (matches) std::copy(r->matches.begin(), r->matches.end(), matches);
+  });
+}
+
+int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wall_s_out) {
+  return guarded([&] {
+    if (!r) fail(BMG_INVALID_ARGUMENT, "null result");
+    if (counters_out) std::copy(r->counters, r->counters + 6, counters_out);
+    if (wall_s_out) *wall_s_out = r->wall_s;
+  });
+}
+
+uint64_t bmg_result_iteration_count(const bmg_result* r) { return r ? r->iterations.size() / 3 : 0; }
+
+int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out3[3]) {
+  return guarded([&] {
+    if (!r || !out3 || i >= r->iterations.size() / 3) fail(BMG_INVALID_ARGUMENT, "bad iteration index");
+    std::copy(r->iterations.begin() + 3 * i, r->iterations.begin() + 3 * i + 3, out3);
+  });
+}
+
+void bmg_result_free(bmg_result* r) { delete r; }
+
+uint64_t bmg_launch_count(bmg_context* c) { return c ? c->launches : 0; }
+
+int bmg_set_profiling(bmg_context* c, int enabled) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    for (auto& t : c->timers) {
+      c->free_events.push_back(t.a);
+      c->free_events.push_back(t.b);
+    }
+    c->timers.clear();
+    c->profiling = enabled != 0;
+  });
+}
+
+int bmg_kernel_time(bmg_context* c, const char* cls, double* total_ms, uint64_t* launches) {
+  return guarded([&] {
+    if (!c || !cls) fail(BMG_INVALID_ARGUMENT, "null argument");
+    set_device(*c);
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    double ms = 0.0;
+    uint64_t n = 0;
+    for (auto& t : c->timers) {
+      if (t.cls != cls) continue;
+      float x = 0.f;
+      BMG_CUDA(cudaEventElapsedTime(&x, t.a, t.b));
+      ms += x;
+      ++n;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = n;
+  });
+}
+
+int bmg_fixup_counts(bmg_context* c, uint64_t* code_bits, uint64_t* rerank_queries) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    unsigned long long d[4] = {0, 0, 0, 0};
+    if (c->d_diag.p) {
+      BMG_CUDA(cudaMemcpyAsync(d, c->d_diag.p, sizeof(d), cudaMemcpyDeviceToHost, c->s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    }
+    if (code_bits) *code_bits = d[0];
+    if (rerank_queries) *rerank_queries = d[1];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// bmg_internal.h -- device-side data layout shared by the sm_100a kernels and
+// the host runtime (bmg_api.cpp).  See DESIGN.md §3 for the HBM layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace bmg {
+
+constexpr int kDim = 128;
+
+// One image as seen by the kernels during a block row: descriptors live in
+// the HBM arena; codes and bucket tables live in the row scratch buffer.
+struct ImgDev {
+  const float* desc;   // [n][128] row-major (Descriptor layout, features.hpp:23-44)
+  uint32_t* coarse;    // [n][tables] bucket ids            (HashCodeSet::coarse)
+  uint64_t* fine;      // [n][fwp] fine code words, fwp >= ceil(fine_bits/64), zero padded
+  uint32_t* offsets;   // [tables][n_buckets+1] bucket starts (hashmatch.cpp:125-135)
+  uint32_t* cursor;    // [tables][n_buckets]   scatter cursors (scratch)
+  uint32_t* slots;     // [tables][n] train indices grouped by bucket (:136-145)
+  uint32_t n;
+  uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
+};
+
+struct HashDev {
+  int tables, coarse_bits, fine_bits;
+  int n_planes;        // tables*coarse_bits + fine_bits
+  int fw;              // ceil(fine_bits/64)
+  int fwp;             // padded words (1,2,4,8,16)
+  int n_buckets;       // 1 << coarse_bits
+  const float* planes_t;   // [128][n_planes_pad] transposed planes, zero padded
+  const float* planes;     // [n_planes][128] planes (coarse first, then fine)
+  const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
+  int n_planes_pad;
+};
+
+// An ambiguous projection whose sign the FP32 pass could not certify; the
+// fixup kernel recomputes it in the reference's FP64 order.
+struct Fixup {
+  uint32_t img, desc, plane, pad;
+};
+
+// One CTA of the match kernel: a query range of one image pair.
+struct PairWork {
+  uint32_t q_img, t_img;  // row-slot indices into the ImgDev table
+  uint32_t q_begin, q_end;
+  uint32_t pair;          // index of the pair within the launch
+  uint32_t pad[3];
+};
+
+struct MatchLaunch {
+  const ImgDev* imgs;
+  const PairWork* work;
+  const uint64_t* dense_off;   // [n_pairs] offset of each pair's dense result array
+  int32_t* dense;              // train idx or -1 per query
+  uint32_t* pair_count;        // [n_pairs] number of matches per pair
+  unsigned long long* exact_queries;  // diagnostics: queries that took the FP64 path
+  int tables, n_buckets, k, idx_bits;
+  double ratio;
+};
+
+// ---- launchers (kernels.cu) ----
+void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
+                     cudaStream_t s);
+void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                  const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
+                  uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s);
+void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,
+                        const Fixup* fix, const uint32_t* fix_count, uint32_t fix_cap,
+                        unsigned long long* fixed_bits, cudaStream_t s);
+void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                   const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s);
+void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev& any_train_max,
+                  uint32_t max_train_n, cudaStream_t s, int* smem_used);
+void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
+                        unsigned long long* running_total, cudaStream_t s);
+void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
+                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);
+
+constexpr int kCodesTile = 128;   // descriptors per codes CTA
+constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)
+constexpr int kMatchThreads = 1024;
+
+}  // namespace bmg

@@ -1,0 +1,787 @@
+// kernels.cu -- hand-written sm_100a kernels for the cascade-hashing hot path.
+//
+//   K1 row_mean_kernel        engine.cpp:446-461   exact sequential FP64 chain
+//   K2 codes_kernel           hashmatch.cpp:71-100 FP32 projection + certified sign
+//      codes_fixup_kernel                          FP64 reference-order recompute of
+//      codes_overflow_kernel                       the uncertified signs
+//   K3 tables_{hist,scan,scatter}  hashmatch.cpp:120-145 bucket index per (image,row)
+//   K4 match_kernel           hashmatch.cpp:147-208 bucket union + Hamming top-K +
+//                                                  certified Euclidean re-rank + ratio
+//   K6 scan_counts / compact  engine.cpp:475-487   ascending-query match lists
+//
+// Exactness contract: every decision equals the
+// reference's IEEE-754 double computation.  FP32 is only used as a certified
+// filter: a result is accepted when a rigorous forward error bound proves the
+// FP64 result has the same sign / ordering; otherwise the FP64 path recomputes
+// it with __dadd_rn/__dmul_rn/__dsub_rn/__dsqrt_rn in the reference order.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "bmg_internal.h"
+
+namespace bmg {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// K1: row centering mean.  acc[c] += (double)d.v[c] over images in ascending
+// id order, descriptors in index order; mean = float(acc / total).  One
+// thread per channel keeps the reference's exact addition order; loads run
+// 64 descriptors ahead of the DADD chain (double-buffered) with an L2
+// prefetch stream further ahead, so the kernel is bound by DADD latency.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) row_mean_kernel(const ImgDev* __restrict__ imgs,
+                                                       int n_imgs, float* __restrict__ mean_out,
+                                                       double* __restrict__ acc_out) {
+  constexpr int U = 32;
+  constexpr int PF = 512;  // prefetch distance in descriptors
+  const int c = threadIdx.x;
+  double acc = 0.0;
+  unsigned long long total = 0;
+  for (int im = 0; im < n_imgs; ++im) {
+    const float* base = imgs[im].desc;
+    const uint32_t n = imgs[im].n;
+    const float* d = base + c;
+    uint32_t i = 0;
+    float v[U], w[U];
+    if (n >= U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(d + (size_t)u * kDim);
+    }
+    for (; i + 2 * U <= n; i += U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(i + U + u) * kDim);
+      {
+        const uint32_t row = i + PF + (c >> 2);
+        if (row < n) {
+          const char* p = reinterpret_cast<const char*>(base + (size_t)row * kDim) + (c & 3) * 128;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)v[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = w[u];
+    }
+    if (i + U <= n) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)v[u]);
+      i += U;
+    }
+    for (; i < n; ++i) acc = __dadd_rn(acc, (double)__ldg(d + (size_t)i * kDim));
+    total += n;
+  }
+  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+  if (acc_out) acc_out[c] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K2: projections.  CTA = 128 descriptors x 192 planes, 512 threads; each
+// thread accumulates 4 descriptors x 12 planes in FP32 (48 FFMA per 4
+// LDS.128).  Planes live transposed in shared memory, descriptors centered
+// in shared memory (row stride 132 floats: conflict-free LDS.128).
+//
+// Certificate: |s32 - s_exact| <= gamma_{130} * sum|a_c||p_c|
+//                               <= 8e-6 * ||d-m||_2 * ||p||_2   (Cauchy-Schwarz)
+// and the reference FP64 result is within 1.5e-14*||d-m||*||p|| of s_exact,
+// so s32 > B  =>  s64 > 0 (bit 1) and s32 < -B => s64 < 0 (bit 0).  Anything
+// in [-B, B] goes to the FP64 fixup list.
+// ---------------------------------------------------------------------------
+constexpr int kAStride = 132;
+constexpr int kMaskWords = kPlaneChunk / 32 + 2;  // +2 guard words for 64-bit extracts
+constexpr float kDotBound = 8.0e-6f;
+constexpr float kDotBoundAbs = 1.0e-37f;
+
+__device__ __forceinline__ uint64_t extract_bits(const uint32_t* w, int start, int len) {
+  const int wi = start >> 5, sh = start & 31;
+  const uint64_t lo = (uint64_t)w[wi] | ((uint64_t)w[wi + 1] << 32);
+  const uint64_t hi = w[wi + 2];
+  uint64_t v = (lo >> sh) | (sh ? (hi << (64 - sh)) : 0ull);
+  return len >= 64 ? v : (v & ((1ull << len) - 1ull));
+}
+
+__global__ void __launch_bounds__(512, 1)
+    codes_kernel(HashDev h, const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
+                 const uint32_t* __restrict__ tile_start, const float* __restrict__ mean,
+                 Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
+                 uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) float smem_f[];
+  float* sP = smem_f;                                  // [128][192]
+  float* sA = sP + kDim * kPlaneChunk;                 // [128][132]
+  float* sNrm = sA + kCodesTile * kAStride;            // [128]
+  float* sPn = sNrm + kCodesTile;                      // [192]
+  float* sMean = sPn + kPlaneChunk;                    // [128]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(sMean + kDim);  // [128][8]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t img = tile_img[blockIdx.x];
+  const ImgDev im = imgs[img];
+  const uint32_t i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(im.n - i0));
+  const int p0 = blockIdx.y * kPlaneChunk;
+  const int np = min(kPlaneChunk, h.n_planes - p0);
+  const bool single_chunk = gridDim.y == 1;
+
+  // planes chunk -> smem (coalesced float4 rows of the transposed matrix)
+  for (int e = tid; e < kDim * (kPlaneChunk / 4); e += blockDim.x) {
+    const int c = e / (kPlaneChunk / 4), q4 = e % (kPlaneChunk / 4);
+    reinterpret_cast<float4*>(sP)[e] =
+        __ldg(reinterpret_cast<const float4*>(h.planes_t + (size_t)c * h.n_planes_pad + p0) + q4);
+  }
+  for (int e = tid; e < kPlaneChunk; e += blockDim.x) sPn[e] = __ldg(h.plane_norm + p0 + e);
+  if (tid < kDim) sMean[tid] = mean[tid];
+  for (int e = tid; e < kCodesTile * kMaskWords; e += blockDim.x) sMask[e] = 0u;
+  __syncthreads();
+
+  // centered descriptor tile + norms (one warp per row, float4 per lane)
+  for (int r = warp; r < kCodesTile; r += 16) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < nd) {
+      const float4 d = __ldg(reinterpret_cast<const float4*>(im.desc + (size_t)(i0 + r) * kDim) + lane);
+      const float4 m = reinterpret_cast<const float4*>(sMean)[lane];
+      a = make_float4(d.x - m.x, d.y - m.y, d.z - m.z, d.w - m.w);
+    }
+    *reinterpret_cast<float4*>(sA + r * kAStride + 4 * lane) = a;
+    float ss = a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+    if (lane == 0) sNrm[r] = sqrtf(ss) * 1.00001f;
+  }
+  __syncthreads();
+
+  const int pg = warp;  // 16 plane groups x 12 planes
+  float acc[4][12];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int j = 0; j < 12; ++j) acc[r][j] = 0.f;
+
+#pragma unroll 2
+  for (int c4 = 0; c4 < kDim / 4; ++c4) {
+    float4 a[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      a[r] = *reinterpret_cast<const float4*>(sA + (r * 32 + lane) * kAStride + c4 * 4);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const float* prow = sP + (c4 * 4 + cc) * kPlaneChunk + pg * 12;
+      const float4 q0 = *reinterpret_cast<const float4*>(prow);
+      const float4 q1 = *reinterpret_cast<const float4*>(prow + 4);
+      const float4 q2 = *reinterpret_cast<const float4*>(prow + 8);
+      const float pv[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float av = cc == 0 ? a[r].x : cc == 1 ? a[r].y : cc == 2 ? a[r].z : a[r].w;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) acc[r][j] = fmaf(av, pv[j], acc[r][j]);
+      }
+    }
+  }
+
+  // certified signs -> per-descriptor plane mask in smem
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = r * 32 + lane;
+    if (i < nd) {
+      const float bn = kDotBound * sNrm[i];
+      uint32_t bits = 0;
+#pragma unroll
+      for (int j = 0; j < 12; ++j) {
+        const int p = pg * 12 + j;
+        if (p < np) {
+          const float s = acc[r][j];
+          const float B = fmaf(bn, sPn[p], kDotBoundAbs);
+          if (s > B) {
+            bits |= 1u << j;
+          } else if (!(s < -B)) {
+            const uint32_t slot = atomicAdd(fix_count, 1u);
+            if (slot < fix_cap) {
+              Fixup f;
+              f.img = img;
+              f.desc = i0 + i;
+              f.plane = p0 + p;
+              f.pad = 0;
+              fix[slot] = f;
+            } else {
+              atomicOr(overflow + img, 1u);
+            }
+          }
+        }
+      }
+      if (bits) {
+        const int off = pg * 12, wi = off >> 5, sh = off & 31;
+        atomicOr(&sMask[i * kMaskWords + wi], bits << sh);
+        if (sh > 20) atomicOr(&sMask[i * kMaskWords + wi + 1], bits >> (32 - sh));
+      }
+    }
+  }
+  __syncthreads();
+
+  // assemble coarse bucket ids and fine words (4 threads per descriptor)
+  const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
+  const int n_words = L + h.fwp;
+  for (int e = tid; e < nd * n_words; e += blockDim.x) {
+    const int i = e / n_words, wd = e % n_words;
+    const uint32_t* mk = sMask + i * kMaskWords;
+    const size_t gi = i0 + i;
+    if (wd < L) {
+      const int lo = max(wd * m, p0), hi = min(wd * m + m, p0 + np);
+      if (lo < hi) {
+        const uint32_t v = (uint32_t)(extract_bits(mk, lo - p0, hi - lo) << (lo - wd * m));
+        if (single_chunk) im.coarse[gi * L + wd] = v;
+        else if (v) atomicOr(im.coarse + gi * L + wd, v);
+      }
+    } else {
+      const int fwi = wd - L;
+      const int b0 = coarse_planes + 64 * fwi;
+      const int lo = max(b0, p0), hi = min(min(b0 + 64, coarse_planes + fb), p0 + np);
+      uint64_t v = 0;
+      if (lo < hi) v = extract_bits(mk, lo - p0, hi - lo) << (lo - b0);
+      if (single_chunk) im.fine[gi * h.fwp + fwi] = v;
+      else if (v) atomicOr(reinterpret_cast<unsigned long long*>(im.fine + gi * h.fwp + fwi),
+                           (unsigned long long)v);
+    }
+  }
+}
+
+__device__ __forceinline__ double centered_dot_ref(const float* __restrict__ d,
+                                                   const float* __restrict__ mean,
+                                                   const float* __restrict__ p) {
+  // hashmatch.cpp:27-33: s += ((double)d - (double)mean) * (double)p, no contraction
+  double s = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < kDim; ++c)
+    s = __dadd_rn(s, __dmul_rn(__dsub_rn((double)d[c], (double)mean[c]), (double)p[c]));
+  return s;
+}
+
+__device__ __forceinline__ void set_code_bit(const HashDev& h, const ImgDev& im, uint32_t desc,
+                                             uint32_t plane) {
+  const uint32_t cp = (uint32_t)(h.tables * h.coarse_bits);
+  if (plane < cp) {
+    const uint32_t t = plane / h.coarse_bits, b = plane % h.coarse_bits;
+    atomicOr(im.coarse + (size_t)desc * h.tables + t, 1u << b);
+  } else {
+    const uint32_t f = plane - cp;
+    atomicOr(reinterpret_cast<unsigned long long*>(im.fine + (size_t)desc * h.fwp + (f >> 6)),
+             1ull << (f & 63));
+  }
+}
+
+__global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
+                                   const float* __restrict__ mean, const Fixup* __restrict__ fix,
+                                   const uint32_t* __restrict__ fix_count, uint32_t fix_cap,
+                                   unsigned long long* fixed_bits) {
+  const uint32_t n = min(*fix_count, fix_cap);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const Fixup f = fix[e];
+    const ImgDev im = imgs[f.img];
+    const double s = centered_dot_ref(im.desc + (size_t)f.desc * kDim, mean,
+                                      h.planes + (size_t)f.plane * kDim);
+    if (s > 0.0) set_code_bit(h, im, f.desc, f.plane);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && fixed_bits) atomicAdd(fixed_bits, (unsigned long long)n);
+}
+
+// Fixup-list overflow (pathological inputs, e.g. thousands of descriptors
+// equal to the mean): recompute every projection of the flagged images in
+// FP64 and OR in the positive ones (certified 1-bits are already set).
+__global__ void codes_overflow_kernel(HashDev h, const ImgDev* __restrict__ imgs, int n_imgs,
+                                      const float* __restrict__ mean,
+                                      const uint32_t* __restrict__ overflow) {
+  for (int ii = 0; ii < n_imgs; ++ii) {
+    if (!overflow[ii]) continue;
+    const ImgDev im = imgs[ii];
+    const uint64_t total = (uint64_t)im.n * h.n_planes;
+    for (uint64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t desc = (uint32_t)(e / h.n_planes), plane = (uint32_t)(e % h.n_planes);
+      const double s = centered_dot_ref(im.desc + (size_t)desc * kDim, mean,
+                                        h.planes + (size_t)plane * kDim);
+      if (s > 0.0) set_code_bit(h, im, desc, plane);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: bucket index per (image, row): histogram -> per-table scan -> scatter.
+// The order of train indices inside a bucket is irrelevant to the result:
+// candidates are ranked by the unique key (hamming, train_idx).
+// ---------------------------------------------------------------------------
+__global__ void tables_hist_kernel(HashDev h, const ImgDev* __restrict__ imgs,
+                                   const uint32_t* __restrict__ tile_img,
+                                   const uint32_t* __restrict__ tile_start) {
+  const ImgDev im = imgs[tile_img[blockIdx.x]];
+  const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
+  if (i >= im.n) return;
+  for (int t = 0; t < h.tables; ++t) {
+    const uint32_t b = im.coarse[(size_t)i * h.tables + t];
+    atomicAdd(im.offsets + (size_t)t * (h.n_buckets + 1) + b + 1, 1u);
+  }
+}
+
+__device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) s_warp[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    s_warp[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) v += s_warp[warp - 1];
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry;
+  const ImgDev im = imgs[blockIdx.x];
+  const int t = blockIdx.y;
+  uint32_t* off = im.offsets + (size_t)t * (h.n_buckets + 1);
+  uint32_t* cur = im.cursor + (size_t)t * h.n_buckets;
+  uint32_t carry = 0;
+  for (int base = 0; base < h.n_buckets; base += blockDim.x) {
+    const int b = base + threadIdx.x;
+    const uint32_t v = b < h.n_buckets ? off[b + 1] : 0u;
+    const uint32_t incl = block_incl_scan(v, s_warp) + carry;
+    if (b < h.n_buckets) {
+      off[b + 1] = incl;
+      cur[b] = incl - v;
+    }
+    if (threadIdx.x == blockDim.x - 1) s_carry = incl;
+    __syncthreads();
+    carry = s_carry;
+    __syncthreads();
+  }
+}
+
+__global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs,
+                                      const uint32_t* __restrict__ tile_img,
+                                      const uint32_t* __restrict__ tile_start) {
+  const ImgDev im = imgs[tile_img[blockIdx.x]];
+  const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
+  if (i >= im.n) return;
+  for (int t = 0; t < h.tables; ++t) {
+    const uint32_t b = im.coarse[(size_t)i * h.tables + t];
+    const uint32_t pos = atomicAdd(im.cursor + (size_t)t * h.n_buckets + b, 1u);
+    im.slots[(size_t)t * im.n + pos] = i;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: the cascade.  CTA = (image pair, 1024-query range), thread per query.
+//   1. train fine codes -> shared memory with one TMA bulk copy
+//      (cp.async.bulk + mbarrier complete_tx) while each thread loads its
+//      query code and bucket ids;
+//   2. bucket union over the tables, 128-bit Hamming via POPC, top-K of the
+//      unique key (hamming << idx_bits | train_idx) kept sorted in registers
+//      (duplicates from several tables have identical keys and are skipped:
+//      this is the reference's last_seen dedup + counting sort, :154-200);
+//   3. warp-cooperative re-rank: per query, lane l holds dims 4l..4l+3 and
+//      every kept candidate row is one coalesced 512-byte load; FP32 squared
+//      distances with relative error <= 8e-6 certify the (dist, idx) argmin
+//      and the ratio test; uncertified queries are recomputed with the
+//      reference's sequential FP64 euclidean (:35-42) and sort (:201-208).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int FWP, int KM, int NT, bool SMEM>
+__global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long s_bar;
+  const PairWork w = a.work[blockIdx.x];
+  const ImgDev T = a.imgs[w.t_img];
+  const ImgDev Q = a.imgs[w.q_img];
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  const uint64_t* tcodes = T.fine;
+  if constexpr (SMEM) {
+    const uint32_t bytes = ((T.n * FWP * 8u) + 15u) & ~15u;
+    if (tid == 0) {
+      const uint32_t bar = smem_addr(&s_bar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                   : "memory");
+      constexpr uint32_t kChunk = 1u << 15;
+      for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t sz = min(kChunk, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(smem_raw + off)),
+            "l"(reinterpret_cast<const char*>(T.fine) + off), "r"(sz), "r"(bar)
+            : "memory");
+      }
+    }
+  }
+
+  const uint32_t q = w.q_begin + tid;
+  const bool active = q < w.q_end;
+  const uint32_t idx_mask = (1u << a.idx_bits) - 1u;
+  uint64_t qc[FWP];
+#pragma unroll
+  for (int x = 0; x < FWP; ++x) qc[x] = active ? __ldg(Q.fine + (size_t)q * FWP + x) : 0ull;
+
+  if constexpr (SMEM) {
+    __syncthreads();  // mbarrier init visible
+    const uint32_t bar = smem_addr(&s_bar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  }
+
+  uint32_t top[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) top[k] = kEmpty;
+  uint32_t thr = kEmpty;
+  const int K = a.k;
+
+  if (active) {
+    const int nb1 = a.n_buckets + 1;
+    for (int t = 0; t < a.tables; ++t) {
+      const uint32_t b = __ldg(Q.coarse + (size_t)q * a.tables + t);
+      const uint32_t* off = T.offsets + (size_t)t * nb1;
+      const uint32_t lo = __ldg(off + b), hi = __ldg(off + b + 1);
+      const uint32_t* sl = T.slots + (size_t)t * T.n;
+      for (uint32_t s = lo; s < hi; ++s) {
+        const uint32_t j = __ldg(sl + s);
+        uint32_t hsum = 0;
+        if constexpr (SMEM && FWP % 2 == 0) {
+          const ulonglong2* sc = reinterpret_cast<const ulonglong2*>(smem_raw) + (size_t)j * (FWP / 2);
+#pragma unroll
+          for (int x = 0; x < FWP / 2; ++x) {
+            const ulonglong2 v = sc[x];
+            hsum += __popcll(qc[2 * x] ^ v.x) + __popcll(qc[2 * x + 1] ^ v.y);
+          }
+        } else if constexpr (SMEM) {
+          const uint64_t* sc = reinterpret_cast<const uint64_t*>(smem_raw) + (size_t)j * FWP;
+#pragma unroll
+          for (int x = 0; x < FWP; ++x) hsum += __popcll(qc[x] ^ sc[x]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < FWP; ++x) hsum += __popcll(qc[x] ^ __ldg(tcodes + (size_t)j * FWP + x));
+        }
+        const uint32_t key = (hsum << a.idx_bits) | j;
+        if (key < thr) {
+          bool dup = false;
+#pragma unroll
+          for (int k = 0; k < KM; ++k) dup |= top[k] == key;
+          if (!dup) {
+#pragma unroll
+            for (int k = KM - 1; k > 0; --k)
+              top[k] = top[k - 1] > key ? top[k - 1] : (top[k] > key ? key : top[k]);
+            top[0] = top[0] > key ? key : top[0];
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+              if (k == K - 1) thr = top[k];
+          }
+        }
+      }
+    }
+  }
+
+  // ---- re-rank + ratio test, one query at a time per warp ----
+  const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
+  const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
+  const double ratio = a.ratio;
+  const double r2 = ratio * ratio;
+  int32_t my_result = -1;
+  for (int src = 0; src < 32; ++src) {
+    const int act = __shfl_sync(kFull, active ? 1 : 0, src);
+    if (!act) continue;
+    const uint32_t qs = __shfl_sync(kFull, q, src);
+    uint32_t cand[KM];
+    int kept = 0;
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      cand[k] = __shfl_sync(kFull, top[k], src);
+      kept += (k < K && cand[k] != kEmpty) ? 1 : 0;
+    }
+    int32_t result = -1;
+    if (kept == 1) {
+      result = (int32_t)(cand[0] & idx_mask);
+    } else if (kept > 1) {
+      const float4 qv = __ldg(Qd + (size_t)qs * 32 + lane);
+      float part[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        part[k] = 0.f;
+        if (k < kept) {
+          const float4 tv = __ldg(Td + (size_t)(cand[k] & idx_mask) * 32 + lane);
+          const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
+          part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+        }
+      }
+      // transpose-reduce: after log2(KM) halving steps lane l holds the sum
+      // of candidate idx(l); the remaining steps finish the 32-lane sum.
+      constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
+#pragma unroll
+      for (int st = 0; st < kLog; ++st) {
+        const int half = (KM >> st) >> 1, m = 16 >> st;
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < KM / 2; ++i) {
+          if (i < half) {
+            const float send = up ? part[i] : part[i + half];
+            const float keep = up ? part[i + half] : part[i];
+            part[i] = keep + __shfl_xor_sync(kFull, send, m);
+          }
+        }
+      }
+      float red = part[0];
+#pragma unroll
+      for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
+      float sv[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        // lane holding candidate k: bit b of k sits at lane bit (4 - (kLog-1-b))
+        int src_lane = 0;
+#pragma unroll
+        for (int b = 0; b < kLog; ++b)
+          if (k & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
+        sv[k] = __shfl_sync(kFull, red, src_lane);
+      }
+      // certified decision: argmin by (s32, train_idx), then the runner-up value
+      int is = 0;
+      float s_min = sv[0];
+      uint32_t i_min = cand[0] & idx_mask;
+#pragma unroll
+      for (int k = 1; k < KM; ++k)
+        if (k < kept) {
+          const uint32_t ik = cand[k] & idx_mask;
+          if (sv[k] < s_min || (sv[k] == s_min && ik < i_min)) {
+            is = k;
+            s_min = sv[k];
+            i_min = ik;
+          }
+        }
+      float s_2 = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int k = 0; k < KM; ++k)
+        if (k < kept && k != is) s_2 = fminf(s_2, sv[k]);
+      const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
+      const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
+      const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
+      const bool reject = finite && (double)s_min * lo_f >= r2 * ((double)s_2 * hi_f);
+      if (accept) {
+        result = (int32_t)i_min;
+      } else if (!reject) {
+        // FP64 reference path (hashmatch.cpp:35-42, :196-208)
+        uint32_t mine = kEmpty;
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+          if (k == lane) mine = cand[k];
+        double e = 0.0;
+        if (lane < kept) {
+          const float* qd = Q.desc + (size_t)qs * kDim;
+          const float* td = T.desc + (size_t)(mine & idx_mask) * kDim;
+          double s = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < kDim; ++c) {
+            const double d = __dsub_rn((double)__ldg(qd + c), (double)__ldg(td + c));
+            s = __dadd_rn(s, __dmul_rn(d, d));
+          }
+          e = __dsqrt_rn(s);
+        }
+        int first = 0;
+        double e_first = __shfl_sync(kFull, e, 0);
+        uint32_t i_first = cand[0] & idx_mask;
+        double ev[KM];
+#pragma unroll
+        for (int k = 0; k < KM; ++k) ev[k] = __shfl_sync(kFull, e, k);
+#pragma unroll
+        for (int k = 1; k < KM; ++k)
+          if (k < kept) {
+            const uint32_t ik = cand[k] & idx_mask;
+            if (ev[k] < e_first || (ev[k] == e_first && ik < i_first)) {
+              first = k;
+              e_first = ev[k];
+              i_first = ik;
+            }
+          }
+        double e_second = __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+          if (k < kept && k != first) e_second = fmin(e_second, ev[k]);
+        if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
+        if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
+      }
+    }
+    if (lane == src) my_result = result;
+  }
+
+  if (active) a.dense[a.dense_off[w.pair] + q] = my_result;
+  const unsigned hit = __ballot_sync(kFull, active && my_result >= 0);
+  if (lane == 0 && hit) atomicAdd(a.pair_count + w.pair, (uint32_t)__popc(hit));
+}
+
+// ---------------------------------------------------------------------------
+// K6: per-launch exclusive scan of match counts (appending after the running
+// total of earlier rows) and ascending-query compaction of the dense arrays.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __restrict__ counts, int n,
+                                                           uint64_t* __restrict__ offsets,
+                                                           unsigned long long* running_total) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ unsigned long long s_carry;
+  if (threadIdx.x == 0) s_carry = *running_total;
+  __syncthreads();
+  if (threadIdx.x == 0) offsets[0] = s_carry;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < n ? counts[i] : 0u;
+    const unsigned long long carry = s_carry;
+    const uint32_t incl = block_incl_scan(v, s_warp);
+    if (i < n) offsets[i + 1] = carry + incl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = carry + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *running_total = s_carry;
+}
+
+__global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict__ dense,
+                                                       const uint64_t* __restrict__ dense_off,
+                                                       const uint32_t* __restrict__ nq,
+                                                       const uint64_t* __restrict__ out_off,
+                                                       int32_t* __restrict__ out) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_base;
+  const int p = blockIdx.x;
+  const int32_t* d = dense + dense_off[p];
+  const uint32_t n = nq[p];
+  uint64_t base = out_off[p];
+  for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x) {
+    const uint32_t q = q0 + threadIdx.x;
+    const int32_t v = q < n ? d[q] : -1;
+    const uint32_t f = v >= 0 ? 1u : 0u;
+    const uint32_t incl = block_incl_scan(f, s_warp);
+    if (f) {
+      const uint64_t o = base + incl - 1;
+      out[2 * o] = (int32_t)q;
+      out[2 * o + 1] = v;
+    }
+    if (threadIdx.x == blockDim.x - 1) s_base = incl;
+    __syncthreads();
+    base += s_base;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
+                     cudaStream_t s) {
+  row_mean_kernel<<<1, 128, 0, s>>>(imgs, n_imgs, mean_out, acc_out);
+}
+
+static size_t codes_smem_bytes() {
+  return sizeof(float) * (kDim * kPlaneChunk + kCodesTile * kAStride + kCodesTile + kPlaneChunk + kDim) +
+         sizeof(uint32_t) * kCodesTile * kMaskWords;
+}
+
+void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                  const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
+                  uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = codes_smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  // overflow flags live right after the fixup counter (see bmg_api.cpp)
+  uint32_t* overflow = fix_count + 1;
+  dim3 grid(n_tiles, (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
+  codes_kernel<<<grid, 512, smem, s>>>(h, imgs_dev, tile_img, tile_start, mean, fix, fix_count,
+                                       fix_cap, overflow);
+}
+
+void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,
+                        const Fixup* fix, const uint32_t* fix_count, uint32_t fix_cap,
+                        unsigned long long* fixed_bits, cudaStream_t s) {
+  codes_fixup_kernel<<<148, 256, 0, s>>>(h, imgs_dev, mean, fix, fix_count, fix_cap, fixed_bits);
+  codes_overflow_kernel<<<148, 256, 0, s>>>(h, imgs_dev, n_imgs, mean, fix_count + 1);
+}
+
+void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                   const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s) {
+  tables_hist_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
+  tables_scan_kernel<<<dim3(n_imgs, h.tables), 1024, 0, s>>>(h, imgs_dev);
+  tables_scatter_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
+}
+
+template <int FWP, int KM, int NT, bool SMEM>
+static void launch_match_t(const MatchLaunch& a, int n_work, size_t smem, cudaStream_t s) {
+  static int configured = -1;
+  if (configured != (int)smem) {
+    cudaFuncSetAttribute(match_kernel<FWP, KM, NT, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = (int)smem;
+  }
+  match_kernel<FWP, KM, NT, SMEM><<<n_work, NT, smem, s>>>(a);
+}
+
+template <int FWP>
+static void launch_match_fw(const MatchLaunch& a, int n_work, uint32_t max_train_n, cudaStream_t s,
+                            int* smem_used) {
+  const size_t code_bytes = (((size_t)max_train_n * FWP * 8u) + 15u) & ~size_t(15);
+  const bool use_smem = code_bytes <= (size_t)200 * 1024;
+  const size_t smem = use_smem ? code_bytes : 0;
+  if (smem_used) *smem_used = (int)smem;
+  if (a.k <= 8) {
+    if (use_smem) launch_match_t<FWP, 8, kMatchThreads, true>(a, n_work, smem, s);
+    else launch_match_t<FWP, 8, kMatchThreads, false>(a, n_work, 0, s);
+  } else {
+    if (use_smem) launch_match_t<FWP, 32, 256, true>(a, n_work, smem, s);
+    else launch_match_t<FWP, 32, 256, false>(a, n_work, 0, s);
+  }
+}
+
+void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev&, uint32_t max_train_n,
+                  cudaStream_t s, int* smem_used) {
+  switch (fwp) {
+    case 1: launch_match_fw<1>(a, n_work, max_train_n, s, smem_used); break;
+    case 2: launch_match_fw<2>(a, n_work, max_train_n, s, smem_used); break;
+    case 4: launch_match_fw<4>(a, n_work, max_train_n, s, smem_used); break;
+    case 8: launch_match_fw<8>(a, n_work, max_train_n, s, smem_used); break;
+    default: launch_match_fw<16>(a, n_work, max_train_n, s, smem_used); break;
+  }
+}
+
+void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
+                        unsigned long long* running_total, cudaStream_t s) {
+  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total);
+}
+
+void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
+                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s) {
+  if (n_pairs > 0) compact_kernel<<<n_pairs, 1024, 0, s>>>(dense, dense_off, nq, out_off, out);
+}
+
+}  // namespace bmg

@@ -1,0 +1,310 @@
+"""Python mirror of bandmatch's executor surface (include/bandmatch/engine.hpp,
+include/bandmatch/mbr.hpp): SchedulePlan + plan JSON (mbr.cpp:378-463),
+DeviceArena counters, ``execute_plan`` (engine.cpp:411-527) whose row body runs
+on the B200 through the C ABI (``bmg_execute_plan``).
+
+The block scheduler itself stays on the host and is an *input* here: plans are
+read from the reference's plan JSON.  Verification (SAO + RANSAC) stays on the
+CPU: pass ``on_pair`` to receive every pair's initial matches as soon as they
+are in host memory (the reference's VerifyPool hand-off, engine.cpp:478-479).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import BandmatchError, check, ptr
+from .hashmatch import FeatureSet, HashFunctions, Matcher, MatchParams, PairMatches
+
+__all__ = ["ScheduleBlock", "BlockRow", "ScheduleIteration", "SchedulePlan", "read_plan",
+           "write_plan", "plan_from_json", "DeviceArena", "ExecuteOptions", "IterationMetrics",
+           "PipelineMetrics", "ExecutionResult", "execute_plan", "arena_units_for", "flatten_plan"]
+
+
+@dataclass
+class ScheduleBlock:
+    row_chunk: int = 0
+    col_chunk: int = 0
+    row_images: list = field(default_factory=list)
+    col_images: list = field(default_factory=list)
+    pairs: list = field(default_factory=list)  # [(a, b)] with a < b
+
+
+@dataclass
+class BlockRow:
+    row_chunk: int = 0
+    row_images: list = field(default_factory=list)
+    blocks: list = field(default_factory=list)
+    evict_after: list = field(default_factory=list)
+
+    def needed(self) -> list:
+        """engine.cpp:434-436: row_images ∪ every block's col_images, ascending."""
+        s = set(self.row_images)
+        for b in self.blocks:
+            s.update(b.col_images)
+        return sorted(s)
+
+
+@dataclass
+class ScheduleIteration:
+    dimension: int = 0
+    bandwidth_before: int = 0
+    bandwidth_after: int = 0
+    rows: list = field(default_factory=list)
+
+    def pair_count(self) -> int:
+        return sum(len(b.pairs) for r in self.rows for b in r.blocks)
+
+
+@dataclass
+class SchedulePlan:
+    strategy: str = ""
+    size_blk: int = 0
+    size_gpu: int = 0
+    final_dimension: int = 0
+    iterations: list = field(default_factory=list)
+
+    def pair_count(self) -> int:
+        return sum(it.pair_count() for it in self.iterations)
+
+    def pairs(self) -> list:
+        return sorted(tuple(p) for it in self.iterations for r in it.rows for b in r.blocks
+                      for p in b.pairs)
+
+
+def plan_from_json(j: dict) -> SchedulePlan:
+    try:
+        plan = SchedulePlan(j["strategy"], j["budget"]["size_blk"], j["budget"]["size_gpu"],
+                            j["final_dimension"])
+        for ji in j["iterations"]:
+            it = ScheduleIteration(ji["dimension"], ji["bandwidth_before"], ji["bandwidth_after"])
+            for jr in ji["rows"]:
+                row = BlockRow(jr["row_chunk"], list(jr["row_images"]), [], list(jr["evict_after"]))
+                for jb in jr["blocks"]:
+                    row.blocks.append(ScheduleBlock(
+                        jb["row_chunk"], jb["col_chunk"], list(jb["row_images"]),
+                        list(jb["col_images"]),
+                        [(min(a, b), max(a, b)) for a, b in jb["pairs"]]))
+                it.rows.append(row)
+            plan.iterations.append(it)
+    except (KeyError, TypeError) as e:
+        raise BandmatchError("FormatError", f"plan JSON missing fields: {e}")
+    return plan
+
+
+def read_plan(path) -> SchedulePlan:
+    """read_plan, mbr.cpp:421-463."""
+    try:
+        with open(path) as f:
+            j = json.load(f)
+    except OSError:
+        raise BandmatchError("FormatError", f"cannot open {path} for reading")
+    except json.JSONDecodeError as e:
+        raise BandmatchError("FormatError", f"invalid plan JSON in {path}: {e}")
+    return plan_from_json(j)
+
+
+def write_plan(path, plan: SchedulePlan, config_echo: str | None = None) -> None:
+    """write_plan, mbr.cpp:378-419."""
+    j = {}
+    if config_echo is not None:
+        j["config"] = json.loads(config_echo)
+    j.update({"strategy": plan.strategy,
+              "budget": {"size_blk": plan.size_blk, "size_gpu": plan.size_gpu},
+              "final_dimension": plan.final_dimension, "iterations": []})
+    for it in plan.iterations:
+        ji = {"dimension": it.dimension, "bandwidth_before": it.bandwidth_before,
+              "bandwidth_after": it.bandwidth_after, "rows": []}
+        for r in it.rows:
+            ji["rows"].append({"row_chunk": r.row_chunk, "row_images": r.row_images,
+                               "evict_after": r.evict_after,
+                               "blocks": [{"row_chunk": b.row_chunk, "col_chunk": b.col_chunk,
+                                           "row_images": b.row_images, "col_images": b.col_images,
+                                           "pairs": [list(p) for p in b.pairs]}
+                                          for b in r.blocks]})
+        j["iterations"].append(ji)
+    with open(path, "w") as f:
+        f.write(json.dumps(j, indent=2) + "\n")
+
+
+@dataclass
+class FlatPlan:
+    """SchedulePlan flattened into the bmg_plan arrays (include/bandmatch_gpu.h)."""
+    rows_per_iteration: np.ndarray
+    row_needed_offsets: np.ndarray
+    needed_ids: np.ndarray
+    row_pair_offsets: np.ndarray
+    pairs: np.ndarray
+    row_evict_offsets: np.ndarray
+    evict_ids: np.ndarray
+
+    def c(self):
+        return _lib.PlanC(len(self.rows_per_iteration), ptr(self.rows_per_iteration),
+                          len(self.row_needed_offsets) - 1, ptr(self.row_needed_offsets),
+                          ptr(self.needed_ids), ptr(self.row_pair_offsets), ptr(self.pairs),
+                          ptr(self.row_evict_offsets), ptr(self.evict_ids))
+
+
+def flatten_plan(plan: SchedulePlan, rows=None) -> FlatPlan:
+    """Flatten (optionally only the rows with the given global indices, which
+    keeps their iteration grouping -- used to shard rows across GPUs)."""
+    rpi, nd_off, nd, p_off, prs, ev_off, ev = [], [0], [], [0], [], [0], []
+    g = 0
+    for it in plan.iterations:
+        cnt = 0
+        for r in it.rows:
+            take = rows is None or g in rows
+            g += 1
+            if not take:
+                continue
+            cnt += 1
+            nd.extend(r.needed())
+            nd_off.append(len(nd))
+            for b in r.blocks:
+                for a, bb in b.pairs:
+                    prs.extend((a, bb))
+            p_off.append(len(prs) // 2)
+            ev.extend(r.evict_after)
+            ev_off.append(len(ev))
+        rpi.append(cnt)
+    u = lambda x: np.ascontiguousarray(x if len(x) else [0], np.uint64)
+    return FlatPlan(u(rpi) if rpi else np.zeros(1, np.uint64)[:0].copy(), u(nd_off), u(nd),
+                    u(p_off), u(prs), u(ev_off), u(ev))
+
+
+class DeviceArena:
+    """DeviceArena (engine.hpp:20-44) backed by a B200 context: capacity in
+    descriptor units, uploads are real H2D copies into HBM."""
+
+    def __init__(self, capacity_units: int, hf: HashFunctions, device: int = 0):
+        self.matcher = Matcher(hf, capacity_units, device)
+
+    def _s(self):
+        return self.matcher.arena_stats()
+
+    def capacity(self): return self._s()["capacity"]
+    def occupancy(self): return self._s()["occupancy"]
+    def peak_occupancy(self): return self._s()["peak_occupancy"]
+    def uploads(self): return self._s()["uploads"]
+    def evictions(self): return self._s()["evictions"]
+    def units_uploaded(self): return self._s()["units_uploaded"]
+    def resident_count(self): return self._s()["resident_count"]
+    def resident(self, image_id): return self.matcher.resident(image_id)
+    def upload(self, image_id, desc): self.matcher.upload(image_id, desc)
+    def evict(self, image_id): self.matcher.evict(image_id)
+
+
+@dataclass
+class ExecuteOptions:
+    match: MatchParams = field(default_factory=MatchParams)
+    on_pair: object = None    # callable(query_image, train_image, matches (n,2) int32)
+    on_upload: object = None  # DeviceBackend::on_upload(image_id, units)
+    on_evict: object = None   # DeviceBackend::on_evict(image_id)
+
+
+@dataclass
+class IterationMetrics:
+    pairs: int = 0
+    uploads: int = 0
+    units_uploaded: int = 0
+
+
+@dataclass
+class PipelineMetrics:
+    strategy: str = ""
+    pairs_matched: int = 0
+    initial_matches: int = 0
+    verified_matches: int = 0
+    uploads: int = 0
+    evictions: int = 0
+    units_uploaded: int = 0
+    peak_occupancy: int = 0
+    utilization_proxy: float = 0.0
+    per_iteration: list = field(default_factory=list)
+    wall_time_s: float = 0.0
+    pairs_per_second: float = 0.0
+
+
+@dataclass
+class ExecutionResult:
+    matches: list
+    metrics: PipelineMetrics
+    outcomes: list = field(default_factory=list)
+
+
+def arena_units_for(features: dict, gpu_images: int) -> int:
+    """arena_units_for, engine.cpp:403-409."""
+    largest = max((fs.size() for fs in features.values()), default=0)
+    return largest * max(0, gpu_images)
+
+
+def _feature_views(features: dict):
+    views = (_lib.FeatureViewC * max(1, len(features)))()
+    keep = []
+    for i, (iid, fs) in enumerate(features.items()):
+        d = fs.descriptors if isinstance(fs, FeatureSet) else np.ascontiguousarray(fs, np.float32)
+        keep.append(d)
+        views[i] = _lib.FeatureViewC(int(iid), ptr(d) if d.size else None, d.shape[0])
+    return views, keep
+
+
+def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
+                 opts: ExecuteOptions = ExecuteOptions(), rows=None, flat: FlatPlan | None = None,
+                 views=None) -> ExecutionResult:
+    """execute_plan (engine.cpp:411-527) with verification off: the row body
+    (uploads, mean, codes, bucket tables, cascade matching) runs on the B200.
+    Results are sorted by IdPair.  ``rows`` restricts execution to a subset of
+    global row indices (multi-GPU sharding)."""
+    L = _lib.load()
+    flat = flat or flatten_plan(plan, rows)
+    views, keep = views or _feature_views(features)
+    pc = flat.c()
+    cbs = []
+
+    def wrap(fn, ctype, conv):
+        if fn is None:
+            return ctype()
+        cb = ctype(conv)
+        cbs.append(cb)
+        return cb
+
+    on_pair = wrap(opts.on_pair, _lib.PAIR_CB,
+                   lambda u, q, t, m, n: opts.on_pair(
+                       q, t, np.ctypeslib.as_array(m, (2 * n,)).reshape(-1, 2).copy() if n else
+                       np.zeros((0, 2), np.int32)))
+    on_up = wrap(opts.on_upload, _lib.UPLOAD_HOOK, lambda u, i, n: opts.on_upload(i, n))
+    on_ev = wrap(opts.on_evict, _lib.EVICT_HOOK, lambda u, i: opts.on_evict(i))
+    oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None)
+    h = C.c_void_p()
+    check(L.bmg_execute_plan(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc),
+                             C.byref(h)))
+    try:
+        npairs = L.bmg_result_pair_count(h)
+        nm = L.bmg_result_match_count(h)
+        ids = np.zeros(2 * max(npairs, 1), np.uint64)
+        offs = np.zeros(npairs + 1, np.uint64)
+        m = np.zeros(2 * max(nm, 1), np.int32)
+        check(L.bmg_result_copy(h, ptr(ids), ptr(offs), ptr(m)))
+        counters = np.zeros(6, np.uint64)
+        wall = C.c_double(0)
+        check(L.bmg_result_metrics(h, ptr(counters), C.byref(wall)))
+        its = []
+        for i in range(L.bmg_result_iteration_count(h)):
+            o = np.zeros(3, np.uint64)
+            check(L.bmg_result_iteration(h, i, ptr(o)))
+            its.append(IterationMetrics(int(o[0]), int(o[1]), int(o[2])))
+    finally:
+        L.bmg_result_free(h)
+    matches = [PairMatches(int(ids[2 * p]), int(ids[2 * p + 1]),
+                           m[2 * int(offs[p]): 2 * int(offs[p + 1])].reshape(-1, 2).copy())
+               for p in range(npairs)]
+    c = [int(x) for x in counters]
+    met = PipelineMetrics(plan.strategy, c[0], c[1], 0, c[2], c[3], c[4], c[5],
+                          c[0] / c[2] if c[2] else 0.0, its, wall.value,
+                          c[0] / wall.value if wall.value > 0 else 0.0)
+    del keep
+    return ExecutionResult(matches, met)

@@ -1,0 +1,98 @@
+"""GPU execute_plan (engine.cpp:411-527, verification off) against the
+compiled reference's execute_plan on the same scene and MBR plan: identical
+match lists per pair, identical arena counters (test_engine.cpp:265-324)."""
+import numpy as np
+import pytest
+
+import paper_2505_22089_b200 as bm
+from paper_2505_22089_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(reference, tmp_path, n_images, ppi, band, size_blk, size_gpu, seed=7, k=8,
+             ratio=0.5):
+    imgs, pairs = reference.generate_synthetic(n_images, ppi, band, 0.02, 0.2, seed)
+    plan_path = tmp_path / "plan.json"
+    reference.iterate_schedule(np.arange(n_images), pairs, size_blk, size_gpu, plan_path)
+    plan = bm.read_plan(plan_path)
+    hseed = bm.seed_for(42, "matching")
+    hf = bm.make_hash_functions(hseed)
+    feats = {i: bm.FeatureSet(i, d) for i, d in enumerate(imgs)}
+    cap = engine.arena_units_for(feats, size_gpu)
+    ref, ref_counters, _ = reference.execute_plan(plan_path, dict(enumerate(imgs)), hseed,
+                                                  k=k, ratio=ratio, capacity_units=cap)
+    arena = bm.DeviceArena(cap, hf)
+    ups, evs = [], []
+    opts = bm.ExecuteOptions(bm.MatchParams(k, ratio), on_upload=lambda i, n: ups.append((i, n)),
+                             on_evict=lambda i: evs.append(i))
+    res = bm.execute_plan(plan, feats, arena, opts)
+    return plan, ref, ref_counters, res, arena, ups, evs, feats
+
+
+def test_band_block_plan_equals_reference(reference, tmp_path):
+    plan, ref, rc, res, arena, ups, evs, feats = run_both(reference, tmp_path, 12, 600, 3, 3, 6)
+    assert len(plan.iterations) >= 1
+    got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    assert list(got) == sorted(ref)
+    for key, m in ref.items():
+        assert np.array_equal(got[key], m), key
+    met = res.metrics
+    assert met.pairs_matched == rc["pairs_matched"]
+    assert met.initial_matches == rc["initial_matches"]
+    assert met.uploads == rc["uploads"] and met.evictions == rc["evictions"]
+    assert met.units_uploaded == rc["units_uploaded"]
+    assert met.peak_occupancy == rc["peak_occupancy"]
+    assert len(ups) == met.uploads and len(evs) == met.evictions
+    assert sum(n for _, n in ups) == met.units_uploaded
+    assert arena.occupancy() == 0
+    assert sum(it.pairs for it in met.per_iteration) == met.pairs_matched
+
+
+def test_config2_block_equals_reference(reference, tmp_path):
+    # BASELINE config 2 shape at reduced descriptor count: 32 images, band 11,
+    # iterate_schedule(16, 32) -> 2 rows, 286 pairs
+    plan, ref, rc, res, *_ = run_both(reference, tmp_path, 32, 1024, 11, 16, 32)
+    assert rc["pairs_matched"] == 286
+    got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    for key, m in ref.items():
+        assert np.array_equal(got[key], m), key
+
+
+def test_capacity_and_missing_image_errors(reference, tmp_path):
+    imgs, pairs = reference.generate_synthetic(6, 50, 1, 0.02, 0.2, 3)
+    plan_path = tmp_path / "plan.json"
+    reference.iterate_schedule(np.arange(6), pairs, 2, 4, plan_path)
+    plan = bm.read_plan(plan_path)
+    hf = bm.make_hash_functions(31)
+    feats = {i: bm.FeatureSet(i, d) for i, d in enumerate(imgs)}
+    with pytest.raises(bm.BandmatchError) as e:
+        bm.execute_plan(plan, feats, bm.DeviceArena(60, hf))
+    assert e.value.code == "CapacityExceeded"
+    del feats[3]
+    with pytest.raises(bm.BandmatchError) as e:
+        bm.execute_plan(plan, feats, bm.DeviceArena(10 ** 6, hf))
+    assert e.value.code == "InvalidArgument"
+
+
+def test_arena_semantics():
+    hf = bm.make_hash_functions(5)
+    a = bm.DeviceArena(10, hf)
+    d = np.zeros((4, 128), np.float32)
+    a.upload(1, d)
+    a.upload(1, d)  # resident: no-op (engine.cpp:19)
+    assert a.uploads() == 1 and a.occupancy() == 4
+    with pytest.raises(bm.BandmatchError) as e:
+        a.upload(2, np.zeros((7, 128), np.float32))
+    assert e.value.code == "CapacityExceeded"
+    a.evict(1)
+    with pytest.raises(bm.BandmatchError) as e:
+        a.evict(1)
+    assert e.value.code == "NotResident"
+    assert a.peak_occupancy() == 4 and a.evictions() == 1
+
+
+def test_empty_plan_executes_to_zeros():
+    hf = bm.make_hash_functions(1)
+    res = bm.execute_plan(bm.SchedulePlan(), {}, bm.DeviceArena(0, hf))
+    assert res.matches == [] and res.metrics.pairs_matched == 0 and res.metrics.uploads == 0
