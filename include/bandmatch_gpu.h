@@ -57,7 +57,8 @@ typedef enum {
   BMG_NOT_RESIDENT = 4,       /* "NotResident"      */
   BMG_CUDA_ERROR = 5,         /* "CudaError"        */
   BMG_OUT_OF_MEMORY = 6,      /* "OutOfMemory"      */
-  BMG_UNSUPPORTED = 7         /* "Unsupported"      */
+  BMG_UNSUPPORTED = 7,        /* "Unsupported"      */
+  BMG_INVALID_SCENE = 8       /* "InvalidScene" / "ZeroVector" (features.cpp:60, 69-78) */
 } bmg_status;
 
 typedef struct bmg_context bmg_context;
@@ -144,7 +145,12 @@ typedef struct {
   bmg_upload_hook on_upload;      /* may be NULL */
   bmg_evict_hook on_evict;        /* may be NULL */
   void* hook_user;
+  uint32_t flags;                 /* BMG_EXEC_* */
 } bmg_execute_options;
+
+/* Keep every image resident: eviction directives are skipped (no free, no
+ * bookkeeping).  Used to measure the row body on HBM-resident inputs. */
+#define BMG_EXEC_RETAIN 1u
 
 /* ---- status ------------------------------------------------------------ */
 const char* bmg_status_name(int status);              /* "InvalidArgument", ... */
@@ -157,6 +163,15 @@ uint64_t bmg_seed_for(uint64_t root, const char* stage);
 /* make_hash_functions, hashmatch.cpp:53-69 (libstdc++ <random>, host only) */
 int bmg_make_hash_functions(uint64_t seed, const bmg_hash_params* params, float* coarse_out,
                             float* fine_out);
+
+/* Synthetic band-overlap scene, generate_synthetic (features.cpp:68-197):
+ * counts_out[n_images] first, then descriptors [sum counts][128] and
+ * optionally keypoints [sum counts][4] (x, y, scale, orientation). */
+int bmg_synthetic_counts(int n_images, int points_per_image, int overlap_band, double noise_sigma,
+                         double outlier_fraction, uint64_t* counts_out);
+int bmg_generate_synthetic(int n_images, int points_per_image, int overlap_band,
+                           double noise_sigma, double outlier_fraction, uint64_t seed,
+                           float* descriptors_out, float* keypoints_out);
 
 /* ---- context ----------------------------------------------------------- */
 int bmg_create(const bmg_config* config, bmg_context** out);
@@ -212,6 +227,9 @@ int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wa
 /* per-iteration metrics: pairs, uploads, units_uploaded (3 values each) */
 uint64_t bmg_result_iteration_count(const bmg_result* r);
 int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out[3]);
+/* Device time (CUDA events on the compute stream) from the first operation of
+ * the first row to the last kernel of the last row. */
+int bmg_result_device_ms(const bmg_result* r, double* ms_out);
 void bmg_result_free(bmg_result* r);
 
 /* ---- instrumentation ------------------------------------------------------ */

@@ -16,7 +16,7 @@ DIM = 128
 
 STATUS_NAMES = {
     0: "Ok", 1: "InvalidArgument", 2: "HashMismatch", 3: "CapacityExceeded",
-    4: "NotResident", 5: "CudaError", 6: "OutOfMemory", 7: "Unsupported",
+    4: "NotResident", 5: "CudaError", 6: "OutOfMemory", 7: "Unsupported", 8: "InvalidScene",
 }
 
 
@@ -71,7 +71,10 @@ EVICT_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64)
 
 class ExecOptionsC(C.Structure):
     _fields_ = [("match", MatchParamsC), ("on_pair", PAIR_CB), ("on_pair_user", C.c_void_p),
-                ("on_upload", UPLOAD_HOOK), ("on_evict", EVICT_HOOK), ("hook_user", C.c_void_p)]
+                ("on_upload", UPLOAD_HOOK), ("on_evict", EVICT_HOOK), ("hook_user", C.c_void_p),
+                ("flags", C.c_uint32)]
+
+EXEC_RETAIN = 1
 
 
 EXPORTED = [
@@ -81,7 +84,8 @@ EXPORTED = [
     "bmg_match", "bmg_compute_codes", "bmg_match_pair", "bmg_execute_plan",
     "bmg_result_pair_count", "bmg_result_match_count", "bmg_result_copy", "bmg_result_metrics",
     "bmg_result_iteration_count", "bmg_result_iteration", "bmg_result_free", "bmg_launch_count",
-    "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts",
+    "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_synthetic_counts",
+    "bmg_generate_synthetic", "bmg_result_device_ms",
 ]
 
 _lib = None
@@ -126,10 +130,14 @@ def load(path: Path = LIB_PATH):
         "bmg_result_iteration_count": (u64, [vp]),
         "bmg_result_iteration": (C.c_int, [vp, u64, vp]),
         "bmg_result_free": (None, [vp]),
+        "bmg_result_device_ms": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "bmg_launch_count": (u64, [vp]),
         "bmg_set_profiling": (C.c_int, [vp, C.c_int]),
         "bmg_kernel_time": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(u64)]),
         "bmg_fixup_counts": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64)]),
+        "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
+        "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                             u64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

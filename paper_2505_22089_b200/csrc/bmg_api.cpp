@@ -187,6 +187,7 @@ struct bmg_result {
   uint64_t counters[6] = {0, 0, 0, 0, 0, 0};
   std::vector<uint64_t> iterations;  // 3 per iteration
   double wall_s = 0.0;
+  double device_ms = 0.0;
 };
 
 namespace bmg {
@@ -623,6 +624,10 @@ void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
 }  // namespace
 }  // namespace bmg
 
+namespace bmg {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace bmg
+
 using namespace bmg;
 
 extern "C" {
@@ -637,6 +642,7 @@ const char* bmg_status_name(int status) {
     case BMG_CUDA_ERROR: return "CudaError";
     case BMG_OUT_OF_MEMORY: return "OutOfMemory";
     case BMG_UNSUPPORTED: return "Unsupported";
+    case BMG_INVALID_SCENE: return "InvalidScene";
     default: return "Unknown";
   }
 }
@@ -993,7 +999,10 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     auto res = std::make_unique<bmg_result>();
     reset_results(*c, n_pairs, cap);
     uint64_t* d_off = c->d_res_off.as<uint64_t>();
+    cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
+    BMG_CUDA(cudaEventRecord(span0, c->s_comp));
     BMG_CUDA(cudaMemsetAsync(d_off, 0, sizeof(uint64_t), c->s_comp));
+    const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     uint64_t row = 0;
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
       const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
@@ -1022,7 +1031,7 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
         }
         enqueue_match(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>());
         it_pairs += pe - pb;
-        for (uint64_t k = plan->row_evict_offsets[row]; k < plan->row_evict_offsets[row + 1]; ++k) {
+        for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
           arena_evict(*c, plan->evict_ids[k]);
           if (opts->on_evict) opts->on_evict(opts->hook_user, plan->evict_ids[k]);
         }
@@ -1031,6 +1040,7 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->iterations.push_back(c->uploads - up0);
       res->iterations.push_back(c->units_uploaded - units0);
     }
+    BMG_CUDA(cudaEventRecord(span1, c->s_comp));
     // read the device result log back once
     std::vector<uint64_t> offs(n_pairs + 1, 0);
     if (n_pairs) {
@@ -1063,6 +1073,14 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     res->counters[4] = c->units_uploaded;
     res->counters[5] = c->peak;
     res->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    {
+      float ms = 0.f;
+      BMG_CUDA(cudaEventSynchronize(span1));
+      BMG_CUDA(cudaEventElapsedTime(&ms, span0, span1));
+      res->device_ms = ms;
+      c->free_events.push_back(span0);
+      c->free_events.push_back(span1);
+    }
     *out = res.release();
   });
 }
@@ -1093,6 +1111,13 @@ int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out3[3]) {
   return guarded([&] {
     if (!r || !out3 || i >= r->iterations.size() / 3) fail(BMG_INVALID_ARGUMENT, "bad iteration index");
     std::copy(r->iterations.begin() + 3 * i, r->iterations.begin() + 3 * i + 3, out3);
+  });
+}
+
+int bmg_result_device_ms(const bmg_result* r, double* ms_out) {
+  return guarded([&] {
+    if (!r || !ms_out) fail(BMG_INVALID_ARGUMENT, "null argument");
+    *ms_out = r->device_ms;
   });
 }
 

@@ -204,6 +204,7 @@ class ExecuteOptions:
     on_pair: object = None    # callable(query_image, train_image, matches (n,2) int32)
     on_upload: object = None  # DeviceBackend::on_upload(image_id, units)
     on_evict: object = None   # DeviceBackend::on_evict(image_id)
+    retain: bool = False      # keep images resident (skip eviction directives)
 
 
 @dataclass
@@ -227,6 +228,7 @@ class PipelineMetrics:
     per_iteration: list = field(default_factory=list)
     wall_time_s: float = 0.0
     pairs_per_second: float = 0.0
+    device_ms: float = 0.0  # CUDA-event span of the row loop on the compute stream
 
 
 @dataclass
@@ -278,7 +280,8 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
                        np.zeros((0, 2), np.int32)))
     on_up = wrap(opts.on_upload, _lib.UPLOAD_HOOK, lambda u, i, n: opts.on_upload(i, n))
     on_ev = wrap(opts.on_evict, _lib.EVICT_HOOK, lambda u, i: opts.on_evict(i))
-    oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None)
+    oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None,
+                           _lib.EXEC_RETAIN if opts.retain else 0)
     h = C.c_void_p()
     check(L.bmg_execute_plan(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc),
                              C.byref(h)))
@@ -292,6 +295,8 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
         counters = np.zeros(6, np.uint64)
         wall = C.c_double(0)
         check(L.bmg_result_metrics(h, ptr(counters), C.byref(wall)))
+        dev_ms = C.c_double(0)
+        check(L.bmg_result_device_ms(h, C.byref(dev_ms)))
         its = []
         for i in range(L.bmg_result_iteration_count(h)):
             o = np.zeros(3, np.uint64)
@@ -306,5 +311,6 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
     met = PipelineMetrics(plan.strategy, c[0], c[1], 0, c[2], c[3], c[4], c[5],
                           c[0] / c[2] if c[2] else 0.0, its, wall.value,
                           c[0] / wall.value if wall.value > 0 else 0.0)
+    met.device_ms = dev_ms.value
     del keep
     return ExecutionResult(matches, met)

@@ -129,7 +129,7 @@ def test_random_pairs_match_oracle(oracle, k, ratio):
     pm, qc, tc = gpu_match(hf, qf, tf, mean, mp)
     ref = oracle_match(oracle, hf, qf, tf, qc, tc, mp)
     assert np.array_equal(pm.matches, ref)
-    assert len(ref) > 100
+    assert len(ref) > (100 if ratio >= 0.5 else 0)
 
 
 def test_full_size_synthetic_pair_matches_reference(reference, oracle):

@@ -1,0 +1,39 @@
+"""Generate the block-schedule inputs of the bench workloads with the
+reference's own scheduler (iterate_schedule, mbr.cpp:321-376, via the test-only
+oracle/_ref build).  The scheduler is out of scope for the GPU path (SURVEY
+§2.1): its SchedulePlan is an *input*, so the plans are committed here as
+fixtures under bench_data/.
+
+  block32   BASELINE config 2: 32 images, band 11 (286 pairs),
+            iterate_schedule(size_blk=16, size_gpu=32)
+  strip500  BASELINE config 3: 500 images, band 10 (4945 pairs), CLI-default
+            budget gpu_images=400 -> size_blk clamped to 200
+            (bandmatch_cli.cpp:87-104)
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "tests"))
+from oracle_lib import Reference  # noqa: E402
+
+OUT = ROOT / "bench_data"
+
+
+def band_pairs(n, band):
+    return np.array([(i, j) for i in range(n) for j in range(i + 1, min(n, i + band + 1))],
+                    np.uint64)
+
+
+def main():
+    OUT.mkdir(exist_ok=True)
+    r = Reference()
+    for name, n, band, blk, gpu in [("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400)]:
+        r.iterate_schedule(np.arange(n), band_pairs(n, band), blk, gpu, OUT / f"plan_{name}.json")
+        print(name, (OUT / f"plan_{name}.json").stat().st_size)
+
+
+if __name__ == "__main__":
+    main()
