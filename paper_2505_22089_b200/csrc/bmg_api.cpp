@@ -113,8 +113,9 @@ struct PinnedRing {
     size_t bytes = align_up(std::max<size_t>(count * sizeof(T), 16), 256);
     if (bytes > cap) fail(BMG_OUT_OF_MEMORY, "metadata exceeds the pinned staging ring");
     if (head + bytes > cap) {
-      BMG_CUDA(cudaStreamSynchronize(a));
-      BMG_CUDA(cudaStreamSynchronize(b));
+      (void)a;
+      (void)b;
+      BMG_CUDA(cudaDeviceSynchronize());  // every stream that may read the ring
       head = 0;
     }
     T* out = reinterpret_cast<T*>(base + head);
@@ -154,7 +155,14 @@ struct bmg_context {
   // arena (DeviceArena, engine.hpp:20-44)
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
-  cudaStream_t s_copy = nullptr, s_comp = nullptr;
+  cudaStream_t s_copy = nullptr, s_comp = nullptr, s_mean = nullptr;
+  // row means run on their own stream so row r+1's sequential chain overlaps
+  // row r's codes and matching; slots are recycled through events
+  static constexpr int kMeanSlots = 4;
+  bmg::DevBuf d_mean_slot[kMeanSlots], d_mean_imgs[kMeanSlots];
+  cudaEvent_t ev_mean_done[kMeanSlots] = {}, ev_mean_free[kMeanSlots] = {};
+  uint64_t mean_seq = 0;
+  float* cur_mean = nullptr;
   cudaMemPool_t pool = nullptr;
   cudaEvent_t ev_uploaded = nullptr;
   bool pending_upload = false;
@@ -311,6 +319,7 @@ void join_uploads(Ctx& c) {
   if (!c.pending_upload) return;
   BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
   BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_uploaded, 0));
+  BMG_CUDA(cudaStreamWaitEvent(c.s_mean, c.ev_uploaded, 0));
   c.pending_upload = false;
 }
 
@@ -400,6 +409,14 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
 
   const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
   float* d_mean = c.d_mean.as<float>();
+  int mean_slot = -1;
+  if (!mean_dev && !mean_host && compute_mean) {
+    mean_slot = static_cast<int>(c.mean_seq++ % Ctx::kMeanSlots);
+    c.d_mean_slot[mean_slot].ensure(sizeof(float) * kDim + sizeof(double) * kDim);
+    c.d_mean_imgs[mean_slot].ensure(sizeof(ImgDev) * std::max(n_imgs, 1));
+    d_mean = c.d_mean_slot[mean_slot].as<float>();
+  }
+  c.cur_mean = d_mean;
   if (mean_dev) {
     BMG_CUDA(cudaMemcpyAsync(d_mean, mean_dev, sizeof(float) * kDim, cudaMemcpyDeviceToDevice, s));
   } else if (mean_host) {
@@ -407,12 +424,26 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     std::memcpy(hm, mean_host, sizeof(float) * kDim);
     BMG_CUDA(cudaMemcpyAsync(d_mean, hm, sizeof(float) * kDim, cudaMemcpyHostToDevice, s));
   } else if (compute_mean) {
-    Timed t(c, "mean", s);
-    launch_row_mean(d_imgs, n_imgs, d_mean, c.d_acc.as<double>(), s);
-    ++c.launches;
-    check_launch();
+    cudaStream_t sm = c.s_mean;
+    BMG_CUDA(cudaStreamWaitEvent(sm, c.ev_mean_free[mean_slot], 0));
+    ImgDev* hm = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
+    std::memcpy(hm, c.row_imgs.data(), sizeof(ImgDev) * n_imgs);
+    BMG_CUDA(cudaMemcpyAsync(c.d_mean_imgs[mean_slot].p, hm, sizeof(ImgDev) * n_imgs,
+                             cudaMemcpyHostToDevice, sm));
+    {
+      Timed t(c, "mean", sm);
+      launch_row_mean(c.d_mean_imgs[mean_slot].as<ImgDev>(), n_imgs, d_mean,
+                      reinterpret_cast<double*>(d_mean + kDim), sm);
+      ++c.launches;
+      check_launch();
+    }
+    BMG_CUDA(cudaEventRecord(c.ev_mean_done[mean_slot], sm));
+    BMG_CUDA(cudaStreamWaitEvent(s, c.ev_mean_done[mean_slot], 0));
   }
-  if (n_tiles == 0) return;
+  if (n_tiles == 0) {
+    if (mean_slot >= 0) BMG_CUDA(cudaEventRecord(c.ev_mean_free[mean_slot], s));
+    return;
+  }
   const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
   const uint32_t* d_tile_start = d_tile_img + n_tiles;
   unsigned long long* diag = c.d_diag.as<unsigned long long>();
@@ -430,6 +461,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     c.launches += 2;
     check_launch();
   }
+  if (mean_slot >= 0) BMG_CUDA(cudaEventRecord(c.ev_mean_free[mean_slot], s));
   {
     Timed t(c, "tables", s);
     launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(n_tiles), n_imgs, s);
@@ -478,7 +510,8 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
   const HashDev& h = c.hd;
-  const int chunk = mp.k_nearest <= 8 ? kMatchThreads : 256;
+  const int chunk = kMatchQueries;
+  if (h.tables > 32) fail(BMG_UNSUPPORTED, "more than 32 hash tables is not supported by the GPU matcher");
   const int idx_bits = 32 - bit_width(static_cast<uint32_t>(h.fine_bits));
   std::vector<int> order(n_pairs);
   for (int p = 0; p < n_pairs; ++p) order[p] = p;
@@ -683,6 +716,12 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     c->capacity = cfg->capacity_units;
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    BMG_CUDA(cudaStreamCreateWithFlags(&c->s_mean, cudaStreamNonBlocking));
+    for (int i = 0; i < bmg_context::kMeanSlots; ++i) {
+      BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_done[i], cudaEventDisableTiming));
+      BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_free[i], cudaEventDisableTiming));
+      BMG_CUDA(cudaEventRecord(c->ev_mean_free[i], c->s_comp));
+    }
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
@@ -724,6 +763,13 @@ int bmg_destroy(bmg_context* c) {
     if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
+    for (int i = 0; i < bmg_context::kMeanSlots; ++i) {
+      c->d_mean_slot[i].release();
+      c->d_mean_imgs[i].release();
+      if (c->ev_mean_done[i]) cudaEventDestroy(c->ev_mean_done[i]);
+      if (c->ev_mean_free[i]) cudaEventDestroy(c->ev_mean_free[i]);
+    }
+    if (c->s_mean) cudaStreamDestroy(c->s_mean);
     delete c;
   });
 }
@@ -733,6 +779,7 @@ int bmg_synchronize(bmg_context* c) {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    BMG_CUDA(cudaStreamSynchronize(c->s_mean));
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
   });
 }
@@ -781,7 +828,7 @@ int bmg_row_mean(bmg_context* c, float* mean_out) {
     if (!c || !mean_out) fail(BMG_INVALID_ARGUMENT, "null argument");
     if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
     set_device(*c);
-    BMG_CUDA(cudaMemcpyAsync(mean_out, c->d_mean.p, sizeof(float) * kDim, cudaMemcpyDeviceToHost, c->s_comp));
+    BMG_CUDA(cudaMemcpyAsync(mean_out, c->cur_mean, sizeof(float) * kDim, cudaMemcpyDeviceToHost, c->s_comp));
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
   });
 }
@@ -1001,6 +1048,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     uint64_t* d_off = c->d_res_off.as<uint64_t>();
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->s_comp));
+    BMG_CUDA(cudaStreamWaitEvent(c->s_mean, span0, 0));
+    BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
     BMG_CUDA(cudaMemsetAsync(d_off, 0, sizeof(uint64_t), c->s_comp));
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     uint64_t row = 0;

@@ -79,6 +79,7 @@ void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint3
 
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
 constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)
-constexpr int kMatchThreads = 1024;
+constexpr int kMatchThreads = 1024;  // 32 warps, one query per warp at a time
+constexpr int kMatchQueries = 1024;  // queries per match CTA
 
 }  // namespace bmg

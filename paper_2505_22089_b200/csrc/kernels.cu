@@ -27,6 +27,10 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kEmpty = 0xffffffffu;
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // ---------------------------------------------------------------------------
 // K1: row centering mean.  acc[c] += (double)d.v[c] over images in ascending
 // id order, descriptors in index order; mean = float(acc / total).  One
@@ -47,33 +51,158 @@ __global__ void __launch_bounds__(128) row_mean_kernel(const ImgDev* __restrict_
     const uint32_t n = imgs[im].n;
     const float* d = base + c;
     uint32_t i = 0;
-    float v[U], w[U];
-    if (n >= U) {
+    // three-stage software pipeline per batch of U descriptors:
+    //   loads of batch i+2  ->  F2F conversion of batch i+1  ->  DADD chain of batch i
+    // so neither a load nor a conversion ever sits on the dependent chain.
+    float w[U];
+    double da[U], db[U];
+    if (n >= 2 * U) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldg(d + (size_t)u * kDim);
-    }
-    for (; i + 2 * U <= n; i += U) {
+      for (int u = 0; u < U; ++u) da[u] = (double)__ldg(d + (size_t)u * kDim);
 #pragma unroll
-      for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(i + U + u) * kDim);
-      {
-        const uint32_t row = i + PF + (c >> 2);
-        if (row < n) {
-          const char* p = reinterpret_cast<const char*>(base + (size_t)row * kDim) + (c & 3) * 128;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(U + u) * kDim);
+      for (; i + 3 * U <= n; i += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) db[u] = (double)w[u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(i + 2 * U + u) * kDim);
+        {
+          const uint32_t row = i + PF + (c >> 2);
+          if (row < n) {
+            const char* p = reinterpret_cast<const char*>(base + (size_t)row * kDim) + (c & 3) * 128;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+          }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, da[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) da[u] = db[u];
       }
+      // drain: batch i (in da) and batch i+1 (in w)
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)v[u]);
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, da[u]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = w[u];
-    }
-    if (i + U <= n) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)v[u]);
-      i += U;
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)w[u]);
+      i += 2 * U;
     }
     for (; i < n; ++i) acc = __dadd_rn(acc, (double)__ldg(d + (size_t)i * kDim));
     total += n;
+  }
+  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+  if (acc_out) acc_out[c] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// K1 (v2): the same exact chain fed by a TMA ring.  One producer warp streams
+// 32-row chunks (16 KB) of every image, in the reference's order, into an
+// 8-stage shared-memory ring with cp.async.bulk + mbarrier complete_tx (128 KB
+// in flight hides HBM latency); 4 consumer warps (thread = channel) read
+// their column from shared memory one chunk ahead and run the DADD chain.
+// Rows past an image's end are read as +0.0, an exact no-op for an
+// accumulator that starts at +0.0 (it can never become -0.0 under RN).
+// ---------------------------------------------------------------------------
+constexpr int kMeanRows = 32;
+constexpr int kMeanStages = 8;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(160, 1) row_mean_tma_kernel(const ImgDev* __restrict__ imgs,
+                                                              int n_imgs, float* __restrict__ mean_out,
+                                                              double* __restrict__ acc_out) {
+  extern __shared__ __align__(128) float ring[];  // [stages][rows][128]
+  __shared__ __align__(8) unsigned long long full_bar[kMeanStages], empty_bar[kMeanStages];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kMeanStages; ++s) {
+      mbar_init(smem_addr(&full_bar[s]), 1);
+      mbar_init(smem_addr(&empty_bar[s]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t ring_base = smem_addr(ring);
+  constexpr uint32_t kStageBytes = kMeanRows * kDim * 4;
+
+  if (warp == 4) {  // ---- producer
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int im = 0; im < n_imgs; ++im) {
+        const float* src = imgs[im].desc;
+        const uint32_t n = imgs[im].n;
+        for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
+          const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
+          mbar_wait(smem_addr(&empty_bar[s]), ph ^ 1u);
+          const uint32_t bytes = min((uint32_t)kMeanRows, n - r0) * kDim * 4u;
+          mbar_expect_tx(smem_addr(&full_bar[s]), bytes);
+          tma_bulk_g2s(ring_base + s * kStageBytes, src + (size_t)r0 * kDim, bytes,
+                       smem_addr(&full_bar[s]));
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: thread c owns channel c
+  const int c = tid;
+  double acc = 0.0;
+  unsigned long long total = 0;
+  double da[kMeanRows];
+  bool have = false;  // da holds a converted chunk awaiting its chain
+  uint32_t g = 0;
+  for (int im = 0; im < n_imgs; ++im) {
+    const uint32_t n = imgs[im].n;
+    total += n;
+    for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
+      const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
+      const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
+      mbar_wait(smem_addr(&full_bar[s]), ph);
+      float w[kMeanRows];
+      const float* st = ring + (size_t)s * kMeanRows * kDim + c;
+#pragma unroll
+      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kDim] : 0.0f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty_bar[s]));
+      double db[kMeanRows];
+#pragma unroll
+      for (int r = 0; r < kMeanRows; ++r) db[r] = (double)w[r];
+      if (have) {
+#pragma unroll
+        for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < kMeanRows; ++r) da[r] = db[r];
+      have = true;
+    }
+  }
+  if (have) {
+#pragma unroll
+    for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
   }
   mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
   if (acc_out) acc_out[c] = acc;
@@ -385,34 +514,61 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 }
 
 // ---------------------------------------------------------------------------
-// K4: the cascade.  CTA = (image pair, 1024-query range), thread per query.
-//   1. train fine codes -> shared memory with one TMA bulk copy
-//      (cp.async.bulk + mbarrier complete_tx) while each thread loads its
-//      query code and bucket ids;
-//   2. bucket union over the tables, 128-bit Hamming via POPC, top-K of the
-//      unique key (hamming << idx_bits | train_idx) kept sorted in registers
-//      (duplicates from several tables have identical keys and are skipped:
-//      this is the reference's last_seen dedup + counting sort, :154-200);
-//   3. warp-cooperative re-rank: per query, lane l holds dims 4l..4l+3 and
-//      every kept candidate row is one coalesced 512-byte load; FP32 squared
-//      distances with relative error <= 8e-6 certify the (dist, idx) argmin
-//      and the ratio test; uncertified queries are recomputed with the
-//      reference's sequential FP64 euclidean (:35-42) and sort (:201-208).
+// K4: the cascade.  CTA = (image pair, query range); one WARP per query.
+//   1. the train image's fine codes are staged in shared memory by one TMA
+//      bulk copy (cp.async.bulk + mbarrier complete_tx);
+//   2. the query's bucket union over the L tables (hashmatch.cpp:154-169) is
+//      walked as one flattened list, 32 candidates per round (one per lane):
+//      slot load, 128-bit Hamming via POPC, unique key
+//      (hamming << idx_bits | train_idx).  The first round is bitonic-sorted
+//      across the warp; later rounds are filtered with a warp ballot against
+//      the current K-th key and survivors are inserted into a sorted list
+//      distributed over lanes 0..KM-1.  Equal keys are the same train index
+//      reached from two tables and are inserted once -- the reference's
+//      last_seen dedup + stable counting sort by (hamming, idx) (:171-200);
+//   3. re-rank (:196-208): lane l holds dims 4l..4l+3, every kept candidate
+//      row is one coalesced 512-byte load; FP32 squared distances with a
+//      certified relative error <= 8e-6 decide the (dist, idx) argmin and the
+//      ratio test; uncertified queries rerun the reference's sequential FP64
+//      euclidean (:35-42) lane-per-candidate.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+constexpr int kMaxTables = 32;
+
+
+template <int FWP, bool SMEM>
+__device__ __forceinline__ uint32_t hamming(const unsigned char* smem_codes,
+                                            const uint64_t* __restrict__ gcodes, uint32_t j,
+                                            const uint64_t (&qc)[FWP]) {
+  uint32_t h = 0;
+  if constexpr (SMEM && FWP % 2 == 0) {
+    const ulonglong2* sc = reinterpret_cast<const ulonglong2*>(smem_codes) + (size_t)j * (FWP / 2);
+#pragma unroll
+    for (int x = 0; x < FWP / 2; ++x) {
+      const ulonglong2 v = sc[x];
+      h += __popcll(qc[2 * x] ^ v.x) + __popcll(qc[2 * x + 1] ^ v.y);
+    }
+  } else if constexpr (SMEM) {
+    const uint64_t* sc = reinterpret_cast<const uint64_t*>(smem_codes) + (size_t)j * FWP;
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ sc[x]);
+  } else {
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ __ldg(gcodes + (size_t)j * FWP + x));
+  }
+  return h;
 }
 
 template <int FWP, int KM, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar;
+  __shared__ uint32_t s_tab[NT / 32][2 * kMaxTables + 2];
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = NT / 32;
 
-  const uint64_t* tcodes = T.fine;
   if constexpr (SMEM) {
     const uint32_t bytes = ((T.n * FWP * 8u) + 15u) & ~15u;
     if (tid == 0) {
@@ -431,17 +587,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
             : "memory");
       }
     }
-  }
-
-  const uint32_t q = w.q_begin + tid;
-  const bool active = q < w.q_end;
-  const uint32_t idx_mask = (1u << a.idx_bits) - 1u;
-  uint64_t qc[FWP];
-#pragma unroll
-  for (int x = 0; x < FWP; ++x) qc[x] = active ? __ldg(Q.fine + (size_t)q * FWP + x) : 0ull;
-
-  if constexpr (SMEM) {
-    __syncthreads();  // mbarrier init visible
+    __syncthreads();  // mbarrier initialised before anyone waits on it
     const uint32_t bar = smem_addr(&s_bar);
     uint32_t done = 0;
     while (!done) {
@@ -453,90 +599,98 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     }
   }
 
-  uint32_t top[KM];
-#pragma unroll
-  for (int k = 0; k < KM; ++k) top[k] = kEmpty;
-  uint32_t thr = kEmpty;
-  const int K = a.k;
-
-  if (active) {
-    const int nb1 = a.n_buckets + 1;
-    for (int t = 0; t < a.tables; ++t) {
-      const uint32_t b = __ldg(Q.coarse + (size_t)q * a.tables + t);
-      const uint32_t* off = T.offsets + (size_t)t * nb1;
-      const uint32_t lo = __ldg(off + b), hi = __ldg(off + b + 1);
-      const uint32_t* sl = T.slots + (size_t)t * T.n;
-      for (uint32_t s = lo; s < hi; ++s) {
-        const uint32_t j = __ldg(sl + s);
-        uint32_t hsum = 0;
-        if constexpr (SMEM && FWP % 2 == 0) {
-          const ulonglong2* sc = reinterpret_cast<const ulonglong2*>(smem_raw) + (size_t)j * (FWP / 2);
-#pragma unroll
-          for (int x = 0; x < FWP / 2; ++x) {
-            const ulonglong2 v = sc[x];
-            hsum += __popcll(qc[2 * x] ^ v.x) + __popcll(qc[2 * x + 1] ^ v.y);
-          }
-        } else if constexpr (SMEM) {
-          const uint64_t* sc = reinterpret_cast<const uint64_t*>(smem_raw) + (size_t)j * FWP;
-#pragma unroll
-          for (int x = 0; x < FWP; ++x) hsum += __popcll(qc[x] ^ sc[x]);
-        } else {
-#pragma unroll
-          for (int x = 0; x < FWP; ++x) hsum += __popcll(qc[x] ^ __ldg(tcodes + (size_t)j * FWP + x));
-        }
-        const uint32_t key = (hsum << a.idx_bits) | j;
-        if (key < thr) {
-          bool dup = false;
-#pragma unroll
-          for (int k = 0; k < KM; ++k) dup |= top[k] == key;
-          if (!dup) {
-#pragma unroll
-            for (int k = KM - 1; k > 0; --k)
-              top[k] = top[k - 1] > key ? top[k - 1] : (top[k] > key ? key : top[k]);
-            top[0] = top[0] > key ? key : top[0];
-#pragma unroll
-            for (int k = 0; k < KM; ++k)
-              if (k == K - 1) thr = top[k];
-          }
-        }
-      }
-    }
-  }
-
-  // ---- re-rank + ratio test, one query at a time per warp ----
+  const int L = a.tables, K = a.k, ib = a.idx_bits;
+  const uint32_t idx_mask = (1u << ib) - 1u;
+  const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
   const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
   const double ratio = a.ratio;
   const double r2 = ratio * ratio;
-  int32_t my_result = -1;
-  for (int src = 0; src < 32; ++src) {
-    const int act = __shfl_sync(kFull, active ? 1 : 0, src);
-    if (!act) continue;
-    const uint32_t qs = __shfl_sync(kFull, q, src);
-    uint32_t cand[KM];
-    int kept = 0;
-#pragma unroll
-    for (int k = 0; k < KM; ++k) {
-      cand[k] = __shfl_sync(kFull, top[k], src);
-      kept += (k < K && cand[k] != kEmpty) ? 1 : 0;
+  uint32_t* tab = s_tab[warp];
+  uint32_t n_matched = 0;
+
+  for (uint32_t q = w.q_begin + warp; q < w.q_end; q += kWarps) {
+    // ---- per-query bucket ranges, flattened: table t covers [cum_t, cum_t+sz_t)
+    uint32_t lo = 0, sz = 0;
+    if (lane < L) {
+      const uint32_t b = __ldg(Q.coarse + (size_t)q * L + lane);
+      const uint32_t* off = T.offsets + (size_t)lane * nb1;
+      lo = __ldg(off + b);
+      sz = __ldg(off + b + 1) - lo;
     }
+    uint32_t incl = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, L - 1);
+    if (lane < L) {
+      tab[lane] = incl - sz;                             // cum_t
+      tab[kMaxTables + 1 + lane] = lane * T.n + lo - (incl - sz);  // slot base for entry e
+    }
+    if (lane == 0) tab[L] = total;                      // sentinel end of the last table
+    __syncwarp();
+    uint64_t qc[FWP];
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
+
+    // ---- candidate rounds: 32 candidates per round, one per lane.  Keys
+    // below the current K-th key are pulled out in ascending order with a
+    // single-instruction warp min (REDUX); every lane holding that key clears
+    // it, so a train index reached from several tables is taken once.
+    uint32_t lst = kEmpty, thr = kEmpty;
+    int t = 0;
+    uint32_t t_end = tab[1];
+    const uint32_t* sp = T.slots + tab[kMaxTables + 1] + lane;
+    for (uint32_t base = 0; base < total; base += 32, sp += 32) {
+      const uint32_t e = base + lane;
+      uint32_t key = kEmpty;
+      if (e < total) {
+        if (e >= t_end) {
+          do {
+            ++t;
+            t_end = tab[t + 1];
+          } while (e >= t_end);
+          sp = T.slots + tab[kMaxTables + 1 + t] + e;
+        }
+        const uint32_t j = __ldg(sp);
+        key = (hamming<FWP, SMEM>(smem_raw, T.fine, j, qc) << ib) | j;
+        key = key < thr ? key : kEmpty;
+      }
+      for (;;) {
+        const uint32_t m = __reduce_min_sync(kFull, key);
+        if (m >= thr) break;
+        if (key == m) key = kEmpty;
+        if (!__any_sync(kFull, lane < KM && lst == m)) {
+          const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
+          const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
+          lst = lane < KM ? nv : kEmpty;
+          thr = __shfl_sync(kFull, lst, K - 1);
+        }
+      }
+    }
+
+    // ---- re-rank + ratio test
+    const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
     int32_t result = -1;
     if (kept == 1) {
-      result = (int32_t)(cand[0] & idx_mask);
+      result = (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask);
     } else if (kept > 1) {
-      const float4 qv = __ldg(Qd + (size_t)qs * 32 + lane);
+      const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
       float part[KM];
 #pragma unroll
       for (int k = 0; k < KM; ++k) {
+        const uint32_t jk = __shfl_sync(kFull, lst, k) & idx_mask;
         part[k] = 0.f;
         if (k < kept) {
-          const float4 tv = __ldg(Td + (size_t)(cand[k] & idx_mask) * 32 + lane);
+          const float4 tv = __ldg(Td + (size_t)jk * 32 + lane);
           const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
           part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
         }
       }
-      // transpose-reduce: after log2(KM) halving steps lane l holds the sum
-      // of candidate idx(l); the remaining steps finish the 32-lane sum.
+      // transpose-reduce: after log2(KM) halving steps the lane whose bits
+      // (4, 3, .., 5-log2 KM) spell k holds candidate k's partial sum
       constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
 #pragma unroll
       for (int st = 0; st < kLog; ++st) {
@@ -554,34 +708,31 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       float red = part[0];
 #pragma unroll
       for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
-      float sv[KM];
+      int src_lane = 0;
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        // lane holding candidate k: bit b of k sits at lane bit (4 - (kLog-1-b))
-        int src_lane = 0;
+      for (int b = 0; b < kLog; ++b)
+        if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
+      const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
+      const bool mine = lane < kept;
+      const uint32_t my_idx = lst & idx_mask;
+      // argmin of (s, idx) and runner-up value over lanes < kept
+      float bs = mine ? s_own : __int_as_float(0x7f800000);
+      uint32_t bi = mine ? my_idx : 0xffffffffu;
 #pragma unroll
-        for (int b = 0; b < kLog; ++b)
-          if (k & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
-        sv[k] = __shfl_sync(kFull, red, src_lane);
-      }
-      // certified decision: argmin by (s32, train_idx), then the runner-up value
-      int is = 0;
-      float s_min = sv[0];
-      uint32_t i_min = cand[0] & idx_mask;
-#pragma unroll
-      for (int k = 1; k < KM; ++k)
-        if (k < kept) {
-          const uint32_t ik = cand[k] & idx_mask;
-          if (sv[k] < s_min || (sv[k] == s_min && ik < i_min)) {
-            is = k;
-            s_min = sv[k];
-            i_min = ik;
-          }
+      for (int o = KM / 2; o > 0; o >>= 1) {
+        const float os = __shfl_xor_sync(kFull, bs, o);
+        const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
+        if (os < bs || (os == bs && oi < bi)) {
+          bs = os;
+          bi = oi;
         }
-      float s_2 = __int_as_float(0x7f800000);
+      }
+      const float s_min = __shfl_sync(kFull, bs, 0);
+      const uint32_t i_min = __shfl_sync(kFull, bi, 0);
+      float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
 #pragma unroll
-      for (int k = 0; k < KM; ++k)
-        if (k < kept && k != is) s_2 = fminf(s_2, sv[k]);
+      for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
+      const float s_2 = __shfl_sync(kFull, s2, 0);
       const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
       const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
       const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
@@ -590,14 +741,10 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         result = (int32_t)i_min;
       } else if (!reject) {
         // FP64 reference path (hashmatch.cpp:35-42, :196-208)
-        uint32_t mine = kEmpty;
-#pragma unroll
-        for (int k = 0; k < KM; ++k)
-          if (k == lane) mine = cand[k];
-        double e = 0.0;
-        if (lane < kept) {
-          const float* qd = Q.desc + (size_t)qs * kDim;
-          const float* td = T.desc + (size_t)(mine & idx_mask) * kDim;
+        double e = __longlong_as_double(0x7ff0000000000000ll);
+        if (mine) {
+          const float* qd = Q.desc + (size_t)q * kDim;
+          const float* td = T.desc + (size_t)my_idx * kDim;
           double s = 0.0;
 #pragma unroll 8
           for (int c = 0; c < kDim; ++c) {
@@ -606,36 +753,34 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           }
           e = __dsqrt_rn(s);
         }
-        int first = 0;
-        double e_first = __shfl_sync(kFull, e, 0);
-        uint32_t i_first = cand[0] & idx_mask;
-        double ev[KM];
+        double be = e;
+        uint32_t bj = mine ? my_idx : 0xffffffffu;
 #pragma unroll
-        for (int k = 0; k < KM; ++k) ev[k] = __shfl_sync(kFull, e, k);
-#pragma unroll
-        for (int k = 1; k < KM; ++k)
-          if (k < kept) {
-            const uint32_t ik = cand[k] & idx_mask;
-            if (ev[k] < e_first || (ev[k] == e_first && ik < i_first)) {
-              first = k;
-              e_first = ev[k];
-              i_first = ik;
-            }
+        for (int o = KM / 2; o > 0; o >>= 1) {
+          const double oe = __shfl_xor_sync(kFull, be, o);
+          const uint32_t oj = __shfl_xor_sync(kFull, bj, o);
+          if (oe < be || (oe == be && oj < bj)) {
+            be = oe;
+            bj = oj;
           }
-        double e_second = __longlong_as_double(0x7ff0000000000000ll);
+        }
+        const double e_first = __shfl_sync(kFull, be, 0);
+        const uint32_t i_first = __shfl_sync(kFull, bj, 0);
+        double e2 = (mine && my_idx != i_first) ? e : __longlong_as_double(0x7ff0000000000000ll);
 #pragma unroll
-        for (int k = 0; k < KM; ++k)
-          if (k < kept && k != first) e_second = fmin(e_second, ev[k]);
+        for (int o = KM / 2; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(kFull, e2, o));
+        const double e_second = __shfl_sync(kFull, e2, 0);
         if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
         if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
       }
     }
-    if (lane == src) my_result = result;
+    if (lane == 0) {
+      a.dense[a.dense_off[w.pair] + q] = result;
+      n_matched += result >= 0 ? 1u : 0u;
+    }
+    __syncwarp();
   }
-
-  if (active) a.dense[a.dense_off[w.pair] + q] = my_result;
-  const unsigned hit = __ballot_sync(kFull, active && my_result >= 0);
-  if (lane == 0 && hit) atomicAdd(a.pair_count + w.pair, (uint32_t)__popc(hit));
+  if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
 }
 
 // ---------------------------------------------------------------------------
@@ -698,7 +843,13 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // ---------------------------------------------------------------------------
 void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
                      cudaStream_t s) {
-  row_mean_kernel<<<1, 128, 0, s>>>(imgs, n_imgs, mean_out, acc_out);
+  constexpr int smem = kMeanStages * kMeanRows * kDim * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(row_mean_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  row_mean_tma_kernel<<<1, 160, smem, s>>>(imgs, n_imgs, mean_out, acc_out);
 }
 
 static size_t codes_smem_bytes() {
@@ -758,8 +909,8 @@ static void launch_match_fw(const MatchLaunch& a, int n_work, uint32_t max_train
     if (use_smem) launch_match_t<FWP, 8, kMatchThreads, true>(a, n_work, smem, s);
     else launch_match_t<FWP, 8, kMatchThreads, false>(a, n_work, 0, s);
   } else {
-    if (use_smem) launch_match_t<FWP, 32, 256, true>(a, n_work, smem, s);
-    else launch_match_t<FWP, 32, 256, false>(a, n_work, 0, s);
+    if (use_smem) launch_match_t<FWP, 32, 512, true>(a, n_work, smem, s);
+    else launch_match_t<FWP, 32, 512, false>(a, n_work, 0, s);
   }
 }
 
