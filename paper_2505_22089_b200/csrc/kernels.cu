@@ -32,77 +32,20 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: row centering mean.  acc[c] += (double)d.v[c] over images in ascending
-// id order, descriptors in index order; mean = float(acc / total).  One
-// thread per channel keeps the reference's exact addition order; loads run
-// 64 descriptors ahead of the DADD chain (double-buffered) with an L2
-// prefetch stream further ahead, so the kernel is bound by DADD latency.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) row_mean_kernel(const ImgDev* __restrict__ imgs,
-                                                       int n_imgs, float* __restrict__ mean_out,
-                                                       double* __restrict__ acc_out) {
-  constexpr int U = 32;
-  constexpr int PF = 512;  // prefetch distance in descriptors
-  const int c = threadIdx.x;
-  double acc = 0.0;
-  unsigned long long total = 0;
-  for (int im = 0; im < n_imgs; ++im) {
-    const float* base = imgs[im].desc;
-    const uint32_t n = imgs[im].n;
-    const float* d = base + c;
-    uint32_t i = 0;
-    // three-stage software pipeline per batch of U descriptors:
-    //   loads of batch i+2  ->  F2F conversion of batch i+1  ->  DADD chain of batch i
-    // so neither a load nor a conversion ever sits on the dependent chain.
-    float w[U];
-    double da[U], db[U];
-    if (n >= 2 * U) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) da[u] = (double)__ldg(d + (size_t)u * kDim);
-#pragma unroll
-      for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(U + u) * kDim);
-      for (; i + 3 * U <= n; i += U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) db[u] = (double)w[u];
-#pragma unroll
-        for (int u = 0; u < U; ++u) w[u] = __ldg(d + (size_t)(i + 2 * U + u) * kDim);
-        {
-          const uint32_t row = i + PF + (c >> 2);
-          if (row < n) {
-            const char* p = reinterpret_cast<const char*>(base + (size_t)row * kDim) + (c & 3) * 128;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, da[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) da[u] = db[u];
-      }
-      // drain: batch i (in da) and batch i+1 (in w)
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, da[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)w[u]);
-      i += 2 * U;
-    }
-    for (; i < n; ++i) acc = __dadd_rn(acc, (double)__ldg(d + (size_t)i * kDim));
-    total += n;
-  }
-  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
-  if (acc_out) acc_out[c] = acc;
-}
-
-// ---------------------------------------------------------------------------
-// K1 (v2): the same exact chain fed by a TMA ring.  One producer warp streams
-// 32-row chunks (16 KB) of every image, in the reference's order, into an
-// 8-stage shared-memory ring with cp.async.bulk + mbarrier complete_tx (128 KB
-// in flight hides HBM latency); 4 consumer warps (thread = channel) read
-// their column from shared memory one chunk ahead and run the DADD chain.
-// Rows past an image's end are read as +0.0, an exact no-op for an
-// accumulator that starts at +0.0 (it can never become -0.0 under RN).
+// K1: row centering mean (engine.cpp:446-461).  acc[c] += (double)d.v[c] over
+// images in ascending id order, descriptors in index order, then
+// mean = float(acc / total): a dependent FP64 chain per channel, reproduced
+// literally.  A producer warp streams 32-row chunks of every image, in the
+// reference's order, into a 16-stage shared-memory ring with cp.async.bulk +
+// mbarrier complete_tx (128 KB in flight hides HBM latency); consumer warps
+// (thread = channel) run the DADD chain out of shared memory.  Rows past an
+// image's end are read as +0.0, an exact no-op for an accumulator that starts
+// at +0.0 (it can never become -0.0 under round-to-nearest).
 // ---------------------------------------------------------------------------
 constexpr int kMeanRows = 32;
-constexpr int kMeanStages = 8;
+constexpr int kMeanStages = 16;
+constexpr int kMeanCh = 64;                 // channels per CTA (grid = 128 / kMeanCh)
+constexpr int kMeanThreads = kMeanCh + 32;  // consumers + one producer warp
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -132,48 +75,59 @@ __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint
       : "memory");
 }
 
-__global__ void __launch_bounds__(160, 1) row_mean_tma_kernel(const ImgDev* __restrict__ imgs,
-                                                              int n_imgs, float* __restrict__ mean_out,
-                                                              double* __restrict__ acc_out) {
-  extern __shared__ __align__(128) float ring[];  // [stages][rows][128]
+// Grid: 2 CTAs x 64 channels, so each SM converts (F2F on the XU pipe) and
+// chains half of the channels; the producer issues one 256-byte bulk copy
+// per row (the CTA's half of the 512-byte descriptor).  Consumers convert
+// chunk g+1 interleaved with the DADD chain of chunk g, so the conversions
+// fill the 8-cycle shadow of each dependent DADD.
+__global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const ImgDev* __restrict__ imgs,
+                                                                       int n_imgs, float* __restrict__ mean_out,
+                                                                       double* __restrict__ acc_out) {
+  extern __shared__ __align__(128) float ring[];  // [stages][rows][kMeanCh]
   __shared__ __align__(8) unsigned long long full_bar[kMeanStages], empty_bar[kMeanStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kConsumerWarps = kMeanCh / 32;
   if (tid == 0) {
     for (int s = 0; s < kMeanStages; ++s) {
       mbar_init(smem_addr(&full_bar[s]), 1);
-      mbar_init(smem_addr(&empty_bar[s]), 4);
+      mbar_init(smem_addr(&empty_bar[s]), kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const uint32_t ring_base = smem_addr(ring);
-  constexpr uint32_t kStageBytes = kMeanRows * kDim * 4;
+  constexpr uint32_t kRowBytes = kMeanCh * 4;
+  constexpr uint32_t kStageBytes = kMeanRows * kRowBytes;
+  const int c0 = blockIdx.x * kMeanCh;
 
-  if (warp == 4) {  // ---- producer
+  if (warp == kConsumerWarps) {  // ---- producer
     if (lane == 0) {
       uint32_t g = 0;
       for (int im = 0; im < n_imgs; ++im) {
-        const float* src = imgs[im].desc;
+        const float* src = imgs[im].desc + c0;
         const uint32_t n = imgs[im].n;
         for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
           const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
           mbar_wait(smem_addr(&empty_bar[s]), ph ^ 1u);
-          const uint32_t bytes = min((uint32_t)kMeanRows, n - r0) * kDim * 4u;
-          mbar_expect_tx(smem_addr(&full_bar[s]), bytes);
-          tma_bulk_g2s(ring_base + s * kStageBytes, src + (size_t)r0 * kDim, bytes,
-                       smem_addr(&full_bar[s]));
+          const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
+          const uint32_t bar = smem_addr(&full_bar[s]);
+          mbar_expect_tx(bar, rows * kRowBytes);
+          for (uint32_t r = 0; r < rows; ++r)
+            tma_bulk_g2s(ring_base + s * kStageBytes + r * kRowBytes, src + (size_t)(r0 + r) * kDim,
+                         kRowBytes, bar);
         }
       }
     }
     return;
   }
 
-  // ---- consumers: thread c owns channel c
+  // ---- consumers: thread c owns channel c0 + c
   const int c = tid;
   double acc = 0.0;
   unsigned long long total = 0;
   double da[kMeanRows];
-  bool have = false;  // da holds a converted chunk awaiting its chain
+#pragma unroll
+  for (int r = 0; r < kMeanRows; ++r) da[r] = 0.0;  // +0.0: exact no-ops on the chain
   uint32_t g = 0;
   for (int im = 0; im < n_imgs; ++im) {
     const uint32_t n = imgs[im].n;
@@ -183,29 +137,23 @@ __global__ void __launch_bounds__(160, 1) row_mean_tma_kernel(const ImgDev* __re
       const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
       mbar_wait(smem_addr(&full_bar[s]), ph);
       float w[kMeanRows];
-      const float* st = ring + (size_t)s * kMeanRows * kDim + c;
+      const float* st = ring + (size_t)s * kMeanRows * kMeanCh + c;
 #pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kDim] : 0.0f;
+      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kMeanCh] : 0.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[s]));
-      double db[kMeanRows];
 #pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) db[r] = (double)w[r];
-      if (have) {
-#pragma unroll
-        for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
+      for (int r = 0; r < kMeanRows; ++r) {
+        const double x = (double)w[r];   // next chunk's row r (XU)
+        acc = __dadd_rn(acc, da[r]);     // this chunk's row r (dependent DADD)
+        da[r] = x;
       }
-#pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) da[r] = db[r];
-      have = true;
     }
   }
-  if (have) {
 #pragma unroll
-    for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
-  }
-  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
-  if (acc_out) acc_out[c] = acc;
+  for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
+  mean_out[c0 + c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+  if (acc_out) acc_out[c0 + c] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -533,6 +481,7 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //      euclidean (:35-42) lane-per-candidate.
 // ---------------------------------------------------------------------------
 constexpr int kMaxTables = 32;
+constexpr int kBaseOff = kMaxTables + 2;  // s_tab: cum_t at [0, L+1], slot base_t at kBaseOff + t
 
 
 template <int FWP, bool SMEM>
@@ -562,7 +511,9 @@ template <int FWP, int KM, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar;
-  __shared__ uint32_t s_tab[NT / 32][2 * kMaxTables + 2];
+  __shared__ uint32_t s_tab[NT / 32][kBaseOff + kMaxTables];
+  constexpr uint32_t kSeg = 256;
+  __shared__ uint32_t s_slots[NT / 32][kSeg];
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
@@ -627,48 +578,95 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     const uint32_t total = __shfl_sync(kFull, incl, L - 1);
     if (lane < L) {
       tab[lane] = incl - sz;                             // cum_t
-      tab[kMaxTables + 1 + lane] = lane * T.n + lo - (incl - sz);  // slot base for entry e
+      tab[kBaseOff + lane] = lane * T.n + lo - (incl - sz);  // slot base for entry e
     }
-    if (lane == 0) tab[L] = total;                      // sentinel end of the last table
+    if (lane == 0) tab[L] = tab[L + 1] = total;         // sentinels past the last table
     __syncwarp();
     uint64_t qc[FWP];
 #pragma unroll
     for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
 
-    // ---- candidate rounds: 32 candidates per round, one per lane.  Keys
-    // below the current K-th key are pulled out in ascending order with a
-    // single-instruction warp min (REDUX); every lane holding that key clears
-    // it, so a train index reached from several tables is taken once.
-    uint32_t lst = kEmpty, thr = kEmpty;
-    int t = 0;
-    uint32_t t_end = tab[1];
-    const uint32_t* sp = T.slots + tab[kMaxTables + 1] + lane;
-    for (uint32_t base = 0; base < total; base += 32, sp += 32) {
-      const uint32_t e = base + lane;
-      uint32_t key = kEmpty;
-      if (e < total) {
-        if (e >= t_end) {
-          do {
-            ++t;
-            t_end = tab[t + 1];
-          } while (e >= t_end);
-          sp = T.slots + tab[kMaxTables + 1 + t] + e;
+    // The flattened union is consumed in segments of kSeg entries: a
+    // table-major, coalesced copy of the segment's train indices into this
+    // warp's shared buffer, then 32-wide rounds over the buffer.
+    uint32_t* seg_buf = s_slots[warp];
+    auto for_each_round = [&](auto&& round) {
+      int t_first = 0;
+      for (uint32_t seg = 0; seg < total; seg += kSeg) {
+        const uint32_t seg_end = min(total, seg + kSeg);
+        while (tab[t_first + 1] <= seg) ++t_first;
+        for (int t = t_first; t < L && tab[t] < seg_end; ++t) {
+          const uint32_t lo_e = max(tab[t], seg), hi_e = min(tab[t + 1], seg_end);
+          const uint32_t gbase = tab[kBaseOff + t];
+          for (uint32_t e = lo_e + lane; e < hi_e; e += 32) seg_buf[e - seg] = __ldg(T.slots + gbase + e);
         }
-        const uint32_t j = __ldg(sp);
-        key = (hamming<FWP, SMEM>(smem_raw, T.fine, j, qc) << ib) | j;
+        __syncwarp();
+        for (uint32_t b = 0; b < seg_end - seg; b += 32) {
+          const uint32_t e = b + lane;
+          const bool valid = e < seg_end - seg;
+          const uint32_t j = valid ? seg_buf[e] : 0u;
+          round(valid, valid ? (hamming<FWP, SMEM>(smem_raw, T.fine, j, qc) << ib) | j : kEmpty);
+        }
+        __syncwarp();
+      }
+    };
+    uint32_t lst = kEmpty;
+    bool exact = KM != 8;
+    if constexpr (KM == 8) {
+      // ---- fast path: each lane keeps the 4 smallest keys it sees
+      // (branchless sorted insert), then the warp pulls the K smallest out of
+      // the lanes' lists with the single-instruction warp min (REDUX), popping
+      // every copy of the pulled key (a train index reached from several
+      // tables has the same key).  Exact unless some lane gave up all 4 list
+      // entries while having dropped a 5th key -- then the query reruns on the
+      // exact path below.
+      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty;
+      bool dropped = false;
+      for_each_round([&](bool valid, uint32_t key) {
+        dropped |= valid && (k3 != kEmpty) && (key < k3 || k3 < key);
+        k3 = max(k2, min(k3, key));
+        k2 = max(k1, min(k2, key));
+        k1 = max(k0, min(k1, key));
+        k0 = min(k0, key);
+      });
+      int popped = 0;
+      for (int r = 0; r < K; ++r) {
+        const uint32_t m = __reduce_min_sync(kFull, k0);
+        if (m == kEmpty) break;
+        if (lane == r) lst = m;
+        while (k0 == m) {
+          k0 = k1;
+          k1 = k2;
+          k2 = k3;
+          k3 = kEmpty;
+          ++popped;
+        }
+      }
+      exact = __any_sync(kFull, dropped && popped >= 4);
+    }
+    if (exact) {
+      // ---- exact path: keys below the current K-th key are pulled out in
+      // ascending order with REDUX and inserted into the sorted list held by
+      // lanes 0..KM-1.  Every lane holding the pulled key clears it, and a
+      // key already listed is skipped, so a train index reached from several
+      // tables is taken once.
+      lst = kEmpty;
+      uint32_t thr = kEmpty;
+      for_each_round([&](bool, uint32_t key) {
         key = key < thr ? key : kEmpty;
-      }
-      for (;;) {
-        const uint32_t m = __reduce_min_sync(kFull, key);
-        if (m >= thr) break;
-        if (key == m) key = kEmpty;
-        if (!__any_sync(kFull, lane < KM && lst == m)) {
-          const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
-          const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
-          lst = lane < KM ? nv : kEmpty;
-          thr = __shfl_sync(kFull, lst, K - 1);
+        for (;;) {
+          const uint32_t m = __reduce_min_sync(kFull, key);
+          if (m >= thr) break;
+          if (key == m) key = kEmpty;
+          if (!__any_sync(kFull, lane < KM && lst == m)) {
+            const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
+            const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
+            lst = lane < KM ? nv : kEmpty;
+            thr = __shfl_sync(kFull, lst, K - 1);
+          }
         }
-      }
+      });
+      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
     }
 
     // ---- re-rank + ratio test
@@ -843,13 +841,13 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // ---------------------------------------------------------------------------
 void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
                      cudaStream_t s) {
-  constexpr int smem = kMeanStages * kMeanRows * kDim * 4;
+  constexpr int smem = kMeanStages * kMeanRows * kMeanCh * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(row_mean_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  row_mean_tma_kernel<<<1, 160, smem, s>>>(imgs, n_imgs, mean_out, acc_out);
+  row_mean_tma_kernel<<<kDim / kMeanCh, kMeanThreads, smem, s>>>(imgs, n_imgs, mean_out, acc_out);
 }
 
 static size_t codes_smem_bytes() {
