@@ -131,7 +131,11 @@ struct PinnedRing {
 struct ArenaImage {
   float* d = nullptr;
   uint64_t n = 0;
+  uint32_t flag_slot = 0;  // ready flag in d_flags, written after the H2D
+  uint32_t gen = 0;        // upload generation (flags only increase per slot)
 };
+
+constexpr uint32_t kFlagSlots = 1u << 20;
 
 struct Timer {
   std::string cls;
@@ -155,6 +159,9 @@ struct bmg_context {
   // arena (DeviceArena, engine.hpp:20-44)
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
+  bmg::DevBuf d_flags;  // u32[kFlagSlots] upload-completion generations
+  std::vector<uint32_t> free_flag_slots;
+  uint32_t next_flag_slot = 0, gen_counter = 0;
   cudaStream_t s_copy = nullptr, s_comp = nullptr, s_mean = nullptr;
   // row means run on their own stream so row r+1's sequential chain overlaps
   // row r's codes and matching; slots are recycled through events
@@ -292,9 +299,25 @@ void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
   ArenaImage im;
   im.n = n;
+  if (!c.free_flag_slots.empty()) {
+    im.flag_slot = c.free_flag_slots.back();
+    c.free_flag_slots.pop_back();
+  } else {
+    if (c.next_flag_slot >= kFlagSlots) fail(BMG_OUT_OF_MEMORY, "too many resident images");
+    im.flag_slot = c.next_flag_slot++;
+  }
+  im.gen = ++c.gen_counter;
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
                            c.s_copy));
   stage_h2d(c, im.d, desc, n * 512);
+  {
+    // publish "image landed" in stream order after its copy; the value lives
+    // in the pinned ring until a wrap, which synchronises the device
+    uint32_t* hv = c.ring.alloc<uint32_t>(1, c.s_comp, c.s_copy);
+    *hv = im.gen;
+    BMG_CUDA(cudaMemcpyAsync(c.d_flags.as<uint32_t>() + im.flag_slot, hv, sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, c.s_copy));
+  }
   c.resident.emplace(id, im);
   c.occupancy += n;
   c.peak = std::max(c.peak, c.occupancy);
@@ -309,6 +332,7 @@ void arena_evict(Ctx& c, uint64_t id) {
     fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
   // stream-ordered free after every kernel already queued on the compute stream
   BMG_CUDA(cudaFreeAsync(it->second.d, c.s_comp));
+  c.free_flag_slots.push_back(it->second.flag_slot);
   c.occupancy -= it->second.n;
   c.resident.erase(it);
   ++c.evictions;
@@ -319,7 +343,7 @@ void join_uploads(Ctx& c) {
   if (!c.pending_upload) return;
   BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
   BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_uploaded, 0));
-  BMG_CUDA(cudaStreamWaitEvent(c.s_mean, c.ev_uploaded, 0));
+  // (the mean stream does not wait: its producer polls each image's flag)
   c.pending_upload = false;
 }
 
@@ -329,7 +353,8 @@ void join_uploads(Ctx& c) {
 // scratch, computes the mean (unless given) and launches codes, fixup and
 // bucket-table kernels on the compute stream.
 void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
-                       const float* mean_host, const float* mean_dev, bool compute_mean) {
+                       const float* mean_host, const float* mean_dev, bool compute_mean,
+                       const std::vector<std::pair<const uint32_t*, uint32_t>>* ready = nullptr) {
   const HashDev& h = c.hd;
   const int n_imgs = static_cast<int>(descs.size());
   const int L = h.tables;
@@ -373,6 +398,8 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.cursor = reinterpret_cast<uint32_t*>(base + lay[i].cursor_off);
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
     im.overflow = 0;
+    im.ready = ready ? (*ready)[i].first : nullptr;
+    im.ready_gen = ready ? (*ready)[i].second : 0u;
   }
   // metadata
   ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
@@ -472,7 +499,9 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
 
 void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
   std::vector<std::pair<const float*, uint64_t>> descs;
+  std::vector<std::pair<const uint32_t*, uint32_t>> ready;
   descs.reserve(n);
+  ready.reserve(n);
   c.row_ids.assign(ids, ids + n);
   c.row_slot.clear();
   for (uint64_t i = 0; i < n; ++i) {
@@ -482,10 +511,11 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
     descs.emplace_back(it->second.d, it->second.n);
+    ready.emplace_back(c.d_flags.as<uint32_t>() + it->second.flag_slot, it->second.gen);
     c.row_slot[ids[i]] = static_cast<int>(i);
   }
   c.row_valid = false;
-  prepare_row_views(c, descs, mean_host, nullptr, true);
+  prepare_row_views(c, descs, mean_host, nullptr, true, &ready);
   c.row_valid = true;
 }
 
@@ -733,6 +763,8 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
       BMG_CUDA(cudaEventRecord(c->stage_ev[i], c->s_copy));
     }
     c->ring.init(64u << 20);
+    c->d_flags.ensure(sizeof(uint32_t) * kFlagSlots);
+    BMG_CUDA(cudaMemset(c->d_flags.p, 0, sizeof(uint32_t) * kFlagSlots));
     c->hd = build_hash(*c, cfg->hash, cfg->coarse_planes, cfg->fine_planes);
     *out = c.release();
   });
@@ -748,7 +780,8 @@ int bmg_destroy(bmg_context* c) {
     for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
                       &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
                       &c->d_work, &c->d_dense, &c->d_dense_off, &c->d_pair_count, &c->d_nq,
-                      &c->d_res_off, &c->d_res, &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes})
+                      &c->d_res_off, &c->d_res, &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes,
+                      &c->d_flags})
       b->release();
     for (int i = 0; i < 2; ++i) {
       if (c->stage[i]) cudaFreeHost(c->stage[i]);

@@ -20,6 +20,12 @@ struct ImgDev {
   uint32_t* slots;     // [tables][n] train indices grouped by bucket (:136-145)
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
+  // upload completion flag written by the copy stream after the image's H2D
+  // (value = upload generation); the row-mean producer waits on it so the
+  // mean chain overlaps the transfers.  nullptr = already resident.
+  const uint32_t* ready;
+  uint32_t ready_gen;
+  uint32_t pad_;
 };
 
 struct HashDev {

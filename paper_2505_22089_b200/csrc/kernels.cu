@@ -106,6 +106,21 @@ __global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const Img
       for (int im = 0; im < n_imgs; ++im) {
         const float* src = imgs[im].desc + c0;
         const uint32_t n = imgs[im].n;
+        if (const uint32_t* flag = imgs[im].ready) {
+          // stream the image as soon as its H2D has landed (bounded wait)
+          const uint32_t gen = imgs[im].ready_gen;
+          unsigned long long t0, now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if ((int32_t)(v - gen) >= 0) break;  // generations only grow per slot
+            __nanosleep(256);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (now - t0 > 20000000000ull) __trap();  // 20 s: an upload never completed
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
           const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
           mbar_wait(smem_addr(&empty_bar[s]), ph ^ 1u);
