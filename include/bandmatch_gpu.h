@@ -151,6 +151,14 @@ typedef struct {
 /* Keep every image resident: eviction directives are skipped (no free, no
  * bookkeeping).  Used to measure the row body on HBM-resident inputs. */
 #define BMG_EXEC_RETAIN 1u
+/* Row-mean speculation (default: rows with >= 32768 descriptors compute their
+ * codes from a parallel mean while the exact sequential mean runs alongside;
+ * a bit-pattern check gates a re-do with the exact mean).  Results are
+ * identical either way; these flags only steer where the time goes.
+ * FORCE_REDO is a test hook that always takes the re-do path. */
+#define BMG_EXEC_NO_SPECULATION 2u
+#define BMG_EXEC_FORCE_SPECULATION 4u
+#define BMG_EXEC_FORCE_REDO 8u
 
 /* ---- status ------------------------------------------------------------ */
 const char* bmg_status_name(int status);              /* "InvalidArgument", ... */

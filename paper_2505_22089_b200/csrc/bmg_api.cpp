@@ -136,6 +136,9 @@ struct ArenaImage {
 };
 
 constexpr uint32_t kFlagSlots = 1u << 20;
+// Rows at least this large compute codes from the speculative parallel mean
+// (below it the exact chain takes < ~0.1 ms and is simply waited for).
+constexpr uint64_t kSpeculateMinDescriptors = 32768;
 
 struct Timer {
   std::string cls;
@@ -144,6 +147,16 @@ struct Timer {
 
 struct RowLayout {
   size_t coarse_off, fine_off, offsets_off, cursor_off, slots_off;
+};
+
+// What the codes/tables kernels of the current row need to be (re)issued.
+struct RowState {
+  int n_imgs = 0;
+  size_t n_tiles = 0;
+  uint32_t fix_cap = 0;
+  uint64_t total_desc = 0;
+  size_t codes_bytes = 0, offsets_begin = 0, offsets_bytes = 0;
+  int spec_slot = -1;  // mean slot awaiting verification (speculative row), or -1
 };
 
 }  // namespace
@@ -170,6 +183,9 @@ struct bmg_context {
   cudaEvent_t ev_mean_done[kMeanSlots] = {}, ev_mean_free[kMeanSlots] = {};
   uint64_t mean_seq = 0;
   float* cur_mean = nullptr;
+  bmg::RowState rs;
+  bmg::DevBuf d_mean_fast, d_partial, d_redo;
+  uint64_t spec_rows = 0;  // rows whose codes were computed speculatively
   cudaMemPool_t pool = nullptr;
   cudaEvent_t ev_uploaded = nullptr;
   bool pending_upload = false;
@@ -349,12 +365,60 @@ void join_uploads(Ctx& c) {
 
 // ---- row body -------------------------------------------------------------
 
+// Codes (+ FP64 fixups) and bucket tables for the current row views, centred
+// on `d_mean`.  With a gate, every kernel (and the clears) is a no-op unless
+// *gate != 0: the re-do pass after a mean speculation miss.
+void enqueue_codes_tables(Ctx& c, const float* d_mean, const uint32_t* gate) {
+  const RowState& rs = c.rs;
+  if (rs.n_tiles == 0) return;
+  cudaStream_t s = c.s_comp;
+  HashDev h = c.hd;
+  h.gate = gate;
+  char* base = c.d_scratch.as<char>();
+  const int plane_chunks = (h.n_planes + kPlaneChunk - 1) / kPlaneChunk;
+  if (gate) {
+    launch_gated_clear(base + rs.offsets_begin, rs.offsets_bytes, gate, s);
+    if (plane_chunks > 1) launch_gated_clear(base, rs.codes_bytes, gate, s);
+    launch_gated_clear(c.d_fixcnt.p, sizeof(uint32_t) * (1 + rs.n_imgs), gate, s);
+    c.launches += plane_chunks > 1 ? 3 : 2;
+  } else {
+    BMG_CUDA(cudaMemsetAsync(base + rs.offsets_begin, 0, rs.offsets_bytes, s));
+    if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, rs.codes_bytes, s));
+    BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + rs.n_imgs), s));
+  }
+  const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
+  const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
+  const uint32_t* d_tile_start = d_tile_img + rs.n_tiles;
+  unsigned long long* diag = c.d_diag.as<unsigned long long>();
+  {
+    Timed t(c, "codes", s);
+    launch_codes(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), d_mean,
+                 c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(), rs.fix_cap, s);
+    ++c.launches;
+    check_launch();
+  }
+  {
+    Timed t(c, "fixup", s);
+    launch_codes_fixup(h, d_imgs, rs.n_imgs, d_mean, c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(),
+                       rs.fix_cap, diag, s);
+    c.launches += 2;
+    check_launch();
+  }
+  {
+    Timed t(c, "tables", s);
+    launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), rs.n_imgs, s);
+    c.launches += 3;
+    check_launch();
+  }
+}
+
 // Lays out codes + tables for `descs` (device pointers, counts) in the row
 // scratch, computes the mean (unless given) and launches codes, fixup and
 // bucket-table kernels on the compute stream.
 void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
                        const float* mean_host, const float* mean_dev, bool compute_mean,
-                       const std::vector<std::pair<const uint32_t*, uint32_t>>* ready = nullptr) {
+                       const std::vector<std::pair<const uint32_t*, uint32_t>>* ready = nullptr,
+                       bool speculate = false) {
   const HashDev& h = c.hd;
   const int n_imgs = static_cast<int>(descs.size());
   const int L = h.tables;
@@ -427,11 +491,16 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   if (n_tiles)
     BMG_CUDA(cudaMemcpyAsync(c.d_tiles.p, h_tiles, sizeof(uint32_t) * 2 * n_tiles,
                              cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemsetAsync(base + codes_end, 0, offsets_end - codes_end, s));
-  const int plane_chunks = (h.n_planes + kPlaneChunk - 1) / kPlaneChunk;
-  if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, codes_end, s));
-  BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + n_imgs), s));
   BMG_CUDA(cudaMemsetAsync(c.d_diag.p, 0, sizeof(unsigned long long) * 4, s));
+  RowState& rs = c.rs;
+  rs.n_imgs = n_imgs;
+  rs.n_tiles = n_tiles;
+  rs.fix_cap = fix_cap;
+  rs.total_desc = total_desc;
+  rs.codes_bytes = codes_end;
+  rs.offsets_begin = codes_end;
+  rs.offsets_bytes = offsets_end - codes_end;
+  rs.spec_slot = -1;
   join_uploads(c);
 
   const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
@@ -451,6 +520,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     std::memcpy(hm, mean_host, sizeof(float) * kDim);
     BMG_CUDA(cudaMemcpyAsync(d_mean, hm, sizeof(float) * kDim, cudaMemcpyHostToDevice, s));
   } else if (compute_mean) {
+    // the exact sequential chain, on its own stream
     cudaStream_t sm = c.s_mean;
     BMG_CUDA(cudaStreamWaitEvent(sm, c.ev_mean_free[mean_slot], 0));
     ImgDev* hm = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
@@ -465,39 +535,30 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
       check_launch();
     }
     BMG_CUDA(cudaEventRecord(c.ev_mean_done[mean_slot], sm));
+    if (speculate && n_tiles) {
+      // codes from the parallel mean now; verified after the row's matches
+      c.d_mean_fast.ensure(sizeof(float) * kDim);
+      c.d_partial.ensure(sizeof(double) * kDim * n_tiles);
+      {
+        Timed t(c, "mean_fast", s);
+        launch_mean_fast(d_imgs, c.d_tiles.as<uint32_t>(), c.d_tiles.as<uint32_t>() + n_tiles,
+                         static_cast<int>(n_tiles), c.d_partial.as<double>(), total_desc,
+                         c.d_mean_fast.as<float>(), s);
+        c.launches += 2;
+        check_launch();
+      }
+      rs.spec_slot = mean_slot;
+      enqueue_codes_tables(c, c.d_mean_fast.as<float>(), nullptr);
+      return;
+    }
     BMG_CUDA(cudaStreamWaitEvent(s, c.ev_mean_done[mean_slot], 0));
   }
-  if (n_tiles == 0) {
-    if (mean_slot >= 0) BMG_CUDA(cudaEventRecord(c.ev_mean_free[mean_slot], s));
-    return;
-  }
-  const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
-  const uint32_t* d_tile_start = d_tile_img + n_tiles;
-  unsigned long long* diag = c.d_diag.as<unsigned long long>();
-  {
-    Timed t(c, "codes", s);
-    launch_codes(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(n_tiles), d_mean,
-                 c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(), fix_cap, s);
-    ++c.launches;
-    check_launch();
-  }
-  {
-    Timed t(c, "fixup", s);
-    launch_codes_fixup(h, d_imgs, n_imgs, d_mean, c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(),
-                       fix_cap, diag, s);
-    c.launches += 2;
-    check_launch();
-  }
+  enqueue_codes_tables(c, d_mean, nullptr);
   if (mean_slot >= 0) BMG_CUDA(cudaEventRecord(c.ev_mean_free[mean_slot], s));
-  {
-    Timed t(c, "tables", s);
-    launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(n_tiles), n_imgs, s);
-    c.launches += 3;
-    check_launch();
-  }
 }
 
-void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
+void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host,
+                 bool speculate = false) {
   std::vector<std::pair<const float*, uint64_t>> descs;
   std::vector<std::pair<const uint32_t*, uint32_t>> ready;
   descs.reserve(n);
@@ -515,7 +576,7 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     c.row_slot[ids[i]] = static_cast<int>(i);
   }
   c.row_valid = false;
-  prepare_row_views(c, descs, mean_host, nullptr, true, &ready);
+  prepare_row_views(c, descs, mean_host, nullptr, true, &ready, speculate);
   c.row_valid = true;
 }
 
@@ -535,7 +596,8 @@ void check_match_params(const Ctx& c, const bmg_match_params& mp) {
 // current row views.  Offsets (absolute positions in d_res) go to
 // out_off[0..n_pairs], appended after *d_running.
 void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
-                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res) {
+                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res,
+                   const uint32_t* gate = nullptr) {
   check_match_params(c, mp);
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
@@ -591,7 +653,12 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   BMG_CUDA(cudaMemcpyAsync(c.d_dense_off.p, h_dense_off, sizeof(uint64_t) * n_pairs,
                            cudaMemcpyHostToDevice, s));
   BMG_CUDA(cudaMemcpyAsync(c.d_nq.p, h_nq, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
+  if (gate) {
+    launch_gated_clear(c.d_pair_count.p, sizeof(uint32_t) * n_pairs, gate, s);
+    ++c.launches;
+  } else {
+    BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
+  }
   MatchLaunch a{};
   a.imgs = c.d_imgs.as<ImgDev>();
   a.work = c.d_work.as<PairWork>();
@@ -604,6 +671,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   a.k = mp.k_nearest;
   a.idx_bits = idx_bits;
   a.ratio = mp.ratio;
+  a.gate = gate;
   if (n_work) {
     Timed t(c, "match", s);
     launch_match(a, h.fwp, static_cast<int>(n_work), c.row_imgs[0], max_train_n, s, nullptr);
@@ -613,12 +681,40 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   {
     Timed t(c, "compact", s);
     launch_scan_counts(c.d_pair_count.as<uint32_t>(), n_pairs, out_off,
-                       c.d_running.as<unsigned long long>(), s);
+                       c.d_running.as<unsigned long long>(), gate, s);
     launch_compact(c.d_dense.as<int32_t>(), c.d_dense_off.as<uint64_t>(), c.d_nq.as<uint32_t>(),
-                   out_off, n_pairs, d_res, s);
+                   out_off, n_pairs, d_res, gate, s);
     c.launches += 2;
     check_launch();
   }
+}
+
+// After a speculative row's matches: wait for the exact sequential mean,
+// compare bit patterns, and enqueue the gated re-do of codes, tables and
+// matches (kernels exit at once unless the check found a difference; a re-do
+// appends the correct lists to the result log and rewrites the row's offsets).
+void enqueue_row_verify(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
+                        const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res,
+                        bool force_redo) {
+  const int slot = c.rs.spec_slot;
+  if (slot < 0) return;
+  cudaStream_t s = c.s_comp;
+  c.d_redo.ensure(sizeof(uint32_t));
+  uint32_t* redo = c.d_redo.as<uint32_t>();
+  const float* exact = c.d_mean_slot[slot].as<float>();
+  BMG_CUDA(cudaStreamWaitEvent(s, c.ev_mean_done[slot], 0));
+  if (force_redo) {
+    BMG_CUDA(cudaMemsetAsync(redo, 0xff, sizeof(uint32_t), s));  // test hook: always re-do
+  } else {
+    launch_mean_check(c.d_mean_fast.as<float>(), exact, redo, s);
+    ++c.launches;
+    check_launch();
+  }
+  enqueue_codes_tables(c, exact, redo);
+  enqueue_match(c, slot_pairs, mp, out_off, d_res, redo);
+  BMG_CUDA(cudaEventRecord(c.ev_mean_free[slot], s));
+  c.rs.spec_slot = -1;
+  ++c.spec_rows;
 }
 
 HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const float* fine) {
@@ -1100,7 +1196,12 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
           }
         }
-        prepare_row(*c, needed, ne - nb, nullptr);
+        uint64_t row_desc = 0;
+        for (uint64_t k = nb; k < ne; ++k) row_desc += c->resident.at(plan->needed_ids[k]).n;
+        const bool speculate = (opts->flags & BMG_EXEC_NO_SPECULATION) == 0 &&
+                               ((opts->flags & (BMG_EXEC_FORCE_SPECULATION | BMG_EXEC_FORCE_REDO)) ||
+                                row_desc >= kSpeculateMinDescriptors);
+        prepare_row(*c, needed, ne - nb, nullptr, speculate);
         const uint64_t pb = plan->row_pair_offsets[row], pe = plan->row_pair_offsets[row + 1];
         std::vector<std::pair<int, int>> sp;
         sp.reserve(pe - pb);
@@ -1112,6 +1213,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           sp.emplace_back(qa->second, tb->second);
         }
         enqueue_match(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>());
+        enqueue_row_verify(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>(),
+                           (opts->flags & BMG_EXEC_FORCE_REDO) != 0);
         it_pairs += pe - pb;
         for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
           arena_evict(*c, plan->evict_ids[k]);

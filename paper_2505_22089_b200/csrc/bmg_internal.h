@@ -38,6 +38,9 @@ struct HashDev {
   const float* planes;     // [n_planes][128] planes (coarse first, then fine)
   const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
   int n_planes_pad;
+  // when non-null, kernels return immediately unless *gate != 0 (the
+  // re-do pass after a mean speculation miss; see bmg_api.cpp)
+  const uint32_t* gate;
 };
 
 // An ambiguous projection whose sign the FP32 pass could not certify; the
@@ -63,6 +66,7 @@ struct MatchLaunch {
   unsigned long long* exact_queries;  // diagnostics: queries that took the FP64 path
   int tables, n_buckets, k, idx_bits;
   double ratio;
+  const uint32_t* gate;        // see HashDev::gate
 };
 
 // ---- launchers (kernels.cu) ----
@@ -79,9 +83,18 @@ void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* til
 void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev& any_train_max,
                   uint32_t max_train_n, cudaStream_t s, int* smem_used);
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, cudaStream_t s);
+                        unsigned long long* running_total, const uint32_t* gate, cudaStream_t s);
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
-                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);
+                    const uint64_t* out_off, int n_pairs, int32_t* out, const uint32_t* gate,
+                    cudaStream_t s);
+// speculative row mean: order-free FP64 sums per 128-descriptor tile, then a
+// fixed-order reduction -> float(sum / total)
+void launch_mean_fast(const ImgDev* imgs, const uint32_t* tile_img, const uint32_t* tile_start,
+                      int n_tiles, double* partial, unsigned long long total, float* mean_out,
+                      cudaStream_t s);
+// *redo = any bit of the speculative mean differs from the exact one
+void launch_mean_check(const float* fast, const float* exact, uint32_t* redo, cudaStream_t s);
+void launch_gated_clear(void* p, size_t bytes, const uint32_t* gate, cudaStream_t s);
 
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
 constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)

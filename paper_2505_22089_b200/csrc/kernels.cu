@@ -16,6 +16,7 @@
 // it with __dadd_rn/__dmul_rn/__dsub_rn/__dsqrt_rn in the reference order.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 
 #include "bmg_internal.h"
@@ -31,6 +32,77 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Re-do pass gate (uniform across the grid): the kernel is a no-op unless the
+// mean speculation of its row missed.
+__device__ __forceinline__ bool gated_off(const uint32_t* gate) {
+  return gate != nullptr && *reinterpret_cast<const volatile uint32_t*>(gate) == 0u;
+}
+
+// ---------------------------------------------------------------------------
+// Speculative row mean.  The exact mean is a 128-lane sequential FP64 chain
+// (K1 below) -- a latency-bound millisecond per large row.  The row's codes,
+// tables and matches are instead computed from a parallel FP64 mean (order-
+// free tile sums, fixed-order reduction; a few double ulps from the
+// sequential sum, so its float rounding is almost always identical) while K1
+// runs on its own stream; mean_check compares the bit patterns and, on any
+// difference, the row is recomputed by a gated second pass with the exact
+// mean.  Results are therefore always those of the reference's sequential
+// mean; only the time of a (rare) miss is paid twice.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDim) mean_partial_kernel(const ImgDev* __restrict__ imgs,
+                                                            const uint32_t* __restrict__ tile_img,
+                                                            const uint32_t* __restrict__ tile_start,
+                                                            double* __restrict__ partial) {
+  const int c = threadIdx.x;
+  const ImgDev im = imgs[tile_img[blockIdx.x]];
+  const uint32_t i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(im.n - i0));
+  const float* d = im.desc + (size_t)i0 * kDim + c;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int r = 0;
+  for (; r + 4 <= nd; r += 4) {
+    s0 += (double)__ldg(d + (size_t)r * kDim);
+    s1 += (double)__ldg(d + (size_t)(r + 1) * kDim);
+    s2 += (double)__ldg(d + (size_t)(r + 2) * kDim);
+    s3 += (double)__ldg(d + (size_t)(r + 3) * kDim);
+  }
+  for (; r < nd; ++r) s0 += (double)__ldg(d + (size_t)r * kDim);
+  partial[(size_t)blockIdx.x * kDim + c] = (s0 + s1) + (s2 + s3);
+}
+
+__global__ void __launch_bounds__(1024) mean_final_kernel(const double* __restrict__ partial, int n_tiles,
+                                                          unsigned long long total,
+                                                          float* __restrict__ mean_out) {
+  __shared__ double s_part[8][kDim];
+  const int c = threadIdx.x & (kDim - 1), part = threadIdx.x >> 7;  // 8 parts x 128 channels
+  double s = 0.0;
+  for (int t = part; t < n_tiles; t += 8) s += partial[(size_t)t * kDim + c];
+  s_part[part][c] = s;
+  __syncthreads();
+  if (part == 0) {
+    double a = 0.0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) a += s_part[p][c];
+    mean_out[c] = total ? __double2float_rn(a / (double)total) : 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(kDim) mean_check_kernel(const float* __restrict__ fast,
+                                                          const float* __restrict__ exact,
+                                                          uint32_t* __restrict__ redo) {
+  const int c = threadIdx.x;
+  const int diff = __float_as_uint(fast[c]) != __float_as_uint(exact[c]);
+  const int any = __syncthreads_or(diff);
+  if (c == 0) *redo = any ? 1u : 0u;
+}
+
+__global__ void gated_clear_kernel(uint32_t* __restrict__ p, size_t words, const uint32_t* gate) {
+  if (gated_off(gate)) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+
 // ---------------------------------------------------------------------------
 // K1: row centering mean (engine.cpp:446-461).  acc[c] += (double)d.v[c] over
 // images in ascending id order, descriptors in index order, then
@@ -43,7 +115,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // at +0.0 (it can never become -0.0 under round-to-nearest).
 // ---------------------------------------------------------------------------
 constexpr int kMeanRows = 32;
-constexpr int kMeanStages = 16;
+constexpr int kMeanStages = 12;  // 12 x 16 KB stages
 constexpr int kMeanCh = 64;                 // channels per CTA (grid = 128 / kMeanCh)
 constexpr int kMeanThreads = kMeanCh + 32;  // consumers + one producer warp
 
@@ -83,7 +155,7 @@ __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint
 __global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const ImgDev* __restrict__ imgs,
                                                                        int n_imgs, float* __restrict__ mean_out,
                                                                        double* __restrict__ acc_out) {
-  extern __shared__ __align__(128) float ring[];  // [stages][rows][kMeanCh]
+  extern __shared__ __align__(128) float ring[];  // [stages][rows][128]
   __shared__ __align__(8) unsigned long long full_bar[kMeanStages], empty_bar[kMeanStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kConsumerWarps = kMeanCh / 32;
@@ -96,15 +168,14 @@ __global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const Img
   }
   __syncthreads();
   const uint32_t ring_base = smem_addr(ring);
-  constexpr uint32_t kRowBytes = kMeanCh * 4;
-  constexpr uint32_t kStageBytes = kMeanRows * kRowBytes;
+  constexpr uint32_t kStageBytes = kMeanRows * kDim * 4;
   const int c0 = blockIdx.x * kMeanCh;
 
   if (warp == kConsumerWarps) {  // ---- producer
     if (lane == 0) {
       uint32_t g = 0;
       for (int im = 0; im < n_imgs; ++im) {
-        const float* src = imgs[im].desc + c0;
+        const float* src = imgs[im].desc;
         const uint32_t n = imgs[im].n;
         if (const uint32_t* flag = imgs[im].ready) {
           // stream the image as soon as its H2D has landed (bounded wait)
@@ -124,12 +195,12 @@ __global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const Img
         for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
           const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
           mbar_wait(smem_addr(&empty_bar[s]), ph ^ 1u);
+          // whole rows in one bulk copy (per-row copies are TMA-issue bound);
+          // each CTA then reads only its half of every row from the stage
           const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
           const uint32_t bar = smem_addr(&full_bar[s]);
-          mbar_expect_tx(bar, rows * kRowBytes);
-          for (uint32_t r = 0; r < rows; ++r)
-            tma_bulk_g2s(ring_base + s * kStageBytes + r * kRowBytes, src + (size_t)(r0 + r) * kDim,
-                         kRowBytes, bar);
+          mbar_expect_tx(bar, rows * kDim * 4u);
+          tma_bulk_g2s(ring_base + s * kStageBytes, src + (size_t)r0 * kDim, rows * kDim * 4u, bar);
         }
       }
     }
@@ -152,9 +223,9 @@ __global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const Img
       const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
       mbar_wait(smem_addr(&full_bar[s]), ph);
       float w[kMeanRows];
-      const float* st = ring + (size_t)s * kMeanRows * kMeanCh + c;
+      const float* st = ring + (size_t)s * kMeanRows * kDim + c0 + c;
 #pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kMeanCh] : 0.0f;
+      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kDim] : 0.0f;
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty_bar[s]));
 #pragma unroll
@@ -201,6 +272,7 @@ __global__ void __launch_bounds__(512, 1)
                  const uint32_t* __restrict__ tile_start, const float* __restrict__ mean,
                  Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
                  uint32_t* __restrict__ overflow) {
+  if (gated_off(h.gate)) return;
   extern __shared__ __align__(16) float smem_f[];
   float* sP = smem_f;                                  // [128][192]
   float* sA = sP + kDim * kPlaneChunk;                 // [128][132]
@@ -368,6 +440,7 @@ __global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                    const float* __restrict__ mean, const Fixup* __restrict__ fix,
                                    const uint32_t* __restrict__ fix_count, uint32_t fix_cap,
                                    unsigned long long* fixed_bits) {
+  if (gated_off(h.gate)) return;
   const uint32_t n = min(*fix_count, fix_cap);
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const Fixup f = fix[e];
@@ -385,6 +458,7 @@ __global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
 __global__ void codes_overflow_kernel(HashDev h, const ImgDev* __restrict__ imgs, int n_imgs,
                                       const float* __restrict__ mean,
                                       const uint32_t* __restrict__ overflow) {
+  if (gated_off(h.gate)) return;
   for (int ii = 0; ii < n_imgs; ++ii) {
     if (!overflow[ii]) continue;
     const ImgDev im = imgs[ii];
@@ -407,6 +481,7 @@ __global__ void codes_overflow_kernel(HashDev h, const ImgDev* __restrict__ imgs
 __global__ void tables_hist_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                    const uint32_t* __restrict__ tile_img,
                                    const uint32_t* __restrict__ tile_start) {
+  if (gated_off(h.gate)) return;
   const ImgDev im = imgs[tile_img[blockIdx.x]];
   const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
   if (i >= im.n) return;
@@ -441,6 +516,7 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp
 }
 
 __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
+  if (gated_off(h.gate)) return;
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry;
   const ImgDev im = imgs[blockIdx.x];
@@ -466,6 +542,7 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
 __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                       const uint32_t* __restrict__ tile_img,
                                       const uint32_t* __restrict__ tile_start) {
+  if (gated_off(h.gate)) return;
   const ImgDev im = imgs[tile_img[blockIdx.x]];
   const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
   if (i >= im.n) return;
@@ -500,21 +577,26 @@ constexpr int kBaseOff = kMaxTables + 2;  // s_tab: cum_t at [0, L+1], slot base
 
 
 template <int FWP, bool SMEM>
-__device__ __forceinline__ uint32_t hamming(const unsigned char* smem_codes,
+__device__ __forceinline__ uint32_t hamming(uint32_t smem_codes,  // shared-window address
                                             const uint64_t* __restrict__ gcodes, uint32_t j,
                                             const uint64_t (&qc)[FWP]) {
   uint32_t h = 0;
   if constexpr (SMEM && FWP % 2 == 0) {
-    const ulonglong2* sc = reinterpret_cast<const ulonglong2*>(smem_codes) + (size_t)j * (FWP / 2);
+    const uint32_t addr = smem_codes + j * (FWP * 8u);
 #pragma unroll
     for (int x = 0; x < FWP / 2; ++x) {
-      const ulonglong2 v = sc[x];
-      h += __popcll(qc[2 * x] ^ v.x) + __popcll(qc[2 * x + 1] ^ v.y);
+      unsigned long long v0, v1;
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "r"(addr + 16u * x));
+      h += __popcll(qc[2 * x] ^ v0) + __popcll(qc[2 * x + 1] ^ v1);
     }
   } else if constexpr (SMEM) {
-    const uint64_t* sc = reinterpret_cast<const uint64_t*>(smem_codes) + (size_t)j * FWP;
+    const uint32_t addr = smem_codes + j * (FWP * 8u);
 #pragma unroll
-    for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ sc[x]);
+    for (int x = 0; x < FWP; ++x) {
+      unsigned long long v;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr + 8u * x));
+      h += __popcll(qc[x] ^ v);
+    }
   } else {
 #pragma unroll
     for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ __ldg(gcodes + (size_t)j * FWP + x));
@@ -527,8 +609,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ uint32_t s_tab[NT / 32][kBaseOff + kMaxTables];
-  constexpr uint32_t kSeg = 256;
-  __shared__ uint32_t s_slots[NT / 32][kSeg];
+  if (gated_off(a.gate)) return;
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
@@ -566,6 +647,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   }
 
   const int L = a.tables, K = a.k, ib = a.idx_bits;
+  const uint32_t scodes = smem_addr(smem_raw);
   const uint32_t idx_mask = (1u << ib) - 1u;
   const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
@@ -601,28 +683,28 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 #pragma unroll
     for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
 
-    // The flattened union is consumed in segments of kSeg entries: a
-    // table-major, coalesced copy of the segment's train indices into this
-    // warp's shared buffer, then 32-wide rounds over the buffer.
-    uint32_t* seg_buf = s_slots[warp];
+    // The flattened union is walked 32 entries per round, lane l taking entry
+    // base + l.  Each lane keeps its own cursor (table, end, slot base): a
+    // round advances it by 32 entries, i.e. across at most ~1 table boundary.
     auto for_each_round = [&](auto&& round) {
-      int t_first = 0;
-      for (uint32_t seg = 0; seg < total; seg += kSeg) {
-        const uint32_t seg_end = min(total, seg + kSeg);
-        while (tab[t_first + 1] <= seg) ++t_first;
-        for (int t = t_first; t < L && tab[t] < seg_end; ++t) {
-          const uint32_t lo_e = max(tab[t], seg), hi_e = min(tab[t + 1], seg_end);
-          const uint32_t gbase = tab[kBaseOff + t];
-          for (uint32_t e = lo_e + lane; e < hi_e; e += 32) seg_buf[e - seg] = __ldg(T.slots + gbase + e);
+      int t = 0;
+      uint32_t t_end = tab[1], sbase = tab[kBaseOff];
+      for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t e = base + lane;
+        const bool valid = e < total;
+        uint32_t key = kEmpty;
+        if (valid) {
+          if (e >= t_end) {
+            do {
+              ++t;
+              t_end = tab[t + 1];
+            } while (e >= t_end);
+            sbase = tab[kBaseOff + t];
+          }
+          const uint32_t j = __ldg(T.slots + sbase + e);
+          key = (hamming<FWP, SMEM>(scodes, T.fine, j, qc) << ib) | j;
         }
-        __syncwarp();
-        for (uint32_t b = 0; b < seg_end - seg; b += 32) {
-          const uint32_t e = b + lane;
-          const bool valid = e < seg_end - seg;
-          const uint32_t j = valid ? seg_buf[e] : 0u;
-          round(valid, valid ? (hamming<FWP, SMEM>(smem_raw, T.fine, j, qc) << ib) | j : kEmpty);
-        }
-        __syncwarp();
+        round(valid, key);
       }
     };
     uint32_t lst = kEmpty;
@@ -802,7 +884,9 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __restrict__ counts, int n,
                                                            uint64_t* __restrict__ offsets,
-                                                           unsigned long long* running_total) {
+                                                           unsigned long long* running_total,
+                                                           const uint32_t* gate) {
+  if (gated_off(gate)) return;
   __shared__ uint32_t s_warp[32];
   __shared__ unsigned long long s_carry;
   if (threadIdx.x == 0) s_carry = *running_total;
@@ -825,7 +909,9 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
                                                        const uint64_t* __restrict__ dense_off,
                                                        const uint32_t* __restrict__ nq,
                                                        const uint64_t* __restrict__ out_off,
-                                                       int32_t* __restrict__ out) {
+                                                       int32_t* __restrict__ out,
+                                                       const uint32_t* gate) {
+  if (gated_off(gate)) return;
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_base;
   const int p = blockIdx.x;
@@ -856,7 +942,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // ---------------------------------------------------------------------------
 void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
                      cudaStream_t s) {
-  constexpr int smem = kMeanStages * kMeanRows * kMeanCh * 4;
+  constexpr int smem = kMeanStages * kMeanRows * kDim * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(row_mean_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -939,13 +1025,32 @@ void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev&, uint
 }
 
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, cudaStream_t s) {
-  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total);
+                        unsigned long long* running_total, const uint32_t* gate, cudaStream_t s) {
+  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total, gate);
 }
 
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
-                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s) {
-  if (n_pairs > 0) compact_kernel<<<n_pairs, 1024, 0, s>>>(dense, dense_off, nq, out_off, out);
+                    const uint64_t* out_off, int n_pairs, int32_t* out, const uint32_t* gate,
+                    cudaStream_t s) {
+  if (n_pairs > 0) compact_kernel<<<n_pairs, 1024, 0, s>>>(dense, dense_off, nq, out_off, out, gate);
+}
+
+void launch_mean_fast(const ImgDev* imgs, const uint32_t* tile_img, const uint32_t* tile_start,
+                      int n_tiles, double* partial, unsigned long long total, float* mean_out,
+                      cudaStream_t s) {
+  if (n_tiles > 0) mean_partial_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, partial);
+  mean_final_kernel<<<1, 1024, 0, s>>>(partial, n_tiles, total, mean_out);
+}
+
+void launch_mean_check(const float* fast, const float* exact, uint32_t* redo, cudaStream_t s) {
+  mean_check_kernel<<<1, kDim, 0, s>>>(fast, exact, redo);
+}
+
+void launch_gated_clear(void* p, size_t bytes, const uint32_t* gate, cudaStream_t s) {
+  const size_t words = bytes / 4;
+  if (words == 0) return;
+  const int blocks = (int)std::min<size_t>(148 * 4, (words + 255) / 256);
+  gated_clear_kernel<<<blocks, 256, 0, s>>>(static_cast<uint32_t*>(p), words, gate);
 }
 
 }  // namespace bmg

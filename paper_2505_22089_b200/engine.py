@@ -205,6 +205,15 @@ class ExecuteOptions:
     on_upload: object = None  # DeviceBackend::on_upload(image_id, units)
     on_evict: object = None   # DeviceBackend::on_evict(image_id)
     retain: bool = False      # keep images resident (skip eviction directives)
+    # row-mean speculation: "auto" (rows >= 32768 descriptors), "off", "force",
+    # or "force_redo" (test hook: always take the exact re-do path)
+    speculation: str = "auto"
+
+    def flags(self) -> int:
+        spec = {"auto": 0, "off": 2, "force": 4, "force_redo": 8}
+        if self.speculation not in spec:
+            raise BandmatchError("InvalidArgument", f"unknown speculation mode {self.speculation!r}")
+        return (_lib.EXEC_RETAIN if self.retain else 0) | spec[self.speculation]
 
 
 @dataclass
@@ -280,8 +289,7 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
                        np.zeros((0, 2), np.int32)))
     on_up = wrap(opts.on_upload, _lib.UPLOAD_HOOK, lambda u, i, n: opts.on_upload(i, n))
     on_ev = wrap(opts.on_evict, _lib.EVICT_HOOK, lambda u, i: opts.on_evict(i))
-    oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None,
-                           _lib.EXEC_RETAIN if opts.retain else 0)
+    oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None, opts.flags())
     h = C.c_void_p()
     check(L.bmg_execute_plan(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc),
                              C.byref(h)))
