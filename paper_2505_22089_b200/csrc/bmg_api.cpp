@@ -774,7 +774,7 @@ void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fi
 }
 
 void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
-  c.d_res_off.ensure(sizeof(uint64_t) * (n_pairs + 1));
+  c.d_res_off.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
   c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
   c.d_running.ensure(sizeof(unsigned long long));
   BMG_CUDA(cudaMemsetAsync(c.d_running.p, 0, sizeof(unsigned long long), c.s_comp));
@@ -998,9 +998,13 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
       offsets_out[0] = 0;
       return;
     }
-    BMG_CUDA(cudaMemcpyAsync(offsets_out, c->d_res_off.p, sizeof(uint64_t) * (n_pairs + 1),
+    std::vector<uint64_t> ranges(2 * n_pairs);
+    BMG_CUDA(cudaMemcpyAsync(ranges.data(), c->d_res_off.p, sizeof(uint64_t) * 2 * n_pairs,
                              cudaMemcpyDeviceToHost, c->s_comp));
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    // one pass, so the pairs' ranges are contiguous from 0
+    offsets_out[0] = 0;
+    for (uint64_t p = 0; p < n_pairs; ++p) offsets_out[p + 1] = ranges[2 * p + 1];
     const uint64_t total = offsets_out[n_pairs];
     if (total > capacity) fail(BMG_INVALID_ARGUMENT, "match output capacity too small");
     if (total) {
@@ -1173,13 +1177,14 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       cap += features_of(a).count;
     }
     auto res = std::make_unique<bmg_result>();
-    reset_results(*c, n_pairs, cap);
+    // a row re-done after a mean speculation miss appends its lists again
+    const bool may_redo = (opts->flags & BMG_EXEC_NO_SPECULATION) == 0;
+    reset_results(*c, n_pairs, may_redo ? 2 * cap : cap);
     uint64_t* d_off = c->d_res_off.as<uint64_t>();
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->s_comp));
     BMG_CUDA(cudaStreamWaitEvent(c->s_mean, span0, 0));
     BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
-    BMG_CUDA(cudaMemsetAsync(d_off, 0, sizeof(uint64_t), c->s_comp));
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     uint64_t row = 0;
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
@@ -1212,8 +1217,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
           sp.emplace_back(qa->second, tb->second);
         }
-        enqueue_match(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>());
-        enqueue_row_verify(*c, sp, opts->match, d_off + pb, c->d_res.as<int32_t>(),
+        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, c->d_res.as<int32_t>());
+        enqueue_row_verify(*c, sp, opts->match, d_off + 2 * pb, c->d_res.as<int32_t>(),
                            (opts->flags & BMG_EXEC_FORCE_REDO) != 0);
         it_pairs += pe - pb;
         for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
@@ -1226,17 +1231,22 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->iterations.push_back(c->units_uploaded - units0);
     }
     BMG_CUDA(cudaEventRecord(span1, c->s_comp));
-    // read the device result log back once
-    std::vector<uint64_t> offs(n_pairs + 1, 0);
+    // read the device result log back once: per-pair [begin, end) ranges,
+    // then the log up to its running total (a row re-done after a mean
+    // speculation miss left its first lists unreferenced in the log)
+    std::vector<uint64_t> ranges(2 * n_pairs, 0);
+    unsigned long long log_total = 0;
     if (n_pairs) {
-      BMG_CUDA(cudaMemcpyAsync(offs.data(), d_off, sizeof(uint64_t) * (n_pairs + 1), cudaMemcpyDeviceToHost,
+      BMG_CUDA(cudaMemcpyAsync(ranges.data(), d_off, sizeof(uint64_t) * 2 * n_pairs,
+                               cudaMemcpyDeviceToHost, c->s_comp));
+      BMG_CUDA(cudaMemcpyAsync(&log_total, c->d_running.p, sizeof(log_total), cudaMemcpyDeviceToHost,
                                c->s_comp));
       BMG_CUDA(cudaStreamSynchronize(c->s_comp));
     }
-    const uint64_t total = offs[n_pairs];
-    std::vector<int32_t> flat(2 * total);
-    if (total)
-      BMG_CUDA(cudaMemcpy(flat.data(), c->d_res.p, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> flat(2 * log_total);
+    if (log_total)
+      BMG_CUDA(cudaMemcpy(flat.data(), c->d_res.p, sizeof(int32_t) * 2 * log_total, cudaMemcpyDeviceToHost));
+    uint64_t total = 0;
     // results keyed and sorted by IdPair (engine.cpp:419, 506-512); a pair
     // planned twice keeps its last match list, like the reference's map
     std::map<std::pair<uint64_t, uint64_t>, uint64_t> last;
@@ -1245,8 +1255,9 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     for (const auto& [key, p] : last) {
       res->pair_ids.push_back(key.first);
       res->pair_ids.push_back(key.second);
-      const uint64_t b = offs[p], e = offs[p + 1];
+      const uint64_t b = ranges[2 * p], e = ranges[2 * p + 1];
       res->matches.insert(res->matches.end(), flat.begin() + 2 * b, flat.begin() + 2 * e);
+      total += e - b;
       res->offsets.push_back(res->matches.size() / 2);
       if (opts->on_pair)
         opts->on_pair(opts->on_pair_user, key.first, key.second, flat.data() + 2 * b, e - b);

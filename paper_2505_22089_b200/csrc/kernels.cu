@@ -882,8 +882,11 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 // K6: per-launch exclusive scan of match counts (appending after the running
 // total of earlier rows) and ascending-query compaction of the dense arrays.
 // ---------------------------------------------------------------------------
+// ranges[2i], ranges[2i+1] = [begin, end) of pair i's matches in the result
+// log.  Per-pair ranges (not shared boundary offsets) so a re-do pass can
+// re-point one row's pairs without touching its neighbours.
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __restrict__ counts, int n,
-                                                           uint64_t* __restrict__ offsets,
+                                                           uint64_t* __restrict__ ranges,
                                                            unsigned long long* running_total,
                                                            const uint32_t* gate) {
   if (gated_off(gate)) return;
@@ -891,13 +894,15 @@ __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __res
   __shared__ unsigned long long s_carry;
   if (threadIdx.x == 0) s_carry = *running_total;
   __syncthreads();
-  if (threadIdx.x == 0) offsets[0] = s_carry;
   for (int base = 0; base < n; base += blockDim.x) {
     const int i = base + threadIdx.x;
     const uint32_t v = i < n ? counts[i] : 0u;
     const unsigned long long carry = s_carry;
     const uint32_t incl = block_incl_scan(v, s_warp);
-    if (i < n) offsets[i + 1] = carry + incl;
+    if (i < n) {
+      ranges[2 * i] = carry + incl - v;
+      ranges[2 * i + 1] = carry + incl;
+    }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) s_carry = carry + incl;
     __syncthreads();
@@ -917,7 +922,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
   const int p = blockIdx.x;
   const int32_t* d = dense + dense_off[p];
   const uint32_t n = nq[p];
-  uint64_t base = out_off[p];
+  uint64_t base = out_off[2 * p];  // [begin, end) ranges from scan_counts
   for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x) {
     const uint32_t q = q0 + threadIdx.x;
     const int32_t v = q < n ? d[q] : -1;

@@ -132,6 +132,24 @@ def test_random_pairs_match_oracle(oracle, k, ratio):
     assert len(ref) > (100 if ratio >= 0.5 else 0)
 
 
+@pytest.mark.parametrize("nq,nt", [(3000, 16384), (16384, 5000), (1, 20000)])
+def test_large_train_images_use_the_global_code_path(oracle, nq, nt):
+    # > 12,800 train descriptors do not fit the shared-memory code stage, so
+    # the kernel reads fine codes through L1/L2 (BASELINE configs 4 and 5)
+    hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
+    rng = np.random.default_rng(nq + nt)
+    base = unit_rows(rng, max(nq, nt))
+    t = base[:nt]
+    q = base[:nq] + 0.04 * rng.standard_normal((nq, 128)).astype(np.float32)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    qf, tf = FeatureSet(1, q), FeatureSet(2, t)
+    mean = np.mean(np.concatenate([q, t]), axis=0).astype(np.float32)
+    pm, qc, tc = gpu_match(hf, qf, tf, mean)
+    oc = oracle.compute_codes(t, hf.coarse, hf.fine, mean)
+    assert np.array_equal(tc.coarse, oc[0]) and np.array_equal(tc.fine, oc[1])
+    assert np.array_equal(pm.matches, oracle_match(oracle, hf, qf, tf, qc, tc))
+
+
 def test_full_size_synthetic_pair_matches_reference(reference, oracle):
     # BASELINE config 1: images (band, band+1) of generate_synthetic(ppi=8192)
     band = 11

@@ -1,0 +1,88 @@
+"""BASELINE config 5: descriptor-count sweep (1k..32k features/image) on a fixed
+pair list, for roofline characterisation.
+
+For each n: generate_synthetic(106 images, n per image, band 10) (the first
+10 images are short by construction), one block row holding all 106 images,
+the first 1,000 band pairs of band_graph(106, 10) matched in it.  Reports
+device time per kernel class (CUDA events), pairs/s, and the match kernel's
+achieved algorithmic bandwidth (1024*n bytes per pair) against the measured HBM
+peak.  Prints one JSON line per n; `--out` also writes a markdown table.
+
+    python tools/sweep.py --sizes 1024 2048 4096 8192 16384 32768 --out profiles/r1_sweep.md
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2505_22089_b200 as bm  # noqa: E402
+from paper_2505_22089_b200.features import SyntheticScene, generate_synthetic  # noqa: E402
+
+
+def run(n: int, reps: int, hbm: float) -> dict:
+    imgs, _ = generate_synthetic(SyntheticScene(106, n, 10, 0.02, 0.2, 11))
+    pairs = [(i, j) for i in range(106) for j in range(i + 1, min(106, i + 11))][:1000]
+    hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
+    m = bm.Matcher(hf)
+    for fs in imgs:
+        m.upload(fs.image_id, fs.descriptors)
+    m.synchronize()
+    m.row(range(106))
+    m.match(pairs)  # warm-up
+    m.set_profiling(True)
+    for _ in range(reps):
+        m.row(range(106))
+        m.match(pairs)
+    t = {k: m.kernel_time(k)[0] / reps for k in ("mean", "codes", "fixup", "tables", "match",
+                                                 "compact")}
+    m.close()
+    pair_bytes = sum(1024.0 * (len(imgs[a].descriptors) + len(imgs[b].descriptors)) / 2
+                     for a, b in pairs)
+    match_s = t["match"] * 1e-3
+    row_s = sum(t.values()) * 1e-3
+    return {"n": n, "pairs": len(pairs), "kernel_ms": t,
+            "match_pairs_per_s": len(pairs) / match_s,
+            "row_pairs_per_s": len(pairs) / row_s,
+            "match_achieved_gbs": pair_bytes / match_s / 1e9,
+            "match_frac_of_hbm": pair_bytes / match_s / 1e9 / hbm}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", type=int, nargs="+", default=[1024, 2048, 4096, 8192, 16384, 32768])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out")
+    a = ap.parse_args()
+    try:
+        hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        hbm = 6650.0
+    rows = []
+    for n in a.sizes:
+        r = run(n, a.reps, hbm)
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+    if a.out:
+        lines = ["# descriptor-count sweep (BASELINE config 5)", "",
+                 "106-image band-10 scene, one block row, first 1,000 band pairs; device time "
+                 "per kernel class from CUDA events (mean of reps).", "",
+                 "| n | mean ms | codes ms | tables ms | match ms | match pairs/s | row pairs/s | "
+                 "match GB/s (1024n B/pair) | frac of HBM |", "|---|---|---|---|---|---|---|---|---|"]
+        for r in rows:
+            k = r["kernel_ms"]
+            lines.append(f"| {r['n']} | {k['mean']:.3f} | {k['codes'] + k['fixup']:.3f} | "
+                         f"{k['tables']:.3f} | {k['match']:.3f} | {r['match_pairs_per_s']:.0f} | "
+                         f"{r['row_pairs_per_s']:.0f} | {r['match_achieved_gbs']:.0f} | "
+                         f"{r['match_frac_of_hbm']:.3f} |")
+        Path(a.out).write_text("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
