@@ -133,6 +133,13 @@ struct ArenaImage {
   uint64_t n = 0;
   uint32_t flag_slot = 0;  // ready flag in d_flags, written after the H2D
   uint32_t gen = 0;        // upload generation (flags only increase per slot)
+  double* dt = nullptr;    // channel-major FP64 copy for the row-mean chain
+};
+
+struct ReadyView {
+  const uint32_t* flag;
+  uint32_t gen;
+  const double* dt;
 };
 
 constexpr uint32_t kFlagSlots = 1u << 20;
@@ -187,7 +194,7 @@ struct bmg_context {
   bmg::DevBuf d_mean_fast, d_partial, d_redo;
   uint64_t spec_rows = 0;  // rows whose codes were computed speculatively
   cudaMemPool_t pool = nullptr;
-  cudaEvent_t ev_uploaded = nullptr;
+  cudaEvent_t ev_uploaded = nullptr, ev_mean_tail = nullptr;
   bool pending_upload = false;
   char* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -326,6 +333,11 @@ void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
                            c.s_copy));
   stage_h2d(c, im.d, desc, n * 512);
+  BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.dt), std::max<size_t>(n * 1024, 1024), c.pool,
+                           c.s_copy));
+  launch_widen_transpose(im.d, static_cast<uint32_t>(n), im.dt, c.s_copy);
+  ++c.launches;
+  check_launch();
   {
     // publish "image landed" in stream order after its copy; the value lives
     // in the pinned ring until a wrap, which synchronises the device
@@ -348,6 +360,10 @@ void arena_evict(Ctx& c, uint64_t id) {
     fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
   // stream-ordered free after every kernel already queued on the compute stream
   BMG_CUDA(cudaFreeAsync(it->second.d, c.s_comp));
+  // the mean chain reads dt on the mean stream: free it after that stream's work too
+  BMG_CUDA(cudaEventRecord(c.ev_mean_tail, c.s_mean));
+  BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_mean_tail, 0));
+  BMG_CUDA(cudaFreeAsync(it->second.dt, c.s_comp));
   c.free_flag_slots.push_back(it->second.flag_slot);
   c.occupancy -= it->second.n;
   c.resident.erase(it);
@@ -417,7 +433,7 @@ void enqueue_codes_tables(Ctx& c, const float* d_mean, const uint32_t* gate) {
 // bucket-table kernels on the compute stream.
 void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
                        const float* mean_host, const float* mean_dev, bool compute_mean,
-                       const std::vector<std::pair<const uint32_t*, uint32_t>>* ready = nullptr,
+                       const std::vector<ReadyView>* ready = nullptr,
                        bool speculate = false) {
   const HashDev& h = c.hd;
   const int n_imgs = static_cast<int>(descs.size());
@@ -462,8 +478,9 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.cursor = reinterpret_cast<uint32_t*>(base + lay[i].cursor_off);
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
     im.overflow = 0;
-    im.ready = ready ? (*ready)[i].first : nullptr;
-    im.ready_gen = ready ? (*ready)[i].second : 0u;
+    im.ready = ready ? (*ready)[i].flag : nullptr;
+    im.ready_gen = ready ? (*ready)[i].gen : 0u;
+    im.dt = ready ? (*ready)[i].dt : nullptr;
   }
   // metadata
   ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
@@ -560,7 +577,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
 void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host,
                  bool speculate = false) {
   std::vector<std::pair<const float*, uint64_t>> descs;
-  std::vector<std::pair<const uint32_t*, uint32_t>> ready;
+  std::vector<ReadyView> ready;
   descs.reserve(n);
   ready.reserve(n);
   c.row_ids.assign(ids, ids + n);
@@ -572,7 +589,7 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
     descs.emplace_back(it->second.d, it->second.n);
-    ready.emplace_back(c.d_flags.as<uint32_t>() + it->second.flag_slot, it->second.gen);
+    ready.push_back({c.d_flags.as<uint32_t>() + it->second.flag_slot, it->second.gen, it->second.dt});
     c.row_slot[ids[i]] = static_cast<int>(i);
   }
   c.row_valid = false;
@@ -849,6 +866,7 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
       BMG_CUDA(cudaEventRecord(c->ev_mean_free[i], c->s_comp));
     }
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
+    BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_tail, cudaEventDisableTiming));
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
     BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
@@ -871,7 +889,10 @@ int bmg_destroy(bmg_context* c) {
   return guarded([&] {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    for (auto& [id, im] : c->resident) cudaFree(im.d);
+    for (auto& [id, im] : c->resident) {
+      cudaFree(im.d);
+      cudaFree(im.dt);
+    }
     c->resident.clear();
     for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
                       &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
@@ -890,6 +911,7 @@ int bmg_destroy(bmg_context* c) {
     }
     for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
     if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
+    if (c->ev_mean_tail) cudaEventDestroy(c->ev_mean_tail);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
     for (int i = 0; i < bmg_context::kMeanSlots; ++i) {

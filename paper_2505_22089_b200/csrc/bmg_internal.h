@@ -26,6 +26,9 @@ struct ImgDev {
   const uint32_t* ready;
   uint32_t ready_gen;
   uint32_t pad_;
+  // channel-major FP64 copy [128][n] made once per upload (exact widening),
+  // streamed by the row-mean chain; nullptr for non-arena images
+  const double* dt;
 };
 
 struct HashDev {
@@ -70,6 +73,8 @@ struct MatchLaunch {
 };
 
 // ---- launchers (kernels.cu) ----
+// float [n][128] -> double [128][n] (exact), for the row-mean chain
+void launch_widen_transpose(const float* desc, uint32_t n, double* dt, cudaStream_t s);
 void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
                      cudaStream_t s);
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,

@@ -107,17 +107,9 @@ __global__ void gated_clear_kernel(uint32_t* __restrict__ p, size_t words, const
 // K1: row centering mean (engine.cpp:446-461).  acc[c] += (double)d.v[c] over
 // images in ascending id order, descriptors in index order, then
 // mean = float(acc / total): a dependent FP64 chain per channel, reproduced
-// literally.  A producer warp streams 32-row chunks of every image, in the
-// reference's order, into a 16-stage shared-memory ring with cp.async.bulk +
-// mbarrier complete_tx (128 KB in flight hides HBM latency); consumer warps
-// (thread = channel) run the DADD chain out of shared memory.  Rows past an
-// image's end are read as +0.0, an exact no-op for an accumulator that starts
-// at +0.0 (it can never become -0.0 under round-to-nearest).
+// literally (runs on its own stream; the row's codes are computed from the
+// speculative parallel mean above and verified against this one).
 // ---------------------------------------------------------------------------
-constexpr int kMeanRows = 32;
-constexpr int kMeanStages = 12;  // 12 x 16 KB stages
-constexpr int kMeanCh = 64;                 // channels per CTA (grid = 128 / kMeanCh)
-constexpr int kMeanThreads = kMeanCh + 32;  // consumers + one producer warp
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -147,99 +139,115 @@ __device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint
       : "memory");
 }
 
-// Grid: 2 CTAs x 64 channels, so each SM converts (F2F on the XU pipe) and
-// chains half of the channels; the producer issues one 256-byte bulk copy
-// per row (the CTA's half of the 512-byte descriptor).  Consumers convert
-// chunk g+1 interleaved with the DADD chain of chunk g, so the conversions
-// fill the 8-cycle shadow of each dependent DADD.
-__global__ void __launch_bounds__(kMeanThreads, 1) row_mean_tma_kernel(const ImgDev* __restrict__ imgs,
-                                                                       int n_imgs, float* __restrict__ mean_out,
-                                                                       double* __restrict__ acc_out) {
-  extern __shared__ __align__(128) float ring[];  // [stages][rows][128]
-  __shared__ __align__(8) unsigned long long full_bar[kMeanStages], empty_bar[kMeanStages];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int kConsumerWarps = kMeanCh / 32;
-  if (tid == 0) {
-    for (int s = 0; s < kMeanStages; ++s) {
-      mbar_init(smem_addr(&full_bar[s]), 1);
-      mbar_init(smem_addr(&empty_bar[s]), kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+// Exact widening + transpose at upload: dt[c][i] = (double)desc[i][c], so a
+// channel's terms are contiguous for the chain and no F2F (XU pipe, as slow
+// per warp as the DADD latency) sits in the chain's issue stream.
+__global__ void __launch_bounds__(256) widen_transpose_kernel(const float* __restrict__ desc, uint32_t n,
+                                                              double* __restrict__ dt) {
+  __shared__ float tile[32][kDim + 1];
+  const uint32_t r0 = blockIdx.x * 32;
+  const int rows = min(32u, n - r0);
+  for (int e = threadIdx.x; e < 32 * kDim; e += blockDim.x) {
+    const int r = e / kDim, c = e % kDim;
+    tile[r][c] = r < rows ? __ldg(desc + (size_t)(r0 + r) * kDim + c) : 0.0f;
   }
   __syncthreads();
-  const uint32_t ring_base = smem_addr(ring);
-  constexpr uint32_t kStageBytes = kMeanRows * kDim * 4;
-  const int c0 = blockIdx.x * kMeanCh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < kDim; c += blockDim.x / 32)
+    if (lane < rows) dt[(size_t)c * n + r0 + lane] = (double)tile[lane][c];
+}
 
-  if (warp == kConsumerWarps) {  // ---- producer
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (int im = 0; im < n_imgs; ++im) {
-        const float* src = imgs[im].desc;
-        const uint32_t n = imgs[im].n;
-        if (const uint32_t* flag = imgs[im].ready) {
-          // stream the image as soon as its H2D has landed (bounded wait)
-          const uint32_t gen = imgs[im].ready_gen;
-          unsigned long long t0, now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          for (;;) {
-            uint32_t v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-            if ((int32_t)(v - gen) >= 0) break;  // generations only grow per slot
-            __nanosleep(256);
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            if (now - t0 > 20000000000ull) __trap();  // 20 s: an upload never completed
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
-          const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
-          mbar_wait(smem_addr(&empty_bar[s]), ph ^ 1u);
-          // whole rows in one bulk copy (per-row copies are TMA-issue bound);
-          // each CTA then reads only its half of every row from the stage
-          const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
-          const uint32_t bar = smem_addr(&full_bar[s]);
-          mbar_expect_tx(bar, rows * kDim * 4u);
-          tma_bulk_g2s(ring_base + s * kStageBytes, src + (size_t)r0 * kDim, rows * kDim * 4u, bar);
-        }
-      }
-    }
-    return;
+// The chain: one warp per CTA, 4 CTAs x 32 channels.  Each thread streams its
+// channel's contiguous doubles image by image through a 4-stage cp.async
+// ring in shared memory (32 doubles per stage per thread, ~40 KB in flight per
+// warp on top of the L2 prefetch stream), so the DADD chain issues back to
+// back at the FP64 add latency.
+constexpr int kMeanBatch = 32;   // doubles per stage per thread
+constexpr int kMeanStages = 6;   // 48 KB of static shared memory
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void wait_upload(const uint32_t* flag, uint32_t gen) {
+  // stream the image as soon as its H2D + widening have landed (bounded wait)
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - gen) >= 0) break;  // generations only grow per slot
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > 20000000000ull) __trap();  // 20 s: an upload never completed
   }
+}
 
-  // ---- consumers: thread c owns channel c0 + c
-  const int c = tid;
+__global__ void __launch_bounds__(32, 1) row_mean_kernel(const ImgDev* __restrict__ imgs, int n_imgs,
+                                                         float* __restrict__ mean_out,
+                                                         double* __restrict__ acc_out) {
+  // [stage][pair k2 = 0..kMeanBatch/2)[lane] x 2 doubles: a warp's LDS.128 is contiguous
+  __shared__ __align__(16) double ring[kMeanStages][kMeanBatch / 2][32][2];
+  const int lane = threadIdx.x;
+  const int c = blockIdx.x * 32 + lane;
   double acc = 0.0;
   unsigned long long total = 0;
-  double da[kMeanRows];
-#pragma unroll
-  for (int r = 0; r < kMeanRows; ++r) da[r] = 0.0;  // +0.0: exact no-ops on the chain
-  uint32_t g = 0;
   for (int im = 0; im < n_imgs; ++im) {
     const uint32_t n = imgs[im].n;
     total += n;
-    for (uint32_t r0 = 0; r0 < n; r0 += kMeanRows, ++g) {
-      const uint32_t s = g % kMeanStages, ph = (g / kMeanStages) & 1u;
-      const uint32_t rows = min((uint32_t)kMeanRows, n - r0);
-      mbar_wait(smem_addr(&full_bar[s]), ph);
-      float w[kMeanRows];
-      const float* st = ring + (size_t)s * kMeanRows * kDim + c0 + c;
-#pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) w[r] = (uint32_t)r < rows ? st[r * kDim] : 0.0f;
+    if (n == 0) continue;
+    if (imgs[im].ready) {
+      if (lane == 0) wait_upload(imgs[im].ready, imgs[im].ready_gen);
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_addr(&empty_bar[s]));
-#pragma unroll
-      for (int r = 0; r < kMeanRows; ++r) {
-        const double x = (double)w[r];   // next chunk's row r (XU)
-        acc = __dadd_rn(acc, da[r]);     // this chunk's row r (dependent DADD)
-        da[r] = x;
-      }
     }
-  }
+    const double* col = imgs[im].dt + (size_t)c * n;
+    // a channel column starts 16-byte aligned iff c*n is even: peel one term
+    uint32_t i = 0;
+    if ((c * (size_t)n) & 1u) {
+      acc = __dadd_rn(acc, __ldcg(col));
+      i = 1;
+    }
+    const uint32_t nb = (n - i) / kMeanBatch;
+    auto issue = [&](uint32_t b) {
+      const int st = b % kMeanStages;
+      const double* src = col + i + (size_t)b * kMeanBatch;
 #pragma unroll
-  for (int r = 0; r < kMeanRows; ++r) acc = __dadd_rn(acc, da[r]);
-  mean_out[c0 + c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
-  if (acc_out) acc_out[c0 + c] = acc;
+      for (int k2 = 0; k2 < kMeanBatch / 2; ++k2)
+        cp_async16(smem_addr(&ring[st][k2][lane][0]), src + 2 * k2);
+    };
+#pragma unroll
+    for (int p = 0; p < kMeanStages - 1; ++p) {
+      if ((uint32_t)p < nb) issue(p);
+      cp_async_commit();
+    }
+    for (uint32_t b = 0; b < nb; ++b) {
+      if (b + kMeanStages - 1 < nb) {
+        issue(b + kMeanStages - 1);
+        const double* pf = col + i + (size_t)(b + 16) * kMeanBatch;
+        if (pf < col + n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      }
+      cp_async_commit();
+      cp_async_wait<kMeanStages - 1>();  // batch b has landed
+      __syncwarp();
+      const int st = b % kMeanStages;
+#pragma unroll
+      for (int k2 = 0; k2 < kMeanBatch / 2; ++k2) {
+        const double2 v = *reinterpret_cast<const double2*>(&ring[st][k2][lane][0]);
+        acc = __dadd_rn(acc, v.x);
+        acc = __dadd_rn(acc, v.y);
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    for (i += nb * kMeanBatch; i < n; ++i) acc = __dadd_rn(acc, __ldcg(col + i));
+  }
+  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+  if (acc_out) acc_out[c] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -726,20 +734,27 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         k1 = max(k0, min(k1, key));
         k0 = min(k0, key);
       });
+      // pull the K smallest; each lane pops the pulled key (and one more copy
+      // of it -- a train index reached from two tables that landed in the
+      // same lane); a third copy is left for the exact path to resolve
       int popped = 0;
+      bool dup3 = false;
       for (int r = 0; r < K; ++r) {
         const uint32_t m = __reduce_min_sync(kFull, k0);
         if (m == kEmpty) break;
-        if (lane == r) lst = m;
-        while (k0 == m) {
-          k0 = k1;
-          k1 = k2;
-          k2 = k3;
-          k3 = kEmpty;
-          ++popped;
+        lst = lane == r ? m : lst;
+#pragma unroll
+        for (int rep = 0; rep < 2; ++rep) {
+          const bool pop = k0 == m;
+          k0 = pop ? k1 : k0;
+          k1 = pop ? k2 : k1;
+          k2 = pop ? k3 : k2;
+          k3 = pop ? kEmpty : k3;
+          popped += pop ? 1 : 0;
         }
+        dup3 |= k0 == m;
       }
-      exact = __any_sync(kFull, dropped && popped >= 4);
+      exact = __any_sync(kFull, (dropped && popped >= 4) || dup3);
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
@@ -947,13 +962,11 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // ---------------------------------------------------------------------------
 void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
                      cudaStream_t s) {
-  constexpr int smem = kMeanStages * kMeanRows * kDim * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(row_mean_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  row_mean_tma_kernel<<<kDim / kMeanCh, kMeanThreads, smem, s>>>(imgs, n_imgs, mean_out, acc_out);
+  row_mean_kernel<<<kDim / 32, 32, 0, s>>>(imgs, n_imgs, mean_out, acc_out);
+}
+
+void launch_widen_transpose(const float* desc, uint32_t n, double* dt, cudaStream_t s) {
+  if (n) widen_transpose_kernel<<<(n + 31) / 32, 256, 0, s>>>(desc, n, dt);
 }
 
 static size_t codes_smem_bytes() {

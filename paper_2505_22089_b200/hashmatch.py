@@ -215,7 +215,9 @@ class Matcher:
         pairs = list(pairs)
         q = np.ascontiguousarray([a for a, _ in pairs], np.uint64)
         t = np.ascontiguousarray([b for _, b in pairs], np.uint64)
-        cap = max_matches if max_matches is not None else max(1, 1 << 22)
+        counts = getattr(self, "_keep", {})
+        cap = max_matches if max_matches is not None else max(
+            1, sum(len(counts[a]) if a in counts else 1 << 20 for a, _ in pairs))
         offs = np.zeros(len(pairs) + 1, np.uint64)
         out = np.zeros(2 * cap, np.int32)
         mpc = mp.c()
