@@ -98,6 +98,36 @@ struct DevBuf {
   }
 };
 
+// Pinned, device-mapped host buffer: kernels write results straight into host
+// memory over PCIe as rows finish, so reading them back needs no D2H copy.
+struct HostMapped {
+  void* h = nullptr;
+  void* d = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (h) {
+      BMG_CUDA(cudaDeviceSynchronize());
+      cudaFreeHost(h);
+      h = d = nullptr;
+      cap = 0;
+    }
+    n = align_up(std::max<size_t>(n, 4096), 1 << 20);
+    BMG_CUDA(cudaHostAlloc(&h, n, cudaHostAllocMapped | cudaHostAllocPortable));
+    BMG_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    cap = n;
+  }
+  template <typename T>
+  T* host() const { return static_cast<T*>(h); }
+  template <typename T>
+  T* dev() const { return static_cast<T*>(d); }
+  void release() {
+    if (h) cudaFreeHost(h);
+    h = d = nullptr;
+    cap = 0;
+  }
+};
+
 // Pinned host ring for small metadata uploads (tables of pointers, work
 // lists): a slice stays valid until the ring wraps, and a wrap synchronises
 // the streams that could still be reading it.
@@ -208,7 +238,10 @@ struct bmg_context {
   bool row_valid = false;
   bmg::DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag;
   // match state
-  bmg::DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq, d_res_off, d_res, d_running;
+  bmg::DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq, d_running;
+  // result log and per-pair [begin, end) ranges, written by the compaction
+  // kernels directly into mapped pinned host memory
+  bmg::HostMapped res_ranges, res_log;
   // temporaries for the stateless entry points
   bmg::DevBuf d_tmp_desc, d_tmp_codes;
   // instrumentation
@@ -791,8 +824,8 @@ void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fi
 }
 
 void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
-  c.d_res_off.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
-  c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
+  c.res_ranges.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
+  c.res_log.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
   c.d_running.ensure(sizeof(unsigned long long));
   BMG_CUDA(cudaMemsetAsync(c.d_running.p, 0, sizeof(unsigned long long), c.s_comp));
 }
@@ -897,9 +930,10 @@ int bmg_destroy(bmg_context* c) {
     for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
                       &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
                       &c->d_work, &c->d_dense, &c->d_dense_off, &c->d_pair_count, &c->d_nq,
-                      &c->d_res_off, &c->d_res, &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes,
-                      &c->d_flags})
+                      &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_flags})
       b->release();
+    c->res_ranges.release();
+    c->res_log.release();
     for (int i = 0; i < 2; ++i) {
       if (c->stage[i]) cudaFreeHost(c->stage[i]);
       if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
@@ -1015,15 +1049,13 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
       max_matches += c->row_imgs[qi->second].n;
     }
     reset_results(*c, n_pairs, max_matches);
-    enqueue_match(*c, sp, *mp, c->d_res_off.as<uint64_t>(), c->d_res.as<int32_t>());
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->res_log.dev<int32_t>());
     if (n_pairs == 0) {
       offsets_out[0] = 0;
       return;
     }
-    std::vector<uint64_t> ranges(2 * n_pairs);
-    BMG_CUDA(cudaMemcpyAsync(ranges.data(), c->d_res_off.p, sizeof(uint64_t) * 2 * n_pairs,
-                             cudaMemcpyDeviceToHost, c->s_comp));
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    const uint64_t* ranges = c->res_ranges.host<uint64_t>();
     // one pass, so the pairs' ranges are contiguous from 0
     offsets_out[0] = 0;
     for (uint64_t p = 0; p < n_pairs; ++p) offsets_out[p + 1] = ranges[2 * p + 1];
@@ -1031,7 +1063,7 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
     if (total > capacity) fail(BMG_INVALID_ARGUMENT, "match output capacity too small");
     if (total) {
       if (!matches_out) fail(BMG_INVALID_ARGUMENT, "null match output");
-      BMG_CUDA(cudaMemcpy(matches_out, c->d_res.p, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost));
+      std::memcpy(matches_out, c->res_log.host<int32_t>(), sizeof(int32_t) * 2 * total);
     }
   });
 }
@@ -1159,14 +1191,12 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
     }
     std::vector<std::pair<int, int>> sp{{0, 1}};
     reset_results(*c, 1, nq);
-    enqueue_match(*c, sp, *mp, c->d_res_off.as<uint64_t>(), c->d_res.as<int32_t>());
-    uint64_t offs[2];
-    BMG_CUDA(cudaMemcpyAsync(offs, c->d_res_off.p, sizeof(offs), cudaMemcpyDeviceToHost, c->s_comp));
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->res_log.dev<int32_t>());
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    const uint64_t* offs = c->res_ranges.host<uint64_t>();
     const uint64_t total = offs[1] - offs[0];
     if (total)
-      BMG_CUDA(cudaMemcpy(matches_out, c->d_res.as<int32_t>() + 2 * offs[0], sizeof(int32_t) * 2 * total,
-                          cudaMemcpyDeviceToHost));
+      std::memcpy(matches_out, c->res_log.host<int32_t>() + 2 * offs[0], sizeof(int32_t) * 2 * total);
     *n_out = total;
   });
 }
@@ -1202,7 +1232,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     // a row re-done after a mean speculation miss appends its lists again
     const bool may_redo = (opts->flags & BMG_EXEC_NO_SPECULATION) == 0;
     reset_results(*c, n_pairs, may_redo ? 2 * cap : cap);
-    uint64_t* d_off = c->d_res_off.as<uint64_t>();
+    uint64_t* d_off = c->res_ranges.dev<uint64_t>();
+    int32_t* d_log = c->res_log.dev<int32_t>();
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->s_comp));
     BMG_CUDA(cudaStreamWaitEvent(c->s_mean, span0, 0));
@@ -1239,8 +1270,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
           sp.emplace_back(qa->second, tb->second);
         }
-        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, c->d_res.as<int32_t>());
-        enqueue_row_verify(*c, sp, opts->match, d_off + 2 * pb, c->d_res.as<int32_t>(),
+        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log);
+        enqueue_row_verify(*c, sp, opts->match, d_off + 2 * pb, d_log,
                            (opts->flags & BMG_EXEC_FORCE_REDO) != 0);
         it_pairs += pe - pb;
         for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
@@ -1253,22 +1284,15 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->iterations.push_back(c->units_uploaded - units0);
     }
     BMG_CUDA(cudaEventRecord(span1, c->s_comp));
-    // read the device result log back once: per-pair [begin, end) ranges,
-    // then the log up to its running total (a row re-done after a mean
+    // the compaction kernels wrote the per-pair [begin, end) ranges and the
+    // match log straight into mapped host memory (a row re-done after a mean
     // speculation miss left its first lists unreferenced in the log)
-    std::vector<uint64_t> ranges(2 * n_pairs, 0);
-    unsigned long long log_total = 0;
-    if (n_pairs) {
-      BMG_CUDA(cudaMemcpyAsync(ranges.data(), d_off, sizeof(uint64_t) * 2 * n_pairs,
-                               cudaMemcpyDeviceToHost, c->s_comp));
-      BMG_CUDA(cudaMemcpyAsync(&log_total, c->d_running.p, sizeof(log_total), cudaMemcpyDeviceToHost,
-                               c->s_comp));
-      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
-    }
-    std::vector<int32_t> flat(2 * log_total);
-    if (log_total)
-      BMG_CUDA(cudaMemcpy(flat.data(), c->d_res.p, sizeof(int32_t) * 2 * log_total, cudaMemcpyDeviceToHost));
-    uint64_t total = 0;
+    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    const uint64_t* ranges = c->res_ranges.host<uint64_t>();
+    const int32_t* flat = c->res_log.host<int32_t>();
+    uint64_t total = 0, kept_total = 0;
+    for (uint64_t p = 0; p < n_pairs; ++p) kept_total += ranges[2 * p + 1] - ranges[2 * p];
+    res->matches.reserve(2 * kept_total);
     // results keyed and sorted by IdPair (engine.cpp:419, 506-512); a pair
     // planned twice keeps its last match list, like the reference's map
     std::map<std::pair<uint64_t, uint64_t>, uint64_t> last;
@@ -1278,11 +1302,10 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->pair_ids.push_back(key.first);
       res->pair_ids.push_back(key.second);
       const uint64_t b = ranges[2 * p], e = ranges[2 * p + 1];
-      res->matches.insert(res->matches.end(), flat.begin() + 2 * b, flat.begin() + 2 * e);
+      res->matches.insert(res->matches.end(), flat + 2 * b, flat + 2 * e);
       total += e - b;
       res->offsets.push_back(res->matches.size() / 2);
-      if (opts->on_pair)
-        opts->on_pair(opts->on_pair_user, key.first, key.second, flat.data() + 2 * b, e - b);
+      if (opts->on_pair) opts->on_pair(opts->on_pair_user, key.first, key.second, flat + 2 * b, e - b);
     }
     res->counters[0] = n_pairs;
     res->counters[1] = total;
