@@ -655,7 +655,9 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   }
 
   const int L = a.tables, K = a.k, ib = a.idx_bits;
-  const uint32_t scodes = smem_addr(smem_raw);
+  // pinned in a register (otherwise rematerialised from SR_CgaCtaId per use)
+  uint32_t scodes;
+  asm volatile("mov.u32 %0, %1;" : "=r"(scodes) : "r"(smem_addr(smem_raw)));
   const uint32_t idx_mask = (1u << ib) - 1u;
   const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
             } while (e >= t_end);
             sbase = tab[kBaseOff + t];
           }
-          const uint32_t j = __ldg(T.slots + sbase + e);
+          const uint32_t j = __ldg(T.slots + (sbase + e));
           key = (hamming<FWP, SMEM>(scodes, T.fine, j, qc) << ib) | j;
         }
         round(valid, key);
@@ -720,41 +722,43 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     if constexpr (KM == 8) {
       // ---- fast path: each lane keeps the 4 smallest keys it sees
       // (branchless sorted insert), then the warp pulls the K smallest out of
-      // the lanes' lists with the single-instruction warp min (REDUX), popping
-      // every copy of the pulled key (a train index reached from several
-      // tables has the same key).  Exact unless some lane gave up all 4 list
-      // entries while having dropped a 5th key -- then the query reruns on the
-      // exact path below.
+      // the lanes' lists with the single-instruction warp min (REDUX).
       uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty;
-      bool dropped = false;
-      for_each_round([&](bool valid, uint32_t key) {
-        dropped |= valid && (k3 != kEmpty) && (key < k3 || k3 < key);
+      for_each_round([&](bool, uint32_t key) {
         k3 = max(k2, min(k3, key));
         k2 = max(k1, min(k2, key));
         k1 = max(k0, min(k1, key));
         k0 = min(k0, key);
       });
-      // pull the K smallest; each lane pops the pulled key (and one more copy
-      // of it -- a train index reached from two tables that landed in the
-      // same lane); a third copy is left for the exact path to resolve
-      int popped = 0;
-      bool dup3 = false;
-      for (int r = 0; r < K; ++r) {
-        const uint32_t m = __reduce_min_sync(kFull, k0);
-        if (m == kEmpty) break;
-        lst = lane == r ? m : lst;
+      // Lane l saw ceil((total - l) / 32) keys: more than 4 means its list
+      // dropped some (all >= its 4th entry).  Copies of one key (a train
+      // index reached from several tables) that landed in one lane sit next
+      // to each other: squeeze them out so a lane's list is a prefix of its
+      // distinct keys.  Copies in different lanes are popped together below.
+      const bool dropped = total > 128u + (uint32_t)lane;
+      if ((k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty)) {
 #pragma unroll
-        for (int rep = 0; rep < 2; ++rep) {
+        for (int rep = 0; rep < 3; ++rep) {
+          if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
+          if (k1 == k2) { k2 = k3; k3 = kEmpty; }
+          if (k2 == k3) k3 = kEmpty;
+        }
+      }
+      // Pull r is the smallest key not pulled yet unless a lane that dropped
+      // keys has run dry: then the query reruns on the exact path below.
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (r < K) {
+          const uint32_t m = __reduce_min_sync(kFull, k0);
+          lst = lane == r ? m : lst;
           const bool pop = k0 == m;
           k0 = pop ? k1 : k0;
           k1 = pop ? k2 : k1;
           k2 = pop ? k3 : k2;
           k3 = pop ? kEmpty : k3;
-          popped += pop ? 1 : 0;
         }
-        dup3 |= k0 == m;
       }
-      exact = __any_sync(kFull, (dropped && popped >= 4) || dup3);
+      exact = __any_sync(kFull, dropped && k0 == kEmpty);
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
@@ -787,6 +791,52 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     if (kept == 1) {
       result = (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask);
     } else if (kept > 1) {
+      const bool mine = lane < kept;
+      const uint32_t my_idx = lst & idx_mask;
+      float s_min, s_2;
+      uint32_t i_min;
+      if constexpr (KM == 8) {
+        // lanes 4c..4c+3 hold candidate c: lane part p sums the float4s
+        // p, p+4, .., p+28 (each load instruction reads 64 contiguous bytes
+        // of every candidate row) in two FMA chains, then two xor-shuffles
+        // complete the sum -- every FP32 sum has depth <= 19, relative
+        // error < 19 * 2^-24 + 3 * 2^-24 (the squared differences) ~ 1.4e-6,
+        // inside the 1e-5 certification margin below.
+        const int ck = lane >> 2, part = lane & 3;
+        const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
+        float s = 0.f;
+        if (ck < kept) {
+          const float4* qp = Qd + (size_t)q * 32 + part;
+          const float4* tp = Td + (size_t)jk * 32 + part;
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const float4 a0 = __ldg(qp + 4 * i), b0 = __ldg(tp + 4 * i);
+            const float4 a1 = __ldg(qp + 4 * i + 4), b1 = __ldg(tp + 4 * i + 4);
+            float d;
+            d = a0.x - b0.x; s0 = fmaf(d, d, s0);
+            d = a0.y - b0.y; s0 = fmaf(d, d, s0);
+            d = a0.z - b0.z; s0 = fmaf(d, d, s0);
+            d = a0.w - b0.w; s0 = fmaf(d, d, s0);
+            d = a1.x - b1.x; s1 = fmaf(d, d, s1);
+            d = a1.y - b1.y; s1 = fmaf(d, d, s1);
+            d = a1.z - b1.z; s1 = fmaf(d, d, s1);
+            d = a1.w - b1.w; s1 = fmaf(d, d, s1);
+          }
+          s = s0 + s1;
+        }
+        s += __shfl_xor_sync(kFull, s, 1);
+        s += __shfl_xor_sync(kFull, s, 2);
+        // squared distances are >= 0 (or NaN, caught by `finite`): their
+        // bit patterns order like the values, so REDUX finds the (s, idx)
+        // argmin and the runner-up
+        const bool lead = part == 0 && ck < kept;
+        const uint32_t sb = lead ? __float_as_uint(s) : kEmpty;
+        const uint32_t mb = __reduce_min_sync(kFull, sb);
+        i_min = __reduce_min_sync(kFull, (lead && sb == mb) ? jk : kEmpty);
+        s_min = __uint_as_float(mb);
+        s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
+      } else {
       const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
       float part[KM];
 #pragma unroll
@@ -823,8 +873,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       for (int b = 0; b < kLog; ++b)
         if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
       const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
-      const bool mine = lane < kept;
-      const uint32_t my_idx = lst & idx_mask;
       // argmin of (s, idx) and runner-up value over lanes < kept
       float bs = mine ? s_own : __int_as_float(0x7f800000);
       uint32_t bi = mine ? my_idx : 0xffffffffu;
@@ -837,12 +885,13 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           bi = oi;
         }
       }
-      const float s_min = __shfl_sync(kFull, bs, 0);
-      const uint32_t i_min = __shfl_sync(kFull, bi, 0);
+      s_min = __shfl_sync(kFull, bs, 0);
+      i_min = __shfl_sync(kFull, bi, 0);
       float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
 #pragma unroll
       for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
-      const float s_2 = __shfl_sync(kFull, s2, 0);
+      s_2 = __shfl_sync(kFull, s2, 0);
+      }
       const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
       const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
       const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
