@@ -151,14 +151,11 @@ typedef struct {
 /* Keep every image resident: eviction directives are skipped (no free, no
  * bookkeeping).  Used to measure the row body on HBM-resident inputs. */
 #define BMG_EXEC_RETAIN 1u
-/* Row-mean speculation (default: rows with >= 32768 descriptors compute their
- * codes from a parallel mean while the exact sequential mean runs alongside;
- * a bit-pattern check gates a re-do with the exact mean).  Results are
- * identical either way; these flags only steer where the time goes.
- * FORCE_REDO is a test hook that always takes the re-do path. */
-#define BMG_EXEC_NO_SPECULATION 2u
-#define BMG_EXEC_FORCE_SPECULATION 4u
-#define BMG_EXEC_FORCE_REDO 8u
+/* Row means (engine.cpp:446-461) are reconstructed exactly in parallel from
+ * 128-bit fixed-point prefix sums plus the chain's rare rounding steps; this
+ * flag computes them with the literal sequential FP64 chain instead (the
+ * fallback path, exposed as a test hook -- results are identical). */
+#define BMG_EXEC_MEAN_CHAIN 2u
 
 /* ---- status ------------------------------------------------------------ */
 const char* bmg_status_name(int status);              /* "InvalidArgument", ... */
@@ -253,6 +250,11 @@ int bmg_kernel_time(bmg_context* ctx, const char* kernel_class, double* total_ms
 /* Number of projection bits / ratio decisions resolved by the FP64 fixup
  * path in the last row / match (diagnostics). */
 int bmg_fixup_counts(bmg_context* ctx, uint64_t* code_bits, uint64_t* rerank_queries);
+/* How the last computed row mean was obtained (diagnostics): `rounds` =
+ * walk/resolve rounds the parallel reconstruction ran (rounding steps + 1),
+ * `used_chain` = 1 when the sequential FP64 chain produced it (fallback or
+ * BMG_EXEC_MEAN_CHAIN). */
+int bmg_row_mean_info(bmg_context* ctx, uint32_t* rounds, int* used_chain);
 
 #ifdef __cplusplus
 }

@@ -161,21 +161,7 @@ struct PinnedRing {
 struct ArenaImage {
   float* d = nullptr;
   uint64_t n = 0;
-  uint32_t flag_slot = 0;  // ready flag in d_flags, written after the H2D
-  uint32_t gen = 0;        // upload generation (flags only increase per slot)
-  double* dt = nullptr;    // channel-major FP64 copy for the row-mean chain
 };
-
-struct ReadyView {
-  const uint32_t* flag;
-  uint32_t gen;
-  const double* dt;
-};
-
-constexpr uint32_t kFlagSlots = 1u << 20;
-// Rows at least this large compute codes from the speculative parallel mean
-// (below it the exact chain takes < ~0.1 ms and is simply waited for).
-constexpr uint64_t kSpeculateMinDescriptors = 32768;
 
 struct Timer {
   std::string cls;
@@ -193,7 +179,6 @@ struct RowState {
   uint32_t fix_cap = 0;
   uint64_t total_desc = 0;
   size_t codes_bytes = 0, offsets_begin = 0, offsets_bytes = 0;
-  int spec_slot = -1;  // mean slot awaiting verification (speculative row), or -1
 };
 
 }  // namespace
@@ -209,22 +194,15 @@ struct bmg_context {
   // arena (DeviceArena, engine.hpp:20-44)
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
-  bmg::DevBuf d_flags;  // u32[kFlagSlots] upload-completion generations
-  std::vector<uint32_t> free_flag_slots;
-  uint32_t next_flag_slot = 0, gen_counter = 0;
-  cudaStream_t s_copy = nullptr, s_comp = nullptr, s_mean = nullptr;
-  // row means run on their own stream so row r+1's sequential chain overlaps
-  // row r's codes and matching; slots are recycled through events
-  static constexpr int kMeanSlots = 4;
-  bmg::DevBuf d_mean_slot[kMeanSlots], d_mean_imgs[kMeanSlots];
-  cudaEvent_t ev_mean_done[kMeanSlots] = {}, ev_mean_free[kMeanSlots] = {};
-  uint64_t mean_seq = 0;
+  cudaStream_t s_copy = nullptr, s_comp = nullptr;
   float* cur_mean = nullptr;
   bmg::RowState rs;
-  bmg::DevBuf d_mean_fast, d_partial, d_redo;
-  uint64_t spec_rows = 0;  // rows whose codes were computed speculatively
+  // exact parallel row mean: F96 tile sums + state (kernels.cu K1)
+  bmg::DevBuf d_mean_sums, d_mean_state;
+  bool mean_chain_only = false;  // test hook: the literal sequential chain
+  bool last_mean_chain_only = false;
   cudaMemPool_t pool = nullptr;
-  cudaEvent_t ev_uploaded = nullptr, ev_mean_tail = nullptr;
+  cudaEvent_t ev_uploaded = nullptr;
   bool pending_upload = false;
   char* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -241,7 +219,11 @@ struct bmg_context {
   bmg::DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq, d_running;
   // result log and per-pair [begin, end) ranges, written by the compaction
   // kernels directly into mapped pinned host memory
+  // (the per-pair ranges are tiny: mapped host memory written by the scan
+  // kernel; the log itself is compacted in HBM and read back with one DMA
+  // into pinned memory -- kernel stores across PCIe are ~10x slower)
   bmg::HostMapped res_ranges, res_log;
+  bmg::DevBuf d_res;
   // temporaries for the stateless entry points
   bmg::DevBuf d_tmp_desc, d_tmp_codes;
   // instrumentation
@@ -355,30 +337,9 @@ void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
   ArenaImage im;
   im.n = n;
-  if (!c.free_flag_slots.empty()) {
-    im.flag_slot = c.free_flag_slots.back();
-    c.free_flag_slots.pop_back();
-  } else {
-    if (c.next_flag_slot >= kFlagSlots) fail(BMG_OUT_OF_MEMORY, "too many resident images");
-    im.flag_slot = c.next_flag_slot++;
-  }
-  im.gen = ++c.gen_counter;
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
                            c.s_copy));
   stage_h2d(c, im.d, desc, n * 512);
-  BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.dt), std::max<size_t>(n * 1024, 1024), c.pool,
-                           c.s_copy));
-  launch_widen_transpose(im.d, static_cast<uint32_t>(n), im.dt, c.s_copy);
-  ++c.launches;
-  check_launch();
-  {
-    // publish "image landed" in stream order after its copy; the value lives
-    // in the pinned ring until a wrap, which synchronises the device
-    uint32_t* hv = c.ring.alloc<uint32_t>(1, c.s_comp, c.s_copy);
-    *hv = im.gen;
-    BMG_CUDA(cudaMemcpyAsync(c.d_flags.as<uint32_t>() + im.flag_slot, hv, sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, c.s_copy));
-  }
   c.resident.emplace(id, im);
   c.occupancy += n;
   c.peak = std::max(c.peak, c.occupancy);
@@ -393,11 +354,6 @@ void arena_evict(Ctx& c, uint64_t id) {
     fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
   // stream-ordered free after every kernel already queued on the compute stream
   BMG_CUDA(cudaFreeAsync(it->second.d, c.s_comp));
-  // the mean chain reads dt on the mean stream: free it after that stream's work too
-  BMG_CUDA(cudaEventRecord(c.ev_mean_tail, c.s_mean));
-  BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_mean_tail, 0));
-  BMG_CUDA(cudaFreeAsync(it->second.dt, c.s_comp));
-  c.free_flag_slots.push_back(it->second.flag_slot);
   c.occupancy -= it->second.n;
   c.resident.erase(it);
   ++c.evictions;
@@ -408,33 +364,23 @@ void join_uploads(Ctx& c) {
   if (!c.pending_upload) return;
   BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
   BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_uploaded, 0));
-  // (the mean stream does not wait: its producer polls each image's flag)
   c.pending_upload = false;
 }
 
 // ---- row body -------------------------------------------------------------
 
 // Codes (+ FP64 fixups) and bucket tables for the current row views, centred
-// on `d_mean`.  With a gate, every kernel (and the clears) is a no-op unless
-// *gate != 0: the re-do pass after a mean speculation miss.
-void enqueue_codes_tables(Ctx& c, const float* d_mean, const uint32_t* gate) {
+// on `d_mean`.
+void enqueue_codes_tables(Ctx& c, const float* d_mean) {
   const RowState& rs = c.rs;
   if (rs.n_tiles == 0) return;
   cudaStream_t s = c.s_comp;
-  HashDev h = c.hd;
-  h.gate = gate;
+  const HashDev& h = c.hd;
   char* base = c.d_scratch.as<char>();
   const int plane_chunks = (h.n_planes + kPlaneChunk - 1) / kPlaneChunk;
-  if (gate) {
-    launch_gated_clear(base + rs.offsets_begin, rs.offsets_bytes, gate, s);
-    if (plane_chunks > 1) launch_gated_clear(base, rs.codes_bytes, gate, s);
-    launch_gated_clear(c.d_fixcnt.p, sizeof(uint32_t) * (1 + rs.n_imgs), gate, s);
-    c.launches += plane_chunks > 1 ? 3 : 2;
-  } else {
-    BMG_CUDA(cudaMemsetAsync(base + rs.offsets_begin, 0, rs.offsets_bytes, s));
-    if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, rs.codes_bytes, s));
-    BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + rs.n_imgs), s));
-  }
+  BMG_CUDA(cudaMemsetAsync(base + rs.offsets_begin, 0, rs.offsets_bytes, s));
+  if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, rs.codes_bytes, s));
+  BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + rs.n_imgs), s));
   const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
   const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
   const uint32_t* d_tile_start = d_tile_img + rs.n_tiles;
@@ -465,9 +411,7 @@ void enqueue_codes_tables(Ctx& c, const float* d_mean, const uint32_t* gate) {
 // scratch, computes the mean (unless given) and launches codes, fixup and
 // bucket-table kernels on the compute stream.
 void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
-                       const float* mean_host, const float* mean_dev, bool compute_mean,
-                       const std::vector<ReadyView>* ready = nullptr,
-                       bool speculate = false) {
+                       const float* mean_host, const float* mean_dev, bool compute_mean) {
   const HashDev& h = c.hd;
   const int n_imgs = static_cast<int>(descs.size());
   const int L = h.tables;
@@ -511,9 +455,6 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.cursor = reinterpret_cast<uint32_t*>(base + lay[i].cursor_off);
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
     im.overflow = 0;
-    im.ready = ready ? (*ready)[i].flag : nullptr;
-    im.ready_gen = ready ? (*ready)[i].gen : 0u;
-    im.dt = ready ? (*ready)[i].dt : nullptr;
   }
   // metadata
   ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
@@ -550,18 +491,10 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   rs.codes_bytes = codes_end;
   rs.offsets_begin = codes_end;
   rs.offsets_bytes = offsets_end - codes_end;
-  rs.spec_slot = -1;
   join_uploads(c);
 
   const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
   float* d_mean = c.d_mean.as<float>();
-  int mean_slot = -1;
-  if (!mean_dev && !mean_host && compute_mean) {
-    mean_slot = static_cast<int>(c.mean_seq++ % Ctx::kMeanSlots);
-    c.d_mean_slot[mean_slot].ensure(sizeof(float) * kDim + sizeof(double) * kDim);
-    c.d_mean_imgs[mean_slot].ensure(sizeof(ImgDev) * std::max(n_imgs, 1));
-    d_mean = c.d_mean_slot[mean_slot].as<float>();
-  }
   c.cur_mean = d_mean;
   if (mean_dev) {
     BMG_CUDA(cudaMemcpyAsync(d_mean, mean_dev, sizeof(float) * kDim, cudaMemcpyDeviceToDevice, s));
@@ -570,49 +503,26 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     std::memcpy(hm, mean_host, sizeof(float) * kDim);
     BMG_CUDA(cudaMemcpyAsync(d_mean, hm, sizeof(float) * kDim, cudaMemcpyHostToDevice, s));
   } else if (compute_mean) {
-    // the exact sequential chain, on its own stream
-    cudaStream_t sm = c.s_mean;
-    BMG_CUDA(cudaStreamWaitEvent(sm, c.ev_mean_free[mean_slot], 0));
-    ImgDev* hm = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
-    std::memcpy(hm, c.row_imgs.data(), sizeof(ImgDev) * n_imgs);
-    BMG_CUDA(cudaMemcpyAsync(c.d_mean_imgs[mean_slot].p, hm, sizeof(ImgDev) * n_imgs,
-                             cudaMemcpyHostToDevice, sm));
-    {
-      Timed t(c, "mean", sm);
-      launch_row_mean(c.d_mean_imgs[mean_slot].as<ImgDev>(), n_imgs, d_mean,
-                      reinterpret_cast<double*>(d_mean + kDim), sm);
-      ++c.launches;
-      check_launch();
-    }
-    BMG_CUDA(cudaEventRecord(c.ev_mean_done[mean_slot], sm));
-    if (speculate && n_tiles) {
-      // codes from the parallel mean now; verified after the row's matches
-      c.d_mean_fast.ensure(sizeof(float) * kDim);
-      c.d_partial.ensure(sizeof(double) * kDim * n_tiles);
-      {
-        Timed t(c, "mean_fast", s);
-        launch_mean_fast(d_imgs, c.d_tiles.as<uint32_t>(), c.d_tiles.as<uint32_t>() + n_tiles,
-                         static_cast<int>(n_tiles), c.d_partial.as<double>(), total_desc,
-                         c.d_mean_fast.as<float>(), s);
-        c.launches += 2;
-        check_launch();
-      }
-      rs.spec_slot = mean_slot;
-      enqueue_codes_tables(c, c.d_mean_fast.as<float>(), nullptr);
-      return;
-    }
-    BMG_CUDA(cudaStreamWaitEvent(s, c.ev_mean_done[mean_slot], 0));
+    // exact row mean (engine.cpp:446-461): F96 reconstruction of the FP64
+    // chain, the chain itself only as fallback (rows over 2^22 descriptors
+    // exceed the F96 headroom and take the chain directly)
+    const bool chain_only = c.mean_chain_only || total_desc > (1ull << 22) || n_tiles == 0;
+    c.last_mean_chain_only = chain_only;
+    c.d_mean_sums.ensure(sizeof(__int128) * kDim * std::max<size_t>(n_tiles, 1));
+    c.d_mean_state.ensure(sizeof(MeanState));
+    Timed t(c, "mean", s);
+    c.launches += launch_row_mean(d_imgs, n_imgs, c.d_tiles.as<uint32_t>(),
+                                  c.d_tiles.as<uint32_t>() + n_tiles, static_cast<int>(n_tiles),
+                                  total_desc, c.d_mean_sums.p, c.d_mean_state.as<MeanState>(), d_mean,
+                                  c.d_acc.as<double>(), chain_only, s);
+    check_launch();
   }
-  enqueue_codes_tables(c, d_mean, nullptr);
-  if (mean_slot >= 0) BMG_CUDA(cudaEventRecord(c.ev_mean_free[mean_slot], s));
+  enqueue_codes_tables(c, d_mean);
 }
 
-void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host,
-                 bool speculate = false) {
+void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
   std::vector<std::pair<const float*, uint64_t>> descs;
-  std::vector<ReadyView> ready;
   descs.reserve(n);
-  ready.reserve(n);
   c.row_ids.assign(ids, ids + n);
   c.row_slot.clear();
   for (uint64_t i = 0; i < n; ++i) {
@@ -622,11 +532,10 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
     descs.emplace_back(it->second.d, it->second.n);
-    ready.push_back({c.d_flags.as<uint32_t>() + it->second.flag_slot, it->second.gen, it->second.dt});
     c.row_slot[ids[i]] = static_cast<int>(i);
   }
   c.row_valid = false;
-  prepare_row_views(c, descs, mean_host, nullptr, true, &ready, speculate);
+  prepare_row_views(c, descs, mean_host, nullptr, true);
   c.row_valid = true;
 }
 
@@ -646,8 +555,7 @@ void check_match_params(const Ctx& c, const bmg_match_params& mp) {
 // current row views.  Offsets (absolute positions in d_res) go to
 // out_off[0..n_pairs], appended after *d_running.
 void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
-                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res,
-                   const uint32_t* gate = nullptr) {
+                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res) {
   check_match_params(c, mp);
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
@@ -703,12 +611,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   BMG_CUDA(cudaMemcpyAsync(c.d_dense_off.p, h_dense_off, sizeof(uint64_t) * n_pairs,
                            cudaMemcpyHostToDevice, s));
   BMG_CUDA(cudaMemcpyAsync(c.d_nq.p, h_nq, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, s));
-  if (gate) {
-    launch_gated_clear(c.d_pair_count.p, sizeof(uint32_t) * n_pairs, gate, s);
-    ++c.launches;
-  } else {
-    BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
-  }
+  BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
   MatchLaunch a{};
   a.imgs = c.d_imgs.as<ImgDev>();
   a.work = c.d_work.as<PairWork>();
@@ -721,7 +624,6 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   a.k = mp.k_nearest;
   a.idx_bits = idx_bits;
   a.ratio = mp.ratio;
-  a.gate = gate;
   if (n_work) {
     Timed t(c, "match", s);
     launch_match(a, h.fwp, static_cast<int>(n_work), c.row_imgs[0], max_train_n, s, nullptr);
@@ -731,40 +633,12 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   {
     Timed t(c, "compact", s);
     launch_scan_counts(c.d_pair_count.as<uint32_t>(), n_pairs, out_off,
-                       c.d_running.as<unsigned long long>(), gate, s);
+                       c.d_running.as<unsigned long long>(), s);
     launch_compact(c.d_dense.as<int32_t>(), c.d_dense_off.as<uint64_t>(), c.d_nq.as<uint32_t>(),
-                   out_off, n_pairs, d_res, gate, s);
+                   out_off, n_pairs, d_res, s);
     c.launches += 2;
     check_launch();
   }
-}
-
-// After a speculative row's matches: wait for the exact sequential mean,
-// compare bit patterns, and enqueue the gated re-do of codes, tables and
-// matches (kernels exit at once unless the check found a difference; a re-do
-// appends the correct lists to the result log and rewrites the row's offsets).
-void enqueue_row_verify(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
-                        const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res,
-                        bool force_redo) {
-  const int slot = c.rs.spec_slot;
-  if (slot < 0) return;
-  cudaStream_t s = c.s_comp;
-  c.d_redo.ensure(sizeof(uint32_t));
-  uint32_t* redo = c.d_redo.as<uint32_t>();
-  const float* exact = c.d_mean_slot[slot].as<float>();
-  BMG_CUDA(cudaStreamWaitEvent(s, c.ev_mean_done[slot], 0));
-  if (force_redo) {
-    BMG_CUDA(cudaMemsetAsync(redo, 0xff, sizeof(uint32_t), s));  // test hook: always re-do
-  } else {
-    launch_mean_check(c.d_mean_fast.as<float>(), exact, redo, s);
-    ++c.launches;
-    check_launch();
-  }
-  enqueue_codes_tables(c, exact, redo);
-  enqueue_match(c, slot_pairs, mp, out_off, d_res, redo);
-  BMG_CUDA(cudaEventRecord(c.ev_mean_free[slot], s));
-  c.rs.spec_slot = -1;
-  ++c.spec_rows;
 }
 
 HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const float* fine) {
@@ -826,8 +700,18 @@ void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fi
 void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
   c.res_ranges.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
   c.res_log.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
+  c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
   c.d_running.ensure(sizeof(unsigned long long));
   BMG_CUDA(cudaMemsetAsync(c.d_running.p, 0, sizeof(unsigned long long), c.s_comp));
+}
+
+// After the compute stream drained: DMA the log entries [0, end) into the
+// pinned host mirror and return it.
+const int32_t* fetch_log(Ctx& c, uint64_t end) {
+  if (end)
+    BMG_CUDA(cudaMemcpy(c.res_log.host<int32_t>(), c.d_res.p, sizeof(int32_t) * 2 * end,
+                        cudaMemcpyDeviceToHost));
+  return c.res_log.host<int32_t>();
 }
 
 }  // namespace
@@ -892,14 +776,7 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     c->capacity = cfg->capacity_units;
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
-    BMG_CUDA(cudaStreamCreateWithFlags(&c->s_mean, cudaStreamNonBlocking));
-    for (int i = 0; i < bmg_context::kMeanSlots; ++i) {
-      BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_done[i], cudaEventDisableTiming));
-      BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_free[i], cudaEventDisableTiming));
-      BMG_CUDA(cudaEventRecord(c->ev_mean_free[i], c->s_comp));
-    }
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
-    BMG_CUDA(cudaEventCreateWithFlags(&c->ev_mean_tail, cudaEventDisableTiming));
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
     BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
@@ -910,8 +787,6 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
       BMG_CUDA(cudaEventRecord(c->stage_ev[i], c->s_copy));
     }
     c->ring.init(64u << 20);
-    c->d_flags.ensure(sizeof(uint32_t) * kFlagSlots);
-    BMG_CUDA(cudaMemset(c->d_flags.p, 0, sizeof(uint32_t) * kFlagSlots));
     c->hd = build_hash(*c, cfg->hash, cfg->coarse_planes, cfg->fine_planes);
     *out = c.release();
   });
@@ -922,18 +797,17 @@ int bmg_destroy(bmg_context* c) {
   return guarded([&] {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    for (auto& [id, im] : c->resident) {
-      cudaFree(im.d);
-      cudaFree(im.dt);
-    }
+    for (auto& [id, im] : c->resident) cudaFree(im.d);
     c->resident.clear();
     for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
                       &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
                       &c->d_work, &c->d_dense, &c->d_dense_off, &c->d_pair_count, &c->d_nq,
-                      &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_flags})
+                      &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_mean_sums,
+                      &c->d_mean_state})
       b->release();
     c->res_ranges.release();
     c->res_log.release();
+    c->d_res.release();
     for (int i = 0; i < 2; ++i) {
       if (c->stage[i]) cudaFreeHost(c->stage[i]);
       if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
@@ -945,16 +819,8 @@ int bmg_destroy(bmg_context* c) {
     }
     for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
     if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
-    if (c->ev_mean_tail) cudaEventDestroy(c->ev_mean_tail);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
     if (c->s_comp) cudaStreamDestroy(c->s_comp);
-    for (int i = 0; i < bmg_context::kMeanSlots; ++i) {
-      c->d_mean_slot[i].release();
-      c->d_mean_imgs[i].release();
-      if (c->ev_mean_done[i]) cudaEventDestroy(c->ev_mean_done[i]);
-      if (c->ev_mean_free[i]) cudaEventDestroy(c->ev_mean_free[i]);
-    }
-    if (c->s_mean) cudaStreamDestroy(c->s_mean);
     delete c;
   });
 }
@@ -964,7 +830,6 @@ int bmg_synchronize(bmg_context* c) {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
-    BMG_CUDA(cudaStreamSynchronize(c->s_mean));
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
   });
 }
@@ -1049,7 +914,7 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
       max_matches += c->row_imgs[qi->second].n;
     }
     reset_results(*c, n_pairs, max_matches);
-    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->res_log.dev<int32_t>());
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>());
     if (n_pairs == 0) {
       offsets_out[0] = 0;
       return;
@@ -1063,7 +928,7 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
     if (total > capacity) fail(BMG_INVALID_ARGUMENT, "match output capacity too small");
     if (total) {
       if (!matches_out) fail(BMG_INVALID_ARGUMENT, "null match output");
-      std::memcpy(matches_out, c->res_log.host<int32_t>(), sizeof(int32_t) * 2 * total);
+      std::memcpy(matches_out, fetch_log(*c, total), sizeof(int32_t) * 2 * total);
     }
   });
 }
@@ -1191,12 +1056,12 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
     }
     std::vector<std::pair<int, int>> sp{{0, 1}};
     reset_results(*c, 1, nq);
-    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->res_log.dev<int32_t>());
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>());
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
     const uint64_t* offs = c->res_ranges.host<uint64_t>();
     const uint64_t total = offs[1] - offs[0];
     if (total)
-      std::memcpy(matches_out, c->res_log.host<int32_t>() + 2 * offs[0], sizeof(int32_t) * 2 * total);
+      std::memcpy(matches_out, fetch_log(*c, offs[1]) + 2 * offs[0], sizeof(int32_t) * 2 * total);
     *n_out = total;
   });
 }
@@ -1229,16 +1094,18 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       cap += features_of(a).count;
     }
     auto res = std::make_unique<bmg_result>();
-    // a row re-done after a mean speculation miss appends its lists again
-    const bool may_redo = (opts->flags & BMG_EXEC_NO_SPECULATION) == 0;
-    reset_results(*c, n_pairs, may_redo ? 2 * cap : cap);
+    reset_results(*c, n_pairs, cap);
     uint64_t* d_off = c->res_ranges.dev<uint64_t>();
-    int32_t* d_log = c->res_log.dev<int32_t>();
+    int32_t* d_log = c->d_res.as<int32_t>();
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->s_comp));
-    BMG_CUDA(cudaStreamWaitEvent(c->s_mean, span0, 0));
     BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
+    struct ChainHook {
+      Ctx& c;
+      ~ChainHook() { c.mean_chain_only = false; }
+    } chain_hook{*c};
+    c->mean_chain_only = (opts->flags & BMG_EXEC_MEAN_CHAIN) != 0;
     uint64_t row = 0;
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
       const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
@@ -1254,12 +1121,7 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
           }
         }
-        uint64_t row_desc = 0;
-        for (uint64_t k = nb; k < ne; ++k) row_desc += c->resident.at(plan->needed_ids[k]).n;
-        const bool speculate = (opts->flags & BMG_EXEC_NO_SPECULATION) == 0 &&
-                               ((opts->flags & (BMG_EXEC_FORCE_SPECULATION | BMG_EXEC_FORCE_REDO)) ||
-                                row_desc >= kSpeculateMinDescriptors);
-        prepare_row(*c, needed, ne - nb, nullptr, speculate);
+        prepare_row(*c, needed, ne - nb, nullptr);
         const uint64_t pb = plan->row_pair_offsets[row], pe = plan->row_pair_offsets[row + 1];
         std::vector<std::pair<int, int>> sp;
         sp.reserve(pe - pb);
@@ -1271,8 +1133,6 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           sp.emplace_back(qa->second, tb->second);
         }
         enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log);
-        enqueue_row_verify(*c, sp, opts->match, d_off + 2 * pb, d_log,
-                           (opts->flags & BMG_EXEC_FORCE_REDO) != 0);
         it_pairs += pe - pb;
         for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
           arena_evict(*c, plan->evict_ids[k]);
@@ -1284,14 +1144,16 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->iterations.push_back(c->units_uploaded - units0);
     }
     BMG_CUDA(cudaEventRecord(span1, c->s_comp));
-    // the compaction kernels wrote the per-pair [begin, end) ranges and the
-    // match log straight into mapped host memory (a row re-done after a mean
-    // speculation miss left its first lists unreferenced in the log)
+    // per-pair [begin, end) ranges are in mapped host memory; the log is
+    // read back in one DMA
     BMG_CUDA(cudaStreamSynchronize(c->s_comp));
     const uint64_t* ranges = c->res_ranges.host<uint64_t>();
-    const int32_t* flat = c->res_log.host<int32_t>();
-    uint64_t total = 0, kept_total = 0;
-    for (uint64_t p = 0; p < n_pairs; ++p) kept_total += ranges[2 * p + 1] - ranges[2 * p];
+    uint64_t total = 0, kept_total = 0, log_end = 0;
+    for (uint64_t p = 0; p < n_pairs; ++p) {
+      kept_total += ranges[2 * p + 1] - ranges[2 * p];
+      log_end = std::max(log_end, ranges[2 * p + 1]);
+    }
+    const int32_t* flat = fetch_log(*c, log_end);
     res->matches.reserve(2 * kept_total);
     // results keyed and sorted by IdPair (engine.cpp:419, 506-512); a pair
     // planned twice keeps its last match list, like the reference's map
@@ -1410,6 +1272,20 @@ int bmg_fixup_counts(bmg_context* c, uint64_t* code_bits, uint64_t* rerank_queri
     }
     if (code_bits) *code_bits = d[0];
     if (rerank_queries) *rerank_queries = d[1];
+  });
+}
+
+int bmg_row_mean_info(bmg_context* c, uint32_t* rounds, int* used_chain) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    MeanState st{};
+    if (c->d_mean_state.p && !c->last_mean_chain_only) {
+      BMG_CUDA(cudaMemcpyAsync(&st, c->d_mean_state.p, sizeof(st), cudaMemcpyDeviceToHost, c->s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    }
+    if (rounds) *rounds = st.rounds;
+    if (used_chain) *used_chain = (c->last_mean_chain_only || st.need_chain) ? 1 : 0;
   });
 }
 

@@ -20,15 +20,7 @@ struct ImgDev {
   uint32_t* slots;     // [tables][n] train indices grouped by bucket (:136-145)
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
-  // upload completion flag written by the copy stream after the image's H2D
-  // (value = upload generation); the row-mean producer waits on it so the
-  // mean chain overlaps the transfers.  nullptr = already resident.
-  const uint32_t* ready;
-  uint32_t ready_gen;
   uint32_t pad_;
-  // channel-major FP64 copy [128][n] made once per upload (exact widening),
-  // streamed by the row-mean chain; nullptr for non-arena images
-  const double* dt;
 };
 
 struct HashDev {
@@ -41,9 +33,6 @@ struct HashDev {
   const float* planes;     // [n_planes][128] planes (coarse first, then fine)
   const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
   int n_planes_pad;
-  // when non-null, kernels return immediately unless *gate != 0 (the
-  // re-do pass after a mean speculation miss; see bmg_api.cpp)
-  const uint32_t* gate;
 };
 
 // An ambiguous projection whose sign the FP32 pass could not certify; the
@@ -69,14 +58,31 @@ struct MatchLaunch {
   unsigned long long* exact_queries;  // diagnostics: queries that took the FP64 path
   int tables, n_buckets, k, idx_bits;
   double ratio;
-  const uint32_t* gate;        // see HashDev::gate
 };
 
+// Device state of the exact parallel row mean (kernels.cu K1): per channel the
+// F96 total, the current rounding offset delta, the first unchecked step and
+// the first non-representable step found by the last walk.
+struct MeanState {
+  uint32_t bad;         // a descriptor value outside the F96 range
+  uint32_t done;        // the last walk found no rounding step
+  uint32_t need_chain;  // gate of the sequential fallback
+  uint32_t rounds;
+  uint32_t pending[kDim];
+  uint32_t k_start[kDim];
+  uint32_t first_event[kDim];
+  alignas(16) __int128 sum[kDim];
+  alignas(16) __int128 delta[kDim];
+};
+constexpr int kMeanRounds = 6;
+
 // ---- launchers (kernels.cu) ----
-// float [n][128] -> double [128][n] (exact), for the row-mean chain
-void launch_widen_transpose(const float* desc, uint32_t n, double* dt, cudaStream_t s);
-void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
-                     cudaStream_t s);
+// Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
+// parallel reconstruction with the sequential chain as gated fallback, or the
+// chain alone.  tile_sums: 16 * 128 * n_tiles bytes.  Returns kernel launches.
+int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
+                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* tile_sums,
+                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s);
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                   const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
                   uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s);
@@ -88,18 +94,9 @@ void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* til
 void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev& any_train_max,
                   uint32_t max_train_n, cudaStream_t s, int* smem_used);
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, const uint32_t* gate, cudaStream_t s);
+                        unsigned long long* running_total, cudaStream_t s);
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
-                    const uint64_t* out_off, int n_pairs, int32_t* out, const uint32_t* gate,
-                    cudaStream_t s);
-// speculative row mean: order-free FP64 sums per 128-descriptor tile, then a
-// fixed-order reduction -> float(sum / total)
-void launch_mean_fast(const ImgDev* imgs, const uint32_t* tile_img, const uint32_t* tile_start,
-                      int n_tiles, double* partial, unsigned long long total, float* mean_out,
-                      cudaStream_t s);
-// *redo = any bit of the speculative mean differs from the exact one
-void launch_mean_check(const float* fast, const float* exact, uint32_t* redo, cudaStream_t s);
-void launch_gated_clear(void* p, size_t bytes, const uint32_t* gate, cudaStream_t s);
+                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);
 
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
 constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)

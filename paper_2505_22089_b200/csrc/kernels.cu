@@ -32,167 +32,222 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Re-do pass gate (uniform across the grid): the kernel is a no-op unless the
-// mean speculation of its row missed.
+// Gate (uniform across the grid): the kernel is a no-op when *gate == 0 (the
+// chain fallback runs only when the exact parallel mean gave up).
 __device__ __forceinline__ bool gated_off(const uint32_t* gate) {
   return gate != nullptr && *reinterpret_cast<const volatile uint32_t*>(gate) == 0u;
 }
 
 // ---------------------------------------------------------------------------
-// Speculative row mean.  The exact mean is a 128-lane sequential FP64 chain
-// (K1 below) -- a latency-bound millisecond per large row.  The row's codes,
-// tables and matches are instead computed from a parallel FP64 mean (order-
-// free tile sums, fixed-order reduction; a few double ulps from the
-// sequential sum, so its float rounding is almost always identical) while K1
-// runs on its own stream; mean_check compares the bit patterns and, on any
-// difference, the row is recomputed by a gated second pass with the exact
-// mean.  Results are therefore always those of the reference's sequential
-// mean; only the time of a (rare) miss is paid twice.
+// K1: row centering mean (engine.cpp:446-461): acc[c] += (double)d.v[c] over
+// the row's images in ascending id order, descriptors in index order, then
+// mean[c] = float(acc[c] / (double)total).
+//
+// Reproduced bit for bit without running the 128 dependent FP64 chains.
+// Descriptor values in (-2^8, 2^8) whose lowest set bit is >= 2^-96 are exact
+// in 128-bit fixed point with 96 fractional bits ("F96"), and so is every
+// prefix sum S_k of up to 2^22 of them.  The chain's state is
+// acc_k = RN(acc_{k-1} + x_k); when the exact value acc_{k-1} + x_k fits a
+// binary64 (its F96 bit span is <= 53 bits) the add is exact.  Hence
+// acc_k = S_k + delta, where delta changes only at the steps whose exact sum
+// needs rounding -- about 30 of the 262k x 128 steps of a BASELINE config-2
+// row, at most 2 per channel -- and there delta' = RN(S_k + delta) - S_k.
+//   mean_sums     per 128-descriptor tile: F96 tile sums, range check
+//   mean_scan     per channel: exclusive prefix of the tile sums
+//   mean_walk     per tile: re-walks S_k from the tile prefix and reports each
+//                 channel's first step >= k_start whose S_k + delta does not
+//                 fit a double
+//   mean_resolve  applies that step's rounding (delta, k_start = step + 1)
+// walk/resolve repeat kMeanRounds times (no-ops once a walk found nothing).
+// A row outside the F96 range, or with more rounding steps in one channel
+// than rounds, falls back to mean_chain_kernel, the literal chain.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kDim) mean_partial_kernel(const ImgDev* __restrict__ imgs,
+using i128 = __int128;
+using u128 = unsigned __int128;
+constexpr uint32_t kNoEvent = 0xffffffffu;
+
+// x * 2^96 as an integer; ok = false when that is not exact or |x| >= 2^8
+__device__ __forceinline__ i128 to_f96(float x, bool& ok) {
+  const uint32_t u = __float_as_uint(x);
+  const int e = (u >> 23) & 0xff;
+  const uint32_t m = (u & 0x7fffffu) | 0x800000u;
+  u128 mag = 0;
+  if (e >= 54 && e < 127 + 8) {
+    mag = (u128)m << (e - 54);  // x = m * 2^(e-150) = m << (e-54) F96 units
+  } else if (e == 0) {
+    ok &= (u & 0x7fffffu) == 0u;  // +-0 (subnormals are below 2^-96)
+  } else if (e < 54 && e > 54 - 24) {
+    const int sh = 54 - e;
+    ok &= (m & ((1u << sh) - 1u)) == 0u;
+    mag = m >> sh;
+  } else {
+    ok = false;
+  }
+  return (u >> 31) ? -(i128)mag : (i128)mag;
+}
+
+__device__ __forceinline__ u128 abs128(i128 v) { return v < 0 ? (u128)(-v) : (u128)v; }
+
+__device__ __forceinline__ int top_bit(u128 a) {  // a != 0
+  const uint64_t hi = (uint64_t)(a >> 64), lo = (uint64_t)a;
+  return hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+}
+
+// is the F96 value v exactly representable as a binary64?
+__device__ __forceinline__ bool fits_double(i128 v) {
+  const u128 a = abs128(v);
+  const uint64_t hi = (uint64_t)(a >> 64), lo = (uint64_t)a;
+  if ((hi | lo) == 0) return true;
+  const int bot = lo ? __ffsll((long long)lo) - 1 : 63 + __ffsll((long long)hi);
+  return top_bit(a) - bot <= 52;
+}
+
+// round-to-nearest-even of v to 53 significant bits (the FP64 add's rounding)
+__device__ __forceinline__ i128 round53(i128 v) {
+  u128 a = abs128(v);
+  if (a == 0) return v;
+  const int sh = top_bit(a) - 52;
+  if (sh > 0) {
+    u128 q = a >> sh;
+    const u128 rem = a - (q << sh), half = (u128)1 << (sh - 1);
+    if (rem > half || (rem == half && (q & 1))) q += 1;
+    a = q << sh;
+  }
+  return v < 0 ? -(i128)a : (i128)a;
+}
+
+// v fits a double (checked by the walk): exact conversion
+__device__ __forceinline__ double f96_to_double(i128 v) {
+  const u128 a = abs128(v);
+  const double hi = __ull2double_rn((unsigned long long)(a >> 64));
+  const double lo = __ull2double_rn((unsigned long long)a);
+  const double r = __dmul_rn(__dadd_rn(__dmul_rn(hi, 18446744073709551616.0), lo), 0x1p-96);
+  return v < 0 ? -r : r;
+}
+
+__global__ void __launch_bounds__(kDim) mean_sums_kernel(const ImgDev* __restrict__ imgs,
+                                                         const uint32_t* __restrict__ tile_img,
+                                                         const uint32_t* __restrict__ tile_start,
+                                                         i128* __restrict__ tile_sum, MeanState* st) {
+  const int c = threadIdx.x;
+  const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
+  const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
+  i128 s = 0;
+  bool ok = true;
+#pragma unroll 8
+  for (int r = 0; r < nd; ++r) s += to_f96(__ldg(d + (size_t)r * kDim), ok);
+  tile_sum[(size_t)blockIdx.x * kDim + c] = s;
+  if (__syncthreads_or(!ok) && c == 0) st->bad = 1u;
+}
+
+// one CTA per channel: exclusive scan of its tile sums, in place
+__global__ void __launch_bounds__(256) mean_scan_kernel(i128* __restrict__ tile_sum, int n_tiles,
+                                                        MeanState* st) {
+  __shared__ i128 part[256];
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const int per = (n_tiles + 255) / 256;
+  const int t0 = min(n_tiles, tid * per), t1 = min(n_tiles, t0 + per);
+  i128 loc = 0;
+  for (int t = t0; t < t1; ++t) loc += tile_sum[(size_t)t * kDim + c];
+  part[tid] = loc;
+  __syncthreads();
+  if (tid == 0) {
+    i128 run = 0;
+    for (int i = 0; i < 256; ++i) {
+      const i128 v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    st->sum[c] = run;
+    st->delta[c] = 0;
+    st->k_start[c] = 0;
+    st->pending[c] = 1u;
+    st->first_event[c] = kNoEvent;
+  }
+  __syncthreads();
+  i128 run = part[tid];
+  for (int t = t0; t < t1; ++t) {
+    const i128 v = tile_sum[(size_t)t * kDim + c];
+    tile_sum[(size_t)t * kDim + c] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kDim) mean_walk_kernel(const ImgDev* __restrict__ imgs,
+                                                         const uint32_t* __restrict__ tile_img,
+                                                         const uint32_t* __restrict__ tile_start,
+                                                         const i128* __restrict__ prefix, MeanState* st) {
+  if (st->done | st->bad) return;
+  const int c = threadIdx.x;
+  if (!st->pending[c]) return;
+  const uint32_t ks = st->k_start[c], p0 = blockIdx.x * (uint32_t)kCodesTile;
+  const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
+  if (p0 + nd <= ks) return;
+  const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
+  i128 S = prefix[(size_t)blockIdx.x * kDim + c];
+  const i128 dl = st->delta[c];
+  bool ok = true;
+#pragma unroll 4
+  for (int r = 0; r < nd; ++r) {
+    S += to_f96(__ldg(d + (size_t)r * kDim), ok);
+    if (p0 + r >= ks && !fits_double(S + dl)) {
+      atomicMin(&st->first_event[c], p0 + r);
+      break;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDim) mean_resolve_kernel(const ImgDev* __restrict__ imgs,
                                                             const uint32_t* __restrict__ tile_img,
                                                             const uint32_t* __restrict__ tile_start,
-                                                            double* __restrict__ partial) {
+                                                            const i128* __restrict__ prefix, MeanState* st) {
+  if (st->done | st->bad) return;
   const int c = threadIdx.x;
-  const ImgDev im = imgs[tile_img[blockIdx.x]];
-  const uint32_t i0 = tile_start[blockIdx.x];
-  const int nd = min(kCodesTile, (int)(im.n - i0));
-  const float* d = im.desc + (size_t)i0 * kDim + c;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int r = 0;
-  for (; r + 4 <= nd; r += 4) {
-    s0 += (double)__ldg(d + (size_t)r * kDim);
-    s1 += (double)__ldg(d + (size_t)(r + 1) * kDim);
-    s2 += (double)__ldg(d + (size_t)(r + 2) * kDim);
-    s3 += (double)__ldg(d + (size_t)(r + 3) * kDim);
+  const uint32_t p = st->first_event[c];
+  const bool ev = p != kNoEvent;
+  if (ev) {
+    const uint32_t tile = p / kCodesTile, r = p % kCodesTile;
+    const uint32_t img = tile_img[tile], i0 = tile_start[tile];
+    const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
+    i128 S = prefix[(size_t)tile * kDim + c];
+    bool ok = true;
+    for (uint32_t q = 0; q <= r; ++q) S += to_f96(__ldg(d + (size_t)q * kDim), ok);
+    st->delta[c] = round53(S + st->delta[c]) - S;
+    st->k_start[c] = p + 1;
+    st->first_event[c] = kNoEvent;
   }
-  for (; r < nd; ++r) s0 += (double)__ldg(d + (size_t)r * kDim);
-  partial[(size_t)blockIdx.x * kDim + c] = (s0 + s1) + (s2 + s3);
-}
-
-__global__ void __launch_bounds__(1024) mean_final_kernel(const double* __restrict__ partial, int n_tiles,
-                                                          unsigned long long total,
-                                                          float* __restrict__ mean_out) {
-  __shared__ double s_part[8][kDim];
-  const int c = threadIdx.x & (kDim - 1), part = threadIdx.x >> 7;  // 8 parts x 128 channels
-  double s = 0.0;
-  for (int t = part; t < n_tiles; t += 8) s += partial[(size_t)t * kDim + c];
-  s_part[part][c] = s;
-  __syncthreads();
-  if (part == 0) {
-    double a = 0.0;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) a += s_part[p][c];
-    mean_out[c] = total ? __double2float_rn(a / (double)total) : 0.0f;
+  st->pending[c] = ev ? 1u : 0u;
+  const int any = __syncthreads_or(ev);
+  if (c == 0) {
+    st->done = any ? 0u : 1u;
+    ++st->rounds;
   }
 }
 
-__global__ void __launch_bounds__(kDim) mean_check_kernel(const float* __restrict__ fast,
-                                                          const float* __restrict__ exact,
-                                                          uint32_t* __restrict__ redo) {
+__global__ void __launch_bounds__(kDim) mean_finalize_kernel(MeanState* st, unsigned long long total,
+                                                             float* __restrict__ mean_out,
+                                                             double* __restrict__ acc_out) {
   const int c = threadIdx.x;
-  const int diff = __float_as_uint(fast[c]) != __float_as_uint(exact[c]);
-  const int any = __syncthreads_or(diff);
-  if (c == 0) *redo = any ? 1u : 0u;
+  const bool chain = st->bad || !st->done;
+  if (c == 0) st->need_chain = chain ? 1u : 0u;
+  if (chain) return;
+  const double acc = f96_to_double(st->sum[c] + st->delta[c]);
+  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+  if (acc_out) acc_out[c] = acc;
 }
 
-__global__ void gated_clear_kernel(uint32_t* __restrict__ p, size_t words, const uint32_t* gate) {
+// The literal chain (fallback and test reference): 4 CTAs x 32 channels, one
+// thread per channel; the loads of the next 32 descriptors are in flight
+// while the current 32 dependent DADDs issue, with an L2 prefetch stream 8
+// batches ahead.
+constexpr int kChainBatch = 32;
+
+__global__ void __launch_bounds__(32, 1) mean_chain_kernel(const ImgDev* __restrict__ imgs, int n_imgs,
+                                                           const uint32_t* gate, float* __restrict__ mean_out,
+                                                           double* __restrict__ acc_out) {
   if (gated_off(gate)) return;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words;
-       i += (size_t)gridDim.x * blockDim.x)
-    p[i] = 0u;
-}
-
-// ---------------------------------------------------------------------------
-// K1: row centering mean (engine.cpp:446-461).  acc[c] += (double)d.v[c] over
-// images in ascending id order, descriptors in index order, then
-// mean = float(acc / total): a dependent FP64 chain per channel, reproduced
-// literally (runs on its own stream; the row's codes are computed from the
-// speculative parallel mean above and verified against this one).
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                             uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-// Exact widening + transpose at upload: dt[c][i] = (double)desc[i][c], so a
-// channel's terms are contiguous for the chain and no F2F (XU pipe, as slow
-// per warp as the DADD latency) sits in the chain's issue stream.
-__global__ void __launch_bounds__(256) widen_transpose_kernel(const float* __restrict__ desc, uint32_t n,
-                                                              double* __restrict__ dt) {
-  __shared__ float tile[32][kDim + 1];
-  const uint32_t r0 = blockIdx.x * 32;
-  const int rows = min(32u, n - r0);
-  for (int e = threadIdx.x; e < 32 * kDim; e += blockDim.x) {
-    const int r = e / kDim, c = e % kDim;
-    tile[r][c] = r < rows ? __ldg(desc + (size_t)(r0 + r) * kDim + c) : 0.0f;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < kDim; c += blockDim.x / 32)
-    if (lane < rows) dt[(size_t)c * n + r0 + lane] = (double)tile[lane][c];
-}
-
-// The chain: one warp per CTA, 4 CTAs x 32 channels.  Each thread streams its
-// channel's contiguous doubles image by image through a 4-stage cp.async
-// ring in shared memory (32 doubles per stage per thread, ~40 KB in flight per
-// warp on top of the L2 prefetch stream), so the DADD chain issues back to
-// back at the FP64 add latency.
-constexpr int kMeanBatch = 32;   // doubles per stage per thread
-constexpr int kMeanStages = 6;   // 48 KB of static shared memory
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void wait_upload(const uint32_t* flag, uint32_t gen) {
-  // stream the image as soon as its H2D + widening have landed (bounded wait)
-  unsigned long long t0, now;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if ((int32_t)(v - gen) >= 0) break;  // generations only grow per slot
-    __nanosleep(256);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (now - t0 > 20000000000ull) __trap();  // 20 s: an upload never completed
-  }
-}
-
-__global__ void __launch_bounds__(32, 1) row_mean_kernel(const ImgDev* __restrict__ imgs, int n_imgs,
-                                                         float* __restrict__ mean_out,
-                                                         double* __restrict__ acc_out) {
-  // [stage][pair k2 = 0..kMeanBatch/2)[lane] x 2 doubles: a warp's LDS.128 is contiguous
-  __shared__ __align__(16) double ring[kMeanStages][kMeanBatch / 2][32][2];
   const int lane = threadIdx.x;
   const int c = blockIdx.x * 32 + lane;
   double acc = 0.0;
@@ -200,51 +255,27 @@ __global__ void __launch_bounds__(32, 1) row_mean_kernel(const ImgDev* __restric
   for (int im = 0; im < n_imgs; ++im) {
     const uint32_t n = imgs[im].n;
     total += n;
-    if (n == 0) continue;
-    if (imgs[im].ready) {
-      if (lane == 0) wait_upload(imgs[im].ready, imgs[im].ready_gen);
-      __syncwarp();
-    }
-    const double* col = imgs[im].dt + (size_t)c * n;
-    // a channel column starts 16-byte aligned iff c*n is even: peel one term
-    uint32_t i = 0;
-    if ((c * (size_t)n) & 1u) {
-      acc = __dadd_rn(acc, __ldcg(col));
-      i = 1;
-    }
-    const uint32_t nb = (n - i) / kMeanBatch;
-    auto issue = [&](uint32_t b) {
-      const int st = b % kMeanStages;
-      const double* src = col + i + (size_t)b * kMeanBatch;
+    const float* d = imgs[im].desc + c;
+    const uint32_t nb = n / kChainBatch;
+    float cur[kChainBatch], nxt[kChainBatch];
+    if (nb) {
 #pragma unroll
-      for (int k2 = 0; k2 < kMeanBatch / 2; ++k2)
-        cp_async16(smem_addr(&ring[st][k2][lane][0]), src + 2 * k2);
-    };
-#pragma unroll
-    for (int p = 0; p < kMeanStages - 1; ++p) {
-      if ((uint32_t)p < nb) issue(p);
-      cp_async_commit();
+      for (int r = 0; r < kChainBatch; ++r) cur[r] = __ldcg(d + (size_t)r * kDim);
     }
     for (uint32_t b = 0; b < nb; ++b) {
-      if (b + kMeanStages - 1 < nb) {
-        issue(b + kMeanStages - 1);
-        const double* pf = col + i + (size_t)(b + 16) * kMeanBatch;
-        if (pf < col + n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-      }
-      cp_async_commit();
-      cp_async_wait<kMeanStages - 1>();  // batch b has landed
-      __syncwarp();
-      const int st = b % kMeanStages;
+      const size_t row = (size_t)(b + 1) * kChainBatch;
+      if (b + 1 < nb) {
 #pragma unroll
-      for (int k2 = 0; k2 < kMeanBatch / 2; ++k2) {
-        const double2 v = *reinterpret_cast<const double2*>(&ring[st][k2][lane][0]);
-        acc = __dadd_rn(acc, v.x);
-        acc = __dadd_rn(acc, v.y);
+        for (int r = 0; r < kChainBatch; ++r) nxt[r] = __ldcg(d + (row + r) * kDim);
       }
-      __syncwarp();
+      const size_t pf = row + 8 * kChainBatch + lane;
+      if (pf < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(imgs[im].desc + pf * kDim + blockIdx.x * 32));
+#pragma unroll
+      for (int r = 0; r < kChainBatch; ++r) acc = __dadd_rn(acc, (double)cur[r]);
+#pragma unroll
+      for (int r = 0; r < kChainBatch; ++r) cur[r] = nxt[r];
     }
-    cp_async_wait<0>();
-    for (i += nb * kMeanBatch; i < n; ++i) acc = __dadd_rn(acc, __ldcg(col + i));
+    for (uint32_t i = nb * kChainBatch; i < n; ++i) acc = __dadd_rn(acc, (double)__ldcg(d + (size_t)i * kDim));
   }
   mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
   if (acc_out) acc_out[c] = acc;
@@ -280,7 +311,6 @@ __global__ void __launch_bounds__(512, 1)
                  const uint32_t* __restrict__ tile_start, const float* __restrict__ mean,
                  Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
                  uint32_t* __restrict__ overflow) {
-  if (gated_off(h.gate)) return;
   extern __shared__ __align__(16) float smem_f[];
   float* sP = smem_f;                                  // [128][192]
   float* sA = sP + kDim * kPlaneChunk;                 // [128][132]
@@ -448,7 +478,6 @@ __global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                    const float* __restrict__ mean, const Fixup* __restrict__ fix,
                                    const uint32_t* __restrict__ fix_count, uint32_t fix_cap,
                                    unsigned long long* fixed_bits) {
-  if (gated_off(h.gate)) return;
   const uint32_t n = min(*fix_count, fix_cap);
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const Fixup f = fix[e];
@@ -466,7 +495,6 @@ __global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
 __global__ void codes_overflow_kernel(HashDev h, const ImgDev* __restrict__ imgs, int n_imgs,
                                       const float* __restrict__ mean,
                                       const uint32_t* __restrict__ overflow) {
-  if (gated_off(h.gate)) return;
   for (int ii = 0; ii < n_imgs; ++ii) {
     if (!overflow[ii]) continue;
     const ImgDev im = imgs[ii];
@@ -489,7 +517,6 @@ __global__ void codes_overflow_kernel(HashDev h, const ImgDev* __restrict__ imgs
 __global__ void tables_hist_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                    const uint32_t* __restrict__ tile_img,
                                    const uint32_t* __restrict__ tile_start) {
-  if (gated_off(h.gate)) return;
   const ImgDev im = imgs[tile_img[blockIdx.x]];
   const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
   if (i >= im.n) return;
@@ -524,7 +551,6 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp
 }
 
 __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
-  if (gated_off(h.gate)) return;
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry;
   const ImgDev im = imgs[blockIdx.x];
@@ -550,7 +576,6 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
 __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                       const uint32_t* __restrict__ tile_img,
                                       const uint32_t* __restrict__ tile_start) {
-  if (gated_off(h.gate)) return;
   const ImgDev im = imgs[tile_img[blockIdx.x]];
   const uint32_t i = tile_start[blockIdx.x] + threadIdx.x;
   if (i >= im.n) return;
@@ -617,7 +642,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ uint32_t s_tab[NT / 32][kBaseOff + kMaxTables];
-  if (gated_off(a.gate)) return;
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
@@ -951,9 +975,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 // re-point one row's pairs without touching its neighbours.
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __restrict__ counts, int n,
                                                            uint64_t* __restrict__ ranges,
-                                                           unsigned long long* running_total,
-                                                           const uint32_t* gate) {
-  if (gated_off(gate)) return;
+                                                           unsigned long long* running_total) {
   __shared__ uint32_t s_warp[32];
   __shared__ unsigned long long s_carry;
   if (threadIdx.x == 0) s_carry = *running_total;
@@ -978,9 +1000,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
                                                        const uint64_t* __restrict__ dense_off,
                                                        const uint32_t* __restrict__ nq,
                                                        const uint64_t* __restrict__ out_off,
-                                                       int32_t* __restrict__ out,
-                                                       const uint32_t* gate) {
-  if (gated_off(gate)) return;
+                                                       int32_t* __restrict__ out) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_base;
   const int p = blockIdx.x;
@@ -1009,13 +1029,26 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-void launch_row_mean(const ImgDev* imgs, int n_imgs, float* mean_out, double* acc_out,
-                     cudaStream_t s) {
-  row_mean_kernel<<<kDim / 32, 32, 0, s>>>(imgs, n_imgs, mean_out, acc_out);
-}
-
-void launch_widen_transpose(const float* desc, uint32_t n, double* dt, cudaStream_t s) {
-  if (n) widen_transpose_kernel<<<(n + 31) / 32, 256, 0, s>>>(desc, n, dt);
+int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
+                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* tile_sums,
+                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s) {
+  int launches = 0;
+  const uint32_t* gate = nullptr;
+  if (!chain_only && n_tiles > 0) {
+    i128* sums = static_cast<i128*>(tile_sums);
+    cudaMemsetAsync(st, 0, sizeof(MeanState), s);
+    mean_sums_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
+    mean_scan_kernel<<<kDim, 256, 0, s>>>(sums, n_tiles, st);
+    for (int r = 0; r < kMeanRounds; ++r) {
+      mean_walk_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
+      mean_resolve_kernel<<<1, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
+    }
+    mean_finalize_kernel<<<1, kDim, 0, s>>>(st, total, mean_out, acc_out);
+    launches += 3 + 2 * kMeanRounds;
+    gate = &st->need_chain;
+  }
+  mean_chain_kernel<<<kDim / 32, 32, 0, s>>>(imgs, n_imgs, gate, mean_out, acc_out);
+  return launches + 1;
 }
 
 static size_t codes_smem_bytes() {
@@ -1092,32 +1125,13 @@ void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev&, uint
 }
 
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, const uint32_t* gate, cudaStream_t s) {
-  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total, gate);
+                        unsigned long long* running_total, cudaStream_t s) {
+  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total);
 }
 
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
-                    const uint64_t* out_off, int n_pairs, int32_t* out, const uint32_t* gate,
-                    cudaStream_t s) {
-  if (n_pairs > 0) compact_kernel<<<n_pairs, 1024, 0, s>>>(dense, dense_off, nq, out_off, out, gate);
-}
-
-void launch_mean_fast(const ImgDev* imgs, const uint32_t* tile_img, const uint32_t* tile_start,
-                      int n_tiles, double* partial, unsigned long long total, float* mean_out,
-                      cudaStream_t s) {
-  if (n_tiles > 0) mean_partial_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, partial);
-  mean_final_kernel<<<1, 1024, 0, s>>>(partial, n_tiles, total, mean_out);
-}
-
-void launch_mean_check(const float* fast, const float* exact, uint32_t* redo, cudaStream_t s) {
-  mean_check_kernel<<<1, kDim, 0, s>>>(fast, exact, redo);
-}
-
-void launch_gated_clear(void* p, size_t bytes, const uint32_t* gate, cudaStream_t s) {
-  const size_t words = bytes / 4;
-  if (words == 0) return;
-  const int blocks = (int)std::min<size_t>(148 * 4, (words + 255) / 256);
-  gated_clear_kernel<<<blocks, 256, 0, s>>>(static_cast<uint32_t*>(p), words, gate);
+                    const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s) {
+  if (n_pairs > 0) compact_kernel<<<n_pairs, 1024, 0, s>>>(dense, dense_off, nq, out_off, out);
 }
 
 }  // namespace bmg

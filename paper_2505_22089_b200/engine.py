@@ -205,15 +205,15 @@ class ExecuteOptions:
     on_upload: object = None  # DeviceBackend::on_upload(image_id, units)
     on_evict: object = None   # DeviceBackend::on_evict(image_id)
     retain: bool = False      # keep images resident (skip eviction directives)
-    # row-mean speculation: "auto" (rows >= 32768 descriptors), "off", "force",
-    # or "force_redo" (test hook: always take the exact re-do path)
-    speculation: str = "auto"
+    # row means: "exact" (parallel F96 reconstruction, the default) or
+    # "chain" (the literal sequential FP64 chain; a test hook, same results)
+    mean: str = "exact"
 
     def flags(self) -> int:
-        spec = {"auto": 0, "off": 2, "force": 4, "force_redo": 8}
-        if self.speculation not in spec:
-            raise BandmatchError("InvalidArgument", f"unknown speculation mode {self.speculation!r}")
-        return (_lib.EXEC_RETAIN if self.retain else 0) | spec[self.speculation]
+        modes = {"exact": 0, "chain": _lib.EXEC_MEAN_CHAIN}
+        if self.mean not in modes:
+            raise BandmatchError("InvalidArgument", f"unknown mean mode {self.mean!r}")
+        return (_lib.EXEC_RETAIN if self.retain else 0) | modes[self.mean]
 
 
 @dataclass

@@ -267,6 +267,12 @@ class Matcher:
         check(self._L.bmg_fixup_counts(self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def row_mean_info(self):
+        """(rounds, used_chain) of the last computed row mean (diagnostics)."""
+        r, u = C.c_uint32(0), C.c_int(0)
+        check(self._L.bmg_row_mean_info(self.handle, C.byref(r), C.byref(u)))
+        return r.value, bool(u.value)
+
 
 def _codeset_c(cs: HashCodeSet):
     coarse = np.ascontiguousarray(cs.coarse, np.uint32)

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_both(reference, tmp_path, n_images, ppi, band, size_blk, size_gpu, seed=7, k=8,
-             ratio=0.5, speculation="auto"):
+             ratio=0.5, mean="exact"):
     imgs, pairs = reference.generate_synthetic(n_images, ppi, band, 0.02, 0.2, seed)
     plan_path = tmp_path / "plan.json"
     reference.iterate_schedule(np.arange(n_images), pairs, size_blk, size_gpu, plan_path)
@@ -25,7 +25,7 @@ def run_both(reference, tmp_path, n_images, ppi, band, size_blk, size_gpu, seed=
     arena = bm.DeviceArena(cap, hf)
     ups, evs = [], []
     opts = bm.ExecuteOptions(bm.MatchParams(k, ratio), on_upload=lambda i, n: ups.append((i, n)),
-                             on_evict=lambda i: evs.append(i), speculation=speculation)
+                             on_evict=lambda i: evs.append(i), mean=mean)
     res = bm.execute_plan(plan, feats, arena, opts)
     return plan, ref, ref_counters, res, arena, ups, evs, feats
 
@@ -49,14 +49,14 @@ def test_band_block_plan_equals_reference(reference, tmp_path):
     assert sum(it.pairs for it in met.per_iteration) == met.pairs_matched
 
 
-@pytest.mark.parametrize("speculation", ["auto", "off", "force", "force_redo"])
-def test_config2_block_equals_reference(reference, tmp_path, speculation):
+@pytest.mark.parametrize("mean", ["exact", "chain"])
+def test_config2_block_equals_reference(reference, tmp_path, mean):
     # BASELINE config 2 shape at reduced descriptor count: 32 images, band 11,
-    # iterate_schedule(16, 32) -> 2 rows, 286 pairs.  Every row-mean strategy
-    # (exact chain first, parallel speculation + check, forced re-do pass)
-    # must give the reference's lists.
+    # iterate_schedule(16, 32) -> 2 rows, 286 pairs.  Both row-mean paths
+    # (parallel F96 reconstruction, literal FP64 chain) must give the
+    # reference's lists.
     plan, ref, rc, res, *_ = run_both(reference, tmp_path, 32, 1024, 11, 16, 32,
-                                      speculation=speculation)
+                                      mean=mean)
     assert rc["pairs_matched"] == 286
     got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
     for key, m in ref.items():
