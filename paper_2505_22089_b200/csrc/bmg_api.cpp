@@ -508,7 +508,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     // exceed the F96 headroom and take the chain directly)
     const bool chain_only = c.mean_chain_only || total_desc > (1ull << 22) || n_tiles == 0;
     c.last_mean_chain_only = chain_only;
-    c.d_mean_sums.ensure(sizeof(__int128) * kDim * std::max<size_t>(n_tiles, 1));
+    c.d_mean_sums.ensure(mean_scratch_bytes(std::max<size_t>(n_tiles, 1)));
     c.d_mean_state.ensure(sizeof(MeanState));
     Timed t(c, "mean", s);
     c.launches += launch_row_mean(d_imgs, n_imgs, c.d_tiles.as<uint32_t>(),

@@ -79,9 +79,12 @@ constexpr int kMeanRounds = 6;
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
 // parallel reconstruction with the sequential chain as gated fallback, or the
-// chain alone.  tile_sums: 16 * 128 * n_tiles bytes.  Returns kernel launches.
+// chain alone.  scratch: mean_scratch_bytes(n_tiles).  Returns kernel launches.
+inline size_t mean_scratch_bytes(size_t n_tiles) {
+  return n_tiles * (2 * 16 * kDim + 4 * kDim * 128);  // tile sums, event sums, channel-major tiles
+}
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
-                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* tile_sums,
+                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,
                     MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s);
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                   const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,

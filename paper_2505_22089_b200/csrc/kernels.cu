@@ -125,18 +125,41 @@ __device__ __forceinline__ double f96_to_double(i128 v) {
   return v < 0 ? -r : r;
 }
 
+// Tile sums, and the tile re-laid out channel-major (tr[tile][c][0..128)) so
+// every later walk of one channel over one tile is a contiguous 512-byte read.
+constexpr int kHalfTile = kCodesTile / 2;
+
 __global__ void __launch_bounds__(kDim) mean_sums_kernel(const ImgDev* __restrict__ imgs,
                                                          const uint32_t* __restrict__ tile_img,
                                                          const uint32_t* __restrict__ tile_start,
-                                                         i128* __restrict__ tile_sum, MeanState* st) {
-  const int c = threadIdx.x;
+                                                         i128* __restrict__ tile_sum, float* __restrict__ tr,
+                                                         MeanState* st) {
+  __shared__ float sm[kHalfTile][kDim + 1];
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
   const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
   const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
   const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
+  float* out = tr + (size_t)blockIdx.x * kDim * kCodesTile;
   i128 s = 0;
   bool ok = true;
+  for (int h = 0; h * kHalfTile < nd; ++h) {
+    const int rows = min(kHalfTile, nd - h * kHalfTile);
 #pragma unroll 8
-  for (int r = 0; r < nd; ++r) s += to_f96(__ldg(d + (size_t)r * kDim), ok);
+    for (int r = 0; r < rows; ++r) {
+      const float x = __ldg(d + (size_t)(h * kHalfTile + r) * kDim);
+      sm[r][c] = x;
+      s += to_f96(x, ok);
+    }
+    __syncthreads();
+    // warp w writes channels w, w+4, ..: lane l rows 2l, 2l+1 (256 contiguous bytes)
+    for (int ch = warp; ch < kDim; ch += kDim / 32) {
+      if (2 * lane < rows) {
+        const float2 v = make_float2(sm[2 * lane][ch], 2 * lane + 1 < rows ? sm[2 * lane + 1][ch] : 0.f);
+        *reinterpret_cast<float2*>(out + (size_t)ch * kCodesTile + h * kHalfTile + 2 * lane) = v;
+      }
+    }
+    __syncthreads();
+  }
   tile_sum[(size_t)blockIdx.x * kDim + c] = s;
   if (__syncthreads_or(!ok) && c == 0) st->bad = 1u;
 }
@@ -174,10 +197,15 @@ __global__ void __launch_bounds__(256) mean_scan_kernel(i128* __restrict__ tile_
   }
 }
 
+// thread (tile, c): walk channel c through the tile from its exact prefix;
+// the first step >= k_start whose S + delta does not fit a double is
+// reported (atomicMin) with its S recorded for the resolve
 __global__ void __launch_bounds__(kDim) mean_walk_kernel(const ImgDev* __restrict__ imgs,
                                                          const uint32_t* __restrict__ tile_img,
                                                          const uint32_t* __restrict__ tile_start,
-                                                         const i128* __restrict__ prefix, MeanState* st) {
+                                                         const i128* __restrict__ prefix,
+                                                         const float* __restrict__ tr,
+                                                         i128* __restrict__ ev_S, MeanState* st) {
   if (st->done | st->bad) return;
   const int c = threadIdx.x;
   if (!st->pending[c]) return;
@@ -185,35 +213,34 @@ __global__ void __launch_bounds__(kDim) mean_walk_kernel(const ImgDev* __restric
   const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
   const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
   if (p0 + nd <= ks) return;
-  const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
+  const float4* col = reinterpret_cast<const float4*>(tr + ((size_t)blockIdx.x * kDim + c) * kCodesTile);
   i128 S = prefix[(size_t)blockIdx.x * kDim + c];
   const i128 dl = st->delta[c];
   bool ok = true;
-#pragma unroll 4
-  for (int r = 0; r < nd; ++r) {
-    S += to_f96(__ldg(d + (size_t)r * kDim), ok);
-    if (p0 + r >= ks && !fits_double(S + dl)) {
-      atomicMin(&st->first_event[c], p0 + r);
-      break;
+  for (int r = 0; r < nd; r += 4) {
+    const float4 v = __ldg(col + r / 4);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (r + i < nd) {
+        S += to_f96(x[i], ok);
+        if (p0 + r + i >= ks && !fits_double(S + dl)) {
+          ev_S[(size_t)blockIdx.x * kDim + c] = S;
+          atomicMin(&st->first_event[c], p0 + r + i);
+          return;
+        }
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(kDim) mean_resolve_kernel(const ImgDev* __restrict__ imgs,
-                                                            const uint32_t* __restrict__ tile_img,
-                                                            const uint32_t* __restrict__ tile_start,
-                                                            const i128* __restrict__ prefix, MeanState* st) {
+__global__ void __launch_bounds__(kDim) mean_resolve_kernel(const i128* __restrict__ ev_S, MeanState* st) {
   if (st->done | st->bad) return;
   const int c = threadIdx.x;
   const uint32_t p = st->first_event[c];
   const bool ev = p != kNoEvent;
   if (ev) {
-    const uint32_t tile = p / kCodesTile, r = p % kCodesTile;
-    const uint32_t img = tile_img[tile], i0 = tile_start[tile];
-    const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
-    i128 S = prefix[(size_t)tile * kDim + c];
-    bool ok = true;
-    for (uint32_t q = 0; q <= r; ++q) S += to_f96(__ldg(d + (size_t)q * kDim), ok);
+    const i128 S = ev_S[(size_t)(p / kCodesTile) * kDim + c];
     st->delta[c] = round53(S + st->delta[c]) - S;
     st->k_start[c] = p + 1;
     st->first_event[c] = kNoEvent;
@@ -691,18 +718,21 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   uint32_t* tab = s_tab[warp];
   uint32_t n_matched = 0;
 
+  // the next query's bucket ids are loaded one query ahead
+  uint32_t b_next = 0;
+  if (lane < L && w.q_begin + warp < w.q_end) b_next = __ldg(Q.coarse + (size_t)(w.q_begin + warp) * L + lane);
   for (uint32_t q = w.q_begin + warp; q < w.q_end; q += kWarps) {
     // ---- per-query bucket ranges, flattened: table t covers [cum_t, cum_t+sz_t)
+    const uint32_t b = b_next;
+    if (lane < L && q + kWarps < w.q_end) b_next = __ldg(Q.coarse + (size_t)(q + kWarps) * L + lane);
     uint32_t lo = 0, sz = 0;
     if (lane < L) {
-      const uint32_t b = __ldg(Q.coarse + (size_t)q * L + lane);
       const uint32_t* off = T.offsets + (size_t)lane * nb1;
       lo = __ldg(off + b);
       sz = __ldg(off + b + 1) - lo;
     }
     uint32_t incl = sz;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int o = 1; o < L; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, incl, o);
       if (lane >= o) incl += y;
     }
@@ -720,25 +750,31 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     // The flattened union is walked 32 entries per round, lane l taking entry
     // base + l.  Each lane keeps its own cursor (table, end, slot base): a
     // round advances it by 32 entries, i.e. across at most ~1 table boundary.
+    // The slot (train index) of the next round is loaded while the current
+    // round's Hamming distances are computed.
     auto for_each_round = [&](auto&& round) {
       int t = 0;
       uint32_t t_end = tab[1], sbase = tab[kBaseOff];
+      auto slot = [&](uint32_t e) -> uint32_t {
+        if (e >= total) return 0u;
+        if (e >= t_end) {
+          do {
+            ++t;
+            t_end = tab[t + 1];
+          } while (e >= t_end);
+          sbase = tab[kBaseOff + t];
+        }
+        return __ldg(T.slots + (sbase + e));
+      };
+      uint32_t e = lane, j = slot(e);
       for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t e = base + lane;
+        const uint32_t j_next = slot(e + 32);
         const bool valid = e < total;
         uint32_t key = kEmpty;
-        if (valid) {
-          if (e >= t_end) {
-            do {
-              ++t;
-              t_end = tab[t + 1];
-            } while (e >= t_end);
-            sbase = tab[kBaseOff + t];
-          }
-          const uint32_t j = __ldg(T.slots + (sbase + e));
-          key = (hamming<FWP, SMEM>(scodes, T.fine, j, qc) << ib) | j;
-        }
+        if (valid) key = (hamming<FWP, SMEM>(scodes, T.fine, j, qc) << ib) | j;
         round(valid, key);
+        e += 32;
+        j = j_next;
       }
     };
     uint32_t lst = kEmpty;
@@ -1030,18 +1066,20 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
 // launchers
 // ---------------------------------------------------------------------------
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
-                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* tile_sums,
+                    const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,
                     MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s) {
   int launches = 0;
   const uint32_t* gate = nullptr;
   if (!chain_only && n_tiles > 0) {
-    i128* sums = static_cast<i128*>(tile_sums);
+    i128* sums = static_cast<i128*>(scratch);
+    i128* ev_S = sums + (size_t)n_tiles * kDim;
+    float* tr = reinterpret_cast<float*>(ev_S + (size_t)n_tiles * kDim);
     cudaMemsetAsync(st, 0, sizeof(MeanState), s);
-    mean_sums_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
+    mean_sums_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, tr, st);
     mean_scan_kernel<<<kDim, 256, 0, s>>>(sums, n_tiles, st);
     for (int r = 0; r < kMeanRounds; ++r) {
-      mean_walk_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
-      mean_resolve_kernel<<<1, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, st);
+      mean_walk_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, tr, ev_S, st);
+      mean_resolve_kernel<<<1, kDim, 0, s>>>(ev_S, st);
     }
     mean_finalize_kernel<<<1, kDim, 0, s>>>(st, total, mean_out, acc_out);
     launches += 3 + 2 * kMeanRounds;
