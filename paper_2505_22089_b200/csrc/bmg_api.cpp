@@ -169,7 +169,7 @@ struct Timer {
 };
 
 struct RowLayout {
-  size_t coarse_off, fine_off, offsets_off, cursor_off, slots_off;
+  size_t coarse_off, fine_off, offsets_off, cursor_off, slots_off, bfine_off;
 };
 
 // What the codes/tables kernels of the current row need to be (re)issued.
@@ -441,6 +441,8 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     off = align_up(off + L * NB * 4, 256);
     lay[i].slots_off = off;
     off = align_up(off + descs[i].second * L * 4, 256);
+    lay[i].bfine_off = off;
+    off = align_up(off + descs[i].second * L * h.fwp * 8, 256);
   }
   c.d_scratch.ensure(off);
   char* base = c.d_scratch.as<char>();
@@ -454,6 +456,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.offsets = reinterpret_cast<uint32_t*>(base + lay[i].offsets_off);
     im.cursor = reinterpret_cast<uint32_t*>(base + lay[i].cursor_off);
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
+    im.bfine = reinterpret_cast<uint64_t*>(base + lay[i].bfine_off);
     im.overflow = 0;
   }
   // metadata

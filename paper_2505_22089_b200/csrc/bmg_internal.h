@@ -18,6 +18,7 @@ struct ImgDev {
   uint32_t* offsets;   // [tables][n_buckets+1] bucket starts (hashmatch.cpp:125-135)
   uint32_t* cursor;    // [tables][n_buckets]   scatter cursors (scratch)
   uint32_t* slots;     // [tables][n] train indices grouped by bucket (:136-145)
+  uint64_t* bfine;     // [tables][n][fwp] fine codes in slot order (coalesced candidate walk)
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
   uint32_t pad_;

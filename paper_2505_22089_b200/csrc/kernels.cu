@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "bmg_internal.h"
 
@@ -127,41 +128,45 @@ __device__ __forceinline__ double f96_to_double(i128 v) {
 
 // Tile sums, and the tile re-laid out channel-major (tr[tile][c][0..128)) so
 // every later walk of one channel over one tile is a contiguous 512-byte read.
-constexpr int kHalfTile = kCodesTile / 2;
+// 256 threads: thread (h, c) sums rows 64h..64h+63 of channel c.
+constexpr int kSumsThreads = 256;
+constexpr int kSumsStride = kDim + 1;  // smem row stride (conflict-free both ways)
+constexpr size_t kSumsSmem = sizeof(float) * kCodesTile * kSumsStride;
 
-__global__ void __launch_bounds__(kDim) mean_sums_kernel(const ImgDev* __restrict__ imgs,
-                                                         const uint32_t* __restrict__ tile_img,
-                                                         const uint32_t* __restrict__ tile_start,
-                                                         i128* __restrict__ tile_sum, float* __restrict__ tr,
-                                                         MeanState* st) {
-  __shared__ float sm[kHalfTile][kDim + 1];
-  const int c = threadIdx.x, lane = c & 31, warp = c >> 5;
+__global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* __restrict__ imgs,
+                                                                 const uint32_t* __restrict__ tile_img,
+                                                                 const uint32_t* __restrict__ tile_start,
+                                                                 i128* __restrict__ tile_sum,
+                                                                 float* __restrict__ tr, MeanState* st) {
+  extern __shared__ float sm[];  // [128][kSumsStride]
+  __shared__ i128 s_part[kDim];
+  const int c = threadIdx.x & (kDim - 1), h = threadIdx.x >> 7;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
   const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
   const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
-  float* out = tr + (size_t)blockIdx.x * kDim * kCodesTile;
+  const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
   i128 s = 0;
   bool ok = true;
-  for (int h = 0; h * kHalfTile < nd; ++h) {
-    const int rows = min(kHalfTile, nd - h * kHalfTile);
-#pragma unroll 8
-    for (int r = 0; r < rows; ++r) {
-      const float x = __ldg(d + (size_t)(h * kHalfTile + r) * kDim);
-      sm[r][c] = x;
-      s += to_f96(x, ok);
-    }
-    __syncthreads();
-    // warp w writes channels w, w+4, ..: lane l rows 2l, 2l+1 (256 contiguous bytes)
-    for (int ch = warp; ch < kDim; ch += kDim / 32) {
-      if (2 * lane < rows) {
-        const float2 v = make_float2(sm[2 * lane][ch], 2 * lane + 1 < rows ? sm[2 * lane + 1][ch] : 0.f);
-        *reinterpret_cast<float2*>(out + (size_t)ch * kCodesTile + h * kHalfTile + 2 * lane) = v;
-      }
-    }
-    __syncthreads();
+#pragma unroll 16
+  for (int r = r0; r < r1; ++r) {
+    const float x = __ldg(d + (size_t)r * kDim);
+    sm[r * kSumsStride + c] = x;
+    s += to_f96(x, ok);
   }
-  tile_sum[(size_t)blockIdx.x * kDim + c] = s;
-  if (__syncthreads_or(!ok) && c == 0) st->bad = 1u;
+  if (h == 1) s_part[c] = s;
+  const int bad = __syncthreads_or(!ok);
+  if (h == 0) tile_sum[(size_t)blockIdx.x * kDim + c] = s + s_part[c];
+  if (bad && threadIdx.x == 0) st->bad = 1u;
+  // channel-major copy: warp w writes channels w, w+8, ..; 128 B per store
+  float* out = tr + (size_t)blockIdx.x * kDim * kCodesTile;
+  for (int ch = warp; ch < kDim; ch += kSumsThreads / 32) {
+#pragma unroll
+    for (int q = 0; q < kCodesTile / 32; ++q) {
+      const int r = q * 32 + lane;
+      if (r < nd) out[(size_t)ch * kCodesTile + r] = sm[r * kSumsStride + ch];
+    }
+  }
 }
 
 // one CTA per channel: exclusive scan of its tile sums, in place
@@ -217,17 +222,24 @@ __global__ void __launch_bounds__(kDim) mean_walk_kernel(const ImgDev* __restric
   i128 S = prefix[(size_t)blockIdx.x * kDim + c];
   const i128 dl = st->delta[c];
   bool ok = true;
-  for (int r = 0; r < nd; r += 4) {
-    const float4 v = __ldg(col + r / 4);
-    const float x[4] = {v.x, v.y, v.z, v.w};
+  // 64 descriptors per batch: the 16 loads are in flight together
+  for (int r0 = 0; r0 < nd; r0 += 64) {
+    float4 v[16];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (r + i < nd) {
-        S += to_f96(x[i], ok);
-        if (p0 + r + i >= ks && !fits_double(S + dl)) {
-          ev_S[(size_t)blockIdx.x * kDim + c] = S;
-          atomicMin(&st->first_event[c], p0 + r + i);
-          return;
+    for (int i = 0; i < 16; ++i) v[i] = r0 + 4 * i < nd ? __ldg(col + r0 / 4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = r0 + 4 * i + k;
+        if (r < nd) {
+          S += to_f96(x[k], ok);
+          if (p0 + r >= ks && !fits_double(S + dl)) {
+            ev_S[(size_t)blockIdx.x * kDim + c] = S;
+            atomicMin(&st->first_event[c], p0 + r);
+            return;
+          }
         }
       }
     }
@@ -609,7 +621,11 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
   for (int t = 0; t < h.tables; ++t) {
     const uint32_t b = im.coarse[(size_t)i * h.tables + t];
     const uint32_t pos = atomicAdd(im.cursor + (size_t)t * h.n_buckets + b, 1u);
-    im.slots[(size_t)t * im.n + pos] = i;
+    const size_t si = (size_t)t * im.n + pos;
+    im.slots[si] = i;
+    // the fine code again in slot order: the matcher's candidate walk then
+    // reads consecutive entries (coalesced) instead of gathering by index
+    for (int x = 0; x < h.fwp; ++x) im.bfine[si * h.fwp + x] = im.fine[(size_t)i * h.fwp + x];
   }
 }
 
@@ -636,32 +652,43 @@ constexpr int kMaxTables = 32;
 constexpr int kBaseOff = kMaxTables + 2;  // s_tab: cum_t at [0, L+1], slot base_t at kBaseOff + t
 
 
-template <int FWP, bool SMEM>
-__device__ __forceinline__ uint32_t hamming(uint32_t smem_codes,  // shared-window address
-                                            const uint64_t* __restrict__ gcodes, uint32_t j,
-                                            const uint64_t (&qc)[FWP]) {
+// 128-bit (FWP words) Hamming distance against a train code staged in
+// shared memory at index j (the SMEM variant)
+template <int FWP>
+__device__ __forceinline__ uint32_t hamming_smem(uint32_t smem_codes, uint32_t j, const uint64_t (&qc)[FWP]) {
   uint32_t h = 0;
-  if constexpr (SMEM && FWP % 2 == 0) {
-    const uint32_t addr = smem_codes + j * (FWP * 8u);
+  const uint32_t addr = smem_codes + j * (FWP * 8u);
+  if constexpr (FWP % 2 == 0) {
 #pragma unroll
     for (int x = 0; x < FWP / 2; ++x) {
       unsigned long long v0, v1;
       asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "r"(addr + 16u * x));
       h += __popcll(qc[2 * x] ^ v0) + __popcll(qc[2 * x + 1] ^ v1);
     }
-  } else if constexpr (SMEM) {
-    const uint32_t addr = smem_codes + j * (FWP * 8u);
+  } else {
 #pragma unroll
     for (int x = 0; x < FWP; ++x) {
       unsigned long long v;
       asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr + 8u * x));
       h += __popcll(qc[x] ^ v);
     }
-  } else {
-#pragma unroll
-    for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ __ldg(gcodes + (size_t)j * FWP + x));
   }
   return h;
+}
+
+// FWP code words of one bucket-ordered entry (16-byte loads where possible)
+template <int FWP>
+__device__ __forceinline__ void load_code(const uint64_t* __restrict__ p, uint64_t (&c)[FWP]) {
+  if constexpr (FWP % 2 == 0) {
+#pragma unroll
+    for (int x = 0; x < FWP / 2; ++x) {
+      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p) + x);
+      c[2 * x] = v.x;
+      c[2 * x + 1] = v.y;
+    }
+  } else {
+    c[0] = __ldg(p);
+  }
 }
 
 template <int FWP, int KM, int NT, bool SMEM>
@@ -750,13 +777,12 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     // The flattened union is walked 32 entries per round, lane l taking entry
     // base + l.  Each lane keeps its own cursor (table, end, slot base): a
     // round advances it by 32 entries, i.e. across at most ~1 table boundary.
-    // The slot (train index) of the next round is loaded while the current
-    // round's Hamming distances are computed.
+    // The next round's slot (train index) and -- bucket-ordered layout --
+    // its fine code are loaded while the current round is processed.
     auto for_each_round = [&](auto&& round) {
       int t = 0;
       uint32_t t_end = tab[1], sbase = tab[kBaseOff];
-      auto slot = [&](uint32_t e) -> uint32_t {
-        if (e >= total) return 0u;
+      auto locate = [&](uint32_t e) -> uint32_t {  // slot index of entry e < total
         if (e >= t_end) {
           do {
             ++t;
@@ -764,17 +790,44 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           } while (e >= t_end);
           sbase = tab[kBaseOff + t];
         }
-        return __ldg(T.slots + (sbase + e));
+        return sbase + e;
       };
-      uint32_t e = lane, j = slot(e);
+      uint32_t e = lane, j = 0;
+      uint64_t cw[FWP];
+#pragma unroll
+      for (int x = 0; x < FWP; ++x) cw[x] = 0;
+      auto fetch = [&](uint32_t en, uint32_t& jo, uint64_t (&co)[FWP]) {
+        if (en < total) {
+          const uint32_t si = locate(en);
+          jo = __ldg(T.slots + si);
+          if constexpr (!SMEM) load_code<FWP>(T.bfine + (size_t)si * FWP, co);
+        }
+      };
+      fetch(e, j, cw);
       for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t j_next = slot(e + 32);
+        uint32_t jn = 0;
+        uint64_t cn[FWP];
+#pragma unroll
+        for (int x = 0; x < FWP; ++x) cn[x] = 0;
+        fetch(e + 32, jn, cn);
         const bool valid = e < total;
         uint32_t key = kEmpty;
-        if (valid) key = (hamming<FWP, SMEM>(scodes, T.fine, j, qc) << ib) | j;
+        if (valid) {
+          uint32_t h;
+          if constexpr (SMEM) {
+            h = hamming_smem<FWP>(scodes, j, qc);
+          } else {
+            h = 0;
+#pragma unroll
+            for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ cw[x]);
+          }
+          key = (h << ib) | j;
+        }
         round(valid, key);
         e += 32;
-        j = j_next;
+        j = jn;
+#pragma unroll
+        for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
       }
     };
     uint32_t lst = kEmpty;
@@ -1075,7 +1128,12 @@ int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
     i128* ev_S = sums + (size_t)n_tiles * kDim;
     float* tr = reinterpret_cast<float*>(ev_S + (size_t)n_tiles * kDim);
     cudaMemsetAsync(st, 0, sizeof(MeanState), s);
-    mean_sums_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, tr, st);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(mean_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumsSmem);
+      configured = true;
+    }
+    mean_sums_kernel<<<n_tiles, kSumsThreads, kSumsSmem, s>>>(imgs, tile_img, tile_start, sums, tr, st);
     mean_scan_kernel<<<kDim, 256, 0, s>>>(sums, n_tiles, st);
     for (int r = 0; r < kMeanRounds; ++r) {
       mean_walk_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, tr, ev_S, st);
@@ -1139,7 +1197,11 @@ template <int FWP>
 static void launch_match_fw(const MatchLaunch& a, int n_work, uint32_t max_train_n, cudaStream_t s,
                             int* smem_used) {
   const size_t code_bytes = (((size_t)max_train_n * FWP * 8u) + 15u) & ~size_t(15);
-  const bool use_smem = code_bytes <= (size_t)200 * 1024;
+  static const bool smem_env = [] {
+    const char* v = getenv("BMG_MATCH_SMEM");  // A/B switch: stage codes in smem
+    return v && v[0] == '1';
+  }();
+  const bool use_smem = smem_env && code_bytes <= (size_t)200 * 1024;
   const size_t smem = use_smem ? code_bytes : 0;
   if (smem_used) *smem_used = (int)smem;
   if (a.k <= 8) {
