@@ -995,7 +995,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
       const int L = h.tables;
       const size_t NB = h.n_buckets;
       size_t off = 0;
-      size_t co[2], fo[2], oo[2], cu[2], so[2];
+      size_t co[2], fo[2], oo[2], cu[2], so[2], bo[2];
       for (int i = 0; i < 2; ++i) {
         co[i] = off; off = align_up(off + two[i].second * L * 4, 256);
         fo[i] = off; off = align_up(off + align_up(two[i].second, 2) * h.fwp * 8, 256);
@@ -1005,6 +1005,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
       for (int i = 0; i < 2; ++i) {
         cu[i] = off; off = align_up(off + L * NB * 4, 256);
         so[i] = off; off = align_up(off + two[i].second * L * 4, 256);
+        bo[i] = off; off = align_up(off + two[i].second * L * h.fwp * 8, 256);
       }
       c->d_scratch.ensure(off);
       char* base = c->d_scratch.as<char>();
@@ -1018,6 +1019,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
         im.offsets = reinterpret_cast<uint32_t*>(base + oo[i]);
         im.cursor = reinterpret_cast<uint32_t*>(base + cu[i]);
         im.slots = reinterpret_cast<uint32_t*>(base + so[i]);
+        im.bfine = reinterpret_cast<uint64_t*>(base + bo[i]);
         c->row_imgs.push_back(im);
         const uint64_t n = two[i].second;
         for (uint64_t j = 0; j < n * L; ++j)
