@@ -251,7 +251,8 @@ int bmg_kernel_time(bmg_context* ctx, const char* kernel_class, double* total_ms
  * path in the last row / match (diagnostics). */
 int bmg_fixup_counts(bmg_context* ctx, uint64_t* code_bits, uint64_t* rerank_queries);
 /* How the last computed row mean was obtained (diagnostics): `rounds` =
- * walk/resolve rounds the parallel reconstruction ran (rounding steps + 1),
+ * 1 + the largest number of tiles any channel had to walk (tiles the F96
+ * certificate could not clear; every rounding step lies in one of them),
  * `used_chain` = 1 when the sequential FP64 chain produced it (fallback or
  * BMG_EXEC_MEAN_CHAIN). */
 int bmg_row_mean_info(bmg_context* ctx, uint32_t* rounds, int* used_chain);

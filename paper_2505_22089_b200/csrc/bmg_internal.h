@@ -61,28 +61,20 @@ struct MatchLaunch {
   double ratio;
 };
 
-// Device state of the exact parallel row mean (kernels.cu K1): per channel the
-// F96 total, the current rounding offset delta, the first unchecked step and
-// the first non-representable step found by the last walk.
+// Device state of the exact parallel row mean (kernels.cu K1).
 struct MeanState {
   uint32_t bad;         // a descriptor value outside the F96 range
-  uint32_t done;        // the last walk found no rounding step
   uint32_t need_chain;  // gate of the sequential fallback
-  uint32_t rounds;
-  uint32_t pending[kDim];
-  uint32_t k_start[kDim];
-  uint32_t first_event[kDim];
-  alignas(16) __int128 sum[kDim];
-  alignas(16) __int128 delta[kDim];
+  uint32_t rounds;      // max over channels of walked tiles + 1
+  uint32_t events;      // rounding steps replayed (all channels)
 };
-constexpr int kMeanRounds = 6;
 
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
 // parallel reconstruction with the sequential chain as gated fallback, or the
 // chain alone.  scratch: mean_scratch_bytes(n_tiles).  Returns kernel launches.
 inline size_t mean_scratch_bytes(size_t n_tiles) {
-  return n_tiles * (2 * 16 * kDim + 4 * kDim * 128);  // tile sums, event sums, channel-major tiles
+  return n_tiles * kDim * (16 + 32 + 4);  // F96 tile sums, partial-sum ranges, lowest set bits
 }
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
                     const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,

@@ -51,21 +51,25 @@ __device__ __forceinline__ bool gated_off(const uint32_t* gate) {
 // acc_k = RN(acc_{k-1} + x_k); when the exact value acc_{k-1} + x_k fits a
 // binary64 (its F96 bit span is <= 53 bits) the add is exact.  Hence
 // acc_k = S_k + delta, where delta changes only at the steps whose exact sum
-// needs rounding -- about 30 of the 262k x 128 steps of a BASELINE config-2
-// row, at most 2 per channel -- and there delta' = RN(S_k + delta) - S_k.
-//   mean_sums     per 128-descriptor tile: F96 tile sums, range check
-//   mean_scan     per channel: exclusive prefix of the tile sums
-//   mean_walk     per tile: re-walks S_k from the tile prefix and reports each
-//                 channel's first step >= k_start whose S_k + delta does not
-//                 fit a double
-//   mean_resolve  applies that step's rounding (delta, k_start = step + 1)
-// walk/resolve repeat kMeanRounds times (no-ops once a walk found nothing).
-// A row outside the F96 range, or with more rounding steps in one channel
-// than rounds, falls back to mean_chain_kernel, the literal chain.
+// needs rounding ("events", a few per channel in a BASELINE row), and there
+// delta' = RN(S_k + delta) - S_k.
+//   mean_sums     per 128-descriptor tile and channel: the F96 tile sum, the
+//                 range of its partial sums and the lowest set bit of any x
+//   mean_resolve  one CTA per channel: exclusive scan of the tile sums, then
+//                 a tile certificate -- every partial sum of tile t is a
+//                 multiple of 2^low inside [P_t + delta + lo, P_t + delta + hi],
+//                 so its bit span is bounded without walking it.  All tiles
+//                 are certified in parallel against the current delta; the
+//                 first one that is not is walked by one warp (warp scan of
+//                 its 128 steps, every event replayed in order), delta is
+//                 updated and certification resumes after it.
+// A row outside the F96 range, or with more than kMeanMaxWalks uncertified
+// tiles in a channel, falls back to mean_chain_kernel, the literal chain.
 // ---------------------------------------------------------------------------
 using i128 = __int128;
 using u128 = unsigned __int128;
-constexpr uint32_t kNoEvent = 0xffffffffu;
+constexpr uint32_t kNoLow = 0xffffu;          // tile of zeros: adds nothing
+constexpr int kMeanMaxWalks = 1024;
 
 // x * 2^96 as an integer; ok = false when that is not exact or |x| >= 2^8
 __device__ __forceinline__ i128 to_f96(float x, bool& ok) {
@@ -94,13 +98,15 @@ __device__ __forceinline__ int top_bit(u128 a) {  // a != 0
   return hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
 }
 
+__device__ __forceinline__ int low_bit(u128 a) {  // a != 0
+  const uint64_t hi = (uint64_t)(a >> 64), lo = (uint64_t)a;
+  return lo ? __ffsll((long long)lo) - 1 : 63 + __ffsll((long long)hi);
+}
+
 // is the F96 value v exactly representable as a binary64?
 __device__ __forceinline__ bool fits_double(i128 v) {
   const u128 a = abs128(v);
-  const uint64_t hi = (uint64_t)(a >> 64), lo = (uint64_t)a;
-  if ((hi | lo) == 0) return true;
-  const int bot = lo ? __ffsll((long long)lo) - 1 : 63 + __ffsll((long long)hi);
-  return top_bit(a) - bot <= 52;
+  return a == 0 || top_bit(a) - low_bit(a) <= 52;
 }
 
 // round-to-nearest-even of v to 53 significant bits (the FP64 add's rounding)
@@ -117,7 +123,7 @@ __device__ __forceinline__ i128 round53(i128 v) {
   return v < 0 ? -(i128)a : (i128)a;
 }
 
-// v fits a double (checked by the walk): exact conversion
+// v fits a double (checked): exact conversion
 __device__ __forceinline__ double f96_to_double(i128 v) {
   const u128 a = abs128(v);
   const double hi = __ull2double_rn((unsigned long long)(a >> 64));
@@ -126,55 +132,107 @@ __device__ __forceinline__ double f96_to_double(i128 v) {
   return v < 0 ? -r : r;
 }
 
-// Tile sums, and the tile re-laid out channel-major (tr[tile][c][0..128)) so
-// every later walk of one channel over one tile is a contiguous 512-byte read.
-// 256 threads: thread (h, c) sums rows 64h..64h+63 of channel c.
+__device__ __forceinline__ i128 shfl_i128(i128 v, int src) {
+  const uint64_t lo = __shfl_sync(kFull, (unsigned long long)(uint64_t)v, src);
+  const uint64_t hi = __shfl_sync(kFull, (unsigned long long)(uint64_t)((u128)v >> 64), src);
+  return (i128)(((u128)hi << 64) | lo);
+}
+
+__device__ __forceinline__ i128 shfl_up_i128(i128 v, int d) {
+  const uint64_t lo = __shfl_up_sync(kFull, (unsigned long long)(uint64_t)v, d);
+  const uint64_t hi = __shfl_up_sync(kFull, (unsigned long long)(uint64_t)((u128)v >> 64), d);
+  return (i128)(((u128)hi << 64) | lo);
+}
+
+// 256 threads: thread (h, c) covers rows 64h..64h+63 of channel c; row-major
+// loads (512 contiguous bytes per row across the CTA).  Per tile and channel:
+// the F96 sum, the range [lo, hi] of its partial sums (relative to the tile
+// start) and the lowest set F96 bit of any value.
 constexpr int kSumsThreads = 256;
-constexpr int kSumsStride = kDim + 1;  // smem row stride (conflict-free both ways)
-constexpr size_t kSumsSmem = sizeof(float) * kCodesTile * kSumsStride;
+
+struct TileRange {
+  i128 lo, hi;
+};
 
 __global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* __restrict__ imgs,
                                                                  const uint32_t* __restrict__ tile_img,
                                                                  const uint32_t* __restrict__ tile_start,
                                                                  i128* __restrict__ tile_sum,
-                                                                 float* __restrict__ tr, MeanState* st) {
-  extern __shared__ float sm[];  // [128][kSumsStride]
-  __shared__ i128 s_part[kDim];
+                                                                 TileRange* __restrict__ tile_rng,
+                                                                 uint32_t* __restrict__ tile_low, MeanState* st) {
+  __shared__ i128 s_sum[kDim], s_lo[kDim], s_hi[kDim];
+  __shared__ uint32_t s_low[kDim];
   const int c = threadIdx.x & (kDim - 1), h = threadIdx.x >> 7;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
   const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
   const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
   const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
-  i128 s = 0;
+  i128 s = 0, lo = 0, hi = 0;
+  uint32_t low = kNoLow;
   bool ok = true;
 #pragma unroll 16
   for (int r = r0; r < r1; ++r) {
     const float x = __ldg(d + (size_t)r * kDim);
-    sm[r * kSumsStride + c] = x;
     s += to_f96(x, ok);
+    lo = s < lo ? s : lo;
+    hi = s > hi ? s : hi;
+    const uint32_t u = __float_as_uint(x);
+    // lowest set F96 bit: (e - 54) + ctz(mantissa with the implicit bit)
+    const uint32_t lb = (uint32_t)(((u >> 23) & 0xff) - 54 + (__ffs((int)((u & 0x7fffffu) | 0x800000u)) - 1));
+    low = (u & 0x7fffffffu) ? min(low, lb) : low;
   }
-  if (h == 1) s_part[c] = s;
+  if (h == 0) {
+    s_sum[c] = s;
+    s_lo[c] = lo;
+    s_hi[c] = hi;
+    s_low[c] = low;
+  }
   const int bad = __syncthreads_or(!ok);
-  if (h == 0) tile_sum[(size_t)blockIdx.x * kDim + c] = s + s_part[c];
-  if (bad && threadIdx.x == 0) st->bad = 1u;
-  // channel-major copy: warp w writes channels w, w+8, ..; 128 B per store
-  float* out = tr + (size_t)blockIdx.x * kDim * kCodesTile;
-  for (int ch = warp; ch < kDim; ch += kSumsThreads / 32) {
-#pragma unroll
-    for (int q = 0; q < kCodesTile / 32; ++q) {
-      const int r = q * 32 + lane;
-      if (r < nd) out[(size_t)ch * kCodesTile + r] = sm[r * kSumsStride + ch];
-    }
+  if (h == 1) {
+    // second half's partial sums are offset by the first half's total
+    const i128 s0 = s_sum[c], lo0 = s_lo[c], hi0 = s_hi[c];
+    const size_t o = (size_t)blockIdx.x * kDim + c;
+    tile_sum[o] = s0 + s;
+    TileRange rg;
+    rg.lo = (s0 + lo) < lo0 ? (s0 + lo) : lo0;
+    rg.hi = (s0 + hi) > hi0 ? (s0 + hi) : hi0;
+    tile_rng[o] = rg;
+    tile_low[o] = min(low, s_low[c]);
   }
+  if (bad && threadIdx.x == 0) st->bad = 1u;
 }
 
-// one CTA per channel: exclusive scan of its tile sums, in place
-__global__ void __launch_bounds__(256) mean_scan_kernel(i128* __restrict__ tile_sum, int n_tiles,
-                                                        MeanState* st) {
-  __shared__ i128 part[256];
-  const int c = blockIdx.x, tid = threadIdx.x;
-  const int per = (n_tiles + 255) / 256;
+// Certificate for tile t with the accumulator v = P_t + delta at its start:
+// every partial sum v + p_k is a multiple of 2^low and lies in
+// [v + lo, v + hi], so its magnitude is at most the larger end's; no step
+// needs rounding when that bit span is <= 52.
+__device__ __forceinline__ bool tile_certified(i128 v, const TileRange& rg, uint32_t lowx) {
+  if (lowx == kNoLow) return true;  // all zeros: the accumulator stays v
+  const u128 a = abs128(v);
+  int low = (int)lowx;
+  if (a) low = min(low, low_bit(a));
+  const u128 m0 = abs128(v + rg.lo), m1 = abs128(v + rg.hi);
+  const u128 m = m0 > m1 ? m0 : m1;
+  return m == 0 || top_bit(m) - low <= 52;
+}
+
+constexpr int kResolveThreads = 256;
+
+__global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
+    const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
+    const uint32_t* __restrict__ tile_start, i128* __restrict__ tile_sum, const TileRange* __restrict__ tile_rng,
+    const uint32_t* __restrict__ tile_low, int n_tiles, unsigned long long total, MeanState* st,
+    float* __restrict__ mean_out, double* __restrict__ acc_out) {
+  __shared__ i128 part[kResolveThreads];
+  __shared__ i128 s_delta;
+  __shared__ int s_fail;
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  if (*reinterpret_cast<const volatile uint32_t*>(&st->bad)) {
+    if (tid == 0) st->need_chain = 1u;
+    return;
+  }
+  // ---- exclusive scan of the tile sums of channel c (in place)
+  const int per = (n_tiles + kResolveThreads - 1) / kResolveThreads;
   const int t0 = min(n_tiles, tid * per), t1 = min(n_tiles, t0 + per);
   i128 loc = 0;
   for (int t = t0; t < t1; ++t) loc += tile_sum[(size_t)t * kDim + c];
@@ -182,99 +240,96 @@ __global__ void __launch_bounds__(256) mean_scan_kernel(i128* __restrict__ tile_
   __syncthreads();
   if (tid == 0) {
     i128 run = 0;
-    for (int i = 0; i < 256; ++i) {
+    for (int i = 0; i < kResolveThreads; ++i) {
       const i128 v = part[i];
       part[i] = run;
       run += v;
     }
-    st->sum[c] = run;
-    st->delta[c] = 0;
-    st->k_start[c] = 0;
-    st->pending[c] = 1u;
-    st->first_event[c] = kNoEvent;
+    s_delta = run;  // temporarily: the row total
   }
   __syncthreads();
-  i128 run = part[tid];
-  for (int t = t0; t < t1; ++t) {
-    const i128 v = tile_sum[(size_t)t * kDim + c];
-    tile_sum[(size_t)t * kDim + c] = run;
-    run += v;
-  }
-}
-
-// thread (tile, c): walk channel c through the tile from its exact prefix;
-// the first step >= k_start whose S + delta does not fit a double is
-// reported (atomicMin) with its S recorded for the resolve
-__global__ void __launch_bounds__(kDim) mean_walk_kernel(const ImgDev* __restrict__ imgs,
-                                                         const uint32_t* __restrict__ tile_img,
-                                                         const uint32_t* __restrict__ tile_start,
-                                                         const i128* __restrict__ prefix,
-                                                         const float* __restrict__ tr,
-                                                         i128* __restrict__ ev_S, MeanState* st) {
-  if (st->done | st->bad) return;
-  const int c = threadIdx.x;
-  if (!st->pending[c]) return;
-  const uint32_t ks = st->k_start[c], p0 = blockIdx.x * (uint32_t)kCodesTile;
-  const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
-  const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
-  if (p0 + nd <= ks) return;
-  const float4* col = reinterpret_cast<const float4*>(tr + ((size_t)blockIdx.x * kDim + c) * kCodesTile);
-  i128 S = prefix[(size_t)blockIdx.x * kDim + c];
-  const i128 dl = st->delta[c];
-  bool ok = true;
-  // 64 descriptors per batch: the 16 loads are in flight together
-  for (int r0 = 0; r0 < nd; r0 += 64) {
-    float4 v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = r0 + 4 * i < nd ? __ldg(col + r0 / 4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int r = r0 + 4 * i + k;
-        if (r < nd) {
-          S += to_f96(x[k], ok);
-          if (p0 + r >= ks && !fits_double(S + dl)) {
-            ev_S[(size_t)blockIdx.x * kDim + c] = S;
-            atomicMin(&st->first_event[c], p0 + r);
-            return;
-          }
-        }
-      }
+  {
+    i128 run = part[tid];
+    for (int t = t0; t < t1; ++t) {
+      const i128 v = tile_sum[(size_t)t * kDim + c];
+      tile_sum[(size_t)t * kDim + c] = run;
+      run += v;
     }
   }
-}
+  const i128 row_total = s_delta;
+  __syncthreads();
+  if (tid == 0) s_delta = 0;
 
-__global__ void __launch_bounds__(kDim) mean_resolve_kernel(const i128* __restrict__ ev_S, MeanState* st) {
-  if (st->done | st->bad) return;
-  const int c = threadIdx.x;
-  const uint32_t p = st->first_event[c];
-  const bool ev = p != kNoEvent;
-  if (ev) {
-    const i128 S = ev_S[(size_t)(p / kCodesTile) * kDim + c];
-    st->delta[c] = round53(S + st->delta[c]) - S;
-    st->k_start[c] = p + 1;
-    st->first_event[c] = kNoEvent;
+  // ---- certify / walk
+  i128 delta = 0;
+  int cur = 0, walked = 0, events = 0;
+  bool give_up = false;
+  for (;;) {
+    if (tid == 0) s_fail = 0x7fffffff;
+    __syncthreads();
+    for (int t = cur + tid; t < n_tiles; t += kResolveThreads) {
+      const size_t o = (size_t)t * kDim + c;
+      if (!tile_certified(tile_sum[o] + delta, tile_rng[o], tile_low[o])) {
+        atomicMin(&s_fail, t);
+        break;
+      }
+    }
+    __syncthreads();
+    const int f = s_fail;
+    if (f == 0x7fffffff) break;
+    if (walked >= kMeanMaxWalks) {
+      give_up = true;
+      break;
+    }
+    if (tid < 32) {
+      // walk tile f: lane l takes step b + l of each 32-step batch; the warp
+      // scan gives every S_k, the ballot the first step that needs rounding
+      const uint32_t img = tile_img[f], i0 = tile_start[f];
+      const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
+      const float* col = imgs[img].desc + (size_t)i0 * kDim + c;
+      i128 V = tile_sum[(size_t)f * kDim + c];
+      i128 dl = delta;
+      for (int b = 0; b < nd; b += 32) {
+        const int r = b + lane;
+        bool ok = true;
+        const i128 x = r < nd ? to_f96(__ldg(col + (size_t)r * kDim), ok) : (i128)0;
+        i128 incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const i128 y = shfl_up_i128(incl, o);
+          if (lane >= o) incl += y;
+        }
+        const i128 S = V + incl;
+        int start = 0;
+        for (;;) {
+          const bool fail = r < nd && lane >= start && !fits_double(S + dl);
+          const unsigned m = __ballot_sync(kFull, fail);
+          if (!m) break;
+          const int fl = __ffs(m) - 1;
+          dl = shfl_i128(round53(S + dl) - S, fl);
+          start = fl + 1;
+          ++events;
+        }
+        V = shfl_i128(S, 31);
+      }
+      if (tid == 0) s_delta = dl;
+    }
+    __syncthreads();
+    delta = s_delta;
+    cur = f + 1;
+    ++walked;
   }
-  st->pending[c] = ev ? 1u : 0u;
-  const int any = __syncthreads_or(ev);
-  if (c == 0) {
-    st->done = any ? 0u : 1u;
-    ++st->rounds;
+  if (tid == 0) {
+    atomicMax(&st->rounds, (uint32_t)walked + 1u);
+    atomicAdd(&st->events, (uint32_t)events);
+    if (give_up) {
+      st->need_chain = 1u;
+    } else {
+      const double acc = f96_to_double(row_total + delta);
+      mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
+      if (acc_out) acc_out[c] = acc;
+    }
   }
-}
-
-__global__ void __launch_bounds__(kDim) mean_finalize_kernel(MeanState* st, unsigned long long total,
-                                                             float* __restrict__ mean_out,
-                                                             double* __restrict__ acc_out) {
-  const int c = threadIdx.x;
-  const bool chain = st->bad || !st->done;
-  if (c == 0) st->need_chain = chain ? 1u : 0u;
-  if (chain) return;
-  const double acc = f96_to_double(st->sum[c] + st->delta[c]);
-  mean_out[c] = total ? __double2float_rn(__ddiv_rn(acc, (double)total)) : 0.0f;
-  if (acc_out) acc_out[c] = acc;
 }
 
 // The literal chain (fallback and test reference): 4 CTAs x 32 channels, one
@@ -1125,22 +1180,13 @@ int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
   const uint32_t* gate = nullptr;
   if (!chain_only && n_tiles > 0) {
     i128* sums = static_cast<i128*>(scratch);
-    i128* ev_S = sums + (size_t)n_tiles * kDim;
-    float* tr = reinterpret_cast<float*>(ev_S + (size_t)n_tiles * kDim);
+    TileRange* rng = reinterpret_cast<TileRange*>(sums + (size_t)n_tiles * kDim);
+    uint32_t* low = reinterpret_cast<uint32_t*>(rng + (size_t)n_tiles * kDim);
     cudaMemsetAsync(st, 0, sizeof(MeanState), s);
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(mean_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSumsSmem);
-      configured = true;
-    }
-    mean_sums_kernel<<<n_tiles, kSumsThreads, kSumsSmem, s>>>(imgs, tile_img, tile_start, sums, tr, st);
-    mean_scan_kernel<<<kDim, 256, 0, s>>>(sums, n_tiles, st);
-    for (int r = 0; r < kMeanRounds; ++r) {
-      mean_walk_kernel<<<n_tiles, kDim, 0, s>>>(imgs, tile_img, tile_start, sums, tr, ev_S, st);
-      mean_resolve_kernel<<<1, kDim, 0, s>>>(ev_S, st);
-    }
-    mean_finalize_kernel<<<1, kDim, 0, s>>>(st, total, mean_out, acc_out);
-    launches += 3 + 2 * kMeanRounds;
+    mean_sums_kernel<<<n_tiles, kSumsThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, st);
+    mean_resolve_kernel<<<kDim, kResolveThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, n_tiles,
+                                                         total, st, mean_out, acc_out);
+    launches += 2;
     gate = &st->need_chain;
   }
   mean_chain_kernel<<<kDim / 32, 32, 0, s>>>(imgs, n_imgs, gate, mean_out, acc_out);

@@ -40,7 +40,8 @@ def test_bench_scale_row(hf, oracle):
     descs = [f.descriptors for f in imgs[11:]]
     mean, (rounds, chained) = row_mean(hf, descs)
     assert same_bits(mean, oracle.row_mean(descs))
-    assert not chained and 1 <= rounds <= 4  # the row has <= 2 rounding steps per channel
+    # a few uncertified tiles per channel are walked; no fallback
+    assert not chained and 1 <= rounds <= 8
 
 
 @pytest.mark.parametrize("sizes", [(1,), (127, 1, 129), (0, 5, 0, 300), (4096, 4096, 17)])
@@ -63,17 +64,29 @@ def test_rounding_steps_replayed(hf, oracle):
     d[0, 2], d[1, 2], d[2, 2] = 200.0, 2.0 ** -50, -200.0
     mean, (rounds, chained) = row_mean(hf, [d])
     assert same_bits(mean, oracle.row_mean([d]))
-    assert not chained and rounds >= 4
+    assert not chained and rounds >= 2  # the tile was walked
 
 
-@pytest.mark.parametrize("case", ["many_steps", "large_value", "subnormal", "tiny"])
+def test_many_rounding_steps_replayed(hf, oracle):
+    # 39 rounding steps in one tile of channel 5, one step in every tile of
+    # channel 7: all replayed exactly, no fallback
+    rng = np.random.default_rng(2)
+    d = unit_rows(rng, 3000)
+    d[0, 5] = 1.0
+    d[1:40, 5] = 2.0 ** -54
+    d[:, 7] = 0.0
+    d[0, 7] = 1.0
+    d[1::128, 7] = 2.0 ** -54
+    mean, (rounds, chained) = row_mean(hf, [d[:1000], d[1000:]])
+    assert same_bits(mean, oracle.row_mean([d[:1000], d[1000:]]))
+    assert not chained and rounds >= 20
+
+
+@pytest.mark.parametrize("case", ["large_value", "subnormal", "tiny"])
 def test_chain_fallback(hf, oracle, case):
     rng = np.random.default_rng(2)
     d = unit_rows(rng, 3000)
-    if case == "many_steps":
-        d[0, 5] = 1.0
-        d[1:40, 5] = 2.0 ** -54
-    elif case == "large_value":
+    if case == "large_value":
         d[17, 9] = 300.0
     elif case == "subnormal":
         d[2999, 0] = np.float32(1e-40)

@@ -7,7 +7,8 @@ against the oracle in tests/test_gpu_mean.py."""
 import numpy as np
 import pytest
 
-ROUNDS = 6  # kMeanRounds (bmg_internal.h)
+TILE = 128      # kCodesTile: descriptors per tile of the F96 tile sums
+MAX_WALKS = 1024  # kMeanMaxWalks (kernels.cu)
 
 
 def to_f96(x):
@@ -50,20 +51,61 @@ def round53(v):
     return -a if v < 0 else a
 
 
-def model_channel(xs):
-    """Final chain accumulator of one channel (as F96 int), or None = chain fallback."""
+def low_bit(v):
+    return (abs(v) & -abs(v)).bit_length() - 1
+
+
+def certified(v, rng, lowx):
+    """kernels.cu tile_certified: every partial sum of the tile is a multiple
+    of 2^low inside [v + lo, v + hi]."""
+    if lowx is None:
+        return True
+    low = lowx if v == 0 else min(lowx, low_bit(v))
+    m = max(abs(v + rng[0]), abs(v + rng[1]))
+    return m == 0 or m.bit_length() - 1 - low <= 52
+
+
+def partial_range(t):
+    lo = hi = run = 0
+    for v in t:
+        run += v
+        lo, hi = min(lo, run), max(hi, run)
+    return lo, hi
+
+
+def model_channel(xs, tile=TILE, stats=None):
+    """Final chain accumulator of one channel (as F96 int), or None = chain
+    fallback: tile sums -> exclusive prefix -> certify tiles against the
+    current delta -> walk the first uncertified tile, replaying its rounding
+    steps -> resume after it (mean_sums / mean_resolve)."""
     f = [to_f96(x) for x in xs]
     if any(v is None for v in f):
         return None
-    prefix = np.cumsum(np.array(f, dtype=object)) if f else []
-    delta, k_start = 0, 0
-    for _ in range(ROUNDS):
-        event = next((k for k in range(k_start, len(f)) if not fits_double(prefix[k] + delta)), None)
-        if event is None:
-            return (prefix[-1] if len(f) else 0) + delta
-        delta = round53(prefix[event] + delta) - prefix[event]
-        k_start = event + 1
-    return None
+    tiles = [f[i:i + tile] for i in range(0, len(f), tile)]
+    sums = [sum(t) for t in tiles]
+    rngs = [partial_range(t) for t in tiles]
+    lows = [min((low_bit(v) for v in t if v), default=None) for t in tiles]
+    prefix, run = [], 0
+    for s_ in sums:
+        prefix.append(run)
+        run += s_
+    delta, cur, walked = 0, 0, 0
+    while True:
+        fail = next((t for t in range(cur, len(tiles))
+                     if not certified(prefix[t] + delta, rngs[t], lows[t])), None)
+        if fail is None:
+            break
+        if walked >= MAX_WALKS:
+            return None
+        S = prefix[fail]
+        for v in tiles[fail]:
+            S += v
+            if not fits_double(S + delta):
+                delta = round53(S + delta) - S
+        cur, walked = fail + 1, walked + 1
+    if stats is not None:
+        stats["walked"] = walked
+    return run + delta
 
 
 def chain(xs):
@@ -93,7 +135,7 @@ def test_random_unit_descriptor_channels():
 
 def test_rounding_steps_are_replayed():
     # 1.0 then k additions of 2^-54 (each rounds back to 1.0), ties to even
-    for k in range(0, ROUNDS):
+    for k in range(0, 300, 7):
         check([1.0] + [2.0 ** -54] * k)
     check([1.0, 2.0 ** -52, 2.0 ** -53, 3.0, 2.0 ** -53, -4.0, 2.0 ** -60])
     check([1.5, 2.0 ** -53, 2.0 ** -53])          # tie, even stays
@@ -101,8 +143,39 @@ def test_rounding_steps_are_replayed():
     check([200.0, 2.0 ** -50, -200.0, 2.0 ** -50])
 
 
-def test_too_many_rounding_steps_fall_back():
-    check([1.0] + [2.0 ** -54] * (ROUNDS + 3), expect_fallback=True)
+def test_rounding_steps_spread_over_tiles():
+    # events in many tiles: each uncertified tile is walked once
+    xs = []
+    for t in range(40):
+        xs += [1.0 if t == 0 else 0.25] + [2.0 ** -54] * 3 + [0.0] * 124
+    stats = {}
+    check(xs)
+    model_channel(xs, stats=stats)
+    assert stats["walked"] >= 39
+
+
+def test_certificate_skips_clean_tiles():
+    rng = np.random.default_rng(9)
+    xs = (np.round(rng.standard_normal(5000) * 512) / 512).astype(np.float32)
+    stats = {}
+    check(xs)
+    model_channel(xs, stats=stats)
+    assert stats["walked"] == 0
+
+
+def test_small_tiles_match_the_chain():
+    rng = np.random.default_rng(11)
+    xs = (rng.standard_normal(600) * np.exp2(rng.integers(-40, 3, 600))).astype(np.float32)
+    for tile in (1, 3, 32, 128):
+        got = model_channel(xs, tile=tile)
+        assert got is not None and float(got) / 2 ** 96 == chain(xs)
+
+
+def test_too_many_uncertified_tiles_fall_back():
+    xs = []
+    for t in range(MAX_WALKS + 5):
+        xs += [1.0, 2.0 ** -54]
+    assert model_channel(xs, tile=2) is None
 
 
 def test_out_of_range_values_fall_back():

@@ -1,4 +1,5 @@
-mkdir -p gpurun_out/r1c
-timeout 300 compute-sanitizer --tool memcheck --print-limit 5 tests/cpp/_bin/test_reference_binding > gpurun_out/r1c/sanitizer.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/r1c/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/r1c/pytest_gpu.log
-tail -30 gpurun_out/r1c/pytest_gpu.log; tail -30 gpurun_out/r1c/sanitizer.log
+t=${1:-r1d}
+mkdir -p gpurun_out/$t
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/$t/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/$t/pytest_gpu.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/$t/bench.json 2> gpurun_out/$t/bench.err
+tail -15 gpurun_out/$t/pytest_gpu.log; cat gpurun_out/$t/bench.json; tail -3 gpurun_out/$t/bench.err

@@ -1,0 +1,14 @@
+#!/bin/bash
+# Full ncu captures of the hot kernels + a launch list (bench.py workload).
+# usage: gpurun --timeout 1800 -- bash tools/gpu_prof.sh <tag>
+tag=${1:-prof}
+out=gpurun_out/$tag
+mkdir -p $out
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
+for k in match_kernel codes_kernel mean_walk_kernel mean_sums_kernel; do
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 \
+      -o $out/prof_$k $B > $out/ncu_$k.log 2>&1
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $out/ncu_launch.log 2>&1
+ls -la $out

@@ -77,6 +77,7 @@ def main():
     ap.add_argument("--mean")
     ap.add_argument("--codes")
     ap.add_argument("--launches")
+    ap.add_argument("--rep", action="append", default=[], help="key=path.ncu-rep (any kernel)")
     a = ap.parse_args()
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
@@ -85,7 +86,9 @@ def main():
           "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
           "(gpurun), one launch per kernel, bench.py workload (block32, 2 rows). "
           "ncu times are cold-cache and serialised: compare shares, not absolutes.", ""]
-    for key, rep in (("match_kernel", a.match), ("row_mean_tma_kernel", a.mean), ("codes_kernel", a.codes)):
+    reps = [("match_kernel", a.match), ("row_mean_tma_kernel", a.mean), ("codes_kernel", a.codes)]
+    reps += [tuple(r.split("=", 1)) for r in a.rep]
+    for key, rep in reps:
         if not rep:
             continue
         d = raw(Path(rep))
