@@ -573,13 +573,11 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return slot_pairs[x].second < slot_pairs[y].second; });
   size_t n_work = 0;
-  uint32_t max_train_n = 0;
   for (int p = 0; p < n_pairs; ++p) {
     const ImgDev& q = c.row_imgs[slot_pairs[p].first];
     const ImgDev& t = c.row_imgs[slot_pairs[p].second];
     if (t.n > (1u << idx_bits) - 1u) fail(BMG_UNSUPPORTED, "train image too large for the key packing");
     n_work += (q.n + chunk - 1) / chunk;
-    max_train_n = std::max(max_train_n, t.n);
   }
   PairWork* h_work = c.ring.alloc<PairWork>(std::max<size_t>(n_work, 1), c.s_comp, c.s_copy);
   uint64_t* h_dense_off = c.ring.alloc<uint64_t>(n_pairs, c.s_comp, c.s_copy);
@@ -629,7 +627,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   a.ratio = mp.ratio;
   if (n_work) {
     Timed t(c, "match", s);
-    launch_match(a, h.fwp, static_cast<int>(n_work), c.row_imgs[0], max_train_n, s, nullptr);
+    launch_match(a, h.fwp, static_cast<int>(n_work), s);
     ++c.launches;
     check_launch();
   }

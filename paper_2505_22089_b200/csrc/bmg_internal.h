@@ -87,8 +87,7 @@ void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, co
                         unsigned long long* fixed_bits, cudaStream_t s);
 void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                    const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s);
-void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev& any_train_max,
-                  uint32_t max_train_n, cudaStream_t s, int* smem_used);
+void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s);
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
                         unsigned long long* running_total, cudaStream_t s);
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,

@@ -29,10 +29,6 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kEmpty = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 // Gate (uniform across the grid): the kernel is a no-op when *gate == 0 (the
 // chain fallback runs only when the exact parallel mean gave up).
 __device__ __forceinline__ bool gated_off(const uint32_t* gate) {
@@ -686,50 +682,30 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 
 // ---------------------------------------------------------------------------
 // K4: the cascade.  CTA = (image pair, query range); one WARP per query.
-//   1. the train image's fine codes are staged in shared memory by one TMA
-//      bulk copy (cp.async.bulk + mbarrier complete_tx);
-//   2. the query's bucket union over the L tables (hashmatch.cpp:154-169) is
-//      walked as one flattened list, 32 candidates per round (one per lane):
-//      slot load, 128-bit Hamming via POPC, unique key
-//      (hamming << idx_bits | train_idx).  The first round is bitonic-sorted
-//      across the warp; later rounds are filtered with a warp ballot against
-//      the current K-th key and survivors are inserted into a sorted list
-//      distributed over lanes 0..KM-1.  Equal keys are the same train index
-//      reached from two tables and are inserted once -- the reference's
-//      last_seen dedup + stable counting sort by (hamming, idx) (:171-200);
-//   3. re-rank (:196-208): lane l holds dims 4l..4l+3, every kept candidate
-//      row is one coalesced 512-byte load; FP32 squared distances with a
-//      certified relative error <= 8e-6 decide the (dist, idx) argmin and the
-//      ratio test; uncertified queries rerun the reference's sequential FP64
-//      euclidean (:35-42) lane-per-candidate.
+//   1. the query's bucket union over the L tables (hashmatch.cpp:154-169):
+//      table t contributes the bucket range [lo_t, lo_t + sz_t) of the train
+//      image's bucket-ordered slot / fine-code arrays (written by the tables
+//      scatter).  Each range is cut into 8-entry chunks and the warp's four
+//      8-lane groups take four chunks per round, so a lane's entry is
+//      chunk_base + (lane & 7): coalesced 128-byte code loads, no per-lane
+//      table search.  Chunk descriptors are built one per lane (32 per page)
+//      and fetched per round with two shuffles; loads run one round ahead;
+//   2. per candidate: 128-bit Hamming via POPC and the unique key
+//      (hamming << idx_bits | train_idx).  Each lane keeps its 4 smallest
+//      keys (branch-free sorted insert); the warp then pulls the K smallest
+//      out of the lanes' lists with the single-instruction warp min (REDUX).
+//      Equal keys are the same train index reached from several tables and
+//      are taken once -- the reference's last_seen dedup + stable counting
+//      sort by (hamming, idx) (:160-200).  If a lane that saw more than 4
+//      keys runs dry during the pulls, the query reruns on the exact path
+//      (sorted list over lanes 0..KM-1, REDUX-driven insertion);
+//   3. re-rank (:196-208): lanes 4c..4c+3 hold candidate c; FP32 squared
+//      distances (packed FFMA2) with a certified relative error <= 1e-5
+//      decide the (dist, idx) argmin and the ratio test; uncertified queries
+//      rerun the reference's sequential FP64 euclidean (:35-42)
+//      lane-per-candidate.
 // ---------------------------------------------------------------------------
 constexpr int kMaxTables = 32;
-constexpr int kBaseOff = kMaxTables + 2;  // s_tab: cum_t at [0, L+1], slot base_t at kBaseOff + t
-
-
-// 128-bit (FWP words) Hamming distance against a train code staged in
-// shared memory at index j (the SMEM variant)
-template <int FWP>
-__device__ __forceinline__ uint32_t hamming_smem(uint32_t smem_codes, uint32_t j, const uint64_t (&qc)[FWP]) {
-  uint32_t h = 0;
-  const uint32_t addr = smem_codes + j * (FWP * 8u);
-  if constexpr (FWP % 2 == 0) {
-#pragma unroll
-    for (int x = 0; x < FWP / 2; ++x) {
-      unsigned long long v0, v1;
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "r"(addr + 16u * x));
-      h += __popcll(qc[2 * x] ^ v0) + __popcll(qc[2 * x + 1] ^ v1);
-    }
-  } else {
-#pragma unroll
-    for (int x = 0; x < FWP; ++x) {
-      unsigned long long v;
-      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr + 8u * x));
-      h += __popcll(qc[x] ^ v);
-    }
-  }
-  return h;
-}
 
 // FWP code words of one bucket-ordered entry (16-byte loads where possible)
 template <int FWP>
@@ -746,164 +722,120 @@ __device__ __forceinline__ void load_code(const uint64_t* __restrict__ p, uint64
   }
 }
 
-template <int FWP, int KM, int NT, bool SMEM>
+template <int FWP>
+__device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint64_t (&t)[FWP]) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int x = 0; x < FWP; ++x) h += __popcll(q[x] ^ t[x]);
+  return h;
+}
+
+// Walks the union; round(valid, key) is called by every lane once per round
+// (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket
+// range; other lanes hold zeros.
+template <int FWP, typename F>
+__device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, int ib,
+                                           const uint64_t (&qc)[FWP], F&& round) {
+  const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+  const uint32_t nch = (sz + 7u) >> 3;
+  uint32_t cend = nch;  // inclusive scan of the chunk counts over tables
+  for (int o = 1; o < L; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, cend, o);
+    if (lane >= o) cend += y;
+  }
+  const uint32_t n_chunks = __shfl_sync(kFull, cend, L - 1);
+  const uint32_t cstart = cend - nch;
+  const uint32_t sbase = (uint32_t)lane * T.n + lo;
+  for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
+    // lane j describes chunk pg + j: table = #tables ending at or before it
+    const uint32_t k = pg + lane;
+    uint32_t t = 0;
+    for (int tt = 0; tt < L - 1; ++tt) t += __shfl_sync(kFull, cend, tt) <= k ? 1u : 0u;
+    const uint32_t ts = __shfl_sync(kFull, cstart, t);
+    const uint32_t tb = __shfl_sync(kFull, sbase, t);
+    const uint32_t tz = __shfl_sync(kFull, sz, t);
+    const uint32_t o8 = (k - ts) * 8u;
+    const uint32_t my_base = tb + o8;
+    const uint32_t my_len = k < n_chunks ? min(8u, tz - o8) : 0u;
+    const uint32_t nr = (min(32u, n_chunks - pg) + 3u) >> 2;
+    uint32_t base = __shfl_sync(kFull, my_base, grp);
+    bool v = (uint32_t)sub < __shfl_sync(kFull, my_len, grp);
+    uint32_t j = 0;
+    uint64_t cw[FWP];
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) cw[x] = 0;
+    if (v) {
+      j = __ldg(T.slots + base + sub);
+      load_code<FWP>(T.bfine + (size_t)(base + sub) * FWP, cw);
+    }
+    for (uint32_t r = 0; r < nr; ++r) {
+      const int kk = min(4 * (int)(r + 1) + grp, 31);
+      const uint32_t nbase = __shfl_sync(kFull, my_base, kk);
+      const bool nv = r + 1 < nr && (uint32_t)sub < __shfl_sync(kFull, my_len, kk);
+      uint32_t jn = 0;
+      uint64_t cn[FWP];
+#pragma unroll
+      for (int x = 0; x < FWP; ++x) cn[x] = 0;
+      if (nv) {
+        jn = __ldg(T.slots + nbase + sub);
+        load_code<FWP>(T.bfine + (size_t)(nbase + sub) * FWP, cn);
+      }
+      round(v, v ? (hamming<FWP>(qc, cw) << ib) | j : kEmpty);
+      v = nv;
+      j = jn;
+#pragma unroll
+      for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
+    }
+  }
+}
+
+template <int FWP, int KM, int NT>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) unsigned long long s_bar;
-  __shared__ uint32_t s_tab[NT / 32][kBaseOff + kMaxTables];
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = NT / 32;
 
-  if constexpr (SMEM) {
-    const uint32_t bytes = ((T.n * FWP * 8u) + 15u) & ~15u;
-    if (tid == 0) {
-      const uint32_t bar = smem_addr(&s_bar);
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                   : "memory");
-      constexpr uint32_t kChunk = 1u << 15;
-      for (uint32_t off = 0; off < bytes; off += kChunk) {
-        const uint32_t sz = min(kChunk, bytes - off);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_addr(smem_raw + off)),
-            "l"(reinterpret_cast<const char*>(T.fine) + off), "r"(sz), "r"(bar)
-            : "memory");
-      }
-    }
-    __syncthreads();  // mbarrier initialised before anyone waits on it
-    const uint32_t bar = smem_addr(&s_bar);
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(bar)
-          : "memory");
-    }
-  }
-
   const int L = a.tables, K = a.k, ib = a.idx_bits;
-  // pinned in a register (otherwise rematerialised from SR_CgaCtaId per use)
-  uint32_t scodes;
-  asm volatile("mov.u32 %0, %1;" : "=r"(scodes) : "r"(smem_addr(smem_raw)));
   const uint32_t idx_mask = (1u << ib) - 1u;
   const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
   const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
   const double ratio = a.ratio;
   const double r2 = ratio * ratio;
-  uint32_t* tab = s_tab[warp];
   uint32_t n_matched = 0;
 
   // the next query's bucket ids are loaded one query ahead
   uint32_t b_next = 0;
   if (lane < L && w.q_begin + warp < w.q_end) b_next = __ldg(Q.coarse + (size_t)(w.q_begin + warp) * L + lane);
   for (uint32_t q = w.q_begin + warp; q < w.q_end; q += kWarps) {
-    // ---- per-query bucket ranges, flattened: table t covers [cum_t, cum_t+sz_t)
     const uint32_t b = b_next;
     if (lane < L && q + kWarps < w.q_end) b_next = __ldg(Q.coarse + (size_t)(q + kWarps) * L + lane);
     uint32_t lo = 0, sz = 0;
     if (lane < L) {
-      const uint32_t* off = T.offsets + (size_t)lane * nb1;
-      lo = __ldg(off + b);
-      sz = __ldg(off + b + 1) - lo;
+      const uint32_t* off = T.offsets + (size_t)lane * nb1 + b;
+      lo = __ldg(off);
+      sz = __ldg(off + 1) - lo;
     }
-    uint32_t incl = sz;
-    for (int o = 1; o < L; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const uint32_t total = __shfl_sync(kFull, incl, L - 1);
-    if (lane < L) {
-      tab[lane] = incl - sz;                             // cum_t
-      tab[kBaseOff + lane] = lane * T.n + lo - (incl - sz);  // slot base for entry e
-    }
-    if (lane == 0) tab[L] = tab[L + 1] = total;         // sentinels past the last table
-    __syncwarp();
     uint64_t qc[FWP];
 #pragma unroll
     for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
 
-    // The flattened union is walked 32 entries per round, lane l taking entry
-    // base + l.  Each lane keeps its own cursor (table, end, slot base): a
-    // round advances it by 32 entries, i.e. across at most ~1 table boundary.
-    // The next round's slot (train index) and -- bucket-ordered layout --
-    // its fine code are loaded while the current round is processed.
-    auto for_each_round = [&](auto&& round) {
-      int t = 0;
-      uint32_t t_end = tab[1], sbase = tab[kBaseOff];
-      auto locate = [&](uint32_t e) -> uint32_t {  // slot index of entry e < total
-        if (e >= t_end) {
-          do {
-            ++t;
-            t_end = tab[t + 1];
-          } while (e >= t_end);
-          sbase = tab[kBaseOff + t];
-        }
-        return sbase + e;
-      };
-      uint32_t e = lane, j = 0;
-      uint64_t cw[FWP];
-#pragma unroll
-      for (int x = 0; x < FWP; ++x) cw[x] = 0;
-      auto fetch = [&](uint32_t en, uint32_t& jo, uint64_t (&co)[FWP]) {
-        if (en < total) {
-          const uint32_t si = locate(en);
-          jo = __ldg(T.slots + si);
-          if constexpr (!SMEM) load_code<FWP>(T.bfine + (size_t)si * FWP, co);
-        }
-      };
-      fetch(e, j, cw);
-      for (uint32_t base = 0; base < total; base += 32) {
-        uint32_t jn = 0;
-        uint64_t cn[FWP];
-#pragma unroll
-        for (int x = 0; x < FWP; ++x) cn[x] = 0;
-        fetch(e + 32, jn, cn);
-        const bool valid = e < total;
-        uint32_t key = kEmpty;
-        if (valid) {
-          uint32_t h;
-          if constexpr (SMEM) {
-            h = hamming_smem<FWP>(scodes, j, qc);
-          } else {
-            h = 0;
-#pragma unroll
-            for (int x = 0; x < FWP; ++x) h += __popcll(qc[x] ^ cw[x]);
-          }
-          key = (h << ib) | j;
-        }
-        round(valid, key);
-        e += 32;
-        j = jn;
-#pragma unroll
-        for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
-      }
-    };
     uint32_t lst = kEmpty;
     bool exact = KM != 8;
     if constexpr (KM == 8) {
-      // ---- fast path: each lane keeps the 4 smallest keys it sees
-      // (branchless sorted insert), then the warp pulls the K smallest out of
-      // the lanes' lists with the single-instruction warp min (REDUX).
-      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty;
-      for_each_round([&](bool, uint32_t key) {
+      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool valid, uint32_t key) {
         k3 = max(k2, min(k3, key));
         k2 = max(k1, min(k2, key));
         k1 = max(k0, min(k1, key));
         k0 = min(k0, key);
+        seen += valid ? 1u : 0u;
       });
-      // Lane l saw ceil((total - l) / 32) keys: more than 4 means its list
-      // dropped some (all >= its 4th entry).  Copies of one key (a train
-      // index reached from several tables) that landed in one lane sit next
-      // to each other: squeeze them out so a lane's list is a prefix of its
-      // distinct keys.  Copies in different lanes are popped together below.
-      const bool dropped = total > 128u + (uint32_t)lane;
+      // Copies of one key that landed in one lane sit next to each other:
+      // squeeze them out so a lane's list is a prefix of its distinct keys.
+      // Copies in different lanes are popped together below.
       if ((k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty)) {
 #pragma unroll
         for (int rep = 0; rep < 3; ++rep) {
@@ -926,7 +858,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           k3 = pop ? kEmpty : k3;
         }
       }
-      exact = __any_sync(kFull, dropped && k0 == kEmpty);
+      exact = __any_sync(kFull, seen > 4u && k0 == kEmpty);
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
@@ -936,7 +868,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // tables is taken once.
       lst = kEmpty;
       uint32_t thr = kEmpty;
-      for_each_round([&](bool, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
         key = key < thr ? key : kEmpty;
         for (;;) {
           const uint32_t m = __reduce_min_sync(kFull, key);
@@ -964,34 +896,30 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       float s_min, s_2;
       uint32_t i_min;
       if constexpr (KM == 8) {
-        // lanes 4c..4c+3 hold candidate c: lane part p sums the float4s
+        // lanes 4c..4c+3 hold candidate c: lane part p covers the float4s
         // p, p+4, .., p+28 (each load instruction reads 64 contiguous bytes
-        // of every candidate row) in two FMA chains, then two xor-shuffles
-        // complete the sum -- every FP32 sum has depth <= 19, relative
-        // error < 19 * 2^-24 + 3 * 2^-24 (the squared differences) ~ 1.4e-6,
-        // inside the 1e-5 certification margin below.
+        // of every candidate row) in two packed FP32x2 chains; the lane sum
+        // and two xor-shuffles complete it.  Every FP32 sum has depth <= 13:
+        // relative error < (13 + 3) * 2^-24 ~ 1e-6, inside the 1e-5
+        // certification margin below.
         const int ck = lane >> 2, part = lane & 3;
         const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
         float s = 0.f;
         if (ck < kept) {
           const float4* qp = Qd + (size_t)q * 32 + part;
           const float4* tp = Td + (size_t)jk * 32 + part;
-          float s0 = 0.f, s1 = 0.f;
+          const float2 neg1 = make_float2(-1.f, -1.f);
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int i = 0; i < 8; i += 2) {
-            const float4 a0 = __ldg(qp + 4 * i), b0 = __ldg(tp + 4 * i);
-            const float4 a1 = __ldg(qp + 4 * i + 4), b1 = __ldg(tp + 4 * i + 4);
-            float d;
-            d = a0.x - b0.x; s0 = fmaf(d, d, s0);
-            d = a0.y - b0.y; s0 = fmaf(d, d, s0);
-            d = a0.z - b0.z; s0 = fmaf(d, d, s0);
-            d = a0.w - b0.w; s0 = fmaf(d, d, s0);
-            d = a1.x - b1.x; s1 = fmaf(d, d, s1);
-            d = a1.y - b1.y; s1 = fmaf(d, d, s1);
-            d = a1.z - b1.z; s1 = fmaf(d, d, s1);
-            d = a1.w - b1.w; s1 = fmaf(d, d, s1);
+          for (int i = 0; i < 8; ++i) {
+            const float4 av = __ldg(qp + 4 * i), bv = __ldg(tp + 4 * i);
+            // d = a - b exactly rounded (b * -1 + a), then s += d * d
+            const float2 d0 = __ffma2_rn(make_float2(bv.x, bv.y), neg1, make_float2(av.x, av.y));
+            const float2 d1 = __ffma2_rn(make_float2(bv.z, bv.w), neg1, make_float2(av.z, av.w));
+            s0 = __ffma2_rn(d0, d0, s0);
+            s1 = __ffma2_rn(d1, d1, s1);
           }
-          s = s0 + s1;
+          s = (s0.x + s0.y) + (s1.x + s1.y);
         }
         s += __shfl_xor_sync(kFull, s, 1);
         s += __shfl_xor_sync(kFull, s, 2);
@@ -1005,60 +933,60 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         s_min = __uint_as_float(mb);
         s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
       } else {
-      const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
-      float part[KM];
+        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
+        float part[KM];
 #pragma unroll
-      for (int k = 0; k < KM; ++k) {
-        const uint32_t jk = __shfl_sync(kFull, lst, k) & idx_mask;
-        part[k] = 0.f;
-        if (k < kept) {
-          const float4 tv = __ldg(Td + (size_t)jk * 32 + lane);
-          const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
-          part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-        }
-      }
-      // transpose-reduce: after log2(KM) halving steps the lane whose bits
-      // (4, 3, .., 5-log2 KM) spell k holds candidate k's partial sum
-      constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
-#pragma unroll
-      for (int st = 0; st < kLog; ++st) {
-        const int half = (KM >> st) >> 1, m = 16 >> st;
-        const bool up = (lane & m) != 0;
-#pragma unroll
-        for (int i = 0; i < KM / 2; ++i) {
-          if (i < half) {
-            const float send = up ? part[i] : part[i + half];
-            const float keep = up ? part[i + half] : part[i];
-            part[i] = keep + __shfl_xor_sync(kFull, send, m);
+        for (int k = 0; k < KM; ++k) {
+          const uint32_t jk = __shfl_sync(kFull, lst, k) & idx_mask;
+          part[k] = 0.f;
+          if (k < kept) {
+            const float4 tv = __ldg(Td + (size_t)jk * 32 + lane);
+            const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
+            part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
           }
         }
-      }
-      float red = part[0];
+        // transpose-reduce: after log2(KM) halving steps the lane whose bits
+        // (4, 3, .., 5-log2 KM) spell k holds candidate k's partial sum
+        constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
 #pragma unroll
-      for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
-      int src_lane = 0;
+        for (int st = 0; st < kLog; ++st) {
+          const int half = (KM >> st) >> 1, m = 16 >> st;
+          const bool up = (lane & m) != 0;
 #pragma unroll
-      for (int b = 0; b < kLog; ++b)
-        if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
-      const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
-      // argmin of (s, idx) and runner-up value over lanes < kept
-      float bs = mine ? s_own : __int_as_float(0x7f800000);
-      uint32_t bi = mine ? my_idx : 0xffffffffu;
-#pragma unroll
-      for (int o = KM / 2; o > 0; o >>= 1) {
-        const float os = __shfl_xor_sync(kFull, bs, o);
-        const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
-        if (os < bs || (os == bs && oi < bi)) {
-          bs = os;
-          bi = oi;
+          for (int i = 0; i < KM / 2; ++i) {
+            if (i < half) {
+              const float send = up ? part[i] : part[i + half];
+              const float keep = up ? part[i + half] : part[i];
+              part[i] = keep + __shfl_xor_sync(kFull, send, m);
+            }
+          }
         }
-      }
-      s_min = __shfl_sync(kFull, bs, 0);
-      i_min = __shfl_sync(kFull, bi, 0);
-      float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
+        float red = part[0];
 #pragma unroll
-      for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
-      s_2 = __shfl_sync(kFull, s2, 0);
+        for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
+        int src_lane = 0;
+#pragma unroll
+        for (int b = 0; b < kLog; ++b)
+          if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
+        const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
+        // argmin of (s, idx) and runner-up value over lanes < kept
+        float bs = mine ? s_own : __int_as_float(0x7f800000);
+        uint32_t bi = mine ? my_idx : 0xffffffffu;
+#pragma unroll
+        for (int o = KM / 2; o > 0; o >>= 1) {
+          const float os = __shfl_xor_sync(kFull, bs, o);
+          const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
+          if (os < bs || (os == bs && oi < bi)) {
+            bs = os;
+            bi = oi;
+          }
+        }
+        s_min = __shfl_sync(kFull, bs, 0);
+        i_min = __shfl_sync(kFull, bi, 0);
+        float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
+#pragma unroll
+        for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
+        s_2 = __shfl_sync(kFull, s2, 0);
       }
       const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
       const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
@@ -1105,7 +1033,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       a.dense[a.dense_off[w.pair] + q] = result;
       n_matched += result >= 0 ? 1u : 0u;
     }
-    __syncwarp();
   }
   if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
 }
@@ -1228,45 +1155,24 @@ void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* til
   tables_scatter_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
 }
 
-template <int FWP, int KM, int NT, bool SMEM>
-static void launch_match_t(const MatchLaunch& a, int n_work, size_t smem, cudaStream_t s) {
-  static int configured = -1;
-  if (configured != (int)smem) {
-    cudaFuncSetAttribute(match_kernel<FWP, KM, NT, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = (int)smem;
-  }
-  match_kernel<FWP, KM, NT, SMEM><<<n_work, NT, smem, s>>>(a);
+template <int FWP, int KM, int NT>
+static void launch_match_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
+  match_kernel<FWP, KM, NT><<<n_work, NT, 0, s>>>(a);
 }
 
 template <int FWP>
-static void launch_match_fw(const MatchLaunch& a, int n_work, uint32_t max_train_n, cudaStream_t s,
-                            int* smem_used) {
-  const size_t code_bytes = (((size_t)max_train_n * FWP * 8u) + 15u) & ~size_t(15);
-  static const bool smem_env = [] {
-    const char* v = getenv("BMG_MATCH_SMEM");  // A/B switch: stage codes in smem
-    return v && v[0] == '1';
-  }();
-  const bool use_smem = smem_env && code_bytes <= (size_t)200 * 1024;
-  const size_t smem = use_smem ? code_bytes : 0;
-  if (smem_used) *smem_used = (int)smem;
-  if (a.k <= 8) {
-    if (use_smem) launch_match_t<FWP, 8, kMatchThreads, true>(a, n_work, smem, s);
-    else launch_match_t<FWP, 8, kMatchThreads, false>(a, n_work, 0, s);
-  } else {
-    if (use_smem) launch_match_t<FWP, 32, 512, true>(a, n_work, smem, s);
-    else launch_match_t<FWP, 32, 512, false>(a, n_work, 0, s);
-  }
+static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
+  if (a.k <= 8) launch_match_t<FWP, 8, kMatchThreads>(a, n_work, s);
+  else launch_match_t<FWP, 32, 512>(a, n_work, s);
 }
 
-void launch_match(const MatchLaunch& a, int fwp, int n_work, const ImgDev&, uint32_t max_train_n,
-                  cudaStream_t s, int* smem_used) {
+void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
   switch (fwp) {
-    case 1: launch_match_fw<1>(a, n_work, max_train_n, s, smem_used); break;
-    case 2: launch_match_fw<2>(a, n_work, max_train_n, s, smem_used); break;
-    case 4: launch_match_fw<4>(a, n_work, max_train_n, s, smem_used); break;
-    case 8: launch_match_fw<8>(a, n_work, max_train_n, s, smem_used); break;
-    default: launch_match_fw<16>(a, n_work, max_train_n, s, smem_used); break;
+    case 1: launch_match_fw<1>(a, n_work, s); break;
+    case 2: launch_match_fw<2>(a, n_work, s); break;
+    case 4: launch_match_fw<4>(a, n_work, s); break;
+    case 8: launch_match_fw<8>(a, n_work, s); break;
+    default: launch_match_fw<16>(a, n_work, s); break;
   }
 }
 
