@@ -226,6 +226,11 @@ uint64_t bmg_result_pair_count(const bmg_result* r);
 uint64_t bmg_result_match_count(const bmg_result* r);
 /* pair_ids[2*n_pairs], offsets[n_pairs+1], matches[2*n_matches] */
 int bmg_result_copy(const bmg_result* r, uint64_t* pair_ids, uint64_t* offsets, int32_t* matches);
+/* Zero-copy view, valid until bmg_result_free: pair_ids[2*n_pairs] (sorted
+ * by IdPair), ranges[2*n_pairs] = [begin, end) of each pair's matches in
+ * `log`, an int32 (query_idx, train_idx) array in pinned host memory. */
+int bmg_result_view(const bmg_result* r, const uint64_t** pair_ids, const uint64_t** ranges,
+                    const int32_t** log);
 /* PipelineMetrics, engine.hpp:57-78: pairs_matched, initial_matches, uploads,
  * evictions, units_uploaded, peak_occupancy (6 values) + wall seconds */
 int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wall_s_out);

@@ -86,7 +86,7 @@ EXPORTED = [
     "bmg_result_pair_count", "bmg_result_match_count", "bmg_result_copy", "bmg_result_metrics",
     "bmg_result_iteration_count", "bmg_result_iteration", "bmg_result_free", "bmg_launch_count",
     "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_synthetic_counts",
-    "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info",
+    "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
 ]
 
 _lib = None
@@ -127,6 +127,8 @@ def load(path: Path = LIB_PATH):
         "bmg_result_pair_count": (u64, [vp]),
         "bmg_result_match_count": (u64, [vp]),
         "bmg_result_copy": (C.c_int, [vp, vp, vp, vp]),
+        "bmg_result_view": (C.c_int, [vp, C.POINTER(C.POINTER(u64)), C.POINTER(C.POINTER(u64)),
+                                      C.POINTER(C.POINTER(i32))]),
         "bmg_result_metrics": (C.c_int, [vp, vp, C.POINTER(C.c_double)]),
         "bmg_result_iteration_count": (u64, [vp]),
         "bmg_result_iteration": (C.c_int, [vp, u64, vp]),

@@ -16,9 +16,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -135,7 +138,8 @@ struct PinnedRing {
   char* base = nullptr;
   size_t cap = 0, head = 0;
   void init(size_t n) {
-    BMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&base), n));
+    // mapped: the row streams' meta_kernel reads slices straight from here
+    BMG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n, cudaHostAllocMapped | cudaHostAllocPortable));
     cap = n;
   }
   template <typename T>
@@ -161,6 +165,49 @@ struct PinnedRing {
 struct ArenaImage {
   float* d = nullptr;
   uint64_t n = 0;
+  cudaEvent_t ev = nullptr;  // recorded on the copy stream after the H2D
+  uint64_t seq = 0;          // upload order on the copy stream
+};
+
+// Process-wide pool of pinned host buffers that execution results own (the
+// row regions of the result log are DMA'd straight into them; freeing the
+// result returns the buffer).
+class PinnedPool {
+ public:
+  static void* acquire(size_t bytes, size_t* got) {
+    std::lock_guard<std::mutex> g(mu());
+    auto& f = free_list();
+    auto it = f.lower_bound(bytes);
+    if (it != f.end()) {
+      void* p = it->second;
+      *got = it->first;
+      f.erase(it);
+      return p;
+    }
+    const size_t n = align_up(std::max<size_t>(bytes, 1), 1 << 20);
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      fail(BMG_OUT_OF_MEMORY, "pinned result buffer allocation failed");
+    }
+    *got = n;
+    return p;
+  }
+  static void release(void* p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu());
+    free_list().emplace(bytes, p);
+  }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::multimap<size_t, void*>& free_list() {
+    static auto* f = new std::multimap<size_t, void*>();  // leaked at exit on purpose
+    return *f;
+  }
 };
 
 struct Timer {
@@ -185,6 +232,37 @@ struct RowState {
 
 }  // namespace bmg
 
+namespace bmg {
+namespace {
+// Everything one block row needs on the device while it is in flight.
+// bmg_execute_plan alternates two slots so row r+1 (its own stream, scratch
+// and match buffers) overlaps row r; the single-row entry points use slot 0.
+struct RowSlot {
+  cudaStream_t s_comp = nullptr;
+  RowState rs;
+  float* cur_mean = nullptr;
+  // exact parallel row mean: F96 tile sums + state (kernels.cu K1)
+  DevBuf d_mean_sums, d_mean_state;
+  bool last_mean_chain_only = false;
+  std::vector<uint64_t> row_ids;
+  std::unordered_map<uint64_t, int> row_slot;
+  std::vector<ImgDev> row_imgs;
+  bool row_valid = false;
+  DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag;
+  // match state
+  DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq;
+  MetaBatch meta{};  // pending metadata copies / zero fills for s_comp
+  void release() {
+    for (DevBuf* b : {&d_imgs, &d_tiles, &d_scratch, &d_mean, &d_acc, &d_fix, &d_fixcnt, &d_diag, &d_work,
+                      &d_dense, &d_dense_off, &d_pair_count, &d_nq, &d_mean_sums, &d_mean_state})
+      b->release();
+    if (s_comp) cudaStreamDestroy(s_comp);
+    s_comp = nullptr;
+  }
+};
+}  // namespace
+}  // namespace bmg
+
 struct bmg_context {
   int device = 0;
   bmg_hash_params hp{};
@@ -194,13 +272,11 @@ struct bmg_context {
   // arena (DeviceArena, engine.hpp:20-44)
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
-  cudaStream_t s_copy = nullptr, s_comp = nullptr;
-  float* cur_mean = nullptr;
-  bmg::RowState rs;
-  // exact parallel row mean: F96 tile sums + state (kernels.cu K1)
-  bmg::DevBuf d_mean_sums, d_mean_state;
+  cudaStream_t s_copy = nullptr;
+  bmg::RowSlot slot[2];
+  int cur = 0;
+  bmg::RowSlot& S() { return slot[cur]; }
   bool mean_chain_only = false;  // test hook: the literal sequential chain
-  bool last_mean_chain_only = false;
   cudaMemPool_t pool = nullptr;
   cudaEvent_t ev_uploaded = nullptr;
   bool pending_upload = false;
@@ -209,19 +285,9 @@ struct bmg_context {
   int stage_i = 0;
   size_t stage_bytes = 0;
   bmg::PinnedRing ring;
-  // row state
-  std::vector<uint64_t> row_ids;
-  std::unordered_map<uint64_t, int> row_slot;
-  std::vector<bmg::ImgDev> row_imgs;
-  bool row_valid = false;
-  bmg::DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag;
-  // match state
-  bmg::DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq, d_running;
-  // result log and per-pair [begin, end) ranges, written by the compaction
-  // kernels directly into mapped pinned host memory
-  // (the per-pair ranges are tiny: mapped host memory written by the scan
-  // kernel; the log itself is compacted in HBM and read back with one DMA
-  // into pinned memory -- kernel stores across PCIe are ~10x slower)
+  // result log (compacted per row into its own region of d_res) and the
+  // per-pair [begin, end) ranges, written by the scan kernels straight into
+  // mapped pinned host memory
   bmg::HostMapped res_ranges, res_log;
   bmg::DevBuf d_res;
   // temporaries for the stateless entry points
@@ -231,16 +297,21 @@ struct bmg_context {
   bool profiling = false;
   std::vector<bmg::Timer> timers;
   std::vector<cudaEvent_t> free_events;
+  // BMG_TIMELINE diagnostics: labelled events recorded by the row body
+  std::vector<std::pair<std::string, cudaEvent_t>>* marks = nullptr;
 };
 
 struct bmg_result {
-  std::vector<uint64_t> pair_ids;
-  std::vector<uint64_t> offsets;
-  std::vector<int32_t> matches;
+  std::vector<uint64_t> pair_ids;  // (query image, train image) per pair, sorted by IdPair
+  std::vector<uint64_t> ranges;    // [begin, end) of each pair's matches in `log` (entries)
+  int32_t* log = nullptr;          // pinned: (query_idx, train_idx) int32 pairs
+  size_t log_bytes = 0;
+  uint64_t n_matches = 0;
   uint64_t counters[6] = {0, 0, 0, 0, 0, 0};
   std::vector<uint64_t> iterations;  // 3 per iteration
   double wall_s = 0.0;
   double device_ms = 0.0;
+  ~bmg_result() { bmg::PinnedPool::release(log, log_bytes); }
 };
 
 namespace bmg {
@@ -280,6 +351,26 @@ struct Timed {
 };
 
 void set_device(Ctx& c) { BMG_CUDA(cudaSetDevice(c.device)); }
+
+void check_launch();
+
+void meta_flush(Ctx& c) {
+  RowSlot& S = c.S();
+  if (!S.meta.n) return;
+  launch_meta(S.meta, S.s_comp);
+  S.meta.n = 0;
+  ++c.launches;
+  check_launch();
+}
+
+// queue a small copy (src may be mapped pinned host memory) or, with
+// src == nullptr, a zero fill on the current row stream
+void meta_add(Ctx& c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  RowSlot& S = c.S();
+  if (S.meta.n == kMetaOps) meta_flush(c);
+  S.meta.op[S.meta.n++] = MetaOp{dst, src, bytes};
+}
 
 void check_launch() {
   const cudaError_t e = cudaGetLastError();
@@ -327,8 +418,9 @@ void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
   }
 }
 
-void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
-  if (c.resident.count(id)) return;  // engine.cpp:19
+// DeviceArena::upload bookkeeping (engine.cpp:18-25): capacity check,
+// counters and the stream-ordered allocation; the copy is issued separately.
+ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (c.occupancy + n > c.capacity)
     fail(BMG_CAPACITY_EXCEEDED, "uploading image " + std::to_string(id) + " (" + std::to_string(n) +
                                     " units) would raise occupancy to " +
@@ -339,31 +431,58 @@ void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   im.n = n;
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
                            c.s_copy));
-  stage_h2d(c, im.d, desc, n * 512);
-  c.resident.emplace(id, im);
+  ArenaImage& out = c.resident.emplace(id, im).first->second;
   c.occupancy += n;
   c.peak = std::max(c.peak, c.occupancy);
   ++c.uploads;
   c.units_uploaded += n;
+  return out;
+}
+
+uint64_t g_upload_seq = 0;
+
+// The H2D of a reserved image on the copy stream, followed by its event.
+void arena_copy(Ctx& c, ArenaImage& im, const float* desc) {
+  stage_h2d(c, im.d, desc, im.n * 512);
+  if (!im.ev) im.ev = take_event(c);
+  BMG_CUDA(cudaEventRecord(im.ev, c.s_copy));
+  im.seq = ++g_upload_seq;
   c.pending_upload = true;
+}
+
+void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
+  if (c.resident.count(id)) return;  // engine.cpp:19
+  arena_copy(c, arena_reserve(c, id, desc, n), desc);
 }
 
 void arena_evict(Ctx& c, uint64_t id) {
   const auto it = c.resident.find(id);
   if (it == c.resident.end())
     fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
-  // stream-ordered free after every kernel already queued on the compute stream
-  BMG_CUDA(cudaFreeAsync(it->second.d, c.s_comp));
+  // stream-ordered free after every kernel already queued on the compute
+  // streams that may read the image (the current slot's, and the other
+  // slot's row still in flight)
+  RowSlot& S = c.S();
+  RowSlot& O = c.slot[c.cur ^ 1];
+  if (O.s_comp) {
+    cudaEvent_t e = take_event(c);
+    BMG_CUDA(cudaEventRecord(e, O.s_comp));
+    BMG_CUDA(cudaStreamWaitEvent(S.s_comp, e, 0));
+    c.free_events.push_back(e);
+  }
+  BMG_CUDA(cudaFreeAsync(it->second.d, S.s_comp));
+  if (it->second.ev) c.free_events.push_back(it->second.ev);
   c.occupancy -= it->second.n;
   c.resident.erase(it);
   ++c.evictions;
-  if (c.row_slot.count(id)) c.row_valid = false;
+  if (S.row_slot.count(id)) S.row_valid = false;
+  if (O.row_slot.count(id)) O.row_valid = false;
 }
 
 void join_uploads(Ctx& c) {
   if (!c.pending_upload) return;
   BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
-  BMG_CUDA(cudaStreamWaitEvent(c.s_comp, c.ev_uploaded, 0));
+  BMG_CUDA(cudaStreamWaitEvent(c.S().s_comp, c.ev_uploaded, 0));
   c.pending_upload = false;
 }
 
@@ -372,29 +491,33 @@ void join_uploads(Ctx& c) {
 // Codes (+ FP64 fixups) and bucket tables for the current row views, centred
 // on `d_mean`.
 void enqueue_codes_tables(Ctx& c, const float* d_mean) {
-  const RowState& rs = c.rs;
-  if (rs.n_tiles == 0) return;
-  cudaStream_t s = c.s_comp;
+  const RowState& rs = c.S().rs;
+  if (rs.n_tiles == 0) {
+    meta_flush(c);
+    return;
+  }
+  cudaStream_t s = c.S().s_comp;
   const HashDev& h = c.hd;
-  char* base = c.d_scratch.as<char>();
+  char* base = c.S().d_scratch.as<char>();
   const int plane_chunks = (h.n_planes + kPlaneChunk - 1) / kPlaneChunk;
-  BMG_CUDA(cudaMemsetAsync(base + rs.offsets_begin, 0, rs.offsets_bytes, s));
-  if (plane_chunks > 1) BMG_CUDA(cudaMemsetAsync(base, 0, rs.codes_bytes, s));
-  BMG_CUDA(cudaMemsetAsync(c.d_fixcnt.p, 0, sizeof(uint32_t) * (1 + rs.n_imgs), s));
-  const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
-  const uint32_t* d_tile_img = c.d_tiles.as<uint32_t>();
+  meta_add(c, base + rs.offsets_begin, nullptr, rs.offsets_bytes);
+  if (plane_chunks > 1) meta_add(c, base, nullptr, rs.codes_bytes);
+  meta_add(c, c.S().d_fixcnt.p, nullptr, sizeof(uint32_t) * (1 + rs.n_imgs));
+  meta_flush(c);
+  const ImgDev* d_imgs = c.S().d_imgs.as<ImgDev>();
+  const uint32_t* d_tile_img = c.S().d_tiles.as<uint32_t>();
   const uint32_t* d_tile_start = d_tile_img + rs.n_tiles;
-  unsigned long long* diag = c.d_diag.as<unsigned long long>();
+  unsigned long long* diag = c.S().d_diag.as<unsigned long long>();
   {
     Timed t(c, "codes", s);
     launch_codes(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), d_mean,
-                 c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(), rs.fix_cap, s);
+                 c.S().d_fix.as<Fixup>(), c.S().d_fixcnt.as<uint32_t>(), rs.fix_cap, s);
     ++c.launches;
     check_launch();
   }
   {
     Timed t(c, "fixup", s);
-    launch_codes_fixup(h, d_imgs, rs.n_imgs, d_mean, c.d_fix.as<Fixup>(), c.d_fixcnt.as<uint32_t>(),
+    launch_codes_fixup(h, d_imgs, rs.n_imgs, d_mean, c.S().d_fix.as<Fixup>(), c.S().d_fixcnt.as<uint32_t>(),
                        rs.fix_cap, diag, s);
     c.launches += 2;
     check_launch();
@@ -444,11 +567,11 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     lay[i].bfine_off = off;
     off = align_up(off + descs[i].second * L * h.fwp * 8, 256);
   }
-  c.d_scratch.ensure(off);
-  char* base = c.d_scratch.as<char>();
-  c.row_imgs.assign(n_imgs, ImgDev{});
+  c.S().d_scratch.ensure(off);
+  char* base = c.S().d_scratch.as<char>();
+  c.S().row_imgs.assign(n_imgs, ImgDev{});
   for (int i = 0; i < n_imgs; ++i) {
-    ImgDev& im = c.row_imgs[i];
+    ImgDev& im = c.S().row_imgs[i];
     im.desc = descs[i].first;
     im.n = static_cast<uint32_t>(descs[i].second);
     im.coarse = reinterpret_cast<uint32_t*>(base + lay[i].coarse_off);
@@ -460,9 +583,9 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.overflow = 0;
   }
   // metadata
-  ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.s_comp, c.s_copy);
-  std::memcpy(h_imgs, c.row_imgs.data(), sizeof(ImgDev) * n_imgs);
-  uint32_t* h_tiles = c.ring.alloc<uint32_t>(2 * std::max<size_t>(n_tiles, 1), c.s_comp, c.s_copy);
+  ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.S().s_comp, c.s_copy);
+  std::memcpy(h_imgs, c.S().row_imgs.data(), sizeof(ImgDev) * n_imgs);
+  uint32_t* h_tiles = c.ring.alloc<uint32_t>(2 * std::max<size_t>(n_tiles, 1), c.S().s_comp, c.s_copy);
   {
     size_t t = 0;
     for (int i = 0; i < n_imgs; ++i)
@@ -472,21 +595,20 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
         ++t;
       }
   }
-  c.d_imgs.ensure(sizeof(ImgDev) * std::max(n_imgs, 1));
-  c.d_tiles.ensure(sizeof(uint32_t) * 2 * std::max<size_t>(n_tiles, 1));
-  c.d_mean.ensure(sizeof(float) * kDim);
-  c.d_acc.ensure(sizeof(double) * kDim);
+  c.S().d_imgs.ensure(sizeof(ImgDev) * std::max(n_imgs, 1));
+  c.S().d_tiles.ensure(sizeof(uint32_t) * 2 * std::max<size_t>(n_tiles, 1));
+  c.S().d_mean.ensure(sizeof(float) * kDim);
+  c.S().d_acc.ensure(sizeof(double) * kDim);
   const uint32_t fix_cap = static_cast<uint32_t>(std::max<size_t>(65536, total_desc / 4));
-  c.d_fix.ensure(sizeof(Fixup) * fix_cap);
-  c.d_fixcnt.ensure(sizeof(uint32_t) * (1 + std::max(n_imgs, 1)));
-  c.d_diag.ensure(sizeof(unsigned long long) * 4);
-  cudaStream_t s = c.s_comp;
-  BMG_CUDA(cudaMemcpyAsync(c.d_imgs.p, h_imgs, sizeof(ImgDev) * n_imgs, cudaMemcpyHostToDevice, s));
-  if (n_tiles)
-    BMG_CUDA(cudaMemcpyAsync(c.d_tiles.p, h_tiles, sizeof(uint32_t) * 2 * n_tiles,
-                             cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemsetAsync(c.d_diag.p, 0, sizeof(unsigned long long) * 4, s));
-  RowState& rs = c.rs;
+  c.S().d_fix.ensure(sizeof(Fixup) * fix_cap);
+  c.S().d_fixcnt.ensure(sizeof(uint32_t) * (1 + std::max(n_imgs, 1)));
+  c.S().d_diag.ensure(sizeof(unsigned long long) * 4);
+  cudaStream_t s = c.S().s_comp;
+  (void)s;
+  meta_add(c, c.S().d_imgs.p, h_imgs, sizeof(ImgDev) * n_imgs);
+  meta_add(c, c.S().d_tiles.p, h_tiles, sizeof(uint32_t) * 2 * n_tiles);
+  meta_add(c, c.S().d_diag.p, nullptr, sizeof(unsigned long long) * 4);
+  RowState& rs = c.S().rs;
   rs.n_imgs = n_imgs;
   rs.n_tiles = n_tiles;
   rs.fix_cap = fix_cap;
@@ -496,29 +618,37 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   rs.offsets_bytes = offsets_end - codes_end;
   join_uploads(c);
 
-  const ImgDev* d_imgs = c.d_imgs.as<ImgDev>();
-  float* d_mean = c.d_mean.as<float>();
-  c.cur_mean = d_mean;
+  const ImgDev* d_imgs = c.S().d_imgs.as<ImgDev>();
+  float* d_mean = c.S().d_mean.as<float>();
+  c.S().cur_mean = d_mean;
   if (mean_dev) {
-    BMG_CUDA(cudaMemcpyAsync(d_mean, mean_dev, sizeof(float) * kDim, cudaMemcpyDeviceToDevice, s));
+    meta_add(c, d_mean, mean_dev, sizeof(float) * kDim);
   } else if (mean_host) {
-    float* hm = c.ring.alloc<float>(kDim, c.s_comp, c.s_copy);
+    float* hm = c.ring.alloc<float>(kDim, c.S().s_comp, c.s_copy);
     std::memcpy(hm, mean_host, sizeof(float) * kDim);
-    BMG_CUDA(cudaMemcpyAsync(d_mean, hm, sizeof(float) * kDim, cudaMemcpyHostToDevice, s));
+    meta_add(c, d_mean, hm, sizeof(float) * kDim);
   } else if (compute_mean) {
     // exact row mean (engine.cpp:446-461): F96 reconstruction of the FP64
     // chain, the chain itself only as fallback (rows over 2^22 descriptors
     // exceed the F96 headroom and take the chain directly)
     const bool chain_only = c.mean_chain_only || total_desc > (1ull << 22) || n_tiles == 0;
-    c.last_mean_chain_only = chain_only;
-    c.d_mean_sums.ensure(mean_scratch_bytes(std::max<size_t>(n_tiles, 1)));
-    c.d_mean_state.ensure(sizeof(MeanState));
+    c.S().last_mean_chain_only = chain_only;
+    c.S().d_mean_sums.ensure(mean_scratch_bytes(std::max<size_t>(n_tiles, 1)));
+    c.S().d_mean_state.ensure(sizeof(MeanState));
+    meta_add(c, c.S().d_mean_state.p, nullptr, sizeof(MeanState));
+    meta_flush(c);
     Timed t(c, "mean", s);
-    c.launches += launch_row_mean(d_imgs, n_imgs, c.d_tiles.as<uint32_t>(),
-                                  c.d_tiles.as<uint32_t>() + n_tiles, static_cast<int>(n_tiles),
-                                  total_desc, c.d_mean_sums.p, c.d_mean_state.as<MeanState>(), d_mean,
-                                  c.d_acc.as<double>(), chain_only, s);
+    c.launches += launch_row_mean(d_imgs, n_imgs, c.S().d_tiles.as<uint32_t>(),
+                                  c.S().d_tiles.as<uint32_t>() + n_tiles, static_cast<int>(n_tiles),
+                                  total_desc, c.S().d_mean_sums.p, c.S().d_mean_state.as<MeanState>(), d_mean,
+                                  c.S().d_acc.as<double>(), chain_only, s);
     check_launch();
+  }
+  if (c.marks) {
+    cudaEvent_t e;
+    BMG_CUDA(cudaEventCreate(&e));
+    BMG_CUDA(cudaEventRecord(e, s));
+    c.marks->emplace_back("  mean done", e);
   }
   enqueue_codes_tables(c, d_mean);
 }
@@ -526,8 +656,8 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
 void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
   std::vector<std::pair<const float*, uint64_t>> descs;
   descs.reserve(n);
-  c.row_ids.assign(ids, ids + n);
-  c.row_slot.clear();
+  c.S().row_ids.assign(ids, ids + n);
+  c.S().row_slot.clear();
   for (uint64_t i = 0; i < n; ++i) {
     if (i && ids[i] <= ids[i - 1])
       fail(BMG_INVALID_ARGUMENT, "needed image ids must be strictly ascending");
@@ -535,11 +665,11 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
     descs.emplace_back(it->second.d, it->second.n);
-    c.row_slot[ids[i]] = static_cast<int>(i);
+    c.S().row_slot[ids[i]] = static_cast<int>(i);
   }
-  c.row_valid = false;
+  c.S().row_valid = false;
   prepare_row_views(c, descs, mean_host, nullptr, true);
-  c.row_valid = true;
+  c.S().row_valid = true;
 }
 
 // ---- matching ---------------------------------------------------------------
@@ -555,10 +685,10 @@ void check_match_params(const Ctx& c, const bmg_match_params& mp) {
 }
 
 // Enqueues match + scan + compact for (query slot, train slot) pairs of the
-// current row views.  Offsets (absolute positions in d_res) go to
-// out_off[0..n_pairs], appended after *d_running.
+// current row views.  Pair i's matches land in d_res at the [begin, end)
+// written to out_off[2i], out_off[2i+1]; the launch packs them from `base`.
 void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
-                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res) {
+                   const bmg_match_params& mp, uint64_t* out_off, int32_t* d_res, uint64_t base) {
   check_match_params(c, mp);
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
@@ -574,18 +704,18 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
                    [&](int x, int y) { return slot_pairs[x].second < slot_pairs[y].second; });
   size_t n_work = 0;
   for (int p = 0; p < n_pairs; ++p) {
-    const ImgDev& q = c.row_imgs[slot_pairs[p].first];
-    const ImgDev& t = c.row_imgs[slot_pairs[p].second];
+    const ImgDev& q = c.S().row_imgs[slot_pairs[p].first];
+    const ImgDev& t = c.S().row_imgs[slot_pairs[p].second];
     if (t.n > (1u << idx_bits) - 1u) fail(BMG_UNSUPPORTED, "train image too large for the key packing");
     n_work += (q.n + chunk - 1) / chunk;
   }
-  PairWork* h_work = c.ring.alloc<PairWork>(std::max<size_t>(n_work, 1), c.s_comp, c.s_copy);
-  uint64_t* h_dense_off = c.ring.alloc<uint64_t>(n_pairs, c.s_comp, c.s_copy);
-  uint32_t* h_nq = c.ring.alloc<uint32_t>(n_pairs, c.s_comp, c.s_copy);
+  PairWork* h_work = c.ring.alloc<PairWork>(std::max<size_t>(n_work, 1), c.S().s_comp, c.s_copy);
+  uint64_t* h_dense_off = c.ring.alloc<uint64_t>(n_pairs, c.S().s_comp, c.s_copy);
+  uint32_t* h_nq = c.ring.alloc<uint32_t>(n_pairs, c.S().s_comp, c.s_copy);
   uint64_t dense_total = 0;
   for (int p = 0; p < n_pairs; ++p) {
     h_dense_off[p] = dense_total;
-    h_nq[p] = c.row_imgs[slot_pairs[p].first].n;
+    h_nq[p] = c.S().row_imgs[slot_pairs[p].first].n;
     dense_total += h_nq[p];
   }
   size_t w = 0;
@@ -601,25 +731,24 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
       pw.pair = static_cast<uint32_t>(p);
     }
   }
-  c.d_work.ensure(sizeof(PairWork) * std::max<size_t>(n_work, 1));
-  c.d_dense_off.ensure(sizeof(uint64_t) * n_pairs);
-  c.d_nq.ensure(sizeof(uint32_t) * n_pairs);
-  c.d_pair_count.ensure(sizeof(uint32_t) * n_pairs);
-  c.d_dense.ensure(sizeof(int32_t) * std::max<uint64_t>(dense_total, 1));
-  cudaStream_t s = c.s_comp;
-  if (n_work)
-    BMG_CUDA(cudaMemcpyAsync(c.d_work.p, h_work, sizeof(PairWork) * n_work, cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemcpyAsync(c.d_dense_off.p, h_dense_off, sizeof(uint64_t) * n_pairs,
-                           cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemcpyAsync(c.d_nq.p, h_nq, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, s));
-  BMG_CUDA(cudaMemsetAsync(c.d_pair_count.p, 0, sizeof(uint32_t) * n_pairs, s));
+  c.S().d_work.ensure(sizeof(PairWork) * std::max<size_t>(n_work, 1));
+  c.S().d_dense_off.ensure(sizeof(uint64_t) * n_pairs);
+  c.S().d_nq.ensure(sizeof(uint32_t) * n_pairs);
+  c.S().d_pair_count.ensure(sizeof(uint32_t) * n_pairs);
+  c.S().d_dense.ensure(sizeof(int32_t) * std::max<uint64_t>(dense_total, 1));
+  cudaStream_t s = c.S().s_comp;
+  meta_add(c, c.S().d_work.p, h_work, sizeof(PairWork) * n_work);
+  meta_add(c, c.S().d_dense_off.p, h_dense_off, sizeof(uint64_t) * n_pairs);
+  meta_add(c, c.S().d_nq.p, h_nq, sizeof(uint32_t) * n_pairs);
+  meta_add(c, c.S().d_pair_count.p, nullptr, sizeof(uint32_t) * n_pairs);
+  meta_flush(c);
   MatchLaunch a{};
-  a.imgs = c.d_imgs.as<ImgDev>();
-  a.work = c.d_work.as<PairWork>();
-  a.dense_off = c.d_dense_off.as<uint64_t>();
-  a.dense = c.d_dense.as<int32_t>();
-  a.pair_count = c.d_pair_count.as<uint32_t>();
-  a.exact_queries = c.d_diag.as<unsigned long long>() + 1;
+  a.imgs = c.S().d_imgs.as<ImgDev>();
+  a.work = c.S().d_work.as<PairWork>();
+  a.dense_off = c.S().d_dense_off.as<uint64_t>();
+  a.dense = c.S().d_dense.as<int32_t>();
+  a.pair_count = c.S().d_pair_count.as<uint32_t>();
+  a.exact_queries = c.S().d_diag.as<unsigned long long>() + 1;
   a.tables = h.tables;
   a.n_buckets = h.n_buckets;
   a.k = mp.k_nearest;
@@ -633,9 +762,8 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   }
   {
     Timed t(c, "compact", s);
-    launch_scan_counts(c.d_pair_count.as<uint32_t>(), n_pairs, out_off,
-                       c.d_running.as<unsigned long long>(), s);
-    launch_compact(c.d_dense.as<int32_t>(), c.d_dense_off.as<uint64_t>(), c.d_nq.as<uint32_t>(),
+    launch_scan_counts(c.S().d_pair_count.as<uint32_t>(), n_pairs, out_off, base, s);
+    launch_compact(c.S().d_dense.as<int32_t>(), c.S().d_dense_off.as<uint64_t>(), c.S().d_nq.as<uint32_t>(),
                    out_off, n_pairs, d_res, s);
     c.launches += 2;
     check_launch();
@@ -685,25 +813,23 @@ void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fi
   const size_t n = im.n;
   if (coarse_out && n)
     BMG_CUDA(cudaMemcpyAsync(coarse_out, im.coarse, n * h.tables * sizeof(uint32_t),
-                             cudaMemcpyDeviceToHost, c.s_comp));
+                             cudaMemcpyDeviceToHost, c.S().s_comp));
   if (fine_out && n) {
     if (h.fw == h.fwp) {
       BMG_CUDA(cudaMemcpyAsync(fine_out, im.fine, n * h.fw * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                               c.s_comp));
+                               c.S().s_comp));
     } else {
       BMG_CUDA(cudaMemcpy2DAsync(fine_out, h.fw * sizeof(uint64_t), im.fine, h.fwp * sizeof(uint64_t),
-                                 h.fw * sizeof(uint64_t), n, cudaMemcpyDeviceToHost, c.s_comp));
+                                 h.fw * sizeof(uint64_t), n, cudaMemcpyDeviceToHost, c.S().s_comp));
     }
   }
-  BMG_CUDA(cudaStreamSynchronize(c.s_comp));
+  BMG_CUDA(cudaStreamSynchronize(c.S().s_comp));
 }
 
 void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
   c.res_ranges.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
   c.res_log.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
   c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
-  c.d_running.ensure(sizeof(unsigned long long));
-  BMG_CUDA(cudaMemsetAsync(c.d_running.p, 0, sizeof(unsigned long long), c.s_comp));
 }
 
 // After the compute stream drained: DMA the log entries [0, end) into the
@@ -776,7 +902,7 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     c->seed = cfg->function_seed;
     c->capacity = cfg->capacity_units;
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
-    BMG_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamCreateWithFlags(&sl.s_comp, cudaStreamNonBlocking));
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
@@ -798,14 +924,15 @@ int bmg_destroy(bmg_context* c) {
   return guarded([&] {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    for (auto& [id, im] : c->resident) cudaFree(im.d);
+    for (auto& [id, im] : c->resident) {
+      cudaFree(im.d);
+      if (im.ev) cudaEventDestroy(im.ev);
+      im.ev = nullptr;
+    }
     c->resident.clear();
-    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_imgs, &c->d_tiles,
-                      &c->d_scratch, &c->d_mean, &c->d_acc, &c->d_fix, &c->d_fixcnt, &c->d_diag,
-                      &c->d_work, &c->d_dense, &c->d_dense_off, &c->d_pair_count, &c->d_nq,
-                      &c->d_running, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_mean_sums,
-                      &c->d_mean_state})
+    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_tmp_desc, &c->d_tmp_codes})
       b->release();
+    for (RowSlot& sl : c->slot) sl.release();
     c->res_ranges.release();
     c->res_log.release();
     c->d_res.release();
@@ -821,7 +948,6 @@ int bmg_destroy(bmg_context* c) {
     for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
     if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
-    if (c->s_comp) cudaStreamDestroy(c->s_comp);
     delete c;
   });
 }
@@ -831,7 +957,7 @@ int bmg_synchronize(bmg_context* c) {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
   });
 }
 
@@ -877,21 +1003,21 @@ int bmg_row(bmg_context* c, const uint64_t* needed, uint64_t n, const float* mea
 int bmg_row_mean(bmg_context* c, float* mean_out) {
   return guarded([&] {
     if (!c || !mean_out) fail(BMG_INVALID_ARGUMENT, "null argument");
-    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    if (!c->S().row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
     set_device(*c);
-    BMG_CUDA(cudaMemcpyAsync(mean_out, c->cur_mean, sizeof(float) * kDim, cudaMemcpyDeviceToHost, c->s_comp));
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    BMG_CUDA(cudaMemcpyAsync(mean_out, c->S().cur_mean, sizeof(float) * kDim, cudaMemcpyDeviceToHost, c->S().s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
   });
 }
 
 int bmg_codes(bmg_context* c, uint64_t id, uint32_t* coarse_out, uint64_t* fine_out) {
   return guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
-    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
-    const auto it = c->row_slot.find(id);
-    if (it == c->row_slot.end()) fail(BMG_INVALID_ARGUMENT, "image " + std::to_string(id) + " is not in the current row");
+    if (!c->S().row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    const auto it = c->S().row_slot.find(id);
+    if (it == c->S().row_slot.end()) fail(BMG_INVALID_ARGUMENT, "image " + std::to_string(id) + " is not in the current row");
     set_device(*c);
-    copy_codes_out(*c, c->row_imgs[it->second], coarse_out, fine_out);
+    copy_codes_out(*c, c->S().row_imgs[it->second], coarse_out, fine_out);
   });
 }
 
@@ -902,25 +1028,25 @@ int bmg_match(bmg_context* c, const uint64_t* qids, const uint64_t* tids, uint64
     if (!c || !mp || !offsets_out || (n_pairs && (!qids || !tids)))
       fail(BMG_INVALID_ARGUMENT, "null argument");
     check_match_params(*c, *mp);
-    if (!c->row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
+    if (!c->S().row_valid) fail(BMG_INVALID_ARGUMENT, "no row has been prepared");
     set_device(*c);
     std::vector<std::pair<int, int>> sp;
     uint64_t max_matches = 0;
     for (uint64_t p = 0; p < n_pairs; ++p) {
-      const auto qi = c->row_slot.find(qids[p]);
-      const auto ti = c->row_slot.find(tids[p]);
-      if (qi == c->row_slot.end() || ti == c->row_slot.end())
+      const auto qi = c->S().row_slot.find(qids[p]);
+      const auto ti = c->S().row_slot.find(tids[p]);
+      if (qi == c->S().row_slot.end() || ti == c->S().row_slot.end())
         fail(BMG_INVALID_ARGUMENT, "pair image not in the current row");
       sp.emplace_back(qi->second, ti->second);
-      max_matches += c->row_imgs[qi->second].n;
+      max_matches += c->S().row_imgs[qi->second].n;
     }
     reset_results(*c, n_pairs, max_matches);
-    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>());
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>(), 0);
     if (n_pairs == 0) {
       offsets_out[0] = 0;
       return;
     }
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     const uint64_t* ranges = c->res_ranges.host<uint64_t>();
     // one pass, so the pairs' ranges are contiguous from 0
     offsets_out[0] = 0;
@@ -940,14 +1066,14 @@ int bmg_compute_codes(bmg_context* c, const float* desc, uint64_t count, const f
     if (!c || !mean || (count && (!desc || !coarse_out || !fine_out)))
       fail(BMG_INVALID_ARGUMENT, "null argument");
     set_device(*c);
-    c->row_valid = false;
+    c->S().row_valid = false;
     c->d_tmp_desc.ensure(std::max<uint64_t>(count, 1) * 512);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
     stage_h2d(*c, c->d_tmp_desc.p, desc, count * 512);
     c->pending_upload = true;
     std::vector<std::pair<const float*, uint64_t>> one{{c->d_tmp_desc.as<float>(), count}};
     prepare_row_views(*c, one, mean, nullptr, false);
-    copy_codes_out(*c, c->row_imgs[0], coarse_out, fine_out);
+    copy_codes_out(*c, c->S().row_imgs[0], coarse_out, fine_out);
   });
 }
 
@@ -972,13 +1098,13 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
     if (!qdesc || !tdesc || !qc->coarse || !qc->fine || !tc->coarse || !tc->fine || !matches_out)
       fail(BMG_INVALID_ARGUMENT, "null data pointer");
     set_device(*c);
-    c->row_valid = false;
+    c->S().row_valid = false;
     const HashDev& h = c->hd;
     const uint64_t nq = qc->count, nt = tc->count;
     // descriptors
     c->d_tmp_desc.ensure((nq + nt) * 512);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     float* dq = c->d_tmp_desc.as<float>();
     float* dt = dq + nq * kDim;
     stage_h2d(*c, dq, qdesc, nq * 512);
@@ -987,7 +1113,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
     // lay out two images (no codes computed: the given codes are uploaded)
     std::vector<std::pair<const float*, uint64_t>> two{{dq, nq}, {dt, nt}};
     // reuse the row layout, but skip the projection kernels: upload codes into place
-    c->row_imgs.clear();
+    c->S().row_imgs.clear();
     {
       // layout only
       const int L = h.tables;
@@ -1005,8 +1131,8 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
         so[i] = off; off = align_up(off + two[i].second * L * 4, 256);
         bo[i] = off; off = align_up(off + two[i].second * L * h.fwp * 8, 256);
       }
-      c->d_scratch.ensure(off);
-      char* base = c->d_scratch.as<char>();
+      c->S().d_scratch.ensure(off);
+      char* base = c->S().d_scratch.as<char>();
       const bmg_code_set* sets[2] = {qc, tc};
       for (int i = 0; i < 2; ++i) {
         ImgDev im{};
@@ -1018,49 +1144,49 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
         im.cursor = reinterpret_cast<uint32_t*>(base + cu[i]);
         im.slots = reinterpret_cast<uint32_t*>(base + so[i]);
         im.bfine = reinterpret_cast<uint64_t*>(base + bo[i]);
-        c->row_imgs.push_back(im);
+        c->S().row_imgs.push_back(im);
         const uint64_t n = two[i].second;
         for (uint64_t j = 0; j < n * L; ++j)
           if (sets[i]->coarse[j] >= static_cast<uint32_t>(h.n_buckets))
             fail(BMG_INVALID_ARGUMENT, "bucket id out of range for coarse_bits");
-        uint32_t* hc = c->ring.alloc<uint32_t>(n * L, c->s_comp, c->s_copy);
+        uint32_t* hc = c->ring.alloc<uint32_t>(n * L, c->S().s_comp, c->s_copy);
         std::memcpy(hc, sets[i]->coarse, n * L * 4);
-        BMG_CUDA(cudaMemcpyAsync(im.coarse, hc, n * L * 4, cudaMemcpyHostToDevice, c->s_comp));
-        uint64_t* hf = c->ring.alloc<uint64_t>(n * h.fwp, c->s_comp, c->s_copy);
+        meta_add(*c, im.coarse, hc, n * L * 4);
+        uint64_t* hf = c->ring.alloc<uint64_t>(n * h.fwp, c->S().s_comp, c->s_copy);
         std::memset(hf, 0, n * h.fwp * 8);
         for (uint64_t j = 0; j < n; ++j)
           std::memcpy(hf + j * h.fwp, sets[i]->fine + j * h.fw, h.fw * 8);
-        BMG_CUDA(cudaMemcpyAsync(im.fine, hf, n * h.fwp * 8, cudaMemcpyHostToDevice, c->s_comp));
+        meta_add(*c, im.fine, hf, n * h.fwp * 8);
       }
-      BMG_CUDA(cudaMemsetAsync(base + off_begin, 0, off_end - off_begin, c->s_comp));
-      ImgDev* hi = c->ring.alloc<ImgDev>(2, c->s_comp, c->s_copy);
-      std::memcpy(hi, c->row_imgs.data(), sizeof(ImgDev) * 2);
-      c->d_imgs.ensure(sizeof(ImgDev) * 2);
-      BMG_CUDA(cudaMemcpyAsync(c->d_imgs.p, hi, sizeof(ImgDev) * 2, cudaMemcpyHostToDevice, c->s_comp));
+      meta_add(*c, base + off_begin, nullptr, off_end - off_begin);
+      ImgDev* hi = c->ring.alloc<ImgDev>(2, c->S().s_comp, c->s_copy);
+      std::memcpy(hi, c->S().row_imgs.data(), sizeof(ImgDev) * 2);
+      c->S().d_imgs.ensure(sizeof(ImgDev) * 2);
+      meta_add(*c, c->S().d_imgs.p, hi, sizeof(ImgDev) * 2);
       // tables for the train image only (slot 1)
       const size_t n_tiles = (nt + kCodesTile - 1) / kCodesTile;
-      uint32_t* ht = c->ring.alloc<uint32_t>(2 * n_tiles, c->s_comp, c->s_copy);
+      uint32_t* ht = c->ring.alloc<uint32_t>(2 * n_tiles, c->S().s_comp, c->s_copy);
       for (size_t t = 0; t < n_tiles; ++t) {
         ht[t] = 1;
         ht[n_tiles + t] = static_cast<uint32_t>(t * kCodesTile);
       }
-      c->d_tiles.ensure(sizeof(uint32_t) * 2 * n_tiles);
-      BMG_CUDA(cudaMemcpyAsync(c->d_tiles.p, ht, sizeof(uint32_t) * 2 * n_tiles, cudaMemcpyHostToDevice,
-                               c->s_comp));
-      c->d_diag.ensure(sizeof(unsigned long long) * 4);
-      BMG_CUDA(cudaMemsetAsync(c->d_diag.p, 0, sizeof(unsigned long long) * 4, c->s_comp));
+      c->S().d_tiles.ensure(sizeof(uint32_t) * 2 * n_tiles);
+      meta_add(*c, c->S().d_tiles.p, ht, sizeof(uint32_t) * 2 * n_tiles);
+      c->S().d_diag.ensure(sizeof(unsigned long long) * 4);
+      meta_add(*c, c->S().d_diag.p, nullptr, sizeof(unsigned long long) * 4);
+      meta_flush(*c);
       join_uploads(*c);
       // the scan kernel for slot 1 only: run tables on a 2-image table but
       // the hist/scatter tiles reference image 1 only
-      launch_tables(h, c->d_imgs.as<ImgDev>(), c->d_tiles.as<uint32_t>(), c->d_tiles.as<uint32_t>() + n_tiles,
-                    static_cast<int>(n_tiles), 2, c->s_comp);
+      launch_tables(h, c->S().d_imgs.as<ImgDev>(), c->S().d_tiles.as<uint32_t>(), c->S().d_tiles.as<uint32_t>() + n_tiles,
+                    static_cast<int>(n_tiles), 2, c->S().s_comp);
       c->launches += 3;
       check_launch();
     }
     std::vector<std::pair<int, int>> sp{{0, 1}};
     reset_results(*c, 1, nq);
-    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>());
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    enqueue_match(*c, sp, *mp, c->res_ranges.dev<uint64_t>(), c->d_res.as<int32_t>(), 0);
+    BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     const uint64_t* offs = c->res_ranges.host<uint64_t>();
     const uint64_t total = offs[1] - offs[0];
     if (total)
@@ -1090,52 +1216,114 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     for (uint64_t i = 0; i < plan->n_iterations; ++i) total_rows += plan->rows_per_iteration[i];
     if (total_rows != plan->n_rows) fail(BMG_INVALID_ARGUMENT, "rows_per_iteration does not sum to n_rows");
     const uint64_t n_pairs = plan->n_rows ? plan->row_pair_offsets[plan->n_rows] : 0;
-    uint64_t cap = 0;
-    for (uint64_t p = 0; p < n_pairs; ++p) {
-      const uint64_t a = plan->pairs[2 * p], b = plan->pairs[2 * p + 1];
-      if (a >= b) fail(BMG_INVALID_ARGUMENT, "plan pairs must be (lower id, higher id)");
-      cap += features_of(a).count;
+    // row r's matches are packed into its own region [row_base[r], row_base[r+1])
+    // of the result log (capacity: one match per query of each pair)
+    std::vector<uint64_t> row_base(plan->n_rows + 1, 0);
+    for (uint64_t r = 0; r < plan->n_rows; ++r) {
+      uint64_t cap = 0;
+      for (uint64_t p = plan->row_pair_offsets[r]; p < plan->row_pair_offsets[r + 1]; ++p) {
+        const uint64_t a = plan->pairs[2 * p], b = plan->pairs[2 * p + 1];
+        if (a >= b) fail(BMG_INVALID_ARGUMENT, "plan pairs must be (lower id, higher id)");
+        cap += features_of(a).count;
+      }
+      row_base[r + 1] = row_base[r] + cap;
     }
+    const uint64_t total_cap = row_base[plan->n_rows];
+    // the last row that needs each image: uploads of a row are issued in
+    // descending order of it, so later rows can start before earlier rows'
+    // other images have arrived
+    std::unordered_map<uint64_t, uint64_t> last_need;
+    for (uint64_t r = 0; r < plan->n_rows; ++r)
+      for (uint64_t k = plan->row_needed_offsets[r]; k < plan->row_needed_offsets[r + 1]; ++k)
+        last_need[plan->needed_ids[k]] = r;
+
     auto res = std::make_unique<bmg_result>();
-    reset_results(*c, n_pairs, cap);
+    reset_results(*c, n_pairs, total_cap);
+    res->log = static_cast<int32_t*>(PinnedPool::acquire(8 * std::max<uint64_t>(total_cap, 1), &res->log_bytes));
     uint64_t* d_off = c->res_ranges.dev<uint64_t>();
     int32_t* d_log = c->d_res.as<int32_t>();
+    c->cur = 0;
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
-    BMG_CUDA(cudaEventRecord(span0, c->s_comp));
+    BMG_CUDA(cudaEventRecord(span0, c->slot[0].s_comp));
     BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
+    BMG_CUDA(cudaStreamWaitEvent(c->slot[1].s_comp, span0, 0));
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     struct ChainHook {
       Ctx& c;
-      ~ChainHook() { c.mean_chain_only = false; }
+      ~ChainHook() {
+        c.mean_chain_only = false;
+        c.cur = 0;
+      }
     } chain_hook{*c};
     c->mean_chain_only = (opts->flags & BMG_EXEC_MEAN_CHAIN) != 0;
     uint64_t row = 0;
+    std::vector<uint64_t> missing;
+    // BMG_TIMELINE=1: per-row event timeline on stderr (diagnostics)
+    static const bool timeline = [] {
+      const char* v = getenv("BMG_TIMELINE");
+      return v && v[0] == '1';
+    }();
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    auto mark = [&](const std::string& what, cudaStream_t st) {
+      if (!timeline) return;
+      cudaEvent_t e = take_event(*c);
+      BMG_CUDA(cudaEventRecord(e, st));
+      const double host_ms = 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      marks.emplace_back(what + " (host issue " + std::to_string(host_ms) + " ms)", e);
+    };
+    if (timeline) c->marks = &marks;
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
       const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
       uint64_t it_pairs = 0;
       for (uint64_t r = 0; r < plan->rows_per_iteration[it]; ++r, ++row) {
+        c->cur = static_cast<int>(row & 1);
+        RowSlot& S = c->S();
         const uint64_t nb = plan->row_needed_offsets[row], ne = plan->row_needed_offsets[row + 1];
         const uint64_t* needed = plan->needed_ids + nb;
+        // uploads: bookkeeping + hooks in the reference order (engine.cpp:438-444),
+        // the copies in the order that lets later rows start early
+        missing.clear();
         for (uint64_t k = nb; k < ne; ++k) {
           const uint64_t id = plan->needed_ids[k];
           const bmg_feature_view& fv = features_of(id);
           if (!c->resident.count(id)) {
-            arena_upload(*c, id, fv.descriptors, fv.count);
+            arena_reserve(*c, id, fv.descriptors, fv.count);
             if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
+            missing.push_back(id);
           }
         }
+        std::stable_sort(missing.begin(), missing.end(),
+                         [&](uint64_t x, uint64_t y) { return last_need[x] > last_need[y]; });
+        for (uint64_t id : missing) arena_copy(*c, c->resident.at(id), features_of(id).descriptors);
+        if (!missing.empty()) mark("row " + std::to_string(row) + " uploads done", c->s_copy);
+        // the row's stream waits for the last-issued copy among its images
+        const ArenaImage* last = nullptr;
+        for (uint64_t k = 0; k < ne - nb; ++k) {
+          const auto f = c->resident.find(needed[k]);
+          if (f != c->resident.end() && f->second.ev && (!last || f->second.seq > last->seq)) last = &f->second;
+        }
+        if (last) BMG_CUDA(cudaStreamWaitEvent(S.s_comp, last->ev, 0));
+        c->pending_upload = false;
+        mark("row " + std::to_string(row) + " start", S.s_comp);
         prepare_row(*c, needed, ne - nb, nullptr);
+        mark("row " + std::to_string(row) + " codes+tables done", S.s_comp);
         const uint64_t pb = plan->row_pair_offsets[row], pe = plan->row_pair_offsets[row + 1];
         std::vector<std::pair<int, int>> sp;
         sp.reserve(pe - pb);
         for (uint64_t p = pb; p < pe; ++p) {
-          const auto qa = c->row_slot.find(plan->pairs[2 * p]);
-          const auto tb = c->row_slot.find(plan->pairs[2 * p + 1]);
-          if (qa == c->row_slot.end() || tb == c->row_slot.end())
+          const auto qa = S.row_slot.find(plan->pairs[2 * p]);
+          const auto tb = S.row_slot.find(plan->pairs[2 * p + 1]);
+          if (qa == S.row_slot.end() || tb == S.row_slot.end())
             fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
           sp.emplace_back(qa->second, tb->second);
         }
-        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log);
+        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log, row_base[row]);
+        mark("row " + std::to_string(row) + " match done", S.s_comp);
+        // the row's log region goes to the result's pinned buffer while the
+        // next row computes
+        if (row_base[row + 1] > row_base[row])
+          BMG_CUDA(cudaMemcpyAsync(res->log + 2 * row_base[row], d_log + 2 * row_base[row],
+                                   8 * (row_base[row + 1] - row_base[row]), cudaMemcpyDeviceToHost, S.s_comp));
         it_pairs += pe - pb;
         for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
           arena_evict(*c, plan->evict_ids[k]);
@@ -1146,32 +1334,51 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->iterations.push_back(c->uploads - up0);
       res->iterations.push_back(c->units_uploaded - units0);
     }
-    BMG_CUDA(cudaEventRecord(span1, c->s_comp));
-    // per-pair [begin, end) ranges are in mapped host memory; the log is
-    // read back in one DMA
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
-    const uint64_t* ranges = c->res_ranges.host<uint64_t>();
-    uint64_t total = 0, kept_total = 0, log_end = 0;
-    for (uint64_t p = 0; p < n_pairs; ++p) {
-      kept_total += ranges[2 * p + 1] - ranges[2 * p];
-      log_end = std::max(log_end, ranges[2 * p + 1]);
+    // join the second slot into the first for the span end
+    {
+      cudaEvent_t j = take_event(*c);
+      BMG_CUDA(cudaEventRecord(j, c->slot[1].s_comp));
+      BMG_CUDA(cudaStreamWaitEvent(c->slot[0].s_comp, j, 0));
+      c->free_events.push_back(j);
     }
-    const int32_t* flat = fetch_log(*c, log_end);
-    res->matches.reserve(2 * kept_total);
+    BMG_CUDA(cudaEventRecord(span1, c->slot[0].s_comp));
+    BMG_CUDA(cudaStreamSynchronize(c->slot[0].s_comp));
+    for (auto& [what, e] : marks) {
+      float ms = 0.f;
+      BMG_CUDA(cudaEventSynchronize(e));
+      BMG_CUDA(cudaEventElapsedTime(&ms, span0, e));
+      fprintf(stderr, "[bmg timeline] %8.3f ms  %s\n", ms, what.c_str());
+      c->free_events.push_back(e);
+    }
+    c->marks = nullptr;
+    if (timeline)
+      for (int k = 0; k < 2; ++k)
+        if (c->slot[k].d_mean_state.p) {
+          MeanState st{};
+          BMG_CUDA(cudaMemcpy(&st, c->slot[k].d_mean_state.p, sizeof(st), cudaMemcpyDeviceToHost));
+          fprintf(stderr, "[bmg timeline] slot %d mean: bad %u need_chain %u rounds %u events %u\n", k, st.bad,
+                  st.need_chain, st.rounds, st.events);
+        }
+    // per-pair [begin, end) ranges are in mapped host memory; the matches
+    // are already in the result's pinned log
+    const uint64_t* ranges = c->res_ranges.host<uint64_t>();
     // results keyed and sorted by IdPair (engine.cpp:419, 506-512); a pair
     // planned twice keeps its last match list, like the reference's map
     std::map<std::pair<uint64_t, uint64_t>, uint64_t> last;
     for (uint64_t p = 0; p < n_pairs; ++p) last[{plan->pairs[2 * p], plan->pairs[2 * p + 1]}] = p;
-    res->offsets.push_back(0);
+    res->pair_ids.reserve(2 * last.size());
+    res->ranges.reserve(2 * last.size());
+    uint64_t total = 0;
     for (const auto& [key, p] : last) {
       res->pair_ids.push_back(key.first);
       res->pair_ids.push_back(key.second);
       const uint64_t b = ranges[2 * p], e = ranges[2 * p + 1];
-      res->matches.insert(res->matches.end(), flat + 2 * b, flat + 2 * e);
+      res->ranges.push_back(b);
+      res->ranges.push_back(e);
       total += e - b;
-      res->offsets.push_back(res->matches.size() / 2);
-      if (opts->on_pair) opts->on_pair(opts->on_pair_user, key.first, key.second, flat + 2 * b, e - b);
+      if (opts->on_pair) opts->on_pair(opts->on_pair_user, key.first, key.second, res->log + 2 * b, e - b);
     }
+    res->n_matches = total;
     res->counters[0] = n_pairs;
     res->counters[1] = total;
     res->counters[2] = c->uploads;
@@ -1192,21 +1399,38 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
 }
 
 uint64_t bmg_result_pair_count(const bmg_result* r) { return r ? r->pair_ids.size() / 2 : 0; }
-uint64_t bmg_result_match_count(const bmg_result* r) { return r ? r->matches.size() / 2 : 0; }
+uint64_t bmg_result_match_count(const bmg_result* r) { return r ? r->n_matches : 0; }
 
 int bmg_result_copy(const bmg_result* r, uint64_t* pair_ids, uint64_t* offsets, int32_t* matches) {
   return guarded([&] {
     if (!r) fail(BMG_INVALID_ARGUMENT, "null result");
-    if (pair_ids) std::copy(r->pair_ids.begin(), r->pair_ids.end(), pair_ids);
-    if (offsets) std::copy(r->offsets.begin(), r->offsets.end(), offsets);
-    if (matches) std::copy(r->matches.begin(), r->matches.end(), matches);
+    const size_t np = r->pair_ids.size() / 2;
+    if (pair_ids && np) std::memcpy(pair_ids, r->pair_ids.data(), sizeof(uint64_t) * 2 * np);
+    uint64_t o = 0;
+    if (offsets) offsets[0] = 0;
+    for (size_t p = 0; p < np; ++p) {
+      const uint64_t b = r->ranges[2 * p], e = r->ranges[2 * p + 1];
+      if (matches && e > b) std::memcpy(matches + 2 * o, r->log + 2 * b, sizeof(int32_t) * 2 * (e - b));
+      o += e - b;
+      if (offsets) offsets[p + 1] = o;
+    }
+  });
+}
+
+int bmg_result_view(const bmg_result* r, const uint64_t** pair_ids, const uint64_t** ranges,
+                    const int32_t** log) {
+  return guarded([&] {
+    if (!r || !pair_ids || !ranges || !log) fail(BMG_INVALID_ARGUMENT, "null argument");
+    *pair_ids = r->pair_ids.data();
+    *ranges = r->ranges.data();
+    *log = r->log;
   });
 }
 
 int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wall_s_out) {
   return guarded([&] {
     if (!r) fail(BMG_INVALID_ARGUMENT, "null result");
-    if (counters_out) std::copy(r->counters, r->counters + 6, counters_out);
+    if (counters_out) std::memcpy(counters_out, r->counters, sizeof(r->counters));
     if (wall_s_out) *wall_s_out = r->wall_s;
   });
 }
@@ -1216,7 +1440,7 @@ uint64_t bmg_result_iteration_count(const bmg_result* r) { return r ? r->iterati
 int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out3[3]) {
   return guarded([&] {
     if (!r || !out3 || i >= r->iterations.size() / 3) fail(BMG_INVALID_ARGUMENT, "bad iteration index");
-    std::copy(r->iterations.begin() + 3 * i, r->iterations.begin() + 3 * i + 3, out3);
+    std::memcpy(out3, r->iterations.data() + 3 * i, sizeof(uint64_t) * 3);
   });
 }
 
@@ -1235,7 +1459,7 @@ int bmg_set_profiling(bmg_context* c, int enabled) {
   return guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
     for (auto& t : c->timers) {
       c->free_events.push_back(t.a);
       c->free_events.push_back(t.b);
@@ -1249,7 +1473,7 @@ int bmg_kernel_time(bmg_context* c, const char* cls, double* total_ms, uint64_t*
   return guarded([&] {
     if (!c || !cls) fail(BMG_INVALID_ARGUMENT, "null argument");
     set_device(*c);
-    BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
     double ms = 0.0;
     uint64_t n = 0;
     for (auto& t : c->timers) {
@@ -1269,9 +1493,9 @@ int bmg_fixup_counts(bmg_context* c, uint64_t* code_bits, uint64_t* rerank_queri
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     unsigned long long d[4] = {0, 0, 0, 0};
-    if (c->d_diag.p) {
-      BMG_CUDA(cudaMemcpyAsync(d, c->d_diag.p, sizeof(d), cudaMemcpyDeviceToHost, c->s_comp));
-      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    if (c->S().d_diag.p) {
+      BMG_CUDA(cudaMemcpyAsync(d, c->S().d_diag.p, sizeof(d), cudaMemcpyDeviceToHost, c->S().s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     }
     if (code_bits) *code_bits = d[0];
     if (rerank_queries) *rerank_queries = d[1];
@@ -1283,12 +1507,12 @@ int bmg_row_mean_info(bmg_context* c, uint32_t* rounds, int* used_chain) {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     MeanState st{};
-    if (c->d_mean_state.p && !c->last_mean_chain_only) {
-      BMG_CUDA(cudaMemcpyAsync(&st, c->d_mean_state.p, sizeof(st), cudaMemcpyDeviceToHost, c->s_comp));
-      BMG_CUDA(cudaStreamSynchronize(c->s_comp));
+    if (c->S().d_mean_state.p && !c->S().last_mean_chain_only) {
+      BMG_CUDA(cudaMemcpyAsync(&st, c->S().d_mean_state.p, sizeof(st), cudaMemcpyDeviceToHost, c->S().s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     }
     if (rounds) *rounds = st.rounds;
-    if (used_chain) *used_chain = (c->last_mean_chain_only || st.need_chain) ? 1 : 0;
+    if (used_chain) *used_chain = (c->S().last_mean_chain_only || st.need_chain) ? 1 : 0;
   });
 }
 

@@ -69,10 +69,26 @@ struct MeanState {
   uint32_t events;      // rounding steps replayed (all channels)
 };
 
+// Small device-side copies / zero fills on a compute stream (kernels.cu
+// meta_kernel); src == nullptr means zero fill.  src may be mapped pinned
+// host memory.  dst and src 16-byte aligned.
+struct MetaOp {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+constexpr int kMetaOps = 8;
+struct MetaBatch {
+  MetaOp op[kMetaOps];
+  int n;
+};
+void launch_meta(const MetaBatch& b, cudaStream_t s);
+
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
 // parallel reconstruction with the sequential chain as gated fallback, or the
-// chain alone.  scratch: mean_scratch_bytes(n_tiles).  Returns kernel launches.
+// chain alone.  scratch: mean_scratch_bytes(n_tiles); *st must be zeroed by
+// the caller (stream-ordered).  Returns kernel launches.
 inline size_t mean_scratch_bytes(size_t n_tiles) {
   return n_tiles * kDim * (16 + 32 + 4);  // F96 tile sums, partial-sum ranges, lowest set bits
 }
@@ -88,8 +104,7 @@ void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, co
 void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                    const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s);
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s);
-void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, cudaStream_t s);
+void launch_scan_counts(const uint32_t* counts, int n, uint64_t* ranges_out, uint64_t base, cudaStream_t s);
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
                     const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);
 

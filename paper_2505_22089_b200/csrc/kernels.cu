@@ -730,12 +730,22 @@ __device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint
   return h;
 }
 
+// Chunk descriptors of one warp: (first slot index, length) of up to 32
+// chunks of the current page, zero-length past the page (read up to index
+// 35 by the look-ahead), plus the tables' chunk ends for the page build.
+constexpr int kChunkSlots = 40;
+struct WalkSmem {
+  uint2 cd[kChunkSlots];
+  uint32_t cend[kMaxTables];
+};
+
 // Walks the union; round(valid, key) is called by every lane once per round
 // (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket
-// range; other lanes hold zeros.
+// range; other lanes hold zeros.  key = hamming * 2^ib + train_idx, or
+// kEmpty for lanes without an entry this round.
 template <int FWP, typename F>
-__device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, int ib,
-                                           const uint64_t (&qc)[FWP], F&& round) {
+__device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, uint32_t mul,
+                                           const uint64_t (&qc)[FWP], WalkSmem& ws, F&& round) {
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const uint32_t nch = (sz + 7u) >> 3;
   uint32_t cend = nch;  // inclusive scan of the chunk counts over tables
@@ -746,59 +756,67 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   const uint32_t n_chunks = __shfl_sync(kFull, cend, L - 1);
   const uint32_t cstart = cend - nch;
   const uint32_t sbase = (uint32_t)lane * T.n + lo;
+  if (lane < L) ws.cend[lane] = cend;
+  __syncwarp();
   for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
-    // lane j describes chunk pg + j: table = #tables ending at or before it
+    // lane j describes chunk pg + j: its table is the number of tables
+    // ending at or before it
     const uint32_t k = pg + lane;
     uint32_t t = 0;
-    for (int tt = 0; tt < L - 1; ++tt) t += __shfl_sync(kFull, cend, tt) <= k ? 1u : 0u;
+    for (int tt = 0; tt < L - 1; ++tt) t += ws.cend[tt] <= k ? 1u : 0u;
     const uint32_t ts = __shfl_sync(kFull, cstart, t);
     const uint32_t tb = __shfl_sync(kFull, sbase, t);
     const uint32_t tz = __shfl_sync(kFull, sz, t);
     const uint32_t o8 = (k - ts) * 8u;
-    const uint32_t my_base = tb + o8;
-    const uint32_t my_len = k < n_chunks ? min(8u, tz - o8) : 0u;
+    ws.cd[lane] = make_uint2(tb + o8, k < n_chunks ? min(8u, tz - o8) : 0u);
+    __syncwarp();
     const uint32_t nr = (min(32u, n_chunks - pg) + 3u) >> 2;
-    uint32_t base = __shfl_sync(kFull, my_base, grp);
-    bool v = (uint32_t)sub < __shfl_sync(kFull, my_len, grp);
-    uint32_t j = 0;
+    uint2 d = ws.cd[grp];
+    bool v = (uint32_t)sub < d.y;
+    uint32_t j = kEmpty;
     uint64_t cw[FWP];
 #pragma unroll
-    for (int x = 0; x < FWP; ++x) cw[x] = 0;
+    for (int x = 0; x < FWP; ++x) cw[x] = qc[x];
     if (v) {
-      j = __ldg(T.slots + base + sub);
-      load_code<FWP>(T.bfine + (size_t)(base + sub) * FWP, cw);
+      const uint32_t si = d.x + sub;
+      j = __ldg(T.slots + si);
+      load_code<FWP>(T.bfine + (size_t)si * FWP, cw);
     }
+#pragma unroll 2
     for (uint32_t r = 0; r < nr; ++r) {
-      const int kk = min(4 * (int)(r + 1) + grp, 31);
-      const uint32_t nbase = __shfl_sync(kFull, my_base, kk);
-      const bool nv = r + 1 < nr && (uint32_t)sub < __shfl_sync(kFull, my_len, kk);
-      uint32_t jn = 0;
-      uint64_t cn[FWP];
-#pragma unroll
-      for (int x = 0; x < FWP; ++x) cn[x] = 0;
+      // next round's chunk (entries past the page have length 0)
+      const uint2 dn = ws.cd[4 * r + 4 + grp];
+      const bool nv = (uint32_t)sub < dn.y;
+      uint32_t jn = kEmpty;
+      uint64_t cn[FWP];  // only read when nv
       if (nv) {
-        jn = __ldg(T.slots + nbase + sub);
-        load_code<FWP>(T.bfine + (size_t)(nbase + sub) * FWP, cn);
+        const uint32_t si = dn.x + sub;
+        jn = __ldg(T.slots + si);
+        load_code<FWP>(T.bfine + (size_t)si * FWP, cn);
       }
-      round(v, v ? (hamming<FWP>(qc, cw) << ib) | j : kEmpty);
+      round(v, v ? hamming<FWP>(qc, cw) * mul + j : kEmpty);
       v = nv;
       j = jn;
 #pragma unroll
       for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
     }
+    __syncwarp();
   }
 }
 
-template <int FWP, int KM, int NT>
+template <int FWP, int KM, int NT, int KC>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
+  __shared__ WalkSmem s_walk[NT / 32];
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = NT / 32;
 
-  const int L = a.tables, K = a.k, ib = a.idx_bits;
-  const uint32_t idx_mask = (1u << ib) - 1u;
+  const int L = a.tables, K = KC ? KC : a.k, ib = a.idx_bits;
+  const uint32_t idx_mask = (1u << ib) - 1u, mul = 1u << ib;
+  WalkSmem& ws = s_walk[warp];
+  if (lane < kChunkSlots - 32) ws.cd[32 + lane] = make_uint2(0u, 0u);
   const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
   const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
@@ -826,7 +844,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     bool exact = KM != 8;
     if constexpr (KM == 8) {
       uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool valid, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, mul, qc, ws, [&](bool valid, uint32_t key) {
         k3 = max(k2, min(k3, key));
         k2 = max(k1, min(k2, key));
         k1 = max(k0, min(k1, key));
@@ -868,7 +886,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // tables is taken once.
       lst = kEmpty;
       uint32_t thr = kEmpty;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, mul, qc, ws, [&](bool, uint32_t key) {
         key = key < thr ? key : kEmpty;
         for (;;) {
           const uint32_t m = __reduce_min_sync(kFull, key);
@@ -1042,17 +1060,15 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 // total of earlier rows) and ascending-query compaction of the dense arrays.
 // ---------------------------------------------------------------------------
 // ranges[2i], ranges[2i+1] = [begin, end) of pair i's matches in the result
-// log.  Per-pair ranges (not shared boundary offsets) so a re-do pass can
-// re-point one row's pairs without touching its neighbours.
+// log; a launch's pairs are packed from `base` (the row's own log region).
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __restrict__ counts, int n,
-                                                           uint64_t* __restrict__ ranges,
-                                                           unsigned long long* running_total) {
+                                                           uint64_t* __restrict__ ranges, uint64_t base) {
   __shared__ uint32_t s_warp[32];
   __shared__ unsigned long long s_carry;
-  if (threadIdx.x == 0) s_carry = *running_total;
+  if (threadIdx.x == 0) s_carry = base;
   __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + threadIdx.x;
+  for (int b0 = 0; b0 < n; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
     const uint32_t v = i < n ? counts[i] : 0u;
     const unsigned long long carry = s_carry;
     const uint32_t incl = block_incl_scan(v, s_warp);
@@ -1064,7 +1080,6 @@ __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* __res
     if (threadIdx.x == blockDim.x - 1) s_carry = carry + incl;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *running_total = s_carry;
 }
 
 __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict__ dense,
@@ -1095,7 +1110,33 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row metadata (pointer tables, tile and work lists) is read from mapped
+// pinned host memory and zero fills are done by this kernel on the row's own
+// stream: cudaMemcpyAsync / cudaMemsetAsync would queue on the copy engines
+// behind the bulk descriptor uploads and stall rows that could already run.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) meta_kernel(MetaBatch b) {
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+  for (int i = 0; i < b.n; ++i) {
+    const MetaOp o = b.op[i];
+    const size_t n16 = o.bytes >> 4;
+    uint4* d = static_cast<uint4*>(o.dst);
+    const uint4* src = static_cast<const uint4*>(o.src);
+    for (size_t k = tid; k < n16; k += nth) d[k] = src ? src[k] : make_uint4(0u, 0u, 0u, 0u);
+    for (size_t k = (n16 << 4) + tid; k < o.bytes; k += nth)
+      static_cast<unsigned char*>(o.dst)[k] = src ? reinterpret_cast<const unsigned char*>(o.src)[k] : 0;
+  }
+}
+
 }  // namespace
+
+void launch_meta(const MetaBatch& b, cudaStream_t s) {
+  size_t units = 0;
+  for (int i = 0; i < b.n; ++i) units = std::max<size_t>(units, (b.op[i].bytes + 15) >> 4);
+  const int grid = (int)std::min<size_t>(148, std::max<size_t>(1, (units + 255) / 256));
+  if (b.n) meta_kernel<<<grid, 256, 0, s>>>(b);
+}
 
 // ---------------------------------------------------------------------------
 // launchers
@@ -1109,7 +1150,6 @@ int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
     i128* sums = static_cast<i128*>(scratch);
     TileRange* rng = reinterpret_cast<TileRange*>(sums + (size_t)n_tiles * kDim);
     uint32_t* low = reinterpret_cast<uint32_t*>(rng + (size_t)n_tiles * kDim);
-    cudaMemsetAsync(st, 0, sizeof(MeanState), s);
     mean_sums_kernel<<<n_tiles, kSumsThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, st);
     mean_resolve_kernel<<<kDim, kResolveThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, n_tiles,
                                                          total, st, mean_out, acc_out);
@@ -1155,15 +1195,16 @@ void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* til
   tables_scatter_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
 }
 
-template <int FWP, int KM, int NT>
+template <int FWP, int KM, int NT, int KC>
 static void launch_match_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  match_kernel<FWP, KM, NT><<<n_work, NT, 0, s>>>(a);
+  match_kernel<FWP, KM, NT, KC><<<n_work, NT, 0, s>>>(a);
 }
 
 template <int FWP>
 static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  if (a.k <= 8) launch_match_t<FWP, 8, kMatchThreads>(a, n_work, s);
-  else launch_match_t<FWP, 32, 512>(a, n_work, s);
+  if (a.k == 8) launch_match_t<FWP, 8, kMatchThreads, 8>(a, n_work, s);  // MatchParams default
+  else if (a.k < 8) launch_match_t<FWP, 8, kMatchThreads, 0>(a, n_work, s);
+  else launch_match_t<FWP, 32, 512, 0>(a, n_work, s);
 }
 
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
@@ -1176,9 +1217,8 @@ void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
   }
 }
 
-void launch_scan_counts(const uint32_t* counts, int n, uint64_t* offsets_out,
-                        unsigned long long* running_total, cudaStream_t s) {
-  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, offsets_out, running_total);
+void launch_scan_counts(const uint32_t* counts, int n, uint64_t* ranges_out, uint64_t base, cudaStream_t s) {
+  scan_counts_kernel<<<1, 1024, 0, s>>>(counts, n, ranges_out, base);
 }
 
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,

@@ -263,6 +263,38 @@ def _feature_views(features: dict):
     return views, keep
 
 
+class _ResultBuffer:
+    """Owns a bmg_result; numpy views of its pinned log keep it alive (the
+    result is freed when the last view is garbage collected)."""
+
+    def __init__(self, L, h):
+        self.L, self.h = L, h
+
+    def wrap(self, arr: np.ndarray) -> np.ndarray:
+        # a base object that carries the owner: slices of `out` keep it alive
+        out = np.ndarray(arr.shape, arr.dtype, buffer=_Owned(arr, self))
+        out.flags.writeable = False
+        return out
+
+    def close(self):
+        if self.h:
+            self.L.bmg_result_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+class _Owned:
+    """Buffer-protocol wrapper around a ctypes-backed array + its owner."""
+
+    def __init__(self, arr, owner):
+        self.arr, self.owner = arr, owner
+
+    def __buffer__(self, flags):
+        return memoryview(self.arr)
+
+
 def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
                  opts: ExecuteOptions = ExecuteOptions(), rows=None, flat: FlatPlan | None = None,
                  views=None) -> ExecutionResult:
@@ -293,28 +325,35 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
     h = C.c_void_p()
     check(L.bmg_execute_plan(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc),
                              C.byref(h)))
-    try:
-        npairs = L.bmg_result_pair_count(h)
-        nm = L.bmg_result_match_count(h)
-        ids = np.zeros(2 * max(npairs, 1), np.uint64)
-        offs = np.zeros(npairs + 1, np.uint64)
-        m = np.zeros(2 * max(nm, 1), np.int32)
-        check(L.bmg_result_copy(h, ptr(ids), ptr(offs), ptr(m)))
-        counters = np.zeros(6, np.uint64)
-        wall = C.c_double(0)
-        check(L.bmg_result_metrics(h, ptr(counters), C.byref(wall)))
-        dev_ms = C.c_double(0)
-        check(L.bmg_result_device_ms(h, C.byref(dev_ms)))
-        its = []
-        for i in range(L.bmg_result_iteration_count(h)):
-            o = np.zeros(3, np.uint64)
-            check(L.bmg_result_iteration(h, i, ptr(o)))
-            its.append(IterationMetrics(int(o[0]), int(o[1]), int(o[2])))
-    finally:
-        L.bmg_result_free(h)
-    matches = [PairMatches(int(ids[2 * p]), int(ids[2 * p + 1]),
-                           m[2 * int(offs[p]): 2 * int(offs[p + 1])].reshape(-1, 2).copy())
-               for p in range(npairs)]
+    holder = _ResultBuffer(L, h)
+    npairs = L.bmg_result_pair_count(h)
+    nm = L.bmg_result_match_count(h)
+    counters = np.zeros(6, np.uint64)
+    wall = C.c_double(0)
+    check(L.bmg_result_metrics(h, ptr(counters), C.byref(wall)))
+    dev_ms = C.c_double(0)
+    check(L.bmg_result_device_ms(h, C.byref(dev_ms)))
+    its = []
+    for i in range(L.bmg_result_iteration_count(h)):
+        o = np.zeros(3, np.uint64)
+        check(L.bmg_result_iteration(h, i, ptr(o)))
+        its.append(IterationMetrics(int(o[0]), int(o[1]), int(o[2])))
+    matches = []
+    if npairs:
+        # zero-copy: every pair's (query_idx, train_idx) array is a view into
+        # the result's pinned log, kept alive by the views themselves
+        pid_p, rng_p, log_p = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)(), C.POINTER(C.c_int32)()
+        check(L.bmg_result_view(h, C.byref(pid_p), C.byref(rng_p), C.byref(log_p)))
+        ids = np.ctypeslib.as_array(pid_p, (2 * npairs,)).tolist()
+        rng = np.ctypeslib.as_array(rng_p, (2 * npairs,)).tolist()
+        top = max(rng[1::2]) if nm else 0
+        log = holder.wrap(np.ctypeslib.as_array(log_p, (max(2 * top, 1),))).reshape(-1, 2) if top else None
+        empty = np.zeros((0, 2), np.int32)
+        for p in range(npairs):
+            b, e = rng[2 * p], rng[2 * p + 1]
+            matches.append(PairMatches(ids[2 * p], ids[2 * p + 1], log[b:e] if e > b else empty))
+    else:
+        holder.close()
     c = [int(x) for x in counters]
     met = PipelineMetrics(plan.strategy, c[0], c[1], 0, c[2], c[3], c[4], c[5],
                           c[0] / c[2] if c[2] else 0.0, its, wall.value,
