@@ -562,10 +562,11 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   for (int i = 0; i < n_imgs; ++i) {
     lay[i].cursor_off = off;
     off = align_up(off + L * NB * 4, 256);
+    const uint64_t ns = slot_stride(descs[i].second, h.n_buckets);
     lay[i].slots_off = off;
-    off = align_up(off + descs[i].second * L * 4, 256);
+    off = align_up(off + ns * L * 4, 256);
     lay[i].bfine_off = off;
-    off = align_up(off + descs[i].second * L * h.fwp * 8, 256);
+    off = align_up(off + ns * L * h.fwp * 8, 256);
   }
   c.S().d_scratch.ensure(off);
   char* base = c.S().d_scratch.as<char>();
@@ -581,6 +582,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
     im.bfine = reinterpret_cast<uint64_t*>(base + lay[i].bfine_off);
     im.overflow = 0;
+    im.ns = slot_stride(im.n, h.n_buckets);
   }
   // metadata
   ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.S().s_comp, c.s_copy);
@@ -693,7 +695,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
   const HashDev& h = c.hd;
-  const int chunk = kMatchQueries;
+  const int chunk = match_queries_per_cta(h.fwp, mp.k_nearest);
   if (h.tables > 32) fail(BMG_UNSUPPORTED, "more than 32 hash tables is not supported by the GPU matcher");
   const int idx_bits = 32 - bit_width(static_cast<uint32_t>(h.fine_bits));
   std::vector<int> order(n_pairs);
@@ -902,7 +904,13 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     c->seed = cfg->function_seed;
     c->capacity = cfg->capacity_units;
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
-    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamCreateWithFlags(&sl.s_comp, cudaStreamNonBlocking));
+    // slot 0 (even rows) gets the higher priority: in a block's first row
+    // pair the even row waits for every upload and then is the critical path,
+    // while the odd row (already resident images) fills in around it
+    int prio_lo = 0, prio_hi = 0;
+    BMG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[0].s_comp, cudaStreamNonBlocking, prio_hi));
+    BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[1].s_comp, cudaStreamNonBlocking, prio_lo));
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
@@ -1128,8 +1136,9 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
       const size_t off_begin = oo[0], off_end = off;
       for (int i = 0; i < 2; ++i) {
         cu[i] = off; off = align_up(off + L * NB * 4, 256);
-        so[i] = off; off = align_up(off + two[i].second * L * 4, 256);
-        bo[i] = off; off = align_up(off + two[i].second * L * h.fwp * 8, 256);
+        const uint64_t ns = slot_stride(two[i].second, h.n_buckets);
+        so[i] = off; off = align_up(off + ns * L * 4, 256);
+        bo[i] = off; off = align_up(off + ns * L * h.fwp * 8, 256);
       }
       c->S().d_scratch.ensure(off);
       char* base = c->S().d_scratch.as<char>();
@@ -1144,6 +1153,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
         im.cursor = reinterpret_cast<uint32_t*>(base + cu[i]);
         im.slots = reinterpret_cast<uint32_t*>(base + so[i]);
         im.bfine = reinterpret_cast<uint64_t*>(base + bo[i]);
+        im.ns = slot_stride(im.n, h.n_buckets);
         c->S().row_imgs.push_back(im);
         const uint64_t n = two[i].second;
         for (uint64_t j = 0; j < n * L; ++j)

@@ -17,11 +17,12 @@ struct ImgDev {
   uint64_t* fine;      // [n][fwp] fine code words, fwp >= ceil(fine_bits/64), zero padded
   uint32_t* offsets;   // [tables][n_buckets+1] bucket starts (hashmatch.cpp:125-135)
   uint32_t* cursor;    // [tables][n_buckets]   scatter cursors (scratch)
-  uint32_t* slots;     // [tables][n] train indices grouped by bucket (:136-145)
-  uint64_t* bfine;     // [tables][n][fwp] fine codes in slot order (coalesced candidate walk)
+  uint32_t* slots;     // [tables][ns] train indices grouped by bucket (:136-145),
+                       // buckets padded to 4 entries (pad index 0xffffffff)
+  uint64_t* bfine;     // [tables][ns][fwp] fine codes in slot order (coalesced candidate walk)
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
-  uint32_t pad_;
+  uint32_t ns;         // slot stride per table: slot_stride(n, n_buckets)
 };
 
 struct HashDev {
@@ -84,6 +85,11 @@ struct MetaBatch {
 };
 void launch_meta(const MetaBatch& b, cudaStream_t s);
 
+// per-table slot capacity with every bucket padded to a multiple of 4
+inline uint32_t slot_stride(uint64_t n, int n_buckets) {
+  return static_cast<uint32_t>((n + 3ull * static_cast<uint64_t>(n_buckets) + 3ull) & ~3ull);
+}
+
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
 // parallel reconstruction with the sequential chain as gated fallback, or the
@@ -111,6 +117,9 @@ void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint3
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
 constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)
 constexpr int kMatchThreads = 1024;  // 32 warps, one query per warp at a time
-constexpr int kMatchQueries = 1024;  // queries per match CTA
+constexpr int kMatchQueries = 256;   // queries per match CTA (short CTAs: a higher-priority row gets SMs soon)
+constexpr int kTmaQueries = 1024;    // queries per TMA-staged match CTA (16 warps)
+// queries per CTA of the match kernel launch_match picks for (fwp, k)
+int match_queries_per_cta(int fwp, int k);
 
 }  // namespace bmg

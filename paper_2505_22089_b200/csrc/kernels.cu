@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(32, 1) mean_chain_kernel(const ImgDev* __restr
 
 // ---------------------------------------------------------------------------
 // K2: projections.  CTA = 128 descriptors x 192 planes, 512 threads; each
-// thread accumulates 4 descriptors x 12 planes in FP32 (48 FFMA per 4
-// LDS.128).  Planes live transposed in shared memory, descriptors centered
+// thread accumulates 4 descriptors x 12 planes in FP32 (24 packed FFMA2 per
+// 4 LDS.128).  Planes live transposed in shared memory, descriptors centered
 // in shared memory (row stride 132 floats: conflict-free LDS.128).
 //
 // Certificate: |s32 - s_exact| <= gamma_{130} * sum|a_c||p_c|
@@ -446,11 +446,14 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
 
   const int pg = warp;  // 16 plane groups x 12 planes
-  float acc[4][12];
+  // packed FP32x2 FMAs (FFMA2, the descriptor value broadcast to both
+  // halves): plane pair jp of row r accumulates in acc[r][jp]; every output
+  // is still one FP32 FMA chain over c = 0..127 in order (same certificate)
+  float2 acc[4][6];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int j = 0; j < 12; ++j) acc[r][j] = 0.f;
+    for (int j = 0; j < 6; ++j) acc[r][j] = make_float2(0.f, 0.f);
 
 #pragma unroll 2
   for (int c4 = 0; c4 < kDim / 4; ++c4) {
@@ -464,12 +467,13 @@ __global__ void __launch_bounds__(512, 1)
       const float4 q0 = *reinterpret_cast<const float4*>(prow);
       const float4 q1 = *reinterpret_cast<const float4*>(prow + 4);
       const float4 q2 = *reinterpret_cast<const float4*>(prow + 8);
-      const float pv[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+      const float2 pv[6] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y),
+                            make_float2(q1.z, q1.w), make_float2(q2.x, q2.y), make_float2(q2.z, q2.w)};
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const float av = cc == 0 ? a[r].x : cc == 1 ? a[r].y : cc == 2 ? a[r].z : a[r].w;
 #pragma unroll
-        for (int j = 0; j < 12; ++j) acc[r][j] = fmaf(av, pv[j], acc[r][j]);
+        for (int j = 0; j < 6; ++j) acc[r][j] = __ffma2_rn(make_float2(av, av), pv[j], acc[r][j]);
       }
     }
   }
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(512, 1)
       for (int j = 0; j < 12; ++j) {
         const int p = pg * 12 + j;
         if (p < np) {
-          const float s = acc[r][j];
+          const float s = (j & 1) ? acc[r][j >> 1].y : acc[r][j >> 1].x;
           const float B = fmaf(bn, sPn[p], kDotBoundAbs);
           if (s > B) {
             bits |= 1u << j;
@@ -640,6 +644,9 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp
   return v;
 }
 
+// Buckets are laid out padded to a multiple of 4 entries (16-byte aligned
+// slot runs, so a bucket's slots and codes can be fetched by bulk copies);
+// pad entries hold train index kEmpty, which makes their match key kEmpty.
 __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry;
@@ -647,14 +654,21 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
   const int t = blockIdx.y;
   uint32_t* off = im.offsets + (size_t)t * (h.n_buckets + 1);
   uint32_t* cur = im.cursor + (size_t)t * h.n_buckets;
+  uint32_t* slots = im.slots + (size_t)t * im.ns;
+  uint64_t* bfine = im.bfine + (size_t)t * im.ns * h.fwp;
   uint32_t carry = 0;
   for (int base = 0; base < h.n_buckets; base += blockDim.x) {
     const int b = base + threadIdx.x;
     const uint32_t v = b < h.n_buckets ? off[b + 1] : 0u;
-    const uint32_t incl = block_incl_scan(v, s_warp) + carry;
+    const uint32_t pv = (v + 3u) & ~3u;
+    const uint32_t incl = block_incl_scan(pv, s_warp) + carry;
     if (b < h.n_buckets) {
       off[b + 1] = incl;
-      cur[b] = incl - v;
+      cur[b] = incl - pv;
+      for (uint32_t k = incl - pv + v; k < incl; ++k) {
+        slots[k] = kEmpty;
+        for (int x = 0; x < h.fwp; ++x) bfine[(size_t)k * h.fwp + x] = 0ull;
+      }
     }
     if (threadIdx.x == blockDim.x - 1) s_carry = incl;
     __syncthreads();
@@ -672,7 +686,7 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
   for (int t = 0; t < h.tables; ++t) {
     const uint32_t b = im.coarse[(size_t)i * h.tables + t];
     const uint32_t pos = atomicAdd(im.cursor + (size_t)t * h.n_buckets + b, 1u);
-    const size_t si = (size_t)t * im.n + pos;
+    const size_t si = (size_t)t * im.ns + pos;
     im.slots[si] = i;
     // the fine code again in slot order: the matcher's candidate walk then
     // reads consecutive entries (coalesced) instead of gathering by index
@@ -730,22 +744,15 @@ __device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint
   return h;
 }
 
-// Chunk descriptors of one warp: (first slot index, length) of up to 32
-// chunks of the current page, zero-length past the page (read up to index
-// 35 by the look-ahead), plus the tables' chunk ends for the page build.
-constexpr int kChunkSlots = 40;
-struct WalkSmem {
-  uint2 cd[kChunkSlots];
-  uint32_t cend[kMaxTables];
-};
-
 // Walks the union; round(valid, key) is called by every lane once per round
-// (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket
-// range; other lanes hold zeros.  key = hamming * 2^ib + train_idx, or
-// kEmpty for lanes without an entry this round.
+// (warp-uniform trip count).  lo / sz: lane t < L holds table t's (padded)
+// bucket range; other lanes hold zeros.  key = hamming << ib | train_idx;
+// pad entries and lanes without an entry carry idx kEmpty, so their key is
+// kEmpty.  Chunk descriptors live in registers, one chunk per lane, and are
+// fetched per round with two shuffles; loads run one round ahead.
 template <int FWP, typename F>
-__device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, uint32_t mul,
-                                           const uint64_t (&qc)[FWP], WalkSmem& ws, F&& round) {
+__device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, int ib,
+                                           const uint64_t (&qc)[FWP], F&& round) {
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const uint32_t nch = (sz + 7u) >> 3;
   uint32_t cend = nch;  // inclusive scan of the chunk counts over tables
@@ -755,58 +762,48 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   }
   const uint32_t n_chunks = __shfl_sync(kFull, cend, L - 1);
   const uint32_t cstart = cend - nch;
-  const uint32_t sbase = (uint32_t)lane * T.n + lo;
-  if (lane < L) ws.cend[lane] = cend;
-  __syncwarp();
+  const uint32_t sbase = (uint32_t)lane * T.ns + lo;
   for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
-    // lane j describes chunk pg + j: its table is the number of tables
-    // ending at or before it
+    // lane j describes chunk pg + j: table = #tables ending at or before it
     const uint32_t k = pg + lane;
     uint32_t t = 0;
-    for (int tt = 0; tt < L - 1; ++tt) t += ws.cend[tt] <= k ? 1u : 0u;
+    for (int tt = 0; tt < L - 1; ++tt) t += __shfl_sync(kFull, cend, tt) <= k ? 1u : 0u;
     const uint32_t ts = __shfl_sync(kFull, cstart, t);
     const uint32_t tb = __shfl_sync(kFull, sbase, t);
     const uint32_t tz = __shfl_sync(kFull, sz, t);
     const uint32_t o8 = (k - ts) * 8u;
-    ws.cd[lane] = make_uint2(tb + o8, k < n_chunks ? min(8u, tz - o8) : 0u);
-    __syncwarp();
+    const uint32_t my_base = tb + o8;
+    const uint32_t my_len = k < n_chunks ? min(8u, tz - o8) : 0u;
     const uint32_t nr = (min(32u, n_chunks - pg) + 3u) >> 2;
-    uint2 d = ws.cd[grp];
-    bool v = (uint32_t)sub < d.y;
+    const uint32_t base = __shfl_sync(kFull, my_base, grp);
+    bool v = (uint32_t)sub < __shfl_sync(kFull, my_len, grp);
     uint32_t j = kEmpty;
     uint64_t cw[FWP];
-#pragma unroll
-    for (int x = 0; x < FWP; ++x) cw[x] = qc[x];
     if (v) {
-      const uint32_t si = d.x + sub;
-      j = __ldg(T.slots + si);
-      load_code<FWP>(T.bfine + (size_t)si * FWP, cw);
+      j = __ldg(T.slots + (base + sub));
+      load_code<FWP>(T.bfine + (size_t)(base + sub) * FWP, cw);
     }
-#pragma unroll 2
     for (uint32_t r = 0; r < nr; ++r) {
-      // next round's chunk (entries past the page have length 0)
-      const uint2 dn = ws.cd[4 * r + 4 + grp];
-      const bool nv = (uint32_t)sub < dn.y;
+      const int kk = min(4 * (int)(r + 1) + grp, 31);
+      const uint32_t nbase = __shfl_sync(kFull, my_base, kk);
+      const bool nv = r + 1 < nr && (uint32_t)sub < __shfl_sync(kFull, my_len, kk);
       uint32_t jn = kEmpty;
       uint64_t cn[FWP];  // only read when nv
       if (nv) {
-        const uint32_t si = dn.x + sub;
-        jn = __ldg(T.slots + si);
-        load_code<FWP>(T.bfine + (size_t)si * FWP, cn);
+        jn = __ldg(T.slots + (nbase + sub));
+        load_code<FWP>(T.bfine + (size_t)(nbase + sub) * FWP, cn);
       }
-      round(v, v ? hamming<FWP>(qc, cw) * mul + j : kEmpty);
+      round(v, (hamming<FWP>(qc, cw) << ib) | j);
       v = nv;
       j = jn;
 #pragma unroll
       for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
     }
-    __syncwarp();
   }
 }
 
 template <int FWP, int KM, int NT, int KC>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
-  __shared__ WalkSmem s_walk[NT / 32];
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];
@@ -814,9 +811,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   constexpr int kWarps = NT / 32;
 
   const int L = a.tables, K = KC ? KC : a.k, ib = a.idx_bits;
-  const uint32_t idx_mask = (1u << ib) - 1u, mul = 1u << ib;
-  WalkSmem& ws = s_walk[warp];
-  if (lane < kChunkSlots - 32) ws.cd[32 + lane] = make_uint2(0u, 0u);
+  const uint32_t idx_mask = (1u << ib) - 1u;
   const int nb1 = a.n_buckets + 1;
   const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
   const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
@@ -844,17 +839,18 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     bool exact = KM != 8;
     if constexpr (KM == 8) {
       uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
-      walk_union<FWP>(T, L, lo, sz, mul, qc, ws, [&](bool valid, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
         k3 = max(k2, min(k3, key));
         k2 = max(k1, min(k2, key));
         k1 = max(k0, min(k1, key));
         k0 = min(k0, key);
-        seen += valid ? 1u : 0u;
+        seen += key != kEmpty ? 1u : 0u;  // pad entries (kEmpty) are not candidates
       });
       // Copies of one key that landed in one lane sit next to each other:
       // squeeze them out so a lane's list is a prefix of its distinct keys.
       // Copies in different lanes are popped together below.
-      if ((k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty)) {
+      if (__any_sync(kFull, (k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) ||
+                                (k2 == k3 && k3 != kEmpty))) {
 #pragma unroll
         for (int rep = 0; rep < 3; ++rep) {
           if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
@@ -886,7 +882,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // tables is taken once.
       lst = kEmpty;
       uint32_t thr = kEmpty;
-      walk_union<FWP>(T, L, lo, sz, mul, qc, ws, [&](bool, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
         key = key < thr ? key : kEmpty;
         for (;;) {
           const uint32_t m = __reduce_min_sync(kFull, key);
@@ -1056,6 +1052,349 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 }
 
 // ---------------------------------------------------------------------------
+// K4b: the cascade with TMA-staged candidates (K <= 8, unions up to `cap`
+// entries).  CTA = 16 warps; a warp takes every 16th query of its range and
+// runs a software pipeline over them:
+//   * as soon as query i's union has been ranked, one bulk copy per table
+//     (cp.async.bulk, completing on an mbarrier) stages query i+1's bucket
+//     runs -- fine codes and train indices, padded to 4 entries -- into the
+//     warp's candidate buffer, back to back, so the union is one flat smem
+//     array (lands while query i-1's re-rank and query i's staging run);
+//   * query i's union is walked from shared memory (lane l takes entries
+//     l, l+32, ..): POPC Hamming, key = hamming << ib | idx (pad entries carry
+//     idx 0xffffffff, i.e. key kEmpty), per-lane top-4, REDUX pulls -- the
+//     same exact ranking as K4;
+//   * query i's K kept rows (and its own row) are bulk-copied into the warp's
+//     re-rank buffer and ranked one query later, after query i+1's walk, so
+//     the gather latency is hidden too.
+// Unions larger than `cap` take K4's global-memory chunked walk.
+// ---------------------------------------------------------------------------
+constexpr int kTmaWarps = 16;
+constexpr int kRowStride = 528;  // 512-byte row + 16: conflict-free LDS.128 across candidates
+constexpr int kRrBytes = 9 * kRowStride;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// generic-proxy accesses to a buffer are ordered before the async-proxy
+// (bulk copy) writes that recycle it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__host__ __device__ constexpr uint32_t tma_warp_bytes(uint32_t cap, int fwp) {
+  return cap * (8u * fwp + 4u) + kRrBytes + 16u;
+}
+
+template <int FWP, int KC>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunch a, uint32_t cap) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  constexpr uint32_t CB = 8u * FWP;
+  const PairWork w = a.work[blockIdx.x];
+  const ImgDev T = a.imgs[w.t_img];
+  const ImgDev Q = a.imgs[w.q_img];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = a.tables, K = KC ? KC : a.k, ib = a.idx_bits;
+  const uint32_t idx_mask = (1u << ib) - 1u;
+  const int nb1 = a.n_buckets + 1;
+  const double ratio = a.ratio;
+  const double r2 = ratio * ratio;
+
+  const uint32_t cand_bytes = cap * (CB + 4u);
+  unsigned char* wb = dsm + (size_t)warp * tma_warp_bytes(cap, FWP);
+  unsigned char* rr = wb + cand_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rr + kRrBytes);  // [0] candidates, [1] re-rank rows
+  if (lane == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t ph0 = 0, ph1 = 0;
+
+  const uint32_t q0 = w.q_begin + warp;
+  const uint32_t nqw = q0 < w.q_end ? (w.q_end - q0 + kTmaWarps - 1) / kTmaWarps : 0u;
+  auto qof = [&](uint32_t i) { return q0 + i * kTmaWarps; };
+  auto load_b = [&](uint32_t i) -> uint32_t {
+    return (lane < L && i < nqw) ? __ldg(Q.coarse + (size_t)qof(i) * L + lane) : 0u;
+  };
+  auto load_range = [&](uint32_t b, uint32_t i, uint32_t& lo, uint32_t& sz) {
+    lo = sz = 0;
+    if (lane < L && i < nqw) {
+      const uint32_t* off = T.offsets + (size_t)lane * nb1 + b;
+      lo = __ldg(off);
+      sz = __ldg(off + 1) - lo;
+    }
+  };
+  // stage a union into the candidate buffer: the flattened entry count
+  // rounded up to a multiple of 32 (slots past the union hold kEmpty), or
+  // kEmpty when it does not fit (the walk then reads global memory)
+  auto issue = [&](uint32_t lo, uint32_t sz) -> uint32_t {
+    uint32_t incl = sz;
+    for (int o = 1; o < L; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, L - 1);
+    const uint32_t padded = (total + 31u) & ~31u;
+    if (padded > cap) return kEmpty;
+    if (total == 0) return 0u;
+    uint32_t* slots = reinterpret_cast<uint32_t*>(wb + (size_t)cap * CB);
+    if (total + lane < padded) slots[total + lane] = kEmpty;
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(bars, total * (CB + 4u));
+    __syncwarp();
+    if (lane < L && sz) {
+      const uint32_t cum = incl - sz;
+      const size_t s0 = (size_t)lane * T.ns + lo;
+      bulk_g2s(wb + (size_t)cum * CB, T.bfine + s0 * FWP, sz * CB, bars);
+      bulk_g2s(slots + cum, T.slots + s0, sz * 4u, bars);
+    }
+    return padded;
+  };
+  auto walk_smem = [&](uint32_t padded, const uint64_t (&qc)[FWP], auto&& round) {
+    const uint32_t* slots = reinterpret_cast<const uint32_t*>(wb + (size_t)cap * CB) + lane;
+    const unsigned char* codes = wb + (size_t)lane * CB;
+#pragma unroll 2
+    for (uint32_t e0 = 0; e0 < padded; e0 += 32) {
+      const uint32_t j = slots[e0];
+      uint64_t c[FWP];
+      if constexpr (FWP % 2 == 0) {
+#pragma unroll
+        for (int x = 0; x < FWP / 2; ++x) {
+          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(codes + (size_t)e0 * CB)[x];
+          c[2 * x] = v.x;
+          c[2 * x + 1] = v.y;
+        }
+      } else {
+        c[0] = *reinterpret_cast<const uint64_t*>(codes + (size_t)e0 * CB);
+      }
+      round((hamming<FWP>(qc, c) << ib) | j);
+    }
+  };
+
+  // deferred re-rank of the previous query
+  uint32_t pq = kEmpty, plst = kEmpty;
+  int pkept = 0;
+  uint32_t n_matched = 0;
+  auto emit = [&](uint32_t q, int32_t result) {
+    if (lane == 0) {
+      a.dense[a.dense_off[w.pair] + q] = result;
+      n_matched += result >= 0 ? 1u : 0u;
+    }
+  };
+  auto finish = [&](uint32_t q, uint32_t lst, int kept) {
+    mbar_wait(bars + 1, ph1);
+    ph1 ^= 1u;
+    const bool mine = lane < kept;
+    const uint32_t my_idx = lst & idx_mask;
+    // lanes 4c..4c+3 hold candidate c (row c+1 of the buffer): lane part p
+    // covers float4s p, p+4, .., p+28 in two packed FP32x2 chains; every FP32
+    // sum has depth <= 13 (relative error ~1e-6, inside the 1e-5 margin)
+    const int ck = lane >> 2, part = lane & 3;
+    const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
+    float s = 0.f;
+    if (ck < kept) {
+      const float4* qp = reinterpret_cast<const float4*>(rr) + part;
+      const float4* tp = reinterpret_cast<const float4*>(rr + (ck + 1) * kRowStride) + part;
+      const float2 neg1 = make_float2(-1.f, -1.f);
+      float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 av = qp[4 * i], bv = tp[4 * i];
+        const float2 d0 = __ffma2_rn(make_float2(bv.x, bv.y), neg1, make_float2(av.x, av.y));
+        const float2 d1 = __ffma2_rn(make_float2(bv.z, bv.w), neg1, make_float2(av.z, av.w));
+        s0 = __ffma2_rn(d0, d0, s0);
+        s1 = __ffma2_rn(d1, d1, s1);
+      }
+      s = (s0.x + s0.y) + (s1.x + s1.y);
+    }
+    s += __shfl_xor_sync(kFull, s, 1);
+    s += __shfl_xor_sync(kFull, s, 2);
+    const bool lead = part == 0 && ck < kept;
+    const uint32_t sb = lead ? __float_as_uint(s) : kEmpty;
+    const uint32_t mb = __reduce_min_sync(kFull, sb);
+    const uint32_t i_min = __reduce_min_sync(kFull, (lead && sb == mb) ? jk : kEmpty);
+    const float s_min = __uint_as_float(mb);
+    const float s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
+    const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
+    const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
+    const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
+    const bool reject = finite && (double)s_min * lo_f >= r2 * ((double)s_2 * hi_f);
+    int32_t result = -1;
+    if (accept) {
+      result = (int32_t)i_min;
+    } else if (!reject) {
+      // FP64 reference path (hashmatch.cpp:35-42, :196-208)
+      double e = __longlong_as_double(0x7ff0000000000000ll);
+      if (mine) {
+        const float* qd = Q.desc + (size_t)q * kDim;
+        const float* td = T.desc + (size_t)my_idx * kDim;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < kDim; ++c) {
+          const double d = __dsub_rn((double)__ldg(qd + c), (double)__ldg(td + c));
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+        e = __dsqrt_rn(acc);
+      }
+      double be = e;
+      uint32_t bj = mine ? my_idx : 0xffffffffu;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(kFull, be, o);
+        const uint32_t oj = __shfl_xor_sync(kFull, bj, o);
+        if (oe < be || (oe == be && oj < bj)) {
+          be = oe;
+          bj = oj;
+        }
+      }
+      const double e_first = __shfl_sync(kFull, be, 0);
+      const uint32_t i_first = __shfl_sync(kFull, bj, 0);
+      double e2 = (mine && my_idx != i_first) ? e : __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(kFull, e2, o));
+      const double e_second = __shfl_sync(kFull, e2, 0);
+      if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
+      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
+    }
+    emit(q, result);
+  };
+
+  uint32_t lo_cur = 0, sz_cur = 0, lo_nx = 0, sz_nx = 0, tot_cur = 0;
+  {
+    const uint32_t b0 = load_b(0);
+    load_range(b0, 0, lo_cur, sz_cur);
+    if (nqw) tot_cur = issue(lo_cur, sz_cur);
+    const uint32_t b1 = load_b(1);
+    load_range(b1, 1, lo_nx, sz_nx);
+  }
+  uint32_t b_nn = load_b(2);
+  for (uint32_t i = 0; i < nqw; ++i) {
+    const uint32_t q = qof(i);
+    uint64_t qc[FWP];
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
+    const bool staged = tot_cur != kEmpty;
+    if (staged && tot_cur) {
+      mbar_wait(bars, ph0);
+      ph0 ^= 1u;
+    }
+
+    // ---- per-lane top-4, REDUX pulls (K4 fast path)
+    uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
+    auto ins = [&](uint32_t key) {
+      k3 = max(k2, min(k3, key));
+      k2 = max(k1, min(k2, key));
+      k1 = max(k0, min(k1, key));
+      k0 = min(k0, key);
+      seen += key != kEmpty ? 1u : 0u;
+    };
+    if (staged) walk_smem(tot_cur, qc, ins);
+    else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](bool, uint32_t key) { ins(key); });
+    if (__any_sync(kFull, (k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty))) {
+#pragma unroll
+      for (int rep = 0; rep < 3; ++rep) {
+        if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
+        if (k1 == k2) { k2 = k3; k3 = kEmpty; }
+        if (k2 == k3) k3 = kEmpty;
+      }
+    }
+    uint32_t lst = kEmpty;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < K) {
+        const uint32_t m = __reduce_min_sync(kFull, k0);
+        lst = lane == r ? m : lst;
+        const bool pop = k0 == m;
+        k0 = pop ? k1 : k0;
+        k1 = pop ? k2 : k1;
+        k2 = pop ? k3 : k2;
+        k3 = pop ? kEmpty : k3;
+      }
+    }
+    if (__any_sync(kFull, seen > 4u && k0 == kEmpty)) {
+      // exact path (see K4): REDUX-driven insertion into a sorted list
+      lst = kEmpty;
+      uint32_t thr = kEmpty;
+      auto exact = [&](uint32_t key) {
+        key = key < thr ? key : kEmpty;
+        for (;;) {
+          const uint32_t m = __reduce_min_sync(kFull, key);
+          if (m >= thr) break;
+          if (key == m) key = kEmpty;
+          if (!__any_sync(kFull, lane < 8 && lst == m)) {
+            const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
+            const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
+            lst = lane < 8 ? nv : kEmpty;
+            thr = __shfl_sync(kFull, lst, K - 1);
+          }
+        }
+      };
+      if (staged) walk_smem(tot_cur, qc, exact);
+      else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](bool, uint32_t key) { exact(key); });
+      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
+    }
+
+    // ---- the buffer is free: stage the next query's union; ranges and
+    // buckets further ahead
+    tot_cur = i + 1 < nqw ? issue(lo_nx, sz_nx) : 0u;
+    lo_cur = lo_nx;
+    sz_cur = sz_nx;
+    load_range(b_nn, i + 2, lo_nx, sz_nx);
+    b_nn = load_b(i + 3);
+
+    // ---- the previous query's re-rank (its rows have landed), then stage ours
+    if (pq != kEmpty) finish(pq, plst, pkept);
+    pq = kEmpty;
+    const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
+    if (kept == 1) {
+      emit(q, (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask));
+    } else if (kept == 0) {
+      emit(q, -1);
+    } else {
+      const uint32_t jc = __shfl_sync(kFull, lst, (lane + 31) & 31) & idx_mask;
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(bars + 1, (uint32_t)(kept + 1) * 512u);
+      __syncwarp();
+      if (lane <= kept) {
+        const float* src = lane == 0 ? Q.desc + (size_t)q * kDim : T.desc + (size_t)jc * kDim;
+        bulk_g2s(rr + lane * kRowStride, src, 512u, bars + 1);
+      }
+      pq = q;
+      plst = lst;
+      pkept = kept;
+    }
+  }
+  if (pq != kEmpty) finish(pq, plst, pkept);
+  if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
+}
+
+// ---------------------------------------------------------------------------
 // K6: per-launch exclusive scan of match counts (appending after the running
 // total of earlier rows) and ascending-query compaction of the dense arrays.
 // ---------------------------------------------------------------------------
@@ -1200,11 +1539,49 @@ static void launch_match_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
   match_kernel<FWP, KM, NT, KC><<<n_work, NT, 0, s>>>(a);
 }
 
+// staged-union capacity that fits kTmaWarps warps in shared memory
+static uint32_t tma_cap(int fwp) {
+  const int budget = 227 * 1024 - 2048;
+  const int per = budget / kTmaWarps - kRrBytes - 16;
+  return (uint32_t)(per / (8 * fwp + 4)) & ~31u;
+}
+
+template <int FWP, int KC>
+static void launch_tma_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
+  const uint32_t cap = tma_cap(FWP);
+  const size_t smem = (size_t)kTmaWarps * tma_warp_bytes(cap, FWP);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(match_tma_kernel<FWP, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  match_tma_kernel<FWP, KC><<<n_work, kTmaWarps * 32, smem, s>>>(a, cap);
+}
+
 template <int FWP>
 static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  if (a.k == 8) launch_match_t<FWP, 8, kMatchThreads, 8>(a, n_work, s);  // MatchParams default
-  else if (a.k < 8) launch_match_t<FWP, 8, kMatchThreads, 0>(a, n_work, s);
-  else launch_match_t<FWP, 32, 512, 0>(a, n_work, s);
+  static const bool tma = [] {
+    const char* v = getenv("BMG_MATCH_TMA");  // A/B switch: the TMA-staged K4b
+    return v && v[0] == '1';
+  }();
+  if (tma && FWP <= 4 && a.k <= 8) {
+    if (a.k == 8) launch_tma_t<FWP, 8>(a, n_work, s);  // MatchParams default
+    else launch_tma_t<FWP, 0>(a, n_work, s);
+  } else if (a.k == 8) {
+    launch_match_t<FWP, 8, kMatchThreads, 8>(a, n_work, s);
+  } else if (a.k < 8) {
+    launch_match_t<FWP, 8, kMatchThreads, 0>(a, n_work, s);
+  } else {
+    launch_match_t<FWP, 32, 512, 0>(a, n_work, s);
+  }
+}
+
+int match_queries_per_cta(int fwp, int k) {
+  static const bool tma = [] {
+    const char* v = getenv("BMG_MATCH_TMA");
+    return v && v[0] == '1';
+  }();
+  return (tma && fwp <= 4 && k <= 8) ? kTmaQueries : kMatchQueries;
 }
 
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
