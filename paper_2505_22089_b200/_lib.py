@@ -6,12 +6,13 @@ device is present, the entry points raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libbmg.so"
+LIB_PATH = Path(os.environ["BMG_LIBBMG"]) if os.environ.get("BMG_LIBBMG") else PKG / "libbmg.so"
 DIM = 128
 
 STATUS_NAMES = {

@@ -562,7 +562,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   for (int i = 0; i < n_imgs; ++i) {
     lay[i].cursor_off = off;
     off = align_up(off + L * NB * 4, 256);
-    const uint64_t ns = slot_stride(descs[i].second, h.n_buckets);
+    const uint64_t ns = slot_stride(descs[i].second, h.n_buckets, h.bucket_pad);
     lay[i].slots_off = off;
     off = align_up(off + ns * L * 4, 256);
     lay[i].bfine_off = off;
@@ -582,7 +582,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
     im.slots = reinterpret_cast<uint32_t*>(base + lay[i].slots_off);
     im.bfine = reinterpret_cast<uint64_t*>(base + lay[i].bfine_off);
     im.overflow = 0;
-    im.ns = slot_stride(im.n, h.n_buckets);
+    im.ns = slot_stride(im.n, h.n_buckets, h.bucket_pad);
   }
   // metadata
   ImgDev* h_imgs = c.ring.alloc<ImgDev>(std::max(n_imgs, 1), c.S().s_comp, c.s_copy);
@@ -782,6 +782,7 @@ HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const 
   h.fwp = padded_words(h.fw);
   h.n_buckets = 1 << p.coarse_bits;
   h.n_planes_pad = static_cast<int>(align_up(h.n_planes, kPlaneChunk));
+  h.bucket_pad = match_tma_enabled() ? 4 : 1;
   const int np = h.n_planes, npp = h.n_planes_pad;
   std::vector<float> planes(static_cast<size_t>(np) * kDim), planes_t(static_cast<size_t>(npp) * kDim, 0.f),
       norm(npp, 0.f);
@@ -1136,7 +1137,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
       const size_t off_begin = oo[0], off_end = off;
       for (int i = 0; i < 2; ++i) {
         cu[i] = off; off = align_up(off + L * NB * 4, 256);
-        const uint64_t ns = slot_stride(two[i].second, h.n_buckets);
+        const uint64_t ns = slot_stride(two[i].second, h.n_buckets, h.bucket_pad);
         so[i] = off; off = align_up(off + ns * L * 4, 256);
         bo[i] = off; off = align_up(off + ns * L * h.fwp * 8, 256);
       }
@@ -1153,7 +1154,7 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
         im.cursor = reinterpret_cast<uint32_t*>(base + cu[i]);
         im.slots = reinterpret_cast<uint32_t*>(base + so[i]);
         im.bfine = reinterpret_cast<uint64_t*>(base + bo[i]);
-        im.ns = slot_stride(im.n, h.n_buckets);
+        im.ns = slot_stride(im.n, h.n_buckets, h.bucket_pad);
         c->S().row_imgs.push_back(im);
         const uint64_t n = two[i].second;
         for (uint64_t j = 0; j < n * L; ++j)

@@ -35,6 +35,7 @@ struct HashDev {
   const float* planes;     // [n_planes][128] planes (coarse first, then fine)
   const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
   int n_planes_pad;
+  int bucket_pad;          // buckets padded to a multiple of this (4 for the TMA-staged matcher, else 1)
 };
 
 // An ambiguous projection whose sign the FP32 pass could not certify; the
@@ -85,10 +86,12 @@ struct MetaBatch {
 };
 void launch_meta(const MetaBatch& b, cudaStream_t s);
 
-// per-table slot capacity with every bucket padded to a multiple of 4
-inline uint32_t slot_stride(uint64_t n, int n_buckets) {
-  return static_cast<uint32_t>((n + 3ull * static_cast<uint64_t>(n_buckets) + 3ull) & ~3ull);
+// per-table slot capacity with every bucket padded to a multiple of `pad`
+inline uint32_t slot_stride(uint64_t n, int n_buckets, int pad) {
+  return static_cast<uint32_t>((n + (pad - 1ull) * static_cast<uint64_t>(n_buckets) + 3ull) & ~3ull);
 }
+// whether the TMA-staged matcher (K4b, needs 4-entry bucket padding) is on
+bool match_tma_enabled();
 
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
@@ -117,7 +120,10 @@ void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint3
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
 constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)
 constexpr int kMatchThreads = 1024;  // 32 warps, one query per warp at a time
-constexpr int kMatchQueries = 256;   // queries per match CTA (short CTAs: a higher-priority row gets SMs soon)
+#ifndef BMG_MATCH_QUERIES
+#define BMG_MATCH_QUERIES 1024
+#endif
+constexpr int kMatchQueries = BMG_MATCH_QUERIES;  // queries per match CTA
 constexpr int kTmaQueries = 1024;    // queries per TMA-staged match CTA (16 warps)
 // queries per CTA of the match kernel launch_match picks for (fwp, k)
 int match_queries_per_cta(int fwp, int k);

@@ -644,9 +644,10 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp
   return v;
 }
 
-// Buckets are laid out padded to a multiple of 4 entries (16-byte aligned
-// slot runs, so a bucket's slots and codes can be fetched by bulk copies);
-// pad entries hold train index kEmpty, which makes their match key kEmpty.
+// With the TMA-staged matcher, buckets are laid out padded to a multiple of
+// 4 entries (16-byte aligned slot runs, so a bucket's slots and codes can be
+// fetched by bulk copies); pad entries hold train index kEmpty, which makes
+// their match key kEmpty.
 __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry;
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
   for (int base = 0; base < h.n_buckets; base += blockDim.x) {
     const int b = base + threadIdx.x;
     const uint32_t v = b < h.n_buckets ? off[b + 1] : 0u;
-    const uint32_t pv = (v + 3u) & ~3u;
+    const uint32_t pv = (v + (uint32_t)h.bucket_pad - 1u) / (uint32_t)h.bucket_pad * (uint32_t)h.bucket_pad;
     const uint32_t incl = block_incl_scan(pv, s_warp) + carry;
     if (b < h.n_buckets) {
       off[b + 1] = incl;
@@ -784,9 +785,11 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
       load_code<FWP>(T.bfine + (size_t)(base + sub) * FWP, cw);
     }
     for (uint32_t r = 0; r < nr; ++r) {
+      // both shuffles unconditional (no divergence around them)
       const int kk = min(4 * (int)(r + 1) + grp, 31);
       const uint32_t nbase = __shfl_sync(kFull, my_base, kk);
-      const bool nv = r + 1 < nr && (uint32_t)sub < __shfl_sync(kFull, my_len, kk);
+      const uint32_t nlen = __shfl_sync(kFull, my_len, kk);
+      const bool nv = (r + 1 < nr) & ((uint32_t)sub < nlen);
       uint32_t jn = kEmpty;
       uint64_t cn[FWP];  // only read when nv
       if (nv) {
@@ -1558,12 +1561,17 @@ static void launch_tma_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
   match_tma_kernel<FWP, KC><<<n_work, kTmaWarps * 32, smem, s>>>(a, cap);
 }
 
-template <int FWP>
-static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
+bool match_tma_enabled() {
   static const bool tma = [] {
     const char* v = getenv("BMG_MATCH_TMA");  // A/B switch: the TMA-staged K4b
     return v && v[0] == '1';
   }();
+  return tma;
+}
+
+template <int FWP>
+static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
+  const bool tma = match_tma_enabled();
   if (tma && FWP <= 4 && a.k <= 8) {
     if (a.k == 8) launch_tma_t<FWP, 8>(a, n_work, s);  // MatchParams default
     else launch_tma_t<FWP, 0>(a, n_work, s);
@@ -1577,11 +1585,7 @@ static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
 }
 
 int match_queries_per_cta(int fwp, int k) {
-  static const bool tma = [] {
-    const char* v = getenv("BMG_MATCH_TMA");
-    return v && v[0] == '1';
-  }();
-  return (tma && fwp <= 4 && k <= 8) ? kTmaQueries : kMatchQueries;
+  return (match_tma_enabled() && fwp <= 4 && k <= 8) ? kTmaQueries : kMatchQueries;
 }
 
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {

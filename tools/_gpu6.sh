@@ -6,4 +6,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 tail -1 gpurun_out/$t/pytest_gpu.log
 python -c "import json;d=json.load(open('gpurun_out/$t/bench.json'));print('value',round(d['value']),'e2e',round(d['e2e']['value']), d['ms_per_step'])"
 python tools/ncu_summary.py --round tmp --launches gpurun_out/$t/launches.csv | tail -22
-git checkout profiles 2>/dev/null
+
