@@ -156,6 +156,9 @@ typedef struct {
  * flag computes them with the literal sequential FP64 chain instead (the
  * fallback path, exposed as a test hook -- results are identical). */
 #define BMG_EXEC_MEAN_CHAIN 2u
+/* Run every row on one stream (no overlap of consecutive rows): used to time
+ * kernels in isolation; results are identical. */
+#define BMG_EXEC_SERIAL 4u
 
 /* ---- status ------------------------------------------------------------ */
 const char* bmg_status_name(int status);              /* "InvalidArgument", ... */

@@ -916,6 +916,11 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
     BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    // never make an upload wait for the compute stream that freed the memory
+    // it would reuse (the DeviceArena's capacity accounting is logical; the
+    // physical pool may grow so the next row's H2D overlaps this row's work)
+    int no = 0;
+    BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &no));
     c->stage_bytes = 8u << 20;
     for (int i = 0; i < 2; ++i) {
       BMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage[i]), c->stage_bytes));
@@ -1287,7 +1292,7 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
       uint64_t it_pairs = 0;
       for (uint64_t r = 0; r < plan->rows_per_iteration[it]; ++r, ++row) {
-        c->cur = static_cast<int>(row & 1);
+        c->cur = (opts->flags & BMG_EXEC_SERIAL) ? 0 : static_cast<int>(row & 1);
         RowSlot& S = c->S();
         const uint64_t nb = plan->row_needed_offsets[row], ne = plan->row_needed_offsets[row + 1];
         const uint64_t* needed = plan->needed_ids + nb;

@@ -205,6 +205,7 @@ class ExecuteOptions:
     on_upload: object = None  # DeviceBackend::on_upload(image_id, units)
     on_evict: object = None   # DeviceBackend::on_evict(image_id)
     retain: bool = False      # keep images resident (skip eviction directives)
+    serial: bool = False      # all rows on one stream (kernel timing; same results)
     # row means: "exact" (parallel F96 reconstruction, the default) or
     # "chain" (the literal sequential FP64 chain; a test hook, same results)
     mean: str = "exact"
@@ -213,7 +214,8 @@ class ExecuteOptions:
         modes = {"exact": 0, "chain": _lib.EXEC_MEAN_CHAIN}
         if self.mean not in modes:
             raise BandmatchError("InvalidArgument", f"unknown mean mode {self.mean!r}")
-        return (_lib.EXEC_RETAIN if self.retain else 0) | modes[self.mean]
+        return ((_lib.EXEC_RETAIN if self.retain else 0) | (_lib.EXEC_SERIAL if self.serial else 0)
+                | modes[self.mean])
 
 
 @dataclass
