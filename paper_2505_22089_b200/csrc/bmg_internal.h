@@ -118,8 +118,11 @@ void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint3
                     const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);
 
 constexpr int kCodesTile = 128;   // descriptors per codes CTA
-constexpr int kPlaneChunk = 192;  // planes per codes CTA (grid.y covers the rest)
-constexpr int kMatchThreads = 1024;  // 32 warps, one query per warp at a time
+constexpr int kPlaneChunk = 180;  // planes per codes CTA: 15 warps x 12 (grid.y covers the rest)
+#ifndef BMG_MATCH_THREADS
+#define BMG_MATCH_THREADS 1024
+#endif
+constexpr int kMatchThreads = BMG_MATCH_THREADS;  // one query per warp at a time
 #ifndef BMG_MATCH_QUERIES
 #define BMG_MATCH_QUERIES 1024
 #endif

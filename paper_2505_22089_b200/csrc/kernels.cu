@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(32, 1) mean_chain_kernel(const ImgDev* __restr
 // in [-B, B] goes to the FP64 fixup list.
 // ---------------------------------------------------------------------------
 constexpr int kAStride = 132;
-constexpr int kMaskWords = kPlaneChunk / 32 + 2;  // +2 guard words for 64-bit extracts
+constexpr int kMaskWords = (kPlaneChunk + 31) / 32 + 2;  // +2 guard words for 64-bit extracts
 constexpr float kDotBound = 8.0e-6f;
 constexpr float kDotBoundAbs = 1.0e-37f;
 
@@ -396,151 +396,231 @@ __device__ __forceinline__ uint64_t extract_bits(const uint32_t* w, int start, i
   return len >= 64 ? v : (v & ((1ull << len) - 1ull));
 }
 
+// Persistent, TMA-fed: a CTA keeps its plane chunk in shared memory and walks
+// descriptor tiles t = blockIdx.x, +gridDim.x, ..; the next-but-one tile's
+// rows arrive by cp.async.bulk (one 512-byte copy per row, 528-byte smem
+// stride) into the other buffer while this one is projected.
+constexpr int kTileStride = kAStride;  // floats per staged row (528 B: conflict-free LDS.128)
+
+__device__ __forceinline__ uint32_t cvta_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 __global__ void __launch_bounds__(512, 1)
     codes_kernel(HashDev h, const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
-                 const uint32_t* __restrict__ tile_start, const float* __restrict__ mean,
-                 Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
-                 uint32_t* __restrict__ overflow) {
-  extern __shared__ __align__(16) float smem_f[];
-  float* sP = smem_f;                                  // [128][192]
-  float* sA = sP + kDim * kPlaneChunk;                 // [128][132]
-  float* sNrm = sA + kCodesTile * kAStride;            // [128]
+                 const uint32_t* __restrict__ tile_start, int n_tiles, int pstride,
+                 const float* __restrict__ mean, Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count,
+                 uint32_t fix_cap, uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(128) float smem_f[];
+  float* sT = smem_f;                                  // [2][128][132] staged tiles (masks overlay)
+  float* sP = sT + 2 * kCodesTile * kTileStride;       // [128][pstride]
+  float* sNrm = sP + kDim * pstride;                   // [128]
   float* sPn = sNrm + kCodesTile;                      // [192]
   float* sMean = sPn + kPlaneChunk;                    // [128]
-  uint32_t* sMask = reinterpret_cast<uint32_t*>(sMean + kDim);  // [128][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMean + kDim);  // [2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t img = tile_img[blockIdx.x];
-  const ImgDev im = imgs[img];
-  const uint32_t i0 = tile_start[blockIdx.x];
-  const int nd = min(kCodesTile, (int)(im.n - i0));
   const int p0 = blockIdx.y * kPlaneChunk;
   const int np = min(kPlaneChunk, h.n_planes - p0);
   const bool single_chunk = gridDim.y == 1;
+  const int n_groups = (np + 11) / 12;  // warps with planes to project
 
-  // planes chunk -> smem (coalesced float4 rows of the transposed matrix)
-  for (int e = tid; e < kDim * (kPlaneChunk / 4); e += blockDim.x) {
-    const int c = e / (kPlaneChunk / 4), q4 = e % (kPlaneChunk / 4);
-    reinterpret_cast<float4*>(sP)[e] =
-        __ldg(reinterpret_cast<const float4*>(h.planes_t + (size_t)c * h.n_planes_pad + p0) + q4);
+  // stage tile t's rows into buffer k (warp 0)
+  auto issue = [&](int t, int k) {
+    const ImgDev im = imgs[tile_img[t]];
+    const uint32_t i0 = tile_start[t];
+    const int nd = min(kCodesTile, (int)(im.n - i0));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cvta_smem(bars + k)),
+                   "r"((uint32_t)nd * 512u)
+                   : "memory");
+    __syncwarp();
+    for (int r = lane; r < nd; r += 32)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+              cvta_smem(sT + ((size_t)k * kCodesTile + r) * kTileStride)),
+          "l"(im.desc + (size_t)(i0 + r) * kDim), "r"(cvta_smem(bars + k))
+          : "memory");
+  };
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(bars + 0)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(bars + 1)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int e = tid; e < kPlaneChunk; e += blockDim.x) sPn[e] = __ldg(h.plane_norm + p0 + e);
+  __syncthreads();
+  if (warp == 0) {
+    if ((int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < n_tiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  // planes chunk -> smem (row c: planes p0 .. p0+pstride, zero past np)
+  for (int e = tid; e < kDim * pstride; e += blockDim.x) {
+    const int c = e / pstride, q = e % pstride;
+    sP[e] = q < np ? __ldg(h.planes_t + (size_t)c * h.n_planes_pad + p0 + q) : 0.f;
+  }
+  for (int e = tid; e < kPlaneChunk; e += blockDim.x) sPn[e] = e < np ? __ldg(h.plane_norm + p0 + e) : 0.f;
   if (tid < kDim) sMean[tid] = mean[tid];
-  for (int e = tid; e < kCodesTile * kMaskWords; e += blockDim.x) sMask[e] = 0u;
   __syncthreads();
 
-  // centered descriptor tile + norms (one warp per row, float4 per lane)
-  for (int r = warp; r < kCodesTile; r += 16) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < nd) {
-      const float4 d = __ldg(reinterpret_cast<const float4*>(im.desc + (size_t)(i0 + r) * kDim) + lane);
-      const float4 m = reinterpret_cast<const float4*>(sMean)[lane];
-      a = make_float4(d.x - m.x, d.y - m.y, d.z - m.z, d.w - m.w);
+  uint32_t ph0 = 0, ph1 = 0;
+  int k = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, k ^= 1) {
+    const uint32_t img = tile_img[t];
+    const ImgDev im = imgs[img];
+    const uint32_t i0 = tile_start[t];
+    const int nd = min(kCodesTile, (int)(im.n - i0));
+    float* sA = sT + (size_t)k * kCodesTile * kTileStride;
+    {
+      const uint32_t par = k ? ph1 : ph0;
+      const uint32_t a = cvta_smem(bars + k);
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(par)
+            : "memory");
+      }
+      if (k) ph1 ^= 1u;
+      else ph0 ^= 1u;
     }
-    *reinterpret_cast<float4*>(sA + r * kAStride + 4 * lane) = a;
-    float ss = a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+    // center in place + row norms: thread (row, quarter) covers 32 floats
+    {
+      const int r = tid >> 2, qq = tid & 3;
+      float4* row = reinterpret_cast<float4*>(sA + r * kTileStride + qq * 32);
+      const float4* mq = reinterpret_cast<const float4*>(sMean + qq * 32);
+      float ss = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
-    if (lane == 0) sNrm[r] = sqrtf(ss) * 1.00001f;
-  }
-  __syncthreads();
+      for (int i = 0; i < 8; ++i) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < nd) {
+          const float4 d = row[i], m = mq[i];
+          v = make_float4(d.x - m.x, d.y - m.y, d.z - m.z, d.w - m.w);
+        }
+        row[i] = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+      ss += __shfl_xor_sync(kFull, ss, 1);
+      ss += __shfl_xor_sync(kFull, ss, 2);
+      if (qq == 0) sNrm[r] = sqrtf(ss) * 1.00001f;
+    }
+    __syncthreads();
 
-  const int pg = warp;  // 16 plane groups x 12 planes
-  // packed FP32x2 FMAs (FFMA2, the descriptor value broadcast to both
-  // halves): plane pair jp of row r accumulates in acc[r][jp]; every output
-  // is still one FP32 FMA chain over c = 0..127 in order (same certificate)
-  float2 acc[4][6];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int j = 0; j < 6; ++j) acc[r][j] = make_float2(0.f, 0.f);
-
-#pragma unroll 2
-  for (int c4 = 0; c4 < kDim / 4; ++c4) {
-    float4 a[4];
+    const int pg = warp;  // plane groups of 12 (warp 15 idles: 180 = 15 x 12)
+    // packed FP32x2 FMAs (FFMA2, the descriptor value broadcast to both
+    // halves): plane pair jp of row r accumulates in acc[r][jp]; every output
+    // is one FP32 FMA chain over c = 0..127 in order (the certificate's model)
+    float2 acc[4][6];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
-      a[r] = *reinterpret_cast<const float4*>(sA + (r * 32 + lane) * kAStride + c4 * 4);
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      const float* prow = sP + (c4 * 4 + cc) * kPlaneChunk + pg * 12;
-      const float4 q0 = *reinterpret_cast<const float4*>(prow);
-      const float4 q1 = *reinterpret_cast<const float4*>(prow + 4);
-      const float4 q2 = *reinterpret_cast<const float4*>(prow + 8);
-      const float2 pv[6] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y),
-                            make_float2(q1.z, q1.w), make_float2(q2.x, q2.y), make_float2(q2.z, q2.w)};
+      for (int j = 0; j < 6; ++j) acc[r][j] = make_float2(0.f, 0.f);
+    if (pg < n_groups) {
+#pragma unroll 2
+      for (int c4 = 0; c4 < kDim / 4; ++c4) {
+        float4 a[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float av = cc == 0 ? a[r].x : cc == 1 ? a[r].y : cc == 2 ? a[r].z : a[r].w;
+        for (int r = 0; r < 4; ++r)
+          a[r] = *reinterpret_cast<const float4*>(sA + (r * 32 + lane) * kTileStride + c4 * 4);
 #pragma unroll
-        for (int j = 0; j < 6; ++j) acc[r][j] = __ffma2_rn(make_float2(av, av), pv[j], acc[r][j]);
-      }
-    }
-  }
-
-  // certified signs -> per-descriptor plane mask in smem
+        for (int cc = 0; cc < 4; ++cc) {
+          const float* prow = sP + (c4 * 4 + cc) * pstride + pg * 12;
+          const float4 q0 = *reinterpret_cast<const float4*>(prow);
+          const float4 q1 = *reinterpret_cast<const float4*>(prow + 4);
+          const float4 q2 = *reinterpret_cast<const float4*>(prow + 8);
+          const float2 pv[6] = {make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y),
+                                make_float2(q1.z, q1.w), make_float2(q2.x, q2.y), make_float2(q2.z, q2.w)};
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int i = r * 32 + lane;
-    if (i < nd) {
-      const float bn = kDotBound * sNrm[i];
-      uint32_t bits = 0;
+          for (int r = 0; r < 4; ++r) {
+            const float av = cc == 0 ? a[r].x : cc == 1 ? a[r].y : cc == 2 ? a[r].z : a[r].w;
 #pragma unroll
-      for (int j = 0; j < 12; ++j) {
-        const int p = pg * 12 + j;
-        if (p < np) {
-          const float s = (j & 1) ? acc[r][j >> 1].y : acc[r][j >> 1].x;
-          const float B = fmaf(bn, sPn[p], kDotBoundAbs);
-          if (s > B) {
-            bits |= 1u << j;
-          } else if (!(s < -B)) {
-            const uint32_t slot = atomicAdd(fix_count, 1u);
-            if (slot < fix_cap) {
-              Fixup f;
-              f.img = img;
-              f.desc = i0 + i;
-              f.plane = p0 + p;
-              f.pad = 0;
-              fix[slot] = f;
-            } else {
-              atomicOr(overflow + img, 1u);
+            for (int j = 0; j < 6; ++j) {
+#ifdef BMG_CODES_FFMA1
+              acc[r][j].x = fmaf(av, pv[j].x, acc[r][j].x);
+              acc[r][j].y = fmaf(av, pv[j].y, acc[r][j].y);
+#else
+              acc[r][j] = __ffma2_rn(make_float2(av, av), pv[j], acc[r][j]);
+#endif
             }
           }
         }
       }
-      if (bits) {
-        const int off = pg * 12, wi = off >> 5, sh = off & 31;
-        atomicOr(&sMask[i * kMaskWords + wi], bits << sh);
-        if (sh > 20) atomicOr(&sMask[i * kMaskWords + wi + 1], bits >> (32 - sh));
-      }
     }
-  }
-  __syncthreads();
+    __syncthreads();  // the tile is consumed: its buffer now holds the masks
+    uint32_t* sMask = reinterpret_cast<uint32_t*>(sA);  // [128][kMaskWords]
+    for (int e = tid; e < kCodesTile * kMaskWords; e += blockDim.x) sMask[e] = 0u;
+    __syncthreads();
 
-  // assemble coarse bucket ids and fine words (4 threads per descriptor)
-  const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
-  const int n_words = L + h.fwp;
-  for (int e = tid; e < nd * n_words; e += blockDim.x) {
-    const int i = e / n_words, wd = e % n_words;
-    const uint32_t* mk = sMask + i * kMaskWords;
-    const size_t gi = i0 + i;
-    if (wd < L) {
-      const int lo = max(wd * m, p0), hi = min(wd * m + m, p0 + np);
-      if (lo < hi) {
-        const uint32_t v = (uint32_t)(extract_bits(mk, lo - p0, hi - lo) << (lo - wd * m));
-        if (single_chunk) im.coarse[gi * L + wd] = v;
-        else if (v) atomicOr(im.coarse + gi * L + wd, v);
+    // certified signs -> per-descriptor plane mask in smem
+    if (pg < n_groups) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = r * 32 + lane;
+        if (i < nd) {
+          const float bn = kDotBound * sNrm[i];
+          uint32_t bits = 0;
+#pragma unroll
+          for (int j = 0; j < 12; ++j) {
+            const int p = pg * 12 + j;
+            if (p < np) {
+              const float sv = (j & 1) ? acc[r][j >> 1].y : acc[r][j >> 1].x;
+              const float B = fmaf(bn, sPn[p], kDotBoundAbs);
+              if (sv > B) {
+                bits |= 1u << j;
+              } else if (!(sv < -B)) {
+                const uint32_t slot = atomicAdd(fix_count, 1u);
+                if (slot < fix_cap) {
+                  Fixup f;
+                  f.img = img;
+                  f.desc = i0 + i;
+                  f.plane = p0 + p;
+                  f.pad = 0;
+                  fix[slot] = f;
+                } else {
+                  atomicOr(overflow + img, 1u);
+                }
+              }
+            }
+          }
+          if (bits) {
+            const int off = pg * 12, wi = off >> 5, sh = off & 31;
+            atomicOr(&sMask[i * kMaskWords + wi], bits << sh);
+            if (sh > 20) atomicOr(&sMask[i * kMaskWords + wi + 1], bits >> (32 - sh));
+          }
+        }
       }
-    } else {
-      const int fwi = wd - L;
-      const int b0 = coarse_planes + 64 * fwi;
-      const int lo = max(b0, p0), hi = min(min(b0 + 64, coarse_planes + fb), p0 + np);
-      uint64_t v = 0;
-      if (lo < hi) v = extract_bits(mk, lo - p0, hi - lo) << (lo - b0);
-      if (single_chunk) im.fine[gi * h.fwp + fwi] = v;
-      else if (v) atomicOr(reinterpret_cast<unsigned long long*>(im.fine + gi * h.fwp + fwi),
-                           (unsigned long long)v);
     }
+    __syncthreads();
+
+    // assemble coarse bucket ids and fine words
+    const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
+    const int n_words = L + h.fwp;
+    for (int e = tid; e < nd * n_words; e += blockDim.x) {
+      const int i = e / n_words, wd = e % n_words;
+      const uint32_t* mk = sMask + i * kMaskWords;
+      const size_t gi = i0 + i;
+      if (wd < L) {
+        const int lo = max(wd * m, p0), hi = min(wd * m + m, p0 + np);
+        if (lo < hi) {
+          const uint32_t v = (uint32_t)(extract_bits(mk, lo - p0, hi - lo) << (lo - wd * m));
+          if (single_chunk) im.coarse[gi * L + wd] = v;
+          else if (v) atomicOr(im.coarse + gi * L + wd, v);
+        }
+      } else {
+        const int fwi = wd - L;
+        const int b0 = coarse_planes + 64 * fwi;
+        const int lo = max(b0, p0), hi = min(min(b0 + 64, coarse_planes + fb), p0 + np);
+        uint64_t v = 0;
+        if (lo < hi) v = extract_bits(mk, lo - p0, hi - lo) << (lo - b0);
+        if (single_chunk) im.fine[gi * h.fwp + fwi] = v;
+        else if (v) atomicOr(reinterpret_cast<unsigned long long*>(im.fine + gi * h.fwp + fwi),
+                             (unsigned long long)v);
+      }
+    }
+    __syncthreads();  // masks read: the buffer takes the next-but-one tile
+    if (warp == 0 && t + 2 * (int)gridDim.x < n_tiles) issue(t + 2 * gridDim.x, k);
   }
 }
 
@@ -1502,25 +1582,30 @@ int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
   return launches + 1;
 }
 
-static size_t codes_smem_bytes() {
-  return sizeof(float) * (kDim * kPlaneChunk + kCodesTile * kAStride + kCodesTile + kPlaneChunk + kDim) +
-         sizeof(uint32_t) * kCodesTile * kMaskWords;
+static int codes_pstride(const HashDev& h) { return (std::min(kPlaneChunk, h.n_planes) + 11) / 12 * 12; }
+
+static size_t codes_smem_bytes(int pstride) {
+  return sizeof(float) * (2 * kCodesTile * kTileStride + kDim * pstride + kCodesTile + kPlaneChunk + kDim) +
+         2 * sizeof(uint64_t);
 }
 
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                   const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
                   uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s) {
-  static bool attr = false;
-  const size_t smem = codes_smem_bytes();
-  if (!attr) {
-    cudaFuncSetAttribute(codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)codes_smem_bytes(kPlaneChunk));
   }
+  const int pstride = codes_pstride(h);
   // overflow flags live right after the fixup counter (see bmg_api.cpp)
   uint32_t* overflow = fix_count + 1;
-  dim3 grid(n_tiles, (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
-  codes_kernel<<<grid, 512, smem, s>>>(h, imgs_dev, tile_img, tile_start, mean, fix, fix_count,
-                                       fix_cap, overflow);
+  dim3 grid(std::min(n_tiles, n_sm), (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
+  codes_kernel<<<grid, 512, codes_smem_bytes(pstride), s>>>(h, imgs_dev, tile_img, tile_start, n_tiles, pstride,
+                                                             mean, fix, fix_count, fix_cap, overflow);
 }
 
 void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,
