@@ -159,6 +159,10 @@ typedef struct {
 /* Run every row on one stream (no overlap of consecutive rows): used to time
  * kernels in isolation; results are identical. */
 #define BMG_EXEC_SERIAL 4u
+/* Recompute the (mean-independent, per-residency) descriptor projections of
+ * every resident image inside the call: used to time the complete row work
+ * on HBM-resident inputs; results are identical. */
+#define BMG_EXEC_REPROJECT 8u
 
 /* ---- status ------------------------------------------------------------ */
 const char* bmg_status_name(int status);              /* "InvalidArgument", ... */

@@ -78,6 +78,7 @@ class ExecOptionsC(C.Structure):
 EXEC_RETAIN = 1
 EXEC_MEAN_CHAIN = 2
 EXEC_SERIAL = 4
+EXEC_REPROJECT = 8
 
 
 EXPORTED = [

@@ -163,10 +163,22 @@ struct PinnedRing {
 };
 
 struct ArenaImage {
-  float* d = nullptr;
+  float* d = nullptr;         // [n][128] descriptors, then proj [n][proj_stride], dnorm [n]
+  float* proj = nullptr;
+  float* dnorm = nullptr;
   uint64_t n = 0;
-  cudaEvent_t ev = nullptr;  // recorded on the copy stream after the H2D
-  uint64_t seq = 0;          // upload order on the copy stream
+  cudaEvent_t ev = nullptr;  // recorded on the projection stream once the image is usable
+  uint64_t seq = 0;          // upload order
+  int pstream = 0;           // projection stream that records `ev`
+  uint64_t reproj = 0;       // execute_plan call that last re-projected it (BMG_EXEC_REPROJECT)
+};
+
+// A row's view of one image (descriptors, their projections and norms).
+struct RowImage {
+  const float* desc;
+  uint64_t n;
+  float* proj;
+  float* dnorm;
 };
 
 // Process-wide pool of pinned host buffers that execution results own (the
@@ -248,12 +260,12 @@ struct RowSlot {
   std::unordered_map<uint64_t, int> row_slot;
   std::vector<ImgDev> row_imgs;
   bool row_valid = false;
-  DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag;
+  DevBuf d_imgs, d_tiles, d_scratch, d_mean, d_acc, d_fix, d_fixcnt, d_diag, d_mproj;
   // match state
   DevBuf d_work, d_dense, d_dense_off, d_pair_count, d_nq;
   MetaBatch meta{};  // pending metadata copies / zero fills for s_comp
   void release() {
-    for (DevBuf* b : {&d_imgs, &d_tiles, &d_scratch, &d_mean, &d_acc, &d_fix, &d_fixcnt, &d_diag, &d_work,
+    for (DevBuf* b : {&d_imgs, &d_tiles, &d_scratch, &d_mean, &d_acc, &d_fix, &d_fixcnt, &d_diag, &d_mproj, &d_work,
                       &d_dense, &d_dense_off, &d_pair_count, &d_nq, &d_mean_sums, &d_mean_state})
       b->release();
     if (s_comp) cudaStreamDestroy(s_comp);
@@ -273,6 +285,11 @@ struct bmg_context {
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
   cudaStream_t s_copy = nullptr;
+  static constexpr int kProjStreams = 4;
+  cudaStream_t s_proj[kProjStreams] = {};  // per-image projections, right behind each upload
+  int proj_rr = 0;
+  cudaEvent_t ev_copied = nullptr;
+  uint64_t exec_serial = 0;        // execute_plan calls so far (re-projection epochs)
   bmg::RowSlot slot[2];
   int cur = 0;
   bmg::RowSlot& S() { return slot[cur]; }
@@ -292,6 +309,7 @@ struct bmg_context {
   bmg::DevBuf d_res;
   // temporaries for the stateless entry points
   bmg::DevBuf d_tmp_desc, d_tmp_codes;
+  bmg::DevBuf d_rp;  // BMG_EXEC_REPROJECT: image table + tile list
   // instrumentation
   uint64_t launches = 0;
   bool profiling = false;
@@ -429,8 +447,10 @@ ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
   ArenaImage im;
   im.n = n;
-  BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(n * 512, 512), c.pool,
-                           c.s_copy));
+  const size_t bytes = n * 512 + align_up(proj_bytes(n, c.hd.proj_stride), 16);
+  BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(bytes, 512), c.pool, c.s_copy));
+  im.proj = im.d + n * kDim;
+  im.dnorm = im.proj + n * c.hd.proj_stride;
   ArenaImage& out = c.resident.emplace(id, im).first->second;
   c.occupancy += n;
   c.peak = std::max(c.peak, c.occupancy);
@@ -441,11 +461,33 @@ ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
 
 uint64_t g_upload_seq = 0;
 
-// The H2D of a reserved image on the copy stream, followed by its event.
+ImgDev proj_view(const ArenaImage& a) {
+  ImgDev v{};
+  v.desc = a.d;
+  v.proj = a.proj;
+  v.dnorm = a.dnorm;
+  v.n = static_cast<uint32_t>(a.n);
+  return v;
+}
+
+// The H2D of a reserved image on the copy stream; the projection stream then
+// computes its mean-independent projections (K2 project_kernel) while the
+// next images upload, and records the image's ready event.
 void arena_copy(Ctx& c, ArenaImage& im, const float* desc) {
   stage_h2d(c, im.d, desc, im.n * 512);
+  BMG_CUDA(cudaEventRecord(c.ev_copied, c.s_copy));
+  im.pstream = c.proj_rr;
+  c.proj_rr = (c.proj_rr + 1) % bmg_context::kProjStreams;
+  cudaStream_t ps = c.s_proj[im.pstream];
+  BMG_CUDA(cudaStreamWaitEvent(ps, c.ev_copied, 0));
+  if (im.n) {
+    Timed t(c, "project", ps);
+    launch_project(c.hd, proj_view(im), ps);
+    ++c.launches;
+    check_launch();
+  }
   if (!im.ev) im.ev = take_event(c);
-  BMG_CUDA(cudaEventRecord(im.ev, c.s_copy));
+  BMG_CUDA(cudaEventRecord(im.ev, ps));
   im.seq = ++g_upload_seq;
   c.pending_upload = true;
 }
@@ -481,8 +523,10 @@ void arena_evict(Ctx& c, uint64_t id) {
 
 void join_uploads(Ctx& c) {
   if (!c.pending_upload) return;
-  BMG_CUDA(cudaEventRecord(c.ev_uploaded, c.s_copy));
-  BMG_CUDA(cudaStreamWaitEvent(c.S().s_comp, c.ev_uploaded, 0));
+  for (cudaStream_t ps : c.s_proj) {
+    BMG_CUDA(cudaEventRecord(c.ev_uploaded, ps));
+    BMG_CUDA(cudaStreamWaitEvent(c.S().s_comp, c.ev_uploaded, 0));
+  }
   c.pending_upload = false;
 }
 
@@ -510,9 +554,10 @@ void enqueue_codes_tables(Ctx& c, const float* d_mean) {
   unsigned long long* diag = c.S().d_diag.as<unsigned long long>();
   {
     Timed t(c, "codes", s);
+    c.S().d_mproj.ensure(sizeof(float) * (h.n_planes + 1));
     launch_codes(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), d_mean,
-                 c.S().d_fix.as<Fixup>(), c.S().d_fixcnt.as<uint32_t>(), rs.fix_cap, s);
-    ++c.launches;
+                 c.S().d_mproj.as<float>(), c.S().d_fix.as<Fixup>(), c.S().d_fixcnt.as<uint32_t>(), rs.fix_cap, s);
+    c.launches += 2;
     check_launch();
   }
   {
@@ -533,8 +578,8 @@ void enqueue_codes_tables(Ctx& c, const float* d_mean) {
 // Lays out codes + tables for `descs` (device pointers, counts) in the row
 // scratch, computes the mean (unless given) and launches codes, fixup and
 // bucket-table kernels on the compute stream.
-void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_t>>& descs,
-                       const float* mean_host, const float* mean_dev, bool compute_mean) {
+void prepare_row_views(Ctx& c, const std::vector<RowImage>& descs, const float* mean_host,
+                       const float* mean_dev, bool compute_mean) {
   const HashDev& h = c.hd;
   const int n_imgs = static_cast<int>(descs.size());
   const int L = h.tables;
@@ -544,7 +589,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   // codes (coarse + fine) of all images first, then all bucket offsets, so
   // each group is one contiguous memset
   for (int i = 0; i < n_imgs; ++i) {
-    const uint64_t n = descs[i].second;
+    const uint64_t n = descs[i].n;
     if (n >= (1ull << 31)) fail(BMG_UNSUPPORTED, "images with >= 2^31 descriptors");
     lay[i].coarse_off = off;
     off = align_up(off + n * L * 4, 256);
@@ -562,7 +607,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   for (int i = 0; i < n_imgs; ++i) {
     lay[i].cursor_off = off;
     off = align_up(off + L * NB * 4, 256);
-    const uint64_t ns = slot_stride(descs[i].second, h.n_buckets, h.bucket_pad);
+    const uint64_t ns = slot_stride(descs[i].n, h.n_buckets, h.bucket_pad);
     lay[i].slots_off = off;
     off = align_up(off + ns * L * 4, 256);
     lay[i].bfine_off = off;
@@ -573,8 +618,10 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   c.S().row_imgs.assign(n_imgs, ImgDev{});
   for (int i = 0; i < n_imgs; ++i) {
     ImgDev& im = c.S().row_imgs[i];
-    im.desc = descs[i].first;
-    im.n = static_cast<uint32_t>(descs[i].second);
+    im.desc = descs[i].desc;
+    im.proj = descs[i].proj;
+    im.dnorm = descs[i].dnorm;
+    im.n = static_cast<uint32_t>(descs[i].n);
     im.coarse = reinterpret_cast<uint32_t*>(base + lay[i].coarse_off);
     im.fine = reinterpret_cast<uint64_t*>(base + lay[i].fine_off);
     im.offsets = reinterpret_cast<uint32_t*>(base + lay[i].offsets_off);
@@ -591,7 +638,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
   {
     size_t t = 0;
     for (int i = 0; i < n_imgs; ++i)
-      for (uint64_t s = 0; s < descs[i].second; s += kCodesTile) {
+      for (uint64_t s = 0; s < descs[i].n; s += kCodesTile) {
         h_tiles[t] = static_cast<uint32_t>(i);
         h_tiles[n_tiles + t] = static_cast<uint32_t>(s);
         ++t;
@@ -656,7 +703,7 @@ void prepare_row_views(Ctx& c, const std::vector<std::pair<const float*, uint64_
 }
 
 void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host) {
-  std::vector<std::pair<const float*, uint64_t>> descs;
+  std::vector<RowImage> descs;
   descs.reserve(n);
   c.S().row_ids.assign(ids, ids + n);
   c.S().row_slot.clear();
@@ -666,7 +713,7 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     const auto it = c.resident.find(ids[i]);
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
-    descs.emplace_back(it->second.d, it->second.n);
+    descs.push_back(RowImage{it->second.d, it->second.n, it->second.proj, it->second.dnorm});
     c.S().row_slot[ids[i]] = static_cast<int>(i);
   }
   c.S().row_valid = false;
@@ -782,6 +829,7 @@ HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const 
   h.fwp = padded_words(h.fw);
   h.n_buckets = 1 << p.coarse_bits;
   h.n_planes_pad = static_cast<int>(align_up(h.n_planes, kPlaneChunk));
+  h.proj_stride = static_cast<int>(align_up(h.n_planes, 4));
   h.bucket_pad = match_tma_enabled() ? 4 : 1;
   const int np = h.n_planes, npp = h.n_planes_pad;
   std::vector<float> planes(static_cast<size_t>(np) * kDim), planes_t(static_cast<size_t>(npp) * kDim, 0.f),
@@ -912,7 +960,11 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     BMG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[0].s_comp, cudaStreamNonBlocking, prio_hi));
     BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[1].s_comp, cudaStreamNonBlocking, prio_lo));
+    // projections feed the next rows' codes: highest priority too
+    for (cudaStream_t& ps : c->s_proj) BMG_CUDA(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, prio_hi));
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
+    BMG_CUDA(cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming));
+
     BMG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, c->device));
     uint64_t thresh = ~0ull;
     BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
@@ -944,7 +996,7 @@ int bmg_destroy(bmg_context* c) {
       im.ev = nullptr;
     }
     c->resident.clear();
-    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_tmp_desc, &c->d_tmp_codes})
+    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_rp})
       b->release();
     for (RowSlot& sl : c->slot) sl.release();
     c->res_ranges.release();
@@ -961,7 +1013,10 @@ int bmg_destroy(bmg_context* c) {
     }
     for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
     if (c->ev_uploaded) cudaEventDestroy(c->ev_uploaded);
+    if (c->ev_copied) cudaEventDestroy(c->ev_copied);
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
+    for (cudaStream_t ps : c->s_proj)
+      if (ps) cudaStreamDestroy(ps);
     delete c;
   });
 }
@@ -971,6 +1026,7 @@ int bmg_synchronize(bmg_context* c) {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
   });
 }
@@ -1081,11 +1137,17 @@ int bmg_compute_codes(bmg_context* c, const float* desc, uint64_t count, const f
       fail(BMG_INVALID_ARGUMENT, "null argument");
     set_device(*c);
     c->S().row_valid = false;
-    c->d_tmp_desc.ensure(std::max<uint64_t>(count, 1) * 512);
+    c->d_tmp_desc.ensure(std::max<uint64_t>(count, 1) * 512 + proj_bytes(count, c->hd.proj_stride) + 16);
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
-    stage_h2d(*c, c->d_tmp_desc.p, desc, count * 512);
-    c->pending_upload = true;
-    std::vector<std::pair<const float*, uint64_t>> one{{c->d_tmp_desc.as<float>(), count}};
+    for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
+    ArenaImage tmp;
+    tmp.d = c->d_tmp_desc.as<float>();
+    tmp.n = count;
+    tmp.proj = tmp.d + count * kDim;
+    tmp.dnorm = tmp.proj + count * c->hd.proj_stride;
+    arena_copy(*c, tmp, desc);
+    c->free_events.push_back(tmp.ev);
+    std::vector<RowImage> one{RowImage{tmp.d, count, tmp.proj, tmp.dnorm}};
     prepare_row_views(*c, one, mean, nullptr, false);
     copy_codes_out(*c, c->S().row_imgs[0], coarse_out, fine_out);
   });
@@ -1262,7 +1324,46 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->slot[0].s_comp));
     BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
+    for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamWaitEvent(ps, span0, 0));
     BMG_CUDA(cudaStreamWaitEvent(c->slot[1].s_comp, span0, 0));
+    if ((opts->flags & BMG_EXEC_REPROJECT) && !c->resident.empty()) {
+      // recompute the projections of every resident image inside this call
+      // (one batched launch on slot 0; slot 1 waits for it)
+      std::vector<ImgDev> v;
+      for (const auto& kv : c->resident)
+        if (kv.second.n) v.push_back(proj_view(kv.second));
+      size_t n_tiles = 0;
+      for (const ImgDev& im : v) n_tiles += (im.n + kCodesTile - 1) / kCodesTile;
+      if (n_tiles) {
+        ImgDev* hi = c->ring.alloc<ImgDev>(v.size(), c->slot[0].s_comp, c->s_copy);
+        std::memcpy(hi, v.data(), sizeof(ImgDev) * v.size());
+        uint32_t* ht = c->ring.alloc<uint32_t>(2 * n_tiles, c->slot[0].s_comp, c->s_copy);
+        size_t t = 0;
+        for (size_t i = 0; i < v.size(); ++i)
+          for (uint32_t s0 = 0; s0 < v[i].n; s0 += kCodesTile, ++t) {
+            ht[t] = static_cast<uint32_t>(i);
+            ht[n_tiles + t] = s0;
+          }
+        const size_t ib = align_up(sizeof(ImgDev) * v.size(), 256);
+        c->d_rp.ensure(ib + sizeof(uint32_t) * 2 * n_tiles);
+        char* base = c->d_rp.as<char>();
+        meta_add(*c, base, hi, sizeof(ImgDev) * v.size());
+        meta_add(*c, base + ib, ht, sizeof(uint32_t) * 2 * n_tiles);
+        meta_flush(*c);
+        const uint32_t* dt = reinterpret_cast<const uint32_t*>(base + ib);
+        {
+          Timed tm(*c, "project", c->slot[0].s_comp);
+          launch_project_tiles(c->hd, reinterpret_cast<const ImgDev*>(base), dt, dt + n_tiles,
+                               static_cast<int>(n_tiles), c->slot[0].s_comp);
+        }
+        ++c->launches;
+        check_launch();
+        cudaEvent_t e = take_event(*c);
+        BMG_CUDA(cudaEventRecord(e, c->slot[0].s_comp));
+        BMG_CUDA(cudaStreamWaitEvent(c->slot[1].s_comp, e, 0));
+        c->free_events.push_back(e);
+      }
+    }
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     struct ChainHook {
       Ctx& c;
@@ -1312,13 +1413,17 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
                          [&](uint64_t x, uint64_t y) { return last_need[x] > last_need[y]; });
         for (uint64_t id : missing) arena_copy(*c, c->resident.at(id), features_of(id).descriptors);
         if (!missing.empty()) mark("row " + std::to_string(row) + " uploads done", c->s_copy);
-        // the row's stream waits for the last-issued copy among its images
-        const ArenaImage* last = nullptr;
+        // the row's stream waits, per projection stream, for the last image
+        // of the row that stream handled (its events are in stream order)
+        const ArenaImage* last[bmg_context::kProjStreams] = {};
         for (uint64_t k = 0; k < ne - nb; ++k) {
           const auto f = c->resident.find(needed[k]);
-          if (f != c->resident.end() && f->second.ev && (!last || f->second.seq > last->seq)) last = &f->second;
+          if (f == c->resident.end() || !f->second.ev) continue;
+          const ArenaImage*& l = last[f->second.pstream];
+          if (!l || f->second.seq > l->seq) l = &f->second;
         }
-        if (last) BMG_CUDA(cudaStreamWaitEvent(S.s_comp, last->ev, 0));
+        for (const ArenaImage* l : last)
+          if (l) BMG_CUDA(cudaStreamWaitEvent(S.s_comp, l->ev, 0));
         c->pending_upload = false;
         mark("row " + std::to_string(row) + " start", S.s_comp);
         prepare_row(*c, needed, ne - nb, nullptr);
@@ -1475,6 +1580,7 @@ int bmg_set_profiling(bmg_context* c, int enabled) {
   return guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
     set_device(*c);
+    for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
     for (auto& t : c->timers) {
       c->free_events.push_back(t.a);
@@ -1489,6 +1595,7 @@ int bmg_kernel_time(bmg_context* c, const char* cls, double* total_ms, uint64_t*
   return guarded([&] {
     if (!c || !cls) fail(BMG_INVALID_ARGUMENT, "null argument");
     set_device(*c);
+    for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
     double ms = 0.0;
     uint64_t n = 0;

@@ -20,9 +20,12 @@ struct ImgDev {
   uint32_t* slots;     // [tables][ns] train indices grouped by bucket (:136-145),
                        // buckets padded to 4 entries (pad index 0xffffffff)
   uint64_t* bfine;     // [tables][ns][fwp] fine codes in slot order (coalesced candidate walk)
+  float* proj;          // [n][proj_stride] fl32(d . p) for every plane (mean-independent, per residency)
+  float* dnorm;         // [n] ||d||_2 rounded up
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
   uint32_t ns;         // slot stride per table: slot_stride(n, n_buckets)
+  uint32_t pad_;
 };
 
 struct HashDev {
@@ -35,6 +38,7 @@ struct HashDev {
   const float* planes;     // [n_planes][128] planes (coarse first, then fine)
   const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
   int n_planes_pad;
+  int proj_stride;         // floats per descriptor row of ImgDev::proj (n_planes rounded up to 4)
   int bucket_pad;          // buckets padded to a multiple of this (4 for the TMA-staged matcher, else 1)
 };
 
@@ -104,8 +108,15 @@ inline size_t mean_scratch_bytes(size_t n_tiles) {
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
                     const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,
                     MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s);
+// fl32 projections + norms of one image (tile t = descriptors [128t, 128t+128))
+// or of a tile list (ImgDev::proj / dnorm are the outputs)
+void launch_project(const HashDev& h, const ImgDev& one, cudaStream_t s);
+void launch_project_tiles(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                          const uint32_t* tile_start, int n_tiles, cudaStream_t s);
+inline size_t proj_bytes(uint64_t n, int proj_stride) { return n * (sizeof(float) * proj_stride + sizeof(float)); }
+// mproj: scratch of n_planes + 1 floats (m . p per plane, ||m||)
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
-                  const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
+                  const uint32_t* tile_start, int n_tiles, const float* mean, float* mproj, Fixup* fix,
                   uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s);
 void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,
                         const Fixup* fix, const uint32_t* fix_count, uint32_t fix_cap,

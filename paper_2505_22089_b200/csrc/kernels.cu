@@ -1,7 +1,8 @@
 // kernels.cu -- hand-written sm_100a kernels for the cascade-hashing hot path.
 //
 //   K1 row_mean_kernel        engine.cpp:446-461   exact sequential FP64 chain
-//   K2 codes_kernel           hashmatch.cpp:71-100 FP32 projection + certified sign
+//   K2 project_kernel         hashmatch.cpp:71-100 FP32 projections d.p per image residency
+//      codes_kernel                                per row: d.p - m.p + certified sign
 //      codes_fixup_kernel                          FP64 reference-order recompute of
 //      codes_overflow_kernel                       the uncertified signs
 //   K3 tables_{hist,scan,scatter}  hashmatch.cpp:120-145 bucket index per (image,row)
@@ -372,19 +373,28 @@ __global__ void __launch_bounds__(32, 1) mean_chain_kernel(const ImgDev* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K2: projections.  CTA = 128 descriptors x 192 planes, 512 threads; each
-// thread accumulates 4 descriptors x 12 planes in FP32 (24 packed FFMA2 per
-// 4 LDS.128).  Planes live transposed in shared memory, descriptors centered
-// in shared memory (row stride 132 floats: conflict-free LDS.128).
+// K2: projections, split into a mean-independent GEMM and a per-row certify.
 //
-// Certificate: |s32 - s_exact| <= gamma_{130} * sum|a_c||p_c|
-//                               <= 8e-6 * ||d-m||_2 * ||p||_2   (Cauchy-Schwarz)
-// and the reference FP64 result is within 1.5e-14*||d-m||*||p|| of s_exact,
-// so s32 > B  =>  s64 > 0 (bit 1) and s32 < -B => s64 < 0 (bit 0).  Anything
-// in [-B, B] goes to the FP64 fixup list.
+//   project_kernel  per image, once per residency (right after its upload,
+//                   overlapping the next uploads): D[i][p] = fl32(d_i . p)
+//                   (packed FFMA2, one FMA chain over c = 0..127 in order) and
+//                   ||d_i||_2 rounded up.  Persistent, TMA-fed: a CTA keeps
+//                   its plane chunk in shared memory and walks descriptor
+//                   tiles whose rows arrive by cp.async.bulk (528-byte smem
+//                   stride, conflict-free LDS.128) into a double buffer.
+//   codes_kernel    per row: s32 = fl32(D[i][p] - fl32(m . p)) and the sign
+//                   certificate below; packs bucket ids and fine words.
+//
+// Certificate: with u = 2^-24, |fl(d.p) - d.p| <= gamma_128 ||d|| ||p||,
+// |fl(m.p) - m.p| <= gamma_128 ||m|| ||p|| and the subtraction adds
+// u(||d|| + ||m||)||p||, so |s32 - s_exact| <= gamma_130 (||d|| + ||m||) ||p||
+// <= 8e-6 (||d|| + ||m||) ||p|| (Cauchy-Schwarz, norms rounded up), where
+// s_exact = sum_c (d_c - m_c) p_c; the reference's FP64 value
+// (hashmatch.cpp:27-33) is within 1.5e-14 ||d - m|| ||p|| of it.  So
+// s32 > B => bit 1, s32 < -B => bit 0; anything in [-B, B] goes to the FP64
+// fixup list (recomputed in the reference's order).
 // ---------------------------------------------------------------------------
 constexpr int kAStride = 132;
-constexpr int kMaskWords = (kPlaneChunk + 31) / 32 + 2;  // +2 guard words for 64-bit extracts
 constexpr float kDotBound = 8.0e-6f;
 constexpr float kDotBoundAbs = 1.0e-37f;
 
@@ -396,39 +406,49 @@ __device__ __forceinline__ uint64_t extract_bits(const uint32_t* w, int start, i
   return len >= 64 ? v : (v & ((1ull << len) - 1ull));
 }
 
-// Persistent, TMA-fed: a CTA keeps its plane chunk in shared memory and walks
-// descriptor tiles t = blockIdx.x, +gridDim.x, ..; the next-but-one tile's
-// rows arrive by cp.async.bulk (one 512-byte copy per row, 528-byte smem
-// stride) into the other buffer while this one is projected.
 constexpr int kTileStride = kAStride;  // floats per staged row (528 B: conflict-free LDS.128)
 
 __device__ __forceinline__ uint32_t cvta_smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(512, 1)
-    codes_kernel(HashDev h, const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
-                 const uint32_t* __restrict__ tile_start, int n_tiles, int pstride,
-                 const float* __restrict__ mean, Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count,
-                 uint32_t fix_cap, uint32_t* __restrict__ overflow) {
+// Tiles of the launch: tile_img == nullptr means one image (`one`), tile t =
+// its descriptors [128t, 128t+128); otherwise the (image, start) lists.
+struct ProjJob {
+  const ImgDev* imgs;
+  const uint32_t* tile_img;
+  const uint32_t* tile_start;
+  int n_tiles;
+  ImgDev one;
+};
+
+__device__ __forceinline__ void job_tile(const ProjJob& j, int t, ImgDev& im, uint32_t& i0) {
+  if (j.tile_img) {
+    im = j.imgs[j.tile_img[t]];
+    i0 = j.tile_start[t];
+  } else {
+    im = j.one;
+    i0 = (uint32_t)t * kCodesTile;
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) project_kernel(HashDev h, ProjJob job, int pstride) {
   extern __shared__ __align__(128) float smem_f[];
-  float* sT = smem_f;                                  // [2][128][132] staged tiles (masks overlay)
+  float* sT = smem_f;                                  // [2][128][132] staged tiles
   float* sP = sT + 2 * kCodesTile * kTileStride;       // [128][pstride]
-  float* sNrm = sP + kDim * pstride;                   // [128]
-  float* sPn = sNrm + kCodesTile;                      // [192]
-  float* sMean = sPn + kPlaneChunk;                    // [128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMean + kDim);  // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kDim * pstride);  // [2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p0 = blockIdx.y * kPlaneChunk;
   const int np = min(kPlaneChunk, h.n_planes - p0);
-  const bool single_chunk = gridDim.y == 1;
   const int n_groups = (np + 11) / 12;  // warps with planes to project
+  const bool norms = blockIdx.y == 0;
 
   // stage tile t's rows into buffer k (warp 0)
   auto issue = [&](int t, int k) {
-    const ImgDev im = imgs[tile_img[t]];
-    const uint32_t i0 = tile_start[t];
+    ImgDev im;
+    uint32_t i0;
+    job_tile(job, t, im, i0);
     const int nd = min(kCodesTile, (int)(im.n - i0));
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
@@ -452,26 +472,29 @@ __global__ void __launch_bounds__(512, 1)
   }
   __syncthreads();
   if (warp == 0) {
-    if ((int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
-    if ((int)(blockIdx.x + gridDim.x) < n_tiles) issue(blockIdx.x + gridDim.x, 1);
+    if ((int)blockIdx.x < job.n_tiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < job.n_tiles) issue(blockIdx.x + gridDim.x, 1);
   }
-  // planes chunk -> smem (row c: planes p0 .. p0+pstride, zero past np)
-  for (int e = tid; e < kDim * pstride; e += blockDim.x) {
-    const int c = e / pstride, q = e % pstride;
-    sP[e] = q < np ? __ldg(h.planes_t + (size_t)c * h.n_planes_pad + p0 + q) : 0.f;
+  // planes chunk -> smem (row c: planes p0 .. p0+pstride; planes_t is zero
+  // padded to a multiple of kPlaneChunk, pstride is a multiple of 4)
+  {
+    const int q4 = pstride / 4;
+    for (int e = tid; e < kDim * q4; e += blockDim.x) {
+      const int c = e / q4, q = e - c * q4;
+      reinterpret_cast<float4*>(sP + c * pstride)[q] =
+          __ldg(reinterpret_cast<const float4*>(h.planes_t + (size_t)c * h.n_planes_pad + p0) + q);
+    }
   }
-  for (int e = tid; e < kPlaneChunk; e += blockDim.x) sPn[e] = e < np ? __ldg(h.plane_norm + p0 + e) : 0.f;
-  if (tid < kDim) sMean[tid] = mean[tid];
   __syncthreads();
 
   uint32_t ph0 = 0, ph1 = 0;
   int k = 0;
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, k ^= 1) {
-    const uint32_t img = tile_img[t];
-    const ImgDev im = imgs[img];
-    const uint32_t i0 = tile_start[t];
+  for (int t = blockIdx.x; t < job.n_tiles; t += gridDim.x, k ^= 1) {
+    ImgDev im;
+    uint32_t i0;
+    job_tile(job, t, im, i0);
     const int nd = min(kCodesTile, (int)(im.n - i0));
-    float* sA = sT + (size_t)k * kCodesTile * kTileStride;
+    const float* sA = sT + (size_t)k * kCodesTile * kTileStride;
     {
       const uint32_t par = k ? ph1 : ph0;
       const uint32_t a = cvta_smem(bars + k);
@@ -486,38 +509,31 @@ __global__ void __launch_bounds__(512, 1)
       if (k) ph1 ^= 1u;
       else ph0 ^= 1u;
     }
-    // center in place + row norms: thread (row, quarter) covers 32 floats
-    {
+    if (norms) {  // ||d||_2 rounded up: thread (row, quarter) covers 32 floats
       const int r = tid >> 2, qq = tid & 3;
-      float4* row = reinterpret_cast<float4*>(sA + r * kTileStride + qq * 32);
-      const float4* mq = reinterpret_cast<const float4*>(sMean + qq * 32);
+      const float4* row = reinterpret_cast<const float4*>(sA + r * kTileStride + qq * 32);
       float ss = 0.f;
+      if (r < nd) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < nd) {
-          const float4 d = row[i], m = mq[i];
-          v = make_float4(d.x - m.x, d.y - m.y, d.z - m.z, d.w - m.w);
+        for (int i = 0; i < 8; ++i) {
+          const float4 v = row[i];
+          ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
         }
-        row[i] = v;
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
       }
       ss += __shfl_xor_sync(kFull, ss, 1);
       ss += __shfl_xor_sync(kFull, ss, 2);
-      if (qq == 0) sNrm[r] = sqrtf(ss) * 1.00001f;
+      if (qq == 0 && r < nd) im.dnorm[i0 + r] = sqrtf(ss) * 1.00001f;
     }
-    __syncthreads();
-
     const int pg = warp;  // plane groups of 12 (warp 15 idles: 180 = 15 x 12)
-    // packed FP32x2 FMAs (FFMA2, the descriptor value broadcast to both
-    // halves): plane pair jp of row r accumulates in acc[r][jp]; every output
-    // is one FP32 FMA chain over c = 0..127 in order (the certificate's model)
-    float2 acc[4][6];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int j = 0; j < 6; ++j) acc[r][j] = make_float2(0.f, 0.f);
     if (pg < n_groups) {
+      // packed FP32x2 FMAs (FFMA2, the descriptor value broadcast to both
+      // halves): plane pair jp of row r accumulates in acc[r][jp]; every
+      // output is one FP32 FMA chain over c = 0..127 in order
+      float2 acc[4][6];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc[r][j] = make_float2(0.f, 0.f);
 #pragma unroll 2
       for (int c4 = 0; c4 < kDim / 4; ++c4) {
         float4 a[4];
@@ -536,91 +552,136 @@ __global__ void __launch_bounds__(512, 1)
           for (int r = 0; r < 4; ++r) {
             const float av = cc == 0 ? a[r].x : cc == 1 ? a[r].y : cc == 2 ? a[r].z : a[r].w;
 #pragma unroll
-            for (int j = 0; j < 6; ++j) {
-#ifdef BMG_CODES_FFMA1
-              acc[r][j].x = fmaf(av, pv[j].x, acc[r][j].x);
-              acc[r][j].y = fmaf(av, pv[j].y, acc[r][j].y);
-#else
-              acc[r][j] = __ffma2_rn(make_float2(av, av), pv[j], acc[r][j]);
-#endif
-            }
+            for (int j = 0; j < 6; ++j) acc[r][j] = __ffma2_rn(make_float2(av, av), pv[j], acc[r][j]);
           }
         }
       }
-    }
-    __syncthreads();  // the tile is consumed: its buffer now holds the masks
-    uint32_t* sMask = reinterpret_cast<uint32_t*>(sA);  // [128][kMaskWords]
-    for (int e = tid; e < kCodesTile * kMaskWords; e += blockDim.x) sMask[e] = 0u;
-    __syncthreads();
-
-    // certified signs -> per-descriptor plane mask in smem
-    if (pg < n_groups) {
+      // D[i][p0 + 12pg + j]
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int i = r * 32 + lane;
         if (i < nd) {
-          const float bn = kDotBound * sNrm[i];
-          uint32_t bits = 0;
+          float* out = im.proj + (size_t)(i0 + i) * h.proj_stride + p0 + pg * 12;
 #pragma unroll
-          for (int j = 0; j < 12; ++j) {
-            const int p = pg * 12 + j;
-            if (p < np) {
-              const float sv = (j & 1) ? acc[r][j >> 1].y : acc[r][j >> 1].x;
-              const float B = fmaf(bn, sPn[p], kDotBoundAbs);
-              if (sv > B) {
-                bits |= 1u << j;
-              } else if (!(sv < -B)) {
-                const uint32_t slot = atomicAdd(fix_count, 1u);
-                if (slot < fix_cap) {
-                  Fixup f;
-                  f.img = img;
-                  f.desc = i0 + i;
-                  f.plane = p0 + p;
-                  f.pad = 0;
-                  fix[slot] = f;
-                } else {
-                  atomicOr(overflow + img, 1u);
-                }
-              }
+          for (int j = 0; j < 6; ++j)
+            if (pg * 12 + 2 * j + 1 < np) *reinterpret_cast<float2*>(out + 2 * j) = acc[r][j];
+            else if (pg * 12 + 2 * j < np) out[2 * j] = acc[r][j].x;
+        }
+      }
+    }
+    __syncthreads();  // the tile is consumed: its buffer takes the next-but-one tile
+    if (warp == 0 && t + 2 * (int)gridDim.x < job.n_tiles) issue(t + 2 * gridDim.x, k);
+  }
+}
+
+// Per row: mproj[p] = fl32(m . p) as one FP32 FMA chain per plane (the
+// certificate's model), mproj[n_planes] = ||m||_2 rounded up.
+__global__ void __launch_bounds__(256) mproj_kernel(HashDev h, const float* __restrict__ mean,
+                                                    float* __restrict__ mproj) {
+  __shared__ float sm[kDim];
+  const int tid = threadIdx.x;
+  if (tid < kDim) sm[tid] = mean[tid];
+  __syncthreads();
+  for (int p = blockIdx.x * blockDim.x + tid; p < h.n_planes; p += gridDim.x * blockDim.x) {
+    const float* pp = h.planes + (size_t)p * kDim;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < kDim; ++c) acc = fmaf(sm[c], __ldg(pp + c), acc);
+    mproj[p] = acc;
+  }
+  if (blockIdx.x == 0 && tid < 32) {
+    float ss = 0.f;
+    for (int c = tid; c < kDim; c += 32) ss = fmaf(sm[c], sm[c], ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+    if (tid == 0) mproj[h.n_planes] = sqrtf(ss) * 1.00001f;
+  }
+}
+
+// Per row: thread (descriptor i of the tile, plane word w) certifies planes
+// 32w .. 32w+31 from D and the row's m.p; words of a descriptor meet in a
+// shared-memory mask that is then cut into bucket ids and fine words.
+constexpr int kCodesThreads = 256;
+
+__global__ void __launch_bounds__(kCodesThreads)
+    codes_kernel(HashDev h, const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
+                 const uint32_t* __restrict__ tile_start, const float* __restrict__ mproj,
+                 Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
+                 uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) uint32_t smem_u[];
+  const int n_pw = (h.n_planes + 31) / 32, mw = n_pw + 2;  // mask words (+2 guards)
+  uint32_t* sMask = smem_u;                                        // [128][mw]
+  float* sMp = reinterpret_cast<float*>(sMask + kCodesTile * mw);  // [n_planes] m . p, then ||m||
+  const int tid = threadIdx.x;
+  const uint32_t img = tile_img[blockIdx.x];
+  const ImgDev im = imgs[img];
+  const uint32_t i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(im.n - i0));
+  for (int p = tid; p <= h.n_planes; p += blockDim.x) sMp[p] = __ldg(mproj + p);
+  for (int e = tid; e < kCodesTile * mw; e += blockDim.x) sMask[e] = 0u;
+  __syncthreads();
+
+  const float mn = sMp[h.n_planes];
+  for (int e = tid; e < nd * n_pw; e += blockDim.x) {
+    const int i = e % nd, w = e / nd;
+    const float* drow = im.proj + (size_t)(i0 + i) * h.proj_stride + 32 * w;
+    const float bn = kDotBound * (__ldg(im.dnorm + i0 + i) + mn);
+    const int pn = min(32, h.n_planes - 32 * w);
+    uint32_t bits = 0;
+    for (int j0 = 0; j0 < pn; j0 += 4) {
+      float4 dv;
+      if (j0 + 3 < pn) {
+        dv = __ldg(reinterpret_cast<const float4*>(drow + j0));
+      } else {
+        dv.x = __ldg(drow + j0);
+        dv.y = j0 + 1 < pn ? __ldg(drow + j0 + 1) : 0.f;
+        dv.z = j0 + 2 < pn ? __ldg(drow + j0 + 2) : 0.f;
+        dv.w = 0.f;
+      }
+      const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + q, p = 32 * w + j;
+        if (j < pn) {
+          const float sv = dd[q] - sMp[p];
+          const float B = fmaf(bn, __ldg(h.plane_norm + p), kDotBoundAbs);
+          if (sv > B) {
+            bits |= 1u << j;
+          } else if (!(sv < -B)) {
+            const uint32_t slot = atomicAdd(fix_count, 1u);
+            if (slot < fix_cap) {
+              Fixup f;
+              f.img = img;
+              f.desc = i0 + i;
+              f.plane = p;
+              f.pad = 0;
+              fix[slot] = f;
+            } else {
+              atomicOr(overflow + img, 1u);
             }
           }
-          if (bits) {
-            const int off = pg * 12, wi = off >> 5, sh = off & 31;
-            atomicOr(&sMask[i * kMaskWords + wi], bits << sh);
-            if (sh > 20) atomicOr(&sMask[i * kMaskWords + wi + 1], bits >> (32 - sh));
-          }
         }
       }
     }
-    __syncthreads();
+    sMask[i * mw + w] = bits;
+  }
+  __syncthreads();
 
-    // assemble coarse bucket ids and fine words
-    const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
-    const int n_words = L + h.fwp;
-    for (int e = tid; e < nd * n_words; e += blockDim.x) {
-      const int i = e / n_words, wd = e % n_words;
-      const uint32_t* mk = sMask + i * kMaskWords;
-      const size_t gi = i0 + i;
-      if (wd < L) {
-        const int lo = max(wd * m, p0), hi = min(wd * m + m, p0 + np);
-        if (lo < hi) {
-          const uint32_t v = (uint32_t)(extract_bits(mk, lo - p0, hi - lo) << (lo - wd * m));
-          if (single_chunk) im.coarse[gi * L + wd] = v;
-          else if (v) atomicOr(im.coarse + gi * L + wd, v);
-        }
-      } else {
-        const int fwi = wd - L;
-        const int b0 = coarse_planes + 64 * fwi;
-        const int lo = max(b0, p0), hi = min(min(b0 + 64, coarse_planes + fb), p0 + np);
-        uint64_t v = 0;
-        if (lo < hi) v = extract_bits(mk, lo - p0, hi - lo) << (lo - b0);
-        if (single_chunk) im.fine[gi * h.fwp + fwi] = v;
-        else if (v) atomicOr(reinterpret_cast<unsigned long long*>(im.fine + gi * h.fwp + fwi),
-                             (unsigned long long)v);
-      }
+  // assemble coarse bucket ids and fine words
+  const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
+  const int n_words = L + h.fwp;
+  for (int e = tid; e < nd * n_words; e += blockDim.x) {
+    const int i = e / n_words, wd = e % n_words;
+    const uint32_t* mk = sMask + i * mw;
+    const size_t gi = i0 + i;
+    if (wd < L) {
+      im.coarse[gi * L + wd] = (uint32_t)extract_bits(mk, wd * m, m);
+    } else {
+      const int fwi = wd - L;
+      const int b0 = coarse_planes + 64 * fwi;
+      const int len = min(64, coarse_planes + fb - b0);
+      im.fine[gi * h.fwp + fwi] = len > 0 ? extract_bits(mk, b0, len) : 0ull;
     }
-    __syncthreads();  // masks read: the buffer takes the next-but-one tile
-    if (warp == 0 && t + 2 * (int)gridDim.x < n_tiles) issue(t + 2 * gridDim.x, k);
   }
 }
 
@@ -1582,30 +1643,60 @@ int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
   return launches + 1;
 }
 
-static int codes_pstride(const HashDev& h) { return (std::min(kPlaneChunk, h.n_planes) + 11) / 12 * 12; }
+static int proj_pstride(const HashDev& h) { return (std::min(kPlaneChunk, h.n_planes) + 11) / 12 * 12; }
 
-static size_t codes_smem_bytes(int pstride) {
-  return sizeof(float) * (2 * kCodesTile * kTileStride + kDim * pstride + kCodesTile + kPlaneChunk + kDim) +
-         2 * sizeof(uint64_t);
+static size_t proj_smem_bytes(int pstride) {
+  return sizeof(float) * (2 * kCodesTile * kTileStride + kDim * pstride) + 2 * sizeof(uint64_t);
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)proj_smem_bytes(kPlaneChunk));
+  }
+  return n;
+}
+
+static void launch_project_job(const HashDev& h, const ProjJob& job, cudaStream_t s) {
+  if (job.n_tiles <= 0) return;
+  const int pstride = proj_pstride(h);
+  dim3 grid(std::min(job.n_tiles, sm_count()), (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
+  project_kernel<<<grid, 512, proj_smem_bytes(pstride), s>>>(h, job, pstride);
+}
+
+void launch_project(const HashDev& h, const ImgDev& one, cudaStream_t s) {
+  // one image right behind its upload (tile per CTA for an 8k image)
+  ProjJob j{};
+  j.n_tiles = (int)((one.n + kCodesTile - 1) / kCodesTile);
+  j.one = one;
+  launch_project_job(h, j, s);
+}
+
+void launch_project_tiles(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                          const uint32_t* tile_start, int n_tiles, cudaStream_t s) {
+  ProjJob j{};
+  j.imgs = imgs_dev;
+  j.tile_img = tile_img;
+  j.tile_start = tile_start;
+  j.n_tiles = n_tiles;
+  launch_project_job(h, j, s);
 }
 
 void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
-                  const uint32_t* tile_start, int n_tiles, const float* mean, Fixup* fix,
+                  const uint32_t* tile_start, int n_tiles, const float* mean, float* mproj, Fixup* fix,
                   uint32_t* fix_count, uint32_t fix_cap, cudaStream_t s) {
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)codes_smem_bytes(kPlaneChunk));
-  }
-  const int pstride = codes_pstride(h);
+  const int mw = (h.n_planes + 31) / 32 + 2;
+  const size_t smem = sizeof(uint32_t) * kCodesTile * mw + sizeof(float) * (h.n_planes + 1);
   // overflow flags live right after the fixup counter (see bmg_api.cpp)
   uint32_t* overflow = fix_count + 1;
-  dim3 grid(std::min(n_tiles, n_sm), (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
-  codes_kernel<<<grid, 512, codes_smem_bytes(pstride), s>>>(h, imgs_dev, tile_img, tile_start, n_tiles, pstride,
-                                                             mean, fix, fix_count, fix_cap, overflow);
+  if (n_tiles <= 0) return;
+  mproj_kernel<<<(h.n_planes + 255) / 256, 256, 0, s>>>(h, mean, mproj);
+  codes_kernel<<<n_tiles, kCodesThreads, smem, s>>>(h, imgs_dev, tile_img, tile_start, mproj, fix, fix_count,
+                                                    fix_cap, overflow);
 }
 
 void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,

@@ -206,6 +206,7 @@ class ExecuteOptions:
     on_evict: object = None   # DeviceBackend::on_evict(image_id)
     retain: bool = False      # keep images resident (skip eviction directives)
     serial: bool = False      # all rows on one stream (kernel timing; same results)
+    reproject: bool = False   # recompute resident images' projections in the call (timing)
     # row means: "exact" (parallel F96 reconstruction, the default) or
     # "chain" (the literal sequential FP64 chain; a test hook, same results)
     mean: str = "exact"
@@ -215,7 +216,7 @@ class ExecuteOptions:
         if self.mean not in modes:
             raise BandmatchError("InvalidArgument", f"unknown mean mode {self.mean!r}")
         return ((_lib.EXEC_RETAIN if self.retain else 0) | (_lib.EXEC_SERIAL if self.serial else 0)
-                | modes[self.mean])
+                | (_lib.EXEC_REPROJECT if self.reproject else 0) | modes[self.mean])
 
 
 @dataclass
