@@ -1054,19 +1054,17 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       float s_min, s_2;
       uint32_t i_min;
       if constexpr (KM == 8) {
-        // lanes 4c..4c+3 hold candidate c: lane part p covers the float4s
-        // p, p+4, .., p+28 (each load instruction reads 64 contiguous bytes
-        // of every candidate row) in two packed FP32x2 chains; the lane sum
-        // and two xor-shuffles complete it.  Every FP32 sum has depth <= 13:
-        // relative error < (13 + 3) * 2^-24 ~ 1e-6, inside the 1e-5
+        // FP32 squared distances (packed FP32x2 ops); every sum has depth
+        // <= 13: relative error < (13 + 3) * 2^-24 ~ 1e-6, inside the 1e-5
         // certification margin below.
         const int ck = lane >> 2, part = lane & 3;
         const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
+        const float2 neg1 = make_float2(-1.f, -1.f);
+#ifdef BMG_RERANK_4LANE
         float s = 0.f;
         if (ck < kept) {
           const float4* qp = Qd + (size_t)q * 32 + part;
           const float4* tp = Td + (size_t)jk * 32 + part;
-          const float2 neg1 = make_float2(-1.f, -1.f);
           float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -1081,6 +1079,42 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         }
         s += __shfl_xor_sync(kFull, s, 1);
         s += __shfl_xor_sync(kFull, s, 2);
+#else
+        // lane l holds dims 4l..4l+3 of the query and of every kept
+        // candidate (each candidate load is one coalesced 512-byte row);
+        // a transpose-reduce over lane bits 4, 3, 2 then two xor steps leave
+        // candidate c's sum in lanes 4c..4c+3.  Depth <= 3 + 5 per sum.
+        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
+        float pt[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
+          pt[c] = 0.f;
+          if (c < kept) {
+            const float4 tv = __ldg(Td + (size_t)jc * 32 + lane);
+            const float2 d0 = __ffma2_rn(make_float2(tv.x, tv.y), neg1, make_float2(qv.x, qv.y));
+            const float2 d1 = __ffma2_rn(make_float2(tv.z, tv.w), neg1, make_float2(qv.z, qv.w));
+            const float2 p2 = __ffma2_rn(d1, d1, __fmul2_rn(d0, d0));
+            pt[c] = p2.x + p2.y;
+          }
+        }
+#pragma unroll
+        for (int st = 0; st < 3; ++st) {
+          const int half = 4 >> st, msk = 16 >> st;
+          const bool up = (lane & msk) != 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i < half) {
+              const float send = up ? pt[i] : pt[i + half];
+              const float keep = up ? pt[i + half] : pt[i];
+              pt[i] = keep + __shfl_xor_sync(kFull, send, msk);
+            }
+          }
+        }
+        float s = pt[0];
+        s += __shfl_xor_sync(kFull, s, 2);
+        s += __shfl_xor_sync(kFull, s, 1);
+#endif
         // squared distances are >= 0 (or NaN, caught by `finite`): their
         // bit patterns order like the values, so REDUX finds the (s, idx)
         // argmin and the runner-up
