@@ -917,28 +917,25 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
     const uint32_t my_base = tb + o8;
     const uint32_t my_len = k < n_chunks ? min(8u, tz - o8) : 0u;
     const uint32_t nr = (min(32u, n_chunks - pg) + 3u) >> 2;
-    const uint32_t base = __shfl_sync(kFull, my_base, grp);
-    bool v = (uint32_t)sub < __shfl_sync(kFull, my_len, grp);
-    uint32_t j = kEmpty;
+    // Loads are unconditional (lanes without an entry read slot 0 and carry
+    // idx kEmpty, so their key is kEmpty): no predicated moves in the loop.
+    auto fetch = [&](int kk, uint32_t& jo, uint64_t (&co)[FWP]) {
+      const uint32_t b = __shfl_sync(kFull, my_base, kk);
+      const uint32_t len = __shfl_sync(kFull, my_len, kk);
+      const bool ok = (uint32_t)sub < len;
+      const uint32_t si = ok ? b + (uint32_t)sub : 0u;
+      const uint32_t jl = __ldg(T.slots + si);
+      load_code<FWP>(T.bfine + (size_t)si * FWP, co);
+      jo = ok ? jl : kEmpty;
+    };
+    uint32_t j;
     uint64_t cw[FWP];
-    if (v) {
-      j = __ldg(T.slots + (base + sub));
-      load_code<FWP>(T.bfine + (size_t)(base + sub) * FWP, cw);
-    }
+    fetch(grp, j, cw);
     for (uint32_t r = 0; r < nr; ++r) {
-      // both shuffles unconditional (no divergence around them)
-      const int kk = min(4 * (int)(r + 1) + grp, 31);
-      const uint32_t nbase = __shfl_sync(kFull, my_base, kk);
-      const uint32_t nlen = __shfl_sync(kFull, my_len, kk);
-      const bool nv = (r + 1 < nr) & ((uint32_t)sub < nlen);
-      uint32_t jn = kEmpty;
-      uint64_t cn[FWP];  // only read when nv
-      if (nv) {
-        jn = __ldg(T.slots + (nbase + sub));
-        load_code<FWP>(T.bfine + (size_t)(nbase + sub) * FWP, cn);
-      }
-      round(v, (hamming<FWP>(qc, cw) << ib) | j);
-      v = nv;
+      uint32_t jn;
+      uint64_t cn[FWP];
+      fetch(min(4 * (int)(r + 1) + grp, 31), jn, cn);  // past the page: len 0 (or discarded)
+      round(j != kEmpty, (hamming<FWP>(qc, cw) << ib) | j);
       j = jn;
 #pragma unroll
       for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
