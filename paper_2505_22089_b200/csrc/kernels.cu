@@ -904,12 +904,20 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   }
   const uint32_t n_chunks = __shfl_sync(kFull, cend, L - 1);
   const uint32_t cstart = cend - nch;
+  const uint32_t cend_s = lane < L ? cend : kEmpty;  // past the tables: never <= k
   const uint32_t sbase = (uint32_t)lane * T.ns + lo;
   for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
     // lane j describes chunk pg + j: table = #tables ending at or before it
+    // (binary search over the nondecreasing chunk ends, one shuffle a step)
     const uint32_t k = pg + lane;
-    uint32_t t = 0;
-    for (int tt = 0; tt < L - 1; ++tt) t += __shfl_sync(kFull, cend, tt) <= k ? 1u : 0u;
+    int t = 0;
+    if (L > 8) {
+      t += __shfl_sync(kFull, cend_s, 15) <= k ? 16 : 0;
+      t += __shfl_sync(kFull, cend_s, t + 7) <= k ? 8 : 0;
+    }
+    t += __shfl_sync(kFull, cend_s, t + 3) <= k ? 4 : 0;
+    t += __shfl_sync(kFull, cend_s, t + 1) <= k ? 2 : 0;
+    t += __shfl_sync(kFull, cend_s, t) <= k ? 1 : 0;
     const uint32_t ts = __shfl_sync(kFull, cstart, t);
     const uint32_t tb = __shfl_sync(kFull, sbase, t);
     const uint32_t tz = __shfl_sync(kFull, sz, t);
