@@ -998,8 +998,8 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // Copies of one key that landed in one lane sit next to each other:
       // squeeze them out so a lane's list is a prefix of its distinct keys.
       // Copies in different lanes are popped together below.
-      if (__any_sync(kFull, (k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) ||
-                                (k2 == k3 && k3 != kEmpty))) {
+      if (__any_sync(kFull, ((k0 == k1) & (k1 != kEmpty)) | ((k1 == k2) & (k2 != kEmpty)) |
+                                ((k2 == k3) & (k3 != kEmpty)))) {
 #pragma unroll
         for (int rep = 0; rep < 3; ++rep) {
           if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
