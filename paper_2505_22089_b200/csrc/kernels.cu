@@ -966,6 +966,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
   const double ratio = a.ratio;
   const double r2 = ratio * ratio;
+  const float r2f = (float)r2;
   uint32_t n_matched = 0;
 
   // the next query's bucket ids are loaded one query ahead
@@ -1185,10 +1186,13 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
         s_2 = __shfl_sync(kFull, s2, 0);
       }
-      const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
+      // certified in FP32: the distances carry relative error < 1e-6, each
+      // product below 2^-24 and r2f its own 2^-24, all far inside the 2e-5
+      // margins (ties d1 == r^2 d2 land in the FP64 band, which rejects them)
+      const float c_hi = 1.0f + 2.0e-5f, c_lo = 1.0f - 2.0e-5f;
       const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
-      const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
-      const bool reject = finite && (double)s_min * lo_f >= r2 * ((double)s_2 * hi_f);
+      const bool accept = finite && s_min * c_hi < r2f * s_2;
+      const bool reject = finite && s_min * c_lo >= (r2f * s_2) * c_hi;
       if (accept) {
         result = (int32_t)i_min;
       } else if (!reject) {
