@@ -100,3 +100,46 @@ def test_empty_plan_executes_to_zeros():
     hf = bm.make_hash_functions(1)
     res = bm.execute_plan(bm.SchedulePlan(), {}, bm.DeviceArena(0, hf))
     assert res.matches == [] and res.metrics.pairs_matched == 0 and res.metrics.uploads == 0
+
+
+@pytest.mark.parametrize("flags", [dict(serial=True), dict(retain=True), dict(retain=True, reproject=True),
+                                   dict(serial=True, reproject=True, retain=True)])
+def test_execution_modes_give_identical_results(reference, tmp_path, flags):
+    # rows on one stream (serial), images kept resident (retain), projections
+    # recomputed in the call (reproject): all must reproduce the reference
+    plan, ref, rc, res, arena, *_ = run_both(reference, tmp_path, 14, 700, 3, 3, 6, seed=11)
+    feats = {i: bm.FeatureSet(i, d) for i, d in
+             enumerate(reference.generate_synthetic(14, 700, 3, 0.02, 0.2, 11)[0])}
+    hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
+    a2 = bm.DeviceArena(engine.arena_units_for(feats, 6) * 3, hf)
+    for _ in range(2):  # the second call runs on whatever the first left resident
+        r2 = bm.execute_plan(plan, feats, a2, bm.ExecuteOptions(**flags))
+        got = {(pm.query_image, pm.train_image): pm.matches for pm in r2.matches}
+        assert list(got) == sorted(ref)
+        for key, m in ref.items():
+            assert np.array_equal(got[key], m), key
+
+
+def test_multi_iteration_plan_with_reuploads(reference, tmp_path):
+    # a small arena forces several iterations, evictions and re-uploads of
+    # images whose projections must be recomputed after each re-upload
+    plan, ref, rc, res, arena, ups, evs, _ = run_both(reference, tmp_path, 20, 500, 4, 2, 4, seed=5)
+    assert len(plan.iterations) >= 2 and rc["uploads"] > 20
+    got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    for key, m in ref.items():
+        assert np.array_equal(got[key], m), key
+    assert res.metrics.uploads == rc["uploads"] and arena.occupancy() == 0
+
+
+def test_result_views_outlive_the_call(reference, tmp_path):
+    # match arrays are zero-copy views of the result's pinned buffer; they
+    # must stay valid (and unchanged) after later calls reuse the context
+    plan, ref, rc, res, arena, *_ = run_both(reference, tmp_path, 12, 600, 3, 3, 6)
+    saved = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    copies = {k: v.copy() for k, v in saved.items()}
+    feats = {i: bm.FeatureSet(i, d) for i, d in
+             enumerate(reference.generate_synthetic(12, 600, 3, 0.02, 0.2, 9)[0])}
+    for _ in range(3):
+        bm.execute_plan(plan, feats, arena)
+    for k in saved:
+        assert np.array_equal(saved[k], copies[k]), k
