@@ -845,7 +845,7 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //      8-lane groups take four chunks per round, so a lane's entry is
 //      chunk_base + (lane & 7): coalesced 128-byte code loads, no per-lane
 //      table search.  Chunk descriptors are built one per lane (32 per page)
-//      and fetched per round with two shuffles; loads run one round ahead;
+//      and fetched per round with two shuffles; loads run two rounds ahead;
 //   2. per candidate: 128-bit Hamming via POPC and the unique key
 //      (hamming << idx_bits | train_idx).  Each lane keeps its 4 smallest
 //      keys (branch-free sorted insert); the warp then pulls the K smallest
@@ -939,15 +939,24 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
     uint32_t j;
     uint64_t cw[FWP];
     fetch(grp, j, cw);
+    // loads two rounds ahead
+    uint32_t j1;
+    uint64_t c1[FWP];
+    fetch(min(4 + grp, 31), j1, c1);
     for (uint32_t r = 0; r < nr; ++r) {
       uint32_t jn;
       uint64_t cn[FWP];
-      fetch(min(4 * (int)(r + 1) + grp, 31), jn, cn);  // past the page: len 0 (or discarded)
+      fetch(min(4 * (int)(r + 2) + grp, 31), jn, cn);  // past the page: len 0 (or discarded)
       round(j != kEmpty, (hamming<FWP>(qc, cw) << ib) | j);
-      j = jn;
+      j = j1;
+      j1 = jn;
 #pragma unroll
-      for (int x = 0; x < FWP; ++x) cw[x] = cn[x];
+      for (int x = 0; x < FWP; ++x) {
+        cw[x] = c1[x];
+        c1[x] = cn[x];
+      }
     }
+
   }
 }
 
