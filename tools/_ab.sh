@@ -4,7 +4,7 @@ mkdir -p gpurun_out/$t
 for v in "$@"; do
   lib=paper_2505_22089_b200/libbmg_$v.so; [ "$v" = base ] && lib=paper_2505_22089_b200/libbmg.so
   BMG_LIBBMG=$PWD/$lib timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/$t/bench_$v.json 2>/dev/null
-  BMG_LIBBMG=$PWD/$lib timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:match -c 40 --csv --log-file gpurun_out/$t/l_$v.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+  BMG_LIBBMG=$PWD/$lib timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:${ABK:-match} -c 40 --csv --log-file gpurun_out/$t/l_$v.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
   python - "$t" "$v" <<'PY'
 import json, sys, csv, io
 t, v = sys.argv[1], sys.argv[2]
