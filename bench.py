@@ -340,7 +340,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": desc_bytes,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step * 1e3},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step * 1e3,
+                    "step_ms": [round(t * 1e3, 3) for t in e2e_times]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "match_kernel", "peak_source": peak_src,

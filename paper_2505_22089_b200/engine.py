@@ -11,6 +11,7 @@ are in host memory (the reference's VerifyPool hand-off, engine.cpp:478-479).
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Sequence
 import json
 from dataclasses import dataclass, field
 
@@ -288,6 +289,36 @@ class _ResultBuffer:
         self.close()
 
 
+class _PairList(Sequence):
+    """ExecutionResult.matches: PairMatches (sorted by IdPair) built on access
+    from the result's pair ids, ranges and pinned match log."""
+
+    _EMPTY = np.zeros((0, 2), np.int32)
+
+    def __init__(self, ids, rng, log):
+        self._ids, self._rng, self._log = ids, rng, log
+
+    def __len__(self):
+        return len(self._ids) // 2
+
+    def __getitem__(self, p):
+        if isinstance(p, slice):
+            return [self[i] for i in range(*p.indices(len(self)))]
+        if p < 0:
+            p += len(self)
+        if not 0 <= p < len(self):
+            raise IndexError(p)
+        b, e = int(self._rng[2 * p]), int(self._rng[2 * p + 1])
+        return PairMatches(int(self._ids[2 * p]), int(self._ids[2 * p + 1]),
+                           self._log[b:e] if e > b else self._EMPTY)
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __reduce__(self):
+        return (list, (list(self),))
+
+
 class _Owned:
     """Buffer-protocol wrapper around a ctypes-backed array + its owner."""
 
@@ -344,17 +375,15 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
     matches = []
     if npairs:
         # zero-copy: every pair's (query_idx, train_idx) array is a view into
-        # the result's pinned log, kept alive by the views themselves
+        # the result's pinned log, kept alive by the views themselves; the
+        # PairMatches objects are made on access
         pid_p, rng_p, log_p = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)(), C.POINTER(C.c_int32)()
         check(L.bmg_result_view(h, C.byref(pid_p), C.byref(rng_p), C.byref(log_p)))
-        ids = np.ctypeslib.as_array(pid_p, (2 * npairs,)).tolist()
-        rng = np.ctypeslib.as_array(rng_p, (2 * npairs,)).tolist()
-        top = max(rng[1::2]) if nm else 0
+        ids = np.ctypeslib.as_array(pid_p, (2 * npairs,)).copy()
+        rng = np.ctypeslib.as_array(rng_p, (2 * npairs,)).copy()
+        top = int(rng[1::2].max()) if nm else 0
         log = holder.wrap(np.ctypeslib.as_array(log_p, (max(2 * top, 1),))).reshape(-1, 2) if top else None
-        empty = np.zeros((0, 2), np.int32)
-        for p in range(npairs):
-            b, e = rng[2 * p], rng[2 * p + 1]
-            matches.append(PairMatches(ids[2 * p], ids[2 * p + 1], log[b:e] if e > b else empty))
+        matches = _PairList(ids, rng, log)
     else:
         holder.close()
     c = [int(x) for x in counters]
