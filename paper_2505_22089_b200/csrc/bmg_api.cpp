@@ -250,7 +250,9 @@ namespace {
 // bmg_execute_plan alternates two slots so row r+1 (its own stream, scratch
 // and match buffers) overlaps row r; the single-row entry points use slot 0.
 struct RowSlot {
-  cudaStream_t s_comp = nullptr;
+  cudaStream_t s_comp = nullptr;  // the stream of the row the slot holds (home or a priority stream)
+  cudaStream_t home = nullptr;    // the slot's own stream (single-row entry points, rows past the levels)
+  cudaEvent_t done = nullptr;     // recorded after the slot's last row
   RowState rs;
   float* cur_mean = nullptr;
   // exact parallel row mean: F96 tile sums + state (kernels.cu K1)
@@ -268,8 +270,10 @@ struct RowSlot {
     for (DevBuf* b : {&d_imgs, &d_tiles, &d_scratch, &d_mean, &d_acc, &d_fix, &d_fixcnt, &d_diag, &d_mproj, &d_work,
                       &d_dense, &d_dense_off, &d_pair_count, &d_nq, &d_mean_sums, &d_mean_state})
       b->release();
-    if (s_comp) cudaStreamDestroy(s_comp);
-    s_comp = nullptr;
+    if (home) cudaStreamDestroy(home);
+    if (done) cudaEventDestroy(done);
+    home = s_comp = nullptr;
+    done = nullptr;
   }
 };
 }  // namespace
@@ -285,6 +289,7 @@ struct bmg_context {
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
   cudaStream_t s_copy = nullptr;
+  std::vector<cudaStream_t> s_prio;  // row streams by priority: row r of a call runs on s_prio[r]
   static constexpr int kProjStreams = 4;
   cudaStream_t s_proj[kProjStreams] = {};  // per-image projections, right behind each upload
   int proj_rr = 0;
@@ -953,13 +958,23 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     c->seed = cfg->function_seed;
     c->capacity = cfg->capacity_units;
     BMG_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
-    // slot 0 (even rows) gets the higher priority: in a block's first row
-    // pair the even row waits for every upload and then is the critical path,
-    // while the odd row (already resident images) fills in around it
+    // both row slots share one priority (which of two overlapping rows is on
+    // the critical path depends on the plan); projections get the higher one
     int prio_lo = 0, prio_hi = 0;
     BMG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[0].s_comp, cudaStreamNonBlocking, prio_hi));
-    BMG_CUDA(cudaStreamCreateWithPriority(&c->slot[1].s_comp, cudaStreamNonBlocking, prio_lo));
+    for (RowSlot& sl : c->slot) {
+      BMG_CUDA(cudaStreamCreateWithPriority(&sl.home, cudaStreamNonBlocking, prio_lo));
+      sl.s_comp = sl.home;
+      BMG_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    // earlier rows of a plan get higher priority (two rows overlap: the
+    // earlier one gates its slot's next row); rows past the levels alternate
+    // between the two equal-priority home streams
+    for (int pr = prio_hi; pr < prio_lo; ++pr) {
+      cudaStream_t st;
+      BMG_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, pr));
+      c->s_prio.push_back(st);
+    }
     // projections feed the next rows' codes: highest priority too
     for (cudaStream_t& ps : c->s_proj) BMG_CUDA(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, prio_hi));
     BMG_CUDA(cudaEventCreateWithFlags(&c->ev_uploaded, cudaEventDisableTiming));
@@ -1017,6 +1032,7 @@ int bmg_destroy(bmg_context* c) {
     if (c->s_copy) cudaStreamDestroy(c->s_copy);
     for (cudaStream_t ps : c->s_proj)
       if (ps) cudaStreamDestroy(ps);
+    for (cudaStream_t ps : c->s_prio) cudaStreamDestroy(ps);
     delete c;
   });
 }
@@ -1028,6 +1044,7 @@ int bmg_synchronize(bmg_context* c) {
     BMG_CUDA(cudaStreamSynchronize(c->s_copy));
     for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
+    for (cudaStream_t ps : c->s_prio) BMG_CUDA(cudaStreamSynchronize(ps));
   });
 }
 
@@ -1364,14 +1381,20 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
         c->free_events.push_back(e);
       }
     }
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaEventRecord(sl.done, sl.home));
     const bool retain = (opts->flags & BMG_EXEC_RETAIN) != 0;
     struct ChainHook {
       Ctx& c;
       ~ChainHook() {
         c.mean_chain_only = false;
         c.cur = 0;
+        for (RowSlot& sl : c.slot) {
+          if (sl.s_comp != sl.home) cudaStreamWaitEvent(sl.home, sl.done, 0);
+          sl.s_comp = sl.home;
+        }
       }
     } chain_hook{*c};
+    for (RowSlot& sl : c->slot) BMG_CUDA(cudaEventRecord(sl.done, sl.home));
     c->mean_chain_only = (opts->flags & BMG_EXEC_MEAN_CHAIN) != 0;
     uint64_t row = 0;
     std::vector<uint64_t> missing;
@@ -1395,6 +1418,11 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       for (uint64_t r = 0; r < plan->rows_per_iteration[it]; ++r, ++row) {
         c->cur = (opts->flags & BMG_EXEC_SERIAL) ? 0 : static_cast<int>(row & 1);
         RowSlot& S = c->S();
+        if (!(opts->flags & BMG_EXEC_SERIAL)) {
+          cudaStream_t st = row < c->s_prio.size() ? c->s_prio[row] : S.home;
+          if (st != S.s_comp) BMG_CUDA(cudaStreamWaitEvent(st, S.done, 0));
+          S.s_comp = st;
+        }
         const uint64_t nb = plan->row_needed_offsets[row], ne = plan->row_needed_offsets[row + 1];
         const uint64_t* needed = plan->needed_ids + nb;
         // uploads: bookkeeping + hooks in the reference order (engine.cpp:438-444),
@@ -1450,20 +1478,20 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           arena_evict(*c, plan->evict_ids[k]);
           if (opts->on_evict) opts->on_evict(opts->hook_user, plan->evict_ids[k]);
         }
+        BMG_CUDA(cudaEventRecord(S.done, S.s_comp));
       }
       res->iterations.push_back(it_pairs);
       res->iterations.push_back(c->uploads - up0);
       res->iterations.push_back(c->units_uploaded - units0);
     }
-    // join the second slot into the first for the span end
-    {
-      cudaEvent_t j = take_event(*c);
-      BMG_CUDA(cudaEventRecord(j, c->slot[1].s_comp));
-      BMG_CUDA(cudaStreamWaitEvent(c->slot[0].s_comp, j, 0));
-      c->free_events.push_back(j);
+    // join both slots' last rows into slot 0's home stream for the span end
+    for (RowSlot& sl : c->slot) {
+      BMG_CUDA(cudaStreamWaitEvent(c->slot[0].home, sl.done, 0));
+      sl.s_comp = sl.home;
     }
-    BMG_CUDA(cudaEventRecord(span1, c->slot[0].s_comp));
-    BMG_CUDA(cudaStreamSynchronize(c->slot[0].s_comp));
+    BMG_CUDA(cudaStreamWaitEvent(c->slot[1].home, c->slot[1].done, 0));
+    BMG_CUDA(cudaEventRecord(span1, c->slot[0].home));
+    BMG_CUDA(cudaStreamSynchronize(c->slot[0].home));
     for (auto& [what, e] : marks) {
       float ms = 0.f;
       BMG_CUDA(cudaEventSynchronize(e));

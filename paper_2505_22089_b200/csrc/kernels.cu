@@ -262,17 +262,23 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
   int cur = 0, walked = 0, events = 0;
   bool give_up = false;
   for (;;) {
-    if (tid == 0) s_fail = 0x7fffffff;
-    __syncthreads();
-    for (int t = cur + tid; t < n_tiles; t += kResolveThreads) {
-      const size_t o = (size_t)t * kDim + c;
-      if (!tile_certified(tile_sum[o] + delta, tile_rng[o], tile_low[o])) {
-        atomicMin(&s_fail, t);
-        break;
+    // certify forward from `cur`, one tile per thread per window, stopping
+    // at the first window holding an uncertified tile (so a row costs about
+    // one pass over its tiles plus one window per walked tile)
+    int f = 0x7fffffff;
+    for (int w0 = cur; w0 < n_tiles; w0 += kResolveThreads) {
+      if (tid == 0) s_fail = 0x7fffffff;
+      __syncthreads();
+      const int t = w0 + tid;
+      if (t < n_tiles) {
+        const size_t o = (size_t)t * kDim + c;
+        if (!tile_certified(tile_sum[o] + delta, tile_rng[o], tile_low[o])) atomicMin(&s_fail, t);
       }
+      __syncthreads();
+      f = s_fail;
+      __syncthreads();
+      if (f != 0x7fffffff) break;
     }
-    __syncthreads();
-    const int f = s_fail;
     if (f == 0x7fffffff) break;
     if (walked >= kMeanMaxWalks) {
       give_up = true;

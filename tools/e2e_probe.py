@@ -12,7 +12,7 @@ from paper_2505_22089_b200.engine import _feature_views
 keep = []
 def pinned(nbytes):
     t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True); keep.append(t); return t.numpy()
-feats, plan = bench.build_workload("block32", 7, pinned)
+feats, plan = bench.build_workload(sys.argv[1] if len(sys.argv) > 1 else "block32", 7, pinned)
 hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
 cap = bm.arena_units_for(feats, plan.size_gpu)
 flat = bm.flatten_plan(plan)
