@@ -683,9 +683,9 @@ void prepare_row_views(Ctx& c, const std::vector<RowImage>& descs, const float* 
     meta_add(c, d_mean, hm, sizeof(float) * kDim);
   } else if (compute_mean) {
     // exact row mean (engine.cpp:446-461): F96 reconstruction of the FP64
-    // chain, the chain itself only as fallback (rows over 2^22 descriptors
+    // chain, the chain itself only as fallback (rows over 2^23 descriptors
     // exceed the F96 headroom and take the chain directly)
-    const bool chain_only = c.mean_chain_only || total_desc > (1ull << 22) || n_tiles == 0;
+    const bool chain_only = c.mean_chain_only || total_desc > (1ull << 23) || n_tiles == 0;
     c.S().last_mean_chain_only = chain_only;
     c.S().d_mean_sums.ensure(mean_scratch_bytes(std::max<size_t>(n_tiles, 1)));
     c.S().d_mean_state.ensure(sizeof(MeanState));

@@ -42,9 +42,9 @@ __device__ __forceinline__ bool gated_off(const uint32_t* gate) {
 // mean[c] = float(acc[c] / (double)total).
 //
 // Reproduced bit for bit without running the 128 dependent FP64 chains.
-// Descriptor values in (-2^8, 2^8) whose lowest set bit is >= 2^-96 are exact
+// Descriptor values in (-2^7, 2^7) whose lowest set bit is >= 2^-96 are exact
 // in 128-bit fixed point with 96 fractional bits ("F96"), and so is every
-// prefix sum S_k of up to 2^22 of them.  The chain's state is
+// prefix sum S_k of up to 2^23 of them (|S_k| < 2^30, i128 holds 2^31).  The chain's state is
 // acc_k = RN(acc_{k-1} + x_k); when the exact value acc_{k-1} + x_k fits a
 // binary64 (its F96 bit span is <= 53 bits) the add is exact.  Hence
 // acc_k = S_k + delta, where delta changes only at the steps whose exact sum
@@ -68,13 +68,13 @@ using u128 = unsigned __int128;
 constexpr uint32_t kNoLow = 0xffffu;          // tile of zeros: adds nothing
 constexpr int kMeanMaxWalks = 1024;
 
-// x * 2^96 as an integer; ok = false when that is not exact or |x| >= 2^8
+// x * 2^96 as an integer; ok = false when that is not exact or |x| >= 2^7
 __device__ __forceinline__ i128 to_f96(float x, bool& ok) {
   const uint32_t u = __float_as_uint(x);
   const int e = (u >> 23) & 0xff;
   const uint32_t m = (u & 0x7fffffu) | 0x800000u;
   u128 mag = 0;
-  if (e >= 54 && e < 127 + 8) {
+  if (e >= 54 && e < 127 + 7) {
     mag = (u128)m << (e - 54);  // x = m * 2^(e-150) = m << (e-54) F96 units
   } else if (e == 0) {
     ok &= (u & 0x7fffffu) == 0u;  // +-0 (subnormals are below 2^-96)

@@ -61,7 +61,7 @@ def test_rounding_steps_replayed(hf, oracle):
     d[0, 0] = 1.0
     d[1:4, 0] = 2.0 ** -54
     d[0, 1], d[1, 1], d[2, 1] = 1.0, 2.0 ** -52, 2.0 ** -53
-    d[0, 2], d[1, 2], d[2, 2] = 200.0, 2.0 ** -50, -200.0
+    d[0, 2], d[1, 2], d[2, 2] = 100.0, 2.0 ** -50, -100.0
     mean, (rounds, chained) = row_mean(hf, [d])
     assert same_bits(mean, oracle.row_mean([d]))
     assert not chained and rounds >= 2  # the tile was walked

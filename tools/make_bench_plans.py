@@ -9,6 +9,9 @@ fixtures under bench_data/.
   strip500  BASELINE config 3: 500 images, band 10 (4945 pairs), CLI-default
             budget gpu_images=400 -> size_blk clamped to 200
             (bandmatch_cli.cpp:87-104)
+  shard16k  BASELINE config 4, one GPU's shard: 640 of the 5,000 images at
+            16,384 descriptors, band 15 (the 30 nearest neighbours), same
+            CLI-default budget
 """
 import sys
 from pathlib import Path
@@ -30,7 +33,8 @@ def band_pairs(n, band):
 def main():
     OUT.mkdir(exist_ok=True)
     r = Reference()
-    for name, n, band, blk, gpu in [("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400)]:
+    for name, n, band, blk, gpu in [("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400),
+                                    ("shard16k", 640, 15, 200, 400)]:
         r.iterate_schedule(np.arange(n), band_pairs(n, band), blk, gpu, OUT / f"plan_{name}.json")
         print(name, (OUT / f"plan_{name}.json").stat().st_size)
 
