@@ -835,7 +835,7 @@ HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const 
   h.n_buckets = 1 << p.coarse_bits;
   h.n_planes_pad = static_cast<int>(align_up(h.n_planes, kPlaneChunk));
   h.proj_stride = static_cast<int>(align_up(h.n_planes, 4));
-  h.bucket_pad = match_tma_enabled() ? 4 : 1;
+  h.bucket_pad = kBucketPad;
   const int np = h.n_planes, npp = h.n_planes_pad;
   std::vector<float> planes(static_cast<size_t>(np) * kDim), planes_t(static_cast<size_t>(npp) * kDim, 0.f),
       norm(npp, 0.f);

@@ -18,7 +18,8 @@ struct ImgDev {
   uint32_t* offsets;   // [tables][n_buckets+1] bucket starts (hashmatch.cpp:125-135)
   uint32_t* cursor;    // [tables][n_buckets]   scatter cursors (scratch)
   uint32_t* slots;     // [tables][ns] train indices grouped by bucket (:136-145),
-                       // buckets padded to 4 entries (pad index 0xffffffff)
+                       // buckets padded to 8 entries (pad index 0xffffffff); the
+                       // last 8 entries of each table are an all-pad sentinel chunk
   uint64_t* bfine;     // [tables][ns][fwp] fine codes in slot order (coalesced candidate walk)
   float* proj;          // [n][proj_stride] fl32(d . p) for every plane (mean-independent, per residency)
   float* dnorm;         // [n] ||d||_2 rounded up
@@ -39,7 +40,7 @@ struct HashDev {
   const float* plane_norm; // [n_planes_pad] ||p||_2 rounded up, 0 for padding
   int n_planes_pad;
   int proj_stride;         // floats per descriptor row of ImgDev::proj (n_planes rounded up to 4)
-  int bucket_pad;          // buckets padded to a multiple of this (4 for the TMA-staged matcher, else 1)
+  int bucket_pad;          // buckets padded to a multiple of this (kBucketPad)
 };
 
 // An ambiguous projection whose sign the FP32 pass could not certify; the
@@ -90,9 +91,14 @@ struct MetaBatch {
 };
 void launch_meta(const MetaBatch& b, cudaStream_t s);
 
-// per-table slot capacity with every bucket padded to a multiple of `pad`
+// Buckets are padded to whole 8-entry chunks (the candidate walk's unit), so
+// every chunk a query walks is full and a lane's entry needs no bounds test.
+constexpr int kBucketPad = 8;
+constexpr uint32_t kSentinel = 8;  // all-pad chunk at the end of each table
+// per-table slot capacity with every bucket padded to a multiple of `pad`,
+// plus the sentinel chunk
 inline uint32_t slot_stride(uint64_t n, int n_buckets, int pad) {
-  return static_cast<uint32_t>((n + (pad - 1ull) * static_cast<uint64_t>(n_buckets) + 3ull) & ~3ull);
+  return static_cast<uint32_t>(((n + (pad - 1ull) * static_cast<uint64_t>(n_buckets) + 7ull) & ~7ull) + kSentinel);
 }
 // whether the TMA-staged matcher (K4b, needs 4-entry bucket padding) is on
 bool match_tma_enabled();

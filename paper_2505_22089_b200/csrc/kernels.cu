@@ -791,10 +791,11 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t v, uint32_t* s_warp
   return v;
 }
 
-// With the TMA-staged matcher, buckets are laid out padded to a multiple of
-// 4 entries (16-byte aligned slot runs, so a bucket's slots and codes can be
-// fetched by bulk copies); pad entries hold train index kEmpty, which makes
-// their match key kEmpty.
+// Buckets are laid out padded to whole 8-entry chunks (kBucketPad; also
+// 16-byte aligned slot runs for the TMA-staged matcher's bulk copies); pad
+// entries hold train index kEmpty, which makes their match key kEmpty.  The
+// last chunk of each table's slot range is an all-pad sentinel: walk lanes
+// past the end of a query's union read it instead of testing bounds.
 __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry;
@@ -823,6 +824,11 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
     carry = s_carry;
     __syncthreads();
   }
+  if (threadIdx.x < kSentinel) {
+    const uint32_t k = im.ns - kSentinel + threadIdx.x;
+    slots[k] = kEmpty;
+    for (int x = 0; x < h.fwp; ++x) bfine[(size_t)k * h.fwp + x] = 0ull;
+  }
 }
 
 __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs,
@@ -847,20 +853,22 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //   1. the query's bucket union over the L tables (hashmatch.cpp:154-169):
 //      table t contributes the bucket range [lo_t, lo_t + sz_t) of the train
 //      image's bucket-ordered slot / fine-code arrays (written by the tables
-//      scatter).  Each range is cut into 8-entry chunks and the warp's four
-//      8-lane groups take four chunks per round, so a lane's entry is
+//      scatter).  Buckets are padded to whole 8-entry chunks and the warp's
+//      four 8-lane groups take four chunks per round, so a lane's entry is
 //      chunk_base + (lane & 7): coalesced 128-byte code loads, no per-lane
-//      table search.  Chunk descriptors are built one per lane (32 per page)
-//      and fetched per round with two shuffles; loads run two rounds ahead;
+//      table search or bounds test.  Chunk descriptors are built one per
+//      lane (32 per page) and fetched per round with one shuffle; loads run
+//      two rounds ahead;
 //   2. per candidate: 128-bit Hamming via POPC and the unique key
 //      (hamming << idx_bits | train_idx).  Each lane keeps its 4 smallest
 //      keys (branch-free sorted insert); the warp then pulls the K smallest
 //      out of the lanes' lists with the single-instruction warp min (REDUX).
 //      Equal keys are the same train index reached from several tables and
 //      are taken once -- the reference's last_seen dedup + stable counting
-//      sort by (hamming, idx) (:160-200).  If a lane that saw more than 4
-//      keys runs dry during the pulls, the query reruns on the exact path
-//      (sorted list over lanes 0..KM-1, REDUX-driven insertion);
+//      sort by (hamming, idx) (:160-200).  Each lane also keeps the
+//      smallest key that fell off its list; if one lies below the last
+//      pull, the query reruns on the exact path (sorted list over lanes
+//      0..KM-1, REDUX-driven insertion);
 //   3. re-rank (:196-208): lanes 4c..4c+3 hold candidate c; FP32 squared
 //      distances (packed FFMA2) with a certified relative error <= 1e-5
 //      decide the (dist, idx) argmin and the ratio test; uncertified queries
@@ -892,17 +900,17 @@ __device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint
   return h;
 }
 
-// Walks the union; round(valid, key) is called by every lane once per round
-// (warp-uniform trip count).  lo / sz: lane t < L holds table t's (padded)
-// bucket range; other lanes hold zeros.  key = hamming << ib | train_idx;
-// pad entries and lanes without an entry carry idx kEmpty, so their key is
-// kEmpty.  Chunk descriptors live in registers, one chunk per lane, and are
-// fetched per round with two shuffles; loads run one round ahead.
+// Walks the union; round(key) is called by every lane once per round
+// (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket range
+// (a whole number of 8-entry chunks); other lanes hold zeros.
+// key = hamming << ib | train_idx; pad entries carry idx kEmpty, so their key
+// is kEmpty.  Chunk descriptors live in registers, one chunk per lane, and
+// are fetched per round with one shuffle; loads run two rounds ahead.
 template <int FWP, typename F>
 __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, uint32_t sz, int ib,
                                            const uint64_t (&qc)[FWP], F&& round) {
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-  const uint32_t nch = (sz + 7u) >> 3;
+  const uint32_t nch = sz >> 3;
   uint32_t cend = nch;  // inclusive scan of the chunk counts over tables
   for (int o = 1; o < L; o <<= 1) {
     const uint32_t y = __shfl_up_sync(kFull, cend, o);
@@ -912,6 +920,7 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   const uint32_t cstart = cend - nch;
   const uint32_t cend_s = lane < L ? cend : kEmpty;  // past the tables: never <= k
   const uint32_t sbase = (uint32_t)lane * T.ns + lo;
+  const uint32_t sentinel = T.ns - kSentinel;  // all-pad chunk of table 0
   for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
     // lane j describes chunk pg + j: table = #tables ending at or before it
     // (binary search over the nondecreasing chunk ends, one shuffle a step)
@@ -926,34 +935,28 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
     t += __shfl_sync(kFull, cend_s, t) <= k ? 1 : 0;
     const uint32_t ts = __shfl_sync(kFull, cstart, t);
     const uint32_t tb = __shfl_sync(kFull, sbase, t);
-    const uint32_t tz = __shfl_sync(kFull, sz, t);
-    const uint32_t o8 = (k - ts) * 8u;
-    const uint32_t my_base = tb + o8;
-    const uint32_t my_len = k < n_chunks ? min(8u, tz - o8) : 0u;
+    // chunks past the union read the sentinel: every load is in bounds and
+    // every entry of a full chunk is used, so the loop has no bounds tests
+    const uint32_t my_base = k < n_chunks ? tb + (k - ts) * 8u : sentinel;
     const uint32_t nr = (min(32u, n_chunks - pg) + 3u) >> 2;
-    // Loads are unconditional (lanes without an entry read slot 0 and carry
-    // idx kEmpty, so their key is kEmpty): no predicated moves in the loop.
+    // source lane 4r + grp wraps past 31 only for rounds >= 8 >= nr, whose
+    // loads are discarded
     auto fetch = [&](int kk, uint32_t& jo, uint64_t (&co)[FWP]) {
-      const uint32_t b = __shfl_sync(kFull, my_base, kk);
-      const uint32_t len = __shfl_sync(kFull, my_len, kk);
-      const bool ok = (uint32_t)sub < len;
-      const uint32_t si = ok ? b + (uint32_t)sub : 0u;
-      const uint32_t jl = __ldg(T.slots + si);
+      const uint32_t si = __shfl_sync(kFull, my_base, kk) + (uint32_t)sub;
+      jo = __ldg(T.slots + si);
       load_code<FWP>(T.bfine + (size_t)si * FWP, co);
-      jo = ok ? jl : kEmpty;
     };
     uint32_t j;
     uint64_t cw[FWP];
     fetch(grp, j, cw);
-    // loads two rounds ahead
     uint32_t j1;
     uint64_t c1[FWP];
-    fetch(min(4 + grp, 31), j1, c1);
+    fetch(4 + grp, j1, c1);
     for (uint32_t r = 0; r < nr; ++r) {
       uint32_t jn;
       uint64_t cn[FWP];
-      fetch(min(4 * (int)(r + 2) + grp, 31), jn, cn);  // past the page: len 0 (or discarded)
-      round(j != kEmpty, (hamming<FWP>(qc, cw) << ib) | j);
+      fetch(4 * (int)(r + 2) + grp, jn, cn);
+      round((hamming<FWP>(qc, cw) << ib) | j);
       j = j1;
       j1 = jn;
 #pragma unroll
@@ -962,7 +965,6 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
         c1[x] = cn[x];
       }
     }
-
   }
 }
 
@@ -1003,13 +1005,14 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     uint32_t lst = kEmpty;
     bool exact = KM != 8;
     if constexpr (KM == 8) {
-      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
+      // dmin: the smallest key that fell off this lane's list
+      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, dmin = kEmpty;
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
+        dmin = min(dmin, max(k3, key));
         k3 = max(k2, min(k3, key));
         k2 = max(k1, min(k2, key));
         k1 = max(k0, min(k1, key));
         k0 = min(k0, key);
-        seen += key != kEmpty ? 1u : 0u;  // pad entries (kEmpty) are not candidates
       });
       // Copies of one key that landed in one lane sit next to each other:
       // squeeze them out so a lane's list is a prefix of its distinct keys.
@@ -1023,12 +1026,15 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           if (k2 == k3) k3 = kEmpty;
         }
       }
-      // Pull r is the smallest key not pulled yet unless a lane that dropped
-      // keys has run dry: then the query reruns on the exact path below.
+      // Pull r is the smallest key not pulled yet, unless some lane dropped a
+      // key below the last pull (it may be missing from the lists; a dropped
+      // copy of a listed key also counts): then the query reruns on the
+      // exact path below.
+      uint32_t m = kEmpty;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         if (r < K) {
-          const uint32_t m = __reduce_min_sync(kFull, k0);
+          m = __reduce_min_sync(kFull, k0);
           lst = lane == r ? m : lst;
           const bool pop = k0 == m;
           k0 = pop ? k1 : k0;
@@ -1037,7 +1043,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           k3 = pop ? kEmpty : k3;
         }
       }
-      exact = __any_sync(kFull, seen > 4u && k0 == kEmpty);
+      exact = __any_sync(kFull, dmin < m);
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
@@ -1047,7 +1053,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // tables is taken once.
       lst = kEmpty;
       uint32_t thr = kEmpty;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](bool, uint32_t key) {
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
         key = key < thr ? key : kEmpty;
         for (;;) {
           const uint32_t m = __reduce_min_sync(kFull, key);
@@ -1507,16 +1513,16 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunc
     }
 
     // ---- per-lane top-4, REDUX pulls (K4 fast path)
-    uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, seen = 0;
+    uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, dmin = kEmpty;
     auto ins = [&](uint32_t key) {
+      dmin = min(dmin, max(k3, key));
       k3 = max(k2, min(k3, key));
       k2 = max(k1, min(k2, key));
       k1 = max(k0, min(k1, key));
       k0 = min(k0, key);
-      seen += key != kEmpty ? 1u : 0u;
     };
     if (staged) walk_smem(tot_cur, qc, ins);
-    else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](bool, uint32_t key) { ins(key); });
+    else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](uint32_t key) { ins(key); });
     if (__any_sync(kFull, (k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty))) {
 #pragma unroll
       for (int rep = 0; rep < 3; ++rep) {
@@ -1525,11 +1531,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunc
         if (k2 == k3) k3 = kEmpty;
       }
     }
-    uint32_t lst = kEmpty;
+    uint32_t lst = kEmpty, mlast = kEmpty;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       if (r < K) {
         const uint32_t m = __reduce_min_sync(kFull, k0);
+        mlast = m;
         lst = lane == r ? m : lst;
         const bool pop = k0 == m;
         k0 = pop ? k1 : k0;
@@ -1538,7 +1545,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunc
         k3 = pop ? kEmpty : k3;
       }
     }
-    if (__any_sync(kFull, seen > 4u && k0 == kEmpty)) {
+    if (__any_sync(kFull, dmin < mlast)) {
       // exact path (see K4): REDUX-driven insertion into a sorted list
       lst = kEmpty;
       uint32_t thr = kEmpty;
@@ -1557,7 +1564,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunc
         }
       };
       if (staged) walk_smem(tot_cur, qc, exact);
-      else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](bool, uint32_t key) { exact(key); });
+      else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](uint32_t key) { exact(key); });
       if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
     }
 

@@ -1,0 +1,12 @@
+#!/bin/bash
+out=gpurun_out/r1t; mkdir -p $out
+timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "rc=$?" >> $out/pytest_gpu.log
+for c in block32 strip500; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $out/bench_$c.json 2> $out/bench_$c.err; done
+timeout 600 python bench.py --config shard16k --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_shard16k.json 2> $out/bench_shard16k.err
+tail -2 $out/pytest_gpu.log
+for c in block32 strip500 shard16k; do python - $out/bench_$c.json <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+print(d['config']['workload'][:10], round(d['value']), round(d['e2e']['value']), {k:round(v,3) for k,v in d['kernel_ms_per_step'].items()}, d['roofline']['frac'])
+PY
+done
