@@ -262,6 +262,10 @@ int bmg_kernel_time(bmg_context* ctx, const char* kernel_class, double* total_ms
 /* Number of projection bits / ratio decisions resolved by the FP64 fixup
  * path in the last row / match (diagnostics). */
 int bmg_fixup_counts(bmg_context* ctx, uint64_t* code_bits, uint64_t* rerank_queries);
+/* Number of queries of the last row / match whose candidate top-K was redone
+ * on the matcher's exact insertion path (a lane's short key list may have
+ * dropped a top-K key; diagnostics). */
+int bmg_exact_walk_count(bmg_context* ctx, uint64_t* queries);
 /* How the last computed row mean was obtained (diagnostics): `rounds` =
  * 1 + the largest number of tiles any channel had to walk (tiles the F96
  * certificate could not clear; every rounding step lies in one of them),

@@ -88,7 +88,7 @@ EXPORTED = [
     "bmg_match", "bmg_compute_codes", "bmg_match_pair", "bmg_execute_plan",
     "bmg_result_pair_count", "bmg_result_match_count", "bmg_result_copy", "bmg_result_metrics",
     "bmg_result_iteration_count", "bmg_result_iteration", "bmg_result_free", "bmg_launch_count",
-    "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_synthetic_counts",
+    "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_exact_walk_count", "bmg_synthetic_counts",
     "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
 ]
 
@@ -141,6 +141,7 @@ def load(path: Path = LIB_PATH):
         "bmg_set_profiling": (C.c_int, [vp, C.c_int]),
         "bmg_kernel_time": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_double), C.POINTER(u64)]),
         "bmg_fixup_counts": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64)]),
+        "bmg_exact_walk_count": (C.c_int, [vp, C.POINTER(u64)]),
         "bmg_row_mean_info": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,

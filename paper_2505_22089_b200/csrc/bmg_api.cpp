@@ -1653,6 +1653,19 @@ int bmg_fixup_counts(bmg_context* c, uint64_t* code_bits, uint64_t* rerank_queri
   });
 }
 
+int bmg_exact_walk_count(bmg_context* c, uint64_t* queries) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    set_device(*c);
+    unsigned long long d[4] = {0, 0, 0, 0};
+    if (c->S().d_diag.p) {
+      BMG_CUDA(cudaMemcpyAsync(d, c->S().d_diag.p, sizeof(d), cudaMemcpyDeviceToHost, c->S().s_comp));
+      BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
+    }
+    if (queries) *queries = d[2];
+  });
+}
+
 int bmg_row_mean_info(bmg_context* c, uint32_t* rounds, int* used_chain) {
   return guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");

@@ -860,8 +860,8 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //      lane (32 per page) and fetched per round with one shuffle; loads run
 //      two rounds ahead;
 //   2. per candidate: 128-bit Hamming via POPC and the unique key
-//      (hamming << idx_bits | train_idx).  Each lane keeps its 4 smallest
-//      keys (branch-free sorted insert); the warp then pulls the K smallest
+//      (hamming << idx_bits | train_idx).  Each lane keeps its kLaneKeys (4)
+//      smallest keys (branch-free sorted insert); the warp then pulls the K smallest
 //      out of the lanes' lists with the single-instruction warp min (REDUX).
 //      Equal keys are the same train index reached from several tables and
 //      are taken once -- the reference's last_seen dedup + stable counting
@@ -876,6 +876,17 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //      lane-per-candidate.
 // ---------------------------------------------------------------------------
 constexpr int kMaxTables = 32;
+// keys each lane keeps during the walk (K4 fast path); a query whose top 8
+// crowd more than this into one lane reruns on the exact path (3 measured no
+// faster: the walk is not bound by the sorted insert)
+#ifndef BMG_LANE_KEYS
+#define BMG_LANE_KEYS 4
+#endif
+constexpr int kLaneKeys = BMG_LANE_KEYS;
+#ifndef BMG_STAGED_RERANK
+#define BMG_STAGED_RERANK 0
+#endif
+constexpr bool kStagedRerank = BMG_STAGED_RERANK != 0;
 
 // FWP code words of one bucket-ordered entry (16-byte loads where possible)
 template <int FWP>
@@ -900,6 +911,15 @@ __device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint
   return h;
 }
 
+// 16-byte global -> shared copy that bypasses registers (cp.async, L2 only)
+__device__ __forceinline__ void cp_async16(float4* dst, const float4* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Walks the union; round(key) is called by every lane once per round
 // (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket range
 // (a whole number of 8-entry chunks); other lanes hold zeros.
@@ -912,9 +932,12 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
   const uint32_t nch = sz >> 3;
   uint32_t cend = nch;  // inclusive scan of the chunk counts over tables
-  for (int o = 1; o < L; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, cend, o);
-    if (lane >= o) cend += y;
+#pragma unroll
+  for (int o = 1; o < kMaxTables; o <<= 1) {
+    if (o < L) {  // warp-uniform
+      const uint32_t y = __shfl_up_sync(kFull, cend, o);
+      cend += lane >= o ? y : 0u;
+    }
   }
   const uint32_t n_chunks = __shfl_sync(kFull, cend, L - 1);
   const uint32_t cstart = cend - nch;
@@ -986,92 +1009,24 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   const float r2f = (float)r2;
   uint32_t n_matched = 0;
 
-  // the next query's bucket ids are loaded one query ahead
-  uint32_t b_next = 0;
-  if (lane < L && w.q_begin + warp < w.q_end) b_next = __ldg(Q.coarse + (size_t)(w.q_begin + warp) * L + lane);
-  for (uint32_t q = w.q_begin + warp; q < w.q_end; q += kWarps) {
-    const uint32_t b = b_next;
-    if (lane < L && q + kWarps < w.q_end) b_next = __ldg(Q.coarse + (size_t)(q + kWarps) * L + lane);
-    uint32_t lo = 0, sz = 0;
-    if (lane < L) {
-      const uint32_t* off = T.offsets + (size_t)lane * nb1 + b;
-      lo = __ldg(off);
-      sz = __ldg(off + 1) - lo;
+  // BMG_STAGED_RERANK=1 (A/B variant, K <= 8): the K kept rows of a query
+  // (and its own row) are copied into the warp's shared-memory slot with
+  // cp.async and ranked one query later, after the next query's walk; each
+  // lane copies and later reads only its own 16-byte piece of every row.
+  // Measured slower (1.13 vs 1.09 ms per launch): the 144 KB of slots take
+  // the L1 capacity the walk's chunk loads hit in.
+  constexpr bool kStaged = KM == 8 && kStagedRerank;
+  extern __shared__ float4 s_rows[];
+  float4* rr = s_rows + (kStaged ? warp * 9 * 32 : 0);
+  uint32_t pq = kEmpty, plst = kEmpty;
+  int pkept = 0;
+  auto emit = [&](uint32_t q, int32_t result) {
+    if (lane == 0) {
+      a.dense[a.dense_off[w.pair] + q] = result;
+      n_matched += result >= 0 ? 1u : 0u;
     }
-    uint64_t qc[FWP];
-#pragma unroll
-    for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
-
-    uint32_t lst = kEmpty;
-    bool exact = KM != 8;
-    if constexpr (KM == 8) {
-      // dmin: the smallest key that fell off this lane's list
-      uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, dmin = kEmpty;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
-        dmin = min(dmin, max(k3, key));
-        k3 = max(k2, min(k3, key));
-        k2 = max(k1, min(k2, key));
-        k1 = max(k0, min(k1, key));
-        k0 = min(k0, key);
-      });
-      // Copies of one key that landed in one lane sit next to each other:
-      // squeeze them out so a lane's list is a prefix of its distinct keys.
-      // Copies in different lanes are popped together below.
-      if (__any_sync(kFull, ((k0 == k1) & (k1 != kEmpty)) | ((k1 == k2) & (k2 != kEmpty)) |
-                                ((k2 == k3) & (k3 != kEmpty)))) {
-#pragma unroll
-        for (int rep = 0; rep < 3; ++rep) {
-          if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
-          if (k1 == k2) { k2 = k3; k3 = kEmpty; }
-          if (k2 == k3) k3 = kEmpty;
-        }
-      }
-      // Pull r is the smallest key not pulled yet, unless some lane dropped a
-      // key below the last pull (it may be missing from the lists; a dropped
-      // copy of a listed key also counts): then the query reruns on the
-      // exact path below.
-      uint32_t m = kEmpty;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (r < K) {
-          m = __reduce_min_sync(kFull, k0);
-          lst = lane == r ? m : lst;
-          const bool pop = k0 == m;
-          k0 = pop ? k1 : k0;
-          k1 = pop ? k2 : k1;
-          k2 = pop ? k3 : k2;
-          k3 = pop ? kEmpty : k3;
-        }
-      }
-      exact = __any_sync(kFull, dmin < m);
-    }
-    if (exact) {
-      // ---- exact path: keys below the current K-th key are pulled out in
-      // ascending order with REDUX and inserted into the sorted list held by
-      // lanes 0..KM-1.  Every lane holding the pulled key clears it, and a
-      // key already listed is skipped, so a train index reached from several
-      // tables is taken once.
-      lst = kEmpty;
-      uint32_t thr = kEmpty;
-      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
-        key = key < thr ? key : kEmpty;
-        for (;;) {
-          const uint32_t m = __reduce_min_sync(kFull, key);
-          if (m >= thr) break;
-          if (key == m) key = kEmpty;
-          if (!__any_sync(kFull, lane < KM && lst == m)) {
-            const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
-            const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
-            lst = lane < KM ? nv : kEmpty;
-            thr = __shfl_sync(kFull, lst, K - 1);
-          }
-        }
-      });
-      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
-    }
-
-    // ---- re-rank + ratio test
-    const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
+  };
+  auto finish = [&](uint32_t q, uint32_t lst, int kept) {
     int32_t result = -1;
     if (kept == 1) {
       result = (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask);
@@ -1081,44 +1036,24 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       float s_min, s_2;
       uint32_t i_min;
       if constexpr (KM == 8) {
-        // FP32 squared distances (packed FP32x2 ops); every sum has depth
-        // <= 13: relative error < (13 + 3) * 2^-24 ~ 1e-6, inside the 1e-5
-        // certification margin below.
+        // lane l holds dims 4l..4l+3 of the query and of every kept
+        // candidate (one coalesced 512-byte row per candidate); a transpose-reduce over lane bits 4, 3, 2
+        // then two xor steps leave candidate c's sum in lanes 4c..4c+3.
+        // FP32 squared distances (packed FP32x2 ops), depth <= 3 + 5 per sum:
+        // relative error ~1e-6, inside the certification margin below.
         const int ck = lane >> 2, part = lane & 3;
         const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
         const float2 neg1 = make_float2(-1.f, -1.f);
-#ifdef BMG_RERANK_4LANE
-        float s = 0.f;
-        if (ck < kept) {
-          const float4* qp = Qd + (size_t)q * 32 + part;
-          const float4* tp = Td + (size_t)jk * 32 + part;
-          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 av = __ldg(qp + 4 * i), bv = __ldg(tp + 4 * i);
-            // d = a - b exactly rounded (b * -1 + a), then s += d * d
-            const float2 d0 = __ffma2_rn(make_float2(bv.x, bv.y), neg1, make_float2(av.x, av.y));
-            const float2 d1 = __ffma2_rn(make_float2(bv.z, bv.w), neg1, make_float2(av.z, av.w));
-            s0 = __ffma2_rn(d0, d0, s0);
-            s1 = __ffma2_rn(d1, d1, s1);
-          }
-          s = (s0.x + s0.y) + (s1.x + s1.y);
-        }
-        s += __shfl_xor_sync(kFull, s, 1);
-        s += __shfl_xor_sync(kFull, s, 2);
-#else
-        // lane l holds dims 4l..4l+3 of the query and of every kept
-        // candidate (each candidate load is one coalesced 512-byte row);
-        // a transpose-reduce over lane bits 4, 3, 2 then two xor steps leave
-        // candidate c's sum in lanes 4c..4c+3.  Depth <= 3 + 5 per sum.
-        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
+        const float4 qv = kStaged ? rr[8 * 32 + lane] : __ldg(Qd + (size_t)q * 32 + lane);
         float pt[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
           pt[c] = 0.f;
+          uint32_t jc = 0;
+          if constexpr (!kStaged) jc = __shfl_sync(kFull, my_idx, c);
           if (c < kept) {
-            const float4 tv = __ldg(Td + (size_t)jc * 32 + lane);
+            const float4 tv = kStaged ? rr[c * 32 + lane] : __ldg(Td + (size_t)jc * 32 + lane);
+            // d = q - t exactly rounded (t * -1 + q), then d * d summed
             const float2 d0 = __ffma2_rn(make_float2(tv.x, tv.y), neg1, make_float2(qv.x, qv.y));
             const float2 d1 = __ffma2_rn(make_float2(tv.z, tv.w), neg1, make_float2(qv.z, qv.w));
             const float2 p2 = __ffma2_rn(d1, d1, __fmul2_rn(d0, d0));
@@ -1141,7 +1076,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         float s = pt[0];
         s += __shfl_xor_sync(kFull, s, 2);
         s += __shfl_xor_sync(kFull, s, 1);
-#endif
         // squared distances are >= 0 (or NaN, caught by `finite`): their
         // bit patterns order like the values, so REDUX finds the (s, idx)
         // argmin and the runner-up
@@ -1251,9 +1185,141 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
       }
     }
-    if (lane == 0) {
-      a.dense[a.dense_off[w.pair] + q] = result;
-      n_matched += result >= 0 ? 1u : 0u;
+    emit(q, result);
+  };
+
+  // the next query's bucket ids are loaded two queries ahead and its bucket
+  // ranges one query ahead (lanes >= L and past the range keep 0 / empty)
+  auto load_b = [&](uint32_t q) -> uint32_t {
+    return lane < L && q < w.q_end ? __ldg(Q.coarse + (size_t)q * L + lane) : kEmpty;
+  };
+  auto load_range = [&](uint32_t b, uint32_t& lo, uint32_t& hi) {
+    lo = hi = 0;
+    if (b != kEmpty) {
+      const uint32_t* off = T.offsets + (size_t)lane * nb1 + b;
+      lo = __ldg(off);
+      hi = __ldg(off + 1);
+    }
+  };
+  uint32_t lo_next, hi_next;
+  load_range(load_b(w.q_begin + warp), lo_next, hi_next);
+  uint32_t b_next = load_b(w.q_begin + warp + kWarps);
+  for (uint32_t q = w.q_begin + warp; q < w.q_end; q += kWarps) {
+    const uint32_t lo = lo_next, sz = hi_next - lo_next;
+    load_range(b_next, lo_next, hi_next);
+    b_next = load_b(q + 2 * kWarps);
+    uint64_t qc[FWP];
+#pragma unroll
+    for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
+
+    uint32_t lst = kEmpty;
+    bool exact = KM != 8;
+    if constexpr (KM == 8) {
+      // Each lane keeps its kLaneKeys smallest keys sorted in kl[]; dmin is
+      // the smallest key that fell off the list.
+      uint32_t kl[kLaneKeys], dmin = kEmpty;
+#pragma unroll
+      for (int i = 0; i < kLaneKeys; ++i) kl[i] = kEmpty;
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
+        dmin = min(dmin, max(kl[kLaneKeys - 1], key));
+#pragma unroll
+        for (int i = kLaneKeys - 1; i > 0; --i) kl[i] = max(kl[i - 1], min(kl[i], key));
+        kl[0] = min(kl[0], key);
+      });
+      // Copies of one key that landed in one lane sit next to each other:
+      // squeeze them out so a lane's list is a prefix of its distinct keys.
+      // Copies in different lanes are popped together below.
+      bool dup = false;
+#pragma unroll
+      for (int i = 0; i + 1 < kLaneKeys; ++i) dup |= (kl[i] == kl[i + 1]) & (kl[i + 1] != kEmpty);
+      if (__any_sync(kFull, dup)) {
+#pragma unroll
+        for (int rep = 0; rep + 1 < kLaneKeys; ++rep) {
+#pragma unroll
+          for (int i = 0; i + 1 < kLaneKeys; ++i) {
+            if (kl[i] == kl[i + 1]) {
+#pragma unroll
+              for (int x = i + 1; x + 1 < kLaneKeys; ++x) kl[x] = kl[x + 1];
+              kl[kLaneKeys - 1] = kEmpty;
+            }
+          }
+        }
+      }
+      // Pull r is the smallest key not pulled yet, unless some lane dropped a
+      // key below the last pull (it may be missing from the lists; a dropped
+      // copy of a listed key also counts): then the query reruns on the
+      // exact path below.
+      uint32_t m = kEmpty;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (r < K) {
+          m = __reduce_min_sync(kFull, kl[0]);
+          lst = lane == r ? m : lst;
+          const bool pop = kl[0] == m;
+#pragma unroll
+          for (int i = 0; i + 1 < kLaneKeys; ++i) kl[i] = pop ? kl[i + 1] : kl[i];
+          kl[kLaneKeys - 1] = pop ? kEmpty : kl[kLaneKeys - 1];
+        }
+      }
+      exact = __any_sync(kFull, dmin < m);
+    }
+    if (exact) {
+      // ---- exact path: keys below the current K-th key are pulled out in
+      // ascending order with REDUX and inserted into the sorted list held by
+      // lanes 0..KM-1.  Every lane holding the pulled key clears it, and a
+      // key already listed is skipped, so a train index reached from several
+      // tables is taken once.
+      lst = kEmpty;
+      uint32_t thr = kEmpty;
+      walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
+        key = key < thr ? key : kEmpty;
+        for (;;) {
+          const uint32_t m = __reduce_min_sync(kFull, key);
+          if (m >= thr) break;
+          if (key == m) key = kEmpty;
+          if (!__any_sync(kFull, lane < KM && lst == m)) {
+            const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
+            const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
+            lst = lane < KM ? nv : kEmpty;
+            thr = __shfl_sync(kFull, lst, K - 1);
+          }
+        }
+      });
+      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
+    }
+
+    // ---- re-rank + ratio test
+    const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
+    if constexpr (kStaged) {
+      // rank the previous query from its staged rows, then stage this one's
+      if (pq != kEmpty) {
+        cp_async_wait_all();
+        finish(pq, plst, pkept);
+      }
+      if (kept > 1) {
+        const uint32_t my_idx = lst & idx_mask;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
+          if (c < kept) cp_async16(rr + c * 32 + lane, Td + (size_t)jc * 32 + lane);
+        }
+        cp_async16(rr + 8 * 32 + lane, Qd + (size_t)q * 32 + lane);
+        cp_async_commit();
+        pq = q;
+        plst = lst;
+        pkept = kept;
+      } else {
+        emit(q, kept == 1 ? (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask) : -1);
+        pq = kEmpty;
+      }
+    } else {
+      finish(q, lst, kept);
+    }
+  }
+  if constexpr (kStaged) {
+    if (pq != kEmpty) {
+      cp_async_wait_all();
+      finish(pq, plst, pkept);
     }
   }
   if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
@@ -1780,7 +1846,16 @@ void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* til
 
 template <int FWP, int KM, int NT, int KC>
 static void launch_match_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  match_kernel<FWP, KM, NT, KC><<<n_work, NT, 0, s>>>(a);
+  // K <= 8: one 9-row re-rank slot per warp (staged rows, see match_kernel)
+  constexpr size_t smem = KM == 8 && kStagedRerank ? (size_t)(NT / 32) * 9 * kDim * sizeof(float) : 0;
+  if constexpr (smem > 48 * 1024) {
+    static const bool configured = [] {
+      return cudaFuncSetAttribute(match_kernel<FWP, KM, NT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem) == cudaSuccess;
+    }();
+    (void)configured;
+  }
+  match_kernel<FWP, KM, NT, KC><<<n_work, NT, smem, s>>>(a);
 }
 
 // staged-union capacity that fits kTmaWarps warps in shared memory

@@ -267,6 +267,12 @@ class Matcher:
         check(self._L.bmg_fixup_counts(self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def exact_walk_count(self):
+        """Queries of the last row / match redone on the exact top-K path."""
+        a = C.c_uint64(0)
+        check(self._L.bmg_exact_walk_count(self.handle, C.byref(a)))
+        return a.value
+
     def row_mean_info(self):
         """(rounds, used_chain) of the last computed row mean (diagnostics)."""
         r, u = C.c_uint32(0), C.c_int(0)
