@@ -27,6 +27,7 @@
 #include <string>
 #include <string_view>
 #include <unordered_map>
+#include <unordered_set>
 #include <utility>
 #include <vector>
 
@@ -302,6 +303,9 @@ struct bmg_context {
   cudaMemPool_t pool = nullptr;
   cudaEvent_t ev_uploaded = nullptr;
   bool pending_upload = false;
+  // projection-ready events the current row's codes must wait for (set by
+  // bmg_execute_plan: the row's mean only needs the copies)
+  std::vector<cudaEvent_t> proj_waits;
   char* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int stage_i = 0;
@@ -441,27 +445,37 @@ void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
   }
 }
 
-// DeviceArena::upload bookkeeping (engine.cpp:18-25): capacity check,
-// counters and the stream-ordered allocation; the copy is issued separately.
-ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
+// DeviceArena::upload bookkeeping (engine.cpp:18-25): capacity check and
+// counters.  bmg_execute_plan runs it in the plan's order; the physical
+// allocation (arena_alloc) may happen in another order.
+void arena_account_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (c.occupancy + n > c.capacity)
     fail(BMG_CAPACITY_EXCEEDED, "uploading image " + std::to_string(id) + " (" + std::to_string(n) +
                                     " units) would raise occupancy to " +
                                     std::to_string(c.occupancy + n) + " of " +
                                     std::to_string(c.capacity));
   if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
+  c.occupancy += n;
+  c.peak = std::max(c.peak, c.occupancy);
+  ++c.uploads;
+  c.units_uploaded += n;
+}
+
+// the stream-ordered allocation of an image's HBM block (descriptors, then
+// its projections and norms); the copy is issued separately (arena_copy)
+ArenaImage& arena_alloc(Ctx& c, uint64_t id, uint64_t n) {
   ArenaImage im;
   im.n = n;
   const size_t bytes = n * 512 + align_up(proj_bytes(n, c.hd.proj_stride), 16);
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(bytes, 512), c.pool, c.s_copy));
   im.proj = im.d + n * kDim;
   im.dnorm = im.proj + n * c.hd.proj_stride;
-  ArenaImage& out = c.resident.emplace(id, im).first->second;
-  c.occupancy += n;
-  c.peak = std::max(c.peak, c.occupancy);
-  ++c.uploads;
-  c.units_uploaded += n;
-  return out;
+  return c.resident.emplace(id, im).first->second;
+}
+
+ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
+  arena_account_upload(c, id, desc, n);
+  return arena_alloc(c, id, n);
 }
 
 uint64_t g_upload_seq = 0;
@@ -502,13 +516,12 @@ void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   arena_copy(c, arena_reserve(c, id, desc, n), desc);
 }
 
-void arena_evict(Ctx& c, uint64_t id) {
+// stream-ordered free of a resident image after every kernel already queued
+// on the compute streams that may read it (the current slot's, and the other
+// slot's row still in flight)
+void arena_free(Ctx& c, uint64_t id) {
   const auto it = c.resident.find(id);
-  if (it == c.resident.end())
-    fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
-  // stream-ordered free after every kernel already queued on the compute
-  // streams that may read the image (the current slot's, and the other
-  // slot's row still in flight)
+  if (it == c.resident.end()) fail(BMG_INVALID_ARGUMENT, "freeing image " + std::to_string(id) + ": not allocated");
   RowSlot& S = c.S();
   RowSlot& O = c.slot[c.cur ^ 1];
   if (O.s_comp) {
@@ -519,11 +532,23 @@ void arena_evict(Ctx& c, uint64_t id) {
   }
   BMG_CUDA(cudaFreeAsync(it->second.d, S.s_comp));
   if (it->second.ev) c.free_events.push_back(it->second.ev);
-  c.occupancy -= it->second.n;
   c.resident.erase(it);
-  ++c.evictions;
   if (S.row_slot.count(id)) S.row_valid = false;
   if (O.row_slot.count(id)) O.row_valid = false;
+}
+
+// DeviceArena::evict bookkeeping (engine.cpp:34-40)
+void arena_account_evict(Ctx& c, uint64_t n) {
+  c.occupancy -= n;
+  ++c.evictions;
+}
+
+void arena_evict(Ctx& c, uint64_t id) {
+  const auto it = c.resident.find(id);
+  if (it == c.resident.end())
+    fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
+  arena_account_evict(c, it->second.n);
+  arena_free(c, id);
 }
 
 void join_uploads(Ctx& c) {
@@ -704,6 +729,8 @@ void prepare_row_views(Ctx& c, const std::vector<RowImage>& descs, const float* 
     BMG_CUDA(cudaEventRecord(e, s));
     c.marks->emplace_back("  mean done", e);
   }
+  for (cudaEvent_t e : c.proj_waits) BMG_CUDA(cudaStreamWaitEvent(s, e, 0));
+  c.proj_waits.clear();
   enqueue_codes_tables(c, d_mean);
 }
 
@@ -1324,14 +1351,6 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       row_base[r + 1] = row_base[r] + cap;
     }
     const uint64_t total_cap = row_base[plan->n_rows];
-    // the last row that needs each image: uploads of a row are issued in
-    // descending order of it, so later rows can start before earlier rows'
-    // other images have arrived
-    std::unordered_map<uint64_t, uint64_t> last_need;
-    for (uint64_t r = 0; r < plan->n_rows; ++r)
-      for (uint64_t k = plan->row_needed_offsets[r]; k < plan->row_needed_offsets[r + 1]; ++k)
-        last_need[plan->needed_ids[k]] = r;
-
     auto res = std::make_unique<bmg_result>();
     reset_results(*c, n_pairs, total_cap);
     res->log = static_cast<int32_t*>(PinnedPool::acquire(8 * std::max<uint64_t>(total_cap, 1), &res->log_bytes));
@@ -1412,37 +1431,150 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       marks.emplace_back(what + " (host issue " + std::to_string(host_ms) + " ms)", e);
     };
     if (timeline) c->marks = &marks;
+    uint64_t xrow = 0;  // rows issued so far (stream priority, slot)
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
+      const uint64_t row0 = row, nr = plan->rows_per_iteration[it];
+      row += nr;
       const uint64_t up0 = c->uploads, units0 = c->units_uploaded;
+      // ---- the arena in the reference's order (engine.cpp:438-444, 491-494):
+      // capacity errors, counters and hooks exactly as the reference raises
+      // them; the device work below may run the rows in another order
+      std::unordered_set<uint64_t> logical;
+      for (const auto& kv : c->resident) logical.insert(kv.first);
+      std::unordered_map<uint64_t, uint64_t> evict_row;  // id -> plan row evicting it
+      bool in_order = (opts->flags & BMG_EXEC_SERIAL) != 0;
+      for (uint64_t r = row0; r < row0 + nr; ++r) {
+        for (uint64_t k = plan->row_needed_offsets[r]; k < plan->row_needed_offsets[r + 1]; ++k) {
+          const uint64_t id = plan->needed_ids[k];
+          if (evict_row.count(id)) in_order = true;  // needed again after its eviction
+          if (logical.count(id)) continue;
+          const bmg_feature_view& fv = features_of(id);
+          arena_account_upload(*c, id, fv.descriptors, fv.count);
+          if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
+          logical.insert(id);
+        }
+        for (uint64_t k = plan->row_evict_offsets[r]; !retain && k < plan->row_evict_offsets[r + 1]; ++k) {
+          const uint64_t id = plan->evict_ids[k];
+          if (!logical.count(id))
+            fail(BMG_NOT_RESIDENT, "cannot evict image " + std::to_string(id) + ": not resident");
+          const auto f = c->resident.find(id);
+          arena_account_evict(*c, f != c->resident.end() ? f->second.n : features_of(id).count);
+          if (opts->on_evict) opts->on_evict(opts->hook_user, id);
+          logical.erase(id);
+          evict_row[id] = r;
+        }
+      }
+      // ---- device order: a row can only start once every image it needs
+      // (its whole needed set: the row mean covers it) is in HBM, so the
+      // first row's uploads are exposed.  Rows of an iteration are
+      // independent: run first the row with the fewest bytes to upload, then
+      // greedily the row with the fewest bytes still missing (for band plans
+      // the reverse of the plan order).  Frees of images an earlier-run row
+      // evicts wait until the last row that needs them has run.
+      std::vector<uint64_t> order(nr);
+      for (uint64_t i = 0; i < nr; ++i) order[i] = row0 + i;
+      if (!in_order && nr > 1) {
+        std::unordered_set<uint64_t> have;
+        for (const auto& kv : c->resident) have.insert(kv.first);
+        std::vector<char> done(nr, 0);
+        for (uint64_t e = 0; e < nr; ++e) {
+          uint64_t best = nr, best_units = ~0ull;
+          for (uint64_t i = 0; i < nr; ++i) {
+            if (done[i]) continue;
+            uint64_t units = 0;
+            for (uint64_t k = plan->row_needed_offsets[row0 + i]; k < plan->row_needed_offsets[row0 + i + 1]; ++k)
+              if (!have.count(plan->needed_ids[k])) units += features_of(plan->needed_ids[k]).count + 1;
+            if (units < best_units) best = i, best_units = units;  // ties: plan order
+          }
+          done[best] = 1;
+          order[e] = row0 + best;
+          for (uint64_t k = plan->row_needed_offsets[row0 + best]; k < plan->row_needed_offsets[row0 + best + 1]; ++k)
+            have.insert(plan->needed_ids[k]);
+        }
+      }
+      // position of each row in `order`, the last position needing each
+      // image, when each evicted image can be freed, and the HBM peak (units)
+      std::unordered_map<uint64_t, uint64_t> last_need;
+      std::vector<std::vector<uint64_t>> frees;
+      auto schedule = [&]() -> uint64_t {
+        std::unordered_map<uint64_t, uint64_t> pos_of;
+        last_need.clear();
+        frees.assign(nr, {});
+        for (uint64_t e = 0; e < nr; ++e) {
+          pos_of[order[e]] = e;
+          for (uint64_t k = plan->row_needed_offsets[order[e]]; k < plan->row_needed_offsets[order[e] + 1]; ++k)
+            last_need[plan->needed_ids[k]] = e;
+        }
+        for (const auto& [id, r] : evict_row) {
+          uint64_t e = pos_of[r];
+          const auto f = last_need.find(id);
+          if (f != last_need.end()) e = std::max(e, f->second);
+          frees[e].push_back(id);
+        }
+        for (auto& v : frees) std::sort(v.begin(), v.end());
+        std::unordered_set<uint64_t> have;
+        uint64_t units = 0, peak = 0;
+        for (const auto& kv : c->resident) have.insert(kv.first), units += kv.second.n;
+        for (uint64_t e = 0; e < nr; ++e) {
+          for (uint64_t k = plan->row_needed_offsets[order[e]]; k < plan->row_needed_offsets[order[e] + 1]; ++k)
+            if (have.insert(plan->needed_ids[k]).second) units += features_of(plan->needed_ids[k]).count;
+          peak = std::max(peak, units);
+          for (uint64_t id : frees[e]) units -= features_of(id).count, have.erase(id);
+        }
+        return peak;
+      };
+      const uint64_t peak = schedule();
+      if (peak > c->capacity && !std::is_sorted(order.begin(), order.end())) {
+        // deferred frees would hold more than the arena's capacity: allowed
+        // while the overshoot fits comfortably in free HBM, else plan order
+        size_t free_b = 0, total_b = 0;
+        BMG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t unit_b = 512 + sizeof(float) * (c->hd.proj_stride + 1);
+        if ((peak - c->capacity) * unit_b > free_b / 2) {
+          for (uint64_t i = 0; i < nr; ++i) order[i] = row0 + i;
+          schedule();
+        }
+      }
       uint64_t it_pairs = 0;
-      for (uint64_t r = 0; r < plan->rows_per_iteration[it]; ++r, ++row) {
-        c->cur = (opts->flags & BMG_EXEC_SERIAL) ? 0 : static_cast<int>(row & 1);
+      for (uint64_t e = 0; e < nr; ++e, ++xrow) {
+        const uint64_t r = order[e];
+        c->cur = (opts->flags & BMG_EXEC_SERIAL) ? 0 : static_cast<int>(xrow & 1);
         RowSlot& S = c->S();
         if (!(opts->flags & BMG_EXEC_SERIAL)) {
-          cudaStream_t st = row < c->s_prio.size() ? c->s_prio[row] : S.home;
+          cudaStream_t st = xrow < c->s_prio.size() ? c->s_prio[xrow] : S.home;
           if (st != S.s_comp) BMG_CUDA(cudaStreamWaitEvent(st, S.done, 0));
           S.s_comp = st;
         }
-        const uint64_t nb = plan->row_needed_offsets[row], ne = plan->row_needed_offsets[row + 1];
+        const uint64_t nb = plan->row_needed_offsets[r], ne = plan->row_needed_offsets[r + 1];
         const uint64_t* needed = plan->needed_ids + nb;
-        // uploads: bookkeeping + hooks in the reference order (engine.cpp:438-444),
-        // the copies in the order that lets later rows start early
+        // the row's missing images, copied in descending order of the last
+        // row that needs them, so later rows can start before this row's
+        // other images have arrived
         missing.clear();
         for (uint64_t k = nb; k < ne; ++k) {
           const uint64_t id = plan->needed_ids[k];
-          const bmg_feature_view& fv = features_of(id);
           if (!c->resident.count(id)) {
-            arena_reserve(*c, id, fv.descriptors, fv.count);
-            if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
+            arena_alloc(*c, id, features_of(id).count);
             missing.push_back(id);
           }
         }
         std::stable_sort(missing.begin(), missing.end(),
                          [&](uint64_t x, uint64_t y) { return last_need[x] > last_need[y]; });
-        for (uint64_t id : missing) arena_copy(*c, c->resident.at(id), features_of(id).descriptors);
-        if (!missing.empty()) mark("row " + std::to_string(row) + " uploads done", c->s_copy);
-        // the row's stream waits, per projection stream, for the last image
-        // of the row that stream handled (its events are in stream order)
+        for (size_t k = 0; k < missing.size(); ++k) {
+          arena_copy(*c, c->resident.at(missing[k]), features_of(missing[k]).descriptors);
+          if (timeline && k % 25 == 24) mark("row " + std::to_string(r) + " upload " + std::to_string(k + 1), c->s_copy);
+        }
+        if (!missing.empty()) mark("row " + std::to_string(r) + " uploads done", c->s_copy);
+        // the row's mean waits only for the copies (the copy stream is in
+        // order: an event after this row's copies covers every earlier one);
+        // its codes wait, per projection stream, for the last image of the
+        // row that stream projected (its events are in stream order)
+        {
+          cudaEvent_t e = take_event(*c);
+          BMG_CUDA(cudaEventRecord(e, c->s_copy));
+          BMG_CUDA(cudaStreamWaitEvent(S.s_comp, e, 0));
+          c->free_events.push_back(e);
+        }
         const ArenaImage* last[bmg_context::kProjStreams] = {};
         for (uint64_t k = 0; k < ne - nb; ++k) {
           const auto f = c->resident.find(needed[k]);
@@ -1450,13 +1582,14 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           const ArenaImage*& l = last[f->second.pstream];
           if (!l || f->second.seq > l->seq) l = &f->second;
         }
+        c->proj_waits.clear();
         for (const ArenaImage* l : last)
-          if (l) BMG_CUDA(cudaStreamWaitEvent(S.s_comp, l->ev, 0));
+          if (l) c->proj_waits.push_back(l->ev);
         c->pending_upload = false;
-        mark("row " + std::to_string(row) + " start", S.s_comp);
+        mark("row " + std::to_string(r) + " start", S.s_comp);
         prepare_row(*c, needed, ne - nb, nullptr);
-        mark("row " + std::to_string(row) + " codes+tables done", S.s_comp);
-        const uint64_t pb = plan->row_pair_offsets[row], pe = plan->row_pair_offsets[row + 1];
+        mark("row " + std::to_string(r) + " codes+tables done", S.s_comp);
+        const uint64_t pb = plan->row_pair_offsets[r], pe = plan->row_pair_offsets[r + 1];
         std::vector<std::pair<int, int>> sp;
         sp.reserve(pe - pb);
         for (uint64_t p = pb; p < pe; ++p) {
@@ -1466,18 +1599,15 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
           sp.emplace_back(qa->second, tb->second);
         }
-        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log, row_base[row]);
-        mark("row " + std::to_string(row) + " match done", S.s_comp);
+        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log, row_base[r]);
+        mark("row " + std::to_string(r) + " match done", S.s_comp);
         // the row's log region goes to the result's pinned buffer while the
         // next row computes
-        if (row_base[row + 1] > row_base[row])
-          BMG_CUDA(cudaMemcpyAsync(res->log + 2 * row_base[row], d_log + 2 * row_base[row],
-                                   8 * (row_base[row + 1] - row_base[row]), cudaMemcpyDeviceToHost, S.s_comp));
+        if (row_base[r + 1] > row_base[r])
+          BMG_CUDA(cudaMemcpyAsync(res->log + 2 * row_base[r], d_log + 2 * row_base[r],
+                                   8 * (row_base[r + 1] - row_base[r]), cudaMemcpyDeviceToHost, S.s_comp));
         it_pairs += pe - pb;
-        for (uint64_t k = plan->row_evict_offsets[row]; !retain && k < plan->row_evict_offsets[row + 1]; ++k) {
-          arena_evict(*c, plan->evict_ids[k]);
-          if (opts->on_evict) opts->on_evict(opts->hook_user, plan->evict_ids[k]);
-        }
+        for (uint64_t id : frees[e]) arena_free(*c, id);
         BMG_CUDA(cudaEventRecord(S.done, S.s_comp));
       }
       res->iterations.push_back(it_pairs);

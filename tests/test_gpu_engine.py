@@ -143,3 +143,26 @@ def test_result_views_outlive_the_call(reference, tmp_path):
         bm.execute_plan(plan, feats, arena)
     for k in saved:
         assert np.array_equal(saved[k], copies[k]), k
+
+
+def test_rows_run_out_of_order_but_hooks_follow_the_plan(reference, tmp_path):
+    # the device runs each iteration's rows fewest-uploads-first (band plans:
+    # last row first); the arena's hooks and counters must still follow the
+    # plan's row order (engine.cpp:438-444, 491-494), results unchanged
+    plan, ref, rc, res, arena, ups, evs, feats = run_both(reference, tmp_path, 16, 400, 3, 4, 8, seed=13)
+    assert any(len(it.rows) > 1 for it in plan.iterations)
+    resident, exp_ups, exp_evs = set(), [], []
+    for it in plan.iterations:
+        for row in it.rows:
+            for i in row.needed():
+                if i not in resident:
+                    resident.add(i)
+                    exp_ups.append((i, len(feats[i].descriptors)))
+            for i in row.evict_after:
+                resident.discard(i)
+                exp_evs.append(i)
+    assert ups == exp_ups and evs == exp_evs
+    got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    for key, m in ref.items():
+        assert np.array_equal(got[key], m), key
+    assert res.metrics.peak_occupancy == rc["peak_occupancy"] and arena.occupancy() == 0
