@@ -883,6 +883,11 @@ constexpr int kMaxTables = 32;
 #define BMG_LANE_KEYS 4
 #endif
 constexpr int kLaneKeys = BMG_LANE_KEYS;
+// rounds the candidate walk's loads run ahead of their use
+#ifndef BMG_WALK_DEPTH
+#define BMG_WALK_DEPTH 2
+#endif
+constexpr int kWalkDepth = BMG_WALK_DEPTH;
 #ifndef BMG_STAGED_RERANK
 #define BMG_STAGED_RERANK 0
 #endif
@@ -969,24 +974,25 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
       jo = __ldg(T.slots + si);
       load_code<FWP>(T.bfine + (size_t)si * FWP, co);
     };
-    uint32_t j;
-    uint64_t cw[FWP];
-    fetch(grp, j, cw);
-    uint32_t j1;
-    uint64_t c1[FWP];
-    fetch(4 + grp, j1, c1);
+    // loads run kWalkDepth rounds ahead
+    uint32_t jr[kWalkDepth];
+    uint64_t cr[kWalkDepth][FWP];
+#pragma unroll
+    for (int d = 0; d < kWalkDepth; ++d) fetch(4 * d + grp, jr[d], cr[d]);
     for (uint32_t r = 0; r < nr; ++r) {
       uint32_t jn;
       uint64_t cn[FWP];
-      fetch(4 * (int)(r + 2) + grp, jn, cn);
-      round((hamming<FWP>(qc, cw) << ib) | j);
-      j = j1;
-      j1 = jn;
+      fetch(4 * (int)(r + kWalkDepth) + grp, jn, cn);
+      round((hamming<FWP>(qc, cr[0]) << ib) | jr[0]);
 #pragma unroll
-      for (int x = 0; x < FWP; ++x) {
-        cw[x] = c1[x];
-        c1[x] = cn[x];
+      for (int d = 0; d + 1 < kWalkDepth; ++d) {
+        jr[d] = jr[d + 1];
+#pragma unroll
+        for (int x = 0; x < FWP; ++x) cr[d][x] = cr[d + 1][x];
       }
+      jr[kWalkDepth - 1] = jn;
+#pragma unroll
+      for (int x = 0; x < FWP; ++x) cr[kWalkDepth - 1][x] = cn[x];
     }
   }
 }
