@@ -199,7 +199,7 @@ class PinnedPool {
     }
     const size_t n = align_up(std::max<size_t>(bytes, 1), 1 << 20);
     void* p = nullptr;
-    if (cudaHostAlloc(&p, n, cudaHostAllocPortable) != cudaSuccess) {
+    if (cudaHostAlloc(&p, n, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
       cudaGetLastError();
       fail(BMG_OUT_OF_MEMORY, "pinned result buffer allocation failed");
     }
@@ -909,10 +909,12 @@ void copy_codes_out(Ctx& c, const ImgDev& im, uint32_t* coarse_out, uint64_t* fi
   BMG_CUDA(cudaStreamSynchronize(c.S().s_comp));
 }
 
-void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity) {
+// capacity: matches the device log must hold (0: the caller compacts into
+// its own buffer)
+void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity, bool host_mirror = true) {
   c.res_ranges.ensure(sizeof(uint64_t) * 2 * std::max<uint64_t>(n_pairs, 1));  // [begin, end) per pair
-  c.res_log.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
-  c.d_res.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
+  if (host_mirror) c.res_log.ensure(sizeof(int32_t) * 2 * std::max<uint64_t>(capacity, 1));
+  if (capacity) c.d_res.ensure(sizeof(int32_t) * 2 * capacity);
 }
 
 // After the compute stream drained: DMA the log entries [0, end) into the
@@ -1352,10 +1354,18 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     }
     const uint64_t total_cap = row_base[plan->n_rows];
     auto res = std::make_unique<bmg_result>();
-    reset_results(*c, n_pairs, total_cap);
+    // BMG_LOG_ZC=1 (A/B switch): every row compacts straight into pinned
+    // host memory; default: only the call's last row does
+    static const bool log_zc_all = [] {
+      const char* v = getenv("BMG_LOG_ZC");
+      return v && v[0] == '1';
+    }();
+    reset_results(*c, n_pairs, log_zc_all ? 0 : total_cap, false);
     res->log = static_cast<int32_t*>(PinnedPool::acquire(8 * std::max<uint64_t>(total_cap, 1), &res->log_bytes));
     uint64_t* d_off = c->res_ranges.dev<uint64_t>();
-    int32_t* d_log = c->d_res.as<int32_t>();
+    int32_t* d_log = log_zc_all ? nullptr : c->d_res.as<int32_t>();
+    int32_t* h_log = nullptr;
+    BMG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_log), res->log, 0));
     c->cur = 0;
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->slot[0].s_comp));
@@ -1599,11 +1609,14 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
             fail(BMG_INVALID_ARGUMENT, "block pair image missing from the row's resident set");
           sp.emplace_back(qa->second, tb->second);
         }
-        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, d_log, row_base[r]);
+        // a row's log region goes to the result's pinned buffer by DMA while
+        // later rows compute; the call's last row, whose transfer nothing
+        // hides, compacts straight into pinned host memory over PCIe (only
+        // its matches cross, not its capacity-sized region)
+        const bool log_dma = !log_zc_all && (it + 1 < plan->n_iterations || e + 1 < nr);
+        enqueue_match(*c, sp, opts->match, d_off + 2 * pb, log_dma ? d_log : h_log, row_base[r]);
         mark("row " + std::to_string(r) + " match done", S.s_comp);
-        // the row's log region goes to the result's pinned buffer while the
-        // next row computes
-        if (row_base[r + 1] > row_base[r])
+        if (log_dma && row_base[r + 1] > row_base[r])
           BMG_CUDA(cudaMemcpyAsync(res->log + 2 * row_base[r], d_log + 2 * row_base[r],
                                    8 * (row_base[r + 1] - row_base[r]), cudaMemcpyDeviceToHost, S.s_comp));
         it_pairs += pe - pb;

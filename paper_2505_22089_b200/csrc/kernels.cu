@@ -1718,11 +1718,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* __restrict
     const int32_t v = q < n ? d[q] : -1;
     const uint32_t f = v >= 0 ? 1u : 0u;
     const uint32_t incl = block_incl_scan(f, s_warp);
-    if (f) {
-      const uint64_t o = base + incl - 1;
-      out[2 * o] = (int32_t)q;
-      out[2 * o + 1] = v;
-    }
+    if (f) reinterpret_cast<int2*>(out)[base + incl - 1] = make_int2((int32_t)q, v);
     if (threadIdx.x == blockDim.x - 1) s_base = incl;
     __syncthreads();
     base += s_base;
