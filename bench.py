@@ -152,10 +152,15 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(avg_ctas_per_launch):
+    """DRAM bytes of one match launch from the committed `ncu --set full`
+    capture, scaled by CTA count (one CTA = 1,024 queries of one pair) from
+    the captured launch to this run's average launch (ncu: cold L2,
+    serialised)."""
     try:
-        j = json.loads(NCU_SUMMARY.read_text())
-        return j.get("match_kernel", {}).get("dram_bytes_per_launch")
+        m = json.loads(NCU_SUMMARY.read_text())["match_kernel"]
+        grid = float(str(m["metrics"]["launch__grid_size"]).split()[0].replace(",", ""))
+        return m["dram_bytes_per_launch"] / grid * avg_ctas_per_launch
     except Exception:
         return None
 
@@ -376,7 +381,9 @@ def main():
     avg_launch_s = match_ms * 1e-3 / max(match_n, 1)
     peak, peak_src = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
-    traffic = ncu_traffic()
+    step_ctas = sum(-(-len(feats[a].descriptors) // 1024)
+                    for it in plan.iterations for row in it.rows for b in row.blocks for a, _ in b.pairs)
+    traffic = ncu_traffic(step_ctas * args.steps / max(match_n, 1))
 
     line = None
     if rank == 0:

@@ -12,5 +12,7 @@ done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $out/ncu_launch.log 2>&1
 timeout 900 python bench.py --steps 10 --warmup 3 > $out/bench.json 2> $out/bench.err
-timeout 900 python bench.py --config strip500 --steps 3 --warmup 3 --no-cpu-baseline > $out/bench_strip.json 2> $out/bench_strip.err
+timeout 900 python bench.py --config strip500 --steps 5 --warmup 3 > $out/bench_strip.json 2> $out/bench_strip.err
+timeout 900 python bench.py --config shard16k --steps 5 --warmup 3 > $out/bench_shard16k.json 2> $out/bench_shard16k.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_ref.json 2> $out/bench_ref.err
 ls $out
