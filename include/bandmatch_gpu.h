@@ -58,7 +58,9 @@ typedef enum {
   BMG_CUDA_ERROR = 5,         /* "CudaError"        */
   BMG_OUT_OF_MEMORY = 6,      /* "OutOfMemory"      */
   BMG_UNSUPPORTED = 7,        /* "Unsupported"      */
-  BMG_INVALID_SCENE = 8       /* "InvalidScene" / "ZeroVector" (features.cpp:60, 69-78) */
+  BMG_INVALID_SCENE = 8,      /* "InvalidScene" / "ZeroVector" (features.cpp:60, 69-78) */
+  BMG_FORMAT_ERROR = 9,       /* "FormatError"   (binary_io.hpp:63-67, features.cpp, hashmatch.cpp) */
+  BMG_TRUNCATED_FILE = 10     /* "TruncatedFile" (binary_io.hpp:37-43) */
 } bmg_status;
 
 typedef struct bmg_context bmg_context;
@@ -248,6 +250,27 @@ int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out[3]);
  * the first row to the last kernel of the last row. */
 int bmg_result_device_ms(const bmg_result* r, double* ms_out);
 void bmg_result_free(bmg_result* r);
+/* write_matches_binary (hashmatch.cpp:311-332) of the result: the "BMMT" file
+ * the reference writes for the same ExecutionResult, byte for byte (pairs in
+ * IdPair order, stage Initial), straight from the pinned log. */
+int bmg_result_write_matches(const bmg_result* r, const char* path);
+
+/* ---- file formats either side of the path ------ */
+/* read_features (features.cpp:222-249): header only (image id, count). */
+int bmg_read_features_header(const char* path, uint64_t* image_id, uint64_t* count);
+/* read_features into caller buffers (e.g. pinned host memory for the H2D):
+ * descriptors_out[count][128], keypoints_out[count][4] (x, y, scale,
+ * orientation; may be NULL), capacity = features the buffers hold; the
+ * records are read in large blocks by `threads` threads.  Same checks and
+ * error codes / messages as the reference (FormatError, TruncatedFile). */
+int bmg_read_features(const char* path, uint64_t capacity, float* descriptors_out,
+                      float* keypoints_out, int threads, uint64_t* image_id, uint64_t* count);
+/* write_matches_binary (hashmatch.cpp:311-332) from flat arrays: pair_ids
+ * [2*n_pairs] unique and sorted by IdPair, ranges[2*n_pairs] = [begin, end)
+ * into log (int32 (qi, ti) pairs), stages[n_pairs] (0 = Initial, 1 =
+ * Verified; NULL = all Initial). */
+int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t* pair_ids,
+                             const uint64_t* ranges, const int32_t* log, const uint8_t* stages);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* Number of kernels this context has launched so far. */

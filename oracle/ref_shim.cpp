@@ -35,6 +35,7 @@ int status_of(const std::string& code) {
   if (code == "FormatError") return 5;
   if (code == "BudgetTooSmall") return 6;
   if (code == "EmptyGraph") return 7;
+  if (code == "TruncatedFile") return 8;
   return 99;
 }
 
@@ -339,6 +340,52 @@ int ref_execute_plan_threaded(const char* plan_path, void* features, uint64_t ha
     *pairs_done = done;
     *total_matches = m;
     *wall_s_out = dt.count();
+  });
+}
+
+// File formats: the reference's own writers and
+// reader, for byte-level parity and as the timed CPU baseline of tools/io_bench.py.
+int ref_write_features(const char* path, uint64_t id, const float* desc, const float* kp, uint64_t n) {
+  return guarded([&] {
+    FeatureSet fs = fs_from(id, desc, n);
+    for (uint64_t i = 0; i < n; ++i)
+      fs.keypoints[i] = Keypoint{kp[4 * i], kp[4 * i + 1], kp[4 * i + 2], kp[4 * i + 3]};
+    write_features(path, fs);
+  });
+}
+
+// read_features; desc_out / kp_out may be null (count only)
+int ref_read_features(const char* path, uint64_t capacity, uint64_t* id, uint64_t* n, float* desc_out,
+                      float* kp_out) {
+  return guarded([&] {
+    const FeatureSet fs = read_features(path);
+    *id = fs.image_id;
+    *n = fs.size();
+    if (desc_out && fs.size() <= capacity) {
+      std::memcpy(desc_out, fs.descriptors.data(), fs.size() * sizeof(Descriptor));
+      for (size_t i = 0; i < fs.size(); ++i) {
+        kp_out[4 * i] = fs.keypoints[i].x;
+        kp_out[4 * i + 1] = fs.keypoints[i].y;
+        kp_out[4 * i + 2] = fs.keypoints[i].scale;
+        kp_out[4 * i + 3] = fs.keypoints[i].orientation;
+      }
+    }
+  });
+}
+
+// write_matches_binary of pairs[p] = (q, t) with matches[offsets[p]..offsets[p+1])
+int ref_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t* pair_ids,
+                             const uint64_t* offsets, const int32_t* matches, const uint8_t* stages) {
+  return guarded([&] {
+    std::vector<PairMatches> all(n_pairs);
+    for (uint64_t p = 0; p < n_pairs; ++p) {
+      all[p].query_image = pair_ids[2 * p];
+      all[p].train_image = pair_ids[2 * p + 1];
+      all[p].stage = stages && stages[p] ? PairMatches::Stage::kVerified : PairMatches::Stage::kInitial;
+      for (uint64_t m = offsets[p]; m < offsets[p + 1]; ++m)
+        all[p].matches.emplace_back(matches[2 * m], matches[2 * m + 1]);
+    }
+    write_matches_binary(path, all);
   });
 }
 

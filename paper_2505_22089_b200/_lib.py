@@ -18,6 +18,7 @@ DIM = 128
 STATUS_NAMES = {
     0: "Ok", 1: "InvalidArgument", 2: "HashMismatch", 3: "CapacityExceeded",
     4: "NotResident", 5: "CudaError", 6: "OutOfMemory", 7: "Unsupported", 8: "InvalidScene",
+    9: "FormatError", 10: "TruncatedFile",
 }
 
 
@@ -90,6 +91,8 @@ EXPORTED = [
     "bmg_result_iteration_count", "bmg_result_iteration", "bmg_result_free", "bmg_launch_count",
     "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_exact_walk_count", "bmg_synthetic_counts",
     "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
+    "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
+    "bmg_write_matches_binary",
 ]
 
 _lib = None
@@ -136,6 +139,10 @@ def load(path: Path = LIB_PATH):
         "bmg_result_iteration_count": (u64, [vp]),
         "bmg_result_iteration": (C.c_int, [vp, u64, vp]),
         "bmg_result_free": (None, [vp]),
+        "bmg_result_write_matches": (C.c_int, [vp, C.c_char_p]),
+        "bmg_read_features_header": (C.c_int, [C.c_char_p, C.POINTER(u64), C.POINTER(u64)]),
+        "bmg_read_features": (C.c_int, [C.c_char_p, u64, vp, vp, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
+        "bmg_write_matches_binary": (C.c_int, [C.c_char_p, u64, vp, vp, vp, vp]),
         "bmg_result_device_ms": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "bmg_launch_count": (u64, [vp]),
         "bmg_set_profiling": (C.c_int, [vp, C.c_int]),

@@ -948,6 +948,8 @@ const char* bmg_status_name(int status) {
     case BMG_OUT_OF_MEMORY: return "OutOfMemory";
     case BMG_UNSUPPORTED: return "Unsupported";
     case BMG_INVALID_SCENE: return "InvalidScene";
+    case BMG_FORMAT_ERROR: return "FormatError";
+    case BMG_TRUNCATED_FILE: return "TruncatedFile";
     default: return "Unknown";
   }
 }
@@ -1717,6 +1719,15 @@ int bmg_result_view(const bmg_result* r, const uint64_t** pair_ids, const uint64
     *ranges = r->ranges.data();
     *log = r->log;
   });
+}
+
+int bmg_result_write_matches(const bmg_result* r, const char* path) {
+  if (!r) {
+    bmg::set_last_error("null result");
+    return BMG_INVALID_ARGUMENT;
+  }
+  return bmg_write_matches_binary(path, r->pair_ids.size() / 2, r->pair_ids.data(), r->ranges.data(), r->log,
+                                  nullptr);
 }
 
 int bmg_result_metrics(const bmg_result* r, uint64_t counters_out[6], double* wall_s_out) {

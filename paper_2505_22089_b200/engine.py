@@ -295,8 +295,14 @@ class _PairList(Sequence):
 
     _EMPTY = np.zeros((0, 2), np.int32)
 
-    def __init__(self, ids, rng, log):
-        self._ids, self._rng, self._log = ids, rng, log
+    def __init__(self, ids, rng, log, holder=None):
+        self._ids, self._rng, self._log, self._holder = ids, rng, log, holder
+
+    def _write_bmmt(self, bpath: bytes):
+        """write_matches_binary of the whole result from its pinned log."""
+        if self._holder is None or not self._holder.h:
+            raise BandmatchError("InvalidArgument", "result buffer already released")
+        check(self._holder.L.bmg_result_write_matches(self._holder.h, bpath))
 
     def __len__(self):
         return len(self._ids) // 2
@@ -383,7 +389,7 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
         rng = np.ctypeslib.as_array(rng_p, (2 * npairs,)).copy()
         top = int(rng[1::2].max()) if nm else 0
         log = holder.wrap(np.ctypeslib.as_array(log_p, (max(2 * top, 1),))).reshape(-1, 2) if top else None
-        matches = _PairList(ids, rng, log)
+        matches = _PairList(ids, rng, log, holder)
     else:
         holder.close()
     c = [int(x) for x in counters]

@@ -81,29 +81,26 @@ def write_features(path, fs: FeatureSet) -> None:
         f.write(np.ascontiguousarray(rec, "<f4").tobytes())
 
 
-def read_features(path) -> FeatureSet:
-    """read_features, features.cpp:222-249, as one bulk read."""
-    try:
-        data = Path(path).read_bytes()
-    except OSError:
-        raise BandmatchError("FormatError", f"cannot open {path} for reading")
-    if len(data) < 4:
-        raise BandmatchError("TruncatedFile", "unexpected end of file while reading feature file magic")
-    if data[:4] != _MAGIC:
-        raise BandmatchError("FormatError", 'feature file: bad magic, expected "BMF1"')
-    if len(data) < 24:
-        raise BandmatchError("TruncatedFile", "unexpected end of file while reading header")
-    version, image_id, count, dim = struct.unpack("<IQII", data[4:24])
-    if version != 1:
-        raise BandmatchError("FormatError", f"unsupported feature file version {version}")
-    if dim != DIM:
-        raise BandmatchError("FormatError", f"descriptor dim {dim} != 128")
-    need = count * (4 + DIM) * 4
-    if len(data) - 24 < need:
-        raise BandmatchError("TruncatedFile", "unexpected end of file while reading descriptor")
-    rec = np.frombuffer(data, "<f4", count * (4 + DIM), 24).reshape(count, 4 + DIM)
-    fs = FeatureSet(image_id, np.ascontiguousarray(rec[:, 4:], np.float32))
-    fs.keypoints = np.ascontiguousarray(rec[:, :4], np.float32)
+def read_features(path, pinned=None, threads: int = 8) -> FeatureSet:
+    """read_features, features.cpp:222-249 (same checks, FormatError /
+    TruncatedFile), natively: libbmg reads the 528-byte records in large
+    blocks on ``threads`` threads straight into the arrays.  ``pinned``:
+    optional callable nbytes -> buffer (e.g. pinned host memory) that backs
+    the descriptors, so the arena's H2D reads them directly."""
+    L = _lib.load()
+    bpath = str(path).encode()
+    iid, n = C.c_uint64(0), C.c_uint64(0)
+    check(L.bmg_read_features_header(bpath, C.byref(iid), C.byref(n)))
+    count = n.value
+    if pinned is not None:
+        desc = np.frombuffer(pinned(max(count, 1) * DIM * 4), np.float32, max(count, 1) * DIM)
+        desc = desc[: count * DIM].reshape(count, DIM)
+    else:
+        desc = np.empty((count, DIM), np.float32)
+    kps = np.empty((count, 4), np.float32)
+    check(L.bmg_read_features(bpath, count, ptr(desc), ptr(kps), threads, C.byref(iid), C.byref(n)))
+    fs = FeatureSet(iid.value, desc)
+    fs.keypoints = kps
     return fs
 
 

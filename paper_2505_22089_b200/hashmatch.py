@@ -343,15 +343,25 @@ def _sorted_by_pair(all_pm):
 
 
 def write_matches_binary(path, all_pm) -> None:
-    """BMMT writer, hashmatch.cpp:311-332."""
+    """BMMT writer, hashmatch.cpp:311-332, natively (libbmg).  The matches of
+    an ``execute_plan`` result are written straight from its pinned log;
+    other lists are put in ``sorted_by_pair`` order first (:243-250)."""
+    L = _lib.load()
+    writer = getattr(all_pm, "_write_bmmt", None)
+    if writer is not None:
+        writer(str(path).encode())
+        return
     ordered = _sorted_by_pair(all_pm)
-    with open(path, "wb") as f:
-        f.write(b"BMMT")
-        f.write(struct.pack("<IQ", 1, len(ordered)))
-        for pm in ordered:
-            f.write(struct.pack("<QQBI", pm.query_image, pm.train_image,
-                                1 if pm.stage == "verified" else 0, len(pm.matches)))
-            f.write(np.ascontiguousarray(pm.matches, "<u4").tobytes())
+    n = len(ordered)
+    ids = np.array([(pm.query_image, pm.train_image) for pm in ordered], np.uint64).reshape(-1)
+    counts = np.array([len(pm.matches) for pm in ordered], np.uint64)
+    ends = np.cumsum(counts, dtype=np.uint64)
+    ranges = np.stack([ends - counts, ends], 1).reshape(-1) if n else np.zeros(0, np.uint64)
+    log = (np.concatenate([np.asarray(pm.matches, np.int32).reshape(-1, 2) for pm in ordered])
+           if n else np.zeros((0, 2), np.int32))
+    log = np.ascontiguousarray(log, np.int32)
+    stages = np.array([1 if pm.stage == "verified" else 0 for pm in ordered], np.uint8)
+    check(L.bmg_write_matches_binary(str(path).encode(), n, ptr(ids), ptr(ranges), ptr(log), ptr(stages)))
 
 
 def read_matches_binary(path):

@@ -176,6 +176,39 @@ class Reference:
                                                 C.c_uint64, C.POINTER(C.c_uint64),
                                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
 
+        L.ref_write_features.argtypes = [C.c_char_p, C.c_uint64, _f32p, _f32p, C.c_uint64]
+        L.ref_read_features.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
+        L.ref_write_matches_binary.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_void_p]
+
+    def write_features(self, path, image_id, desc, kp):
+        desc = _arr(desc, np.float32)
+        kp = _arr(kp, np.float32)
+        self._check(self.lib.ref_write_features(str(path).encode(), image_id, desc, kp, len(desc)))
+
+    def read_features(self, path):
+        """(image_id, descriptors, keypoints) via the reference reader."""
+        iid, n = C.c_uint64(0), C.c_uint64(0)
+        self._check(self.lib.ref_read_features(str(path).encode(), 0, C.byref(iid), C.byref(n), None, None))
+        desc = np.empty((n.value, 128), np.float32)
+        kp = np.empty((n.value, 4), np.float32)
+        self._check(self.lib.ref_read_features(str(path).encode(), n.value, C.byref(iid), C.byref(n),
+                                               desc.ctypes.data, kp.ctypes.data))
+        return iid.value, desc, kp
+
+    def write_matches_binary(self, path, pairs, stages=None):
+        """pairs: list of (q, t, int32 [m][2]) in any order (the reference sorts)."""
+        ids = np.array([(q, t) for q, t, _ in pairs], np.uint64).reshape(-1)
+        counts = np.array([len(m) for _, _, m in pairs], np.uint64)
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+        log = (np.ascontiguousarray(np.concatenate([np.asarray(m, np.int32).reshape(-1, 2) for _, _, m in pairs]))
+               if pairs else np.zeros((0, 2), np.int32))
+        st = None if stages is None else np.asarray(stages, np.uint8)
+        self._check(self.lib.ref_write_matches_binary(str(path).encode(), len(pairs), ids.ctypes.data,
+                                                      offs.ctypes.data, log.ctypes.data,
+                                                      None if st is None else st.ctypes.data))
+
     def _check(self, rc):
         if rc != 0:
             msg = self.lib.ref_last_error().decode()

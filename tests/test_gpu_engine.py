@@ -166,3 +166,14 @@ def test_rows_run_out_of_order_but_hooks_follow_the_plan(reference, tmp_path):
     for key, m in ref.items():
         assert np.array_equal(got[key], m), key
     assert res.metrics.peak_occupancy == rc["peak_occupancy"] and arena.occupancy() == 0
+
+
+def test_result_match_file_byte_identical_to_reference(reference, tmp_path):
+    # acceptance gate 10 (acceptance.cpp:718-761): matches.bin of the GPU
+    # execute_plan, written natively from the result's pinned log, equals the
+    # reference writer's file for the reference execute_plan's matches
+    plan, ref, rc, res, *_ = run_both(reference, tmp_path, 14, 700, 3, 3, 6, seed=21)
+    ours, theirs = tmp_path / "ours.bin", tmp_path / "theirs.bin"
+    bm.write_matches_binary(ours, res.matches)
+    reference.write_matches_binary(theirs, [(q, t, m) for (q, t), m in ref.items()])
+    assert ours.read_bytes() == theirs.read_bytes()
