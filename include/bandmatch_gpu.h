@@ -266,7 +266,7 @@ int bmg_read_features_header(const char* path, uint64_t* image_id, uint64_t* cou
 int bmg_read_features(const char* path, uint64_t capacity, float* descriptors_out,
                       float* keypoints_out, int threads, uint64_t* image_id, uint64_t* count);
 /* write_matches_binary (hashmatch.cpp:311-332) from flat arrays: pair_ids
- * [2*n_pairs] unique and sorted by IdPair, ranges[2*n_pairs] = [begin, end)
+ * [2*n_pairs] sorted by IdPair, ranges[2*n_pairs] = [begin, end)
  * into log (int32 (qi, ti) pairs), stages[n_pairs] (0 = Initial, 1 =
  * Verified; NULL = all Initial). */
 int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t* pair_ids,

@@ -168,9 +168,9 @@ int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t*
   }
   for (uint64_t p = 1; p < n_pairs; ++p) {
     const bool ordered = pair_ids[2 * p - 2] < pair_ids[2 * p] ||
-                         (pair_ids[2 * p - 2] == pair_ids[2 * p] && pair_ids[2 * p - 1] < pair_ids[2 * p + 1]);
+                         (pair_ids[2 * p - 2] == pair_ids[2 * p] && pair_ids[2 * p - 1] <= pair_ids[2 * p + 1]);
     if (!ordered) {
-      set_last_error("pairs must be unique and sorted by IdPair (sorted_by_pair, hashmatch.cpp:243-250)");
+      set_last_error("pairs must be sorted by IdPair (sorted_by_pair, hashmatch.cpp:243-250)");
       return BMG_INVALID_ARGUMENT;
     }
   }

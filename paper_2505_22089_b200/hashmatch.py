@@ -336,7 +336,7 @@ def _sorted_by_pair(all_pm):
     res = []
     for pm in out:
         m = np.asarray(pm.matches, np.int32).reshape(-1, 2)
-        if len(m):
+        if len(m) > 1 and not (m[1:, 0] > m[:-1, 0]).all():  # matcher output: ascending qi already
             m = m[np.lexsort((m[:, 1], m[:, 0]))]
         res.append(PairMatches(pm.query_image, pm.train_image, m, pm.stage))
     return res
