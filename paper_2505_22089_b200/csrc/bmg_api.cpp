@@ -285,7 +285,7 @@ struct bmg_context {
   bmg_hash_params hp{};
   bmg::HashDev hd{};
   uint64_t seed = 0;
-  bmg::DevBuf planes_t, planes, plane_norm;
+  bmg::DevBuf planes_t, planes, plane_norm, tc_b, tc_fexp;
   // arena (DeviceArena, engine.hpp:20-44)
   uint64_t capacity = 0, occupancy = 0, peak = 0, uploads = 0, evictions = 0, units_uploaded = 0;
   std::map<uint64_t, bmg::ArenaImage> resident;
@@ -888,6 +888,45 @@ HashDev build_hash(Ctx& c, const bmg_hash_params& p, const float* coarse, const 
   h.planes = c.planes.as<float>();
   h.planes_t = c.planes_t.as<float>();
   h.plane_norm = c.plane_norm.as<float>();
+  // tensor-core K2 operand: each plane scaled by its own power of two and
+  // rounded to a 22-bit integer, split into balanced base-256 digits, laid
+  // out K-major with the 128-byte swizzle (kernels.cu project_tc_kernel)
+  h.tc_npad = static_cast<int>(align_up(np, 16));
+  if (h.tc_npad <= 96) {
+    h.tc_pass0 = h.tc_npad;
+  } else if (h.tc_npad <= 192) {
+    h.tc_pass0 = static_cast<int>(align_up((h.tc_npad + 1) / 2, 16));
+  }
+  if (h.tc_npad <= 192) {
+    const int npad = h.tc_npad;
+    std::vector<int8_t> img(static_cast<size_t>(3) * npad * 128, 0);
+    std::vector<int> fexp(npad, 0);
+    for (int q = 0; q < np; ++q) {
+      float mx = 0.f;
+      for (int d = 0; d < kDim; ++d) mx = std::max(mx, std::fabs(planes[static_cast<size_t>(q) * kDim + d]));
+      int f = 0;
+      if (mx > 0.f) std::frexp(mx, &f);
+      fexp[q] = f;
+      for (int d = 0; d < kDim; ++d) {
+        int x = static_cast<int>(std::nearbyint(std::ldexp(static_cast<double>(planes[static_cast<size_t>(q) * kDim + d]), 22 - f)));
+        const int d0 = static_cast<int8_t>(x & 0xff);
+        x = (x - d0) >> 8;
+        const int d1 = static_cast<int8_t>(x & 0xff);
+        const int d2 = (x - d1) >> 8;
+        const size_t off = static_cast<size_t>(q >> 3) * 1024 + static_cast<size_t>(q & 7) * 128 +
+                           static_cast<size_t>(((d >> 4) ^ (q & 7)) * 16 + (d & 15));
+        img[off] = static_cast<int8_t>(d0);
+        img[static_cast<size_t>(npad) * 128 + off] = static_cast<int8_t>(d1);
+        img[static_cast<size_t>(2) * npad * 128 + off] = static_cast<int8_t>(d2);
+      }
+    }
+    c.tc_b.ensure(img.size());
+    c.tc_fexp.ensure(fexp.size() * sizeof(int));
+    BMG_CUDA(cudaMemcpy(c.tc_b.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+    BMG_CUDA(cudaMemcpy(c.tc_fexp.p, fexp.data(), fexp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    h.tc_b = c.tc_b.as<signed char>();
+    h.tc_fexp = c.tc_fexp.as<int>();
+  }
   return h;
 }
 
@@ -1042,7 +1081,7 @@ int bmg_destroy(bmg_context* c) {
       im.ev = nullptr;
     }
     c->resident.clear();
-    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_rp})
+    for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->tc_b, &c->tc_fexp, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_rp})
       b->release();
     for (RowSlot& sl : c->slot) sl.release();
     c->res_ranges.release();

@@ -41,6 +41,11 @@ struct HashDev {
   int n_planes_pad;
   int proj_stride;         // floats per descriptor row of ImgDev::proj (n_planes rounded up to 4)
   int bucket_pad;          // buckets padded to a multiple of this (kBucketPad)
+  // tensor-core K2 (kernels.cu project_tc_kernel), null when n_planes > 192:
+  const signed char* tc_b; // [3 digits][tc_npad planes][128 B], K-major 128-byte-swizzle image
+  const int* tc_fexp;      // [tc_npad] per-plane exponent f (2^(f-1) <= max|p| < 2^f)
+  int tc_npad;             // planes rounded up to 16
+  int tc_pass0;            // planes in the first MMA pass (<= 96); the rest in the second
 };
 
 // An ambiguous projection whose sign the FP32 pass could not certify; the

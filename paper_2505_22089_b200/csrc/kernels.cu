@@ -16,6 +16,7 @@
 // FP64 result has the same sign / ordering; otherwise the FP64 path recomputes
 // it with __dadd_rn/__dmul_rn/__dsub_rn/__dsqrt_rn in the reference order.
 #include <cuda_runtime.h>
+#include <climits>
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
@@ -578,6 +579,261 @@ __global__ void __launch_bounds__(512, 1) project_kernel(HashDev h, ProjJob job,
     __syncthreads();  // the tile is consumed: its buffer takes the next-but-one tile
     if (warp == 0 && t + 2 * (int)gridDim.x < job.n_tiles) issue(t + 2 * gridDim.x, k);
   }
+}
+
+// ---------------------------------------------------------------------------
+// K2 on the 5th-gen tensor cores (default when n_planes <= 192): the same
+// mean-independent projections D[i][p] ~ d_i . p, computed EXACTLY in integer
+// arithmetic on quantised operands, so the certificate keeps a rigorous bound.
+//   * every descriptor row and every plane is scaled by its own power of two
+//     (2^e > max|x|) and rounded to a 22-bit integer X = rint(x 2^(22-e));
+//     X is split into balanced base-256 digits X = X2 2^16 + X1 2^8 + X0,
+//     |Xk| <= 128 (int8);
+//   * tcgen05.mma kind::i8 (s8 x s8 -> s32, M=128 rows x N planes, K=128
+//     channels in 4 steps of 32) accumulates the 9 digit products into 5 TMEM
+//     accumulators by digit weight s = k + l (|acc_s| < 2^21: no overflow);
+//   * the epilogue (tcgen05.ld) forms sum_s acc_s 2^(8s) in int64 (< 2^53,
+//     exact in FP64), scales by 2^(e+f-44) and rounds once to FP32.
+// Error (Cauchy-Schwarz, |x - X 2^(e-22)| <= 2^(e-23) <= 2^-22 max|x|):
+// |D - d.p| <= 2^-22 sqrt(128) (2 + 1e-6) ||d|| ||p|| + 2^-24 |D|
+//           <= 5.5e-6 ||d|| ||p|| < gamma_128 ||d|| ||p||,
+// inside the bound the codes certificate assumes for fl32(d.p) (K2 above).
+// Rows with a non-finite value get NaN (-> FP64 fixup, as the FP32 chain
+// would); ||d|| is computed on the 2^-e scaled row (no underflow), rounded up.
+// Operands live in shared memory in the canonical K-major 128-byte-swizzle
+// layout (8-row x 128 B atoms, 16-byte chunk j of row r stored at chunk
+// j ^ (r & 7)); the planes' digit image is prepared once per context by the
+// host (bmg_api.cpp build_hash) in exactly that layout.
+// ---------------------------------------------------------------------------
+constexpr int kTcThreads = 256;
+constexpr int kTcRows = 128;                 // UMMA M
+constexpr int kTcDigitBytes = kTcRows * 128; // one digit plane of the A tile
+constexpr uint32_t kTcTmemCols = 512;
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  // SM100 shared-memory matrix descriptor: start address >> 4 [0,14),
+  // leading byte offset (unused for swizzled K-major, 1) [16,30), stride
+  // byte offset 1024 >> 4 [32,46), version 1 [46,48), SWIZZLE_128B (2) [61,64)
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ uint32_t umma_idesc_i8(int n) {
+  // kind::i8: D s32 (2) [4,6), A s8 (1) [7,10), B s8 (1) [10,13), both
+  // K-major, N >> 3 [17,23), M >> 4 [24,29)
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+// balanced base-256 digits of |x| <= 2^22
+__device__ __forceinline__ void digits3(int x, int& d0, int& d1, int& d2) {
+  d0 = (int)(int8_t)(x & 0xff);
+  x = (x - d0) >> 8;
+  d1 = (int)(int8_t)(x & 0xff);
+  d2 = (x - d1) >> 8;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, ProjJob job) {
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-aligned operand region (SWIZZLE_128B atoms)
+  const uint32_t raw = cvta_smem(smem_raw);
+  unsigned char* base = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  unsigned char* sA = base;                                  // [3][128 rows][128 B]
+  unsigned char* sB = sA + 3 * kTcDigitBytes;                // [3][npad rows][128 B]
+  const int npad = h.tc_npad;
+  int* sExp = reinterpret_cast<int*>(sB + 3 * npad * 128);   // [128] row exponents (INT_MIN: non-finite)
+  int* sF = sExp + kTcRows;                                  // [npad] plane exponents
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sF + ((npad + 1) & ~1));
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(mbar + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the planes' digit image and exponents, once per CTA
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(h.tc_b);
+    uint4* dst = reinterpret_cast<uint4*>(sB);
+    for (int i = tid; i < 3 * npad * 8; i += kTcThreads) dst[i] = __ldg(src + i);
+    for (int i = tid; i < npad; i += kTcThreads) sF[i] = __ldg(h.tc_fexp + i);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cvta_smem(sTmem)),
+                 "n"(kTcTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *sTmem;
+  uint32_t phase = 0;
+  const int n_pass = h.tc_pass0 < npad ? 2 : 1;
+
+  for (int t = blockIdx.x; t < job.n_tiles; t += gridDim.x) {
+    ImgDev im;
+    uint32_t i0;
+    job_tile(job, t, im, i0);
+    const int nd = min(kTcRows, (int)(im.n - i0));
+    // ---- quantise: two threads per row (64 channels each)
+    {
+      const int r = tid >> 1, half = tid & 1;
+      float4 x[16];
+      float mx = 0.f;
+      bool finite = true;
+      if (r < nd) {
+        const float4* row = reinterpret_cast<const float4*>(im.desc + (size_t)(i0 + r) * kDim) + half * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = __ldg(row + i);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x[i].x), fabsf(x[i].y)), fmaxf(fabsf(x[i].z), fabsf(x[i].w))));
+          finite &= isfinite(x[i].x) & isfinite(x[i].y) & isfinite(x[i].z) & isfinite(x[i].w);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
+      finite = __shfl_xor_sync(kFull, (int)finite, 1) != 0 && finite;
+      int e = 0;
+      if (mx > 0.f && finite) frexpf(mx, &e);  // 2^(e-1) <= max < 2^e
+      const float sc = finite ? ldexpf(1.f, 22 - e) : 0.f;
+      const float sn = finite ? ldexpf(1.f, -e) : 0.f;
+      float ss = 0.f;
+      // 16 channels per 16-byte chunk: chunk j of the row = channels 16j..16j+15
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 v = x[jj * 4 + q];
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          uint32_t b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float ys = vv[u] * sn;
+            ss = fmaf(ys, ys, ss);
+            int d0, d1, d2;
+            digits3(__float2int_rn(vv[u] * sc), d0, d1, d2);
+            b0 |= (uint32_t)(d0 & 0xff) << (8 * u);
+            b1 |= (uint32_t)(d1 & 0xff) << (8 * u);
+            b2 |= (uint32_t)(d2 & 0xff) << (8 * u);
+          }
+          w0[q] = b0;
+          w1[q] = b1;
+          w2[q] = b2;
+        }
+        const int j = half * 4 + jj;
+        const uint32_t off = (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u + (uint32_t)((j ^ (r & 7)) * 16);
+        *reinterpret_cast<uint4*>(sA + off) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(sA + kTcDigitBytes + off) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4*>(sA + 2 * kTcDigitBytes + off) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      }
+      ss += __shfl_xor_sync(kFull, ss, 1);
+      if (half == 0) {
+        sExp[r] = finite ? e : INT_MIN;
+        // ||d||_2 rounded up, from the 2^-e scaled row
+        if (r < nd) im.dnorm[i0 + r] = finite ? ldexpf(sqrtf(ss), e) * 1.00001f : __int_as_float(0x7f800000);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    for (int pass = 0; pass < n_pass; ++pass) {
+      const int p0 = pass ? h.tc_pass0 : 0;
+      const int np = pass ? npad - h.tc_pass0 : min(h.tc_pass0, npad);
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t idesc = umma_idesc_i8(np);
+        const uint32_t a0 = cvta_smem(sA), b0 = cvta_smem(sB) + (uint32_t)(p0 >> 3) * 1024u;
+#pragma unroll
+        for (int sw = 0; sw < 5; ++sw) {           // digit weight s = k + l
+          bool first = true;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int l = sw - k;
+            if (l < 0 || l > 2) continue;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {        // K = 128 channels in steps of 32 bytes
+              const uint64_t da = umma_desc_sw128(a0 + (uint32_t)k * kTcDigitBytes + kk * 32);
+              const uint64_t db = umma_desc_sw128(b0 + (uint32_t)(l * npad * 128) + kk * 32);
+              umma_i8(tmem + (uint32_t)(sw * np), da, db, idesc, first ? 0u : 1u);
+              first = false;
+            }
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         cvta_smem(mbar))
+                     : "memory");
+      }
+      // wait for the accumulators
+      {
+        uint32_t done = 0;
+        while (!done) {
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done)
+              : "r"(cvta_smem(mbar)), "r"(phase)
+              : "memory");
+        }
+        phase ^= 1u;
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // ---- epilogue: warp w reads TMEM lanes 32(w&3).. (= tile rows), half
+      // (w >> 2) of the pass's planes, 8 columns at a time
+      {
+        const int rg = warp & 3, ch = warp >> 2;
+        const int r = rg * 32 + lane;
+        const int ex = sExp[r];
+        const int cols = np / 2, c0 = ch * cols;
+        const uint32_t tl = tmem + ((uint32_t)(rg * 32) << 16);
+        for (int c = c0; c < c0 + cols; c += 8) {
+          int32_t acc[5][8];
+#pragma unroll
+          for (int sw = 0; sw < 5; ++sw) tmem_ld8(tl + (uint32_t)(sw * np + c), acc[sw]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float out[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long long v = (long long)acc[0][u] + ((long long)acc[1][u] << 8) + ((long long)acc[2][u] << 16) +
+                                ((long long)acc[3][u] << 24) + ((long long)acc[4][u] << 32);
+            const int pe = ex + sF[p0 + c + u] - 44;
+            const double sc = __longlong_as_double((long long)(1023 + max(-1022, min(1023, pe))) << 52);
+            out[u] = ex == INT_MIN ? __int_as_float(0x7fc00000) : __double2float_rn((double)v * sc);
+          }
+          if (r < nd) {
+            float* dst = im.proj + (size_t)(i0 + r) * h.proj_stride + p0 + c;
+            const int valid = min(8, h.n_planes - (p0 + c));
+            if (valid == 8) {
+              reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
+              reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (u < valid) dst[u] = out[u];
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+    }
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcTmemCols));
 }
 
 // Per row: mproj[p] = fl32(m . p) as one FP32 FMA chain per plane (the
@@ -1794,8 +2050,31 @@ static int sm_count() {
   return n;
 }
 
+static size_t proj_tc_smem_bytes(const HashDev& h) {
+  return 1024 + 3 * (size_t)kTcDigitBytes + 3 * (size_t)h.tc_npad * 128 + sizeof(int) * (kTcRows + h.tc_npad + 2) +
+         16;
+}
+
+static bool project_simt_forced() {
+  static const bool v = [] {
+    const char* e = getenv("BMG_PROJECT_SIMT");  // A/B switch: the FP32 SIMT K2
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 static void launch_project_job(const HashDev& h, const ProjJob& job, cudaStream_t s) {
   if (job.n_tiles <= 0) return;
+  if (h.tc_b && !project_simt_forced()) {
+    const size_t smem = proj_tc_smem_bytes(h);
+    static int configured = -1;
+    if (configured != (int)smem) {
+      cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = (int)smem;
+    }
+    project_tc_kernel<<<std::min(job.n_tiles, sm_count()), kTcThreads, smem, s>>>(h, job);
+    return;
+  }
   const int pstride = proj_pstride(h);
   dim3 grid(std::min(job.n_tiles, sm_count()), (h.n_planes + kPlaneChunk - 1) / kPlaneChunk);
   project_kernel<<<grid, 512, proj_smem_bytes(pstride), s>>>(h, job, pstride);
