@@ -116,3 +116,37 @@ def test_sift_like_nonnegative_inputs(hf, oracle):
         cs = m.codes(1, 2048)
         oc = oracle.compute_codes(d[2048:], hf.coarse, hf.fine, mean)
         assert np.array_equal(cs.coarse, oc[0]) and np.array_equal(cs.fine, oc[1])
+
+
+def test_extreme_rows_codes_match_oracle(hf, oracle):
+    # the tensor-core projection quantises every row on its own power-of-two
+    # scale: huge, tiny, mixed-magnitude, subnormal, zero and non-finite rows
+    # must still give the reference's bits (non-finite rows take the FP64 path)
+    rng = np.random.default_rng(11)
+    d = unit_rows(rng, 1024)
+    d[0:8] *= np.float32(1e30)
+    d[8:16] *= np.float32(1e-30)
+    d[16:24, :64] *= np.float32(1e12)
+    d[24:32, 1::2] *= np.float32(1e-12)
+    d[32:36] = 0.0
+    d[36:40, :4] = np.float32(1e-44)
+    d[40, 7] = np.nan
+    d[41, 100] = np.inf
+    d[42, 3] = -np.inf
+    d[43:45] = np.float32(3e38) * np.sign(d[43:45])
+    mean = (0.01 * rng.standard_normal(128)).astype(np.float32)
+    cs = bm.compute_codes(bm.FeatureSet(4, d), hf, mean)
+    oc = oracle.compute_codes(d, hf.coarse, hf.fine, mean)
+    assert np.array_equal(cs.coarse, oc[0])
+    assert np.array_equal(cs.fine, oc[1])
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-20, 1e20])
+def test_row_scale_invariance_of_codes(hf, oracle, scale):
+    # signs of d.p - m.p for rows and mean scaled together
+    rng = np.random.default_rng(12)
+    d = (unit_rows(rng, 600) * np.float32(scale)).astype(np.float32)
+    mean = (0.05 * scale * rng.standard_normal(128)).astype(np.float32)
+    cs = bm.compute_codes(bm.FeatureSet(5, d), hf, mean)
+    oc = oracle.compute_codes(d, hf.coarse, hf.fine, mean)
+    assert np.array_equal(cs.coarse, oc[0]) and np.array_equal(cs.fine, oc[1])
