@@ -165,19 +165,48 @@ __global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* _
   const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
   const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
   const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
-  i128 s = 0, lo = 0, hi = 0;
+  // pass 1: the lowest set F96 bit of the thread's 64 values ((e - 54) +
+  // ctz(mantissa with the implicit bit)) and whether all are multiples of
+  // 2^-49 below 2^7: then pass 2 sums them exactly in int64 at scale 2^49
+  // (|partial sum| < 64 * 2^56): one add and two compares per value instead
+  // of the int128 ones.  Pass 2 re-reads the values (L1 hits).
   uint32_t low = kNoLow;
-  bool ok = true;
+  bool fast = true;
 #pragma unroll 16
   for (int r = r0; r < r1; ++r) {
-    const float x = __ldg(d + (size_t)r * kDim);
-    s += to_f96(x, ok);
-    lo = s < lo ? s : lo;
-    hi = s > hi ? s : hi;
-    const uint32_t u = __float_as_uint(x);
-    // lowest set F96 bit: (e - 54) + ctz(mantissa with the implicit bit)
-    const uint32_t lb = (uint32_t)(((u >> 23) & 0xff) - 54 + (__ffs((int)((u & 0x7fffffu) | 0x800000u)) - 1));
-    low = (u & 0x7fffffffu) ? min(low, lb) : low;
+    const uint32_t u = __float_as_uint(__ldg(d + (size_t)r * kDim));
+    const int e = (int)((u >> 23) & 0xff);
+    const uint32_t lb = (uint32_t)(e - 54 + (__ffs((int)((u & 0x7fffffu) | 0x800000u)) - 1));
+    const bool nz = (u & 0x7fffffffu) != 0u;
+    low = nz ? min(low, lb) : low;
+    fast &= !nz || (e >= 1 && e < 127 + 7 && (int)lb >= 96 - 49);
+  }
+  i128 s = 0, lo = 0, hi = 0;
+  bool ok = true;
+  if (fast) {
+    long long s6 = 0, lo6 = 0, hi6 = 0;
+#pragma unroll 16
+    for (int r = r0; r < r1; ++r) {
+      const uint32_t u = __float_as_uint(__ldg(d + (size_t)r * kDim));
+      const int e = (int)((u >> 23) & 0xff);
+      const long long m = (long long)((u & 0x7fffffu) | 0x800000u);
+      const int sh = e - 101;  // x * 2^49 = m * 2^(e - 101), exact by the fast-path test
+      long long v = sh >= 0 ? m << sh : m >> min(-sh, 63);
+      v = (u & 0x7fffffffu) ? ((u >> 31) ? -v : v) : 0;
+      s6 += v;
+      lo6 = min(lo6, s6);
+      hi6 = max(hi6, s6);
+    }
+    s = (i128)s6 * ((i128)1 << 47);  // F96 = (x * 2^49) * 2^47
+    lo = (i128)lo6 * ((i128)1 << 47);
+    hi = (i128)hi6 * ((i128)1 << 47);
+  } else {
+#pragma unroll 16
+    for (int r = r0; r < r1; ++r) {
+      s += to_f96(__ldg(d + (size_t)r * kDim), ok);
+      lo = s < lo ? s : lo;
+      hi = s > hi ? s : hi;
+    }
   }
   if (h == 0) {
     s_sum[c] = s;
