@@ -159,7 +159,8 @@ def ncu_traffic(avg_ctas_per_launch):
     serialised)."""
     try:
         m = json.loads(NCU_SUMMARY.read_text())["match_kernel"]
-        grid = float(str(m["metrics"]["launch__grid_size"]).split()[0].replace(",", ""))
+        g = m["metrics"]["launch__grid_size"]
+        grid = float(str(g[0] if isinstance(g, (list, tuple)) else g).split()[0].replace(",", ""))
         return m["dram_bytes_per_launch"] / grid * avg_ctas_per_launch
     except Exception:
         return None
