@@ -5,7 +5,7 @@ tag=${1:-prof}
 out=gpurun_out/$tag
 mkdir -p $out
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
-for k in match_kernel project_kernel codes_kernel mean_sums_kernel mean_resolve_kernel tables_scatter_kernel codes_fixup_kernel; do
+for k in match_kernel project_tc_kernel codes_kernel mean_sums_kernel mean_resolve_kernel tables_scatter_kernel codes_fixup_kernel; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 \
       -o $out/prof_$k $B > $out/ncu_$k.log 2>&1
 done
