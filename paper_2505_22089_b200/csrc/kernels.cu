@@ -1000,17 +1000,38 @@ __device__ __forceinline__ void set_code_bit(const HashDev& h, const ImgDev& im,
   }
 }
 
-__global__ void codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
+constexpr int kFixupThreads = 256;
+__global__ void __launch_bounds__(kFixupThreads) codes_fixup_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                    const float* __restrict__ mean, const Fixup* __restrict__ fix,
                                    const uint32_t* __restrict__ fix_count, uint32_t fix_cap,
                                    unsigned long long* fixed_bits) {
+  // one warp per ambiguous bit: lane l loads channels 4l..4l+3 of the
+  // descriptor, mean and plane (coalesced rows) and forms the products
+  // fl(fl(d - m) * p) in FP64 exactly as the reference does per channel; the
+  // reference's sequential sum over c = 0..127 (hashmatch.cpp:27-33) is then
+  // replayed in order by lane 0 from shared memory
+  __shared__ double s_t[kFixupThreads / 32][kDim];
   const uint32_t n = min(*fix_count, fix_cap);
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const float4 mv = __ldg(reinterpret_cast<const float4*>(mean) + lane);
+  for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += (gridDim.x * blockDim.x) >> 5) {
     const Fixup f = fix[e];
     const ImgDev im = imgs[f.img];
-    const double s = centered_dot_ref(im.desc + (size_t)f.desc * kDim, mean,
-                                      h.planes + (size_t)f.plane * kDim);
-    if (s > 0.0) set_code_bit(h, im, f.desc, f.plane);
+    const float4 dv = __ldg(reinterpret_cast<const float4*>(im.desc + (size_t)f.desc * kDim) + lane);
+    const float4 pv = __ldg(reinterpret_cast<const float4*>(h.planes + (size_t)f.plane * kDim) + lane);
+    const float dd[4] = {dv.x, dv.y, dv.z, dv.w}, mm[4] = {mv.x, mv.y, mv.z, mv.w},
+                pp[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      s_t[wib][4 * lane + j] = __dmul_rn(__dsub_rn((double)dd[j], (double)mm[j]), (double)pp[j]);
+    __syncwarp();
+    if (lane == 0) {
+      double acc = 0.0;
+#pragma unroll 16
+      for (int c = 0; c < kDim; ++c) acc = __dadd_rn(acc, s_t[wib][c]);
+      if (acc > 0.0) set_code_bit(h, im, f.desc, f.plane);
+    }
+    __syncwarp();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && fixed_bits) atomicAdd(fixed_bits, (unsigned long long)n);
 }
@@ -2143,7 +2164,7 @@ void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile
 void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, const float* mean,
                         const Fixup* fix, const uint32_t* fix_count, uint32_t fix_cap,
                         unsigned long long* fixed_bits, cudaStream_t s) {
-  codes_fixup_kernel<<<148, 256, 0, s>>>(h, imgs_dev, mean, fix, fix_count, fix_cap, fixed_bits);
+  codes_fixup_kernel<<<4 * 148, kFixupThreads, 0, s>>>(h, imgs_dev, mean, fix, fix_count, fix_cap, fixed_bits);
   codes_overflow_kernel<<<148, 256, 0, s>>>(h, imgs_dev, n_imgs, mean, fix_count + 1);
 }
 
