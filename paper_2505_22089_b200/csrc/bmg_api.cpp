@@ -599,8 +599,7 @@ void enqueue_codes_tables(Ctx& c, const float* d_mean) {
   }
   {
     Timed t(c, "tables", s);
-    launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), rs.n_imgs, s);
-    c.launches += 3;
+    c.launches += launch_tables(h, d_imgs, d_tile_img, d_tile_start, static_cast<int>(rs.n_tiles), rs.n_imgs, s);
     check_launch();
   }
 }
@@ -1341,11 +1340,11 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
       meta_add(*c, c->S().d_diag.p, nullptr, sizeof(unsigned long long) * 4);
       meta_flush(*c);
       join_uploads(*c);
-      // the scan kernel for slot 1 only: run tables on a 2-image table but
-      // the hist/scatter tiles reference image 1 only
-      launch_tables(h, c->S().d_imgs.as<ImgDev>(), c->S().d_tiles.as<uint32_t>(), c->S().d_tiles.as<uint32_t>() + n_tiles,
-                    static_cast<int>(n_tiles), 2, c->S().s_comp);
-      c->launches += 3;
+      // a 2-image table: the tile list covers image 1 only (the global-atomic
+      // path); the fused shared-memory path builds both images' tables
+      c->launches += launch_tables(h, c->S().d_imgs.as<ImgDev>(), c->S().d_tiles.as<uint32_t>(),
+                                   c->S().d_tiles.as<uint32_t>() + n_tiles, static_cast<int>(n_tiles), 2,
+                                   c->S().s_comp);
       check_launch();
     }
     std::vector<std::pair<int, int>> sp{{0, 1}};

@@ -1137,6 +1137,57 @@ __global__ void __launch_bounds__(1024) tables_scan_kernel(HashDev h, const ImgD
   }
 }
 
+// One CTA per (image, table), counting sort in shared memory: histogram with
+// shared atomics, the padded bucket scan (same layout as tables_scan_kernel:
+// buckets padded to kBucketPad with pad entries, the sentinel chunk at the
+// end), then the scatter with shared cursors.  Used for 2^m <= 4096 buckets;
+// the three global-atomic kernels above remain for larger m.
+constexpr int kTablesFusedMaxBuckets = 4096;
+__global__ void __launch_bounds__(1024) tables_fused_kernel(HashDev h, const ImgDev* __restrict__ imgs) {
+  extern __shared__ uint32_t s_cnt[];  // [n_buckets]: counts, then cursors
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry;
+  const ImgDev im = imgs[blockIdx.x];
+  const int t = blockIdx.y, L = h.tables, nb = h.n_buckets;
+  uint32_t* off = im.offsets + (size_t)t * (nb + 1);
+  uint32_t* slots = im.slots + (size_t)t * im.ns;
+  uint64_t* bfine = im.bfine + (size_t)t * im.ns * h.fwp;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cnt[b] = 0u;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < im.n; i += blockDim.x) atomicAdd(s_cnt + im.coarse[(size_t)i * L + t], 1u);
+  __syncthreads();
+  uint32_t carry = 0;
+  if (threadIdx.x == 0) off[0] = 0u;
+  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const int b = b0 + threadIdx.x;
+    const uint32_t v = b < nb ? s_cnt[b] : 0u;
+    const uint32_t pv = (v + (uint32_t)h.bucket_pad - 1u) / (uint32_t)h.bucket_pad * (uint32_t)h.bucket_pad;
+    const uint32_t incl = block_incl_scan(pv, s_warp) + carry;
+    if (b < nb) {
+      off[b + 1] = incl;
+      s_cnt[b] = incl - pv;  // cursor
+      for (uint32_t k = incl - pv + v; k < incl; ++k) {
+        slots[k] = kEmpty;
+        for (int x = 0; x < h.fwp; ++x) bfine[(size_t)k * h.fwp + x] = 0ull;
+      }
+    }
+    if (threadIdx.x == blockDim.x - 1) s_carry = incl;
+    __syncthreads();
+    carry = s_carry;
+    __syncthreads();
+  }
+  if (threadIdx.x < kSentinel) {
+    const uint32_t k = im.ns - kSentinel + threadIdx.x;
+    slots[k] = kEmpty;
+    for (int x = 0; x < h.fwp; ++x) bfine[(size_t)k * h.fwp + x] = 0ull;
+  }
+  for (uint32_t i = threadIdx.x; i < im.n; i += blockDim.x) {
+    const uint32_t pos = atomicAdd(s_cnt + im.coarse[(size_t)i * L + t], 1u);
+    slots[pos] = i;
+    for (int x = 0; x < h.fwp; ++x) bfine[(size_t)pos * h.fwp + x] = im.fine[(size_t)i * h.fwp + x];
+  }
+}
+
 __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs,
                                       const uint32_t* __restrict__ tile_img,
                                       const uint32_t* __restrict__ tile_start) {
@@ -2168,11 +2219,16 @@ void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, co
   codes_overflow_kernel<<<148, 256, 0, s>>>(h, imgs_dev, n_imgs, mean, fix_count + 1);
 }
 
-void launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
-                   const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s) {
+int launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
+                  const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s) {
+  if (h.n_buckets <= kTablesFusedMaxBuckets) {
+    tables_fused_kernel<<<dim3(n_imgs, h.tables), 1024, sizeof(uint32_t) * h.n_buckets, s>>>(h, imgs_dev);
+    return 1;
+  }
   tables_hist_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
   tables_scan_kernel<<<dim3(n_imgs, h.tables), 1024, 0, s>>>(h, imgs_dev);
   tables_scatter_kernel<<<n_tiles, kCodesTile, 0, s>>>(h, imgs_dev, tile_img, tile_start);
+  return 3;
 }
 
 template <int FWP, int KM, int NT, int KC>
