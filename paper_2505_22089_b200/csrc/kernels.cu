@@ -976,6 +976,134 @@ __global__ void __launch_bounds__(kCodesThreads)
   }
 }
 
+// codes_kernel with the tile's projections streamed into shared memory by
+// one bulk copy per tile (the tile's rows of ImgDev::proj are contiguous),
+// double-buffered, persistent over the row's tiles; one warp per descriptor,
+// lane j certifies planes j, j+32, .. and the plane word is a warp ballot.
+// Same arithmetic, bits and fixup list as codes_kernel (used when two tile
+// buffers fit: proj_stride <= 192).
+constexpr int kCodesTmaThreads = 1024;
+__global__ void __launch_bounds__(kCodesTmaThreads, 1)
+    codes_tma_kernel(HashDev h, const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
+                     const uint32_t* __restrict__ tile_start, int n_tiles, const float* __restrict__ mproj,
+                     Fixup* __restrict__ fix, uint32_t* __restrict__ fix_count, uint32_t fix_cap,
+                     uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(128) unsigned char smem_c[];
+  const int n_pw = (h.n_planes + 31) / 32, mw = n_pw + 2;
+  const int ps = h.proj_stride;
+  float* sD = reinterpret_cast<float*>(smem_c);                         // [2][128][ps]
+  uint32_t* sMask = reinterpret_cast<uint32_t*>(sD + 2 * kCodesTile * ps);  // [128][mw]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMask + ((kCodesTile * mw + 1) & ~1));  // [2], 8-byte aligned
+  float* sN = reinterpret_cast<float*>(bars + 2);                       // [2][128] tile norms
+  float* sMp = sN + 2 * kCodesTile;                                     // [n_planes + 1]
+  float* sPn = sMp + h.n_planes + 1;                                    // [n_planes]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kCodesTmaThreads / 32;
+
+  auto issue = [&](int t, int k) {  // thread 0: tile t's projections -> buffer k
+    const ImgDev im = imgs[tile_img[t]];
+    const uint32_t i0 = tile_start[t];
+    const uint32_t nd = min((uint32_t)kCodesTile, im.n - i0);
+    const uint32_t bytes = nd * (uint32_t)ps * 4u;
+    const uint32_t nbytes = (nd * 4u + 15u) & ~15u;  // the norms (ImgDev::dnorm is 16-byte aligned per tile)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cvta_smem(bars + k)),
+                 "r"(bytes + nbytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            cvta_smem(sD + (size_t)k * kCodesTile * ps)),
+        "l"(im.proj + (size_t)i0 * ps), "r"(bytes), "r"(cvta_smem(bars + k))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            cvta_smem(sN + k * kCodesTile)),
+        "l"(im.dnorm + i0), "r"(nbytes), "r"(cvta_smem(bars + k))
+        : "memory");
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(bars + 0)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(bars + 1)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int p = tid; p <= h.n_planes; p += blockDim.x) sMp[p] = __ldg(mproj + p);
+  for (int p = tid; p < h.n_planes; p += blockDim.x) sPn[p] = __ldg(h.plane_norm + p);
+  __syncthreads();
+  if (tid == 0) {
+    if ((int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < n_tiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  const float mn = sMp[h.n_planes];
+  const int L = h.tables, m = h.coarse_bits, fb = h.fine_bits, coarse_planes = L * m;
+  const int n_words = L + h.fwp;
+  uint32_t ph[2] = {0u, 0u};
+  int k = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, k ^= 1) {
+    const uint32_t img = tile_img[t];
+    const ImgDev im = imgs[img];
+    const uint32_t i0 = tile_start[t];
+    const int nd = min(kCodesTile, (int)(im.n - i0));
+    {
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(cvta_smem(bars + k)), "r"(ph[k])
+            : "memory");
+      }
+      ph[k] ^= 1u;
+    }
+    const float* D = sD + (size_t)k * kCodesTile * ps;
+    for (int i = warp; i < nd; i += kWarps) {
+      const float bn = kDotBound * (sN[k * kCodesTile + i] + mn);
+      for (int w = 0; w < n_pw; ++w) {
+        const int p = 32 * w + lane;
+        bool bit = false;
+        if (p < h.n_planes) {
+          const float sv = D[i * ps + p] - sMp[p];
+          const float B = fmaf(bn, sPn[p], kDotBoundAbs);
+          bit = sv > B;
+          if (!bit && !(sv < -B)) {
+            const uint32_t slot = atomicAdd(fix_count, 1u);
+            if (slot < fix_cap) {
+              Fixup f;
+              f.img = img;
+              f.desc = i0 + i;
+              f.plane = p;
+              f.pad = 0;
+              fix[slot] = f;
+            } else {
+              atomicOr(overflow + img, 1u);
+            }
+          }
+        }
+        const uint32_t word = __ballot_sync(kFull, bit);
+        if (lane == 0) sMask[i * mw + w] = word;
+      }
+      if (lane < 2) sMask[i * mw + n_pw + lane] = 0u;  // guards
+    }
+    __syncthreads();  // masks complete; the D buffer is consumed
+    if (tid == 0 && t + 2 * (int)gridDim.x < n_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t + 2 * gridDim.x, k);
+    }
+    for (int e = tid; e < nd * n_words; e += blockDim.x) {
+      const int i = e / n_words, wd = e % n_words;
+      const uint32_t* mk = sMask + i * mw;
+      const size_t gi = i0 + i;
+      if (wd < L) {
+        im.coarse[gi * L + wd] = (uint32_t)extract_bits(mk, wd * m, m);
+      } else {
+        const int fwi = wd - L;
+        const int b0 = coarse_planes + 64 * fwi;
+        const int len = min(64, coarse_planes + fb - b0);
+        im.fine[gi * h.fwp + fwi] = len > 0 ? extract_bits(mk, b0, len) : 0ull;
+      }
+    }
+    __syncthreads();  // sMask reused by the next tile
+  }
+}
+
 __device__ __forceinline__ double centered_dot_ref(const float* __restrict__ d,
                                                    const float* __restrict__ mean,
                                                    const float* __restrict__ p) {
@@ -2208,6 +2336,18 @@ void launch_codes(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile
   uint32_t* overflow = fix_count + 1;
   if (n_tiles <= 0) return;
   mproj_kernel<<<(h.n_planes + 255) / 256, 256, 0, s>>>(h, mean, mproj);
+  if (h.proj_stride <= 192) {
+    const size_t tsmem = sizeof(float) * 2 * kCodesTile * h.proj_stride + sizeof(uint32_t) * (kCodesTile * mw + 2) +
+                         16 + sizeof(float) * (2 * kCodesTile + 2 * h.n_planes + 4) + 32;
+    static size_t configured = 0;
+    if (configured != tsmem) {
+      cudaFuncSetAttribute(codes_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+      configured = tsmem;
+    }
+    codes_tma_kernel<<<std::min(n_tiles, sm_count()), kCodesTmaThreads, tsmem, s>>>(
+        h, imgs_dev, tile_img, tile_start, n_tiles, mproj, fix, fix_count, fix_cap, overflow);
+    return;
+  }
   codes_kernel<<<n_tiles, kCodesThreads, smem, s>>>(h, imgs_dev, tile_img, tile_start, mproj, fix, fix_count,
                                                     fix_cap, overflow);
 }

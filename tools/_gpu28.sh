@@ -1,6 +1,6 @@
 #!/bin/bash
-out=gpurun_out/r1ao; mkdir -p $out
-timeout 900 python -m pytest tests/test_gpu_codes.py tests/test_gpu_engine.py tests/test_gpu_match.py -x -q > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
+out=gpurun_out/r1aq; mkdir -p $out
+timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
 tail -2 $out/pytest.log
 for c in block32; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $out/bench_$c.json 2> $out/bench_$c.err
 python - $out/bench_$c.json <<'PY'
