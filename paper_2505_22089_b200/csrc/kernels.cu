@@ -682,58 +682,87 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
   unsigned char* sA = base;                                  // [3][128 rows][128 B]
   unsigned char* sB = sA + 3 * kTcDigitBytes;                // [3][npad rows][128 B]
   const int npad = h.tc_npad;
-  int* sExp = reinterpret_cast<int*>(sB + 3 * npad * 128);   // [128] row exponents (INT_MIN: non-finite)
-  int* sF = sExp + kTcRows;                                  // [npad] plane exponents
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sF + ((npad + 1) & ~1));
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(mbar + 1);
+  float* sRaw = reinterpret_cast<float*>(sB + 3 * npad * 128);  // [128][128] the next tile's rows (bulk copy)
+  int* sExp = reinterpret_cast<int*>(sRaw + kTcRows * kDim);    // [128] row exponents (INT_MIN: non-finite)
+  int* sF = sExp + kTcRows;                                     // [npad] plane exponents
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sF + ((npad + 1) & ~1));  // [3]: MMA done, raw tile, planes
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(mbar + 3);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // the planes' digit image and exponents, once per CTA
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(h.tc_b);
-    uint4* dst = reinterpret_cast<uint4*>(sB);
-    for (int i = tid; i < 3 * npad * 8; i += kTcThreads) dst[i] = __ldg(src + i);
-    for (int i = tid; i < npad; i += kTcThreads) sF[i] = __ldg(h.tc_fexp + i);
+  // thread 0: tile t's rows (contiguous, nd x 512 B) -> sRaw
+  auto issue_raw = [&](int t) {
+    ImgDev im;
+    uint32_t i0;
+    job_tile(job, t, im, i0);
+    const uint32_t bytes = (uint32_t)min(kTcRows, (int)(im.n - i0)) * 512u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cvta_smem(mbar + 1)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            cvta_smem(sRaw)),
+        "l"(im.desc + (size_t)i0 * kDim), "r"(bytes), "r"(cvta_smem(mbar + 1))
+        : "memory");
+  };
+  auto wait_bar = [&](uint64_t* bar, uint32_t par) {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(cvta_smem(bar)), "r"(par)
+          : "memory");
+    }
+  };
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(mbar + q)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the planes' digit image (prepared once per context) and the first tile
+    const uint32_t bbytes = (uint32_t)(3 * npad * 128);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cvta_smem(mbar + 2)), "r"(bbytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            cvta_smem(sB)),
+        "l"(h.tc_b), "r"(bbytes), "r"(cvta_smem(mbar + 2))
+        : "memory");
+    if ((int)blockIdx.x < job.n_tiles) issue_raw(blockIdx.x);
   }
+  for (int i = tid; i < npad; i += kTcThreads) sF[i] = __ldg(h.tc_fexp + i);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(cvta_smem(sTmem)),
                  "n"(kTcTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cvta_smem(mbar)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *sTmem;
-  uint32_t phase = 0;
+  uint32_t phase = 0, raw_phase = 0;
   const int n_pass = h.tc_pass0 < npad ? 2 : 1;
+  if (tid == 0) wait_bar(mbar + 2, 0);  // the MMA issuer needs the planes
 
   for (int t = blockIdx.x; t < job.n_tiles; t += gridDim.x) {
     ImgDev im;
     uint32_t i0;
     job_tile(job, t, im, i0);
     const int nd = min(kTcRows, (int)(im.n - i0));
-    // ---- quantise: two threads per row (64 channels each)
+    wait_bar(mbar + 1, raw_phase);
+    raw_phase ^= 1u;
+    // ---- quantise from the staged rows: two threads per row (64 channels
+    // each); float4 j of a half is read in a per-row rotation (conflict-free)
     {
       const int r = tid >> 1, half = tid & 1;
-      float4 x[16];
+      const int rot = (r + 8 * half) & 15;
+      const float4* row = reinterpret_cast<const float4*>(sRaw + r * kDim) + half * 16;
       float mx = 0.f;
       bool finite = true;
       if (r < nd) {
-        const float4* row = reinterpret_cast<const float4*>(im.desc + (size_t)(i0 + r) * kDim) + half * 16;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = __ldg(row + i);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x[i].x), fabsf(x[i].y)), fmaxf(fabsf(x[i].z), fabsf(x[i].w))));
-          finite &= isfinite(x[i].x) & isfinite(x[i].y) & isfinite(x[i].z) & isfinite(x[i].w);
+        for (int j = 0; j < 16; ++j) {
+          const float4 v = row[(j + rot) & 15];
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          finite &= isfinite(v.x) & isfinite(v.y) & isfinite(v.z) & isfinite(v.w);
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
       finite = __shfl_xor_sync(kFull, (int)finite, 1) != 0 && finite;
@@ -742,34 +771,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
       const float sc = finite ? ldexpf(1.f, 22 - e) : 0.f;
       const float sn = finite ? ldexpf(1.f, -e) : 0.f;
       float ss = 0.f;
-      // 16 channels per 16-byte chunk: chunk j of the row = channels 16j..16j+15
+      const uint32_t rbase = (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        uint32_t w0[4], w1[4], w2[4];
+      for (int j = 0; j < 16; ++j) {
+        const int f4 = (j + rot) & 15;  // float4 index within the half: channels 64 half + 4 f4 ..
+        const float4 v = r < nd ? row[f4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        uint32_t b0 = 0, b1 = 0, b2 = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 v = x[jj * 4 + q];
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-          uint32_t b0 = 0, b1 = 0, b2 = 0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float ys = vv[u] * sn;
-            ss = fmaf(ys, ys, ss);
-            int d0, d1, d2;
-            digits3(__float2int_rn(vv[u] * sc), d0, d1, d2);
-            b0 |= (uint32_t)(d0 & 0xff) << (8 * u);
-            b1 |= (uint32_t)(d1 & 0xff) << (8 * u);
-            b2 |= (uint32_t)(d2 & 0xff) << (8 * u);
-          }
-          w0[q] = b0;
-          w1[q] = b1;
-          w2[q] = b2;
+        for (int u = 0; u < 4; ++u) {
+          const float ys = vv[u] * sn;
+          ss = fmaf(ys, ys, ss);
+          int d0, d1, d2;
+          digits3(__float2int_rn(vv[u] * sc), d0, d1, d2);
+          b0 |= (uint32_t)(d0 & 0xff) << (8 * u);
+          b1 |= (uint32_t)(d1 & 0xff) << (8 * u);
+          b2 |= (uint32_t)(d2 & 0xff) << (8 * u);
         }
-        const int j = half * 4 + jj;
-        const uint32_t off = (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u + (uint32_t)((j ^ (r & 7)) * 16);
-        *reinterpret_cast<uint4*>(sA + off) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-        *reinterpret_cast<uint4*>(sA + kTcDigitBytes + off) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-        *reinterpret_cast<uint4*>(sA + 2 * kTcDigitBytes + off) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+        // channel c = 64 half + 4 f4: 16-byte chunk c / 16, byte c % 16
+        const int chunk = half * 4 + (f4 >> 2);
+        const uint32_t off = rbase + (uint32_t)((chunk ^ (r & 7)) * 16 + (f4 & 3) * 4);
+        *reinterpret_cast<uint32_t*>(sA + off) = b0;
+        *reinterpret_cast<uint32_t*>(sA + kTcDigitBytes + off) = b1;
+        *reinterpret_cast<uint32_t*>(sA + 2 * kTcDigitBytes + off) = b2;
       }
       ss += __shfl_xor_sync(kFull, ss, 1);
       if (half == 0) {
@@ -780,6 +804,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    // the staged rows are consumed: stream the next tile in under this one's
+    // MMAs and epilogue
+    if (tid == 0 && t + (int)gridDim.x < job.n_tiles) issue_raw(t + gridDim.x);
 
     for (int pass = 0; pass < n_pass; ++pass) {
       const int p0 = pass ? h.tc_pass0 : 0;
@@ -2280,8 +2307,8 @@ static int sm_count() {
 }
 
 static size_t proj_tc_smem_bytes(const HashDev& h) {
-  return 1024 + 3 * (size_t)kTcDigitBytes + 3 * (size_t)h.tc_npad * 128 + sizeof(int) * (kTcRows + h.tc_npad + 2) +
-         16;
+  return 1024 + 3 * (size_t)kTcDigitBytes + 3 * (size_t)h.tc_npad * 128 + sizeof(float) * kTcRows * kDim +
+         sizeof(int) * (kTcRows + h.tc_npad + 2) + 3 * sizeof(uint64_t) + 16;
 }
 
 static bool project_simt_forced() {
