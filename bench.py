@@ -44,9 +44,11 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
 FALLBACK_HBM = 6650.0
 
-CONFIG_NO = {"block32": 2, "strip500": 3, "shard16k": 4}
+CONFIG_NO = {"pair1": 1, "block32": 2, "strip500": 3, "shard16k": 4}
 CONFIGS = {
     # name: (generator n_images, ppi, band, dropped leading images, plan file)
+    # BASELINE config 1: images (band, band+1) of an 11-band 8,192 scene
+    "pair1": (13, 8192, 11, 11, "plan_pair1.json"),
     "block32": (43, 8192, 11, 11, "plan_block32.json"),
     "strip500": (510, 8192, 10, 10, "plan_strip500.json"),
     # BASELINE config 4 is 5,000 x 16,384 sharded over 2/4/8 GPUs: one

@@ -773,7 +773,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   const int n_pairs = static_cast<int>(slot_pairs.size());
   if (n_pairs == 0) return;
   const HashDev& h = c.hd;
-  const int chunk = match_queries_per_cta(h.fwp, mp.k_nearest);
+  int chunk = match_queries_per_cta(h.fwp, mp.k_nearest);
   if (h.tables > 32) fail(BMG_UNSUPPORTED, "more than 32 hash tables is not supported by the GPU matcher");
   const int idx_bits = 32 - bit_width(static_cast<uint32_t>(h.fine_bits));
   std::vector<int> order(n_pairs);
@@ -782,13 +782,22 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   // descriptors during the re-rank gathers)
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return slot_pairs[x].second < slot_pairs[y].second; });
-  size_t n_work = 0;
+  uint64_t total_q = 0;
   for (int p = 0; p < n_pairs; ++p) {
-    const ImgDev& q = c.S().row_imgs[slot_pairs[p].first];
     const ImgDev& t = c.S().row_imgs[slot_pairs[p].second];
     if (t.n > (1u << idx_bits) - 1u) fail(BMG_UNSUPPORTED, "train image too large for the key packing");
-    n_work += (q.n + chunk - 1) / chunk;
+    total_q += c.S().row_imgs[slot_pairs[p].first].n;
   }
+  // few pairs (e.g. a single pair): smaller query ranges so the grid still
+  // covers every SM twice (down to one query per warp)
+  if (!match_tma_enabled()) {
+    const uint64_t want = 2ull * static_cast<uint64_t>(device_sm_count());
+    if ((total_q + chunk - 1) / chunk < want)
+      chunk = static_cast<int>(std::max<uint64_t>(32, (total_q + want - 1) / want + 31) / 32 * 32);
+    chunk = std::min(chunk, match_queries_per_cta(h.fwp, mp.k_nearest));
+  }
+  size_t n_work = 0;
+  for (int p = 0; p < n_pairs; ++p) n_work += (c.S().row_imgs[slot_pairs[p].first].n + chunk - 1) / chunk;
   PairWork* h_work = c.ring.alloc<PairWork>(std::max<size_t>(n_work, 1), c.S().s_comp, c.s_copy);
   uint64_t* h_dense_off = c.ring.alloc<uint64_t>(n_pairs, c.S().s_comp, c.s_copy);
   uint32_t* h_nq = c.ring.alloc<uint32_t>(n_pairs, c.S().s_comp, c.s_copy);

@@ -152,5 +152,6 @@ constexpr int kMatchQueries = BMG_MATCH_QUERIES;  // queries per match CTA
 constexpr int kTmaQueries = 1024;    // queries per TMA-staged match CTA (16 warps)
 // queries per CTA of the match kernel launch_match picks for (fwp, k)
 int match_queries_per_cta(int fwp, int k);
+int device_sm_count();
 
 }  // namespace bmg

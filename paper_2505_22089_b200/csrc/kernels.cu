@@ -2454,6 +2454,8 @@ static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
   }
 }
 
+int device_sm_count() { return sm_count(); }
+
 int match_queries_per_cta(int fwp, int k) {
   return (match_tma_enabled() && fwp <= 4 && k <= 8) ? kTmaQueries : kMatchQueries;
 }

@@ -4,6 +4,8 @@ oracle/_ref build).  The scheduler is out of scope for the GPU path (SURVEY
 §2.1): its SchedulePlan is an *input*, so the plans are committed here as
 fixtures under bench_data/.
 
+  pair1     BASELINE config 1: the single pair (band, band+1) of an
+            11-band scene, one 2-image row
   block32   BASELINE config 2: 32 images, band 11 (286 pairs),
             iterate_schedule(size_blk=16, size_gpu=32)
   strip500  BASELINE config 3: 500 images, band 10 (4945 pairs), CLI-default
@@ -33,7 +35,7 @@ def band_pairs(n, band):
 def main():
     OUT.mkdir(exist_ok=True)
     r = Reference()
-    for name, n, band, blk, gpu in [("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400),
+    for name, n, band, blk, gpu in [("pair1", 2, 1, 1, 2), ("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400),
                                     ("shard16k", 640, 15, 200, 400)]:
         r.iterate_schedule(np.arange(n), band_pairs(n, band), blk, gpu, OUT / f"plan_{name}.json")
         print(name, (OUT / f"plan_{name}.json").stat().st_size)
