@@ -1,29 +1,41 @@
 #!/usr/bin/env python3
 """Benchmark: image match-pairs/sec at 8192 SIFT/img (BASELINE.json metric).
 
-Workload (BASELINE config 2, "one MBR block"): 32 images x 8190 synthetic
-SIFT-like descriptors (the reference generator, features.cpp:68-197, band 11;
-the first 11 images of a 43-image scene are dropped so every image carries the
-full 8190 descriptors), all 286 band pairs, scheduled by the reference's
-iterate_schedule(16, 32) (bench_data/plan_block32.json: 2 block rows).  One
+Default workload (BASELINE config 3, "synthetic UAV strip", the largest
+single-GPU 8,192-descriptor configuration): 500 images x 8,190 synthetic
+SIFT-like descriptors from the reference generator (features.cpp:68-197, band
+10: 20 neighbours per image; the 10 short leading images of a 510-image scene
+are dropped), all 4,945 band pairs, scheduled by the reference's
+iterate_schedule(200, 400) (bench_data/plan_strip500.json: 3 block rows).  One
 step = the whole execute_plan row loop (uploads, row means, codes, bucket
 tables, cascade matching, result read-back) with verification off, exactly
 the reference's `bandmatch match` path (bandmatch_cli.cpp:217-246).
+`--config block32` is BASELINE config 2 (one 32-image MBR block, 286 pairs;
+verification off, like the reference arm), `pair1` config 1, `shard16k` one
+GPU's shard of config 4.
 
   value  device time of the row loop on HBM-resident images (CUDA events on
-         the compute stream), L2 flushed before every step
+         the compute streams), L2 flushed before every step
   e2e    wall time of the public execute_plan call from pinned host buffers:
          H2D of every image + rows + D2H of the matches, every step
+         (e2e_pageable: the same from pageable buffers, like the reference's
+         std::vector FeatureSet)
+  parity the GPU match lists of the e2e run against the compiled reference
+         (oracle/_ref) run on the same inputs in the cpu_baseline leg
 
-Multi-GPU (torchrun): every rank runs its own block (seed 7 + rank) -- blocks
-are independent units with no exchange step, so scaling is weak; times are
-max over ranks.  `--impl reference` times the reference's CPU implementation
-(oracle/_ref, the unmodified reference compiled in place) on rank 0 with every
-host core.
+Multi-GPU (torchrun, --gpus N): ONE plan, sharded (paper_2505_22089_b200.
+multigpu): rows -- split by pairs where a row is larger than a rank's share --
+are partitioned over the ranks with no collective on the data path; each rank
+generates only the images its shard needs; matches are gathered to rank 0
+through shared memory inside the timed region; times are max over ranks
+(strong scaling).  `--impl reference` times the reference's CPU
+implementation (oracle/_ref, the unmodified reference compiled in place) on
+rank 0 with every host core, without loading this package.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -43,6 +55,7 @@ UNIT = "pairs/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
 FALLBACK_HBM = 6650.0
+HASH_ROOT_SEED = 42  # make_hash_functions(seed_for(42, "matching")), bandmatch_cli.cpp:225-226
 
 CONFIG_NO = {"pair1": 1, "block32": 2, "strip500": 3, "shard16k": 4}
 CONFIGS = {
@@ -52,10 +65,10 @@ CONFIGS = {
     "block32": (43, 8192, 11, 11, "plan_block32.json"),
     "strip500": (510, 8192, 10, 10, "plan_strip500.json"),
     # BASELINE config 4 is 5,000 x 16,384 sharded over 2/4/8 GPUs: one
-    # GPU's shard (640 images, band 15 = 30 neighbours); each rank its own
+    # GPU's shard (640 images, band 15 = 30 neighbours)
     "shard16k": (655, 16384, 15, 15, "plan_shard16k.json"),
 }
-# configs whose full reference run is minutes long: the CPU baseline is a
+# configs whose full reference run is minutes long: the CPU figure is a
 # timed sample (compute_codes of 32 images + match_pair of 128 pairs on all
 # host threads) extrapolated to the plan's rows
 SAMPLED = {"shard16k"}
@@ -67,29 +80,65 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=list(CONFIGS), default="block32")
+    p.add_argument("--config", choices=list(CONFIGS), default="strip500")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
 
-def build_workload(config: str, seed: int, pinned_alloc=None):
-    """Scene + plan.  Returns ({id: FeatureSet}, plan, descriptors per image)."""
-    import paper_2505_22089_b200 as bm
-    from paper_2505_22089_b200.features import SyntheticScene, generate_synthetic
+def plan_rows(plan_path):
+    """[(pairs, needed image count)] per row in plan order, straight from the
+    plan JSON (mbr.cpp:378-419 layout)."""
+    j = json.loads(Path(plan_path).read_text())
+    rows = []
+    for it in j["iterations"]:
+        for r in it["rows"]:
+            need = set(r["row_images"])
+            npairs = 0
+            for blk in r["blocks"]:
+                need.update(blk["col_images"])
+                npairs += len(blk["pairs"])
+            rows.append((npairs, len(need)))
+    return rows
 
-    n, ppi, band, drop, plan_file = CONFIGS[config]
-    imgs, _ = generate_synthetic(SyntheticScene(n, ppi, band, 0.02, 0.2, seed), pinned=pinned_alloc)
-    feats = {}
-    for i, fs in enumerate(imgs[drop:]):
-        fs.image_id = i
-        feats[i] = fs
-    plan = bm.read_plan(ROOT / "bench_data" / plan_file)
-    return feats, plan
+
+def workload_config(config, n_images, avg_desc, rows):
+    """The `config` object, identical in both arms."""
+    n_pairs = sum(p for p, _ in rows)
+    n_cfg, ppi, band, drop, plan_file = CONFIGS[config]
+    return {"workload": f"{config}: BASELINE config {CONFIG_NO[config]}, {n_images} images x "
+                        f"{avg_desc:.0f} desc, {n_pairs} pairs, {len(rows)} block rows, "
+                        f"iterate_schedule plan {plan_file}, verification off",
+            "rows": len(rows), "k_nearest": 8, "ratio": 0.5, "hash": "L=6, m=8, n=128",
+            "scene": f"generate_synthetic(n={n_cfg}, ppi={ppi}, band={band}, sigma=0.02, "
+                     f"outliers=0.2, seed=7), first {drop} images dropped",
+            "l2": "GPU: flushed (512 MiB write) before every timed step"}
+
+
+def digest(ids, offs, matches) -> str:
+    """sha256 over the result in IdPair order: pair ids (u64), offsets (u64),
+    (query_idx, train_idx) int32 pairs."""
+    h = hashlib.sha256()
+    for a, dt in ((ids, "<u8"), (offs, "<u8"), (matches, "<i4")):
+        h.update(np.ascontiguousarray(a, dt).tobytes())
+    return h.hexdigest()[:16]
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region: NVML
-    polled every 2 ms in a thread (nvidia-smi's 100 ms loop as fallback)."""
+    polled every 2 ms in a thread (nvidia-smi's 100 ms loop as fallback, also
+    when an NVML read fails mid-run).  The NVML handle is resolved from the
+    CUDA device's PCI bus id, so CUDA_VISIBLE_DEVICES / torchrun remapping
+    samples the right GPU."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -105,47 +154,84 @@ class ClockSampler:
         self.samples = []  # (sm_mhz, max_mhz, reasons) from NVML
         self.stop = threading.Event()
         self.nvml = None
+        self.t = None
+        self.bus_id = None
+
+    def _pci_bus_id(self):
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.device)
+            return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        except Exception:  # noqa: BLE001
+            return None
+
+    def _nvml_read(self, h):
+        pynvml = self.nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:  # older bindings
+            bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return float(sm), float(mx), {n for n, b in self.NVML_BITS.items() if bits & b}
 
     def __enter__(self):
         try:
             import pynvml
             pynvml.nvmlInit()
             self.nvml = pynvml
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.bus_id = self._pci_bus_id()
+            h = (pynvml.nvmlDeviceGetHandleByPciBusId(self.bus_id) if self.bus_id
+                 else pynvml.nvmlDeviceGetHandleByIndex(self.device))
+            self.samples.append(self._nvml_read(h))  # trial read: fail here, not in the thread
 
             def poll():
-                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
                 while not self.stop.is_set():
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.samples.append((float(sm), float(mx), {n for n, b in self.NVML_BITS.items() if bits & b}))
+                    try:
+                        self.samples.append(self._nvml_read(h))
+                    except Exception:  # noqa: BLE001
+                        self._start_smi()
+                        return
                     time.sleep(0.002)
 
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
             return self
-        except Exception:
-            self.nvml = None
+        except Exception:  # noqa: BLE001
+            self._shutdown_nvml()
+        self._start_smi()
+        return self
+
+    def _start_smi(self):
+        if self.proc is not None:
+            return
         try:
+            target = self.bus_id or str(self.device)
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", target, f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
-        return self
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def _shutdown_nvml(self):
+        if self.nvml is not None:
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:  # noqa: BLE001
+                pass
+        self.nvml = None
+
     def __exit__(self, *a):
-        if self.nvml:
-            self.stop.set()
+        self.stop.set()
+        if self.t is not None:
             self.t.join(timeout=1)
-            return
+        self._shutdown_nvml()
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -176,15 +262,16 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         busy = [x for x in sm if x > 0.5 * mx] or sm
+        src = "+".join(s for s, on in (("nvml", self.samples), ("nvidia-smi", self.lines)) if on)
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
+                "samples": len(sm), "source": src}
 
 
 def peaks():
     try:
         j = json.loads(PEAKS.read_text())
         return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
+    except Exception:  # noqa: BLE001
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
@@ -198,68 +285,131 @@ def ncu_traffic(avg_ctas_per_launch):
         g = m["metrics"]["launch__grid_size"]
         grid = float(str(g[0] if isinstance(g, (list, tuple)) else g).split()[0].replace(",", ""))
         return m["dram_bytes_per_launch"] / grid * avg_ctas_per_launch
-    except Exception:
+    except Exception:  # noqa: BLE001
         return None
 
 
-def reference_cpu(feats, plan_path, steps, warmup, threads):
-    """oracle/_ref (the reference sources compiled in place) with rows'
-    independent code computations and pair matches spread over `threads`."""
+# ---------------------------------------------------------------------------
+# the reference (CPU) legs: oracle/_ref only
+# ---------------------------------------------------------------------------
+def _reference():
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import Reference
-
-    import paper_2505_22089_b200 as bm
-
-    ref = Reference()
-    imgs = {i: fs.descriptors for i, fs in feats.items()}
-    hseed = bm.seed_for(42, "matching")
-    times, pairs = [], 0
-    for s in range(warmup + steps):
-        done, m, wall = ref.execute_plan_threaded(plan_path, imgs, hseed, threads=threads)
-        if s >= warmup:
-            times.append(wall)
-            pairs = done
-    return pairs, times
+    return Reference()
 
 
-def reference_cpu_sampled(feats, plan, threads):
+def reference_sampled(ref, images, rows, threads):
     """Bounded CPU sample of the reference on `threads` threads, extrapolated
     to the plan: seconds = sum over rows of (needed images x t_codes + pairs x
-    t_pair) / threads, with t_codes / t_pair measured per call on the sample."""
+    t_pair) / threads, with t_codes / t_pair measured per call on the sample.
+    images: {id: (n,128) f32} (at least the first 32 ids)."""
     import concurrent.futures as cf
 
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import Reference
-
-    import paper_2505_22089_b200 as bm
-
-    ref = Reference()
-    hf = ref.make_hash_functions(bm.seed_for(42, "matching"))
-    ids = sorted(feats)[:32]
-    mean = np.mean(np.concatenate([feats[i].descriptors for i in ids]), axis=0).astype(np.float32)
+    hf = ref.make_hash_functions(ref.seed_for(HASH_ROOT_SEED, "matching"))
+    ids = sorted(images)[:32]
+    mean = np.mean(np.concatenate([images[i] for i in ids]), axis=0).astype(np.float32)
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(threads) as ex:
-        codes = dict(zip(ids, ex.map(lambda i: ref.compute_codes(feats[i].descriptors, hf[0], hf[1], mean), ids)))
+        codes = dict(zip(ids, ex.map(lambda i: ref.compute_codes(images[i], hf[0], hf[1], mean), ids)))
     t_codes = (time.perf_counter() - t0) * threads / len(ids)
     pairs = [(a, b) for a in ids for b in ids if a < b <= a + 15][:128]
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(threads) as ex:
-        list(ex.map(lambda p: ref.match_pair(feats[p[0]].descriptors, codes[p[0]], feats[p[1]].descriptors,
-                                              codes[p[1]], (6, 8, 128)), pairs))
+        list(ex.map(lambda p: ref.match_pair(images[p[0]], codes[p[0]], images[p[1]], codes[p[1]],
+                                              (6, 8, 128)), pairs))
     t_pair = (time.perf_counter() - t0) * threads / len(pairs)
-    secs, n_pairs = 0.0, 0
-    for it in plan.iterations:
-        for row in it.rows:
-            needed = set(row.row_images)
-            for b in row.blocks:
-                needed.update(b.col_images)
-                n_pairs += len(b.pairs)
-                secs += len(b.pairs) * t_pair / threads
-            secs += len(needed) * t_codes / threads
+    secs = sum(p * t_pair + n * t_codes for p, n in rows) / threads
+    n_pairs = sum(p for p, _ in rows)
     sample = (f"extrapolated: compute_codes x {len(ids)} images ({t_codes:.2f} s each) + match_pair x "
               f"{len(pairs)} pairs ({t_pair:.3f} s each) on {threads} threads, scaled to the plan's "
               f"{n_pairs} pairs")
     return n_pairs, secs, sample
+
+
+def reference_arm(args):
+    """`--impl reference`: the reference's own CPU code on every host core.
+    Inputs come from the reference generator (oracle/_ref) -- this package is
+    not imported.  Step s runs block row s mod rows of the plan in full (its
+    mean, compute_codes of its needed images, match_pair of its pairs: the
+    row body of engine.cpp:433-489) so the run stays within minutes; value =
+    pairs / seconds over the timed steps."""
+    n_cfg, ppi, band, drop, plan_file = CONFIGS[args.config]
+    plan_path = ROOT / "bench_data" / plan_file
+    rows = plan_rows(plan_path)
+    cores = os.cpu_count() or 1
+    ref = _reference()
+    hseed = ref.seed_for(HASH_ROOT_SEED, "matching")
+    if args.config in SAMPLED:
+        images, _ = ref.generate_synthetic(n_cfg, ppi, band, 0.02, 0.2, 7)
+        images = {i - drop: d for i, d in enumerate(images) if i >= drop}
+        n_images = len(images)
+        avg = sum(len(d) for d in images.values()) / n_images
+        tot_s, tot_p = 0.0, 0
+        for _ in range(args.steps):
+            p, s, sample = reference_sampled(ref, images, rows, cores)
+            tot_s += s
+            tot_p += p
+        warm = "none (extrapolated sample)"
+    else:
+        table = ref.synth_features(n_cfg, ppi, band, 0.02, 0.2, 7, drop)
+        n_images = table.n
+        avg = sum(table.count(i) for i in range(n_images)) / n_images
+        ref.execute_plan_rows(plan_path, table, hseed, threads=cores, row_begin=0, row_end=1)
+        warm = "one block row (a CPU has no JIT or cache state to warm beyond that)"
+        tot_s, tot_p = 0.0, 0
+        for s in range(args.steps):
+            r = s % len(rows)
+            p, _, wall, _ = ref.execute_plan_rows(plan_path, table, hseed, threads=cores,
+                                                  row_begin=r, row_end=r + 1)
+            tot_s += wall
+            tot_p += p
+        sample = (f"{args.steps} steps, step s = block row s mod {len(rows)} of the plan in full "
+                  f"(row mean + compute_codes of its needed images + match_pair of its pairs)")
+        table.free()
+    v = tot_p / tot_s
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator features.cpp:68-197, oracle/_ref)",
+            "impl": "reference",
+            "config": workload_config(args.config, n_images, avg, rows),
+            "parallelism": f"{cores} host threads over each row's images / pairs",
+            "cpu_warmup": warm,
+            "host_cpu": cpu_model(),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def parity_leg(feats, plan_path, rows, config, gpu_flat, cores):
+    """Runs the compiled reference on the repo arm's own inputs (same
+    arrays): its CPU time is the line's cpu_baseline, its match lists are
+    compared with the GPU's (the e2e run's result)."""
+    ref = _reference()
+    hseed = ref.seed_for(HASH_ROOT_SEED, "matching")
+    images = {i: fs.descriptors for i, fs in feats.items()}
+    if config in SAMPLED:
+        p, secs, sample = reference_sampled(ref, images, rows, cores)
+        cpu = {"value": p / secs, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
+        return cpu, {"status": "not checked in the bench (sampled CPU leg; see tests/test_gpu_parity.py)"}
+    table = ref.feature_table(images)
+    done, m, wall, res = ref.execute_plan_rows(plan_path, table, hseed, threads=cores, want_matches=True)
+    table.free()
+    cpu = {"value": done / wall, "unit": UNIT, "cores": cores, "kind": "reference",
+           "sample": f"whole {config} plan once ({done} pairs, {wall:.1f} s on {cores} threads)"}
+    gi, go, gm = gpu_flat
+    ri, ro, rm = res
+    eq = (np.array_equal(gi, ri) and np.array_equal(go, ro) and np.array_equal(gm, rm))
+    par = {"status": "equal" if eq else "DIFFERENT", "pairs": int(len(ri)), "matches": int(len(rm)),
+           "digest_gpu": digest(gi, go, gm), "digest_reference": digest(ri, ro, rm),
+           "reference": "oracle/_ref execute_plan row body (compute_codes + match_pair), same inputs"}
+    if not eq:
+        par["pairs_differing"] = int(sum(
+            1 for p in range(min(len(gi), len(ri)))
+            if not np.array_equal(gm[go[p]:go[p + 1]], rm[ro[p]:ro[p + 1]])))
+    return cpu, par
 
 
 def main():
@@ -267,49 +417,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n_cfg, ppi, band, drop, plan_file = CONFIGS[args.config]
-    plan_path = ROOT / "bench_data" / plan_file
-    cores = os.cpu_count() or 1
-
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        feats, plan = build_workload(args.config, 7)
-        sample = f"whole {args.config} plan per step"
-        if args.config in SAMPLED:
-            times = []
-            for _ in range(args.steps):
-                pairs, secs, sample = reference_cpu_sampled(feats, plan, cores)
-                times.append(secs)
-        else:
-            pairs, times = reference_cpu(feats, plan_path, args.steps, args.warmup, cores)
-            sample = f"whole {args.config} plan per step ({pairs} pairs)"
-        mean_s = sum(times) / len(times)
-        v = pairs / mean_s
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * mean_s,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (reference generator, features.cpp:68-197)",
-                "impl": "reference",
-                "config": {"workload": f"{args.config}: {len(feats)} images x {ppi - 2} desc, "
-                                       f"{plan.pair_count()} pairs, plan {plan_file}",
-                           "parallelism": f"{cores} host threads over each row's images/pairs"},
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                                 "sample": sample},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return 0
+        return reference_arm(args) if rank == 0 else 0
 
     import torch
     import torch.distributed as dist
 
     import paper_2505_22089_b200 as bm
+    from paper_2505_22089_b200 import multigpu
+    from paper_2505_22089_b200.engine import _feature_views
+    from paper_2505_22089_b200.features import SyntheticScene, generate_synthetic, synthetic_counts
 
+    n_cfg, ppi, band, drop, plan_file = CONFIGS[args.config]
+    plan_path = ROOT / "bench_data" / plan_file
+    rows = plan_rows(plan_path)
+    cores = os.cpu_count() or 1
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
+
+    plan = bm.read_plan(plan_path)
+    n_pairs = plan.pair_count()
+    # this rank's shard of the one plan (the whole plan at N=1)
+    sub = multigpu.shard_plan(plan, world)[rank] if world > 1 else plan
+    mine = multigpu.needed_images(sub)
 
     pinned_keep = []
 
@@ -318,14 +451,23 @@ def main():
         pinned_keep.append(t)
         return t.numpy()
 
-    feats, plan = build_workload(args.config, 7 + rank, pinned_alloc)
-    n_pairs = plan.pair_count()
+    # the scene, generated into pinned memory: only the images this rank needs
+    keep = {i + drop for i in mine}
+    imgs, _ = generate_synthetic(SyntheticScene(n_cfg, ppi, band, 0.02, 0.2, 7), pinned=pinned_alloc,
+                                 keep=keep)
+    feats = {}
+    for i, fs in enumerate(imgs[drop:]):
+        if fs is not None:
+            fs.image_id = i
+            feats[i] = fs
+    counts_all = synthetic_counts(SyntheticScene(n_cfg, ppi, band, 0.02, 0.2, 7))[drop:]
+    n_images = len(counts_all)
+    avg_desc = float(counts_all.sum()) / n_images
+    my_pairs = sub.pair_count()
     desc_bytes = sum(fs.descriptors.nbytes for fs in feats.values())
-    avg_desc = desc_bytes / 512 / len(feats)
-    hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
-    cap = bm.arena_units_for(feats, plan.size_gpu)
-    flat = bm.flatten_plan(plan)
-    from paper_2505_22089_b200.engine import _feature_views
+    hf = bm.make_hash_functions(bm.seed_for(HASH_ROOT_SEED, "matching"))
+    cap = bm.arena_units_for(feats, plan.size_gpu) if feats else 1
+    flat = bm.flatten_plan(sub)
     views = _feature_views(feats)
 
     def barrier():
@@ -340,29 +482,69 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
 
-    # ---- e2e: public API from pinned host memory, every byte every step ----
+    # ---- e2e: the public API from pinned host memory, every byte every step;
+    # at N>1 the shared-memory gather of every rank's matches to rank 0 is
+    # inside the timed region
     arena_e2e = bm.DeviceArena(cap, hf, dev)
     opts = bm.ExecuteOptions()
-    d2h = 0
-    for _ in range(args.warmup):
-        r = bm.execute_plan(plan, feats, arena_e2e, opts, flat=flat, views=views)
+
+    def e2e_step(step):
+        r = bm.execute_plan(sub, feats, arena_e2e, opts, flat=flat, views=views)
+        if world > 1:
+            got = multigpu.gather_results(r, rank, world, lambda: dist.barrier(device_ids=[dev]),
+                                          f"{os.environ.get('MASTER_PORT', '0')}_{step}")
+            return r, got
+        return r, None
+
+    for w in range(args.warmup):
+        e2e_step(f"w{w}")
     barrier()
-    e2e_times = []
-    for _ in range(args.steps):
+    e2e_times, d2h = [], 0
+    r = got = None
+    for s in range(args.steps):
         flush.fill_(1)
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
-        r = bm.execute_plan(plan, feats, arena_e2e, opts, flat=flat, views=views)
+        r, got = e2e_step(s)
         e2e_times.append(time.perf_counter() - t0)
-        d2h = 8 * (n_pairs + 1) + 8 * r.metrics.initial_matches
+        d2h = 8 * (my_pairs + 1) + 8 * r.metrics.initial_matches
     barrier()
-    e2e_step = max_over_ranks(sum(e2e_times) / len(e2e_times))
-    e2e_matches = {(pm.query_image, pm.train_image): pm.matches for pm in r.matches}
+    e2e_step_s = max_over_ranks(sum(e2e_times) / len(e2e_times))
+    h2d_all = sum_over_ranks(desc_bytes)
+    d2h_all = sum_over_ranks(d2h)
+    gpu_flat = multigpu.result_flat(r) if world == 1 else (got[:3] if rank == 0 else None)
+    e2e_result = r
     arena_e2e.matcher.close()
 
-    # ---- value: the same row loop on HBM-resident images --------------------
+    # ---- e2e from pageable host memory (the reference's FeatureSet is a
+    # std::vector): the same call, H2D through the staging ring
+    page_ms = None
+    if world == 1:
+        pfeats = {i: bm.FeatureSet(i, np.array(fs.descriptors)) for i, fs in feats.items()}
+        pviews = _feature_views(pfeats)
+        arena_p = bm.DeviceArena(cap, hf, dev)
+        bm.execute_plan(sub, pfeats, arena_p, opts, flat=flat, views=pviews)
+        pt = []
+        for _ in range(min(args.steps, 5)):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            bm.execute_plan(sub, pfeats, arena_p, opts, flat=flat, views=pviews)
+            pt.append(time.perf_counter() - t0)
+        page_ms = 1e3 * sum(pt) / len(pt)
+        arena_p.matcher.close()
+        del pfeats, pviews
+
+    # ---- value: the same row loop on HBM-resident images ---------------------
     arena = bm.DeviceArena(cap * 2, hf, dev)
     for i, fs in feats.items():
         arena.upload(i, fs.descriptors)
@@ -371,7 +553,7 @@ def main():
     # every step, so the timed work is the complete row work
     vopts = bm.ExecuteOptions(retain=True, reproject=True)
     for _ in range(args.warmup):
-        bm.execute_plan(plan, feats, arena, vopts, flat=flat, views=views)
+        bm.execute_plan(sub, feats, arena, vopts, flat=flat, views=views)
     m = arena.matcher
     l0 = m.launch_count()
     dev_ms = []
@@ -380,15 +562,15 @@ def main():
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
             flush.fill_(2)  # L2 flush between timed steps (outside the event span)
-            torch.cuda.synchronize()
-            r = bm.execute_plan(plan, feats, arena, vopts, flat=flat, views=views)
-            dev_ms.append(r.metrics.device_ms)
+            barrier()
+            rv = bm.execute_plan(sub, feats, arena, vopts, flat=flat, views=views)
+            dev_ms.append(rv.metrics.device_ms)
         barrier()
         t_wall = time.perf_counter() - t_wall0
     launches = m.launch_count() - l0
-    got = {(pm.query_image, pm.train_image): pm.matches for pm in r.matches}
-    consistent = got.keys() == e2e_matches.keys() and all(
-        np.array_equal(got[k], e2e_matches[k]) for k in got)
+    vi, vo, vm = multigpu.result_flat(rv)
+    ei, eo, em = multigpu.result_flat(e2e_result)
+    consistent = (np.array_equal(vi, ei) and np.array_equal(vo, eo) and np.array_equal(vm, em))
     # kernel-timing pass (after the timed region): the same steps with the
     # rows on one stream, CUDA events around every launch on its stream.  In
     # the timed region consecutive rows overlap on two streams, so per-launch
@@ -398,49 +580,53 @@ def main():
     for _ in range(args.steps):
         flush.fill_(3)
         torch.cuda.synchronize()
-        bm.execute_plan(plan, feats, arena, sopts, flat=flat, views=views)
+        bm.execute_plan(sub, feats, arena, sopts, flat=flat, views=views)
     match_ms, match_n = m.kernel_time("match")
     kt = {k: m.kernel_time(k) for k in ("project", "mean", "codes", "fixup", "tables", "match", "compact")}
     m.set_profiling(False)
     step_ms = max_over_ranks(sum(dev_ms) / len(dev_ms))
-    value = world * n_pairs / (step_ms * 1e-3)
-    e2e_value = world * n_pairs / e2e_step
+    value = n_pairs / (step_ms * 1e-3)
+    e2e_value = n_pairs / e2e_step_s
 
     # roofline of the dominant kernel (the cascade match kernel):
     # algorithmic bytes per pair = both descriptor sets in f32 = 1024 * n
     pair_bytes = 0
-    for it in plan.iterations:
+    step_ctas = 0
+    for it in sub.iterations:
         for row in it.rows:
-            for b in row.blocks:
-                for a, bb in b.pairs:
-                    pair_bytes += feats[a].descriptors.nbytes + feats[bb].descriptors.nbytes
+            for blk in row.blocks:
+                for a_, b_ in blk.pairs:
+                    pair_bytes += feats[a_].descriptors.nbytes + feats[b_].descriptors.nbytes
+                    step_ctas += -(-len(feats[a_].descriptors) // 1024)
     per_launch_bytes = pair_bytes * args.steps / max(match_n, 1)
     avg_launch_s = match_ms * 1e-3 / max(match_n, 1)
     peak, peak_src = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
-    step_ctas = sum(-(-len(feats[a].descriptors) // 1024)
-                    for it in plan.iterations for row in it.rows for b in row.blocks for a, _ in b.pairs)
     traffic = ncu_traffic(step_ctas * args.steps / max(match_n, 1))
+    consistent_all = max_over_ranks(0.0 if consistent else 1.0) == 0.0
 
     line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
-            "data": "synthetic (reference generator features.cpp:68-197, seed 7+rank)",
-            "config": {"workload": f"{args.config}: {len(feats)} images x {avg_desc:.0f} desc "
-                                   f"(BASELINE config {CONFIG_NO[args.config]}), {n_pairs} pairs/GPU, "
-                                   f"iterate_schedule plan {plan_file}",
-                       "rows": sum(len(it.rows) for it in plan.iterations),
-                       "k_nearest": 8, "ratio": 0.5, "hash": "L=6, m=8, n=128",
-                       "l2": "flushed (512 MiB write) before every timed step",
-                       "parallelism": f"row-block replicas, {world} GPU(s), no collective"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic (reference generator features.cpp:68-197, seed 7)",
+            "config": workload_config(args.config, n_images, avg_desc, rows),
+            "parallelism": (f"one plan sharded over {world} GPU(s) by rows / pairs "
+                            "(multigpu.shard_plan), no collective on the data path" if world > 1
+                            else "1 GPU, two row slots overlapped"),
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": desc_bytes,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step * 1e3,
-                    "step_ms": [round(t * 1e3, 3) for t in e2e_times]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_all),
+                    "d2h_bytes_per_step": int(d2h_all), "ms_per_step": e2e_step_s * 1e3,
+                    "step_ms": [round(t * 1e3, 3) for t in e2e_times],
+                    "source": "pinned host buffers" + (", matches gathered to rank 0 via shared memory"
+                                                       if world > 1 else "")},
+            "e2e_pageable": (None if page_ms is None else
+                             {"value": n_pairs / (page_ms * 1e-3), "unit": UNIT, "ms_per_step": page_ms,
+                              "source": "pageable host buffers (std::vector FeatureSet), H2D via the "
+                                        "pinned staging pair"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "match_kernel", "peak_source": peak_src,
@@ -449,25 +635,23 @@ def main():
                          "timing": "CUDA events around each launch on its stream, serial-row pass "
                                    "of the same steps after the timed region"},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
-            "results_consistent_e2e_vs_resident": consistent,
+            "results_consistent_e2e_vs_resident": consistent_all,
             "wall_s_timed": t_wall,
+            "host_cpu": cpu_model(),
         }
-    # CPU baseline: rank 0 at N=1 only, bounded sample of the same workload
+    # CPU baseline + parity: rank 0 at N=1 only (the reference on the same
+    # inputs; its match lists against the GPU's)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            if args.config in SAMPLED:
-                pairs, secs, sample = reference_cpu_sampled(feats, plan, cores)
-                line["cpu_baseline"] = {"value": pairs / secs, "unit": UNIT, "cores": cores,
-                                        "kind": "reference", "sample": sample}
-            else:
-                pairs, times = reference_cpu(feats, plan_path, 1, 0, cores)
-                line["cpu_baseline"] = {"value": pairs / times[0], "unit": UNIT, "cores": cores,
-                                        "kind": "reference",
-                                        "sample": f"whole {args.config} plan once ({pairs} pairs, "
-                                                  f"{times[0]:.1f} s on {cores} threads)"}
+            line["cpu_baseline"], line["parity"] = parity_leg(feats, plan_path, rows, args.config,
+                                                              gpu_flat, cores)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
+    elif rank == 0 and world > 1:
+        gi, go, gm = gpu_flat
+        line["parity"] = {"status": "gathered result digest (compare with the N=1 line's digest_gpu)",
+                          "digest_gpu": digest(gi, go, gm), "pairs": int(len(gi)), "matches": int(len(gm))}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -186,6 +186,14 @@ int bmg_synthetic_counts(int n_images, int points_per_image, int overlap_band, d
 int bmg_generate_synthetic(int n_images, int points_per_image, int overlap_band,
                            double noise_sigma, double outlier_fraction, uint64_t seed,
                            float* descriptors_out, float* keypoints_out);
+/* The same scene keeping only the images with keep[i] != 0, stored back to
+ * back in image order (a rank of a sharded plan generates what its shard
+ * needs; the draws of the other images are still made, the observation
+ * stream being shared, features.cpp:131-171). */
+int bmg_generate_synthetic_subset(int n_images, int points_per_image, int overlap_band,
+                                  double noise_sigma, double outlier_fraction, uint64_t seed,
+                                  const uint8_t* keep, float* descriptors_out,
+                                  float* keypoints_out);
 
 /* ---- context ----------------------------------------------------------- */
 int bmg_create(const bmg_config* config, bmg_context** out);
@@ -295,6 +303,13 @@ int bmg_exact_walk_count(bmg_context* ctx, uint64_t* queries);
  * `used_chain` = 1 when the sequential FP64 chain produced it (fallback or
  * BMG_EXEC_MEAN_CHAIN). */
 int bmg_row_mean_info(bmg_context* ctx, uint32_t* rounds, int* used_chain);
+/* Test hooks: route every query of later matches through the exact top-K
+ * walk (the path a lane's dropped key triggers) and / or every ratio
+ * decision through the FP64 reference re-rank (the path near ties take).
+ * Results are identical; only speed changes. */
+#define BMG_TEST_FORCE_EXACT_WALK 1u
+#define BMG_TEST_FORCE_FP64_RERANK 2u
+int bmg_set_test_flags(bmg_context* ctx, uint32_t flags);
 
 #ifdef __cplusplus
 }

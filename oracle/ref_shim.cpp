@@ -101,6 +101,10 @@ struct FeatureTable {
   std::map<ImageId, FeatureSet> features;
 };
 
+struct Results {
+  std::map<IdPair, PairMatches> r;
+};
+
 }  // namespace
 
 extern "C" {
@@ -266,12 +270,15 @@ int ref_execute_plan(const char* plan_path, void* features, uint64_t hash_seed, 
 // from engine.cpp:446-461, compute_codes, match_pair) with the independent
 // per-image code computations and per-pair matches of each row spread over
 // `threads` std::threads.  Output equals execute_plan's (pairs keyed by
-// IdPair).  Returns wall seconds; `max_pairs` > 0 bounds the sample (rows are
-// taken in plan order until the bound is reached).
-int ref_execute_plan_threaded(const char* plan_path, void* features, uint64_t hash_seed,
-                              int tables, int cb, int fb, int k, double ratio, int threads,
-                              uint64_t max_pairs, uint64_t* pairs_done, uint64_t* total_matches,
-                              double* wall_s_out) {
+// IdPair, engine.cpp:419, 506-512).  Runs the plan's rows [row_begin, row_end)
+// (global row numbers in plan order, iteration by iteration; row_end = 0
+// means every row) and returns wall seconds of that work.  When pair_ids is
+// non-null the results are returned like ref_execute_plan's (pairs sorted by
+// IdPair): pair_ids[2*p], offsets[p+1], matches[2*m] with m <= match_cap.
+int ref_execute_plan_rows(const char* plan_path, void* features, uint64_t hash_seed, int tables,
+                          int cb, int fb, int k, double ratio, int threads, uint64_t row_begin,
+                          uint64_t row_end, uint64_t* pairs_done, uint64_t* total_matches,
+                          double* wall_s_out, void** results_out) {
   return guarded([&] {
     const SchedulePlan plan = read_plan(plan_path);
     const HashFunctions hf = make_hash_functions(hash_seed, {tables, cb, fb});
@@ -282,10 +289,11 @@ int ref_execute_plan_threaded(const char* plan_path, void* features, uint64_t ha
     const int T = std::max(1, threads);
     const auto t0 = std::chrono::steady_clock::now();
     std::map<IdPair, PairMatches> results;
-    uint64_t done = 0;
+    uint64_t done = 0, global_row = 0;
     for (const ScheduleIteration& it : plan.iterations) {
       for (const BlockRow& row : it.rows) {
-        if (max_pairs && done >= max_pairs) break;
+        const uint64_t gr = global_row++;
+        if (gr < row_begin || (row_end && gr >= row_end)) continue;
         std::set<ImageId> needed(row.row_images.begin(), row.row_images.end());
         for (const ScheduleBlock& blk : row.blocks)
           needed.insert(blk.col_images.begin(), blk.col_images.end());
@@ -340,7 +348,65 @@ int ref_execute_plan_threaded(const char* plan_path, void* features, uint64_t ha
     *pairs_done = done;
     *total_matches = m;
     *wall_s_out = dt.count();
+    if (results_out) *results_out = new Results{std::move(results)};
   });
+}
+
+uint64_t ref_results_pairs(void* h) { return static_cast<Results*>(h)->r.size(); }
+uint64_t ref_results_matches(void* h) {
+  uint64_t m = 0;
+  for (const auto& [p, pm] : static_cast<Results*>(h)->r) m += pm.matches.size();
+  return m;
+}
+// pair_ids[2*p] (IdPair order), offsets[p+1], matches[2*m]
+void ref_results_copy(void* h, uint64_t* pair_ids, uint64_t* offsets, int32_t* matches) {
+  uint64_t o = 0, p = 0;
+  offsets[0] = 0;
+  for (const auto& [key, pm] : static_cast<Results*>(h)->r) {
+    pair_ids[2 * p] = pm.query_image;
+    pair_ids[2 * p + 1] = pm.train_image;
+    for (const auto& [qi, ti] : pm.matches) {
+      matches[2 * o] = qi;
+      matches[2 * o + 1] = ti;
+      ++o;
+    }
+    offsets[++p] = o;
+  }
+}
+void ref_results_free(void* h) { delete static_cast<Results*>(h); }
+
+// The reference's synthetic scene (features.cpp:68-197) straight into a
+// feature table, images [drop, n_images) renumbered from 0 (the bench
+// workloads drop the short leading images of a band scene).
+void* ref_synth_features(int n_images, int ppi, int band, double sigma, double outlier_fraction,
+                         uint64_t seed, int drop) {
+  FeatureTable* t = new FeatureTable;
+  const int rc = guarded([&] {
+    SyntheticScene sc;
+    sc.n_images = n_images;
+    sc.points_per_image = ppi;
+    sc.overlap_band = band;
+    sc.noise_sigma = sigma;
+    sc.outlier_fraction = outlier_fraction;
+    sc.seed = seed;
+    SyntheticDataset data = generate_synthetic(sc);
+    for (int i = drop; i < n_images; ++i) {
+      FeatureSet fs = std::move(data.images.at(i));
+      fs.image_id = static_cast<ImageId>(i - drop);
+      t->features[fs.image_id] = std::move(fs);
+    }
+  });
+  if (rc != 0) {
+    delete t;
+    return nullptr;
+  }
+  return t;
+}
+
+uint64_t ref_features_count(void* h, uint64_t id) {
+  const auto& f = static_cast<FeatureTable*>(h)->features;
+  const auto it = f.find(id);
+  return it == f.end() ? 0 : it->second.size();
 }
 
 // File formats: the reference's own writers and

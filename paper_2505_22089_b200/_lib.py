@@ -92,7 +92,7 @@ EXPORTED = [
     "bmg_set_profiling", "bmg_kernel_time", "bmg_fixup_counts", "bmg_exact_walk_count", "bmg_synthetic_counts",
     "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
     "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
-    "bmg_write_matches_binary",
+    "bmg_write_matches_binary", "bmg_generate_synthetic_subset", "bmg_set_test_flags",
 ]
 
 _lib = None
@@ -150,9 +150,12 @@ def load(path: Path = LIB_PATH):
         "bmg_fixup_counts": (C.c_int, [vp, C.POINTER(u64), C.POINTER(u64)]),
         "bmg_exact_walk_count": (C.c_int, [vp, C.POINTER(u64)]),
         "bmg_row_mean_info": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
+        "bmg_set_test_flags": (C.c_int, [vp, C.c_uint32]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                              u64, vp, vp]),
+        "bmg_generate_synthetic_subset": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
+                                                    C.c_double, u64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

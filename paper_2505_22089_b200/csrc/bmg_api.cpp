@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -324,6 +325,7 @@ struct bmg_context {
   bool profiling = false;
   std::vector<bmg::Timer> timers;
   std::vector<cudaEvent_t> free_events;
+  uint32_t test_flags = 0;  // bmg_set_test_flags
   // BMG_TIMELINE diagnostics: labelled events recorded by the row body
   std::vector<std::pair<std::string, cudaEvent_t>>* marks = nullptr;
 };
@@ -790,7 +792,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   }
   // few pairs (e.g. a single pair): smaller query ranges so the grid still
   // covers every SM twice (down to one query per warp)
-  if (!match_tma_enabled()) {
+  {
     const uint64_t want = 2ull * static_cast<uint64_t>(device_sm_count());
     if ((total_q + chunk - 1) / chunk < want)
       chunk = static_cast<int>(std::max<uint64_t>(32, (total_q + want - 1) / want + 31) / 32 * 32);
@@ -843,6 +845,7 @@ void enqueue_match(Ctx& c, const std::vector<std::pair<int, int>>& slot_pairs,
   a.k = mp.k_nearest;
   a.idx_bits = idx_bits;
   a.ratio = mp.ratio;
+  a.test_flags = c.test_flags;
   if (n_work) {
     Timed t(c, "match", s);
     launch_match(a, h.fwp, static_cast<int>(n_work), s);
@@ -1020,6 +1023,8 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     if (!cfg || !out) fail(BMG_INVALID_ARGUMENT, "null argument");
     if (!valid_hash_params(cfg->hash))
       fail(BMG_INVALID_ARGUMENT, "hash params out of range (tables>=1, coarse_bits in [1,32], fine_bits>=1)");
+    if (cfg->hash.fine_bits > 1024)
+      fail(BMG_UNSUPPORTED, "fine_bits > 1024 (config.cpp:116-122 range) is not supported on the GPU path");
     if (cfg->hash.coarse_bits > 16)
       fail(BMG_UNSUPPORTED, "coarse_bits > 16 (>65536 buckets per table) is not supported on the GPU path");
     if (!cfg->coarse_planes || !cfg->fine_planes) fail(BMG_INVALID_ARGUMENT, "null hash planes");
@@ -1464,6 +1469,10 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     struct ChainHook {
       Ctx& c;
       ~ChainHook() {
+        // failing part-way: queued D2H copies and zero-copy compactions may
+        // still target the result's pinned log, which returns to the pool
+        // when the result is destroyed right after this -- drain them first
+        if (std::uncaught_exceptions() > 0) cudaDeviceSynchronize();
         c.mean_chain_only = false;
         c.cur = 0;
         for (RowSlot& sl : c.slot) {
@@ -1505,7 +1514,11 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       for (uint64_t r = row0; r < row0 + nr; ++r) {
         for (uint64_t k = plan->row_needed_offsets[r]; k < plan->row_needed_offsets[r + 1]; ++k) {
           const uint64_t id = plan->needed_ids[k];
-          if (evict_row.count(id)) in_order = true;  // needed again after its eviction
+          // needed again after its eviction in this iteration: the reference
+          // re-uploads it (counted below); physically it never left HBM, and
+          // only a later eviction (if any) frees it.  Rows then run in plan
+          // order.
+          if (evict_row.erase(id)) in_order = true;
           if (logical.count(id)) continue;
           const bmg_feature_view& fv = features_of(id);
           arena_account_upload(*c, id, fv.descriptors, fv.count);
@@ -1864,6 +1877,15 @@ int bmg_exact_walk_count(bmg_context* c, uint64_t* queries) {
       BMG_CUDA(cudaStreamSynchronize(c->S().s_comp));
     }
     if (queries) *queries = d[2];
+  });
+}
+
+int bmg_set_test_flags(bmg_context* c, uint32_t flags) {
+  return guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
+    if (flags & ~(BMG_TEST_FORCE_EXACT_WALK | BMG_TEST_FORCE_FP64_RERANK))
+      fail(BMG_INVALID_ARGUMENT, "unknown test flag");
+    c->test_flags = flags;
   });
 }
 

@@ -71,7 +71,10 @@ struct MatchLaunch {
   unsigned long long* exact_queries;  // diagnostics: queries that took the FP64 path
   int tables, n_buckets, k, idx_bits;
   double ratio;
+  uint32_t test_flags;  // BMG_TEST_* (bmg_set_test_flags): force the rare exact paths
 };
+constexpr uint32_t kTestForceExactWalk = 1u;   // BMG_TEST_FORCE_EXACT_WALK
+constexpr uint32_t kTestForceFp64Rerank = 2u;  // BMG_TEST_FORCE_FP64_RERANK
 
 // Device state of the exact parallel row mean (kernels.cu K1).
 struct MeanState {
@@ -105,8 +108,6 @@ constexpr uint32_t kSentinel = 8;  // all-pad chunk at the end of each table
 inline uint32_t slot_stride(uint64_t n, int n_buckets, int pad) {
   return static_cast<uint32_t>(((n + (pad - 1ull) * static_cast<uint64_t>(n_buckets) + 7ull) & ~7ull) + kSentinel);
 }
-// whether the TMA-staged matcher (K4b, needs 4-entry bucket padding) is on
-bool match_tma_enabled();
 
 // ---- launchers (kernels.cu) ----
 // Row mean into mean_out (and the FP64 accumulators into acc_out): the exact
@@ -149,7 +150,6 @@ constexpr int kMatchThreads = BMG_MATCH_THREADS;  // one query per warp at a tim
 #define BMG_MATCH_QUERIES 1024
 #endif
 constexpr int kMatchQueries = BMG_MATCH_QUERIES;  // queries per match CTA
-constexpr int kTmaQueries = 1024;    // queries per TMA-staged match CTA (16 warps)
 // queries per CTA of the match kernel launch_match picks for (fwp, k)
 int match_queries_per_cta(int fwp, int k);
 int device_sm_count();

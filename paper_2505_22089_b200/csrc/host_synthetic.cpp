@@ -17,6 +17,8 @@
 
 #include "../../include/bandmatch_gpu.h"
 
+#include "../../include/bandmatch_gpu.h"
+
 namespace bmg {
 
 uint64_t seed_for(uint64_t root, std::string_view stage);
@@ -113,6 +115,17 @@ int bmg_synthetic_counts(int n_images, int ppi, int band, double sigma, double o
 
 int bmg_generate_synthetic(int n_images, int ppi, int band, double sigma, double outlier_fraction,
                            uint64_t seed, float* desc_out, float* keypoints_out) {
+  return bmg_generate_synthetic_subset(n_images, ppi, band, sigma, outlier_fraction, seed, nullptr,
+                                       desc_out, keypoints_out);
+}
+
+// The same scene, storing only the images with keep[i] != 0 (back to back,
+// in image order).  Every image's random draws are still made -- the
+// observation stream is shared by all images (features.cpp:131-171) -- but
+// generation stops after the last kept image.
+int bmg_generate_synthetic_subset(int n_images, int ppi, int band, double sigma,
+                                  double outlier_fraction, uint64_t seed, const uint8_t* keep,
+                                  float* desc_out, float* keypoints_out) {
   const Scene s = make_scene(n_images, ppi, band, sigma, outlier_fraction, seed);
   if (const int rc = check_scene(s)) return rc;
   struct World {
@@ -145,14 +158,22 @@ int bmg_generate_synthetic(int n_images, int ppi, int band, double sigma, double
     p.sn = std::sin(p.theta);
   }
   std::mt19937_64 rng_obs(seed_for(seed, "scene.observations"));
+  int last = s.n - 1;
+  if (keep) {
+    last = -1;
+    for (int i = 0; i < s.n; ++i)
+      if (keep[i]) last = i;
+  }
+  float scratch_desc[kD], scratch_kp[4];
   size_t k = 0;
-  for (int i = 0; i < s.n; ++i) {
+  for (int i = 0; i <= last; ++i) {
     const Pose& p = poses[i];
+    const bool store = !keep || keep[i];
     for (int a = std::max(0, i - s.band); a <= i; ++a) {
-      for (int q = 0; q < s.ppa; ++q, ++k) {
+      for (int q = 0; q < s.ppa; ++q) {
         const World& w = world[static_cast<size_t>(a) * s.ppa + q];
-        if (keypoints_out) {
-          float* kp = keypoints_out + 4 * k;
+        float* kp = keypoints_out ? (store ? keypoints_out + 4 * k : scratch_kp) : nullptr;
+        if (kp) {
           kp[0] = static_cast<float>(p.sc * (p.c * w.x - p.sn * w.y) + p.tx);
           kp[1] = static_cast<float>(p.sc * (p.sn * w.x + p.c * w.y) + p.ty);
           kp[2] = static_cast<float>(w.scale * p.sc);
@@ -164,25 +185,27 @@ int bmg_generate_synthetic(int n_images, int ppi, int band, double sigma, double
           const Vec noise = gaussian_vector(rng_obs, s.sigma);
           for (int c = 0; c < kD; ++c) raw[c] += noise[c];
         }
-        if (!normalize_into(raw, desc_out + k * kD)) {
+        if (!normalize_into(raw, store ? desc_out + k * kD : scratch_desc)) {
           set_last_error("ZeroVector: cannot normalize an all-zero descriptor");
           return BMG_INVALID_SCENE;
         }
+        k += store;
       }
     }
-    for (int o = 0; o < s.opi; ++o, ++k) {
+    for (int o = 0; o < s.opi; ++o) {
       const float x = static_cast<float>(upos(rng_obs));
       const float y = static_cast<float>(upos(rng_obs));
       const float sc = static_cast<float>(uscale(rng_obs));
       const float th = wrap_angle(uangle(rng_obs));
-      if (keypoints_out) {
-        float* kp = keypoints_out + 4 * k;
+      float* kp = keypoints_out ? (store ? keypoints_out + 4 * k : scratch_kp) : nullptr;
+      if (kp) {
         kp[0] = x;
         kp[1] = y;
         kp[2] = sc;
         kp[3] = th;
       }
-      random_unit(rng_obs, desc_out + k * kD);
+      random_unit(rng_obs, store ? desc_out + k * kD : scratch_desc);
+      k += store;
     }
   }
   return BMG_OK;

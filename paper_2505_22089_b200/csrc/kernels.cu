@@ -1400,10 +1400,6 @@ constexpr int kLaneKeys = BMG_LANE_KEYS;
 #define BMG_WALK_DEPTH 2
 #endif
 constexpr int kWalkDepth = BMG_WALK_DEPTH;
-#ifndef BMG_STAGED_RERANK
-#define BMG_STAGED_RERANK 0
-#endif
-constexpr bool kStagedRerank = BMG_STAGED_RERANK != 0;
 
 // FWP code words of one bucket-ordered entry (16-byte loads where possible)
 template <int FWP>
@@ -1427,15 +1423,6 @@ __device__ __forceinline__ uint32_t hamming(const uint64_t (&q)[FWP], const uint
   for (int x = 0; x < FWP; ++x) h += __popcll(q[x] ^ t[x]);
   return h;
 }
-
-// 16-byte global -> shared copy that bypasses registers (cp.async, L2 only)
-__device__ __forceinline__ void cp_async16(float4* dst, const float4* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Walks the union; round(key) is called by every lane once per round
 // (warp-uniform trip count).  lo / sz: lane t < L holds table t's bucket range
@@ -1527,17 +1514,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   const float r2f = (float)r2;
   uint32_t n_matched = 0;
 
-  // BMG_STAGED_RERANK=1 (A/B variant, K <= 8): the K kept rows of a query
-  // (and its own row) are copied into the warp's shared-memory slot with
-  // cp.async and ranked one query later, after the next query's walk; each
-  // lane copies and later reads only its own 16-byte piece of every row.
-  // Measured slower (1.13 vs 1.09 ms per launch): the 144 KB of slots take
-  // the L1 capacity the walk's chunk loads hit in.
-  constexpr bool kStaged = KM == 8 && kStagedRerank;
-  extern __shared__ float4 s_rows[];
-  float4* rr = s_rows + (kStaged ? warp * 9 * 32 : 0);
-  uint32_t pq = kEmpty, plst = kEmpty;
-  int pkept = 0;
   auto emit = [&](uint32_t q, int32_t result) {
     if (lane == 0) {
       a.dense[a.dense_off[w.pair] + q] = result;
@@ -1562,15 +1538,14 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         const int ck = lane >> 2, part = lane & 3;
         const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
         const float2 neg1 = make_float2(-1.f, -1.f);
-        const float4 qv = kStaged ? rr[8 * 32 + lane] : __ldg(Qd + (size_t)q * 32 + lane);
+        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
         float pt[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           pt[c] = 0.f;
-          uint32_t jc = 0;
-          if constexpr (!kStaged) jc = __shfl_sync(kFull, my_idx, c);
+          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
           if (c < kept) {
-            const float4 tv = kStaged ? rr[c * 32 + lane] : __ldg(Td + (size_t)jc * 32 + lane);
+            const float4 tv = __ldg(Td + (size_t)jc * 32 + lane);
             // d = q - t exactly rounded (t * -1 + q), then d * d summed
             const float2 d0 = __ffma2_rn(make_float2(tv.x, tv.y), neg1, make_float2(qv.x, qv.y));
             const float2 d1 = __ffma2_rn(make_float2(tv.z, tv.w), neg1, make_float2(qv.z, qv.w));
@@ -1662,10 +1637,17 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // certified in FP32: the distances carry relative error < 1e-6, each
       // product below 2^-24 and r2f its own 2^-24, all far inside the 2e-5
       // margins (ties d1 == r^2 d2 land in the FP64 band, which rejects them)
+      // Accept also needs the argmin itself certified (s_min clearly below
+      // s_2): with ratio > 1 a near tie passes the ratio margin, and the FP32
+      // argmin could then differ from the reference's FP64 (dist, idx) first.
+      // ratio <= 0 or NaN: d1 < d2 * ratio never holds (hashmatch.cpp:47-49),
+      // so only lone candidates are kept.
       const float c_hi = 1.0f + 2.0e-5f, c_lo = 1.0f - 2.0e-5f;
       const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
-      const bool accept = finite && s_min * c_hi < r2f * s_2;
-      const bool reject = finite && s_min * c_lo >= (r2f * s_2) * c_hi;
+      const bool rpos = ratio > 0.0;
+      const bool fast = (a.test_flags & kTestForceFp64Rerank) == 0;
+      const bool accept = fast && rpos && finite && s_min * c_hi < r2f * s_2 && s_min * c_hi < s_2;
+      const bool reject = fast && (!rpos || (finite && s_min * c_lo >= (r2f * s_2) * c_hi));
       if (accept) {
         result = (int32_t)i_min;
       } else if (!reject) {
@@ -1779,7 +1761,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
           kl[kLaneKeys - 1] = pop ? kEmpty : kl[kLaneKeys - 1];
         }
       }
-      exact = __any_sync(kFull, dmin < m);
+      exact = __any_sync(kFull, dmin < m) || (a.test_flags & kTestForceExactWalk) != 0;
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
@@ -1808,382 +1790,8 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
 
     // ---- re-rank + ratio test
     const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
-    if constexpr (kStaged) {
-      // rank the previous query from its staged rows, then stage this one's
-      if (pq != kEmpty) {
-        cp_async_wait_all();
-        finish(pq, plst, pkept);
-      }
-      if (kept > 1) {
-        const uint32_t my_idx = lst & idx_mask;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
-          if (c < kept) cp_async16(rr + c * 32 + lane, Td + (size_t)jc * 32 + lane);
-        }
-        cp_async16(rr + 8 * 32 + lane, Qd + (size_t)q * 32 + lane);
-        cp_async_commit();
-        pq = q;
-        plst = lst;
-        pkept = kept;
-      } else {
-        emit(q, kept == 1 ? (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask) : -1);
-        pq = kEmpty;
-      }
-    } else {
-      finish(q, lst, kept);
-    }
+    finish(q, lst, kept);
   }
-  if constexpr (kStaged) {
-    if (pq != kEmpty) {
-      cp_async_wait_all();
-      finish(pq, plst, pkept);
-    }
-  }
-  if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
-}
-
-// ---------------------------------------------------------------------------
-// K4b: the cascade with TMA-staged candidates (K <= 8, unions up to `cap`
-// entries).  CTA = 16 warps; a warp takes every 16th query of its range and
-// runs a software pipeline over them:
-//   * as soon as query i's union has been ranked, one bulk copy per table
-//     (cp.async.bulk, completing on an mbarrier) stages query i+1's bucket
-//     runs -- fine codes and train indices, padded to 4 entries -- into the
-//     warp's candidate buffer, back to back, so the union is one flat smem
-//     array (lands while query i-1's re-rank and query i's staging run);
-//   * query i's union is walked from shared memory (lane l takes entries
-//     l, l+32, ..): POPC Hamming, key = hamming << ib | idx (pad entries carry
-//     idx 0xffffffff, i.e. key kEmpty), per-lane top-4, REDUX pulls -- the
-//     same exact ranking as K4;
-//   * query i's K kept rows (and its own row) are bulk-copied into the warp's
-//     re-rank buffer and ranked one query later, after query i+1's walk, so
-//     the gather latency is hidden too.
-// Unions larger than `cap` take K4's global-memory chunked walk.
-// ---------------------------------------------------------------------------
-constexpr int kTmaWarps = 16;
-constexpr int kRowStride = 528;  // 512-byte row + 16: conflict-free LDS.128 across candidates
-constexpr int kRrBytes = 9 * kRowStride;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-// generic-proxy accesses to a buffer are ordered before the async-proxy
-// (bulk copy) writes that recycle it
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__host__ __device__ constexpr uint32_t tma_warp_bytes(uint32_t cap, int fwp) {
-  return cap * (8u * fwp + 4u) + kRrBytes + 16u;
-}
-
-template <int FWP, int KC>
-__global__ void __launch_bounds__(kTmaWarps * 32, 1) match_tma_kernel(MatchLaunch a, uint32_t cap) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  constexpr uint32_t CB = 8u * FWP;
-  const PairWork w = a.work[blockIdx.x];
-  const ImgDev T = a.imgs[w.t_img];
-  const ImgDev Q = a.imgs[w.q_img];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int L = a.tables, K = KC ? KC : a.k, ib = a.idx_bits;
-  const uint32_t idx_mask = (1u << ib) - 1u;
-  const int nb1 = a.n_buckets + 1;
-  const double ratio = a.ratio;
-  const double r2 = ratio * ratio;
-
-  const uint32_t cand_bytes = cap * (CB + 4u);
-  unsigned char* wb = dsm + (size_t)warp * tma_warp_bytes(cap, FWP);
-  unsigned char* rr = wb + cand_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rr + kRrBytes);  // [0] candidates, [1] re-rank rows
-  if (lane == 0) {
-    mbar_init(bars + 0, 1);
-    mbar_init(bars + 1, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  uint32_t ph0 = 0, ph1 = 0;
-
-  const uint32_t q0 = w.q_begin + warp;
-  const uint32_t nqw = q0 < w.q_end ? (w.q_end - q0 + kTmaWarps - 1) / kTmaWarps : 0u;
-  auto qof = [&](uint32_t i) { return q0 + i * kTmaWarps; };
-  auto load_b = [&](uint32_t i) -> uint32_t {
-    return (lane < L && i < nqw) ? __ldg(Q.coarse + (size_t)qof(i) * L + lane) : 0u;
-  };
-  auto load_range = [&](uint32_t b, uint32_t i, uint32_t& lo, uint32_t& sz) {
-    lo = sz = 0;
-    if (lane < L && i < nqw) {
-      const uint32_t* off = T.offsets + (size_t)lane * nb1 + b;
-      lo = __ldg(off);
-      sz = __ldg(off + 1) - lo;
-    }
-  };
-  // stage a union into the candidate buffer: the flattened entry count
-  // rounded up to a multiple of 32 (slots past the union hold kEmpty), or
-  // kEmpty when it does not fit (the walk then reads global memory)
-  auto issue = [&](uint32_t lo, uint32_t sz) -> uint32_t {
-    uint32_t incl = sz;
-    for (int o = 1; o < L; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const uint32_t total = __shfl_sync(kFull, incl, L - 1);
-    const uint32_t padded = (total + 31u) & ~31u;
-    if (padded > cap) return kEmpty;
-    if (total == 0) return 0u;
-    uint32_t* slots = reinterpret_cast<uint32_t*>(wb + (size_t)cap * CB);
-    if (total + lane < padded) slots[total + lane] = kEmpty;
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_expect_tx(bars, total * (CB + 4u));
-    __syncwarp();
-    if (lane < L && sz) {
-      const uint32_t cum = incl - sz;
-      const size_t s0 = (size_t)lane * T.ns + lo;
-      bulk_g2s(wb + (size_t)cum * CB, T.bfine + s0 * FWP, sz * CB, bars);
-      bulk_g2s(slots + cum, T.slots + s0, sz * 4u, bars);
-    }
-    return padded;
-  };
-  auto walk_smem = [&](uint32_t padded, const uint64_t (&qc)[FWP], auto&& round) {
-    const uint32_t* slots = reinterpret_cast<const uint32_t*>(wb + (size_t)cap * CB) + lane;
-    const unsigned char* codes = wb + (size_t)lane * CB;
-#pragma unroll 2
-    for (uint32_t e0 = 0; e0 < padded; e0 += 32) {
-      const uint32_t j = slots[e0];
-      uint64_t c[FWP];
-      if constexpr (FWP % 2 == 0) {
-#pragma unroll
-        for (int x = 0; x < FWP / 2; ++x) {
-          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(codes + (size_t)e0 * CB)[x];
-          c[2 * x] = v.x;
-          c[2 * x + 1] = v.y;
-        }
-      } else {
-        c[0] = *reinterpret_cast<const uint64_t*>(codes + (size_t)e0 * CB);
-      }
-      round((hamming<FWP>(qc, c) << ib) | j);
-    }
-  };
-
-  // deferred re-rank of the previous query
-  uint32_t pq = kEmpty, plst = kEmpty;
-  int pkept = 0;
-  uint32_t n_matched = 0;
-  auto emit = [&](uint32_t q, int32_t result) {
-    if (lane == 0) {
-      a.dense[a.dense_off[w.pair] + q] = result;
-      n_matched += result >= 0 ? 1u : 0u;
-    }
-  };
-  auto finish = [&](uint32_t q, uint32_t lst, int kept) {
-    mbar_wait(bars + 1, ph1);
-    ph1 ^= 1u;
-    const bool mine = lane < kept;
-    const uint32_t my_idx = lst & idx_mask;
-    // lanes 4c..4c+3 hold candidate c (row c+1 of the buffer): lane part p
-    // covers float4s p, p+4, .., p+28 in two packed FP32x2 chains; every FP32
-    // sum has depth <= 13 (relative error ~1e-6, inside the 1e-5 margin)
-    const int ck = lane >> 2, part = lane & 3;
-    const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
-    float s = 0.f;
-    if (ck < kept) {
-      const float4* qp = reinterpret_cast<const float4*>(rr) + part;
-      const float4* tp = reinterpret_cast<const float4*>(rr + (ck + 1) * kRowStride) + part;
-      const float2 neg1 = make_float2(-1.f, -1.f);
-      float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 av = qp[4 * i], bv = tp[4 * i];
-        const float2 d0 = __ffma2_rn(make_float2(bv.x, bv.y), neg1, make_float2(av.x, av.y));
-        const float2 d1 = __ffma2_rn(make_float2(bv.z, bv.w), neg1, make_float2(av.z, av.w));
-        s0 = __ffma2_rn(d0, d0, s0);
-        s1 = __ffma2_rn(d1, d1, s1);
-      }
-      s = (s0.x + s0.y) + (s1.x + s1.y);
-    }
-    s += __shfl_xor_sync(kFull, s, 1);
-    s += __shfl_xor_sync(kFull, s, 2);
-    const bool lead = part == 0 && ck < kept;
-    const uint32_t sb = lead ? __float_as_uint(s) : kEmpty;
-    const uint32_t mb = __reduce_min_sync(kFull, sb);
-    const uint32_t i_min = __reduce_min_sync(kFull, (lead && sb == mb) ? jk : kEmpty);
-    const float s_min = __uint_as_float(mb);
-    const float s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
-    const double lo_f = 1.0 - 1.0e-5, hi_f = 1.0 + 1.0e-5;
-    const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
-    const bool accept = finite && (double)s_min * hi_f < r2 * ((double)s_2 * lo_f);
-    const bool reject = finite && (double)s_min * lo_f >= r2 * ((double)s_2 * hi_f);
-    int32_t result = -1;
-    if (accept) {
-      result = (int32_t)i_min;
-    } else if (!reject) {
-      // FP64 reference path (hashmatch.cpp:35-42, :196-208)
-      double e = __longlong_as_double(0x7ff0000000000000ll);
-      if (mine) {
-        const float* qd = Q.desc + (size_t)q * kDim;
-        const float* td = T.desc + (size_t)my_idx * kDim;
-        double acc = 0.0;
-#pragma unroll 8
-        for (int c = 0; c < kDim; ++c) {
-          const double d = __dsub_rn((double)__ldg(qd + c), (double)__ldg(td + c));
-          acc = __dadd_rn(acc, __dmul_rn(d, d));
-        }
-        e = __dsqrt_rn(acc);
-      }
-      double be = e;
-      uint32_t bj = mine ? my_idx : 0xffffffffu;
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        const double oe = __shfl_xor_sync(kFull, be, o);
-        const uint32_t oj = __shfl_xor_sync(kFull, bj, o);
-        if (oe < be || (oe == be && oj < bj)) {
-          be = oe;
-          bj = oj;
-        }
-      }
-      const double e_first = __shfl_sync(kFull, be, 0);
-      const uint32_t i_first = __shfl_sync(kFull, bj, 0);
-      double e2 = (mine && my_idx != i_first) ? e : __longlong_as_double(0x7ff0000000000000ll);
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(kFull, e2, o));
-      const double e_second = __shfl_sync(kFull, e2, 0);
-      if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
-      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
-    }
-    emit(q, result);
-  };
-
-  uint32_t lo_cur = 0, sz_cur = 0, lo_nx = 0, sz_nx = 0, tot_cur = 0;
-  {
-    const uint32_t b0 = load_b(0);
-    load_range(b0, 0, lo_cur, sz_cur);
-    if (nqw) tot_cur = issue(lo_cur, sz_cur);
-    const uint32_t b1 = load_b(1);
-    load_range(b1, 1, lo_nx, sz_nx);
-  }
-  uint32_t b_nn = load_b(2);
-  for (uint32_t i = 0; i < nqw; ++i) {
-    const uint32_t q = qof(i);
-    uint64_t qc[FWP];
-#pragma unroll
-    for (int x = 0; x < FWP; ++x) qc[x] = __ldg(Q.fine + (size_t)q * FWP + x);
-    const bool staged = tot_cur != kEmpty;
-    if (staged && tot_cur) {
-      mbar_wait(bars, ph0);
-      ph0 ^= 1u;
-    }
-
-    // ---- per-lane top-4, REDUX pulls (K4 fast path)
-    uint32_t k0 = kEmpty, k1 = kEmpty, k2 = kEmpty, k3 = kEmpty, dmin = kEmpty;
-    auto ins = [&](uint32_t key) {
-      dmin = min(dmin, max(k3, key));
-      k3 = max(k2, min(k3, key));
-      k2 = max(k1, min(k2, key));
-      k1 = max(k0, min(k1, key));
-      k0 = min(k0, key);
-    };
-    if (staged) walk_smem(tot_cur, qc, ins);
-    else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](uint32_t key) { ins(key); });
-    if (__any_sync(kFull, (k0 == k1 && k1 != kEmpty) || (k1 == k2 && k2 != kEmpty) || (k2 == k3 && k3 != kEmpty))) {
-#pragma unroll
-      for (int rep = 0; rep < 3; ++rep) {
-        if (k0 == k1) { k1 = k2; k2 = k3; k3 = kEmpty; }
-        if (k1 == k2) { k2 = k3; k3 = kEmpty; }
-        if (k2 == k3) k3 = kEmpty;
-      }
-    }
-    uint32_t lst = kEmpty, mlast = kEmpty;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (r < K) {
-        const uint32_t m = __reduce_min_sync(kFull, k0);
-        mlast = m;
-        lst = lane == r ? m : lst;
-        const bool pop = k0 == m;
-        k0 = pop ? k1 : k0;
-        k1 = pop ? k2 : k1;
-        k2 = pop ? k3 : k2;
-        k3 = pop ? kEmpty : k3;
-      }
-    }
-    if (__any_sync(kFull, dmin < mlast)) {
-      // exact path (see K4): REDUX-driven insertion into a sorted list
-      lst = kEmpty;
-      uint32_t thr = kEmpty;
-      auto exact = [&](uint32_t key) {
-        key = key < thr ? key : kEmpty;
-        for (;;) {
-          const uint32_t m = __reduce_min_sync(kFull, key);
-          if (m >= thr) break;
-          if (key == m) key = kEmpty;
-          if (!__any_sync(kFull, lane < 8 && lst == m)) {
-            const uint32_t prev = __shfl_up_sync(kFull, lst, 1);
-            const uint32_t nv = lst < m ? lst : ((lane == 0 || prev < m) ? m : prev);
-            lst = lane < 8 ? nv : kEmpty;
-            thr = __shfl_sync(kFull, lst, K - 1);
-          }
-        }
-      };
-      if (staged) walk_smem(tot_cur, qc, exact);
-      else walk_union<FWP>(T, L, lo_cur, sz_cur, ib, qc, [&](uint32_t key) { exact(key); });
-      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries + 1, 1ull);
-    }
-
-    // ---- the buffer is free: stage the next query's union; ranges and
-    // buckets further ahead
-    tot_cur = i + 1 < nqw ? issue(lo_nx, sz_nx) : 0u;
-    lo_cur = lo_nx;
-    sz_cur = sz_nx;
-    load_range(b_nn, i + 2, lo_nx, sz_nx);
-    b_nn = load_b(i + 3);
-
-    // ---- the previous query's re-rank (its rows have landed), then stage ours
-    if (pq != kEmpty) finish(pq, plst, pkept);
-    pq = kEmpty;
-    const int kept = __popc(__ballot_sync(kFull, lane < K && lst != kEmpty));
-    if (kept == 1) {
-      emit(q, (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask));
-    } else if (kept == 0) {
-      emit(q, -1);
-    } else {
-      const uint32_t jc = __shfl_sync(kFull, lst, (lane + 31) & 31) & idx_mask;
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(bars + 1, (uint32_t)(kept + 1) * 512u);
-      __syncwarp();
-      if (lane <= kept) {
-        const float* src = lane == 0 ? Q.desc + (size_t)q * kDim : T.desc + (size_t)jc * kDim;
-        bulk_g2s(rr + lane * kRowStride, src, 512u, bars + 1);
-      }
-      pq = q;
-      plst = lst;
-      pkept = kept;
-    }
-  }
-  if (pq != kEmpty) finish(pq, plst, pkept);
   if (lane == 0 && n_matched) atomicAdd(a.pair_count + w.pair, n_matched);
 }
 
@@ -2400,53 +2008,13 @@ int launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile
 
 template <int FWP, int KM, int NT, int KC>
 static void launch_match_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  // K <= 8: one 9-row re-rank slot per warp (staged rows, see match_kernel)
-  constexpr size_t smem = KM == 8 && kStagedRerank ? (size_t)(NT / 32) * 9 * kDim * sizeof(float) : 0;
-  if constexpr (smem > 48 * 1024) {
-    static const bool configured = [] {
-      return cudaFuncSetAttribute(match_kernel<FWP, KM, NT, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem) == cudaSuccess;
-    }();
-    (void)configured;
-  }
-  match_kernel<FWP, KM, NT, KC><<<n_work, NT, smem, s>>>(a);
-}
-
-// staged-union capacity that fits kTmaWarps warps in shared memory
-static uint32_t tma_cap(int fwp) {
-  const int budget = 227 * 1024 - 2048;
-  const int per = budget / kTmaWarps - kRrBytes - 16;
-  return (uint32_t)(per / (8 * fwp + 4)) & ~31u;
-}
-
-template <int FWP, int KC>
-static void launch_tma_t(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  const uint32_t cap = tma_cap(FWP);
-  const size_t smem = (size_t)kTmaWarps * tma_warp_bytes(cap, FWP);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(match_tma_kernel<FWP, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  match_tma_kernel<FWP, KC><<<n_work, kTmaWarps * 32, smem, s>>>(a, cap);
-}
-
-bool match_tma_enabled() {
-  static const bool tma = [] {
-    const char* v = getenv("BMG_MATCH_TMA");  // A/B switch: the TMA-staged K4b
-    return v && v[0] == '1';
-  }();
-  return tma;
+  match_kernel<FWP, KM, NT, KC><<<n_work, NT, 0, s>>>(a);
 }
 
 template <int FWP>
 static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
-  const bool tma = match_tma_enabled();
-  if (tma && FWP <= 4 && a.k <= 8) {
-    if (a.k == 8) launch_tma_t<FWP, 8>(a, n_work, s);  // MatchParams default
-    else launch_tma_t<FWP, 0>(a, n_work, s);
-  } else if (a.k == 8) {
-    launch_match_t<FWP, 8, kMatchThreads, 8>(a, n_work, s);
+  if (a.k == 8) {
+    launch_match_t<FWP, 8, kMatchThreads, 8>(a, n_work, s);  // MatchParams default
   } else if (a.k < 8) {
     launch_match_t<FWP, 8, kMatchThreads, 0>(a, n_work, s);
   } else {
@@ -2457,7 +2025,9 @@ static void launch_match_fw(const MatchLaunch& a, int n_work, cudaStream_t s) {
 int device_sm_count() { return sm_count(); }
 
 int match_queries_per_cta(int fwp, int k) {
-  return (match_tma_enabled() && fwp <= 4 && k <= 8) ? kTmaQueries : kMatchQueries;
+  (void)fwp;
+  (void)k;
+  return kMatchQueries;
 }
 
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
@@ -2466,7 +2036,8 @@ void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s) {
     case 2: launch_match_fw<2>(a, n_work, s); break;
     case 4: launch_match_fw<4>(a, n_work, s); break;
     case 8: launch_match_fw<8>(a, n_work, s); break;
-    default: launch_match_fw<16>(a, n_work, s); break;
+    case 16: launch_match_fw<16>(a, n_work, s); break;
+    default: break;  // bmg_create rejects fine_bits > 1024 (fwp > 16)
   }
 }
 

@@ -321,6 +321,20 @@ class _PairList(Sequence):
     def __eq__(self, other):
         return list(self) == list(other)
 
+    def flat(self):
+        """(pair_ids [P,2] u64, offsets [P+1] u64, matches [M,2] i32): the
+        result in IdPair order, matches concatenated (the layout of
+        bmg_result_copy)."""
+        ids = np.asarray(self._ids, np.uint64).reshape(-1, 2)
+        rng = np.asarray(self._rng, np.int64).reshape(-1, 2)
+        counts = rng[:, 1] - rng[:, 0]
+        offs = np.zeros(len(counts) + 1, np.uint64)
+        np.cumsum(counts, out=offs[1:])
+        if self._log is None or not counts.sum():
+            return ids, offs, np.zeros((0, 2), np.int32)
+        parts = [self._log[b:e] for b, e in rng if e > b]
+        return ids, offs, np.ascontiguousarray(np.concatenate(parts), np.int32)
+
     def __reduce__(self):
         return (list, (list(self),))
 

@@ -38,23 +38,40 @@ def synthetic_counts(scene: SyntheticScene) -> np.ndarray:
     return counts[: scene.n_images]
 
 
-def generate_synthetic(scene: SyntheticScene, keypoints: bool = False, pinned=None):
+def generate_synthetic(scene: SyntheticScene, keypoints: bool = False, pinned=None, keep=None):
     """generate_synthetic (features.cpp:68-197): returns (images, true_pairs);
     images[i] is a FeatureSet with image_id i.  ``pinned``: optional callable
-    (nbytes) -> writable uint8 buffer (e.g. page-locked memory) to generate into."""
+    (nbytes) -> writable uint8 buffer (e.g. page-locked memory) to generate into.
+    ``keep``: optional set of image indices to store (the others are None in
+    ``images``; their random draws are still made)."""
     L = _lib.load()
     counts = synthetic_counts(scene)
+    if keep is not None:
+        mask = np.zeros(max(scene.n_images, 1), np.uint8)
+        for i in keep:
+            if 0 <= i < scene.n_images:
+                mask[i] = 1
+        counts = np.where(mask[: scene.n_images] != 0, counts, 0).astype(np.uint64)
     total = int(counts.sum())
     if pinned is not None:
         buf = np.frombuffer(pinned(max(total, 1) * DIM * 4), np.float32, max(total, 1) * DIM)
     else:
         buf = np.zeros(max(total, 1) * DIM, np.float32)
     kps = np.zeros(max(total, 1) * 4, np.float32) if keypoints else None
-    check(L.bmg_generate_synthetic(scene.n_images, scene.points_per_image, scene.overlap_band,
-                                   scene.noise_sigma, scene.outlier_fraction, scene.seed,
-                                   ptr(buf), ptr(kps)))
+    if keep is None:
+        check(L.bmg_generate_synthetic(scene.n_images, scene.points_per_image, scene.overlap_band,
+                                       scene.noise_sigma, scene.outlier_fraction, scene.seed,
+                                       ptr(buf), ptr(kps)))
+    else:
+        check(L.bmg_generate_synthetic_subset(scene.n_images, scene.points_per_image,
+                                              scene.overlap_band, scene.noise_sigma,
+                                              scene.outlier_fraction, scene.seed, ptr(mask),
+                                              ptr(buf), ptr(kps)))
     images, off = [], 0
     for i, n in enumerate(counts.tolist()):
+        if keep is not None and not mask[i]:
+            images.append(None)
+            continue
         d = buf[off * DIM:(off + n) * DIM].reshape(n, DIM)
         k = kps[off * 4:(off + n) * 4].reshape(n, 4) if keypoints else None
         fs = FeatureSet.__new__(FeatureSet)

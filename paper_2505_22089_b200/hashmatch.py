@@ -273,6 +273,12 @@ class Matcher:
         check(self._L.bmg_exact_walk_count(self.handle, C.byref(a)))
         return a.value
 
+    def set_test_flags(self, force_exact_walk: bool = False, force_fp64_rerank: bool = False):
+        """Test hooks (bmg_set_test_flags): send every query through the exact
+        top-K walk and / or every ratio decision through the FP64 re-rank."""
+        check(self._L.bmg_set_test_flags(self.handle, (1 if force_exact_walk else 0)
+                                         | (2 if force_fp64_rerank else 0)))
+
     def row_mean_info(self):
         """(rounds, used_chain) of the last computed row mean (diagnostics)."""
         r, u = C.c_uint32(0), C.c_int(0)

@@ -1,84 +1,249 @@
-"""Multi-GPU execution of one SchedulePlan: block rows shard across the GPUs of
+"""Multi-GPU execution of ONE SchedulePlan: its work shards across the GPUs of
 one node with no collective on the data path.
 
-Rows are independent given the plan: a row's mean, codes and matches depend
-only on its own resident image set (engine.cpp:433-465), so each rank takes a
-contiguous, pair-balanced range of every iteration's rows, uploads what its
-rows need into its own HBM arena, and its matches go D2H on that rank.  The
-only communication is the final gather of match lists to rank 0 (host
-objects; the reference keys results by IdPair, engine.cpp:419, so the merge is
-order-independent).  Iterations stay barriers, as in the reference
-(engine.cpp:497-499), because an iteration's plan covers the pairs the
-previous one left.
+Block rows are independent given the plan: a row's mean, codes and matches
+depend only on its own resident image set (engine.cpp:433-465), and a pair's
+matches only on the row's codes of its two images (engine.cpp:467-472).  So
+each iteration's pair sequence (rows in plan order, pairs in block order) is
+cut into `world` contiguous pieces balanced by a cost model -- one unit per
+pair plus `prep_weight` units per needed image of every row a piece touches
+(a rank that takes part of a row computes that row's mean, codes and bucket
+tables itself: they are bit-identical on every GPU) -- and each rank runs the
+sub-plan of its piece through the single-GPU executor.  A row split between
+ranks keeps all of its blocks on every rank (blocks outside the rank's range
+keep their images and lose their pairs), so its needed set -- and hence its
+mean -- is unchanged.  Eviction directives are recomputed per rank the way
+generate_blocks derives them (mbr.cpp:299-317): each arena holds what its
+later rows still need and ends every iteration empty.  Iterations stay
+barriers (engine.cpp:497-499).
+
+The only communication is the final gather of the match lists to rank 0,
+through shared memory (one node): each rank writes its result -- already in
+IdPair order -- into a /dev/shm segment, rank 0 merges the segments by
+IdPair (results are keyed by pair, engine.cpp:419, 506-512).  No objects are
+pickled.
 """
 from __future__ import annotations
 
-from dataclasses import replace
+import os
+import tempfile
+from collections.abc import Sequence
+
+import numpy as np
 
 from .engine import (BlockRow, DeviceArena, ExecuteOptions, ExecutionResult, IterationMetrics,
-                     PipelineMetrics, ScheduleIteration, SchedulePlan, execute_plan)
+                     PipelineMetrics, ScheduleBlock, ScheduleIteration, SchedulePlan, execute_plan)
 from .hashmatch import HashFunctions, PairMatches
 
-__all__ = ["partition_rows", "local_plan", "execute_plan_distributed", "merge_results"]
+__all__ = ["shard_plan", "needed_images", "execute_plan_distributed", "gather_results",
+           "result_flat", "FlatPairs"]
+
+# cost of one needed image of a row (mean + codes + bucket tables) in units of
+# one pair's matching, measured on the B200 (block32: 0.67 ms of row prep for
+# 48 image-rows vs 2.03 ms of matching for 286 pairs)
+PREP_WEIGHT = 2.0
 
 
-def partition_rows(plan: SchedulePlan, world: int) -> list[set[int]]:
-    """Global row indices per rank: each iteration's rows are cut into `world`
-    contiguous ranges with balanced pair counts (MBR order keeps neighbouring
-    rows -- which share images -- on the same GPU)."""
-    out = [set() for _ in range(world)]
-    g = 0
-    for it in plan.iterations:
-        weights = [sum(len(b.pairs) for b in r.blocks) for r in it.rows]
-        total = sum(weights)
-        acc, rank = 0, 0
-        for w in weights:
-            # advance to the next rank once this one holds its share
-            while rank < world - 1 and acc >= total * (rank + 1) / world:
-                rank += 1
-            out[rank].add(g)
-            acc += w
-            g += 1
+def _pieces(costs_pairs: list, row_needed: list, world: int, prep_weight: float) -> list:
+    """Cut one iteration's pair sequence into <= world contiguous pieces:
+    returns [(row, first pair, end pair)] per piece.  costs_pairs[r] = pairs
+    of row r.  Binary search on the largest piece cost; a piece is filled
+    greedily (a piece's cost only grows as it extends, so greedy filling is
+    optimal for a given cap)."""
+    total_pairs = sum(costs_pairs)
+    if total_pairs == 0:
+        return [[] for _ in range(world)]
+
+    def fill(cap):
+        pieces, cur, cost, touched = [], [], 0.0, set()
+        for r, n in enumerate(costs_pairs):
+            p = 0
+            while p < n:
+                add_row = 0.0 if r in touched else prep_weight * row_needed[r]
+                room = cap - cost - add_row
+                if room < 1.0:
+                    if not cur:
+                        return None  # a single pair plus its row does not fit
+                    pieces.append(cur)
+                    cur, cost, touched = [], 0.0, set()
+                    continue
+                take = min(n - p, int(room))
+                cur.append((r, p, p + take))
+                cost += add_row + take
+                touched.add(r)
+                p += take
+        if cur:
+            pieces.append(cur)
+        return pieces
+
+    lo = max(1.0, prep_weight * max((row_needed[r] for r, n in enumerate(costs_pairs) if n), default=0) + 1)
+    hi = float(total_pairs) + prep_weight * sum(row_needed) + 1.0
+    best = fill(hi)
+    for _ in range(60):
+        if hi - lo <= 0.5:
+            break
+        mid = (lo + hi) / 2
+        got = fill(mid)
+        if got is not None and len(got) <= world:
+            best, hi = got, mid
+        else:
+            lo = mid
+    best = best + [[] for _ in range(world - len(best))]
+    return best
+
+
+def _local_evictions(rows: list) -> list:
+    needed = [set(r.needed()) for r in rows]
+    resident: set = set()
+    out = []
+    for t, r in enumerate(rows):
+        resident |= needed[t]
+        later = set().union(*needed[t + 1:]) if t + 1 < len(rows) else set()
+        ev = sorted(x for x in resident if x not in later)
+        resident -= set(ev)
+        out.append(BlockRow(r.row_chunk, list(r.row_images), r.blocks, ev))
     return out
 
 
-def local_plan(plan: SchedulePlan, rows: set[int]) -> SchedulePlan:
-    """The rank's sub-plan: its rows, with eviction directives recomputed the
-    way generate_blocks does (mbr.cpp:299-317) so the local arena holds only
-    what its later rows still need and ends every iteration empty."""
-    lp = SchedulePlan(plan.strategy, plan.size_blk, plan.size_gpu, plan.final_dimension)
-    g = 0
+def shard_plan(plan: SchedulePlan, world: int, prep_weight: float = PREP_WEIGHT) -> list:
+    """One sub-plan per rank; together they cover every planned pair exactly
+    once, with every row's needed set (so its mean and codes) unchanged."""
+    subs = [SchedulePlan(plan.strategy, plan.size_blk, plan.size_gpu, plan.final_dimension)
+            for _ in range(world)]
     for it in plan.iterations:
-        mine = []
-        for r in it.rows:
-            if g in rows:
-                mine.append(r)
-            g += 1
-        needed = [set(r.needed()) for r in mine]
-        resident: set = set()
-        new_rows = []
-        for t, r in enumerate(mine):
-            resident |= needed[t]
-            later = set().union(*needed[t + 1:]) if t + 1 < len(mine) else set()
-            ev = sorted(x for x in resident if x not in later)
-            resident -= set(ev)
-            new_rows.append(BlockRow(r.row_chunk, list(r.row_images), list(r.blocks), ev))
-        lp.iterations.append(ScheduleIteration(it.dimension, it.bandwidth_before,
-                                               it.bandwidth_after, new_rows))
-    return lp
+        pairs_of = [[p for b in r.blocks for p in b.pairs] for r in it.rows]
+        pieces = _pieces([len(x) for x in pairs_of], [len(r.needed()) for r in it.rows], world,
+                         prep_weight)
+        for rank in range(world):
+            rows = []
+            for r, p0, p1 in pieces[rank]:
+                row = it.rows[r]
+                blocks, k = [], 0
+                for b in row.blocks:
+                    lo, hi = max(p0 - k, 0), min(p1 - k, len(b.pairs))
+                    blocks.append(ScheduleBlock(b.row_chunk, b.col_chunk, b.row_images, b.col_images,
+                                                list(b.pairs[lo:hi]) if hi > lo else []))
+                    k += len(b.pairs)
+                rows.append(BlockRow(row.row_chunk, list(row.row_images), blocks, []))
+            subs[rank].iterations.append(ScheduleIteration(it.dimension, it.bandwidth_before,
+                                                           it.bandwidth_after, _local_evictions(rows)))
+    return subs
 
 
-def merge_results(parts: list[ExecutionResult], strategy: str = "") -> ExecutionResult:
-    """Merge per-rank results: pairs sorted by IdPair, counters summed
-    (uploads/evictions/peak are per-device arena figures)."""
-    by_pair: dict = {}
+def needed_images(plan: SchedulePlan) -> set:
+    """Every image any row of the plan needs (what a rank must load)."""
+    return {i for it in plan.iterations for r in it.rows for i in r.needed()}
+
+
+class FlatPairs(Sequence):
+    """A result's pairs as flat arrays (IdPair order): pair_ids [P,2] u64,
+    offsets [P+1] u64, matches [M,2] i32; PairMatches made on access."""
+
+    def __init__(self, ids, offs, matches):
+        self.ids, self.offs, self.m = ids, offs, matches
+
+    def __len__(self):
+        return len(self.ids)
+
+    def __getitem__(self, p):
+        if isinstance(p, slice):
+            return [self[i] for i in range(*p.indices(len(self)))]
+        if p < 0:
+            p += len(self)
+        if not 0 <= p < len(self):
+            raise IndexError(p)
+        return PairMatches(int(self.ids[p, 0]), int(self.ids[p, 1]),
+                           self.m[int(self.offs[p]):int(self.offs[p + 1])])
+
+    def flat(self):
+        return self.ids, self.offs, self.m
+
+
+def result_flat(res: ExecutionResult):
+    """(pair_ids, offsets, matches) of a result in IdPair order."""
+    if hasattr(res.matches, "flat"):
+        return res.matches.flat()
+    pms = sorted(res.matches, key=lambda pm: (pm.query_image, pm.train_image))
+    ids = np.array([(pm.query_image, pm.train_image) for pm in pms], np.uint64).reshape(-1, 2)
+    counts = [len(pm.matches) for pm in pms]
+    offs = np.zeros(len(pms) + 1, np.uint64)
+    np.cumsum(counts, out=offs[1:])
+    m = (np.ascontiguousarray(np.concatenate([np.asarray(pm.matches, np.int32).reshape(-1, 2)
+                                              for pm in pms]))
+         if pms and sum(counts) else np.zeros((0, 2), np.int32))
+    return ids, offs, m
+
+
+def _shm_dir() -> str:
+    return "/dev/shm" if os.path.isdir("/dev/shm") and os.access("/dev/shm", os.W_OK) \
+        else tempfile.gettempdir()
+
+
+def gather_results(res: ExecutionResult, rank: int, world: int, barrier, tag: str):
+    """Gathers every rank's match lists to rank 0 through shared memory.
+    `barrier()` synchronises the ranks (torch.distributed).  Returns the
+    merged (pair_ids, offsets, matches, metrics list) on rank 0, None elsewhere."""
+    import pickle  # metrics only (a few integers per rank)
+
+    ids, offs, m = result_flat(res)
+    path = os.path.join(_shm_dir(), f"bmg_gather_{tag}_{rank}")
+    hdr = np.array([len(ids), len(m)], np.uint64)
+    with open(path, "wb") as f:
+        f.write(hdr.tobytes())
+        f.write(np.ascontiguousarray(ids, np.uint64).tobytes())
+        f.write(np.ascontiguousarray(offs, np.uint64).tobytes())
+        f.write(np.ascontiguousarray(m, np.int32).tobytes())
+        f.write(pickle.dumps(res.metrics))
+    barrier()
+    out = None
+    if rank == 0:
+        all_ids, all_counts, all_starts, all_m, mets = [], [], [], [], []
+        base = 0
+        for r in range(world):
+            p = os.path.join(_shm_dir(), f"bmg_gather_{tag}_{r}")
+            raw = np.fromfile(p, np.uint8)
+            P, M = (int(x) for x in raw[:16].view(np.uint64))
+            o = 16
+            ids_r = raw[o:o + 16 * P].view(np.uint64).reshape(-1, 2)
+            o += 16 * P
+            offs_r = raw[o:o + 8 * (P + 1)].view(np.uint64).astype(np.int64)
+            o += 8 * (P + 1)
+            m_r = raw[o:o + 8 * M].view(np.int32).reshape(-1, 2)
+            o += 8 * M
+            mets.append(pickle.loads(raw[o:].tobytes()))
+            all_ids.append(ids_r)
+            all_counts.append(np.diff(offs_r))
+            all_starts.append(offs_r[:-1] + base)  # run starts in the concatenated logs
+            all_m.append(m_r)
+            base += M
+        ids = np.concatenate(all_ids)
+        counts = np.concatenate(all_counts)
+        starts = np.concatenate(all_starts)
+        mall = np.concatenate(all_m)
+        order = np.lexsort((ids[:, 1], ids[:, 0]))
+        ids, counts, starts = ids[order], counts[order], starts[order]
+        offs = np.zeros(len(ids) + 1, np.uint64)
+        np.cumsum(counts, out=offs[1:])
+        total = int(counts.sum())
+        if total:
+            # each pair's run, in IdPair order, from the concatenated logs
+            first = offs[:-1].astype(np.int64)
+            merged = mall[np.repeat(starts - first, counts) + np.arange(total)]
+        else:
+            merged = np.zeros((0, 2), np.int32)
+        out = (ids, offs, np.ascontiguousarray(merged), mets)
+    barrier()
+    os.unlink(path)
+    return out
+
+
+def merge_metrics(mets: list, strategy: str = "") -> PipelineMetrics:
+    """Per-rank PipelineMetrics summed (uploads/evictions/peak are per-device
+    arena figures; wall and device time are the max over ranks)."""
     met = PipelineMetrics(strategy)
-    n_it = max((len(p.metrics.per_iteration) for p in parts), default=0)
+    n_it = max((len(m.per_iteration) for m in mets), default=0)
     its = [IterationMetrics() for _ in range(n_it)]
-    for p in parts:
-        for pm in p.matches:
-            by_pair[(pm.query_image, pm.train_image)] = pm
-        m = p.metrics
+    for m in mets:
         met.pairs_matched += m.pairs_matched
         met.initial_matches += m.initial_matches
         met.uploads += m.uploads
@@ -94,31 +259,31 @@ def merge_results(parts: list[ExecutionResult], strategy: str = "") -> Execution
     met.per_iteration = its
     met.utilization_proxy = met.pairs_matched / met.uploads if met.uploads else 0.0
     met.pairs_per_second = met.pairs_matched / met.wall_time_s if met.wall_time_s > 0 else 0.0
-    return ExecutionResult([by_pair[k] for k in sorted(by_pair)], met)
+    return met
 
 
-def execute_plan_distributed(plan: SchedulePlan, features: dict, hf: HashFunctions,
-                             capacity_units: int, opts: ExecuteOptions = ExecuteOptions(),
-                             device: int | None = None, executor=None):
+def execute_plan_distributed(plan: SchedulePlan, features: dict, hf: HashFunctions | None = None,
+                             capacity_units: int = 0, opts: ExecuteOptions = ExecuteOptions(),
+                             device: int | None = None, executor=None, arena: DeviceArena | None = None,
+                             tag: str = "plan"):
     """Run `plan` across the ranks of the default torch.distributed group
-    (one process per GPU).  Returns the merged ExecutionResult on rank 0 and
-    the rank-local one elsewhere.  `executor(sub_plan, features)` replaces the
-    GPU row loop (tests inject a CPU stand-in to exercise the sharding)."""
+    (one process per GPU; several ranks may share a device).  `features`
+    needs only the images of this rank's shard (needed_images(shard_plan(
+    plan, world)[rank])).  Returns the merged ExecutionResult on rank 0 and
+    None elsewhere.  `executor(sub_plan, features)` replaces the GPU row loop
+    (tests inject a CPU stand-in)."""
     import torch.distributed as dist
 
     rank, world = dist.get_rank(), dist.get_world_size()
-    sub = local_plan(plan, partition_rows(plan, world)[rank])
+    sub = shard_plan(plan, world)[rank]
     if executor is None:
-        if device is None:
-            device = rank
-        arena = DeviceArena(capacity_units, hf, device)
+        if arena is None:
+            arena = DeviceArena(capacity_units, hf, rank if device is None else device)
         res = execute_plan(sub, features, arena, opts)
     else:
         res = executor(sub, features)
-    payload = ([(pm.query_image, pm.train_image, pm.matches) for pm in res.matches], res.metrics)
-    gathered = [None] * world if rank == 0 else None
-    dist.gather_object(payload, gathered, dst=0)
+    got = gather_results(res, rank, world, dist.barrier, tag)
     if rank != 0:
-        return res
-    parts = [ExecutionResult([PairMatches(q, t, m) for q, t, m in pl], met) for pl, met in gathered]
-    return merge_results(parts, plan.strategy)
+        return None
+    ids, offs, m, mets = got
+    return ExecutionResult(FlatPairs(ids, offs, m), merge_metrics(mets, plan.strategy))

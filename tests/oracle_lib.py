@@ -171,10 +171,22 @@ class Reference:
         L.ref_execute_plan.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int,
                                        C.c_int, C.c_int, C.c_double, C.c_uint64, _u64p, _u64p,
                                        _i32p, C.POINTER(C.c_uint64), C.POINTER(C.c_double), _u64p]
-        L.ref_execute_plan_threaded.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.c_int,
-                                                C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
-                                                C.c_uint64, C.POINTER(C.c_uint64),
-                                                C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.ref_execute_plan_rows.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int,
+                                            C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64,
+                                            C.c_uint64, C.POINTER(C.c_uint64),
+                                            C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                            C.POINTER(C.c_void_p)]
+        L.ref_results_pairs.restype = C.c_uint64
+        L.ref_results_pairs.argtypes = [C.c_void_p]
+        L.ref_results_matches.restype = C.c_uint64
+        L.ref_results_matches.argtypes = [C.c_void_p]
+        L.ref_results_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_results_free.argtypes = [C.c_void_p]
+        L.ref_synth_features.restype = C.c_void_p
+        L.ref_synth_features.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                         C.c_uint64, C.c_int]
+        L.ref_features_count.restype = C.c_uint64
+        L.ref_features_count.argtypes = [C.c_void_p, C.c_uint64]
 
         L.ref_write_features.argtypes = [C.c_char_p, C.c_uint64, _f32p, _f32p, C.c_uint64]
         L.ref_read_features.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64),
@@ -328,18 +340,68 @@ class Reference:
                 "peak_occupancy"]
         return res, dict(zip(keys, map(int, counters))), wall.value
 
-    def execute_plan_threaded(self, plan_path, images, hash_seed, params=(6, 8, 128), k=8,
-                              ratio=0.5, threads=None, max_pairs=0):
+    def synth_features(self, n_images, ppi, band, sigma=0.02, outlier_fraction=0.2, seed=7, drop=0):
+        """The reference generator straight into a reference feature table
+        (images [drop, n) renumbered from 0).  Returns a FeatureTable."""
+        h = self.lib.ref_synth_features(n_images, ppi, band, sigma, outlier_fraction, seed, drop)
+        if not h:
+            self._check(1)
+        return FeatureTable(self, h, n_images - drop)
+
+    def feature_table(self, images):
+        """{id: (n,128) f32} copied into a reference feature table."""
+        return FeatureTable(self, self._features(images), len(images))
+
+    def execute_plan_rows(self, plan_path, features, hash_seed, params=(6, 8, 128), k=8, ratio=0.5,
+                          threads=None, row_begin=0, row_end=0, want_matches=False):
+        """The reference's row body (mean, compute_codes, match_pair) over the
+        plan rows [row_begin, row_end) (0 = all) on `threads` threads.
+        features: a FeatureTable or {id: array}.  Returns (pairs, matches,
+        wall_s, results) with results = (pair_ids [P,2] u64, offsets [P+1]
+        u64, matches [M,2] i32) in IdPair order, or None."""
         threads = threads or os.cpu_count()
-        h = self._features(images)
+        own = not isinstance(features, FeatureTable)
+        table = self.feature_table(features) if own else features
+        res = C.c_void_p(None)
         try:
             done, m, wall = C.c_uint64(0), C.c_uint64(0), C.c_double(0)
-            self._check(self.lib.ref_execute_plan_threaded(
-                str(plan_path).encode(), h, hash_seed, params[0], params[1], params[2], k, ratio,
-                threads, max_pairs, C.byref(done), C.byref(m), C.byref(wall)))
+            self._check(self.lib.ref_execute_plan_rows(
+                str(plan_path).encode(), table.handle, hash_seed, params[0], params[1], params[2], k,
+                ratio, threads, row_begin, row_end, C.byref(done), C.byref(m), C.byref(wall),
+                C.byref(res) if want_matches else None))
+            out = None
+            if want_matches and res.value:
+                np_ = self.lib.ref_results_pairs(res)
+                nm = self.lib.ref_results_matches(res)
+                ids = np.zeros((max(np_, 1), 2), np.uint64)
+                offs = np.zeros(np_ + 1, np.uint64)
+                mt = np.zeros((max(nm, 1), 2), np.int32)
+                self.lib.ref_results_copy(res, ids.ctypes.data, offs.ctypes.data, mt.ctypes.data)
+                out = (ids[:np_], offs, mt[:nm])
         finally:
-            self.lib.ref_features_free(h)
-        return done.value, m.value, wall.value
+            if res.value:
+                self.lib.ref_results_free(res)
+            if own:
+                table.free()
+        return done.value, m.value, wall.value, out
+
+
+class FeatureTable:
+    """A std::map<ImageId, FeatureSet> owned by the reference library."""
+
+    def __init__(self, ref, handle, n):
+        self.ref, self.handle, self.n = ref, handle, n
+
+    def count(self, image_id):
+        return self.ref.lib.ref_features_count(self.handle, image_id)
+
+    def free(self):
+        if self.handle:
+            self.ref.lib.ref_features_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.free()
 
 
 class RefError(Exception):

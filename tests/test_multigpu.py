@@ -1,6 +1,8 @@
-"""Row sharding across ranks on CPU: world_size-2 gloo groups run
-execute_plan_distributed with the C oracle standing in for the GPU row loop;
-the merged result must equal the single-process execution of the whole plan."""
+"""Sharding one plan across ranks on CPU: world_size-2 gloo groups
+run execute_plan_distributed with the C oracle standing in for the GPU row loop
+(the GPU branch is covered by tests/test_gpu_parity.py); the merged result --
+gathered through shared memory -- must equal the single-process execution of
+the whole plan."""
 import os
 import socket
 
@@ -64,10 +66,16 @@ def _worker(rank, world, port, feats, plan, queue):
     from oracle_lib import Oracle
     o = Oracle()
     coarse, fine = o.make_hash_functions(o.seed_for(42, "matching"))
-    res = multigpu.execute_plan_distributed(plan, feats, None, 0,
-                                            executor=oracle_executor(o, coarse, fine))
+    sub = multigpu.shard_plan(plan, world)[rank]
+    mine = {i: feats[i] for i in multigpu.needed_images(sub)}  # only this rank's images
+    res = multigpu.execute_plan_distributed(plan, mine, None, 0,
+                                            executor=oracle_executor(o, coarse, fine),
+                                            tag=f"test{port}")
     if rank == 0:
-        queue.put([(pm.query_image, pm.train_image, pm.matches.tolist()) for pm in res.matches])
+        queue.put([(pm.query_image, pm.train_image, np.asarray(pm.matches).tolist())
+                   for pm in res.matches])
+    else:
+        assert res is None
     dist.barrier()
     dist.destroy_process_group()
 
@@ -78,22 +86,76 @@ def free_port():
         return s.getsockname()[1]
 
 
-def test_partition_is_exact_cover_and_balanced(reference, tmp_path):
+def test_shards_cover_every_pair_once_with_rows_unchanged(reference, tmp_path):
     feats, plan = scene(reference, tmp_path)
-    n_rows = sum(len(it.rows) for it in plan.iterations)
-    for world in (1, 2, 3, 8):
-        parts = multigpu.partition_rows(plan, world)
-        assert sorted(x for p in parts for x in p) == list(range(n_rows))
-        for p in parts:
-            sub = multigpu.local_plan(plan, p)
-            for it in sub.iterations:
+    row_needed = {}
+    for it in plan.iterations:
+        for r in it.rows:
+            row_needed[r.row_chunk, tuple(r.row_images)] = r.needed()
+    for world in (1, 2, 3, 8, 40):
+        subs = multigpu.shard_plan(plan, world)
+        assert len(subs) == world
+        covered = sorted(pr for s in subs for pr in s.pairs())
+        assert covered == plan.pairs()  # exactly once
+        for s in subs:
+            assert len(s.iterations) == len(plan.iterations)  # iterations stay barriers
+            for it in s.iterations:
                 held = set()
                 for r in it.rows:
+                    # a (part of a) row keeps its whole needed set: same mean and codes
+                    assert r.needed() == row_needed[r.row_chunk, tuple(r.row_images)]
                     held |= set(r.needed())
                     held -= set(r.evict_after)
-                assert not held
-        covered = sorted(pr for p in parts for pr in multigpu.local_plan(plan, p).pairs())
-        assert covered == plan.pairs()
+                assert not held  # every rank's arena ends each iteration empty
+
+
+def test_shard_balance_on_the_bench_plans():
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1] / "bench_data"
+    for f in ("plan_strip500.json", "plan_shard16k.json", "plan_block32.json"):
+        plan = bm.read_plan(root / f)
+        for world in (2, 4, 8):
+            subs = multigpu.shard_plan(plan, world)
+            cost = [sum(len(b.pairs) for it in s.iterations for r in it.rows for b in r.blocks)
+                    + multigpu.PREP_WEIGHT * sum(len(r.needed()) for it in s.iterations for r in it.rows)
+                    for s in subs]
+            # no rank far above the mean (prep of shared rows is duplicated)
+            assert max(cost) <= 1.25 * (sum(cost) / world) + 1, (f, world, cost)
+            assert sorted(p for s in subs for p in s.pairs()) == plan.pairs()
+
+
+def test_shared_memory_gather_merges_by_idpair(tmp_path):
+    """gather_results in one process with a fake 3-rank barrier schedule:
+    each 'rank' writes its IdPair-sorted result; rank 0's merge is the union
+    in IdPair order."""
+    rng = np.random.default_rng(1)
+    parts = []
+    for r in range(3):
+        pms = []
+        for k in range(4):
+            a = int(rng.integers(0, 50))
+            m = rng.integers(0, 100, (int(rng.integers(0, 5)), 2)).astype(np.int32)
+            pms.append(bm.PairMatches(a, 100 + 10 * k + r, m))
+        parts.append(ExecutionResult(sorted(pms, key=lambda p: (p.query_image, p.train_image)),
+                                     PipelineMetrics(pairs_matched=4)))
+    # ranks 1, 2 write first (their barrier is a no-op here), then rank 0 merges
+    import threading
+    ev = threading.Barrier(3)
+    out = {}
+
+    def run(r):
+        out[r] = multigpu.gather_results(parts[r], r, 3, ev.wait, "unit")
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    ids, offs, m, mets = out[0]
+    assert out[1] is None and out[2] is None
+    want = sorted((pm.query_image, pm.train_image, pm.matches.tolist()) for p in parts for pm in p.matches)
+    got = [(int(ids[i, 0]), int(ids[i, 1]), m[offs[i]:offs[i + 1]].tolist()) for i in range(len(ids))]
+    assert got == want
+    assert sum(x.pairs_matched for x in mets) == 12
 
 
 def test_two_rank_gloo_execution_equals_single_process(reference, oracle, tmp_path):
@@ -111,5 +173,6 @@ def test_two_rank_gloo_execution_equals_single_process(reference, oracle, tmp_pa
         p.join(timeout=120)
         assert p.exitcode == 0
     assert [(a, b) for a, b, _ in got] == [(pm.query_image, pm.train_image) for pm in single.matches]
+    assert len(got) == len(plan.pairs())
     for (a, b, m), pm in zip(got, single.matches):
         assert np.array_equal(np.array(m, np.int32).reshape(-1, 2), pm.matches)
