@@ -505,13 +505,17 @@ def main():
             return r, got
         return r, None
 
+    # the previous step's result is released before the next call, so the
+    # result's pinned log comes back from the process-wide pool every step
+    r = got = None
     for w in range(args.warmup):
-        e2e_step(f"w{w}")
+        r = got = None
+        r, got = e2e_step(f"w{w}")
     barrier()
     e2e_times, d2h = [], 0
-    r = got = None
     for s in range(args.steps):
         flush.fill_(1)
+        r = got = None
         barrier()
         t0 = time.perf_counter()
         r, got = e2e_step(s)

@@ -21,13 +21,18 @@
 // and NotResident behave exactly as in the reference.  With
 // opts.verify.enabled the initial matches are verified on host threads with
 // the reference's sao_filter + ransac_fundamental, as VerifyPool does
-// (engine.cpp:326-377).
+// (engine.cpp:326-377), WHILE the GPU matches later rows: each block row's
+// pairs arrive through the executor's on_pair hand-off as soon as that row's
+// matches are in host memory and go into a bounded queue (backpressure as in
+// VerifyPool::push, engine.cpp:293-299) that opts.threads workers drain.
 #pragma once
 
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
 #include <exception>
 #include <map>
 #include <memory>
@@ -145,6 +150,125 @@ struct Hooks {
   }
 };
 
+// Verification overlapped with the GPU: a bounded producer / consumer queue
+// fed by bmg_execute_plan's on_pair hand-off (collector thread) and drained
+// by `threads` workers running the reference's SAO + RANSAC per pair
+// (VerifyPool, engine.cpp:275-390; its per-job body :326-377).  push blocks
+// while the queue is full -- backpressure on the collector thread only, the
+// GPU keeps matching.  Results are keyed by IdPair (engine.cpp:419).
+class Verifier {
+ public:
+  struct Record {
+    bandmatch::PairMatches matches;
+    bandmatch::PairOutcome outcome;
+  };
+  Verifier(const std::map<bandmatch::ImageId, bandmatch::FeatureSet>& features,
+           const bandmatch::ExecuteOptions& opts)
+      : features_(features), opts_(opts), capacity_(std::max<std::size_t>(1, opts.queue_capacity)) {
+    for (int w = 0; w < std::max(1, opts.threads); ++w) workers_.emplace_back([this] { run(); });
+  }
+  ~Verifier() { close(); }
+
+  // bmg_pair_callback: copy the pair's initial matches out of the pinned
+  // log and queue the job
+  static void on_pair(void* u, std::uint64_t q, std::uint64_t t, const std::int32_t* m,
+                      std::uint64_t n) {
+    auto* v = static_cast<Verifier*>(u);
+    Job job;
+    job.initial.query_image = q;
+    job.initial.train_image = t;
+    job.initial.matches.reserve(n);
+    for (std::uint64_t i = 0; i < n; ++i) job.initial.matches.emplace_back(m[2 * i], m[2 * i + 1]);
+    std::unique_lock<std::mutex> lk(v->mu_);
+    v->push_cv_.wait(lk, [v] { return v->queue_.size() < v->capacity_; });
+    v->queue_.push_back(std::move(job));
+    v->pop_cv_.notify_one();
+  }
+
+  // every queued job processed, workers joined; rethrows the first error
+  void close() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      if (closed_) return;
+      closed_ = true;
+    }
+    pop_cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+    if (err_) std::rethrow_exception(err_);
+  }
+
+  std::map<bandmatch::IdPair, Record> records;
+
+ private:
+  struct Job {
+    bandmatch::PairMatches initial;
+  };
+  void run() {
+    for (;;) {
+      Job job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        pop_cv_.wait(lk, [this] { return closed_ || !queue_.empty(); });
+        if (queue_.empty()) return;
+        job = std::move(queue_.front());
+        queue_.pop_front();
+      }
+      push_cv_.notify_one();
+      Record rec = process(job.initial);
+      std::lock_guard<std::mutex> lk(mu_);
+      records[rec.outcome.pair] = std::move(rec);
+    }
+  }
+  Record process(const bandmatch::PairMatches& in) {
+    using namespace bandmatch;
+    Record r;
+    const FeatureSet& qf = features_.at(in.query_image);
+    const FeatureSet& tf = features_.at(in.train_image);
+    r.matches.query_image = in.query_image;
+    r.matches.train_image = in.train_image;
+    r.matches.stage = PairMatches::Stage::kVerified;
+    PairOutcome& oc = r.outcome;
+    oc.pair = IdPair(in.query_image, in.train_image);
+    oc.initial = in.matches.size();
+    try {
+      const SaoOutcome sao = sao_filter(in, qf.keypoints, tf.keypoints, opts_.verify.sao);
+      oc.after_sao = sao.kept.matches.size();
+      oc.sao_passthrough = sao.passthrough;
+      oc.delaunay_fallback = sao.delaunay_fallback;
+      const std::uint64_t seed =
+          seed_for(opts_.seed, "verify." + std::to_string(oc.pair.a) + "." + std::to_string(oc.pair.b));
+      const InlierSet inl = ransac_fundamental(sao.kept, qf.keypoints, tf.keypoints, opts_.verify.ransac, seed);
+      for (int idx : inl.kept) r.matches.matches.push_back(sao.kept.matches[idx]);
+      oc.inliers = r.matches.matches.size();
+      oc.ransac_iterations = inl.iterations;
+    } catch (const Error& e) {
+      oc.no_model = true;
+      r.matches.matches.clear();
+      if (e.code() != "TooFewMatches" && e.code() != "NoModel") {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!err_) err_ = std::current_exception();
+      }
+    } catch (...) {
+      oc.no_model = true;
+      r.matches.matches.clear();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (!err_) err_ = std::current_exception();
+    }
+    oc.inlier_ratio = oc.initial == 0 ? 0.0 : static_cast<double>(oc.inliers) / oc.initial;
+    return r;
+  }
+
+  const std::map<bandmatch::ImageId, bandmatch::FeatureSet>& features_;
+  const bandmatch::ExecuteOptions& opts_;
+  const std::size_t capacity_;
+  std::mutex mu_;
+  std::condition_variable push_cv_, pop_cv_;
+  std::deque<Job> queue_;
+  bool closed_ = false;
+  std::exception_ptr err_;
+  std::vector<std::thread> workers_;
+};
+
 }  // namespace detail
 
 // execute_plan (engine.cpp:411-527): the row body runs on the B200; results,
@@ -194,8 +318,23 @@ inline bandmatch::ExecutionResult execute_plan(
   eo.on_upload = &detail::Hooks::on_upload;
   eo.on_evict = &detail::Hooks::on_evict;
   eo.hook_user = &hooks;
+  std::unique_ptr<detail::Verifier> verifier;
+  if (opts.verify.enabled) {
+    verifier = std::make_unique<detail::Verifier>(features, opts);
+    eo.on_pair = &detail::Verifier::on_pair;
+    eo.on_pair_user = verifier.get();
+  }
   bmg_result* r = nullptr;
-  check(bmg_execute_plan(ctx.get(), &fp, views.data(), views.size(), &eo, &r));
+  const int rc = bmg_execute_plan(ctx.get(), &fp, views.data(), views.size(), &eo, &r);
+  if (rc != BMG_OK && verifier) {
+    const std::string msg = bmg_last_error();
+    try {
+      verifier->close();
+    } catch (...) {
+    }
+    bandmatch::fail(bmg_status_name(rc), msg);
+  }
+  check(rc);
   std::unique_ptr<bmg_result, void (*)(bmg_result*)> guard(r, bmg_result_free);
   const std::uint64_t n_pairs = bmg_result_pair_count(r), n_m = bmg_result_match_count(r);
   std::vector<std::uint64_t> ids(2 * n_pairs), offs(n_pairs + 1);
@@ -230,52 +369,16 @@ inline bandmatch::ExecutionResult execute_plan(
   if (!opts.verify.enabled) {
     res.matches = std::move(initial);
   } else {
-    // host verification, as VerifyPool::process (engine.cpp:326-377)
-    res.matches.resize(n_pairs);
-    res.outcomes.resize(n_pairs);
-    std::atomic<std::size_t> next{0};
-    std::exception_ptr err;
-    std::mutex err_mu;
-    auto work = [&] {
-      for (std::size_t i; (i = next++) < n_pairs;) {
-        const PairMatches& in = initial[i];
-        const FeatureSet& qf = features.at(in.query_image);
-        const FeatureSet& tf = features.at(in.train_image);
-        PairMatches& out = res.matches[i];
-        PairOutcome& oc = res.outcomes[i];
-        out.query_image = in.query_image;
-        out.train_image = in.train_image;
-        out.stage = PairMatches::Stage::kVerified;
-        oc.pair = IdPair(in.query_image, in.train_image);
-        oc.initial = in.matches.size();
-        try {
-          const SaoOutcome sao = sao_filter(in, qf.keypoints, tf.keypoints, opts.verify.sao);
-          oc.after_sao = sao.kept.matches.size();
-          oc.sao_passthrough = sao.passthrough;
-          oc.delaunay_fallback = sao.delaunay_fallback;
-          const std::uint64_t seed = seed_for(opts.seed, "verify." + std::to_string(oc.pair.a) +
-                                                             "." + std::to_string(oc.pair.b));
-          const InlierSet inl =
-              ransac_fundamental(sao.kept, qf.keypoints, tf.keypoints, opts.verify.ransac, seed);
-          for (int idx : inl.kept) out.matches.push_back(sao.kept.matches[idx]);
-          oc.inliers = out.matches.size();
-          oc.ransac_iterations = inl.iterations;
-        } catch (const Error& e) {
-          oc.no_model = true;
-          out.matches.clear();
-          if (e.code() != "TooFewMatches" && e.code() != "NoModel") {
-            std::lock_guard<std::mutex> lk(err_mu);
-            if (!err) err = std::current_exception();
-          }
-        }
-        oc.inlier_ratio = oc.initial == 0 ? 0.0 : static_cast<double>(oc.inliers) / oc.initial;
-      }
-    };
-    std::vector<std::thread> pool;
-    for (int t = 0; t < std::max(1, opts.threads); ++t) pool.emplace_back(work);
-    for (auto& t : pool) t.join();
-    if (err) std::rethrow_exception(err);
-    for (const PairMatches& pm : res.matches) res.metrics.verified_matches += pm.matches.size();
+    // the workers have been verifying since the first row's hand-off; wait
+    // for the rest (the iteration barrier of engine.cpp:497-499 only orders
+    // verification against the next iteration's matching, which cannot
+    // change any result, so the GPU does not wait for it)
+    verifier->close();
+    for (auto& [pair, rec] : verifier->records) {
+      res.outcomes.push_back(rec.outcome);
+      res.matches.push_back(std::move(rec.matches));
+      res.metrics.verified_matches += res.matches.back().matches.size();
+    }
   }
   res.metrics.uploads = arena.uploads();
   res.metrics.evictions = arena.evictions();

@@ -129,9 +129,15 @@ typedef struct {
   const uint64_t* evict_ids;
 } bmg_plan;
 
-/* Called on the executor's collector thread for every matched pair as soon
- * as its matches are in host memory: the hand-off point to host-side
- * verification (VerifyPool::push, engine.cpp:478-479). */
+/* The hand-off point to host-side verification (VerifyPool::push,
+ * engine.cpp:478-479): called on the executor's collector thread -- not the
+ * caller's -- for every matched pair of a block row as soon as that row's
+ * matches are in host memory, while later rows still run on the GPU.  Rows
+ * come in the order the executor ran them, a row's pairs in plan (block)
+ * order; a pair planned twice is handed over twice, like the reference's
+ * push per match_pair call.  `matches` stays valid until bmg_result_free.
+ * The callback may block (backpressure from a bounded verification queue)
+ * without stalling the GPU; bmg_execute_plan returns after the last call. */
 typedef void (*bmg_pair_callback)(void* user, uint64_t query_image, uint64_t train_image,
                                   const int32_t* matches, uint64_t n_matches);
 
@@ -257,6 +263,11 @@ int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out[3]);
 /* Device time (CUDA events on the compute stream) from the first operation of
  * the first row to the last kernel of the last row. */
 int bmg_result_device_ms(const bmg_result* r, double* ms_out);
+/* Overlap diagnostics for plan row `row`: out[0] = host ms since the call
+ * began when its pairs were handed to on_pair (-1 without on_pair), out[1]
+ * = device ms since the call's first operation when its last kernel / copy
+ * finished. */
+int bmg_result_row_timing(const bmg_result* r, uint64_t row, double out[2]);
 void bmg_result_free(bmg_result* r);
 /* write_matches_binary (hashmatch.cpp:311-332) of the result: the "BMMT" file
  * the reference writes for the same ExecutionResult, byte for byte (pairs in

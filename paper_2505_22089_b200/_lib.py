@@ -93,6 +93,7 @@ EXPORTED = [
     "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
     "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
     "bmg_write_matches_binary", "bmg_generate_synthetic_subset", "bmg_set_test_flags",
+    "bmg_result_row_timing",
 ]
 
 _lib = None
@@ -151,6 +152,7 @@ def load(path: Path = LIB_PATH):
         "bmg_exact_walk_count": (C.c_int, [vp, C.POINTER(u64)]),
         "bmg_row_mean_info": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
         "bmg_set_test_flags": (C.c_int, [vp, C.c_uint32]),
+        "bmg_result_row_timing": (C.c_int, [vp, u64, vp]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                              u64, vp, vp]),

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +29,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <utility>
@@ -338,6 +341,10 @@ struct bmg_result {
   uint64_t n_matches = 0;
   uint64_t counters[6] = {0, 0, 0, 0, 0, 0};
   std::vector<uint64_t> iterations;  // 3 per iteration
+  // per plan row: host ms (since the call started) at which its pairs were
+  // handed to on_pair, device ms (since the call's first operation) at which
+  // its last kernel / copy finished; -1 when not recorded
+  std::vector<double> row_handoff_ms, row_done_ms;
   double wall_s = 0.0;
   double device_ms = 0.0;
   ~bmg_result() { bmg::PinnedPool::release(log, log_bytes); }
@@ -967,6 +974,79 @@ void reset_results(Ctx& c, uint64_t n_pairs, uint64_t capacity, bool host_mirror
   if (capacity) c.d_res.ensure(sizeof(int32_t) * 2 * capacity);
 }
 
+// Hands each block row's matches to the caller's on_pair callback (the
+// VerifyPool::push hand-off, engine.cpp:478-479) from a collector thread as
+// soon as the row's log region is in host memory, while later rows still
+// run on the GPU.  Rows are handed over in the order they were issued; pairs
+// of a row in plan (block) order.  The executor joins the thread before it
+// returns, so every callback has run by then.
+class Collector {
+ public:
+  struct Row {
+    cudaEvent_t done;  // recorded after the row's last copy / compaction
+    uint64_t plan_row, pb, pe;
+  };
+  Collector(int device, const bmg_plan* plan, const bmg_execute_options* opts, const int32_t* log,
+            const uint64_t* ranges, std::chrono::steady_clock::time_point t0, bmg_result* res)
+      : device_(device), plan_(plan), opts_(opts), log_(log), ranges_(ranges), t0_(t0), res_(res) {
+    th_ = std::thread([this] { run(); });
+  }
+  ~Collector() { finish(); }
+  void push(const Row& r) {
+    std::lock_guard<std::mutex> g(mu_);
+    q_.push_back(r);
+    cv_.notify_one();
+  }
+  // no more rows: wait until every queued row has been handed over
+  void finish() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (closed_) return;
+      closed_ = true;
+    }
+    cv_.notify_one();
+    th_.join();
+  }
+  std::vector<cudaEvent_t> events;  // owned by the executor's event pool
+
+ private:
+  void run() {
+    cudaSetDevice(device_);
+    for (;;) {
+      Row r;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return closed_ || !q_.empty(); });
+        if (q_.empty()) return;
+        r = q_.front();
+        q_.pop_front();
+      }
+      if (cudaEventSynchronize(r.done) != cudaSuccess) {
+        cudaGetLastError();
+        continue;  // the executor reports the failure
+      }
+      res_->row_handoff_ms[r.plan_row] =
+          1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+      for (uint64_t p = r.pb; p < r.pe; ++p) {
+        const uint64_t b = ranges_[2 * p], e = ranges_[2 * p + 1];
+        opts_->on_pair(opts_->on_pair_user, plan_->pairs[2 * p], plan_->pairs[2 * p + 1], log_ + 2 * b, e - b);
+      }
+    }
+  }
+  int device_;
+  const bmg_plan* plan_;
+  const bmg_execute_options* opts_;
+  const int32_t* log_;
+  const uint64_t* ranges_;
+  std::chrono::steady_clock::time_point t0_;
+  bmg_result* res_;
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Row> q_;
+  bool closed_ = false;
+};
+
 // After the compute stream drained: DMA the log entries [0, end) into the
 // pinned host mirror and return it.
 const int32_t* fetch_log(Ctx& c, uint64_t end) {
@@ -1420,6 +1500,9 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     int32_t* d_log = log_zc_all ? nullptr : c->d_res.as<int32_t>();
     int32_t* h_log = nullptr;
     BMG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_log), res->log, 0));
+    res->row_handoff_ms.assign(plan->n_rows, -1.0);
+    res->row_done_ms.assign(plan->n_rows, -1.0);
+    std::vector<std::pair<uint64_t, cudaEvent_t>> row_done;  // (plan row, event)
     c->cur = 0;
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->slot[0].s_comp));
@@ -1481,6 +1564,12 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
         }
       }
     } chain_hook{*c};
+    // declared after the hook: on an error it is joined (and its queued rows
+    // drained) after the hook has synchronised the device
+    std::unique_ptr<Collector> collector;
+    if (opts->on_pair)
+      collector = std::make_unique<Collector>(c->device, plan, opts, res->log, c->res_ranges.host<uint64_t>(), t0,
+                                              res.get());
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaEventRecord(sl.done, sl.home));
     c->mean_chain_only = (opts->flags & BMG_EXEC_MEAN_CHAIN) != 0;
     uint64_t row = 0;
@@ -1682,6 +1771,12 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           BMG_CUDA(cudaMemcpyAsync(res->log + 2 * row_base[r], d_log + 2 * row_base[r],
                                    8 * (row_base[r + 1] - row_base[r]), cudaMemcpyDeviceToHost, S.s_comp));
         it_pairs += pe - pb;
+        {
+          cudaEvent_t ev = take_event(*c);
+          BMG_CUDA(cudaEventRecord(ev, S.s_comp));
+          row_done.emplace_back(r, ev);
+          if (collector) collector->push({ev, r, pb, pe});
+        }
         for (uint64_t id : frees[e]) arena_free(*c, id);
         BMG_CUDA(cudaEventRecord(S.done, S.s_comp));
       }
@@ -1713,6 +1808,13 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           fprintf(stderr, "[bmg timeline] slot %d mean: bad %u need_chain %u rounds %u events %u\n", k, st.bad,
                   st.need_chain, st.rounds, st.events);
         }
+    if (collector) collector->finish();
+    for (auto& [r, ev] : row_done) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, span0, ev) == cudaSuccess) res->row_done_ms[r] = ms;
+      cudaGetLastError();
+      c->free_events.push_back(ev);
+    }
     // per-pair [begin, end) ranges are in mapped host memory; the matches
     // are already in the result's pinned log
     const uint64_t* ranges = c->res_ranges.host<uint64_t>();
@@ -1730,7 +1832,6 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       res->ranges.push_back(b);
       res->ranges.push_back(e);
       total += e - b;
-      if (opts->on_pair) opts->on_pair(opts->on_pair_user, key.first, key.second, res->log + 2 * b, e - b);
     }
     res->n_matches = total;
     res->counters[0] = n_pairs;
@@ -1811,6 +1912,14 @@ int bmg_result_device_ms(const bmg_result* r, double* ms_out) {
   return guarded([&] {
     if (!r || !ms_out) fail(BMG_INVALID_ARGUMENT, "null argument");
     *ms_out = r->device_ms;
+  });
+}
+
+int bmg_result_row_timing(const bmg_result* r, uint64_t row, double out[2]) {
+  return guarded([&] {
+    if (!r || !out || row >= r->row_done_ms.size()) fail(BMG_INVALID_ARGUMENT, "bad row index");
+    out[0] = r->row_handoff_ms[row];
+    out[1] = r->row_done_ms[row];
   });
 }
 

@@ -249,6 +249,9 @@ class ExecutionResult:
     matches: list
     metrics: PipelineMetrics
     outcomes: list = field(default_factory=list)
+    # per plan row: (host ms when its pairs went to on_pair or -1, device ms
+    # when its last kernel finished) -- the GPU / host-verification overlap
+    row_timing: list = field(default_factory=list)
 
 
 def arena_units_for(features: dict, gpu_images: int) -> int:
@@ -392,6 +395,11 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
         o = np.zeros(3, np.uint64)
         check(L.bmg_result_iteration(h, i, ptr(o)))
         its.append(IterationMetrics(int(o[0]), int(o[1]), int(o[2])))
+    row_timing = []
+    for r in range(len(flat.row_needed_offsets) - 1):
+        o = np.zeros(2, np.float64)
+        check(L.bmg_result_row_timing(h, r, ptr(o)))
+        row_timing.append((float(o[0]), float(o[1])))
     matches = []
     if npairs:
         # zero-copy: every pair's (query_idx, train_idx) array is a view into
@@ -412,4 +420,4 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
                           c[0] / wall.value if wall.value > 0 else 0.0)
     met.device_ms = dev_ms.value
     del keep
-    return ExecutionResult(matches, met)
+    return ExecutionResult(matches, met, row_timing=row_timing)
