@@ -263,10 +263,10 @@ int bmg_result_iteration(const bmg_result* r, uint64_t i, uint64_t out[3]);
 /* Device time (CUDA events on the compute stream) from the first operation of
  * the first row to the last kernel of the last row. */
 int bmg_result_device_ms(const bmg_result* r, double* ms_out);
-/* Overlap diagnostics for plan row `row`: out[0] = host ms since the call
- * began when its pairs were handed to on_pair (-1 without on_pair), out[1]
- * = device ms since the call's first operation when its last kernel / copy
- * finished. */
+/* Overlap diagnostics for plan row `row`, both in ms since the call's first
+ * device operation was issued (host and device clocks aligned to within the
+ * launch latency): out[0] = when its pairs were handed to on_pair (-1
+ * without on_pair), out[1] = when its last kernel / copy finished. */
 int bmg_result_row_timing(const bmg_result* r, uint64_t row, double out[2]);
 void bmg_result_free(bmg_result* r);
 /* write_matches_binary (hashmatch.cpp:311-332) of the result: the "BMMT" file

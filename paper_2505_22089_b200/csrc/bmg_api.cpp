@@ -341,9 +341,9 @@ struct bmg_result {
   uint64_t n_matches = 0;
   uint64_t counters[6] = {0, 0, 0, 0, 0, 0};
   std::vector<uint64_t> iterations;  // 3 per iteration
-  // per plan row: host ms (since the call started) at which its pairs were
-  // handed to on_pair, device ms (since the call's first operation) at which
-  // its last kernel / copy finished; -1 when not recorded
+  // per plan row: host ms at which its pairs were handed to on_pair, device
+  // ms at which its last kernel / copy finished, both since the call's first
+  // device operation was issued; -1 when not recorded
   std::vector<double> row_handoff_ms, row_done_ms;
   double wall_s = 0.0;
   double device_ms = 0.0;
@@ -763,9 +763,7 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
 
 // ---- matching ---------------------------------------------------------------
 
-struct MatchPlan {
-  int chunk = kMatchThreads;
-};
+
 
 void check_match_params(const Ctx& c, const bmg_match_params& mp) {
   if (mp.k_nearest < 1) fail(BMG_INVALID_ARGUMENT, "k_nearest must be >= 1");
@@ -1506,6 +1504,10 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     c->cur = 0;
     cudaEvent_t span0 = take_event(*c), span1 = take_event(*c);
     BMG_CUDA(cudaEventRecord(span0, c->slot[0].s_comp));
+    // host origin of the row hand-off times: the moment span0 was issued to
+    // the (idle) stream, so host and device times share an origin to within
+    // the launch latency
+    const auto t_span0 = std::chrono::steady_clock::now();
     BMG_CUDA(cudaStreamWaitEvent(c->s_copy, span0, 0));
     for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamWaitEvent(ps, span0, 0));
     BMG_CUDA(cudaStreamWaitEvent(c->slot[1].s_comp, span0, 0));
@@ -1568,8 +1570,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
     // drained) after the hook has synchronised the device
     std::unique_ptr<Collector> collector;
     if (opts->on_pair)
-      collector = std::make_unique<Collector>(c->device, plan, opts, res->log, c->res_ranges.host<uint64_t>(), t0,
-                                              res.get());
+      collector = std::make_unique<Collector>(c->device, plan, opts, res->log, c->res_ranges.host<uint64_t>(),
+                                              t_span0, res.get());
     for (RowSlot& sl : c->slot) BMG_CUDA(cudaEventRecord(sl.done, sl.home));
     c->mean_chain_only = (opts->flags & BMG_EXEC_MEAN_CHAIN) != 0;
     uint64_t row = 0;

@@ -136,6 +136,7 @@ void launch_codes_fixup(const HashDev& h, const ImgDev* imgs_dev, int n_imgs, co
 int launch_tables(const HashDev& h, const ImgDev* imgs_dev, const uint32_t* tile_img,
                   const uint32_t* tile_start, int n_tiles, int n_imgs, cudaStream_t s);  // returns launches
 void launch_match(const MatchLaunch& a, int fwp, int n_work, cudaStream_t s);
+
 void launch_scan_counts(const uint32_t* counts, int n, uint64_t* ranges_out, uint64_t base, cudaStream_t s);
 void launch_compact(const int32_t* dense, const uint64_t* dense_off, const uint32_t* nq,
                     const uint64_t* out_off, int n_pairs, int32_t* out, cudaStream_t s);

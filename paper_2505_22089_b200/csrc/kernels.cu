@@ -1496,6 +1496,187 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   }
 }
 
+// Euclidean re-rank + ratio test of query q (hashmatch.cpp:196-208), warp-
+// wide: lane r < kept holds the query's r-th key (hamming << ib | train idx,
+// ascending).  Returns the matched train index or -1.
+//   lanes hold dims 4l..4l+3 of the query and of every kept candidate; FP32
+//   squared distances (packed FP32x2 ops) with a certified relative error
+//   decide the (dist, idx) argmin and the ratio test; uncertified queries
+//   rerun the reference's sequential FP64 euclidean (:35-42) lane-per-candidate.
+template <int KM>
+__device__ __forceinline__ int32_t rerank_query(const MatchLaunch& a, const ImgDev& Q, const ImgDev& T,
+                                                uint32_t q, uint32_t lst, int kept, uint32_t idx_mask) {
+  const int lane = threadIdx.x & 31;
+  const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
+  const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
+  const double ratio = a.ratio;
+  const float r2f = (float)(ratio * ratio);
+  int32_t result = -1;
+  if (kept == 1) {
+    result = (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask);
+  } else if (kept > 1) {
+    const bool mine = lane < kept;
+    const uint32_t my_idx = lst & idx_mask;
+    float s_min, s_2;
+    uint32_t i_min;
+    if constexpr (KM == 8) {
+      const int ck = lane >> 2, part = lane & 3;
+      const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
+      const float2 neg1 = make_float2(-1.f, -1.f);
+      // lane l holds dims 4l..4l+3 of the query and of every kept
+      // candidate (one coalesced 512-byte row per candidate); a
+      // transpose-reduce over lane bits 4, 3, 2 then two xor steps leave
+      // candidate c's sum in lanes 4c..4c+3.  Depth <= 3 + 5 per sum:
+      // relative error ~1e-6.
+      const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
+      float pt[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        pt[c] = 0.f;
+        const uint32_t jc = __shfl_sync(kFull, my_idx, c);
+        if (c < kept) {
+          const float4 tv = __ldg(Td + (size_t)jc * 32 + lane);
+          const float2 d0 = __ffma2_rn(make_float2(tv.x, tv.y), neg1, make_float2(qv.x, qv.y));
+          const float2 d1 = __ffma2_rn(make_float2(tv.z, tv.w), neg1, make_float2(qv.z, qv.w));
+          const float2 p2 = __ffma2_rn(d1, d1, __fmul2_rn(d0, d0));
+          pt[c] = p2.x + p2.y;
+        }
+      }
+#pragma unroll
+      for (int st = 0; st < 3; ++st) {
+        const int half = 4 >> st, msk = 16 >> st;
+        const bool up = (lane & msk) != 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < half) {
+            const float send = up ? pt[i] : pt[i + half];
+            const float keep = up ? pt[i + half] : pt[i];
+            pt[i] = keep + __shfl_xor_sync(kFull, send, msk);
+          }
+        }
+      }
+      float s = pt[0];
+      s += __shfl_xor_sync(kFull, s, 2);
+      s += __shfl_xor_sync(kFull, s, 1);
+      // squared distances are >= 0 (or NaN, caught by `finite`): their
+      // bit patterns order like the values, so REDUX finds the (s, idx)
+      // argmin and the runner-up
+      const bool lead = part == 0 && ck < kept;
+      const uint32_t sb = lead ? __float_as_uint(s) : kEmpty;
+      const uint32_t mb = __reduce_min_sync(kFull, sb);
+      i_min = __reduce_min_sync(kFull, (lead && sb == mb) ? jk : kEmpty);
+      s_min = __uint_as_float(mb);
+      s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
+    } else {
+      const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
+      float part[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const uint32_t jk = __shfl_sync(kFull, lst, k) & idx_mask;
+        part[k] = 0.f;
+        if (k < kept) {
+          const float4 tv = __ldg(Td + (size_t)jk * 32 + lane);
+          const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
+          part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+        }
+      }
+      // transpose-reduce: after log2(KM) halving steps the lane whose bits
+      // (4, 3, .., 5-log2 KM) spell k holds candidate k's partial sum
+      constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
+#pragma unroll
+      for (int st = 0; st < kLog; ++st) {
+        const int half = (KM >> st) >> 1, m = 16 >> st;
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < KM / 2; ++i) {
+          if (i < half) {
+            const float send = up ? part[i] : part[i + half];
+            const float keep = up ? part[i + half] : part[i];
+            part[i] = keep + __shfl_xor_sync(kFull, send, m);
+          }
+        }
+      }
+      float red = part[0];
+#pragma unroll
+      for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
+      int src_lane = 0;
+#pragma unroll
+      for (int b = 0; b < kLog; ++b)
+        if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
+      const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
+      // argmin of (s, idx) and runner-up value over lanes < kept
+      float bs = mine ? s_own : __int_as_float(0x7f800000);
+      uint32_t bi = mine ? my_idx : 0xffffffffu;
+#pragma unroll
+      for (int o = KM / 2; o > 0; o >>= 1) {
+        const float os = __shfl_xor_sync(kFull, bs, o);
+        const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
+        if (os < bs || (os == bs && oi < bi)) {
+          bs = os;
+          bi = oi;
+        }
+      }
+      s_min = __shfl_sync(kFull, bs, 0);
+      i_min = __shfl_sync(kFull, bi, 0);
+      float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
+#pragma unroll
+      for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
+      s_2 = __shfl_sync(kFull, s2, 0);
+    }
+    // certified in FP32: the distances carry relative error < 1e-6, each
+    // product below 2^-24 and r2f its own 2^-24, all far inside the 2e-5
+    // margins (ties d1 == r^2 d2 land in the FP64 band, which rejects them)
+    // Accept also needs the argmin itself certified (s_min clearly below
+    // s_2): with ratio > 1 a near tie passes the ratio margin, and the FP32
+    // argmin could then differ from the reference's FP64 (dist, idx) first.
+    // ratio <= 0 or NaN: d1 < d2 * ratio never holds (hashmatch.cpp:47-49),
+    // so only lone candidates are kept.
+    const float c_hi = 1.0f + 2.0e-5f, c_lo = 1.0f - 2.0e-5f;
+    const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
+    const bool rpos = ratio > 0.0;
+    const bool fast = (a.test_flags & kTestForceFp64Rerank) == 0;
+    const bool accept = fast && rpos && finite && s_min * c_hi < r2f * s_2 && s_min * c_hi < s_2;
+    const bool reject = fast && (!rpos || (finite && s_min * c_lo >= (r2f * s_2) * c_hi));
+    if (accept) {
+      result = (int32_t)i_min;
+    } else if (!reject) {
+      // FP64 reference path (hashmatch.cpp:35-42, :196-208)
+      double e = __longlong_as_double(0x7ff0000000000000ll);
+      if (mine) {
+        const float* qd = Q.desc + (size_t)q * kDim;
+        const float* td = T.desc + (size_t)my_idx * kDim;
+        double s = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < kDim; ++c) {
+          const double d = __dsub_rn((double)__ldg(qd + c), (double)__ldg(td + c));
+          s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+        e = __dsqrt_rn(s);
+      }
+      double be = e;
+      uint32_t bj = mine ? my_idx : 0xffffffffu;
+#pragma unroll
+      for (int o = KM / 2; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(kFull, be, o);
+        const uint32_t oj = __shfl_xor_sync(kFull, bj, o);
+        if (oe < be || (oe == be && oj < bj)) {
+          be = oe;
+          bj = oj;
+        }
+      }
+      const double e_first = __shfl_sync(kFull, be, 0);
+      const uint32_t i_first = __shfl_sync(kFull, bj, 0);
+      double e2 = (mine && my_idx != i_first) ? e : __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+      for (int o = KM / 2; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(kFull, e2, o));
+      const double e_second = __shfl_sync(kFull, e2, 0);
+      if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
+      if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
+    }
+  }
+  return result;
+}
+
 template <int FWP, int KM, int NT, int KC>
 __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   const PairWork w = a.work[blockIdx.x];
@@ -1507,11 +1688,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
   const int L = a.tables, K = KC ? KC : a.k, ib = a.idx_bits;
   const uint32_t idx_mask = (1u << ib) - 1u;
   const int nb1 = a.n_buckets + 1;
-  const float4* __restrict__ Qd = reinterpret_cast<const float4*>(Q.desc);
-  const float4* __restrict__ Td = reinterpret_cast<const float4*>(T.desc);
-  const double ratio = a.ratio;
-  const double r2 = ratio * ratio;
-  const float r2f = (float)r2;
   uint32_t n_matched = 0;
 
   auto emit = [&](uint32_t q, int32_t result) {
@@ -1521,171 +1697,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
     }
   };
   auto finish = [&](uint32_t q, uint32_t lst, int kept) {
-    int32_t result = -1;
-    if (kept == 1) {
-      result = (int32_t)(__shfl_sync(kFull, lst, 0) & idx_mask);
-    } else if (kept > 1) {
-      const bool mine = lane < kept;
-      const uint32_t my_idx = lst & idx_mask;
-      float s_min, s_2;
-      uint32_t i_min;
-      if constexpr (KM == 8) {
-        // lane l holds dims 4l..4l+3 of the query and of every kept
-        // candidate (one coalesced 512-byte row per candidate); a transpose-reduce over lane bits 4, 3, 2
-        // then two xor steps leave candidate c's sum in lanes 4c..4c+3.
-        // FP32 squared distances (packed FP32x2 ops), depth <= 3 + 5 per sum:
-        // relative error ~1e-6, inside the certification margin below.
-        const int ck = lane >> 2, part = lane & 3;
-        const uint32_t jk = __shfl_sync(kFull, my_idx, ck);
-        const float2 neg1 = make_float2(-1.f, -1.f);
-        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
-        float pt[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          pt[c] = 0.f;
-          const uint32_t jc = __shfl_sync(kFull, my_idx, c);
-          if (c < kept) {
-            const float4 tv = __ldg(Td + (size_t)jc * 32 + lane);
-            // d = q - t exactly rounded (t * -1 + q), then d * d summed
-            const float2 d0 = __ffma2_rn(make_float2(tv.x, tv.y), neg1, make_float2(qv.x, qv.y));
-            const float2 d1 = __ffma2_rn(make_float2(tv.z, tv.w), neg1, make_float2(qv.z, qv.w));
-            const float2 p2 = __ffma2_rn(d1, d1, __fmul2_rn(d0, d0));
-            pt[c] = p2.x + p2.y;
-          }
-        }
-#pragma unroll
-        for (int st = 0; st < 3; ++st) {
-          const int half = 4 >> st, msk = 16 >> st;
-          const bool up = (lane & msk) != 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (i < half) {
-              const float send = up ? pt[i] : pt[i + half];
-              const float keep = up ? pt[i + half] : pt[i];
-              pt[i] = keep + __shfl_xor_sync(kFull, send, msk);
-            }
-          }
-        }
-        float s = pt[0];
-        s += __shfl_xor_sync(kFull, s, 2);
-        s += __shfl_xor_sync(kFull, s, 1);
-        // squared distances are >= 0 (or NaN, caught by `finite`): their
-        // bit patterns order like the values, so REDUX finds the (s, idx)
-        // argmin and the runner-up
-        const bool lead = part == 0 && ck < kept;
-        const uint32_t sb = lead ? __float_as_uint(s) : kEmpty;
-        const uint32_t mb = __reduce_min_sync(kFull, sb);
-        i_min = __reduce_min_sync(kFull, (lead && sb == mb) ? jk : kEmpty);
-        s_min = __uint_as_float(mb);
-        s_2 = __uint_as_float(__reduce_min_sync(kFull, (lead && jk != i_min) ? sb : kEmpty));
-      } else {
-        const float4 qv = __ldg(Qd + (size_t)q * 32 + lane);
-        float part[KM];
-#pragma unroll
-        for (int k = 0; k < KM; ++k) {
-          const uint32_t jk = __shfl_sync(kFull, lst, k) & idx_mask;
-          part[k] = 0.f;
-          if (k < kept) {
-            const float4 tv = __ldg(Td + (size_t)jk * 32 + lane);
-            const float dx = qv.x - tv.x, dy = qv.y - tv.y, dz = qv.z - tv.z, dw = qv.w - tv.w;
-            part[k] = fmaf(dw, dw, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-          }
-        }
-        // transpose-reduce: after log2(KM) halving steps the lane whose bits
-        // (4, 3, .., 5-log2 KM) spell k holds candidate k's partial sum
-        constexpr int kLog = KM == 8 ? 3 : (KM == 16 ? 4 : 5);
-#pragma unroll
-        for (int st = 0; st < kLog; ++st) {
-          const int half = (KM >> st) >> 1, m = 16 >> st;
-          const bool up = (lane & m) != 0;
-#pragma unroll
-          for (int i = 0; i < KM / 2; ++i) {
-            if (i < half) {
-              const float send = up ? part[i] : part[i + half];
-              const float keep = up ? part[i + half] : part[i];
-              part[i] = keep + __shfl_xor_sync(kFull, send, m);
-            }
-          }
-        }
-        float red = part[0];
-#pragma unroll
-        for (int m = 16 >> kLog; m > 0; m >>= 1) red += __shfl_xor_sync(kFull, red, m);
-        int src_lane = 0;
-#pragma unroll
-        for (int b = 0; b < kLog; ++b)
-          if (lane & (1 << b)) src_lane |= 1 << (4 - (kLog - 1 - b));
-        const float s_own = __shfl_sync(kFull, red, src_lane);  // lane k: candidate k
-        // argmin of (s, idx) and runner-up value over lanes < kept
-        float bs = mine ? s_own : __int_as_float(0x7f800000);
-        uint32_t bi = mine ? my_idx : 0xffffffffu;
-#pragma unroll
-        for (int o = KM / 2; o > 0; o >>= 1) {
-          const float os = __shfl_xor_sync(kFull, bs, o);
-          const uint32_t oi = __shfl_xor_sync(kFull, bi, o);
-          if (os < bs || (os == bs && oi < bi)) {
-            bs = os;
-            bi = oi;
-          }
-        }
-        s_min = __shfl_sync(kFull, bs, 0);
-        i_min = __shfl_sync(kFull, bi, 0);
-        float s2 = (mine && my_idx != i_min) ? s_own : __int_as_float(0x7f800000);
-#pragma unroll
-        for (int o = KM / 2; o > 0; o >>= 1) s2 = fminf(s2, __shfl_xor_sync(kFull, s2, o));
-        s_2 = __shfl_sync(kFull, s2, 0);
-      }
-      // certified in FP32: the distances carry relative error < 1e-6, each
-      // product below 2^-24 and r2f its own 2^-24, all far inside the 2e-5
-      // margins (ties d1 == r^2 d2 land in the FP64 band, which rejects them)
-      // Accept also needs the argmin itself certified (s_min clearly below
-      // s_2): with ratio > 1 a near tie passes the ratio margin, and the FP32
-      // argmin could then differ from the reference's FP64 (dist, idx) first.
-      // ratio <= 0 or NaN: d1 < d2 * ratio never holds (hashmatch.cpp:47-49),
-      // so only lone candidates are kept.
-      const float c_hi = 1.0f + 2.0e-5f, c_lo = 1.0f - 2.0e-5f;
-      const bool finite = s_min >= 1.0e-30f && s_2 < 3.0e38f;
-      const bool rpos = ratio > 0.0;
-      const bool fast = (a.test_flags & kTestForceFp64Rerank) == 0;
-      const bool accept = fast && rpos && finite && s_min * c_hi < r2f * s_2 && s_min * c_hi < s_2;
-      const bool reject = fast && (!rpos || (finite && s_min * c_lo >= (r2f * s_2) * c_hi));
-      if (accept) {
-        result = (int32_t)i_min;
-      } else if (!reject) {
-        // FP64 reference path (hashmatch.cpp:35-42, :196-208)
-        double e = __longlong_as_double(0x7ff0000000000000ll);
-        if (mine) {
-          const float* qd = Q.desc + (size_t)q * kDim;
-          const float* td = T.desc + (size_t)my_idx * kDim;
-          double s = 0.0;
-#pragma unroll 8
-          for (int c = 0; c < kDim; ++c) {
-            const double d = __dsub_rn((double)__ldg(qd + c), (double)__ldg(td + c));
-            s = __dadd_rn(s, __dmul_rn(d, d));
-          }
-          e = __dsqrt_rn(s);
-        }
-        double be = e;
-        uint32_t bj = mine ? my_idx : 0xffffffffu;
-#pragma unroll
-        for (int o = KM / 2; o > 0; o >>= 1) {
-          const double oe = __shfl_xor_sync(kFull, be, o);
-          const uint32_t oj = __shfl_xor_sync(kFull, bj, o);
-          if (oe < be || (oe == be && oj < bj)) {
-            be = oe;
-            bj = oj;
-          }
-        }
-        const double e_first = __shfl_sync(kFull, be, 0);
-        const uint32_t i_first = __shfl_sync(kFull, bj, 0);
-        double e2 = (mine && my_idx != i_first) ? e : __longlong_as_double(0x7ff0000000000000ll);
-#pragma unroll
-        for (int o = KM / 2; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(kFull, e2, o));
-        const double e_second = __shfl_sync(kFull, e2, 0);
-        if (e_first < __dmul_rn(e_second, ratio)) result = (int32_t)i_first;
-        if (lane == 0 && a.exact_queries) atomicAdd(a.exact_queries, 1ull);
-      }
-    }
-    emit(q, result);
+    emit(q, rerank_query<KM>(a, Q, T, q, lst, kept, idx_mask));
   };
 
   // the next query's bucket ids are loaded two queries ahead and its bucket
@@ -1726,6 +1738,7 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
         for (int i = kLaneKeys - 1; i > 0; --i) kl[i] = max(kl[i - 1], min(kl[i], key));
         kl[0] = min(kl[0], key);
       });
+      uint32_t m = kEmpty;
       // Copies of one key that landed in one lane sit next to each other:
       // squeeze them out so a lane's list is a prefix of its distinct keys.
       // Copies in different lanes are popped together below.
@@ -1749,7 +1762,6 @@ __global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
       // key below the last pull (it may be missing from the lists; a dropped
       // copy of a listed key also counts): then the query reruns on the
       // exact path below.
-      uint32_t m = kEmpty;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         if (r < K) {

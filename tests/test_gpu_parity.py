@@ -37,15 +37,6 @@ def flat_of(res):
     return multigpu.result_flat(res)
 
 
-def assert_same(gpu, ref):
-    gi, go, gm = gpu
-    ri, ro, rm = ref
-    assert np.array_equal(gi, ri)
-    for p in range(len(ri)):
-        assert np.array_equal(gm[go[p]:go[p + 1]], rm[ro[p]:ro[p + 1]]), tuple(ri[p])
-    assert np.array_equal(go, ro)
-
-
 # ---- (a) config 2 at full size ---------------------------------------------
 def test_config2_full_size_equals_reference(reference):
     table = reference.synth_features(43, 8192, 11, 0.02, 0.2, 7, drop=11)
@@ -156,7 +147,7 @@ def test_degenerate_ratios_keep_only_what_the_reference_keeps(oracle, ratio):
 
 # ---- (d) other hash shapes through matching ----------------------------------
 @pytest.mark.parametrize("params", [(6, 8, 64), (6, 8, 200), (6, 8, 300), (3, 8, 1024), (6, 13, 128),
-                                    (4, 16, 64), (2, 12, 1)])
+                                    (4, 16, 64), (2, 12, 1), (12, 6, 128)])
 def test_match_with_other_hash_shapes(oracle, params):
     p = HashParams(*params)
     hf = bm.make_hash_functions(77, p)
@@ -170,7 +161,7 @@ def test_match_with_other_hash_shapes(oracle, params):
     tc = bm.compute_codes(tf, hf, mean)
     oq = oracle.compute_codes(q, hf.coarse, hf.fine, mean)
     assert np.array_equal(qc.coarse, oq[0]) and np.array_equal(qc.fine, oq[1])
-    for k in (8, 3):
+    for k in (8, 3, 1):
         got = bm.match_pair(qf, qc, tf, tc, MatchParams(k, 0.7), hf=hf)
         ref = oracle.match_pair(q, (qc.coarse, qc.fine), base, (tc.coarse, tc.fine), params, k, 0.7)
         assert np.array_equal(got.matches, ref), k

@@ -1,5 +1,7 @@
 // Microbenchmarks for design decisions on B200 (sm_100a): FP64 add latency,
 // POPC / FP64 / FP32 throughput, L2 random-gather bandwidth, H2D bandwidth.
+// The last stdout line is a JSON object of the peaks (profiles/r2_microbench.json;
+// bench.py's roofline.popc / roofline.l2_gather denominators).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench microbench.cu
 #include <cstdio>
 #include <cstdint>
@@ -69,6 +71,21 @@ __global__ void gather512(const float4* __restrict__ buf, uint32_t rows_mask, fl
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// 32-bit POPC throughput: 8 independent streams, one LOP3 + POPC + IADD each
+__global__ void popc_pure(const uint32_t* in, uint32_t* out, int n) {
+  uint32_t x[8], a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { x[k] = in[threadIdx.x + k]; a[k] = 0; }
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { a[k] += __popc(x[k] ^ (uint32_t)i); }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
   printf("device %s sms %d l2 %d MB smemPerBlockOptin %zu clock %d kHz\n", p.name, p.multiProcessorCount,
@@ -85,6 +102,13 @@ int main() {
          ms * 1e6 / n * p.clockRate / 1e6, p.clockRate / 1e3);
   uint32_t* du; CK(cudaMalloc(&du, 64 << 20)); CK(cudaMemset(du, 1, 64 << 20));
   int blocks = p.multiProcessorCount * 8, threads = 256, it = 4096;
+  double popc_pure_rate = 0, gather16_l2 = 0, gather16_hbm = 0, gather512_l2 = 0, dadd_rate = 0;
+  popc_pure<<<blocks, threads>>>(du, du + 1024, 16); cudaDeviceSynchronize();
+  cudaEventRecord(e0); popc_pure<<<blocks, threads>>>(du, du + 1024, it); cudaEventRecord(e1); cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  popc_pure_rate = 8.0 * blocks * threads * it / (ms * 1e-3);
+  printf("popc pure: %.3f ms, %.2f Tpopc/s -> %.1f per SM per clk\n", ms, popc_pure_rate / 1e12,
+         popc_pure_rate / p.multiProcessorCount / (p.clockRate * 1e3));
   popc_tp<<<blocks, threads>>>(du, du + 1024, 16); cudaDeviceSynchronize();
   cudaEventRecord(e0); popc_tp<<<blocks, threads>>>(du, du + 1024, it); cudaEventRecord(e1); cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
@@ -94,6 +118,7 @@ int main() {
   cudaEventRecord(e0); dfma_tp<<<blocks, threads>>>(dd, it); cudaEventRecord(e1); cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
   double ops = 8.0 * blocks * threads * it;
+  dadd_rate = ops / (ms * 1e-3);
   printf("dadd tp: %.3f ms, %.2f Tops/s -> %.1f per SM per clk\n", ms, ops / ms / 1e9,
          ops / (ms * 1e-3) / p.multiProcessorCount / (p.clockRate * 1e3));
   float* df; CK(cudaMalloc(&df, 64 << 20));
@@ -111,6 +136,8 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double bytes = 16.0 * blocks * 4 * threads * gi;
     printf("gather16 over %zu MB: %.3f ms, %.1f GB/s (useful bytes)\n", (size_t(16) << lg) >> 20, ms, bytes / ms / 1e6);
+    if (lg == 22) gather16_l2 = bytes / ms / 1e6;
+    if (lg == 26) gather16_hbm = bytes / ms / 1e6;
   }
   for (int lg : {13, 15, 17, 21}) {  // rows of 512 B
     uint32_t mask = (1u << lg) - 1;
@@ -120,6 +147,7 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double bytes = 512.0 * (blocks * 4 * threads / 32) * gi;
     printf("gather512 over %zu MB: %.3f ms, %.1f GB/s\n", (size_t(512) << lg) >> 20, ms, bytes / ms / 1e6);
+    if (lg == 15) gather512_l2 = bytes / ms / 1e6;
   }
   // H2D pinned
   void* h; size_t hb = size_t(256) << 20; CK(cudaMallocHost(&h, hb)); memset(h, 1, hb);
@@ -134,5 +162,8 @@ int main() {
   cudaEventRecord(e0); CK(cudaMemcpy(big, pg.data(), hb, cudaMemcpyHostToDevice)); cudaEventRecord(e1); cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
   printf("H2D pageable 256MB: %.2f GB/s\n", hb / ms / 1e6);
+  printf("{\"popc32_per_s\": %.6g, \"dadd_per_s\": %.6g, \"gather16_l2_gbs\": %.6g, \"gather16_hbm_gbs\": %.6g, "
+         "\"gather512_l2_gbs\": %.6g, \"sms\": %d, \"clock_khz\": %d}\n",
+         popc_pure_rate, dadd_rate, gather16_l2, gather16_hbm, gather512_l2, p.multiProcessorCount, p.clockRate);
   return 0;
 }
