@@ -244,6 +244,24 @@ int bmg_match_pair(bmg_context* ctx, const float* qdesc, const bmg_code_set* qc,
 int bmg_execute_plan(bmg_context* ctx, const bmg_plan* plan, const bmg_feature_view* features,
                      uint64_t n_features, const bmg_execute_options* options,
                      bmg_result** out);
+/* A feature file (the "BMF1" layout of write_features, features.cpp:199-220)
+ * as the source of an image: execute_plan reads it when the image uploads
+ * -- the header checked like read_features (features.cpp:222-236), the
+ * records read in blocks by host threads and de-interleaved straight into
+ * pinned staging slots that the copy engine moves to HBM -- so the feature
+ * map of a large plan need not sit in host memory (
+ * load_features_dir, bandmatch_cli.cpp:56-74, reads everything up front).
+ * `count` is the file's feature count (bmg_read_features_header); a file
+ * that disagrees fails with InvalidArgument, a damaged one with the
+ * reference's FormatError / TruncatedFile. */
+typedef struct {
+  uint64_t image_id;
+  const char* path;
+  uint64_t count;
+} bmg_feature_file;
+int bmg_execute_plan_files(bmg_context* ctx, const bmg_plan* plan, const bmg_feature_file* files,
+                           uint64_t n_files, const bmg_execute_options* options, bmg_result** out);
+
 /* ExecutionResult accessors: pairs sorted by IdPair (engine.cpp:506-512). */
 uint64_t bmg_result_pair_count(const bmg_result* r);
 uint64_t bmg_result_match_count(const bmg_result* r);

@@ -53,6 +53,10 @@ class FeatureViewC(C.Structure):
     _fields_ = [("image_id", C.c_uint64), ("descriptors", C.c_void_p), ("count", C.c_uint64)]
 
 
+class FeatureFileC(C.Structure):
+    _fields_ = [("image_id", C.c_uint64), ("path", C.c_char_p), ("count", C.c_uint64)]
+
+
 class ArenaStatsC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("capacity", "occupancy", "peak_occupancy", "uploads",
                                           "evictions", "units_uploaded", "resident_count")]
@@ -93,7 +97,7 @@ EXPORTED = [
     "bmg_generate_synthetic", "bmg_result_device_ms", "bmg_row_mean_info", "bmg_result_view",
     "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
     "bmg_write_matches_binary", "bmg_generate_synthetic_subset", "bmg_set_test_flags",
-    "bmg_result_row_timing",
+    "bmg_result_row_timing", "bmg_execute_plan_files",
 ]
 
 _lib = None
@@ -153,6 +157,8 @@ def load(path: Path = LIB_PATH):
         "bmg_row_mean_info": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
         "bmg_set_test_flags": (C.c_int, [vp, C.c_uint32]),
         "bmg_result_row_timing": (C.c_int, [vp, u64, vp]),
+        "bmg_execute_plan_files": (C.c_int, [vp, C.POINTER(PlanC), vp, u64, C.POINTER(ExecOptionsC),
+                                             C.POINTER(vp)]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                              u64, vp, vp]),

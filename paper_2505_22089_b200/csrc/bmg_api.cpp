@@ -12,8 +12,12 @@
 //     without host synchronisation; execute_plan reads it back once.
 // No exception crosses the ABI: every entry point returns a bmg_status.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -22,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -167,6 +172,90 @@ struct PinnedRing {
   }
 };
 
+// Fork-join pool of host threads for the staging copies: pageable
+// descriptors memcpy'd into pinned slots, feature files read and
+// de-interleaved into them (one thread of the caller plus workers).
+class HostPool {
+ public:
+  explicit HostPool(int threads) {
+    for (int i = 1; i < threads; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // fn(i) for i in [0, n) on the workers and the caller; returns when all ran
+  template <typename F>
+  void run(int n, F&& fn) {
+    std::function<void(int)> job(std::forward<F>(fn));
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &job;
+      n_ = n;
+      next_.store(0);
+      pending_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work(&job, n);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void work(const std::function<void(int)>* job, int n) {
+    for (int i; (i = next_.fetch_add(1)) < n;) {
+      (*job)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      int n;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+        n = n_;
+      }
+      work(job, n);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, pending_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+int host_threads() {
+  if (const char* v = getenv("BMG_HOST_THREADS")) return std::max(1, atoi(v));
+  const unsigned hc = std::thread::hardware_concurrency();
+  return static_cast<int>(std::clamp(hc > 2 ? hc - 2 : 1u, 1u, 16u));
+}
+
+// Where an image's descriptors come from: a host array (pinned or pageable)
+// or a feature file (features.cpp:199-249 layout), read when it uploads.
+struct Source {
+  const float* desc = nullptr;
+  const char* path = nullptr;
+  uint64_t count = 0;
+};
+
 struct ArenaImage {
   float* d = nullptr;         // [n][128] descriptors, then proj [n][proj_stride], dnorm [n]
   float* proj = nullptr;
@@ -310,10 +399,14 @@ struct bmg_context {
   // projection-ready events the current row's codes must wait for (set by
   // bmg_execute_plan: the row's mean only needs the copies)
   std::vector<cudaEvent_t> proj_waits;
-  char* stage[2] = {nullptr, nullptr};
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // pinned staging slots for pageable / file sources: slot k is refilled
+  // (by the host pool) once the DMA that last read it has finished
+  static constexpr int kStageSlots = 4;
+  char* stage[kStageSlots] = {};
+  cudaEvent_t stage_ev[kStageSlots] = {};
   int stage_i = 0;
   size_t stage_bytes = 0;
+  std::unique_ptr<bmg::HostPool> host;
   bmg::PinnedRing ring;
   // result log (compacted per row into its own region of d_res) and the
   // per-pair [begin, end) ranges, written by the scan kernels straight into
@@ -430,6 +523,24 @@ int bit_width(uint32_t v) {
 
 // ---- arena ----------------------------------------------------------------
 
+HostPool& host_pool(Ctx& c) {
+  if (!c.host) c.host = std::make_unique<HostPool>(host_threads());
+  return *c.host;
+}
+
+// the next staging slot, once the DMA that last read it has finished
+char* next_slot(Ctx& c, int* i) {
+  *i = c.stage_i;
+  c.stage_i = (c.stage_i + 1) % bmg_context::kStageSlots;
+  BMG_CUDA(cudaEventSynchronize(c.stage_ev[*i]));
+  return c.stage[*i];
+}
+
+void slot_dma(Ctx& c, int i, void* dst, size_t bytes) {
+  BMG_CUDA(cudaMemcpyAsync(dst, c.stage[i], bytes, cudaMemcpyHostToDevice, c.s_copy));
+  BMG_CUDA(cudaEventRecord(c.stage_ev[i], c.s_copy));
+}
+
 void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
   cudaPointerAttributes attr{};
   const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
@@ -439,31 +550,97 @@ void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
     if (bytes) BMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.s_copy));
     return;
   }
-  // pageable: chunk through two pinned buffers so the host memcpy of chunk
-  // k+1 overlaps the DMA of chunk k
+  // pageable (a std::vector FeatureSet): the host pool copies each slot-
+  // sized chunk into a pinned slot in parallel while the copy engine DMAs
+  // the previous slots
   const char* s = static_cast<const char*>(src);
   char* d = static_cast<char*>(dst);
+  HostPool& pool = host_pool(c);
   for (size_t off = 0; off < bytes; off += c.stage_bytes) {
     const size_t sz = std::min(c.stage_bytes, bytes - off);
-    const int i = c.stage_i;
-    BMG_CUDA(cudaEventSynchronize(c.stage_ev[i]));
-    std::memcpy(c.stage[i], s + off, sz);
-    BMG_CUDA(cudaMemcpyAsync(d + off, c.stage[i], sz, cudaMemcpyHostToDevice, c.s_copy));
-    BMG_CUDA(cudaEventRecord(c.stage_ev[i], c.s_copy));
-    c.stage_i ^= 1;
+    int i;
+    char* slot = next_slot(c, &i);
+    const int parts = static_cast<int>(std::min<size_t>(pool.size(), (sz + (256u << 10) - 1) >> 18));
+    const size_t per = (sz + parts - 1) / parts;
+    pool.run(parts, [&](int k) {
+      const size_t a = k * per, n = a < sz ? std::min(per, sz - a) : 0;
+      if (n) std::memcpy(slot + a, s + off + a, n);
+    });
+    slot_dma(c, i, d + off, sz);
   }
+}
+
+// A feature file's descriptors straight into HBM: the header is checked like
+// read_features (features.cpp:222-236) and must agree with the planned
+// count; the 528-byte records are read by the host pool with pread and
+// de-interleaved into pinned slots, each DMA'd while the next fills.
+void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
+  uint64_t id = 0, n = 0;
+  if (const int rc = bmg_read_features_header(path, &id, &n); rc != BMG_OK) fail(rc, bmg_last_error());
+  if (n != count)
+    fail(BMG_INVALID_ARGUMENT, std::string(path) + ": holds " + std::to_string(n) + " features, planned " +
+                                   std::to_string(count));
+  const int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) fail(BMG_FORMAT_ERROR, std::string("cannot open ") + path + " for reading");
+  struct FdGuard {
+    int fd;
+    ~FdGuard() { close(fd); }
+  } guard{fd};
+  constexpr size_t kHeader = 24, kRecord = (4 + kDim) * sizeof(float);
+  struct stat st{};
+  if (fstat(fd, &st) != 0) fail(BMG_FORMAT_ERROR, std::string("cannot stat ") + path);
+  const uint64_t body = static_cast<uint64_t>(st.st_size) > kHeader ? static_cast<uint64_t>(st.st_size) - kHeader : 0;
+  if (body < count * kRecord)
+    fail(BMG_TRUNCATED_FILE, std::string("unexpected end of file while reading ") +
+                                 (body % kRecord < 16 ? "keypoint" : "descriptor"));
+  HostPool& pool = host_pool(c);
+  const uint64_t per_slot = c.stage_bytes / (kDim * sizeof(float));
+  char* d = static_cast<char*>(dst);
+  for (uint64_t r0 = 0; r0 < count; r0 += per_slot) {
+    const uint64_t nr = std::min(per_slot, count - r0);
+    int i;
+    float* slot = reinterpret_cast<float*>(next_slot(c, &i));
+    constexpr uint64_t kBlock = 256;  // records per pread (~132 KiB): 32 reads per 8k image
+    const int blocks = static_cast<int>((nr + kBlock - 1) / kBlock);
+    std::atomic<bool> short_read{false};
+    pool.run(blocks, [&](int b) {
+      thread_local std::vector<unsigned char> buf;
+      buf.resize(kBlock * kRecord);
+      const uint64_t b0 = b * kBlock, m = std::min(kBlock, nr - b0);
+      const off_t off = static_cast<off_t>(kHeader + (r0 + b0) * kRecord);
+      size_t have = 0;
+      while (have < m * kRecord) {
+        const ssize_t got = pread(fd, buf.data() + have, m * kRecord - have, off + static_cast<off_t>(have));
+        if (got <= 0) break;
+        have += static_cast<size_t>(got);
+      }
+      if (have < m * kRecord) short_read.store(true);
+      const uint64_t full = have / kRecord;
+      for (uint64_t k = 0; k < full; ++k)
+        std::memcpy(slot + (b0 + k) * kDim, buf.data() + k * kRecord + 16, kDim * sizeof(float));
+    });
+    if (short_read.load()) fail(BMG_TRUNCATED_FILE, "unexpected end of file while reading descriptor");
+    slot_dma(c, i, d + r0 * kDim * sizeof(float), nr * kDim * sizeof(float));
+  }
+}
+
+void stage_source(Ctx& c, void* dst, const Source& src) {
+  if (src.path)
+    stage_file(c, dst, src.path, src.count);
+  else
+    stage_h2d(c, dst, src.desc, src.count * kDim * sizeof(float));
 }
 
 // DeviceArena::upload bookkeeping (engine.cpp:18-25): capacity check and
 // counters.  bmg_execute_plan runs it in the plan's order; the physical
 // allocation (arena_alloc) may happen in another order.
-void arena_account_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
+void arena_account_upload(Ctx& c, uint64_t id, bool has_data, uint64_t n) {
   if (c.occupancy + n > c.capacity)
     fail(BMG_CAPACITY_EXCEEDED, "uploading image " + std::to_string(id) + " (" + std::to_string(n) +
                                     " units) would raise occupancy to " +
                                     std::to_string(c.occupancy + n) + " of " +
                                     std::to_string(c.capacity));
-  if (n && !desc) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
+  if (n && !has_data) fail(BMG_INVALID_ARGUMENT, "null descriptor pointer");
   c.occupancy += n;
   c.peak = std::max(c.peak, c.occupancy);
   ++c.uploads;
@@ -483,7 +660,7 @@ ArenaImage& arena_alloc(Ctx& c, uint64_t id, uint64_t n) {
 }
 
 ArenaImage& arena_reserve(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
-  arena_account_upload(c, id, desc, n);
+  arena_account_upload(c, id, desc != nullptr, n);
   return arena_alloc(c, id, n);
 }
 
@@ -501,8 +678,8 @@ ImgDev proj_view(const ArenaImage& a) {
 // The H2D of a reserved image on the copy stream; the projection stream then
 // computes its mean-independent projections (K2 project_kernel) while the
 // next images upload, and records the image's ready event.
-void arena_copy(Ctx& c, ArenaImage& im, const float* desc) {
-  stage_h2d(c, im.d, desc, im.n * 512);
+void arena_copy(Ctx& c, ArenaImage& im, const Source& src) {
+  stage_source(c, im.d, src);
   BMG_CUDA(cudaEventRecord(c.ev_copied, c.s_copy));
   im.pstream = c.proj_rr;
   c.proj_rr = (c.proj_rr + 1) % bmg_context::kProjStreams;
@@ -522,7 +699,7 @@ void arena_copy(Ctx& c, ArenaImage& im, const float* desc) {
 
 void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
   if (c.resident.count(id)) return;  // engine.cpp:19
-  arena_copy(c, arena_reserve(c, id, desc, n), desc);
+  arena_copy(c, arena_reserve(c, id, desc, n), Source{desc, nullptr, n});
 }
 
 // stream-ordered free of a resident image after every kernel already queued
@@ -1149,8 +1326,8 @@ int bmg_create(const bmg_config* cfg, bmg_context** out) {
     // physical pool may grow so the next row's H2D overlaps this row's work)
     int no = 0;
     BMG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &no));
-    c->stage_bytes = 8u << 20;
-    for (int i = 0; i < 2; ++i) {
+    c->stage_bytes = 16u << 20;
+    for (int i = 0; i < bmg_context::kStageSlots; ++i) {
       BMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->stage[i]), c->stage_bytes));
       BMG_CUDA(cudaEventCreateWithFlags(&c->stage_ev[i], cudaEventDisableTiming));
       BMG_CUDA(cudaEventRecord(c->stage_ev[i], c->s_copy));
@@ -1178,7 +1355,8 @@ int bmg_destroy(bmg_context* c) {
     c->res_ranges.release();
     c->res_log.release();
     c->d_res.release();
-    for (int i = 0; i < 2; ++i) {
+    c->host.reset();
+    for (int i = 0; i < bmg_context::kStageSlots; ++i) {
       if (c->stage[i]) cudaFreeHost(c->stage[i]);
       if (c->stage_ev[i]) cudaEventDestroy(c->stage_ev[i]);
     }
@@ -1323,7 +1501,7 @@ int bmg_compute_codes(bmg_context* c, const float* desc, uint64_t count, const f
     tmp.n = count;
     tmp.proj = tmp.d + count * kDim;
     tmp.dnorm = tmp.proj + count * c->hd.proj_stride;
-    arena_copy(*c, tmp, desc);
+    arena_copy(*c, tmp, Source{desc, nullptr, count});
     c->free_events.push_back(tmp.ev);
     std::vector<RowImage> one{RowImage{tmp.d, count, tmp.proj, tmp.dnorm}};
     prepare_row_views(*c, one, mean, nullptr, false);
@@ -1451,22 +1629,57 @@ int bmg_match_pair(bmg_context* c, const float* qdesc, const bmg_code_set* qc, c
   });
 }
 
+namespace bmg {
+namespace {
+void execute_plan_impl(Ctx* c, const bmg_plan* plan, const std::unordered_map<uint64_t, Source>& fmap,
+                       const bmg_execute_options* opts, bmg_result** out,
+                       std::chrono::steady_clock::time_point t0);
+}  // namespace
+}  // namespace bmg
+
 int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_view* features,
                      uint64_t n_features, const bmg_execute_options* opts, bmg_result** out) {
   return guarded([&] {
     const auto t0 = std::chrono::steady_clock::now();
     if (!c || !plan || !opts || !out || (n_features && !features))
       fail(BMG_INVALID_ARGUMENT, "null argument");
+    std::unordered_map<uint64_t, Source> fmap;
+    for (uint64_t i = 0; i < n_features; ++i)
+      fmap[features[i].image_id] = Source{features[i].descriptors, nullptr, features[i].count};
+    execute_plan_impl(c, plan, fmap, opts, out, t0);
+  });
+}
+
+int bmg_execute_plan_files(bmg_context* c, const bmg_plan* plan, const bmg_feature_file* files,
+                           uint64_t n_files, const bmg_execute_options* opts, bmg_result** out) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!c || !plan || !opts || !out || (n_files && !files)) fail(BMG_INVALID_ARGUMENT, "null argument");
+    std::unordered_map<uint64_t, Source> fmap;
+    for (uint64_t i = 0; i < n_files; ++i) {
+      if (!files[i].path) fail(BMG_INVALID_ARGUMENT, "null feature file path");
+      fmap[files[i].image_id] = Source{nullptr, files[i].path, files[i].count};
+    }
+    execute_plan_impl(c, plan, fmap, opts, out, t0);
+  });
+}
+
+}  // extern "C"
+
+namespace bmg {
+namespace {
+void execute_plan_impl(Ctx* c, const bmg_plan* plan, const std::unordered_map<uint64_t, Source>& fmap,
+                       const bmg_execute_options* opts, bmg_result** out,
+                       std::chrono::steady_clock::time_point t0) {
+  {
     *out = nullptr;
     check_match_params(*c, opts->match);
     set_device(*c);
-    std::unordered_map<uint64_t, const bmg_feature_view*> fmap;
-    for (uint64_t i = 0; i < n_features; ++i) fmap[features[i].image_id] = &features[i];
-    auto features_of = [&](uint64_t id) -> const bmg_feature_view& {
+    auto features_of = [&](uint64_t id) -> const Source& {
       const auto it = fmap.find(id);
       if (it == fmap.end())
         fail(BMG_INVALID_ARGUMENT, "plan references image " + std::to_string(id) + " with no features");
-      return *it->second;
+      return it->second;
     };
     uint64_t total_rows = 0;
     for (uint64_t i = 0; i < plan->n_iterations; ++i) total_rows += plan->rows_per_iteration[i];
@@ -1611,8 +1824,8 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
           // order.
           if (evict_row.erase(id)) in_order = true;
           if (logical.count(id)) continue;
-          const bmg_feature_view& fv = features_of(id);
-          arena_account_upload(*c, id, fv.descriptors, fv.count);
+          const Source& fv = features_of(id);
+          arena_account_upload(*c, id, fv.desc || fv.path, fv.count);
           if (opts->on_upload) opts->on_upload(opts->hook_user, id, fv.count);
           logical.insert(id);
         }
@@ -1724,7 +1937,7 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
         std::stable_sort(missing.begin(), missing.end(),
                          [&](uint64_t x, uint64_t y) { return last_need[x] > last_need[y]; });
         for (size_t k = 0; k < missing.size(); ++k) {
-          arena_copy(*c, c->resident.at(missing[k]), features_of(missing[k]).descriptors);
+          arena_copy(*c, c->resident.at(missing[k]), features_of(missing[k]));
           if (timeline && k % 25 == 24) mark("row " + std::to_string(r) + " upload " + std::to_string(k + 1), c->s_copy);
         }
         if (!missing.empty()) mark("row " + std::to_string(r) + " uploads done", c->s_copy);
@@ -1852,8 +2065,12 @@ int bmg_execute_plan(bmg_context* c, const bmg_plan* plan, const bmg_feature_vie
       c->free_events.push_back(span1);
     }
     *out = res.release();
-  });
+  }
 }
+}  // namespace
+}  // namespace bmg
+
+extern "C" {
 
 uint64_t bmg_result_pair_count(const bmg_result* r) { return r ? r->pair_ids.size() / 2 : 0; }
 uint64_t bmg_result_match_count(const bmg_result* r) { return r ? r->n_matches : 0; }

@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 from collections.abc import Sequence
 import json
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -260,7 +261,27 @@ def arena_units_for(features: dict, gpu_images: int) -> int:
     return largest * max(0, gpu_images)
 
 
+def _is_path(x) -> bool:
+    return isinstance(x, (str, bytes, os.PathLike))
+
+
+def _feature_files(features: dict):
+    """bmg_feature_file array for {id: path to a .feat file}."""
+    L = _lib.load()
+    files = (_lib.FeatureFileC * max(1, len(features)))()
+    keep = []
+    for i, (iid, path) in enumerate(features.items()):
+        b = os.fsencode(path)
+        keep.append(b)
+        fid, n = C.c_uint64(0), C.c_uint64(0)
+        check(L.bmg_read_features_header(b, C.byref(fid), C.byref(n)))
+        files[i] = _lib.FeatureFileC(int(iid), b, n.value)
+    return files, keep
+
+
 def _feature_views(features: dict):
+    if features and all(_is_path(v) for v in features.values()):
+        return _feature_files(features)
     views = (_lib.FeatureViewC * max(1, len(features)))()
     keep = []
     for i, (iid, fs) in enumerate(features.items()):
@@ -358,7 +379,10 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
     """execute_plan (engine.cpp:411-527) with verification off: the row body
     (uploads, mean, codes, bucket tables, cascade matching) runs on the B200.
     Results are sorted by IdPair.  ``rows`` restricts execution to a subset of
-    global row indices (multi-GPU sharding)."""
+    global row indices (multi-GPU sharding).  ``features`` maps image ids to
+    FeatureSets / descriptor arrays (pinned or pageable host memory), or to
+    paths of .feat files, which are then read as their images upload
+    (bmg_execute_plan_files) instead of being loaded up front."""
     L = _lib.load()
     flat = flat or flatten_plan(plan, rows)
     views, keep = views or _feature_views(features)
@@ -380,8 +404,9 @@ def execute_plan(plan: SchedulePlan, features: dict, arena: DeviceArena,
     on_ev = wrap(opts.on_evict, _lib.EVICT_HOOK, lambda u, i: opts.on_evict(i))
     oc = _lib.ExecOptionsC(opts.match.c(), on_pair, None, on_up, on_ev, None, opts.flags())
     h = C.c_void_p()
-    check(L.bmg_execute_plan(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc),
-                             C.byref(h)))
+    run = L.bmg_execute_plan_files if isinstance(views, C.Array) and views._type_ is _lib.FeatureFileC \
+        else L.bmg_execute_plan
+    check(run(arena.matcher.handle, C.byref(pc), views, len(features), C.byref(oc), C.byref(h)))
     holder = _ResultBuffer(L, h)
     npairs = L.bmg_result_pair_count(h)
     nm = L.bmg_result_match_count(h)
