@@ -257,9 +257,12 @@ struct Source {
 };
 
 struct ArenaImage {
-  float* d = nullptr;         // [n][128] descriptors, then proj [n][proj_stride], dnorm [n]
+  float* d = nullptr;         // [n][128] descriptors, then proj [n][proj_stride], dnorm [n], tile statistics
   float* proj = nullptr;
   float* dnorm = nullptr;
+  void* tsum = nullptr;       // row-mean tile statistics (ImgDev::tsum / trng / tlow)
+  void* trng = nullptr;
+  uint32_t* tlow = nullptr;
   uint64_t n = 0;
   cudaEvent_t ev = nullptr;  // recorded on the projection stream once the image is usable
   uint64_t seq = 0;          // upload order
@@ -273,7 +276,15 @@ struct RowImage {
   uint64_t n;
   float* proj;
   float* dnorm;
+  void* tsum = nullptr;
+  void* trng = nullptr;
+  uint32_t* tlow = nullptr;
 };
+
+// the image block after the descriptors: projections, norms, tile statistics
+size_t image_extra_bytes(uint64_t n, int proj_stride) {
+  return align_up(proj_bytes(n, proj_stride), 16) + tile_stats_bytes(n);
+}
 
 // Process-wide pool of pinned host buffers that execution results own (the
 // row regions of the result log are DMA'd straight into them; freeing the
@@ -652,10 +663,15 @@ void arena_account_upload(Ctx& c, uint64_t id, bool has_data, uint64_t n) {
 ArenaImage& arena_alloc(Ctx& c, uint64_t id, uint64_t n) {
   ArenaImage im;
   im.n = n;
-  const size_t bytes = n * 512 + align_up(proj_bytes(n, c.hd.proj_stride), 16);
+  const size_t bytes = n * 512 + image_extra_bytes(n, c.hd.proj_stride);
   BMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&im.d), std::max<size_t>(bytes, 512), c.pool, c.s_copy));
   im.proj = im.d + n * kDim;
   im.dnorm = im.proj + n * c.hd.proj_stride;
+  const size_t nt = (n + kCodesTile - 1) / kCodesTile;
+  char* ts = reinterpret_cast<char*>(im.d) + n * 512 + align_up(proj_bytes(n, c.hd.proj_stride), 16);
+  im.tsum = ts;
+  im.trng = ts + nt * kDim * 16;
+  im.tlow = reinterpret_cast<uint32_t*>(ts + nt * kDim * 48);
   return c.resident.emplace(id, im).first->second;
 }
 
@@ -671,6 +687,9 @@ ImgDev proj_view(const ArenaImage& a) {
   v.desc = a.d;
   v.proj = a.proj;
   v.dnorm = a.dnorm;
+  v.tsum = a.tsum;
+  v.trng = a.trng;
+  v.tlow = a.tlow;
   v.n = static_cast<uint32_t>(a.n);
   return v;
 }
@@ -836,6 +855,9 @@ void prepare_row_views(Ctx& c, const std::vector<RowImage>& descs, const float* 
     im.desc = descs[i].desc;
     im.proj = descs[i].proj;
     im.dnorm = descs[i].dnorm;
+    im.tsum = descs[i].tsum;
+    im.trng = descs[i].trng;
+    im.tlow = descs[i].tlow;
     im.n = static_cast<uint32_t>(descs[i].n);
     im.coarse = reinterpret_cast<uint32_t*>(base + lay[i].coarse_off);
     im.fine = reinterpret_cast<uint64_t*>(base + lay[i].fine_off);
@@ -901,11 +923,18 @@ void prepare_row_views(Ctx& c, const std::vector<RowImage>& descs, const float* 
     c.S().d_mean_state.ensure(sizeof(MeanState));
     meta_add(c, c.S().d_mean_state.p, nullptr, sizeof(MeanState));
     meta_flush(c);
+    // the tile statistics come with the images' projections (tensor-core
+    // K2): the mean waits for those, then only resolves
+    const bool resident = project_writes_tile_stats(c.hd);
+    if (resident) {
+      for (cudaEvent_t e : c.proj_waits) BMG_CUDA(cudaStreamWaitEvent(s, e, 0));
+      c.proj_waits.clear();
+    }
     Timed t(c, "mean", s);
     c.launches += launch_row_mean(d_imgs, n_imgs, c.S().d_tiles.as<uint32_t>(),
                                   c.S().d_tiles.as<uint32_t>() + n_tiles, static_cast<int>(n_tiles),
                                   total_desc, c.S().d_mean_sums.p, c.S().d_mean_state.as<MeanState>(), d_mean,
-                                  c.S().d_acc.as<double>(), chain_only, s);
+                                  c.S().d_acc.as<double>(), chain_only, resident, s);
     check_launch();
   }
   if (c.marks) {
@@ -930,7 +959,8 @@ void prepare_row(Ctx& c, const uint64_t* ids, uint64_t n, const float* mean_host
     const auto it = c.resident.find(ids[i]);
     if (it == c.resident.end())
       fail(BMG_NOT_RESIDENT, "row needs image " + std::to_string(ids[i]) + " which is not resident");
-    descs.push_back(RowImage{it->second.d, it->second.n, it->second.proj, it->second.dnorm});
+    descs.push_back(RowImage{it->second.d, it->second.n, it->second.proj, it->second.dnorm, it->second.tsum,
+                             it->second.trng, it->second.tlow});
     c.S().row_slot[ids[i]] = static_cast<int>(i);
   }
   c.S().row_valid = false;

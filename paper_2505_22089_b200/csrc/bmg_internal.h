@@ -23,6 +23,13 @@ struct ImgDev {
   uint64_t* bfine;     // [tables][ns][fwp] fine codes in slot order (coalesced candidate walk)
   float* proj;          // [n][proj_stride] fl32(d . p) for every plane (mean-independent, per residency)
   float* dnorm;         // [n] ||d||_2 rounded up
+  // row-mean tile statistics of the image (kernels.cu K1), per 128-
+  // descriptor tile and channel, computed with its projections: F96 sum
+  // (i128), range of the partial sums (2 x i128), lowest set F96 bit
+  // (kNoLow: all zeros, kBadTile: a value outside F96); null when absent
+  void* tsum;
+  void* trng;
+  uint32_t* tlow;
   uint32_t n;
   uint32_t overflow;   // set by the codes kernel when its fixup list overflowed
   uint32_t ns;         // slot stride per table: slot_stride(n, n_buckets)
@@ -115,11 +122,20 @@ inline uint32_t slot_stride(uint64_t n, int n_buckets, int pad) {
 // chain alone.  scratch: mean_scratch_bytes(n_tiles); *st must be zeroed by
 // the caller (stream-ordered).  Returns kernel launches.
 inline size_t mean_scratch_bytes(size_t n_tiles) {
-  return n_tiles * kDim * (16 + 32 + 4);  // F96 tile sums, partial-sum ranges, lowest set bits
+  return n_tiles * kDim * 16;  // exclusive prefix of the F96 tile sums
 }
+// bytes of an image's tile statistics (ImgDev::tsum / trng / tlow)
+inline size_t tile_stats_bytes(uint64_t n) {
+  return ((n + kDim - 1) / kDim) * kDim * (16 + 32 + 4);
+}
+// `sums_resident`: every image's tile statistics were computed with its
+// projections, so only the resolve runs; otherwise mean_sums computes them
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
                     const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,
-                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s);
+                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, bool sums_resident,
+                    cudaStream_t s);
+// whether launch_project writes the tile statistics (the tensor-core K2)
+bool project_writes_tile_stats(const HashDev& h);
 // fl32 projections + norms of one image (tile t = descriptors [128t, 128t+128))
 // or of a tile list (ImgDev::proj / dnorm are the outputs)
 void launch_project(const HashDev& h, const ImgDev& one, cudaStream_t s);

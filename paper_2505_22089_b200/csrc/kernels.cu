@@ -142,52 +142,44 @@ __device__ __forceinline__ i128 shfl_up_i128(i128 v, int d) {
   return (i128)(((u128)hi << 64) | lo);
 }
 
-// 256 threads: thread (h, c) covers rows 64h..64h+63 of channel c; row-major
-// loads (512 contiguous bytes per row across the CTA).  Per tile and channel:
-// the F96 sum, the range [lo, hi] of its partial sums (relative to the tile
-// start) and the lowest set F96 bit of any value.
-constexpr int kSumsThreads = 256;
+constexpr uint32_t kBadTile = 0xfffffffeu;  // tile_low: a value outside F96 (row takes the chain)
 
 struct TileRange {
   i128 lo, hi;
 };
 
-__global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* __restrict__ imgs,
-                                                                 const uint32_t* __restrict__ tile_img,
-                                                                 const uint32_t* __restrict__ tile_start,
-                                                                 i128* __restrict__ tile_sum,
-                                                                 TileRange* __restrict__ tile_rng,
-                                                                 uint32_t* __restrict__ tile_low, MeanState* st) {
-  __shared__ i128 s_sum[kDim], s_lo[kDim], s_hi[kDim];
-  __shared__ uint32_t s_low[kDim];
-  const int c = threadIdx.x & (kDim - 1), h = threadIdx.x >> 7;
-  const uint32_t img = tile_img[blockIdx.x], i0 = tile_start[blockIdx.x];
-  const int nd = min(kCodesTile, (int)(imgs[img].n - i0));
-  const float* d = imgs[img].desc + (size_t)i0 * kDim + c;
-  const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
-  // pass 1: the lowest set F96 bit of the thread's 64 values ((e - 54) +
-  // ctz(mantissa with the implicit bit)) and whether all are multiples of
-  // 2^-49 below 2^7: then pass 2 sums them exactly in int64 at scale 2^49
-  // (|partial sum| < 64 * 2^56): one add and two compares per value instead
-  // of the int128 ones.  Pass 2 re-reads the values (L1 hits).
-  uint32_t low = kNoLow;
+// Statistics of rows [r0, r1) of one channel (ld(r) = the value): the F96
+// sum, the range [lo, hi] of the partial sums and the lowest set F96 bit.
+// A check pass finds the lowest set bit and whether every value is a
+// multiple of 2^-49 below 2^7: then the sums run exactly in int64 at scale
+// 2^49 (|partial sum| < 64 * 2^56), one add and two compares per value
+// instead of the int128 ones.
+struct HalfStats {
+  i128 s, lo, hi;
+  uint32_t low;
+  bool ok;
+};
+template <typename Ld>
+__device__ __forceinline__ HalfStats half_tile_stats(int r0, int r1, Ld&& ld) {
+  HalfStats o;
+  o.low = kNoLow;
+  o.ok = true;
   bool fast = true;
 #pragma unroll 16
   for (int r = r0; r < r1; ++r) {
-    const uint32_t u = __float_as_uint(__ldg(d + (size_t)r * kDim));
+    const uint32_t u = __float_as_uint(ld(r));
     const int e = (int)((u >> 23) & 0xff);
     const uint32_t lb = (uint32_t)(e - 54 + (__ffs((int)((u & 0x7fffffu) | 0x800000u)) - 1));
     const bool nz = (u & 0x7fffffffu) != 0u;
-    low = nz ? min(low, lb) : low;
+    o.low = nz ? min(o.low, lb) : o.low;
     fast &= !nz || (e >= 1 && e < 127 + 7 && (int)lb >= 96 - 49);
   }
-  i128 s = 0, lo = 0, hi = 0;
-  bool ok = true;
+  o.s = o.lo = o.hi = 0;
   if (fast) {
     long long s6 = 0, lo6 = 0, hi6 = 0;
 #pragma unroll 16
     for (int r = r0; r < r1; ++r) {
-      const uint32_t u = __float_as_uint(__ldg(d + (size_t)r * kDim));
+      const uint32_t u = __float_as_uint(ld(r));
       const int e = (int)((u >> 23) & 0xff);
       const long long m = (long long)((u & 0x7fffffu) | 0x800000u);
       const int sh = e - 101;  // x * 2^49 = m * 2^(e - 101), exact by the fast-path test
@@ -197,36 +189,65 @@ __global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* _
       lo6 = min(lo6, s6);
       hi6 = max(hi6, s6);
     }
-    s = (i128)s6 * ((i128)1 << 47);  // F96 = (x * 2^49) * 2^47
-    lo = (i128)lo6 * ((i128)1 << 47);
-    hi = (i128)hi6 * ((i128)1 << 47);
+    o.s = (i128)s6 * ((i128)1 << 47);  // F96 = (x * 2^49) * 2^47
+    o.lo = (i128)lo6 * ((i128)1 << 47);
+    o.hi = (i128)hi6 * ((i128)1 << 47);
   } else {
 #pragma unroll 16
     for (int r = r0; r < r1; ++r) {
-      s += to_f96(__ldg(d + (size_t)r * kDim), ok);
-      lo = s < lo ? s : lo;
-      hi = s > hi ? s : hi;
+      o.s += to_f96(ld(r), o.ok);
+      o.lo = o.s < o.lo ? o.s : o.lo;
+      o.hi = o.s > o.hi ? o.s : o.hi;
     }
   }
+  return o;
+}
+
+// Tile statistics of one 128-descriptor tile, 256 threads: thread (h, c)
+// covers rows 64h..64h+63 of channel c; the halves meet in shared memory and
+// the result goes to the image's arrays (ImgDev::tsum / trng / tlow) at
+// tile index ti.  Contains __syncthreads (call from every thread).
+struct TileStatsSmem {
+  i128 sum[kDim], lo[kDim], hi[kDim];
+  uint32_t low[kDim];
+};
+template <typename Ld>
+__device__ __forceinline__ void tile_stats(const ImgDev& im, uint32_t ti, int nd, TileStatsSmem& sm, Ld&& ld) {
+  const int c = threadIdx.x & (kDim - 1), h = threadIdx.x >> 7;
+  const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
+  const HalfStats hs = half_tile_stats(r0, r1, [&](int r) { return ld(r, c); });
   if (h == 0) {
-    s_sum[c] = s;
-    s_lo[c] = lo;
-    s_hi[c] = hi;
-    s_low[c] = low;
+    sm.sum[c] = hs.s;
+    sm.lo[c] = hs.lo;
+    sm.hi[c] = hs.hi;
+    sm.low[c] = hs.low;
   }
-  const int bad = __syncthreads_or(!ok);
+  const int bad = __syncthreads_or(!hs.ok);
   if (h == 1) {
     // second half's partial sums are offset by the first half's total
-    const i128 s0 = s_sum[c], lo0 = s_lo[c], hi0 = s_hi[c];
-    const size_t o = (size_t)blockIdx.x * kDim + c;
-    tile_sum[o] = s0 + s;
+    const i128 s0 = sm.sum[c], lo0 = sm.lo[c], hi0 = sm.hi[c];
+    const size_t o = (size_t)ti * kDim + c;
+    static_cast<i128*>(im.tsum)[o] = s0 + hs.s;
     TileRange rg;
-    rg.lo = (s0 + lo) < lo0 ? (s0 + lo) : lo0;
-    rg.hi = (s0 + hi) > hi0 ? (s0 + hi) : hi0;
-    tile_rng[o] = rg;
-    tile_low[o] = min(low, s_low[c]);
+    rg.lo = (s0 + hs.lo) < lo0 ? (s0 + hs.lo) : lo0;
+    rg.hi = (s0 + hs.hi) > hi0 ? (s0 + hs.hi) : hi0;
+    static_cast<TileRange*>(im.trng)[o] = rg;
+    im.tlow[o] = bad ? kBadTile : min(hs.low, sm.low[c]);
   }
-  if (bad && threadIdx.x == 0) st->bad = 1u;
+}
+
+// Tile statistics for a row's tiles whose images do not carry them yet
+// (the SIMT projection path): one CTA per tile.
+constexpr int kSumsThreads = 256;
+__global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* __restrict__ imgs,
+                                                                 const uint32_t* __restrict__ tile_img,
+                                                                 const uint32_t* __restrict__ tile_start) {
+  __shared__ TileStatsSmem sm;
+  const ImgDev im = imgs[tile_img[blockIdx.x]];
+  const uint32_t i0 = tile_start[blockIdx.x];
+  const int nd = min(kCodesTile, (int)(im.n - i0));
+  const float* d = im.desc + (size_t)i0 * kDim;
+  tile_stats(im, i0 / kCodesTile, nd, sm, [&](int r, int c) { return __ldg(d + (size_t)r * kDim + c); });
 }
 
 // Certificate for tile t with the accumulator v = P_t + delta at its start:
@@ -245,26 +266,43 @@ __device__ __forceinline__ bool tile_certified(i128 v, const TileRange& rg, uint
 
 constexpr int kResolveThreads = 256;
 
+// tile t of the row -> its statistics' offset in its image's arrays
+__device__ __forceinline__ const ImgDev& tile_of(const ImgDev* imgs, const uint32_t* tile_img,
+                                                 const uint32_t* tile_start, int t, int c, size_t& o) {
+  const ImgDev& im = imgs[tile_img[t]];
+  o = (size_t)(tile_start[t] / kCodesTile) * kDim + c;
+  return im;
+}
+
 __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
     const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
-    const uint32_t* __restrict__ tile_start, i128* __restrict__ tile_sum, const TileRange* __restrict__ tile_rng,
-    const uint32_t* __restrict__ tile_low, int n_tiles, unsigned long long total, MeanState* st,
-    float* __restrict__ mean_out, double* __restrict__ acc_out) {
+    const uint32_t* __restrict__ tile_start, i128* __restrict__ tile_sum, int n_tiles, unsigned long long total,
+    MeanState* st, float* __restrict__ mean_out, double* __restrict__ acc_out) {
   __shared__ i128 part[kResolveThreads];
   __shared__ i128 s_delta;
   __shared__ int s_fail;
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  if (*reinterpret_cast<const volatile uint32_t*>(&st->bad)) {
-    if (tid == 0) st->need_chain = 1u;
-    return;
-  }
-  // ---- exclusive scan of the tile sums of channel c (in place)
+  // ---- exclusive scan of the tile sums of channel c (into tile_sum, the
+  // row's prefix scratch); a tile with a value outside F96 sends the row to
+  // the chain
   const int per = (n_tiles + kResolveThreads - 1) / kResolveThreads;
   const int t0 = min(n_tiles, tid * per), t1 = min(n_tiles, t0 + per);
   i128 loc = 0;
-  for (int t = t0; t < t1; ++t) loc += tile_sum[(size_t)t * kDim + c];
+  bool bad = false;
+  for (int t = t0; t < t1; ++t) {
+    size_t o;
+    const ImgDev& im = tile_of(imgs, tile_img, tile_start, t, c, o);
+    loc += static_cast<const i128*>(im.tsum)[o];
+    bad |= im.tlow[o] == kBadTile;
+  }
   part[tid] = loc;
-  __syncthreads();
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) {
+      st->bad = 1u;
+      st->need_chain = 1u;
+    }
+    return;
+  }
   if (tid == 0) {
     i128 run = 0;
     for (int i = 0; i < kResolveThreads; ++i) {
@@ -278,9 +316,10 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
   {
     i128 run = part[tid];
     for (int t = t0; t < t1; ++t) {
-      const i128 v = tile_sum[(size_t)t * kDim + c];
+      size_t o;
+      const ImgDev& im = tile_of(imgs, tile_img, tile_start, t, c, o);
       tile_sum[(size_t)t * kDim + c] = run;
-      run += v;
+      run += static_cast<const i128*>(im.tsum)[o];
     }
   }
   const i128 row_total = s_delta;
@@ -301,8 +340,11 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
       __syncthreads();
       const int t = w0 + tid;
       if (t < n_tiles) {
-        const size_t o = (size_t)t * kDim + c;
-        if (!tile_certified(tile_sum[o] + delta, tile_rng[o], tile_low[o])) atomicMin(&s_fail, t);
+        size_t o;
+        const ImgDev& im = tile_of(imgs, tile_img, tile_start, t, c, o);
+        if (!tile_certified(tile_sum[(size_t)t * kDim + c] + delta, static_cast<const TileRange*>(im.trng)[o],
+                            im.tlow[o]))
+          atomicMin(&s_fail, t);
       }
       __syncthreads();
       f = s_fail;
@@ -687,6 +729,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
   int* sF = sExp + kTcRows;                                     // [npad] plane exponents
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sF + ((npad + 1) & ~1));  // [3]: MMA done, raw tile, planes
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(mbar + 3);
+  // the row-mean tile statistics' half-tile exchange (16-byte aligned)
+  TileStatsSmem& sStats = *reinterpret_cast<TileStatsSmem*>(
+      (reinterpret_cast<uintptr_t>(sTmem + 1) + 15) & ~static_cast<uintptr_t>(15));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // thread 0: tile t's rows (contiguous, nd x 512 B) -> sRaw
@@ -804,11 +849,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // the staged rows are consumed: stream the next tile in under this one's
-    // MMAs and epilogue
-    if (tid == 0 && t + (int)gridDim.x < job.n_tiles) issue_raw(t + gridDim.x);
-
-    for (int pass = 0; pass < n_pass; ++pass) {
+    auto issue_mma = [&](int pass) {
       const int p0 = pass ? h.tc_pass0 : 0;
       const int np = pass ? npad - h.tc_pass0 : min(h.tc_pass0, npad);
       if (tid == 0) {
@@ -835,6 +876,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
                          cvta_smem(mbar))
                      : "memory");
       }
+    };
+    issue_mma(0);
+    // while the first pass's MMAs run: the row-mean tile statistics (K1)
+    // from the same staged rows, so the row's mean only resolves them
+    // (uniform branch: one image per tile)
+    if (im.tsum) {
+      tile_stats(im, i0 / kCodesTile, nd, sStats, [&](int r, int c) { return sRaw[r * kDim + c]; });
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+    }
+    // the staged rows are consumed: stream the next tile in under this one's
+    // MMAs and epilogue
+    if (tid == 0 && t + (int)gridDim.x < job.n_tiles) issue_raw(t + gridDim.x);
+
+    for (int pass = 0; pass < n_pass; ++pass) {
+      const int p0 = pass ? h.tc_pass0 : 0;
+      const int np = pass ? npad - h.tc_pass0 : min(h.tc_pass0, npad);
+      if (pass) issue_mma(pass);
       // wait for the accumulators
       {
         uint32_t done = 0;
@@ -1891,17 +1950,18 @@ void launch_meta(const MetaBatch& b, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 int launch_row_mean(const ImgDev* imgs, int n_imgs, const uint32_t* tile_img,
                     const uint32_t* tile_start, int n_tiles, unsigned long long total, void* scratch,
-                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, cudaStream_t s) {
+                    MeanState* st, float* mean_out, double* acc_out, bool chain_only, bool sums_resident,
+                    cudaStream_t s) {
   int launches = 0;
   const uint32_t* gate = nullptr;
   if (!chain_only && n_tiles > 0) {
-    i128* sums = static_cast<i128*>(scratch);
-    TileRange* rng = reinterpret_cast<TileRange*>(sums + (size_t)n_tiles * kDim);
-    uint32_t* low = reinterpret_cast<uint32_t*>(rng + (size_t)n_tiles * kDim);
-    mean_sums_kernel<<<n_tiles, kSumsThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, st);
-    mean_resolve_kernel<<<kDim, kResolveThreads, 0, s>>>(imgs, tile_img, tile_start, sums, rng, low, n_tiles,
-                                                         total, st, mean_out, acc_out);
-    launches += 2;
+    if (!sums_resident) {
+      mean_sums_kernel<<<n_tiles, kSumsThreads, 0, s>>>(imgs, tile_img, tile_start);
+      ++launches;
+    }
+    mean_resolve_kernel<<<kDim, kResolveThreads, 0, s>>>(imgs, tile_img, tile_start, static_cast<i128*>(scratch),
+                                                         n_tiles, total, st, mean_out, acc_out);
+    ++launches;
     gate = &st->need_chain;
   }
   mean_chain_kernel<<<kDim / 32, 32, 0, s>>>(imgs, n_imgs, gate, mean_out, acc_out);
@@ -1928,8 +1988,9 @@ static int sm_count() {
 
 static size_t proj_tc_smem_bytes(const HashDev& h) {
   return 1024 + 3 * (size_t)kTcDigitBytes + 3 * (size_t)h.tc_npad * 128 + sizeof(float) * kTcRows * kDim +
-         sizeof(int) * (kTcRows + h.tc_npad + 2) + 3 * sizeof(uint64_t) + 16;
+         sizeof(int) * (kTcRows + h.tc_npad + 2) + 3 * sizeof(uint64_t) + 16 + sizeof(TileStatsSmem) + 16;
 }
+
 
 static bool project_simt_forced() {
   static const bool v = [] {
@@ -1938,6 +1999,8 @@ static bool project_simt_forced() {
   }();
   return v;
 }
+
+bool project_writes_tile_stats(const HashDev& h) { return h.tc_b != nullptr && !project_simt_forced(); }
 
 static void launch_project_job(const HashDev& h, const ProjJob& job, cudaStream_t s) {
   if (job.n_tiles <= 0) return;

@@ -37,6 +37,15 @@ def flat_of(res):
     return multigpu.result_flat(res)
 
 
+def assert_same(gpu, ref):
+    gi, go, gm = gpu
+    ri, ro, rm = ref
+    assert np.array_equal(gi, ri)
+    for p in range(len(ri)):
+        assert np.array_equal(gm[go[p]:go[p + 1]], rm[ro[p]:ro[p + 1]]), tuple(ri[p])
+    assert np.array_equal(go, ro)
+
+
 # ---- (a) config 2 at full size ---------------------------------------------
 def test_config2_full_size_equals_reference(reference):
     table = reference.synth_features(43, 8192, 11, 0.02, 0.2, 7, drop=11)
