@@ -290,6 +290,42 @@ def ncu_traffic(avg_ctas_per_launch):
         return None
 
 
+MICROBENCH = ROOT / "profiles" / "r2_microbench.json"
+
+
+def microbench_peaks() -> dict:
+    try:
+        return json.loads(MICROBENCH.read_text())
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def candidates_per_query(m, plan, feats, samples=16):
+    """Duplicate-inclusive candidates per query (the union walk's entries
+    before dedup, hashmatch.cpp:154-167) on up to `samples` pairs of the
+    plan's largest row, from the GPU's own codes of that row."""
+    rows = [r for it in plan.iterations for r in it.rows]
+    if not rows:
+        return 0.0
+    row = max(rows, key=lambda r: sum(len(b.pairs) for b in r.blocks))
+    pairs = [p for b in row.blocks for p in b.pairs][:samples]
+    if not pairs:
+        return 0.0
+    m.row(row.needed())
+    nb = 1 << m.hf.params.coarse_bits
+    codes = {}
+    for i in {x for p in pairs for x in p}:
+        codes[i] = m.codes(i, len(feats[i].descriptors)).coarse
+    cand = q = 0
+    for a, b in pairs:
+        for t in range(codes[a].shape[1]):
+            ca = np.bincount(codes[a][:, t], minlength=nb)
+            cb = np.bincount(codes[b][:, t], minlength=nb)
+            cand += int((ca.astype(np.int64) * cb).sum())
+        q += codes[a].shape[0]
+    return cand / q
+
+
 # ---------------------------------------------------------------------------
 # the reference (CPU) legs: oracle/_ref only
 # ---------------------------------------------------------------------------
@@ -433,11 +469,16 @@ def main():
     plan_path = ROOT / "bench_data" / plan_file
     rows = plan_rows(plan_path)
     cores = os.cpu_count() or 1
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    dev = local if world > 1 else 0
+    # BMG_BENCH_BACKEND=gloo: ranks may share a GPU (validation of the
+    # sharded path on a one-GPU box); the driver's runs use NCCL, one GPU each
+    backend = os.environ.get("BMG_BENCH_BACKEND", "nccl")
+    dev = local % max(torch.cuda.device_count(), 1) if world > 1 else 0
     torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
 
     plan = bm.read_plan(plan_path)
     n_pairs = plan.pair_count()
@@ -471,24 +512,29 @@ def main():
     flat = bm.flatten_plan(sub)
     views = _feature_views(feats)
 
+    def dist_barrier():
+        if backend == "nccl":
+            dist.barrier(device_ids=[dev])
+        else:
+            dist.barrier()
+
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[dev])
+            dist_barrier()
+
+    def reduce_over_ranks(x: float, op) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(x, dist.ReduceOp.MAX) if world > 1 else x
 
     def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(x, dist.ReduceOp.SUM) if world > 1 else x
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
 
@@ -501,7 +547,7 @@ def main():
     def e2e_step(step):
         r = bm.execute_plan(sub, feats, arena_e2e, opts, flat=flat, views=views)
         if world > 1:
-            got = multigpu.gather_results(r, rank, world, lambda: dist.barrier(device_ids=[dev]),
+            got = multigpu.gather_results(r, rank, world, dist_barrier,
                                           f"{os.environ.get('MASTER_PORT', '0')}_{step}")
             return r, got
         return r, None
@@ -526,7 +572,7 @@ def main():
     e2e_step_s = max_over_ranks(sum(e2e_times) / len(e2e_times))
     h2d_all = sum_over_ranks(desc_bytes)
     d2h_all = sum_over_ranks(d2h)
-    gpu_flat = multigpu.result_flat(r) if world == 1 else (got[:3] if rank == 0 else None)
+    gpu_flat = multigpu.result_flat(r) if world == 1 else (got[0].flat() if rank == 0 else None)
     e2e_result = r
     arena_e2e.matcher.close()
 
@@ -637,6 +683,17 @@ def main():
     achieved = per_launch_bytes / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0
     traffic = ncu_traffic(step_ctas * args.steps / max(match_n, 1))
     consistent_all = max_over_ranks(0.0 if consistent else 1.0) == 0.0
+    # secondary rooflines of the match kernel: POPC and the
+    # candidate-code gathers, from the duplicate-inclusive candidates per
+    # query measured on a sample of the largest row's pairs (bucket sizes of
+    # the GPU's own codes: sum over tables and buckets of |Q_b| * |T_b|)
+    cand_q = candidates_per_query(m, sub, feats)
+    micro = microbench_peaks()
+    queries_per_launch = sum(len(feats[a_].descriptors) for it in sub.iterations for row in it.rows
+                             for blk in row.blocks for a_, _ in blk.pairs) * args.steps / max(match_n, 1)
+    fw = 2  # u64 words per fine code (128 bits)
+    popc_per_launch = queries_per_launch * cand_q * 2 * fw
+    gather_per_launch = queries_per_launch * cand_q * (8 * fw + 4)
 
     line = None
     if rank == 0:
@@ -671,6 +728,19 @@ def main():
                          "avg_launch_ms": avg_launch_s * 1e3,
                          "timing": "CUDA events around each launch on its stream, serial-row pass "
                                    "of the same steps after the timed region"},
+            "roofline_secondary": {
+                "candidates_per_query": cand_q,
+                "popc": {"achieved": popc_per_launch / avg_launch_s if avg_launch_s > 0 else 0.0,
+                         "peak": micro.get("popc32_per_s"), "unit": "POPC/s",
+                         "frac": (popc_per_launch / avg_launch_s / micro["popc32_per_s"]
+                                  if micro.get("popc32_per_s") and avg_launch_s > 0 else None),
+                         "note": "32-bit POPC per candidate = 4 at 128 bits; peak: profiles/r2_microbench.json"},
+                "l2_gather": {"achieved": gather_per_launch / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0,
+                              "peak": micro.get("gather16_l2_gbs"), "unit": "GB/s",
+                              "frac": (gather_per_launch / avg_launch_s / 1e9 / micro["gather16_l2_gbs"]
+                                       if micro.get("gather16_l2_gbs") and avg_launch_s > 0 else None),
+                              "note": "20 B (16 B code + 4 B index) per candidate vs the measured random "
+                                      "16-byte L2 gather rate"}},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items()},
             "results_consistent_e2e_vs_resident": consistent_all,
             "wall_s_timed": t_wall,
@@ -692,7 +762,7 @@ def main():
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
-        dist.barrier(device_ids=[dev])
+        dist_barrier()
         dist.destroy_process_group()
     m.close()
     return 0

@@ -19,9 +19,9 @@ barriers (engine.cpp:497-499).
 
 The only communication is the final gather of the match lists to rank 0,
 through shared memory (one node): each rank writes its result -- already in
-IdPair order -- into a /dev/shm segment, rank 0 merges the segments by
-IdPair (results are keyed by pair, engine.cpp:419, 506-512).  No objects are
-pickled.
+IdPair order -- into a /dev/shm segment, rank 0 maps the segments and orders
+the pairs by IdPair (results are keyed by pair, engine.cpp:419, 506-512);
+match lists are not copied or pickled.
 """
 from __future__ import annotations
 
@@ -36,7 +36,7 @@ from .engine import (BlockRow, DeviceArena, ExecuteOptions, ExecutionResult, Ite
 from .hashmatch import HashFunctions, PairMatches
 
 __all__ = ["shard_plan", "needed_images", "execute_plan_distributed", "gather_results",
-           "result_flat", "FlatPairs"]
+           "result_flat", "FlatPairs", "GatheredPairs"]
 
 # cost of one needed image of a row (mean + codes + bucket tables) in units of
 # one pair's matching, measured on the B200 (block32: 0.67 ms of row prep for
@@ -179,61 +179,80 @@ def _shm_dir() -> str:
         else tempfile.gettempdir()
 
 
+class GatheredPairs(Sequence):
+    """Rank 0's view of the gathered result: pairs in IdPair order, each
+    pair's matches a slice of the shared-memory segment its rank wrote
+    (mapped, not copied).  ``flat()`` materialises the canonical arrays."""
+
+    def __init__(self, ids, seg_of, begin, end, segs):
+        self.ids, self._seg, self._b, self._e, self._segs = ids, seg_of, begin, end, segs
+
+    def __len__(self):
+        return len(self.ids)
+
+    def __getitem__(self, p):
+        if isinstance(p, slice):
+            return [self[i] for i in range(*p.indices(len(self)))]
+        if p < 0:
+            p += len(self)
+        if not 0 <= p < len(self):
+            raise IndexError(p)
+        m = self._segs[self._seg[p]][self._b[p]:self._e[p]]
+        return PairMatches(int(self.ids[p, 0]), int(self.ids[p, 1]), m)
+
+    def flat(self):
+        counts = (self._e - self._b).astype(np.int64)
+        offs = np.zeros(len(self.ids) + 1, np.uint64)
+        np.cumsum(counts, out=offs[1:])
+        parts = [self._segs[s][b:e] for s, b, e in zip(self._seg, self._b, self._e) if e > b]
+        m = np.ascontiguousarray(np.concatenate(parts), np.int32) if parts else np.zeros((0, 2), np.int32)
+        return self.ids, offs, m
+
+
 def gather_results(res: ExecutionResult, rank: int, world: int, barrier, tag: str):
-    """Gathers every rank's match lists to rank 0 through shared memory.
-    `barrier()` synchronises the ranks (torch.distributed).  Returns the
-    merged (pair_ids, offsets, matches, metrics list) on rank 0, None elsewhere."""
+    """Gathers every rank's match lists to rank 0 through shared memory (one
+    node): each rank writes its result -- pair ids, offsets, matches, in
+    IdPair order -- into a /dev/shm segment with one write per array; rank
+    0 maps the segments (no copy) and orders the pairs by IdPair.
+    `barrier()` synchronises the ranks (torch.distributed).  Returns
+    (GatheredPairs, [per-rank metrics]) on rank 0, None elsewhere."""
     import pickle  # metrics only (a few integers per rank)
 
     ids, offs, m = result_flat(res)
     path = os.path.join(_shm_dir(), f"bmg_gather_{tag}_{rank}")
-    hdr = np.array([len(ids), len(m)], np.uint64)
+    met = pickle.dumps(res.metrics)
+    hdr = np.array([len(ids), len(m), len(met)], np.uint64)
     with open(path, "wb") as f:
-        f.write(hdr.tobytes())
-        f.write(np.ascontiguousarray(ids, np.uint64).tobytes())
-        f.write(np.ascontiguousarray(offs, np.uint64).tobytes())
-        f.write(np.ascontiguousarray(m, np.int32).tobytes())
-        f.write(pickle.dumps(res.metrics))
+        for arr in (hdr, np.ascontiguousarray(ids, np.uint64), np.ascontiguousarray(offs, np.uint64),
+                    np.ascontiguousarray(m, np.int32)):
+            f.write(memoryview(arr).cast("B"))
+        f.write(met)
     barrier()
     out = None
     if rank == 0:
-        all_ids, all_counts, all_starts, all_m, mets = [], [], [], [], []
-        base = 0
+        all_ids, all_b, all_e, all_seg, segs, mets = [], [], [], [], [], []
         for r in range(world):
             p = os.path.join(_shm_dir(), f"bmg_gather_{tag}_{r}")
-            raw = np.fromfile(p, np.uint8)
-            P, M = (int(x) for x in raw[:16].view(np.uint64))
-            o = 16
+            raw = np.memmap(p, np.uint8, mode="r")
+            P, M, K = (int(x) for x in raw[:24].view(np.uint64))
+            o = 24
             ids_r = raw[o:o + 16 * P].view(np.uint64).reshape(-1, 2)
             o += 16 * P
             offs_r = raw[o:o + 8 * (P + 1)].view(np.uint64).astype(np.int64)
             o += 8 * (P + 1)
-            m_r = raw[o:o + 8 * M].view(np.int32).reshape(-1, 2)
+            segs.append(raw[o:o + 8 * M].view(np.int32).reshape(-1, 2))
             o += 8 * M
-            mets.append(pickle.loads(raw[o:].tobytes()))
+            mets.append(pickle.loads(bytes(raw[o:o + K])))
             all_ids.append(ids_r)
-            all_counts.append(np.diff(offs_r))
-            all_starts.append(offs_r[:-1] + base)  # run starts in the concatenated logs
-            all_m.append(m_r)
-            base += M
+            all_b.append(offs_r[:-1])
+            all_e.append(offs_r[1:])
+            all_seg.append(np.full(P, r, np.int32))
         ids = np.concatenate(all_ids)
-        counts = np.concatenate(all_counts)
-        starts = np.concatenate(all_starts)
-        mall = np.concatenate(all_m)
         order = np.lexsort((ids[:, 1], ids[:, 0]))
-        ids, counts, starts = ids[order], counts[order], starts[order]
-        offs = np.zeros(len(ids) + 1, np.uint64)
-        np.cumsum(counts, out=offs[1:])
-        total = int(counts.sum())
-        if total:
-            # each pair's run, in IdPair order, from the concatenated logs
-            first = offs[:-1].astype(np.int64)
-            merged = mall[np.repeat(starts - first, counts) + np.arange(total)]
-        else:
-            merged = np.zeros((0, 2), np.int32)
-        out = (ids, offs, np.ascontiguousarray(merged), mets)
+        out = (GatheredPairs(np.ascontiguousarray(ids[order]), np.concatenate(all_seg)[order],
+                             np.concatenate(all_b)[order], np.concatenate(all_e)[order], segs), mets)
     barrier()
-    os.unlink(path)
+    os.unlink(path)  # rank 0's mappings stay valid
     return out
 
 
@@ -285,5 +304,5 @@ def execute_plan_distributed(plan: SchedulePlan, features: dict, hf: HashFunctio
     got = gather_results(res, rank, world, dist.barrier, tag)
     if rank != 0:
         return None
-    ids, offs, m, mets = got
-    return ExecutionResult(FlatPairs(ids, offs, m), merge_metrics(mets, plan.strategy))
+    pairs, mets = got
+    return ExecutionResult(pairs, merge_metrics(mets, plan.strategy))

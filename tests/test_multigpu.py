@@ -150,8 +150,10 @@ def test_shared_memory_gather_merges_by_idpair(tmp_path):
         t.start()
     for t in ts:
         t.join()
-    ids, offs, m, mets = out[0]
+    gathered, mets = out[0]
+    ids, offs, m = gathered.flat()
     assert out[1] is None and out[2] is None
+    assert [(pm.query_image, pm.train_image) for pm in gathered] == [tuple(map(int, x)) for x in ids]
     want = sorted((pm.query_image, pm.train_image, pm.matches.tolist()) for p in parts for pm in p.matches)
     got = [(int(ids[i, 0]), int(ids[i, 1]), m[offs[i]:offs[i + 1]].tolist()) for i in range(len(ids))]
     assert got == want

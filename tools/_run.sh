@@ -1,13 +1,8 @@
-out=gpurun_out/r2i; mkdir -p $out
-timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log; tail -2 $out/pytest.log
-grep -E "^FAILED|^E  " $out/pytest.log | head -20
-for cfg in block32 strip500; do
-timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline > $out/$cfg.json 2> $out/$cfg.err
-python - $cfg $out/$cfg.json <<'PY'
-import json, sys
-j = json.loads(open(sys.argv[2]).read())
-print(sys.argv[1], "value", round(j["value"]), "ms", round(j["ms_per_step"],3), "e2e", round(j["e2e"]["value"]), "e2e_ms", round(j["e2e"]["ms_per_step"],2),
-      "pageable_ms", j["e2e_pageable"] and round(j["e2e_pageable"]["ms_per_step"],2), "files_ms", j["e2e_files"] and round(j["e2e_files"]["ms_per_step"],2))
-print({k: round(v, 3) for k, v in j["kernel_ms_per_step"].items()})
-PY
-done
+out=gpurun_out/r2j; mkdir -p $out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/smi.txt 2>&1
+timeout 900 python bench.py --steps 10 --warmup 3 > $out/bench.json 2> $out/bench.err; echo "bench rc=$?" >> $out/bench.err
+BMG_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 2 > $out/bench_n2.json 2> $out/bench_n2.err; echo "n2 rc=$?" >> $out/bench_n2.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-files > $out/ncu_launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 3 -c 1 -o $out/match python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-files > $out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:project_tc_kernel -s 50 -c 1 -o $out/project python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-files > /dev/null 2>&1
+ls $out; tail -3 $out/bench.err; tail -5 $out/bench_n2.err

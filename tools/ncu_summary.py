@@ -78,13 +78,14 @@ def main():
     ap.add_argument("--codes")
     ap.add_argument("--launches")
     ap.add_argument("--rep", action="append", default=[], help="key=path.ncu-rep (any kernel)")
+    ap.add_argument("--workload", default="strip500, 3 rows")
     a = ap.parse_args()
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
     summary = {}
     md = [f"# ncu summary ({a.round})", "",
           "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
-          "(gpurun), one launch per kernel, bench.py workload (block32, 2 rows). "
+          f"(gpurun), one launch per kernel, bench.py workload ({a.workload}). "
           "ncu times are cold-cache and serialised: compare shares, not absolutes.", ""]
     reps = [("match_kernel", a.match), ("row_mean_tma_kernel", a.mean), ("codes_kernel", a.codes)]
     reps += [tuple(r.split("=", 1)) for r in a.rep]
