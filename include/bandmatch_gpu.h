@@ -309,6 +309,27 @@ int bmg_read_features(const char* path, uint64_t capacity, float* descriptors_ou
 int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t* pair_ids,
                              const uint64_t* ranges, const int32_t* log, const uint8_t* stages);
 
+/* ---- host verification, stage 1 --------------------- */
+/* sao_filter (verify.cpp:303-341) with the reference's results: the spatial-
+ * angular-order filter over the pair's initial matches, its Bowyer-Watson
+ * Delaunay (verify.cpp:47-107) run with adjacency (walking point location +
+ * cavity growth) instead of the reference's all-triangle scan per point.
+ * matches[2*m] = (query_idx, train_idx); keypoints [n][4] = (x, y, scale,
+ * orientation) as Keypoint (features.hpp); SaoParams n_neighbors (>= 1) and
+ * score_threshold (>= 0) as in verify.hpp.  Outputs per input match: keep
+ * (score <= threshold) and the score; flags: BMG_SAO_*.  InvalidArgument as
+ * the reference raises it.  Host code: no device needed. */
+/* knn_from_delaunay (verify.cpp:135-196): per point its k neighbours by
+ * Delaunay rings (neighbors_out[n][k], -1 padded); *fallback = 1 when the
+ * set could not be triangulated (duplicates, collinear) and plain nearest
+ * neighbours were used.  xy[n][2] doubles (Point2). */
+int bmg_delaunay_knn(const double* xy, uint64_t n, int k, int32_t* neighbors_out, int* fallback);
+#define BMG_SAO_PASSTHROUGH 1u       /* fewer than n_neighbors + 1 matches: all kept */
+#define BMG_SAO_DELAUNAY_FALLBACK 2u /* a side could not be triangulated: plain k-NN */
+int bmg_sao_filter(const int32_t* matches, uint64_t n_matches, const float* query_keypoints,
+                   uint64_t n_query, const float* train_keypoints, uint64_t n_train, int n_neighbors,
+                   double score_threshold, uint8_t* keep_out, double* scores_out, uint32_t* flags_out);
+
 /* ---- instrumentation ------------------------------------------------------ */
 /* Number of kernels this context has launched so far. */
 uint64_t bmg_launch_count(bmg_context* ctx);

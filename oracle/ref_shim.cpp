@@ -19,6 +19,7 @@
 #include "bandmatch/features.hpp"
 #include "bandmatch/hashmatch.hpp"
 #include "bandmatch/mbr.hpp"
+#include "bandmatch/verify.hpp"
 #include "bandmatch/view_graph.hpp"
 
 using namespace bandmatch;
@@ -407,6 +408,50 @@ uint64_t ref_features_count(void* h, uint64_t id) {
   const auto& f = static_cast<FeatureTable*>(h)->features;
   const auto it = f.find(id);
   return it == f.end() ? 0 : it->second.size();
+}
+
+// ---- verification stage 1 (verify.cpp:135-341, compiled from the reference) --
+
+// knn_from_delaunay: neighbors_out[n * k] (-1 padded), fallback flag
+int ref_knn_from_delaunay(const double* xy, uint64_t n, int k, int32_t* neighbors_out, int* fallback_out) {
+  return guarded([&] {
+    std::vector<Point2> pts(n);
+    for (uint64_t i = 0; i < n; ++i) pts[i] = Point2{xy[2 * i], xy[2 * i + 1]};
+    const DelaunayKnn d = knn_from_delaunay(pts, k);
+    for (uint64_t i = 0; i < n; ++i)
+      for (int j = 0; j < k; ++j)
+        neighbors_out[i * k + j] = j < static_cast<int>(d.neighbors[i].size()) ? d.neighbors[i][j] : -1;
+    *fallback_out = d.used_fallback ? 1 : 0;
+  });
+}
+
+// sao_filter: keep_out[m], scores_out[m], flags (1 passthrough, 2 fallback)
+int ref_sao_filter(const int32_t* matches, uint64_t m, const float* qkp, uint64_t nq, const float* tkp,
+                   uint64_t nt, int n_neighbors, double threshold, uint8_t* keep_out, double* scores_out,
+                   uint32_t* flags_out) {
+  return guarded([&] {
+    PairMatches pm;
+    for (uint64_t i = 0; i < m; ++i) pm.matches.emplace_back(matches[2 * i], matches[2 * i + 1]);
+    auto kps = [](const float* k, uint64_t n) {
+      std::vector<Keypoint> v(n);
+      for (uint64_t i = 0; i < n; ++i) v[i] = Keypoint{k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]};
+      return v;
+    };
+    SaoParams sp;
+    sp.n_neighbors = n_neighbors;
+    sp.score_threshold = threshold;
+    const SaoOutcome o = sao_filter(pm, kps(qkp, nq), kps(tkp, nt), sp);
+    // kept matches are the input ones with score <= threshold, in input order
+    size_t k = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+      const bool kept = k < o.kept.matches.size() && o.kept.matches[k] == pm.matches[i] &&
+                        (o.passthrough || o.scores[i] <= threshold);
+      keep_out[i] = kept ? 1 : 0;
+      k += kept ? 1 : 0;
+      scores_out[i] = o.scores[i];
+    }
+    *flags_out = (o.passthrough ? 1u : 0u) | (o.delaunay_fallback ? 2u : 0u);
+  });
 }
 
 // File formats: the reference's own writers and

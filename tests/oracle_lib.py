@@ -188,11 +188,40 @@ class Reference:
         L.ref_features_count.restype = C.c_uint64
         L.ref_features_count.argtypes = [C.c_void_p, C.c_uint64]
 
+        L.ref_knn_from_delaunay.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p,
+                                            C.POINTER(C.c_int)]
+        L.ref_sao_filter.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                     C.c_uint64, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                     C.POINTER(C.c_uint32)]
         L.ref_write_features.argtypes = [C.c_char_p, C.c_uint64, _f32p, _f32p, C.c_uint64]
         L.ref_read_features.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64),
                                         C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
         L.ref_write_matches_binary.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                                C.c_void_p, C.c_void_p]
+
+    def knn_from_delaunay(self, pts, k):
+        """knn_from_delaunay (verify.cpp:135-196): (neighbors [n][k] padded
+        with -1, used_fallback)."""
+        xy = _arr(pts, np.float64).reshape(-1, 2)
+        n = len(xy)
+        out = np.full(max(n * k, 1), -1, np.int32)
+        fb = C.c_int(0)
+        self._check(self.lib.ref_knn_from_delaunay(xy.ctypes.data, n, k, out.ctypes.data, C.byref(fb)))
+        return out[: n * k].reshape(n, k), bool(fb.value)
+
+    def sao_filter(self, matches, qkp, tkp, n_neighbors=6, threshold=0.5):
+        """sao_filter (verify.cpp:303-341): (keep mask, scores, passthrough,
+        fallback)."""
+        m = _arr(matches, np.int32).reshape(-1, 2)
+        qk = _arr(qkp, np.float32).reshape(-1, 4)
+        tk = _arr(tkp, np.float32).reshape(-1, 4)
+        keep = np.zeros(max(len(m), 1), np.uint8)
+        scores = np.zeros(max(len(m), 1), np.float64)
+        fl = C.c_uint32(0)
+        self._check(self.lib.ref_sao_filter(m.ctypes.data, len(m), qk.ctypes.data, len(qk), tk.ctypes.data,
+                                            len(tk), n_neighbors, threshold, keep.ctypes.data,
+                                            scores.ctypes.data, C.byref(fl)))
+        return keep[: len(m)].astype(bool), scores[: len(m)], bool(fl.value & 1), bool(fl.value & 2)
 
     def write_features(self, path, image_id, desc, kp):
         desc = _arr(desc, np.float32)
