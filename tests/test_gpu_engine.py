@@ -177,3 +177,45 @@ def test_result_match_file_byte_identical_to_reference(reference, tmp_path):
     bm.write_matches_binary(ours, res.matches)
     reference.write_matches_binary(theirs, [(q, t, m) for (q, t), m in ref.items()])
     assert ours.read_bytes() == theirs.read_bytes()
+
+
+def test_image_needed_again_after_its_eviction(reference, tmp_path):
+    """Row 0 evicts image 0, row 1 of the same iteration needs it again and
+    does not evict it: the reference's arena re-uploads it
+    (counters and hooks), keeps it resident afterwards, and a second call
+    starts from that state."""
+    imgs, _ = reference.generate_synthetic(4, 500, 2, 0.02, 0.2, 5)
+    B = bm.ScheduleBlock
+    rows = [bm.BlockRow(0, [0], [B(0, 1, [0], [1], [(0, 1)])], [0]),
+            bm.BlockRow(1, [0], [B(1, 2, [0], [2], [(0, 2)])], [])]
+    plan = bm.SchedulePlan("custom", 2, 4, 4, [bm.ScheduleIteration(4, 0, 0, rows)])
+    plan_path = tmp_path / "plan.json"
+    bm.write_plan(plan_path, plan)
+    hseed = bm.seed_for(42, "matching")
+    feats = {i: bm.FeatureSet(i, d) for i, d in enumerate(imgs)}
+    cap = 10 ** 6
+    ref, rc, _ = reference.execute_plan(plan_path, dict(enumerate(imgs)), hseed, capacity_units=cap)
+    arena = bm.DeviceArena(cap, bm.make_hash_functions(hseed))
+    ups, evs = [], []
+    opts = bm.ExecuteOptions(on_upload=lambda i, n: ups.append(i), on_evict=lambda i: evs.append(i))
+    res = bm.execute_plan(plan, feats, arena, opts)
+    met = res.metrics
+    assert (met.uploads, met.evictions, met.units_uploaded, met.peak_occupancy) == (
+        rc["uploads"], rc["evictions"], rc["units_uploaded"], rc["peak_occupancy"])
+    assert ups == [0, 1, 0, 2] and evs == [0]
+    assert all(arena.resident(i) for i in (0, 1, 2))
+    assert arena.occupancy() == sum(len(imgs[i]) for i in (0, 1, 2))
+    got = {(pm.query_image, pm.train_image): pm.matches for pm in res.matches}
+    for key, m in ref.items():
+        assert np.array_equal(got[key], m), key
+    # second call: 0, 1, 2 resident -> row 0 uploads nothing, evicts 0; row 1
+    # re-uploads 0
+    ups.clear()
+    evs.clear()
+    res2 = bm.execute_plan(plan, feats, arena, opts)
+    assert ups == [0] and evs == [0]
+    assert res2.metrics.uploads == 5 and res2.metrics.evictions == 2
+    for pm in res2.matches:
+        assert np.array_equal(pm.matches, got[pm.query_image, pm.train_image])
+    arena.evict(0)  # still resident in the arena: NotResident would be the bug
+    assert not arena.resident(0)

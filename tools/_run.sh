@@ -1,8 +1,10 @@
-out=gpurun_out/r2j; mkdir -p $out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $out/smi.txt 2>&1
-timeout 900 python bench.py --steps 10 --warmup 3 > $out/bench.json 2> $out/bench.err; echo "bench rc=$?" >> $out/bench.err
-BMG_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 2 > $out/bench_n2.json 2> $out/bench_n2.err; echo "n2 rc=$?" >> $out/bench_n2.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-files > $out/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 3 -c 1 -o $out/match python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-files > $out/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:project_tc_kernel -s 50 -c 1 -o $out/project python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-files > /dev/null 2>&1
-ls $out; tail -3 $out/bench.err; tail -5 $out/bench_n2.err
+out=gpurun_out/r2k; mkdir -p $out
+BMG_MATCH_ORDER=bucket timeout 900 python -m pytest tests/test_gpu_match.py tests/test_gpu_parity.py tests/test_gpu_engine.py -q -p no:cacheprovider -x > $out/pytest_bucket.log 2>&1; echo "rc=$?" >> $out/pytest_bucket.log; tail -2 $out/pytest_bucket.log
+for rep in 1 2; do for o in index bucket; do for cfg in block32 strip500; do
+BMG_MATCH_ORDER=$o timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --no-files > $out/${o}_$cfg.json 2> $out/${o}_$cfg.err
+python - $o $cfg $out/${o}_$cfg.json <<'PY'
+import json, sys
+j = json.loads(open(sys.argv[3]).read()); k = j["kernel_ms_per_step"]
+print(f"{sys.argv[1]:7s} {sys.argv[2]:9s} value {j['value']:9.0f} e2e {j['e2e']['value']:9.0f} match {k['match']:.3f} ms/step  ms/step {j['ms_per_step']:.3f}")
+PY
+done; done; done
