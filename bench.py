@@ -83,6 +83,7 @@ def parse():
     p.add_argument("--config", choices=list(CONFIGS), default="strip500")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-files", action="store_true", help="skip the .feat-file e2e leg")
+    p.add_argument("--no-retrieval", action="store_true", help="skip the VLAD encoding leg (f4)")
     return p.parse_args()
 
 
@@ -449,6 +450,52 @@ def parity_leg(feats, plan_path, rows, config, gpu_flat, cores):
     return cpu, par
 
 
+def retrieval_leg(bm, m, feats, cores, cpu=True, cpu_images=32):
+    """encode_vlad (retrieval.cpp:160-205) of every bench
+    image on the B200 (bmg_encode_vlad, pageable FeatureSets as select_pairs
+    passes them, and pinned) against the compiled reference's encode_vlad on
+    the host cores over a sample, with bit-exact parity on the sample.  The
+    codebook is 64 descriptors sampled from the images (train_codebook's
+    initial centroids; retrieval.cpp:66-96)."""
+    import ctypes as C
+    import torch
+    imgs = [feats[i].descriptors for i in sorted(feats)]
+    rng = np.random.default_rng(64)
+    pool = np.concatenate([im[rng.integers(0, len(im), 4)] for im in imgs])
+    cent = np.ascontiguousarray(pool[rng.choice(len(pool), 64, replace=False)], np.float32)
+    cb = bm.Codebook(64, cent)
+    L = bm.load()
+    bm.encode_vlad_batch(imgs[:4], cb, m)
+    t = time.perf_counter()
+    got = bm.encode_vlad_batch(imgs, cb, m)
+    e2e_pageable = time.perf_counter() - t
+    pinned = [torch.from_numpy(a).pin_memory().numpy() for a in imgs]
+    L.bmg_set_profiling(m.handle, 1)  # (clears earlier timers)
+    t = time.perf_counter()
+    bm.encode_vlad_batch(pinned, cb, m)
+    e2e_pinned = time.perf_counter() - t
+    tot, cnt = C.c_double(0), C.c_uint64(0)
+    L.bmg_kernel_time(m.handle, b"vlad", C.byref(tot), C.byref(cnt))
+    L.bmg_set_profiling(m.handle, 0)
+    n = len(imgs)
+    out = {"workload": f"encode_vlad of the {n} bench images (k_words 64)", "unit": "images/s",
+           "e2e_pageable": n / e2e_pageable, "e2e_pinned": n / e2e_pinned,
+           "kernels": n / (tot.value / 1e3) if tot.value > 0 else None,
+           "h2d_bytes": int(sum(a.nbytes for a in imgs))}
+    if cpu:
+        ref = _reference()
+        k = min(cpu_images, n)
+        t = time.perf_counter()
+        vals, degs = ref.encode_vlad_batch(imgs[:k], cent, threads=cores)
+        dt = time.perf_counter() - t
+        eq = all(np.array_equal(got[i].values.view(np.uint32), vals[i].view(np.uint32))
+                 and got[i].degenerate == degs[i] for i in range(k))
+        out["cpu_baseline"] = {"value": k / dt, "unit": "images/s", "cores": cores, "kind": "reference",
+                               "sample": f"first {k} images"}
+        out["parity"] = "equal" if eq else "DIFFERENT"
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -755,7 +802,12 @@ def main():
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
-    elif rank == 0 and world > 1:
+    if rank == 0 and world == 1 and not args.no_retrieval:
+        try:
+            line["retrieval"] = retrieval_leg(bm, m, feats, cores, cpu=not args.no_cpu_baseline)
+        except Exception as e:  # noqa: BLE001
+            line["retrieval"] = {"unavailable": str(e)}
+    if rank == 0 and world > 1:
         gi, go, gm = gpu_flat
         line["parity"] = {"status": "gathered result digest (compare with the N=1 line's digest_gpu)",
                           "digest_gpu": digest(gi, go, gm), "pairs": int(len(gi)), "matches": int(len(gm))}

@@ -15,6 +15,10 @@
 //   execute_plan(plan, feats, hf, arena,   | bandmatch_b200::execute_plan(ctx, plan, feats, hf,
 //                opts, graph)              |                              arena, opts, graph)
 //     engine.cpp:411-527                   |   (call sites: bandmatch_cli.cpp:234, :278)
+//   encode_vlad(fs, cb) per image          | bandmatch_b200::encode_vlad_batch(ctx, feats, cb)
+//     retrieval.cpp:160-205                |
+//   select_pairs(feats, cb, top_n, hnsw,   | bandmatch_b200::select_pairs(ctx, feats, cb, top_n,
+//                seed) retrieval.cpp:386   |                              hnsw, seed)
 //
 // The caller's DeviceArena is kept in step with the HBM arena through the
 // DeviceBackend hooks (engine.hpp:98-104), so its counters, CapacityExceeded
@@ -44,6 +48,7 @@
 
 #include "bandmatch/engine.hpp"
 #include "bandmatch/hashmatch.hpp"
+#include "bandmatch/retrieval.hpp"
 #include "bandmatch_gpu.h"
 
 namespace bandmatch_b200 {
@@ -390,6 +395,59 @@ inline bandmatch::ExecutionResult execute_plan(
   res.metrics.wall_time_s = wall;
   res.metrics.pairs_per_second = wall > 0.0 ? res.metrics.pairs_matched / wall : 0.0;
   return res;
+}
+
+// ---- retrieval -----------------------------------------
+
+// encode_vlad (retrieval.cpp:160-205) of every image in one device call
+// (bit-exact with the reference's per-image encode_vlad).
+inline std::vector<bandmatch::VladVector> encode_vlad_batch(Context& ctx,
+                                                            const std::vector<bandmatch::FeatureSet>& features,
+                                                            const bandmatch::Codebook& cb) {
+  std::vector<bmg_feature_view> views(features.size());
+  for (std::size_t i = 0; i < features.size(); ++i)
+    views[i] = {features[i].image_id, desc_ptr(features[i]), features[i].size()};
+  const std::size_t dim = static_cast<std::size_t>(std::max(cb.k_words, 0)) * bandmatch::kDescriptorDim;
+  std::vector<float> vals(std::max<std::size_t>(features.size() * dim, 1));
+  std::vector<std::uint8_t> deg(std::max<std::size_t>(features.size(), 1));
+  check(bmg_encode_vlad(ctx.get(), cb.centroids.data(), cb.k_words, views.data(), views.size(), vals.data(),
+                        deg.data()));
+  std::vector<bandmatch::VladVector> out(features.size());
+  for (std::size_t i = 0; i < features.size(); ++i) {
+    out[i].values.assign(vals.begin() + i * dim, vals.begin() + (i + 1) * dim);
+    out[i].degenerate = deg[i] != 0;
+  }
+  return out;
+}
+
+// select_pairs (retrieval.cpp:386-415) with its per-image encode_vlad loop
+// (:397-398) replaced by the batched GPU encoder; the HNSW index and the
+// neighbour union are the reference's own code.
+inline bandmatch::ViewGraph select_pairs(Context& ctx, const std::vector<bandmatch::FeatureSet>& features,
+                                         const bandmatch::Codebook& cb, int retrieval_top_n,
+                                         const bandmatch::HnswParams& params, std::uint64_t seed) {
+  if (retrieval_top_n < 1) bandmatch::fail("InvalidArgument", "retrieval_top_n must be >= 1");
+  std::vector<bandmatch::ImageId> ids;
+  ids.reserve(features.size());
+  for (const bandmatch::FeatureSet& fs : features) ids.push_back(fs.image_id);
+  bandmatch::ViewGraph g{std::move(ids)};
+  const int n = static_cast<int>(features.size());
+  if (n <= 1) return g;
+  const std::vector<bandmatch::VladVector> vlads = encode_vlad_batch(ctx, features, cb);
+  bandmatch::HnswIndex index(cb.k_words * bandmatch::kDescriptorDim, params,
+                             bandmatch::seed_for(seed, "retrieval.hnsw"));
+  for (int i = 0; i < n; ++i) index.insert(i, vlads[i].values);
+  for (int i = 0; i < n; ++i) {
+    const auto found = index.search(vlads[i].values, retrieval_top_n + 1);
+    int added = 0;
+    for (const auto& [j, d] : found) {
+      if (j == i) continue;
+      if (added == retrieval_top_n) break;
+      g.add_edge(i, j);
+      ++added;
+    }
+  }
+  return g;
 }
 
 }  // namespace bandmatch_b200

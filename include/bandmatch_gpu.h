@@ -319,6 +319,18 @@ int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t*
  * score_threshold (>= 0) as in verify.hpp.  Outputs per input match: keep
  * (score <= threshold) and the score; flags: BMG_SAO_*.  InvalidArgument as
  * the reference raises it.  Host code: no device needed. */
+/* Retrieval: encode_vlad (retrieval.hpp:36-47, retrieval.cpp:160-205) for a
+ * batch of images -- what select_pairs (retrieval.cpp:386-399) calls once per
+ * image.  centroids: float[k_words][128] (Codebook::centroids); images[i]:
+ * its descriptors (pinned or pageable host memory; image_id is ignored);
+ * values_out: float[n_images][k_words*128] (VladVector::values);
+ * degenerate_out: uint8[n_images].  Bit-exact with the reference (nearest
+ * centroid, FP64 residual sums in descriptor order, signed square root,
+ * sequential norm).  InvalidArgument "codebook has no words" for k_words < 1;
+ * Unsupported for k_words > 1024. */
+int bmg_encode_vlad(bmg_context* ctx, const float* centroids, int k_words, const bmg_feature_view* images,
+                    uint64_t n_images, float* values_out, uint8_t* degenerate_out);
+
 /* knn_from_delaunay (verify.cpp:135-196): per point its k neighbours by
  * Delaunay rings (neighbors_out[n][k], -1 padded); *fallback = 1 when the
  * set could not be triangulated (duplicates, collinear) and plain nearest

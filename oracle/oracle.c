@@ -350,3 +350,58 @@ int orc_brute_force_match(const float* qdesc, uint64_t nq, const float* tdesc, u
   *out_count = n_out;
   return ORC_OK;
 }
+
+/* encode_vlad -- retrieval.cpp:160-205.  Nearest centroid by the sequential
+ * FP64 squared distance with strict < from +inf (:170-183), residuals summed
+ * in FP64 in descriptor order (:184-187), signed square root and sequential
+ * norm (:189-195), degenerate on an empty image or norm2 <= 0 (:165-168,
+ * :196-199), then float(acc * (1/sqrt(norm2))) (:200-202). */
+int orc_encode_vlad(const float* centroids, int k_words, const float* desc, uint64_t n,
+                    float* values_out, uint8_t* degenerate_out) {
+  if (k_words < 1) return ORC_INVALID_ARGUMENT;
+  const size_t dim = (size_t)k_words * ORC_DIM;
+  for (size_t i = 0; i < dim; ++i) values_out[i] = 0.0f;
+  *degenerate_out = 0;
+  if (n == 0) {
+    *degenerate_out = 1;
+    return ORC_OK;
+  }
+  double* acc = (double*)calloc(dim, sizeof(double));
+  if (!acc) return ORC_INVALID_ARGUMENT;
+  for (uint64_t i = 0; i < n; ++i) {
+    const float* d = desc + i * ORC_DIM;
+    int best = 0;
+    double best_d2 = INFINITY;
+    for (int k = 0; k < k_words; ++k) {
+      const float* c = centroids + (size_t)k * ORC_DIM;
+      double s = 0.0;
+      for (int j = 0; j < ORC_DIM; ++j) {
+        const double diff = (double)d[j] - (double)c[j];
+        s += diff * diff;
+      }
+      if (s < best_d2) {
+        best_d2 = s;
+        best = k;
+      }
+    }
+    double* slot = acc + (size_t)best * ORC_DIM;
+    const float* c = centroids + (size_t)best * ORC_DIM;
+    for (int j = 0; j < ORC_DIM; ++j) slot[j] += (double)d[j] - (double)c[j];
+  }
+  double norm2 = 0.0;
+  for (size_t i = 0; i < dim; ++i) {
+    double v = acc[i];
+    v = v >= 0.0 ? sqrt(v) : -sqrt(-v);
+    acc[i] = v;
+    norm2 += v * v;
+  }
+  if (norm2 <= 0.0) {
+    *degenerate_out = 1;
+    free(acc);
+    return ORC_OK;
+  }
+  const double inv = 1.0 / sqrt(norm2);
+  for (size_t i = 0; i < dim; ++i) values_out[i] = (float)(acc[i] * inv);
+  free(acc);
+  return ORC_OK;
+}

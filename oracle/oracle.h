@@ -83,6 +83,12 @@ int orc_match_pair(const float* qdesc, uint64_t nq, const uint32_t* qcoarse,
 int orc_brute_force_match(const float* qdesc, uint64_t nq, const float* tdesc, uint64_t nt,
                           double ratio, int32_t* out_pairs, uint64_t* out_count);
 
+/* encode_vlad -- retrieval.cpp:160-205.  centroids
+ * [k_words][128]; values_out[k_words*128]; returns ORC_INVALID_ARGUMENT for
+ * k_words < 1 ("codebook has no words"). */
+int orc_encode_vlad(const float* centroids, int k_words, const float* desc, uint64_t n,
+                    float* values_out, uint8_t* degenerate_out);
+
 #ifdef __cplusplus
 }
 #endif

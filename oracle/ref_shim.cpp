@@ -19,6 +19,7 @@
 #include "bandmatch/features.hpp"
 #include "bandmatch/hashmatch.hpp"
 #include "bandmatch/mbr.hpp"
+#include "bandmatch/retrieval.hpp"
 #include "bandmatch/verify.hpp"
 #include "bandmatch/view_graph.hpp"
 
@@ -37,6 +38,8 @@ int status_of(const std::string& code) {
   if (code == "BudgetTooSmall") return 6;
   if (code == "EmptyGraph") return 7;
   if (code == "TruncatedFile") return 8;
+  if (code == "TooFewDescriptors") return 9;
+  if (code == "EmptyInput") return 10;
   return 99;
 }
 
@@ -451,6 +454,75 @@ int ref_sao_filter(const int32_t* matches, uint64_t m, const float* qkp, uint64_
       scores_out[i] = o.scores[i];
     }
     *flags_out = (o.passthrough ? 1u : 0u) | (o.delaunay_fallback ? 2u : 0u);
+  });
+}
+
+// ---- retrieval (retrieval.cpp:14-205, compiled from the reference) --------
+
+// encode_vlad: values_out[k_words * 128], degenerate_out
+int ref_encode_vlad(const float* centroids, int k_words, const float* desc, uint64_t n, float* values_out,
+                    uint8_t* degenerate_out) {
+  return guarded([&] {
+    Codebook cb;
+    cb.k_words = k_words;
+    cb.centroids.assign(centroids, centroids + static_cast<size_t>(std::max(k_words, 0)) * kDescriptorDim);
+    FeatureSet fs;
+    fs.descriptors.resize(n);
+    fs.keypoints.resize(n);
+    if (n) std::memcpy(fs.descriptors.data(), desc, n * kDescriptorDim * sizeof(float));
+    const VladVector v = encode_vlad(fs, cb);
+    std::memcpy(values_out, v.values.data(), v.values.size() * sizeof(float));
+    *degenerate_out = v.degenerate ? 1 : 0;
+  });
+}
+
+// encode_vlad over many images on `threads` host threads (the select_pairs
+// loop, retrieval.cpp:397-398, spread over cores): the CPU baseline
+int ref_encode_vlad_batch(const float* centroids, int k_words, const float* const* descs, const uint64_t* counts,
+                          uint64_t n_images, int threads, float* values_out, uint8_t* degenerate_out) {
+  return guarded([&] {
+    Codebook cb;
+    cb.k_words = k_words;
+    cb.centroids.assign(centroids, centroids + static_cast<size_t>(std::max(k_words, 0)) * kDescriptorDim);
+    const size_t dim = static_cast<size_t>(k_words) * kDescriptorDim;
+    std::atomic<uint64_t> next{0};
+    std::vector<std::string> errs(std::max(threads, 1));
+    auto work = [&](int w) {
+      try {
+        for (uint64_t i; (i = next.fetch_add(1)) < n_images;) {
+          FeatureSet fs;
+          fs.descriptors.resize(counts[i]);
+          fs.keypoints.resize(counts[i]);
+          if (counts[i]) std::memcpy(fs.descriptors.data(), descs[i], counts[i] * kDescriptorDim * sizeof(float));
+          const VladVector v = encode_vlad(fs, cb);
+          std::memcpy(values_out + i * dim, v.values.data(), dim * sizeof(float));
+          degenerate_out[i] = v.degenerate ? 1 : 0;
+        }
+      } catch (const std::exception& e) {
+        errs[w] = e.what();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < threads; ++w) pool.emplace_back(work, w);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+  });
+}
+
+// train_codebook on descriptors [n][128]: centroids_out[k_words * 128],
+// sse_out[max_iters] (entries written: *n_sse)
+int ref_train_codebook(const float* desc, uint64_t n, int k_words, int max_iters, uint64_t seed,
+                       float* centroids_out, double* sse_out, int* n_sse) {
+  return guarded([&] {
+    std::vector<Descriptor> d(n);
+    if (n) std::memcpy(d.data(), desc, n * kDescriptorDim * sizeof(float));
+    std::vector<double> hist;
+    const Codebook cb = train_codebook(d, k_words, max_iters, seed, &hist);
+    std::memcpy(centroids_out, cb.centroids.data(), cb.centroids.size() * sizeof(float));
+    for (size_t i = 0; i < hist.size(); ++i) sse_out[i] = hist[i];
+    *n_sse = static_cast<int>(hist.size());
   });
 }
 

@@ -15,5 +15,7 @@ from .hashmatch import (FeatureSet, HashCodeSet, HashFunctions, HashParams, Matc
 from .engine import (BlockRow, DeviceArena, ExecuteOptions, ExecutionResult,  # noqa: F401
                      PipelineMetrics, ScheduleBlock, ScheduleIteration, SchedulePlan,
                      arena_units_for, execute_plan, flatten_plan, read_plan, write_plan)
+from .retrieval import (Codebook, VladVector, encode_vlad, encode_vlad_batch,  # noqa: F401
+                        read_codebook, write_codebook)
 
 __version__ = "0.1.0"

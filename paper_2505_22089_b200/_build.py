@@ -8,7 +8,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libbmg.so"
-SOURCES = ["kernels.cu", "bmg_api.cpp", "host_random.cpp", "host_synthetic.cpp", "host_io.cpp", "host_sao.cpp"]
+SOURCES = ["kernels.cu", "vlad.cu", "bmg_api.cpp", "host_random.cpp", "host_synthetic.cpp", "host_io.cpp", "host_sao.cpp"]
 HEADERS = ["bmg_internal.h", "../../include/bandmatch_gpu.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++20",

@@ -98,7 +98,7 @@ EXPORTED = [
     "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
     "bmg_write_matches_binary", "bmg_generate_synthetic_subset", "bmg_set_test_flags",
     "bmg_result_row_timing", "bmg_execute_plan_files", "bmg_sao_filter",
-    "bmg_delaunay_knn",
+    "bmg_delaunay_knn", "bmg_encode_vlad",
 ]
 
 _lib = None
@@ -163,6 +163,7 @@ def load(path: Path = LIB_PATH):
         "bmg_sao_filter": (C.c_int, [vp, u64, vp, u64, vp, u64, C.c_int, C.c_double, vp, vp,
                                      C.POINTER(C.c_uint32)]),
         "bmg_delaunay_knn": (C.c_int, [vp, u64, C.c_int, vp, C.POINTER(C.c_int)]),
+        "bmg_encode_vlad": (C.c_int, [vp, vp, C.c_int, vp, u64, vp, vp]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                              u64, vp, vp]),

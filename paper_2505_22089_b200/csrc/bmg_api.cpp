@@ -2176,6 +2176,162 @@ void bmg_result_free(bmg_result* r) { delete r; }
 
 uint64_t bmg_launch_count(bmg_context* c) { return c ? c->launches : 0; }
 
+// ---- retrieval: encode_vlad (retrieval.cpp:160-205) -----------------------
+// Images are encoded in batches of up to 256 MiB of descriptors on
+// the two row slots' home streams: batch b+1's uploads (pinned sources
+// straight to the copy engine, pageable ones through the staging slots)
+// overlap batch b's kernels; each batch's vectors are written by V3 into
+// mapped pinned memory and copied to the caller's arrays once it completes.
+namespace bmg {
+namespace {
+size_t vlad_batch_bytes() {  // BMG_VLAD_BATCH_BYTES: test hook (multi-batch paths)
+  if (const char* e = std::getenv("BMG_VLAD_BATCH_BYTES")) return std::max<size_t>(std::strtoull(e, nullptr, 10), 1);
+  return size_t(256) << 20;
+}
+struct VladSlot {
+  DevBuf desc, assign, fix, fixcnt, acc, members, member_off, dmeta;
+  HostMapped meta, out;
+  cudaEvent_t done = nullptr;
+  std::vector<uint64_t> imgs;  // caller indices of the batch
+};
+}  // namespace
+}  // namespace bmg
+
+int bmg_encode_vlad(bmg_context* c, const float* centroids, int k_words, const bmg_feature_view* images,
+                    uint64_t n_images, float* values_out, uint8_t* degenerate_out) {
+  using namespace bmg;
+  VladSlot vs[2];
+  auto cleanup = [&] {
+    for (VladSlot& v : vs) {
+      if (v.done) cudaEventSynchronize(v.done);
+      for (DevBuf* b : {&v.desc, &v.assign, &v.fix, &v.fixcnt, &v.acc, &v.members, &v.member_off, &v.dmeta})
+        b->release();
+      v.meta.release();
+      v.out.release();
+      if (v.done) cudaEventDestroy(v.done);
+      v.done = nullptr;
+    }
+  };
+  const int rc = guarded([&] {
+    if (!c) fail(BMG_INVALID_ARGUMENT, "null argument");
+    if (k_words < 1) fail(BMG_INVALID_ARGUMENT, "codebook has no words");  // retrieval.cpp:161
+    if (k_words > kVladMaxWords)
+      fail(BMG_UNSUPPORTED, "codebooks of more than " + std::to_string(kVladMaxWords) +
+                                " words are not supported by the GPU VLAD encoder");
+    if (!centroids || (n_images && (!images || !values_out || !degenerate_out)))
+      fail(BMG_INVALID_ARGUMENT, "null argument");
+    for (uint64_t i = 0; i < n_images; ++i)
+      if (images[i].count && !images[i].descriptors) fail(BMG_INVALID_ARGUMENT, "null descriptors");
+    set_device(*c);
+    const size_t dim = static_cast<size_t>(k_words) * kDim;
+    DevBuf d_cent;
+    d_cent.ensure(dim * sizeof(float));
+    BMG_CUDA(cudaMemcpy(d_cent.p, centroids, dim * sizeof(float), cudaMemcpyHostToDevice));
+    auto drain = [&](VladSlot& v) {
+      if (v.imgs.empty()) return;
+      BMG_CUDA(cudaEventSynchronize(v.done));
+      const float* vals = v.out.host<float>();
+      const uint8_t* deg = reinterpret_cast<const uint8_t*>(vals + v.imgs.size() * dim);
+      for (size_t j = 0; j < v.imgs.size(); ++j) {
+        std::memcpy(values_out + v.imgs[j] * dim, vals + j * dim, dim * sizeof(float));
+        degenerate_out[v.imgs[j]] = deg[j];
+      }
+      v.imgs.clear();
+    };
+    for (VladSlot& v : vs) BMG_CUDA(cudaEventCreateWithFlags(&v.done, cudaEventDisableTiming));
+    int si = 0;
+    const size_t batch_bytes = vlad_batch_bytes();
+    for (uint64_t i0 = 0; i0 < n_images;) {
+      // the batch: images [i0, i1)
+      uint64_t i1 = i0, desc_total = 0, tiles = 0;
+      while (i1 < n_images && (i1 == i0 || (desc_total + images[i1].count) * kDim * sizeof(float) <= batch_bytes)) {
+        desc_total += images[i1].count;
+        tiles += (images[i1].count + kVladTile - 1) / kVladTile;
+        ++i1;
+      }
+      const uint64_t nb = i1 - i0;
+      VladSlot& v = vs[si];
+      RowSlot& rs = c->slot[si];
+      si ^= 1;
+      drain(v);  // the slot's previous batch (its buffers are reused below)
+      v.desc.ensure(std::max<uint64_t>(desc_total, 1) * kDim * sizeof(float));
+      v.assign.ensure(std::max<uint64_t>(desc_total, 1) * sizeof(int32_t));
+      v.fix.ensure(std::max<uint64_t>(desc_total, 1) * sizeof(uint2));
+      v.fixcnt.ensure(16);
+      v.acc.ensure(nb * dim * sizeof(double));
+      v.members.ensure(std::max<uint64_t>(desc_total, 1) * sizeof(uint32_t));
+      v.member_off.ensure(nb * (k_words + 1) * sizeof(uint32_t));
+      const size_t meta_bytes = align_up(nb * sizeof(VladImg) + 2 * std::max<uint64_t>(tiles, 1) * sizeof(uint32_t), 16);
+      v.meta.ensure(meta_bytes);
+      v.dmeta.ensure(meta_bytes);
+      v.out.ensure(nb * dim * sizeof(float) + nb);
+      VladImg* mi = v.meta.host<VladImg>();
+      uint32_t* t_img = reinterpret_cast<uint32_t*>(mi + nb);
+      uint32_t* t_start = t_img + std::max<uint64_t>(tiles, 1);
+      float* dd = v.desc.as<float>();
+      uint64_t off = 0, t = 0;
+      for (uint64_t j = 0; j < nb; ++j) {
+        const bmg_feature_view& f = images[i0 + j];
+        if (f.count > 0xffffffffull) fail(BMG_UNSUPPORTED, "image too large for the VLAD encoder");
+        mi[j].desc = dd + off * kDim;
+        mi[j].n = static_cast<uint32_t>(f.count);
+        mi[j].pad_ = 0;
+        mi[j].assign_off = off;
+        for (uint64_t r = 0; r < f.count; r += kVladTile) {
+          t_img[t] = static_cast<uint32_t>(j);
+          t_start[t] = static_cast<uint32_t>(r);
+          ++t;
+        }
+        stage_h2d(*c, dd + off * kDim, f.descriptors, f.count * kDim * sizeof(float));
+        off += f.count;
+        v.imgs.push_back(i0 + j);
+      }
+      cudaEvent_t copied = take_event(*c);
+      BMG_CUDA(cudaEventRecord(copied, c->s_copy));
+      BMG_CUDA(cudaStreamWaitEvent(rs.home, copied, 0));
+      c->free_events.push_back(copied);
+      // image / tile tables into device memory by a kernel (reading them
+      // over PCIe from every CTA would stall it; a memcpy would queue
+      // behind the bulk uploads on the copy engine)
+      MetaBatch mb{};
+      mb.op[0] = MetaOp{v.dmeta.p, v.meta.dev<void>(), meta_bytes};
+      mb.op[1] = MetaOp{v.fixcnt.p, nullptr, 16};
+      mb.n = 2;
+      launch_meta(mb, rs.home);
+      VladBatch b{};
+      b.imgs = v.dmeta.as<VladImg>();
+      b.tile_img = reinterpret_cast<const uint32_t*>(b.imgs + nb);
+      b.tile_start = b.tile_img + std::max<uint64_t>(tiles, 1);
+      b.centroids = d_cent.as<float>();
+      b.k_words = k_words;
+      b.assign = v.assign.as<int32_t>();
+      b.fix = v.fix.as<uint2>();
+      b.fix_count = v.fixcnt.as<uint32_t>();
+      b.fix_cap = static_cast<uint32_t>(std::max<uint64_t>(desc_total, 1));
+      b.members = v.members.as<uint32_t>();
+      b.member_off = v.member_off.as<uint32_t>();
+      b.acc = v.acc.as<double>();
+      b.values = v.out.dev<float>();
+      b.degenerate = reinterpret_cast<uint8_t*>(b.values + nb * dim);
+      {
+        Timed tm(*c, "vlad", rs.home);
+        launch_vlad(b, static_cast<int>(nb), static_cast<int>(tiles), rs.home);
+        c->launches += tiles ? 6 : 4;
+        check_launch();
+      }
+      BMG_CUDA(cudaEventRecord(v.done, rs.home));
+      i0 = i1;
+    }
+    drain(vs[si]);
+    drain(vs[si ^ 1]);
+    // the staging slots / copy stream are idle again before d_cent goes
+    BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+    d_cent.release();
+  });
+  cleanup();
+  return rc;
+}
+
 int bmg_set_profiling(bmg_context* c, int enabled) {
   return guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null context");
@@ -2196,7 +2352,10 @@ int bmg_kernel_time(bmg_context* c, const char* cls, double* total_ms, uint64_t*
     if (!c || !cls) fail(BMG_INVALID_ARGUMENT, "null argument");
     set_device(*c);
     for (cudaStream_t ps : c->s_proj) BMG_CUDA(cudaStreamSynchronize(ps));
-    for (RowSlot& sl : c->slot) BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
+    for (RowSlot& sl : c->slot) {
+      BMG_CUDA(cudaStreamSynchronize(sl.s_comp));
+      BMG_CUDA(cudaStreamSynchronize(sl.home));
+    }
     double ms = 0.0;
     uint64_t n = 0;
     for (auto& t : c->timers) {

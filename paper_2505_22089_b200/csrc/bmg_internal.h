@@ -171,4 +171,32 @@ constexpr int kMatchQueries = BMG_MATCH_QUERIES;  // queries per match CTA
 int match_queries_per_cta(int fwp, int k);
 int device_sm_count();
 
+// ---- VLAD encoding (vlad.cu; retrieval.cpp:160-205) ----
+struct VladImg {
+  const float* desc;    // [n][128] in the batch buffer
+  uint32_t n, pad_;
+  uint64_t assign_off;  // offset of the image's descriptors in VladBatch::assign
+};
+struct VladBatch {
+  const VladImg* imgs;
+  const uint32_t* tile_img;    // per 128-descriptor tile: image, first descriptor
+  const uint32_t* tile_start;
+  const float* centroids;      // [k_words][128] (Codebook::centroids)
+  int k_words;
+  int32_t* assign;             // nearest centroid per descriptor
+  uint2* fix;                  // (image, descriptor) the FP32 filter could not certify
+  uint32_t* fix_count;         // zeroed before the launch
+  uint32_t fix_cap;
+  uint32_t* members;           // descriptors grouped by cluster, descriptor order (per image at assign_off)
+  uint32_t* member_off;        // [images][k_words+1] cluster starts
+  double* acc;                 // [images][k_words*128] residual sums
+  float* values;               // [images][k_words*128] VladVector::values
+  uint8_t* degenerate;         // [images] VladVector::degenerate
+};
+constexpr int kVladTile = 128;
+constexpr int kVladMaxWords = 1024;  // codebook words the GPU encoder supports
+void launch_vlad(const VladBatch& b, int n_imgs, int n_tiles, cudaStream_t s);
+// certified / FP64 assignments of the last launches (diagnostics)
+size_t vlad_assign_smem_bytes();
+
 }  // namespace bmg

@@ -1736,8 +1736,11 @@ __device__ __forceinline__ int32_t rerank_query(const MatchLaunch& a, const ImgD
   return result;
 }
 
+#ifndef BMG_MATCH_MINB
+#define BMG_MATCH_MINB 1  // resident match CTAs per SM the register budget is sized for
+#endif
 template <int FWP, int KM, int NT, int KC>
-__global__ void __launch_bounds__(NT, 1) match_kernel(MatchLaunch a) {
+__global__ void __launch_bounds__(NT, (KM == 8 ? BMG_MATCH_MINB : 1)) match_kernel(MatchLaunch a) {
   const PairWork w = a.work[blockIdx.x];
   const ImgDev T = a.imgs[w.t_img];
   const ImgDev Q = a.imgs[w.q_img];

@@ -5,6 +5,7 @@
 // exists; the binary travels to the GPU box and is run by
 // tests/test_gpu_binding.py.  Prints PASS/FAIL lines, exits non-zero on FAIL.
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <set>
 #include <vector>
@@ -96,6 +97,29 @@ int main() {
   report(bandmatch_b200::match_pair(ctx, q, gq, t, gt, mp).matches ==
              match_pair(q, rq, t, rt, mp).matches,
          "match_pair (K=3, ratio=0.8) equals the reference");
+
+  // retrieval: encode_vlad per image and select_pairs (retrieval.cpp:160-205,
+  // :386-415) with the GPU encoder, against the reference
+  {
+    std::vector<FeatureSet> fv;
+    for (const auto& [id, fs] : feats) fv.push_back(fs);
+    std::vector<Descriptor> pool;
+    for (const FeatureSet& fs : fv)
+      for (std::size_t i = 0; i < fs.size(); i += 7) pool.push_back(fs.descriptors[i]);
+    const Codebook cb = train_codebook(pool, 16, 8, 11);
+    const std::vector<VladVector> gv = bandmatch_b200::encode_vlad_batch(ctx, fv, cb);
+    bool eq = gv.size() == fv.size();
+    for (std::size_t i = 0; eq && i < fv.size(); ++i) {
+      const VladVector rv = encode_vlad(fv[i], cb);
+      eq = rv.degenerate == gv[i].degenerate &&
+           std::memcmp(rv.values.data(), gv[i].values.data(), rv.values.size() * sizeof(float)) == 0;
+    }
+    report(eq, "encode_vlad_batch equals the reference encode_vlad, bit for bit");
+    HnswParams hp;
+    const ViewGraph rg = select_pairs(fv, cb, 3, hp, 5);
+    const ViewGraph gg = bandmatch_b200::select_pairs(ctx, fv, cb, 3, hp, 5);
+    report(rg.pairs() == gg.pairs(), "select_pairs with the GPU encoder equals the reference");
+  }
 
   // error semantics
   auto code_of = [](auto&& f) -> std::string {

@@ -124,6 +124,19 @@ class Oracle:
             return m, cand[:nq], topk[: nq * k].reshape(nq, k)
         return m
 
+    def encode_vlad(self, desc, centroids):
+        """encode_vlad (retrieval.cpp:160-205): (values [k*128], degenerate)."""
+        c = _arr(centroids, np.float32).reshape(-1, DIM)
+        d = _arr(desc, np.float32).reshape(-1, DIM)
+        k = len(c)
+        out = np.zeros(max(k * DIM, 1), np.float32)
+        deg = np.zeros(1, np.uint8)
+        self.lib.orc_encode_vlad.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
+        rc = self.lib.orc_encode_vlad(c.ctypes.data, k, d.ctypes.data, len(d), out.ctypes.data, deg.ctypes.data)
+        if rc != 0:
+            raise ValueError("InvalidArgument: codebook has no words")
+        return out[: k * DIM], bool(deg[0])
+
     def brute_force_match(self, qdesc, tdesc, ratio=0.5):
         qdesc = _arr(qdesc, np.float32).reshape(-1, DIM)
         tdesc = _arr(tdesc, np.float32).reshape(-1, DIM)
@@ -249,6 +262,46 @@ class Reference:
         self._check(self.lib.ref_write_matches_binary(str(path).encode(), len(pairs), ids.ctypes.data,
                                                       offs.ctypes.data, log.ctypes.data,
                                                       None if st is None else st.ctypes.data))
+
+    def encode_vlad(self, desc, centroids):
+        """the reference encode_vlad: (values [k*128], degenerate)."""
+        c = _arr(centroids, np.float32).reshape(-1, DIM)
+        d = _arr(desc, np.float32).reshape(-1, DIM)
+        k = len(c)
+        out = np.zeros(max(k * DIM, 1), np.float32)
+        deg = np.zeros(1, np.uint8)
+        self.lib.ref_encode_vlad.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
+        self._check(self.lib.ref_encode_vlad(c.ctypes.data, k, d.ctypes.data, len(d), out.ctypes.data,
+                                             deg.ctypes.data))
+        return out[: k * DIM], bool(deg[0])
+
+    def encode_vlad_batch(self, images, centroids, threads=1):
+        """the reference encode_vlad over images on `threads` host threads:
+        (values [n][k*128], degenerate [n])."""
+        c = _arr(centroids, np.float32).reshape(-1, DIM)
+        arrs = [_arr(x, np.float32).reshape(-1, DIM) for x in images]
+        n, k = len(arrs), len(c)
+        ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
+        counts = np.array([len(a) for a in arrs] or [0], np.uint64)
+        out = np.zeros((max(n, 1), k * DIM), np.float32)
+        deg = np.zeros(max(n, 1), np.uint8)
+        self.lib.ref_encode_vlad_batch.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                                   C.c_int, C.c_void_p, C.c_void_p]
+        self._check(self.lib.ref_encode_vlad_batch(c.ctypes.data, k, ptrs, counts.ctypes.data, n, threads,
+                                                   out.ctypes.data, deg.ctypes.data))
+        return out[:n], deg[:n].astype(bool)
+
+    def train_codebook(self, desc, k_words, max_iters=25, seed=0):
+        """the reference train_codebook: (centroids [k][128], sse history)."""
+        d = _arr(desc, np.float32).reshape(-1, DIM)
+        out = np.zeros((k_words, DIM), np.float32)
+        sse = np.zeros(max(max_iters, 1), np.float64)
+        nse = C.c_int(0)
+        self.lib.ref_train_codebook.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_uint64,
+                                                C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
+        self._check(self.lib.ref_train_codebook(d.ctypes.data, len(d), k_words, max_iters, seed,
+                                                out.ctypes.data, sse.ctypes.data, C.byref(nse)))
+        return out, sse[: nse.value]
 
     def _check(self, rc):
         if rc != 0:

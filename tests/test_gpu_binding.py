@@ -16,4 +16,4 @@ def test_reference_api_through_the_binding():
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "FAIL" not in r.stdout and r.stdout.count("PASS") >= 9
+    assert "FAIL" not in r.stdout and r.stdout.count("PASS") >= 11
