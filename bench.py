@@ -458,25 +458,31 @@ def retrieval_leg(bm, m, feats, cores, cpu=True, cpu_images=32):
     codebook is 64 descriptors sampled from the images (train_codebook's
     initial centroids; retrieval.cpp:66-96)."""
     import ctypes as C
-    import torch
     imgs = [feats[i].descriptors for i in sorted(feats)]
     rng = np.random.default_rng(64)
     pool = np.concatenate([im[rng.integers(0, len(im), 4)] for im in imgs])
     cent = np.ascontiguousarray(pool[rng.choice(len(pool), 64, replace=False)], np.float32)
     cb = bm.Codebook(64, cent)
     L = bm.load()
-    bm.encode_vlad_batch(imgs[:4], cb, m)
-    t = time.perf_counter()
-    got = bm.encode_vlad_batch(imgs, cb, m)
-    e2e_pageable = time.perf_counter() - t
-    pinned = [torch.from_numpy(a).pin_memory().numpy() for a in imgs]
+    pageable = [np.array(a) for a in imgs]  # the bench images live in pinned memory
+
+    def best(src, reps=2):
+        bm.encode_vlad_batch(src[:4], cb, m)
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            r = bm.encode_vlad_batch(src, cb, m)
+            ts.append(time.perf_counter() - t)
+        return min(ts), r
+
+    e2e_pageable, got = best(pageable)
+    e2e_pinned, _ = best(imgs)
     L.bmg_set_profiling(m.handle, 1)  # (clears earlier timers)
-    t = time.perf_counter()
-    bm.encode_vlad_batch(pinned, cb, m)
-    e2e_pinned = time.perf_counter() - t
+    bm.encode_vlad_batch(imgs, cb, m)
     tot, cnt = C.c_double(0), C.c_uint64(0)
     L.bmg_kernel_time(m.handle, b"vlad", C.byref(tot), C.byref(cnt))
     L.bmg_set_profiling(m.handle, 0)
+    del pageable
     n = len(imgs)
     out = {"workload": f"encode_vlad of the {n} bench images (k_words 64)", "unit": "images/s",
            "e2e_pageable": n / e2e_pageable, "e2e_pinned": n / e2e_pinned,
