@@ -23,12 +23,15 @@ GPU's shard of config 4.
   parity the GPU match lists of the e2e run against the compiled reference
          (oracle/_ref) run on the same inputs in the cpu_baseline leg
 
-Multi-GPU (torchrun, --gpus N): ONE plan, sharded (paper_2505_22089_b200.
+Multi-GPU (torchrun, --gpus N): the plan is sharded (paper_2505_22089_b200.
 multigpu): rows -- split by pairs where a row is larger than a rank's share --
 are partitioned over the ranks with no collective on the data path; each rank
 generates only the images its shard needs; matches are gathered to rank 0
-through shared memory inside the timed region; times are max over ranks
-(strong scaling).  `--impl reference` times the reference's CPU
+through shared memory inside the timed region; times are max over ranks.
+strip500 weak-scales by default (`--scaling weak`): N GPUs run the same UAV
+strip with 500 N images (bench_data/plan_strip{500N}.json from the
+reference's iterate_schedule, ~5,000 pairs per GPU); `--scaling strong`
+shards the one 500-image plan.  `--impl reference` times the reference's CPU
 implementation (oracle/_ref, the unmodified reference compiled in place) on
 rank 0 with every host core, without loading this package.
 """
@@ -84,7 +87,26 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-files", action="store_true", help="skip the .feat-file e2e leg")
     p.add_argument("--no-retrieval", action="store_true", help="skip the VLAD encoding leg (f4)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="N > 1 with strip500: weak = a strip of 500 N images (~5,000 pairs per GPU), "
+                        "strong = the one 500-image plan sharded")
     return p.parse_args()
+
+
+def resolve_config(config, world, scaling):
+    """(generator n, ppi, band, drop, plan file, scaling label, images per GPU
+    note).  strip500 at N > 1 weak-scales by default: the same UAV strip with
+    500 N images (bench_data/plan_strip{500N}.json, the reference's
+    iterate_schedule), so every GPU gets ~5,000 pairs of its own rows."""
+    n_cfg, ppi, band, drop, plan_file = CONFIGS[config]
+    if config == "strip500" and scaling == "weak":
+        if world > 1:
+            name = f"plan_strip{500 * world}.json"
+            if (ROOT / "bench_data" / name).exists():
+                return 500 * world + drop, ppi, band, drop, name, "weak"
+            return n_cfg, ppi, band, drop, plan_file, "strong"
+        return n_cfg, ppi, band, drop, plan_file, "weak"
+    return n_cfg, ppi, band, drop, plan_file, "strong"
 
 
 def plan_rows(plan_path):
@@ -103,11 +125,13 @@ def plan_rows(plan_path):
     return rows
 
 
-def workload_config(config, n_images, avg_desc, rows):
+def workload_config(config, n_images, avg_desc, rows, resolved=None):
     """The `config` object, identical in both arms."""
     n_pairs = sum(p for p, _ in rows)
-    n_cfg, ppi, band, drop, plan_file = CONFIGS[config]
-    return {"workload": f"{config}: BASELINE config {CONFIG_NO[config]}, {n_images} images x "
+    n_cfg, ppi, band, drop, plan_file = (resolved or CONFIGS[config])[:5]
+    if resolved and resolved[5] == "weak" and plan_file != CONFIGS[config][4]:
+        config = f"{config} weak-scaled ({n_images} images)"
+    return {"workload": f"{config}: BASELINE config {CONFIG_NO[config.split()[0]]}, {n_images} images x "
                         f"{avg_desc:.0f} desc, {n_pairs} pairs, {len(rows)} block rows, "
                         f"iterate_schedule plan {plan_file}, verification off",
             "rows": len(rows), "k_nearest": 8, "ratio": 0.5, "hash": "L=6, m=8, n=128",
@@ -371,7 +395,8 @@ def reference_arm(args):
     mean, compute_codes of its needed images, match_pair of its pairs: the
     row body of engine.cpp:433-489) so the run stays within minutes; value =
     pairs / seconds over the timed steps."""
-    n_cfg, ppi, band, drop, plan_file = CONFIGS[args.config]
+    resolved = resolve_config(args.config, args.gpus, args.scaling)
+    n_cfg, ppi, band, drop, plan_file, scaling = resolved
     plan_path = ROOT / "bench_data" / plan_file
     rows = plan_rows(plan_path)
     cores = os.cpu_count() or 1
@@ -407,10 +432,10 @@ def reference_arm(args):
     v = tot_p / tot_s
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator features.cpp:68-197, oracle/_ref)",
             "impl": "reference",
-            "config": workload_config(args.config, n_images, avg, rows),
+            "config": workload_config(args.config, n_images, avg, rows, resolved),
             "parallelism": f"{cores} host threads over each row's images / pairs",
             "cpu_warmup": warm,
             "host_cpu": cpu_model(),
@@ -518,7 +543,8 @@ def main():
     from paper_2505_22089_b200.engine import _feature_views
     from paper_2505_22089_b200.features import SyntheticScene, generate_synthetic, synthetic_counts
 
-    n_cfg, ppi, band, drop, plan_file = CONFIGS[args.config]
+    resolved = resolve_config(args.config, world, args.scaling)
+    n_cfg, ppi, band, drop, plan_file, scaling = resolved
     plan_path = ROOT / "bench_data" / plan_file
     rows = plan_rows(plan_path)
     cores = os.cpu_count() or 1
@@ -753,9 +779,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32+f64",
             "data": "synthetic (reference generator features.cpp:68-197, seed 7)",
-            "config": workload_config(args.config, n_images, avg_desc, rows),
+            "config": workload_config(args.config, n_images, avg_desc, rows, resolved),
             "parallelism": (f"one plan sharded over {world} GPU(s) by rows / pairs "
                             "(multigpu.shard_plan), no collective on the data path" if world > 1
                             else "1 GPU, two row slots overlapped"),

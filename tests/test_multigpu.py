@@ -124,6 +124,36 @@ def test_shard_balance_on_the_bench_plans():
             assert sorted(p for s in subs for p in s.pairs()) == plan.pairs()
 
 
+def test_weak_scaled_strips_give_every_rank_a_strip500_share():
+    """bench.py --gpus N (strip500, --scaling weak): the 500 N-image strip's
+    shards each carry about the one-GPU strip500 work (pairs and image-rows)."""
+    import importlib.util
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    spec = importlib.util.spec_from_file_location("bench", root / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    one = bm.read_plan(root / "bench_data" / "plan_strip500.json")
+    one_pairs = one.pair_count()
+    one_rows = sum(len(r.needed()) for it in one.iterations for r in it.rows)
+    assert bench.resolve_config("strip500", 1, "weak")[4:] == ("plan_strip500.json", "weak")
+    assert bench.resolve_config("strip500", 2, "strong")[4:] == ("plan_strip500.json", "strong")
+    assert bench.resolve_config("block32", 4, "weak")[5] == "strong"
+    for world in (2, 4, 8):
+        n_cfg, _, band, drop, f, lab = bench.resolve_config("strip500", world, "weak")
+        assert lab == "weak" and n_cfg == 500 * world + drop and band == 10
+        plan = bm.read_plan(root / "bench_data" / f)
+        assert len({i for it in plan.iterations for r in it.rows for i in r.needed()}) == 500 * world
+        subs = multigpu.shard_plan(plan, world)
+        one_cost = one_pairs + multigpu.PREP_WEIGHT * one_rows
+        for s in subs:
+            img_rows = sum(len(r.needed()) for it in s.iterations for r in it.rows)
+            assert 0.9 * one_pairs <= s.pair_count() <= 1.1 * one_pairs
+            # a row split between ranks repeats its prep on both (~1.2x the cost model's work)
+            assert s.pair_count() + multigpu.PREP_WEIGHT * img_rows <= 1.25 * one_cost
+        assert sorted(p for s in subs for p in s.pairs()) == plan.pairs()
+
+
 def test_shared_memory_gather_merges_by_idpair(tmp_path):
     """gather_results in one process with a fake 3-rank barrier schedule:
     each 'rank' writes its IdPair-sorted result; rank 0's merge is the union
