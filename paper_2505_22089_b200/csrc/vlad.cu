@@ -388,47 +388,58 @@ __global__ void __launch_bounds__(kDim) vlad_accum_kernel(VladBatch b) {
 }
 
 // signed square root, sequential norm, scale (:189-203).  CTA per image.
-__global__ void __launch_bounds__(256) vlad_final_kernel(VladBatch b) {
+// The norm is one dependent FP64 chain in index order: the CTA squares a
+// chunk of values into shared memory, then one thread adds them up from
+// there (the chain is __dadd_rn-latency bound, not load bound).
+constexpr int kFinalThreads = 256;
+constexpr int kNormChunk = 4096;  // doubles of squares staged per step (32 KiB)
+__global__ void __launch_bounds__(kFinalThreads) vlad_final_kernel(VladBatch b) {
+  __shared__ double s_sq[kNormChunk];
+  __shared__ double s_norm;
   const uint32_t img = blockIdx.x;
   const VladImg im = b.imgs[img];
   const size_t dim = (size_t)b.k_words * kDim;
   double* acc = b.acc + (size_t)img * dim;
   float* out = b.values + (size_t)img * dim;
-  __shared__ double s_norm;
   if (im.n == 0) {
     for (size_t e = threadIdx.x; e < dim; e += blockDim.x) out[e] = 0.f;
     if (threadIdx.x == 0) b.degenerate[img] = 1;
     return;
   }
-  for (size_t e = threadIdx.x; e < dim; e += blockDim.x) {
-    const double v = acc[e];
-    acc[e] = v >= 0.0 ? __dsqrt_rn(v) : -__dsqrt_rn(-v);
+  double n2 = 0.0;  // thread 0's chain
+  for (size_t c0 = 0; c0 < dim; c0 += kNormChunk) {
+    const size_t m = min((size_t)kNormChunk, dim - c0);
+    for (size_t e = threadIdx.x; e < m; e += blockDim.x) {
+      const double v0 = acc[c0 + e];
+      const double v = v0 >= 0.0 ? __dsqrt_rn(v0) : -__dsqrt_rn(-v0);
+      acc[c0 + e] = v;
+      s_sq[e] = __dmul_rn(v, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      size_t e = 0;
+      for (; e + 16 <= m; e += 16) {
+        double q[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) q[u] = s_sq[e + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) n2 = __dadd_rn(n2, q[u]);
+      }
+      for (; e < m; ++e) n2 = __dadd_rn(n2, s_sq[e]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // the reference's order: one dependent chain
-    double n2 = 0.0;
-    size_t e = 0;
-    for (; e + 8 <= dim; e += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(acc + e + u);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) n2 = __dadd_rn(n2, __dmul_rn(v[u], v[u]));
-    }
-    for (; e < dim; ++e) {
-      const double v = __ldcg(acc + e);
-      n2 = __dadd_rn(n2, __dmul_rn(v, v));
-    }
+  if (threadIdx.x == 0) {
     s_norm = n2;
     b.degenerate[img] = (uint8_t)(n2 <= 0.0);
   }
   __syncthreads();
-  const double n2 = s_norm;
-  if (n2 <= 0.0) {
+  const double nn = s_norm;
+  if (nn <= 0.0) {
     for (size_t e = threadIdx.x; e < dim; e += blockDim.x) out[e] = 0.f;
     return;
   }
-  const double inv = __ddiv_rn(1.0, __dsqrt_rn(n2));
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(nn));
   for (size_t e = threadIdx.x; e < dim; e += blockDim.x) out[e] = __double2float_rn(__dmul_rn(acc[e], inv));
 }
 
@@ -453,7 +464,7 @@ void launch_vlad(const VladBatch& b, int n_imgs, int n_tiles, cudaStream_t s) {
   if (n_imgs > 0) {
     vlad_sort_kernel<<<n_imgs, kSortThreads, 32 * sizeof(uint32_t) * b.k_words, s>>>(b);
     vlad_accum_kernel<<<dim3(n_imgs, b.k_words), kDim, 0, s>>>(b);
-    vlad_final_kernel<<<n_imgs, 256, 0, s>>>(b);
+    vlad_final_kernel<<<n_imgs, kFinalThreads, 0, s>>>(b);
   }
 }
 

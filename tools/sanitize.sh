@@ -1,11 +1,12 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / synccheck over a GPU-test subset
 # that reaches every kernel (mean, projection on the tensor cores, codes,
-# fixups, tables, match, compaction, executor streams).
+# fixups, tables, match, compaction, executor streams) and the VLAD encoder
+# (SAN_SEL overrides the test selection).
 # usage: gpurun --timeout 3000 -- bash tools/sanitize.sh TAG
 tag=${1:-san}
 out=gpurun_out/$tag; mkdir -p $out
-SEL="tests/test_gpu_codes.py tests/test_gpu_mean.py tests/test_gpu_match.py tests/test_gpu_engine.py tests/test_gpu_overlap.py::test_results_unchanged_with_and_without_hand_off"
+SEL="${SAN_SEL:-tests/test_gpu_retrieval.py tests/test_gpu_codes.py tests/test_gpu_mean.py tests/test_gpu_match.py tests/test_gpu_engine.py tests/test_gpu_overlap.py::test_results_unchanged_with_and_without_hand_off}"
 DES="not full_size and not large_train and not 16384"
 for tool in memcheck synccheck racecheck; do
   extra=""
