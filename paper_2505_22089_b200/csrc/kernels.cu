@@ -203,36 +203,44 @@ __device__ __forceinline__ HalfStats half_tile_stats(int r0, int r1, Ld&& ld) {
   return o;
 }
 
-// Tile statistics of one 128-descriptor tile, 256 threads: thread (h, c)
-// covers rows 64h..64h+63 of channel c; the halves meet in shared memory and
-// the result goes to the image's arrays (ImgDev::tsum / trng / tlow) at
-// tile index ti.  Contains __syncthreads (call from every thread).
+// Tile statistics of one 128-descriptor tile, 128 P threads: thread (h, c)
+// covers rows [128h/P, 128(h+1)/P) of channel c; the parts meet in shared
+// memory and the result goes to the image's arrays (ImgDev::tsum / trng /
+// tlow) at tile index ti.  Contains __syncthreads (call from every thread).
+template <int P>
 struct TileStatsSmem {
-  i128 sum[kDim], lo[kDim], hi[kDim];
-  uint32_t low[kDim];
+  i128 sum[P][kDim], lo[P][kDim], hi[P][kDim];
+  uint32_t low[P][kDim];
 };
-template <typename Ld>
-__device__ __forceinline__ void tile_stats(const ImgDev& im, uint32_t ti, int nd, TileStatsSmem& sm, Ld&& ld) {
+template <int P, typename Ld>
+__device__ __forceinline__ void tile_stats(const ImgDev& im, uint32_t ti, int nd, TileStatsSmem<P>& sm, Ld&& ld) {
   const int c = threadIdx.x & (kDim - 1), h = threadIdx.x >> 7;
-  const int r0 = h * (kCodesTile / 2), r1 = min(nd, r0 + kCodesTile / 2);
+  const int r0 = h * (kCodesTile / P), r1 = min(nd, r0 + kCodesTile / P);
   const HalfStats hs = half_tile_stats(r0, r1, [&](int r) { return ld(r, c); });
-  if (h == 0) {
-    sm.sum[c] = hs.s;
-    sm.lo[c] = hs.lo;
-    sm.hi[c] = hs.hi;
-    sm.low[c] = hs.low;
-  }
+  sm.sum[h][c] = hs.s;
+  sm.lo[h][c] = hs.lo;
+  sm.hi[h][c] = hs.hi;
+  sm.low[h][c] = hs.low;
   const int bad = __syncthreads_or(!hs.ok);
-  if (h == 1) {
-    // second half's partial sums are offset by the first half's total
-    const i128 s0 = sm.sum[c], lo0 = sm.lo[c], hi0 = sm.hi[c];
+  if (h == P - 1) {
+    // part q's partial sums are offset by the parts before it
+    i128 s0 = 0, lo = 0, hi = 0;
+    uint32_t low = kNoLow;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const i128 l = s0 + sm.lo[q][c], u = s0 + sm.hi[q][c];
+      lo = l < lo ? l : lo;
+      hi = u > hi ? u : hi;
+      s0 += sm.sum[q][c];
+      low = min(low, sm.low[q][c]);
+    }
     const size_t o = (size_t)ti * kDim + c;
-    static_cast<i128*>(im.tsum)[o] = s0 + hs.s;
+    static_cast<i128*>(im.tsum)[o] = s0;
     TileRange rg;
-    rg.lo = (s0 + hs.lo) < lo0 ? (s0 + hs.lo) : lo0;
-    rg.hi = (s0 + hs.hi) > hi0 ? (s0 + hs.hi) : hi0;
+    rg.lo = lo;
+    rg.hi = hi;
     static_cast<TileRange*>(im.trng)[o] = rg;
-    im.tlow[o] = bad ? kBadTile : min(hs.low, sm.low[c]);
+    im.tlow[o] = bad ? kBadTile : low;
   }
 }
 
@@ -242,7 +250,7 @@ constexpr int kSumsThreads = 256;
 __global__ void __launch_bounds__(kSumsThreads) mean_sums_kernel(const ImgDev* __restrict__ imgs,
                                                                  const uint32_t* __restrict__ tile_img,
                                                                  const uint32_t* __restrict__ tile_start) {
-  __shared__ TileStatsSmem sm;
+  __shared__ TileStatsSmem<kSumsThreads / kDim> sm;
   const ImgDev im = imgs[tile_img[blockIdx.x]];
   const uint32_t i0 = tile_start[blockIdx.x];
   const int nd = min(kCodesTile, (int)(im.n - i0));
@@ -676,7 +684,11 @@ __global__ void __launch_bounds__(512, 1) project_kernel(HashDev h, ProjJob job,
 // j ^ (r & 7)); the planes' digit image is prepared once per context by the
 // host (bmg_api.cpp build_hash) in exactly that layout.
 // ---------------------------------------------------------------------------
-constexpr int kTcThreads = 256;
+#ifndef BMG_TC_THREADS
+#define BMG_TC_THREADS 512
+#endif
+constexpr int kTcThreads = BMG_TC_THREADS;  // 256 or 512
+constexpr int kTcParts = kTcThreads / 128;  // threads per tile row (quantise), warps per TMEM lane quadrant
 constexpr int kTcRows = 128;                 // UMMA M
 constexpr int kTcDigitBytes = kTcRows * 128; // one digit plane of the A tile
 constexpr uint32_t kTcTmemCols = 512;
@@ -730,7 +742,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sF + ((npad + 1) & ~1));  // [3]: MMA done, raw tile, planes
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(mbar + 3);
   // the row-mean tile statistics' half-tile exchange (16-byte aligned)
-  TileStatsSmem& sStats = *reinterpret_cast<TileStatsSmem*>(
+  TileStatsSmem<kTcParts>& sStats = *reinterpret_cast<TileStatsSmem<kTcParts>*>(
       (reinterpret_cast<uintptr_t>(sTmem + 1) + 15) & ~static_cast<uintptr_t>(15));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -793,24 +805,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
     const int nd = min(kTcRows, (int)(im.n - i0));
     wait_bar(mbar + 1, raw_phase);
     raw_phase ^= 1u;
-    // ---- quantise from the staged rows: two threads per row (64 channels
-    // each); float4 j of a half is read in a per-row rotation (conflict-free)
+    // ---- quantise from the staged rows: kTcParts threads per row (128 /
+    // kTcParts channels each); float4 j of a part is read in a per-thread
+    // rotation (the 8 threads of a quarter warp hit distinct 16-byte banks)
     {
-      const int r = tid >> 1, half = tid & 1;
-      const int rot = (r + 8 * half) & 15;
-      const float4* row = reinterpret_cast<const float4*>(sRaw + r * kDim) + half * 16;
+      constexpr int kNf = 32 / kTcParts;  // float4s per thread
+      const int r = tid / kTcParts, part = tid % kTcParts;
+      const int rot = (r * kTcParts + part) & (kNf - 1);
+      const float4* row = reinterpret_cast<const float4*>(sRaw + r * kDim) + part * kNf;
       float mx = 0.f;
       bool finite = true;
       if (r < nd) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float4 v = row[(j + rot) & 15];
+        for (int j = 0; j < kNf; ++j) {
+          const float4 v = row[(j + rot) & (kNf - 1)];
           mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
           finite &= isfinite(v.x) & isfinite(v.y) & isfinite(v.z) & isfinite(v.w);
         }
       }
-      mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
-      finite = __shfl_xor_sync(kFull, (int)finite, 1) != 0 && finite;
+#pragma unroll
+      for (int o = 1; o < kTcParts; o <<= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        finite = __shfl_xor_sync(kFull, (int)finite, o) != 0 && finite;
+      }
       int e = 0;
       if (mx > 0.f && finite) frexpf(mx, &e);  // 2^(e-1) <= max < 2^e
       const float sc = finite ? ldexpf(1.f, 22 - e) : 0.f;
@@ -818,8 +835,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
       float ss = 0.f;
       const uint32_t rbase = (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int f4 = (j + rot) & 15;  // float4 index within the half: channels 64 half + 4 f4 ..
+      for (int j = 0; j < kNf; ++j) {
+        const int f4 = (j + rot) & (kNf - 1);  // channels part * 128 / kTcParts + 4 f4 ..
         const float4 v = r < nd ? row[f4] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float vv[4] = {v.x, v.y, v.z, v.w};
         uint32_t b0 = 0, b1 = 0, b2 = 0;
@@ -833,15 +850,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
           b1 |= (uint32_t)(d1 & 0xff) << (8 * u);
           b2 |= (uint32_t)(d2 & 0xff) << (8 * u);
         }
-        // channel c = 64 half + 4 f4: 16-byte chunk c / 16, byte c % 16
-        const int chunk = half * 4 + (f4 >> 2);
+        // channel c = part * 128 / kTcParts + 4 f4: 16-byte chunk c / 16, byte c % 16
+        const int chunk = part * (8 / kTcParts) + (f4 >> 2);
         const uint32_t off = rbase + (uint32_t)((chunk ^ (r & 7)) * 16 + (f4 & 3) * 4);
         *reinterpret_cast<uint32_t*>(sA + off) = b0;
         *reinterpret_cast<uint32_t*>(sA + kTcDigitBytes + off) = b1;
         *reinterpret_cast<uint32_t*>(sA + 2 * kTcDigitBytes + off) = b2;
       }
-      ss += __shfl_xor_sync(kFull, ss, 1);
-      if (half == 0) {
+#pragma unroll
+      for (int o = 1; o < kTcParts; o <<= 1) ss += __shfl_xor_sync(kFull, ss, o);
+      if (part == 0) {
         sExp[r] = finite ? e : INT_MIN;
         // ||d||_2 rounded up, from the 2^-e scaled row
         if (r < nd) im.dnorm[i0 + r] = finite ? ldexpf(sqrtf(ss), e) * 1.00001f : __int_as_float(0x7f800000);
@@ -907,15 +925,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(HashDev h, Pr
         phase ^= 1u;
       }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // ---- epilogue: warp w reads TMEM lanes 32(w&3).. (= tile rows), half
-      // (w >> 2) of the pass's planes, 8 columns at a time
+      // ---- epilogue: warp w reads TMEM lanes 32(w&3).. (= tile rows) and
+      // every kTcParts-th group of 8 columns of the pass's planes from (w >> 2)
       {
         const int rg = warp & 3, ch = warp >> 2;
         const int r = rg * 32 + lane;
         const int ex = sExp[r];
-        const int cols = np / 2, c0 = ch * cols;
         const uint32_t tl = tmem + ((uint32_t)(rg * 32) << 16);
-        for (int c = c0; c < c0 + cols; c += 8) {
+        for (int c = 8 * ch; c < np; c += 8 * kTcParts) {
           int32_t acc[5][8];
 #pragma unroll
           for (int sw = 0; sw < 5; ++sw) tmem_ld8(tl + (uint32_t)(sw * np + c), acc[sw]);
@@ -1991,7 +2008,7 @@ static int sm_count() {
 
 static size_t proj_tc_smem_bytes(const HashDev& h) {
   return 1024 + 3 * (size_t)kTcDigitBytes + 3 * (size_t)h.tc_npad * 128 + sizeof(float) * kTcRows * kDim +
-         sizeof(int) * (kTcRows + h.tc_npad + 2) + 3 * sizeof(uint64_t) + 16 + sizeof(TileStatsSmem) + 16;
+         sizeof(int) * (kTcRows + h.tc_npad + 2) + 3 * sizeof(uint64_t) + 16 + sizeof(TileStatsSmem<kTcParts>) + 16;
 }
 
 
