@@ -60,7 +60,8 @@ typedef enum {
   BMG_UNSUPPORTED = 7,        /* "Unsupported"      */
   BMG_INVALID_SCENE = 8,      /* "InvalidScene" / "ZeroVector" (features.cpp:60, 69-78) */
   BMG_FORMAT_ERROR = 9,       /* "FormatError"   (binary_io.hpp:63-67, features.cpp, hashmatch.cpp) */
-  BMG_TRUNCATED_FILE = 10     /* "TruncatedFile" (binary_io.hpp:37-43) */
+  BMG_TRUNCATED_FILE = 10,    /* "TruncatedFile" (binary_io.hpp:37-43) */
+  BMG_TOO_FEW_DESCRIPTORS = 11 /* "TooFewDescriptors" (retrieval.cpp:62-64, 94-96) */
 } bmg_status;
 
 typedef struct bmg_context bmg_context;
@@ -330,6 +331,19 @@ int bmg_write_matches_binary(const char* path, uint64_t n_pairs, const uint64_t*
  * Unsupported for k_words > 1024. */
 int bmg_encode_vlad(bmg_context* ctx, const float* centroids, int k_words, const bmg_feature_view* images,
                     uint64_t n_images, float* values_out, uint8_t* degenerate_out);
+/* train_codebook (retrieval.hpp:26-34, retrieval.cpp:56-158) on the B200:
+ * Lloyd iterations over descriptors[n][128] with the reference's seeding
+ * (mt19937_64 shuffle, k distinct values), nearest-centroid assignment
+ * (FP64 semantics, certified FP32 filter), FP64 cluster sums in point order,
+ * empty clusters reseeded from the farthest point, stop at an assignment
+ * fixpoint or max_iters.  centroids_out: float[k_words][128]; sse_out (may be
+ * NULL): the within-cluster SSE of every assignment step (at most max_iters),
+ * *n_sse_out their number.  Bit-exact with the reference.  Errors as the
+ * reference: InvalidArgument (k_words < 1, max_iters < 1), TooFewDescriptors
+ * (n < k_words, or fewer than k_words distinct values); Unsupported for
+ * k_words > 1024. */
+int bmg_train_codebook(bmg_context* ctx, const float* descriptors, uint64_t n, int k_words, int max_iters,
+                       uint64_t seed, float* centroids_out, double* sse_out, int* n_sse_out);
 
 /* knn_from_delaunay (verify.cpp:135-196): per point its k neighbours by
  * Delaunay rings (neighbors_out[n][k], -1 padded); *fallback = 1 when the

@@ -16,6 +16,6 @@ from .engine import (BlockRow, DeviceArena, ExecuteOptions, ExecutionResult,  # 
                      PipelineMetrics, ScheduleBlock, ScheduleIteration, SchedulePlan,
                      arena_units_for, execute_plan, flatten_plan, read_plan, write_plan)
 from .retrieval import (Codebook, VladVector, encode_vlad, encode_vlad_batch,  # noqa: F401
-                        read_codebook, write_codebook)
+                        read_codebook, train_codebook, write_codebook)
 
 __version__ = "0.1.0"

@@ -18,7 +18,7 @@ DIM = 128
 STATUS_NAMES = {
     0: "Ok", 1: "InvalidArgument", 2: "HashMismatch", 3: "CapacityExceeded",
     4: "NotResident", 5: "CudaError", 6: "OutOfMemory", 7: "Unsupported", 8: "InvalidScene",
-    9: "FormatError", 10: "TruncatedFile",
+    9: "FormatError", 10: "TruncatedFile", 11: "TooFewDescriptors",
 }
 
 
@@ -98,7 +98,7 @@ EXPORTED = [
     "bmg_result_write_matches", "bmg_read_features_header", "bmg_read_features",
     "bmg_write_matches_binary", "bmg_generate_synthetic_subset", "bmg_set_test_flags",
     "bmg_result_row_timing", "bmg_execute_plan_files", "bmg_sao_filter",
-    "bmg_delaunay_knn", "bmg_encode_vlad",
+    "bmg_delaunay_knn", "bmg_encode_vlad", "bmg_train_codebook",
 ]
 
 _lib = None
@@ -164,6 +164,7 @@ def load(path: Path = LIB_PATH):
                                      C.POINTER(C.c_uint32)]),
         "bmg_delaunay_knn": (C.c_int, [vp, u64, C.c_int, vp, C.POINTER(C.c_int)]),
         "bmg_encode_vlad": (C.c_int, [vp, vp, C.c_int, vp, u64, vp, vp]),
+        "bmg_train_codebook": (C.c_int, [vp, vp, u64, C.c_int, C.c_int, u64, vp, vp, C.POINTER(C.c_int)]),
         "bmg_synthetic_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp]),
         "bmg_generate_synthetic": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                              u64, vp, vp]),

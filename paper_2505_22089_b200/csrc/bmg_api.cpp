@@ -27,10 +27,12 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <new>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -1285,6 +1287,7 @@ const char* bmg_status_name(int status) {
     case BMG_INVALID_SCENE: return "InvalidScene";
     case BMG_FORMAT_ERROR: return "FormatError";
     case BMG_TRUNCATED_FILE: return "TruncatedFile";
+    case BMG_TOO_FEW_DESCRIPTORS: return "TooFewDescriptors";
     default: return "Unknown";
   }
 }
@@ -2330,6 +2333,168 @@ int bmg_encode_vlad(bmg_context* c, const float* centroids, int k_words, const b
   });
   cleanup();
   return rc;
+}
+
+int bmg_train_codebook(bmg_context* c, const float* desc, uint64_t n, int k_words, int max_iters, uint64_t seed,
+                       float* centroids_out, double* sse_out, int* n_sse_out) {
+  using namespace bmg;
+  return guarded([&] {
+    if (!c || !centroids_out || !n_sse_out) fail(BMG_INVALID_ARGUMENT, "null argument");
+    // argument checks in the reference's order (retrieval.cpp:59-64)
+    if (k_words < 1) fail(BMG_INVALID_ARGUMENT, "k_words must be >= 1");
+    if (max_iters < 1) fail(BMG_INVALID_ARGUMENT, "max_iters must be >= 1");
+    if (n < static_cast<uint64_t>(k_words))
+      fail(BMG_TOO_FEW_DESCRIPTORS,
+           "need at least " + std::to_string(k_words) + " descriptors, got " + std::to_string(n));
+    if (k_words > kVladMaxWords)
+      fail(BMG_UNSUPPORTED, "codebooks of more than " + std::to_string(kVladMaxWords) +
+                                " words are not supported by the GPU k-means");
+    if (n > 0xffffffffull) fail(BMG_UNSUPPORTED, "training pools of 2^32 descriptors or more");
+    if (!desc) fail(BMG_INVALID_ARGUMENT, "null descriptors");
+    set_device(*c);
+    *n_sse_out = 0;
+    const size_t K = static_cast<size_t>(k_words), dimk = K * kDim;
+    // initial centroids: k distinct descriptor values in shuffled order (:69-96)
+    std::vector<uint64_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) order[i] = i;
+    std::mt19937_64 rng(seed);
+    std::shuffle(order.begin(), order.end(), rng);
+    std::vector<double> cent(dimk);
+    size_t picked = 0;
+    for (uint64_t idx : order) {
+      if (picked == K) break;
+      const float* d = desc + idx * kDim;
+      bool duplicate = false;
+      for (size_t k = 0; k < picked && !duplicate; ++k) {
+        const double* cc = cent.data() + k * kDim;
+        duplicate = true;
+        for (int j = 0; j < kDim; ++j)
+          if (static_cast<double>(d[j]) != cc[j]) {
+            duplicate = false;
+            break;
+          }
+      }
+      if (duplicate) continue;
+      for (int j = 0; j < kDim; ++j) cent[picked * kDim + j] = d[j];
+      ++picked;
+    }
+    if (picked < K)
+      fail(BMG_TOO_FEW_DESCRIPTORS, "fewer than " + std::to_string(k_words) + " distinct descriptor values");
+    // device state: the pool as one "image", tiles of 128
+    cudaStream_t s = c->slot[0].home;
+    const uint64_t tiles = (n + kVladTile - 1) / kVladTile;
+    DevBuf d_desc, d_cent32, d_cent64, d_zero, d_assign, d_fix, d_fixcnt, d_d2, d_members, d_moff, d_sums, d_meta;
+    d_desc.ensure(n * kDim * sizeof(float));
+    d_cent32.ensure(dimk * sizeof(float));
+    d_cent64.ensure(dimk * sizeof(double));
+    d_zero.ensure(dimk * sizeof(float));
+    d_assign.ensure(n * sizeof(int32_t));
+    d_fix.ensure(n * sizeof(uint2));
+    d_fixcnt.ensure(16);
+    d_d2.ensure(n * sizeof(double));
+    d_members.ensure(n * sizeof(uint32_t));
+    d_moff.ensure((K + 1) * sizeof(uint32_t));
+    d_sums.ensure(dimk * sizeof(double));
+    const size_t meta_bytes = align_up(sizeof(VladImg) + 2 * tiles * sizeof(uint32_t), 16);
+    d_meta.ensure(meta_bytes);
+    {
+      std::vector<char> meta(meta_bytes, 0);
+      VladImg* mi = reinterpret_cast<VladImg*>(meta.data());
+      mi->desc = d_desc.as<float>();
+      mi->n = static_cast<uint32_t>(n);
+      mi->assign_off = 0;
+      uint32_t* ti = reinterpret_cast<uint32_t*>(mi + 1);
+      for (uint64_t t = 0; t < tiles; ++t) {
+        ti[t] = 0;
+        ti[tiles + t] = static_cast<uint32_t>(t * kVladTile);
+      }
+      BMG_CUDA(cudaMemcpyAsync(d_meta.p, meta.data(), meta_bytes, cudaMemcpyHostToDevice, s));
+      BMG_CUDA(cudaMemsetAsync(d_zero.p, 0, dimk * sizeof(float), s));
+      stage_h2d(*c, d_desc.p, desc, n * kDim * sizeof(float));
+      cudaEvent_t e = take_event(*c);
+      BMG_CUDA(cudaEventRecord(e, c->s_copy));
+      BMG_CUDA(cudaStreamWaitEvent(s, e, 0));
+      c->free_events.push_back(e);
+    }
+    VladBatch b{};
+    b.imgs = d_meta.as<VladImg>();
+    b.tile_img = reinterpret_cast<const uint32_t*>(b.imgs + 1);
+    b.tile_start = b.tile_img + tiles;
+    b.k_words = k_words;
+    b.assign = d_assign.as<int32_t>();
+    b.fix = d_fix.as<uint2>();
+    b.fix_count = d_fixcnt.as<uint32_t>();
+    b.fix_cap = static_cast<uint32_t>(n);
+    b.members = d_members.as<uint32_t>();
+    b.member_off = d_moff.as<uint32_t>();
+    b.acc = d_sums.as<double>();
+    b.cent64 = d_cent64.as<double>();
+    b.point_d2 = d_d2.as<double>();
+    std::vector<int32_t> assign(n), prev(n, -1);
+    std::vector<double> d2(n), sums(dimk);
+    std::vector<float> c32(dimk);
+    for (int iter = 0; iter < max_iters; ++iter) {
+      // ---- assignment (:99-117) on the device
+      float cmax = 0.f;
+      for (size_t k = 0; k < K; ++k) {
+        double nn = 0.0;
+        for (int j = 0; j < kDim; ++j) {
+          c32[k * kDim + j] = static_cast<float>(cent[k * kDim + j]);
+          nn += cent[k * kDim + j] * cent[k * kDim + j];
+        }
+        cmax = std::max(cmax, static_cast<float>(std::sqrt(nn)) * 1.0001f);
+      }
+      if (!std::isfinite(cmax)) cmax = std::numeric_limits<float>::infinity();
+      BMG_CUDA(cudaMemcpyAsync(d_cent32.p, c32.data(), dimk * sizeof(float), cudaMemcpyHostToDevice, s));
+      BMG_CUDA(cudaMemcpyAsync(d_cent64.p, cent.data(), dimk * sizeof(double), cudaMemcpyHostToDevice, s));
+      BMG_CUDA(cudaMemsetAsync(d_fixcnt.p, 0, 16, s));
+      b.centroids = d_cent32.as<float>();
+      b.cnorm_max = cmax;
+      {
+        Timed tm(*c, "kmeans", s);
+        launch_kmeans_assign(b, static_cast<int>(tiles), s);
+        c->launches += 3;
+        check_launch();
+      }
+      BMG_CUDA(cudaMemcpyAsync(assign.data(), d_assign.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      BMG_CUDA(cudaMemcpyAsync(d2.data(), d_d2.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      BMG_CUDA(cudaStreamSynchronize(s));
+      double sse = 0.0;  // in point order, as the reference
+      for (uint64_t i = 0; i < n; ++i) sse += d2[i];
+      if (sse_out) sse_out[iter] = sse;
+      *n_sse_out = iter + 1;
+      if (assign == prev) break;
+      prev = assign;
+      // ---- update (:121-136): FP64 sums in point order on the device
+      b.centroids = d_zero.as<float>();  // the residual chains with zero centroids: plain sums
+      {
+        Timed tm(*c, "kmeans", s);
+        launch_kmeans_sums(b, s);
+        c->launches += 2;
+        check_launch();
+      }
+      BMG_CUDA(cudaMemcpyAsync(sums.data(), d_sums.p, dimk * sizeof(double), cudaMemcpyDeviceToHost, s));
+      BMG_CUDA(cudaStreamSynchronize(s));
+      std::vector<uint64_t> counts(K, 0);
+      for (uint64_t i = 0; i < n; ++i) ++counts[static_cast<size_t>(assign[i])];
+      for (size_t k = 0; k < K; ++k) {
+        if (counts[k] == 0) continue;
+        const double inv = 1.0 / static_cast<double>(counts[k]);
+        for (int j = 0; j < kDim; ++j) cent[k * kDim + j] = sums[k * kDim + j] * inv;
+      }
+      // empty clusters take the point worst served by its centroid (:137-147)
+      for (size_t k = 0; k < K; ++k) {
+        if (counts[k] != 0) continue;
+        uint64_t far = 0;
+        for (uint64_t i = 1; i < n; ++i)
+          if (d2[i] > d2[far]) far = i;
+        for (int j = 0; j < kDim; ++j) cent[k * kDim + j] = desc[far * kDim + j];
+        d2[far] = 0.0;
+      }
+    }
+    for (size_t i = 0; i < dimk; ++i) centroids_out[i] = static_cast<float>(cent[i]);
+    BMG_CUDA(cudaStreamSynchronize(c->s_copy));
+  });
 }
 
 int bmg_set_profiling(bmg_context* c, int enabled) {

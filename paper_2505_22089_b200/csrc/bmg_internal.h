@@ -192,10 +192,23 @@ struct VladBatch {
   double* acc;                 // [images][k_words*128] residual sums
   float* values;               // [images][k_words*128] VladVector::values
   uint8_t* degenerate;         // [images] VladVector::degenerate
+  // k-means assignment (train_codebook, retrieval.cpp:99-117): the centroids
+  // are doubles (cent64; `centroids` holds them rounded to float for the FP32
+  // filter, whose bound then adds cnorm_max * sqrt(s) terms), the FP64 loop
+  // starts from centroid 0's distance, and point_d2 gets every point's FP64
+  // distance to its centroid.  Null for encode_vlad.
+  const double* cent64;
+  float cnorm_max;             // max ||c||_2 over the centroids, rounded up
+  double* point_d2;
 };
 constexpr int kVladTile = 128;
 constexpr int kVladMaxWords = 1024;  // codebook words the GPU encoder supports
 void launch_vlad(const VladBatch& b, int n_imgs, int n_tiles, cudaStream_t s);
+// k-means: nearest centroid (+ FP64 fixups) and every point's FP64 distance;
+// then the cluster sums (sort + residual chains with zero centroids: acc =
+// sum of (double)d in point order) when `sums`
+void launch_kmeans_assign(const VladBatch& b, int n_tiles, cudaStream_t s);
+void launch_kmeans_sums(const VladBatch& b, cudaStream_t s);
 // certified / FP64 assignments of the last launches (diagnostics)
 size_t vlad_assign_smem_bytes();
 

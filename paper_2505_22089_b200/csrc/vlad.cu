@@ -210,7 +210,14 @@ __global__ void __launch_bounds__(kVThreads, 2) vlad_assign_kernel(VladBatch b, 
         if (row >= rows) continue;
         const float bs = best[q], s2 = second[q];
         const bool finite = bs <= 3.0e38f;
-        const bool sep = s2 == __int_as_float(0x7f800000) || (s2 >= 1.0e-30f && bs * c_hi < s2 * c_lo);
+        bool sep = s2 == __int_as_float(0x7f800000) || (s2 >= 1.0e-30f && bs * c_hi < s2 * c_lo);
+        if (b.cent64) {
+          // float-rounded double centroids: |s32 - s| <= 132 u s + 2.1 u ||c|| sqrt(s)
+          // + 2 u^2 ||c||^2 (u = 2^-24), taken with generous constants
+          const float cn = b.cnorm_max;
+          auto bound = [&](float x) { return 1.0e-5f * x + 2.5e-7f * cn * sqrtf(x) + 1.0e-13f * cn * cn; };
+          sep = s2 == __int_as_float(0x7f800000) || (s2 >= 1.0e-30f && bs + bound(bs) < s2 - bound(s2));
+        }
         const size_t gi = im.assign_off + i0 + row;
         if (!nan_seen[q] && finite && sep) {
           b.assign[gi] = (int32_t)bidx[q];
@@ -222,6 +229,26 @@ __global__ void __launch_bounds__(kVThreads, 2) vlad_assign_kernel(VladBatch b, 
       }
     }
   }
+}
+
+// sq_dist (retrieval.cpp:45-52): sequential FP64 sum of ((double)d - c)^2
+__device__ __forceinline__ double sq_dist64(const float* __restrict__ d, const double* __restrict__ c) {
+  const float4* dp = reinterpret_cast<const float4*>(d);
+  const double2* cp = reinterpret_cast<const double2*>(c);
+  double s = 0.0;
+#pragma unroll 8
+  for (int c4 = 0; c4 < kDim / 4; ++c4) {
+    const float4 dv = __ldg(dp + c4);
+    const double2 c0 = __ldg(cp + 2 * c4), c1 = __ldg(cp + 2 * c4 + 1);
+    const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
+    const double cc[4] = {c0.x, c0.y, c1.x, c1.y};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double diff = __dsub_rn((double)dd[e], cc[e]);
+      s = __dadd_rn(s, __dmul_rn(diff, diff));
+    }
+  }
+  return s;
 }
 
 // The reference's loop (:170-183) for the uncertified descriptors; one warp
@@ -236,25 +263,34 @@ __global__ void __launch_bounds__(256) vlad_fix_kernel(VladBatch b) {
     const float* d = im.desc + (size_t)e.y * kDim;
     double bv = __longlong_as_double(0x7ff0000000000000ll);  // +inf: s < inf required
     int bk = 0x7fffffff;
+    bool nan0 = false;  // k-means: centroid 0's distance is NaN
     for (int k = lane; k < b.k_words; k += 32) {
-      const float4* cp = reinterpret_cast<const float4*>(b.centroids + (size_t)k * kDim);
-      const float4* dp = reinterpret_cast<const float4*>(d);
       double s = 0.0;
+      if (b.cent64) {
+        s = sq_dist64(d, b.cent64 + (size_t)k * kDim);
+      } else {
+        const float4* cp = reinterpret_cast<const float4*>(b.centroids + (size_t)k * kDim);
+        const float4* dp = reinterpret_cast<const float4*>(d);
 #pragma unroll 8
-      for (int c4 = 0; c4 < kDim / 4; ++c4) {
-        const float4 dv = __ldg(dp + c4), cv = __ldg(cp + c4);
-        const float dd[4] = {dv.x, dv.y, dv.z, dv.w}, cc[4] = {cv.x, cv.y, cv.z, cv.w};
+        for (int c4 = 0; c4 < kDim / 4; ++c4) {
+          const float4 dv = __ldg(dp + c4), cv = __ldg(cp + c4);
+          const float dd[4] = {dv.x, dv.y, dv.z, dv.w}, cc[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double diff = __dsub_rn((double)dd[e], (double)cc[e]);
-          s = __dadd_rn(s, __dmul_rn(diff, diff));
+          for (int e = 0; e < 4; ++e) {
+            const double diff = __dsub_rn((double)dd[e], (double)cc[e]);
+            s = __dadd_rn(s, __dmul_rn(diff, diff));
+          }
         }
       }
+      if (k == 0) nan0 = s != s;
       if (s < bv) {  // lanes visit their k ascending: first minimum per lane
         bv = s;
         bk = k;
       }
     }
+    // train_codebook starts from centroid 0's distance (retrieval.cpp:101-108):
+    // a NaN there is never replaced
+    nan0 = __shfl_sync(kFull, (int)nan0, 0) != 0 && b.cent64;
     // first index of the minimum over lanes; none below +inf -> 0
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -265,8 +301,18 @@ __global__ void __launch_bounds__(256) vlad_fix_kernel(VladBatch b) {
         bk = ok;
       }
     }
-    if (lane == 0) b.assign[im.assign_off + e.y] = bk == 0x7fffffff ? 0 : bk;
+    if (lane == 0) b.assign[im.assign_off + e.y] = (bk == 0x7fffffff || nan0) ? 0 : bk;
   }
+}
+
+// k-means: every point's FP64 distance to its centroid, the reference's
+// best_d2 (retrieval.cpp:99-117: sq_dist with double centroids).
+__global__ void __launch_bounds__(256) kmeans_d2_kernel(VladBatch b, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const VladImg im = b.imgs[0];
+  const int32_t k = b.assign[i];
+  b.point_d2[i] = sq_dist64(im.desc + (size_t)i * kDim, b.cent64 + (size_t)k * kDim);
 }
 
 // Stable counting sort of an image's descriptors by nearest centroid (the
@@ -466,6 +512,28 @@ void launch_vlad(const VladBatch& b, int n_imgs, int n_tiles, cudaStream_t s) {
     vlad_accum_kernel<<<dim3(n_imgs, b.k_words), kDim, 0, s>>>(b);
     vlad_final_kernel<<<n_imgs, kFinalThreads, 0, s>>>(b);
   }
+}
+
+void launch_kmeans_assign(const VladBatch& b, int n_tiles, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(vlad_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(VSmem));
+  }
+  if (n_tiles <= 0) return;
+  vlad_assign_kernel<<<std::min(n_tiles, 2 * sms), kVThreads, sizeof(VSmem), s>>>(b, n_tiles);
+  vlad_fix_kernel<<<sms, 256, 0, s>>>(b);
+  const uint32_t n = (uint32_t)b.fix_cap;  // the pool's size
+  kmeans_d2_kernel<<<(n + 255) / 256, 256, 0, s>>>(b, n);
+}
+
+void launch_kmeans_sums(const VladBatch& b, cudaStream_t s) {
+  cudaFuncSetAttribute(vlad_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(32 * sizeof(uint32_t) * kVladMaxWords));
+  vlad_sort_kernel<<<1, kSortThreads, 32 * sizeof(uint32_t) * b.k_words, s>>>(b);
+  vlad_accum_kernel<<<dim3(1, b.k_words), kDim, 0, s>>>(b);
 }
 
 }  // namespace bmg

@@ -3,8 +3,9 @@
 before its HNSW search (retrieval.cpp:386-399) -- on the B200 (vlad.cu,
 ``bmg_encode_vlad``), bit-exact with ``encode_vlad`` (retrieval.cpp:160-205);
 plus the codebook file format (``write_codebook`` / ``read_codebook``,
-retrieval.cpp:407-450).  Codebook training (k-means) and the HNSW index stay
-on the host (reference code)."""
+retrieval.cpp:407-450) and codebook training (``train_codebook``, k-means,
+retrieval.cpp:56-158, ``bmg_train_codebook``).  The HNSW index stays on the
+host (reference code)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -18,7 +19,7 @@ from ._lib import BandmatchError, DIM, check, ptr
 from .hashmatch import FeatureSet, HashFunctions, Matcher, _matcher_for, make_hash_functions
 
 __all__ = ["Codebook", "VladVector", "encode_vlad", "encode_vlad_batch", "read_codebook",
-           "write_codebook"]
+           "train_codebook", "write_codebook"]
 
 
 @dataclass
@@ -79,6 +80,26 @@ def encode_vlad_batch(images, cb: Codebook, matcher: Matcher | None = None) -> l
 def encode_vlad(fs, cb: Codebook, matcher: Matcher | None = None) -> VladVector:
     """encode_vlad(fs, cb), retrieval.cpp:160-205, on the B200."""
     return encode_vlad_batch([fs], cb, matcher)[0]
+
+
+def train_codebook(descriptors, k_words: int, max_iters: int, seed: int, sse_history: list | None = None,
+                   matcher: Matcher | None = None) -> Codebook:
+    """train_codebook (retrieval.cpp:56-158) on the B200, bit-exact: the
+    reference's seeding, Lloyd iterations with FP64 assignments and sums,
+    empty clusters reseeded from the farthest point.  ``sse_history`` (a
+    list) receives the SSE of every assignment step."""
+    d = _descs(descriptors)
+    n = len(d)
+    cent = np.zeros((max(k_words, 1), DIM), np.float32)
+    sse = np.zeros(max(max_iters, 1), np.float64)
+    n_sse = C.c_int(0)
+    m = _context(matcher)
+    check(_lib.load().bmg_train_codebook(m.handle, ptr(d) if n else None, n, k_words, max_iters, seed,
+                                         ptr(cent), ptr(sse), C.byref(n_sse)))
+    if sse_history is not None:
+        sse_history.clear()
+        sse_history.extend(float(x) for x in sse[: n_sse.value])
+    return Codebook(k_words, cent[:k_words])
 
 
 _MAGIC = b"BMCB"

@@ -84,6 +84,25 @@ def test_16k_multi_row_multi_iteration_plan_equals_reference(reference, tmp_path
     assert_same(flat_of(res), ref)
 
 
+@pytest.mark.parametrize("n", [1024, 4096, 32768])
+def test_descriptor_count_sweep_sizes_equal_reference(reference, tmp_path, n):
+    """BASELINE config 5's descriptor counts (tools/sweep.py, 1k..32k per
+    image): a band-2 scene of 8 images scheduled by the reference, through
+    execute_plan, against the reference row body."""
+    imgs, pairs = reference.generate_synthetic(8, n, 2, 0.02, 0.2, 5 + n)
+    plan_path = tmp_path / "plan.json"
+    reference.iterate_schedule(np.arange(8), pairs, 4, 8, plan_path)
+    hseed = bm.seed_for(42, "matching")
+    _, _, _, ref = reference.execute_plan_rows(plan_path, dict(enumerate(imgs)), hseed, threads=8,
+                                               want_matches=True)
+    plan = bm.read_plan(plan_path)
+    feats = {i: bm.FeatureSet(i, d) for i, d in enumerate(imgs)}
+    arena = bm.DeviceArena(engine.arena_units_for(feats, plan.size_gpu), bm.make_hash_functions(hseed))
+    res = bm.execute_plan(plan, feats, arena)
+    assert res.metrics.pairs_matched == plan.pair_count() > 0
+    assert_same(flat_of(res), ref)
+
+
 def test_row_body_equals_single_thread_execute_plan(reference, tmp_path):
     """The threaded reference row body (the bench's CPU leg and the checker
     above) against the reference execute_plan as shipped."""

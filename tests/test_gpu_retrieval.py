@@ -66,3 +66,40 @@ def test_errors():
         bm.encode_vlad(np.zeros((3, 128), np.float32), bm.Codebook(0, np.zeros((0, 128), np.float32)))
     assert e.value.code == "InvalidArgument" and "codebook has no words" in str(e.value)
     assert bm.encode_vlad_batch([], bm.Codebook(2, np.ones((2, 128), np.float32))) == []
+
+
+# ---- train_codebook (retrieval.cpp:56-158) ------------------------------------
+@pytest.mark.parametrize("n,k,iters,seed", [(2000, 16, 25, 3), (40, 16, 25, 7), (300, 64, 5, 11),
+                                            (64, 64, 3, 1), (5000, 64, 25, 42)])
+def test_train_codebook_equals_reference(reference, n, k, iters, seed):
+    rng = np.random.default_rng(n + k)
+    d = rng.standard_normal((n, 128)).astype(np.float32)
+    d[n // 3: n // 3 + 5] = d[0]  # duplicates: skipped by the seeding's distinct check
+    hist = []
+    got = bm.train_codebook(d, k, iters, seed, sse_history=hist)
+    cent, sse = reference.train_codebook(d, k, iters, seed)
+    assert same(got.centroids, cent)
+    assert np.array_equal(np.asarray(hist), sse)
+
+
+def test_train_codebook_on_scene_sample_equals_reference(reference):
+    imgs, _ = reference.generate_synthetic(14, 8192, 11, 0.02, 0.2, 7)
+    sample = np.concatenate([im[::13] for im in imgs[11:]])
+    hist = []
+    got = bm.train_codebook(sample, 64, 10, 3, sse_history=hist)
+    cent, sse = reference.train_codebook(sample, 64, 10, 3)
+    assert same(got.centroids, cent) and np.array_equal(np.asarray(hist), sse)
+    assert all(a >= b for a, b in zip(sse, sse[1:]))  # Lloyd's SSE is non-increasing
+
+
+def test_train_codebook_errors(reference):
+    d = np.random.default_rng(0).standard_normal((10, 128)).astype(np.float32)
+    for args, code in [((d, 0, 5, 1), "InvalidArgument"), ((d, 4, 0, 1), "InvalidArgument"),
+                       ((d, 11, 5, 1), "TooFewDescriptors"),
+                       ((np.repeat(d[:1], 10, 0), 2, 5, 1), "TooFewDescriptors")]:
+        with pytest.raises(bm.BandmatchError) as e:
+            bm.train_codebook(*args)
+        assert e.value.code == code
+        with pytest.raises(Exception) as r:
+            reference.train_codebook(*args)
+        assert code in str(r.value)
