@@ -1837,6 +1837,10 @@ void execute_plan_impl(Ctx* c, const bmg_plan* plan, const std::unordered_map<ui
     };
     if (timeline) c->marks = &marks;
     uint64_t xrow = 0;  // rows issued so far (stream priority, slot)
+    bool prio_late = false;
+    for (uint64_t k = 0; k < plan->row_needed_offsets[plan->n_rows] && !prio_late; ++k)
+      prio_late = !c->resident.count(plan->needed_ids[k]);
+    if (const char* v = getenv("BMG_PRIO_LATE")) prio_late = v[0] == '1';  // A/B override
     for (uint64_t it = 0; it < plan->n_iterations; ++it) {
       const uint64_t row0 = row, nr = plan->rows_per_iteration[it];
       row += nr;
@@ -1950,7 +1954,13 @@ void execute_plan_impl(Ctx* c, const bmg_plan* plan, const std::unordered_map<ui
         c->cur = (opts->flags & BMG_EXEC_SERIAL) ? 0 : static_cast<int>(xrow & 1);
         RowSlot& S = c->S();
         if (!(opts->flags & BMG_EXEC_SERIAL)) {
-          cudaStream_t st = xrow < c->s_prio.size() ? c->s_prio[xrow] : S.home;
+          // a call that uploads: the last rows get the highest priorities
+          // (the last row's work after the last upload is the end-to-end
+          // tail; its prep must not queue behind the previous row's match);
+          // all images resident: earlier rows first (a row gates its slot's
+          // next row)
+          const uint64_t rank = prio_late ? total_rows - 1 - xrow : xrow;
+          cudaStream_t st = rank < c->s_prio.size() ? c->s_prio[rank] : S.home;
           if (st != S.s_comp) BMG_CUDA(cudaStreamWaitEvent(st, S.done, 0));
           S.s_comp = st;
         }
