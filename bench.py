@@ -60,7 +60,7 @@ NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
 FALLBACK_HBM = 6650.0
 HASH_ROOT_SEED = 42  # make_hash_functions(seed_for(42, "matching")), bandmatch_cli.cpp:225-226
 
-CONFIG_NO = {"pair1": 1, "block32": 2, "strip500": 3, "shard16k": 4}
+CONFIG_NO = {"pair1": 1, "block32": 2, "strip500": 3, "shard16k": 4, "config4": 4}
 CONFIGS = {
     # name: (generator n_images, ppi, band, dropped leading images, plan file)
     # BASELINE config 1: images (band, band+1) of an 11-band 8,192 scene
@@ -70,11 +70,14 @@ CONFIGS = {
     # BASELINE config 4 is 5,000 x 16,384 sharded over 2/4/8 GPUs: one
     # GPU's shard (640 images, band 15 = 30 neighbours)
     "shard16k": (655, 16384, 15, 15, "plan_shard16k.json"),
+    # BASELINE config 4 in full (74,880 pairs, 25 block rows; ~42 GB of
+    # descriptors: fits one B200's HBM, or shards over N GPUs)
+    "config4": (5015, 16384, 15, 15, "plan_config4.json"),
 }
 # configs whose full reference run is minutes long: the CPU figure is a
 # timed sample (compute_codes of 32 images + match_pair of 128 pairs on all
 # host threads) extrapolated to the plan's rows
-SAMPLED = {"shard16k"}
+SAMPLED = {"shard16k", "config4"}
 
 
 def parse():
@@ -446,6 +449,53 @@ def reference_arm(args):
     return 0
 
 
+def sampled_parity(ref, hseed, images, plan_path, gpu_flat, cores, n_pairs=48):
+    """Parity on a sample of a long plan: the reference runs the LAST block
+    row with its whole needed set (so its mean and codes are the full row's)
+    but only the first `n_pairs` pairs of its blocks; their match lists are
+    compared with the GPU's for the same pairs."""
+    import tempfile
+
+    j = json.loads(Path(plan_path).read_text())
+    it = j["iterations"][-1]
+    row = json.loads(json.dumps(it["rows"][-1]))
+    left = n_pairs
+    for blk in row["blocks"]:
+        blk["pairs"] = blk["pairs"][:left]
+        left -= len(blk["pairs"])
+    row["evict_after"] = []
+    sub = dict(j)
+    sub["iterations"] = [dict(it, rows=[row])]
+    need = set(row["row_images"])
+    for blk in row["blocks"]:
+        need.update(blk["col_images"])
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        json.dump(sub, f)
+    try:
+        done, _, wall, res = ref.execute_plan_rows(f.name, {i: images[i] for i in sorted(need)}, hseed,
+                                                   threads=cores, want_matches=True)
+    finally:
+        os.unlink(f.name)
+    ri, ro, rm = res
+    gi, go, gm = gpu_flat
+    where = {(int(a), int(b)): p for p, (a, b) in enumerate(gi)}
+    eq = True
+    mine = []
+    for p, (a, b) in enumerate(ri):
+        g = where.get((int(a), int(b)))
+        got = gm[go[g]:go[g + 1]] if g is not None else None
+        if got is None or not np.array_equal(got, rm[ro[p]:ro[p + 1]]):
+            eq = False
+        mine.append(got if got is not None else np.zeros((0, 2), np.int32))
+    go_s = np.concatenate([[0], np.cumsum([len(x) for x in mine])]).astype(np.uint64)
+    gm_s = np.concatenate(mine) if mine else np.zeros((0, 2), np.int32)
+    return {"status": "equal" if eq else "DIFFERENT", "pairs": int(len(ri)), "matches": int(len(rm)),
+            "digest_gpu": digest(ri, go_s, gm_s), "digest_reference": digest(ri, ro, rm),
+            "reference": (f"oracle/_ref row body on a sample: the plan's last block row with its whole "
+                          f"needed set ({len(need)} images: the full row mean and codes), its first "
+                          f"{len(ri)} pairs; {wall:.1f} s on {cores} threads")}
+
+
 def parity_leg(feats, plan_path, rows, config, gpu_flat, cores):
     """Runs the compiled reference on the repo arm's own inputs (same
     arrays): its CPU time is the line's cpu_baseline, its match lists are
@@ -456,7 +506,7 @@ def parity_leg(feats, plan_path, rows, config, gpu_flat, cores):
     if config in SAMPLED:
         p, secs, sample = reference_sampled(ref, images, rows, cores)
         cpu = {"value": p / secs, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample}
-        return cpu, {"status": "not checked in the bench (sampled CPU leg; see tests/test_gpu_parity.py)"}
+        return cpu, sampled_parity(ref, hseed, images, plan_path, gpu_flat, cores)
     table = ref.feature_table(images)
     done, m, wall, res = ref.execute_plan_rows(plan_path, table, hseed, threads=cores, want_matches=True)
     table.free()
@@ -703,7 +753,9 @@ def main():
             shutil.rmtree(tmpd, ignore_errors=True)
 
     # ---- value: the same row loop on HBM-resident images ---------------------
-    arena = bm.DeviceArena(cap * 2, hf, dev)
+    # every image of the rank stays resident (config 4: ~42 GB of
+    # descriptors + projections; fits one B200)
+    arena = bm.DeviceArena(max(cap * 2, sum(len(fs.descriptors) for fs in feats.values()) + 1), hf, dev)
     for i, fs in feats.items():
         arena.upload(i, fs.descriptors)
     arena.matcher.synchronize()

@@ -14,6 +14,8 @@ fixtures under bench_data/.
   shard16k  BASELINE config 4, one GPU's shard: 640 of the 5,000 images at
             16,384 descriptors, band 15 (the 30 nearest neighbours), same
             CLI-default budget
+  config4   BASELINE config 4 in full: 5,000 images at 16,384 descriptors,
+            band 15 (74,880 pairs), same budget: 25 block rows
   strip1000 / strip2000 / strip4000
             the strip500 workload weak-scaled to 2 / 4 / 8 GPUs: a strip of
             500 N images, same band and budget (bench.py --gpus N shards it
@@ -40,7 +42,8 @@ def main():
     OUT.mkdir(exist_ok=True)
     r = Reference()
     for name, n, band, blk, gpu in [("pair1", 2, 1, 1, 2), ("block32", 32, 11, 16, 32), ("strip500", 500, 10, 200, 400),
-                                    ("shard16k", 640, 15, 200, 400), ("strip1000", 1000, 10, 200, 400),
+                                    ("shard16k", 640, 15, 200, 400), ("config4", 5000, 15, 200, 400),
+                                    ("strip1000", 1000, 10, 200, 400),
                                     ("strip2000", 2000, 10, 200, 400), ("strip4000", 4000, 10, 200, 400)]:
         r.iterate_schedule(np.arange(n), band_pairs(n, band), blk, gpu, OUT / f"plan_{name}.json")
         print(name, (OUT / f"plan_{name}.json").stat().st_size)
