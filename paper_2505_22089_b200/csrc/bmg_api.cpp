@@ -15,6 +15,7 @@
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -554,6 +555,34 @@ void slot_dma(Ctx& c, int i, void* dst, size_t bytes) {
   BMG_CUDA(cudaEventRecord(c.stage_ev[i], c.s_copy));
 }
 
+// Copy into a pinned staging slot with streaming (non-temporal) stores: the
+// slot is only read by the copy engine, so a plain memcpy's read-for-
+// ownership of every destination line is wasted host-memory traffic (the
+// staging competes with the DMA for it).  dst 16-byte aligned.
+void stream_copy(char* dst, const char* src, size_t n) {
+  static const bool plain = [] {
+    const char* v = getenv("BMG_STAGE_MEMCPY");  // A/B switch
+    return v && v[0] == '1';
+  }();
+  if (plain || (reinterpret_cast<uintptr_t>(dst) & 15u)) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  size_t i = 0;
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c2);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  if (i < n) std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();  // the stores are visible before the DMA is issued
+}
+
 void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
   cudaPointerAttributes attr{};
   const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess &&
@@ -574,10 +603,10 @@ void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
     int i;
     char* slot = next_slot(c, &i);
     const int parts = static_cast<int>(std::min<size_t>(pool.size(), (sz + (256u << 10) - 1) >> 18));
-    const size_t per = (sz + parts - 1) / parts;
+    const size_t per = ((sz + parts - 1) / parts + 63) & ~static_cast<size_t>(63);
     pool.run(parts, [&](int k) {
       const size_t a = k * per, n = a < sz ? std::min(per, sz - a) : 0;
-      if (n) std::memcpy(slot + a, s + off + a, n);
+      if (n) stream_copy(slot + a, s + off + a, n);
     });
     slot_dma(c, i, d + off, sz);
   }

@@ -1,7 +1,7 @@
 """Where the end-to-end execute_plan time goes (bench workload, N=1): Python
 wall, C++ wall (bmg_execute_plan), device span, per step.  BMG_TIMELINE=1
 adds the per-row event timeline on stderr.
-usage: python tools/e2e_probe.py [config] [steps]"""
+usage: python tools/e2e_probe.py [config] [steps] [pageable]"""
 import sys, time
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
@@ -14,6 +14,7 @@ from paper_2505_22089_b200.features import SyntheticScene, generate_synthetic
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "strip500"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+pageable = len(sys.argv) > 3 and sys.argv[3] == "pageable"
 keep = []
 def pinned(nbytes):
     t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True); keep.append(t); return t.numpy()
@@ -27,6 +28,9 @@ for i, fs in enumerate(imgs[drop:]):
 hf = bm.make_hash_functions(bm.seed_for(bench.HASH_ROOT_SEED, "matching"))
 cap = bm.arena_units_for(feats, plan.size_gpu)
 flat = bm.flatten_plan(plan)
+if pageable:  # the reference's FeatureSet: pageable std::vector
+    import numpy as np
+    feats = {i: bm.FeatureSet(i, np.array(fs.descriptors)) for i, fs in feats.items()}
 views = _feature_views(feats)
 arena = bm.DeviceArena(cap, hf, 0)
 opts = bm.ExecuteOptions()
