@@ -272,7 +272,40 @@ __device__ __forceinline__ bool tile_certified(i128 v, const TileRange& rg, uint
   return m == 0 || top_bit(m) - low <= 52;
 }
 
-constexpr int kResolveThreads = 256;
+#ifndef BMG_RESOLVE_THREADS
+#define BMG_RESOLVE_THREADS 256
+#endif
+constexpr int kResolveThreads = BMG_RESOLVE_THREADS;
+
+// exclusive block scan of one i128 per thread (warp shuffles, then the warp
+// totals in shared memory); returns the block total in *total
+__device__ __forceinline__ i128 block_excl_scan_i128(i128 v, i128* s_w, i128* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  i128 incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const i128 y = shfl_up_i128(incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    i128 w = lane < nw ? s_w[lane] : (i128)0;
+    i128 wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const i128 y = shfl_up_i128(wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < nw) s_w[lane] = wi - w;  // exclusive warp offsets
+    if (lane == 31) s_w[32] = wi;
+  }
+  __syncthreads();
+  const i128 out = s_w[warp] + incl - v;
+  *total = s_w[32];
+  __syncthreads();
+  return out;
+}
 
 // tile t of the row -> its statistics' offset in its image's arrays
 __device__ __forceinline__ const ImgDev& tile_of(const ImgDev* imgs, const uint32_t* tile_img,
@@ -286,7 +319,7 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
     const ImgDev* __restrict__ imgs, const uint32_t* __restrict__ tile_img,
     const uint32_t* __restrict__ tile_start, i128* __restrict__ tile_sum, int n_tiles, unsigned long long total,
     MeanState* st, float* __restrict__ mean_out, double* __restrict__ acc_out) {
-  __shared__ i128 part[kResolveThreads];
+  __shared__ i128 part[33];
   __shared__ i128 s_delta;
   __shared__ int s_fail;
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
@@ -303,7 +336,6 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
     loc += static_cast<const i128*>(im.tsum)[o];
     bad |= im.tlow[o] == kBadTile;
   }
-  part[tid] = loc;
   if (__syncthreads_or(bad)) {
     if (tid == 0) {
       st->bad = 1u;
@@ -311,18 +343,9 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
     }
     return;
   }
-  if (tid == 0) {
-    i128 run = 0;
-    for (int i = 0; i < kResolveThreads; ++i) {
-      const i128 v = part[i];
-      part[i] = run;
-      run += v;
-    }
-    s_delta = run;  // temporarily: the row total
-  }
-  __syncthreads();
+  i128 row_total;
   {
-    i128 run = part[tid];
+    i128 run = block_excl_scan_i128(loc, part, &row_total);
     for (int t = t0; t < t1; ++t) {
       size_t o;
       const ImgDev& im = tile_of(imgs, tile_img, tile_start, t, c, o);
@@ -330,9 +353,8 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
       run += static_cast<const i128*>(im.tsum)[o];
     }
   }
-  const i128 row_total = s_delta;
-  __syncthreads();
   if (tid == 0) s_delta = 0;
+  __syncthreads();  // the prefixes in tile_sum are read by other threads below
 
   // ---- certify / walk
   i128 delta = 0;
@@ -344,20 +366,24 @@ __global__ void __launch_bounds__(kResolveThreads) mean_resolve_kernel(
     // one pass over its tiles plus one window per walked tile)
     int f = 0x7fffffff;
     for (int w0 = cur; w0 < n_tiles; w0 += kResolveThreads) {
-      if (tid == 0) s_fail = 0x7fffffff;
-      __syncthreads();
       const int t = w0 + tid;
+      bool fail = false;
       if (t < n_tiles) {
         size_t o;
         const ImgDev& im = tile_of(imgs, tile_img, tile_start, t, c, o);
-        if (!tile_certified(tile_sum[(size_t)t * kDim + c] + delta, static_cast<const TileRange*>(im.trng)[o],
-                            im.tlow[o]))
-          atomicMin(&s_fail, t);
+        fail = !tile_certified(tile_sum[(size_t)t * kDim + c] + delta, static_cast<const TileRange*>(im.trng)[o],
+                               im.tlow[o]);
       }
-      __syncthreads();
-      f = s_fail;
-      __syncthreads();
-      if (f != 0x7fffffff) break;
+      // one barrier per certified window; the first failing tile only when
+      // there is one
+      if (__syncthreads_or(fail)) {
+        if (tid == 0) s_fail = 0x7fffffff;
+        __syncthreads();
+        if (fail) atomicMin(&s_fail, t);
+        __syncthreads();
+        f = s_fail;
+        break;
+      }
     }
     if (f == 0x7fffffff) break;
     if (walked >= kMeanMaxWalks) {
@@ -1385,7 +1411,21 @@ __global__ void __launch_bounds__(1024) tables_fused_kernel(HashDev h, const Img
   uint64_t* bfine = im.bfine + (size_t)t * im.ns * h.fwp;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s_cnt[b] = 0u;
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < im.n; i += blockDim.x) atomicAdd(s_cnt + im.coarse[(size_t)i * L + t], 1u);
+  // bucket ids are loaded kTblBatch per thread ahead of their shared
+  // atomics (independent loads in flight instead of load -> atomic chains)
+  constexpr int kTblBatch = 8;
+  const uint32_t* ccol = im.coarse + t;
+  for (uint32_t i0 = 0; i0 < im.n; i0 += kTblBatch * blockDim.x) {
+    uint32_t bk[kTblBatch];
+#pragma unroll
+    for (int j = 0; j < kTblBatch; ++j) {
+      const uint32_t i = i0 + j * blockDim.x + threadIdx.x;
+      bk[j] = i < im.n ? __ldg(ccol + (size_t)i * L) : kEmpty;
+    }
+#pragma unroll
+    for (int j = 0; j < kTblBatch; ++j)
+      if (bk[j] != kEmpty) atomicAdd(s_cnt + bk[j], 1u);
+  }
   __syncthreads();
   uint32_t carry = 0;
   if (threadIdx.x == 0) off[0] = 0u;
@@ -1412,10 +1452,25 @@ __global__ void __launch_bounds__(1024) tables_fused_kernel(HashDev h, const Img
     slots[k] = kEmpty;
     for (int x = 0; x < h.fwp; ++x) bfine[(size_t)k * h.fwp + x] = 0ull;
   }
-  for (uint32_t i = threadIdx.x; i < im.n; i += blockDim.x) {
-    const uint32_t pos = atomicAdd(s_cnt + im.coarse[(size_t)i * L + t], 1u);
-    slots[pos] = i;
-    for (int x = 0; x < h.fwp; ++x) bfine[(size_t)pos * h.fwp + x] = im.fine[(size_t)i * h.fwp + x];
+  for (uint32_t i0 = 0; i0 < im.n; i0 += kTblBatch * blockDim.x) {
+    uint32_t bk[kTblBatch];
+#pragma unroll
+    for (int j = 0; j < kTblBatch; ++j) {
+      const uint32_t i = i0 + j * blockDim.x + threadIdx.x;
+      bk[j] = i < im.n ? __ldg(ccol + (size_t)i * L) : kEmpty;
+    }
+#pragma unroll
+    for (int j = 0; j < kTblBatch; ++j) {
+      if (bk[j] == kEmpty) continue;
+      const uint32_t i = i0 + j * blockDim.x + threadIdx.x;
+      const uint32_t pos = atomicAdd(s_cnt + bk[j], 1u);
+      slots[pos] = i;
+      if (h.fwp == 2) {
+        reinterpret_cast<ulonglong2*>(bfine)[pos] = __ldg(reinterpret_cast<const ulonglong2*>(im.fine) + i);
+      } else {
+        for (int x = 0; x < h.fwp; ++x) bfine[(size_t)pos * h.fwp + x] = im.fine[(size_t)i * h.fwp + x];
+      }
+    }
   }
 }
 
