@@ -728,8 +728,9 @@ ImgDev proj_view(const ArenaImage& a) {
 // The H2D of a reserved image on the copy stream; the projection stream then
 // computes its mean-independent projections (K2 project_kernel) while the
 // next images upload, and records the image's ready event.
-void arena_copy(Ctx& c, ArenaImage& im, const Source& src) {
-  stage_source(c, im.d, src);
+// after an image's H2D is on the copy stream: its projections (and the
+// row-mean tile statistics) right behind it on a projection stream
+void arena_after_copy(Ctx& c, ArenaImage& im) {
   BMG_CUDA(cudaEventRecord(c.ev_copied, c.s_copy));
   im.pstream = c.proj_rr;
   c.proj_rr = (c.proj_rr + 1) % bmg_context::kProjStreams;
@@ -745,6 +746,80 @@ void arena_copy(Ctx& c, ArenaImage& im, const Source& src) {
   BMG_CUDA(cudaEventRecord(im.ev, ps));
   im.seq = ++g_upload_seq;
   c.pending_upload = true;
+}
+
+void arena_copy(Ctx& c, ArenaImage& im, const Source& src) {
+  stage_source(c, im.d, src);
+  arena_after_copy(c, im);
+}
+
+// A row's missing images in order: pinned arrays go straight to the copy
+// engine and files through stage_file, one image at a time; consecutive
+// pageable arrays that fit one staging slot together are memcpy'd into it
+// by one fork-join of the host pool (one wake-up per slot, not per image),
+// then DMA'd image by image, each followed by its projections.
+void arena_copy_many(Ctx& c, const std::vector<std::pair<ArenaImage*, const Source*>>& imgs,
+                     const std::function<void(size_t)>& after) {
+  auto pageable = [&](const Source& src) {
+    if (src.path || !src.desc || src.count == 0) return false;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, src.desc) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return !pinned;
+  };
+  static const bool batch_off = [] {
+    const char* v = getenv("BMG_STAGE_BATCH");  // A/B switch: 0 = one image per fork-join
+    return v && v[0] == '0';
+  }();
+  size_t k = 0;
+  while (k < imgs.size()) {
+    const Source& s0 = *imgs[k].second;
+    const size_t b0 = s0.count * kDim * sizeof(float);
+    if (batch_off || !pageable(s0) || b0 > c.stage_bytes) {
+      arena_copy(c, *imgs[k].first, s0);
+      after(k++);
+      continue;
+    }
+    // pack images [k, e) into one slot
+    size_t e = k + 1, used = b0;
+    while (e < imgs.size()) {
+      const Source& se = *imgs[e].second;
+      const size_t be = align_up(se.count * kDim * sizeof(float), 256);
+      if (!pageable(se) || align_up(used, 256) + be > c.stage_bytes) break;
+      used = align_up(used, 256) + be;
+      ++e;
+    }
+    int si;
+    char* slot = next_slot(c, &si);
+    std::vector<size_t> off(e - k);
+    size_t o = 0;
+    for (size_t j = k; j < e; ++j) {
+      o = align_up(o, 256);
+      off[j - k] = o;
+      o += imgs[j].second->count * kDim * sizeof(float);
+    }
+    constexpr size_t kPart = 256u << 10;
+    std::vector<std::pair<size_t, size_t>> parts;  // (image in batch, byte offset)
+    for (size_t j = k; j < e; ++j) {
+      const size_t bj = imgs[j].second->count * kDim * sizeof(float);
+      for (size_t a = 0; a < bj; a += kPart) parts.emplace_back(j - k, a);
+    }
+    HostPool& pool = host_pool(c);
+    pool.run(static_cast<int>(parts.size()), [&](int q) {
+      const auto [j, a] = parts[q];
+      const Source& src = *imgs[k + j].second;
+      const size_t bj = src.count * kDim * sizeof(float);
+      stream_copy(slot + off[j] + a, reinterpret_cast<const char*>(src.desc) + a, std::min(kPart, bj - a));
+    });
+    for (size_t j = k; j < e; ++j) {
+      BMG_CUDA(cudaMemcpyAsync(imgs[j].first->d, slot + off[j - k], imgs[j].second->count * kDim * sizeof(float),
+                               cudaMemcpyHostToDevice, c.s_copy));
+      if (j + 1 == e) BMG_CUDA(cudaEventRecord(c.stage_ev[si], c.s_copy));
+      arena_after_copy(c, *imgs[j].first);
+      after(j);
+    }
+    k = e;
+  }
 }
 
 void arena_upload(Ctx& c, uint64_t id, const float* desc, uint64_t n) {
@@ -2008,9 +2083,13 @@ void execute_plan_impl(Ctx* c, const bmg_plan* plan, const std::unordered_map<ui
         }
         std::stable_sort(missing.begin(), missing.end(),
                          [&](uint64_t x, uint64_t y) { return last_need[x] > last_need[y]; });
-        for (size_t k = 0; k < missing.size(); ++k) {
-          arena_copy(*c, c->resident.at(missing[k]), features_of(missing[k]));
-          if (timeline && k % 25 == 24) mark("row " + std::to_string(r) + " upload " + std::to_string(k + 1), c->s_copy);
+        {
+          std::vector<std::pair<ArenaImage*, const Source*>> mv;
+          mv.reserve(missing.size());
+          for (uint64_t id : missing) mv.emplace_back(&c->resident.at(id), &features_of(id));
+          arena_copy_many(*c, mv, [&](size_t k) {
+            if (timeline && k % 25 == 24) mark("row " + std::to_string(r) + " upload " + std::to_string(k + 1), c->s_copy);
+          });
         }
         if (!missing.empty()) mark("row " + std::to_string(r) + " uploads done", c->s_copy);
         // the row's mean waits only for the copies (the copy stream is in
