@@ -559,7 +559,7 @@ void slot_dma(Ctx& c, int i, void* dst, size_t bytes) {
 // slot is only read by the copy engine, so a plain memcpy's read-for-
 // ownership of every destination line is wasted host-memory traffic (the
 // staging competes with the DMA for it).  dst 16-byte aligned.
-void stream_copy(char* dst, const char* src, size_t n) {
+void stream_copy(char* dst, const char* src, size_t n, bool fence = true) {
   static const bool plain = [] {
     const char* v = getenv("BMG_STAGE_MEMCPY");  // A/B switch
     return v && v[0] == '1';
@@ -580,7 +580,7 @@ void stream_copy(char* dst, const char* src, size_t n) {
     _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
   }
   if (i < n) std::memcpy(dst + i, src + i, n - i);
-  _mm_sfence();  // the stores are visible before the DMA is issued
+  if (fence) _mm_sfence();  // the stores are visible before the DMA is issued
 }
 
 void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
@@ -659,7 +659,9 @@ void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
       if (have < m * kRecord) short_read.store(true);
       const uint64_t full = have / kRecord;
       for (uint64_t k = 0; k < full; ++k)
-        std::memcpy(slot + (b0 + k) * kDim, buf.data() + k * kRecord + 16, kDim * sizeof(float));
+        stream_copy(reinterpret_cast<char*>(slot + (b0 + k) * kDim),
+                    reinterpret_cast<const char*>(buf.data() + k * kRecord + 16), kDim * sizeof(float), false);
+      _mm_sfence();
     });
     if (short_read.load()) fail(BMG_TRUNCATED_FILE, "unexpected end of file while reading descriptor");
     slot_dma(c, i, d + r0 * kDim * sizeof(float), nr * kDim * sizeof(float));
