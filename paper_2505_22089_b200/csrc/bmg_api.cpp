@@ -616,7 +616,13 @@ void stage_h2d(Ctx& c, void* dst, const void* src, size_t bytes) {
 // read_features (features.cpp:222-236) and must agree with the planned
 // count; the 528-byte records are read by the host pool with pread and
 // de-interleaved into pinned slots, each DMA'd while the next fills.
-void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
+constexpr size_t kFeatHeader = 24, kFeatRecord = (4 + kDim) * sizeof(float);
+constexpr uint64_t kFeatBlock = 256;  // records per pread (~132 KiB): 32 reads per 8k image
+
+// Opens a feature file for streaming: the header is checked like
+// read_features (features.cpp:222-236) and must agree with the planned
+// count, and the body must hold every record.  Returns the descriptor.
+int open_feature_file(const char* path, uint64_t count) {
   uint64_t id = 0, n = 0;
   if (const int rc = bmg_read_features_header(path, &id, &n); rc != BMG_OK) fail(rc, bmg_last_error());
   if (n != count)
@@ -624,17 +630,49 @@ void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
                                    std::to_string(count));
   const int fd = open(path, O_RDONLY | O_CLOEXEC);
   if (fd < 0) fail(BMG_FORMAT_ERROR, std::string("cannot open ") + path + " for reading");
+  struct stat st{};
+  if (fstat(fd, &st) != 0) {
+    close(fd);
+    fail(BMG_FORMAT_ERROR, std::string("cannot stat ") + path);
+  }
+  const uint64_t body =
+      static_cast<uint64_t>(st.st_size) > kFeatHeader ? static_cast<uint64_t>(st.st_size) - kFeatHeader : 0;
+  if (body < count * kFeatRecord) {
+    close(fd);
+    fail(BMG_TRUNCATED_FILE, std::string("unexpected end of file while reading ") +
+                                 (body % kFeatRecord < 16 ? "keypoint" : "descriptor"));
+  }
+  return fd;
+}
+
+// Records [r0, r0 + m) of an open feature file, de-interleaved into dst
+// (streaming stores; the caller fences).  Returns false on a short read.
+bool read_feature_block(int fd, uint64_t r0, uint64_t m, float* dst) {
+  thread_local std::vector<unsigned char> buf;
+  buf.resize(kFeatBlock * kFeatRecord);
+  const off_t off = static_cast<off_t>(kFeatHeader + r0 * kFeatRecord);
+  size_t have = 0;
+  while (have < m * kFeatRecord) {
+    const ssize_t got = pread(fd, buf.data() + have, m * kFeatRecord - have, off + static_cast<off_t>(have));
+    if (got <= 0) break;
+    have += static_cast<size_t>(got);
+  }
+  const uint64_t full = have / kFeatRecord;
+  for (uint64_t k = 0; k < full; ++k)
+    stream_copy(reinterpret_cast<char*>(dst + k * kDim),
+                reinterpret_cast<const char*>(buf.data() + k * kFeatRecord + 16), kDim * sizeof(float), false);
+  return have >= m * kFeatRecord;
+}
+
+// A feature file's descriptors straight into HBM: the 528-byte records are
+// read by the host pool with pread and de-interleaved into pinned slots,
+// each DMA'd while the next fills.
+void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
+  const int fd = open_feature_file(path, count);
   struct FdGuard {
     int fd;
     ~FdGuard() { close(fd); }
   } guard{fd};
-  constexpr size_t kHeader = 24, kRecord = (4 + kDim) * sizeof(float);
-  struct stat st{};
-  if (fstat(fd, &st) != 0) fail(BMG_FORMAT_ERROR, std::string("cannot stat ") + path);
-  const uint64_t body = static_cast<uint64_t>(st.st_size) > kHeader ? static_cast<uint64_t>(st.st_size) - kHeader : 0;
-  if (body < count * kRecord)
-    fail(BMG_TRUNCATED_FILE, std::string("unexpected end of file while reading ") +
-                                 (body % kRecord < 16 ? "keypoint" : "descriptor"));
   HostPool& pool = host_pool(c);
   const uint64_t per_slot = c.stage_bytes / (kDim * sizeof(float));
   char* d = static_cast<char*>(dst);
@@ -642,25 +680,11 @@ void stage_file(Ctx& c, void* dst, const char* path, uint64_t count) {
     const uint64_t nr = std::min(per_slot, count - r0);
     int i;
     float* slot = reinterpret_cast<float*>(next_slot(c, &i));
-    constexpr uint64_t kBlock = 256;  // records per pread (~132 KiB): 32 reads per 8k image
-    const int blocks = static_cast<int>((nr + kBlock - 1) / kBlock);
+    const int blocks = static_cast<int>((nr + kFeatBlock - 1) / kFeatBlock);
     std::atomic<bool> short_read{false};
     pool.run(blocks, [&](int b) {
-      thread_local std::vector<unsigned char> buf;
-      buf.resize(kBlock * kRecord);
-      const uint64_t b0 = b * kBlock, m = std::min(kBlock, nr - b0);
-      const off_t off = static_cast<off_t>(kHeader + (r0 + b0) * kRecord);
-      size_t have = 0;
-      while (have < m * kRecord) {
-        const ssize_t got = pread(fd, buf.data() + have, m * kRecord - have, off + static_cast<off_t>(have));
-        if (got <= 0) break;
-        have += static_cast<size_t>(got);
-      }
-      if (have < m * kRecord) short_read.store(true);
-      const uint64_t full = have / kRecord;
-      for (uint64_t k = 0; k < full; ++k)
-        stream_copy(reinterpret_cast<char*>(slot + (b0 + k) * kDim),
-                    reinterpret_cast<const char*>(buf.data() + k * kRecord + 16), kDim * sizeof(float), false);
+      const uint64_t b0 = b * kFeatBlock, m = std::min(kFeatBlock, nr - b0);
+      if (!read_feature_block(fd, r0 + b0, m, slot + b0 * kDim)) short_read.store(true);
       _mm_sfence();
     });
     if (short_read.load()) fail(BMG_TRUNCATED_FILE, "unexpected end of file while reading descriptor");
@@ -762,6 +786,7 @@ void arena_copy(Ctx& c, ArenaImage& im, const Source& src) {
 // then DMA'd image by image, each followed by its projections.
 void arena_copy_many(Ctx& c, const std::vector<std::pair<ArenaImage*, const Source*>>& imgs,
                      const std::function<void(size_t)>& after) {
+  auto is_file = [&](const Source& src) { return src.path != nullptr && src.count > 0; };
   auto pageable = [&](const Source& src) {
     if (src.path || !src.desc || src.count == 0) return false;
     cudaPointerAttributes attr{};
@@ -777,20 +802,31 @@ void arena_copy_many(Ctx& c, const std::vector<std::pair<ArenaImage*, const Sour
   while (k < imgs.size()) {
     const Source& s0 = *imgs[k].second;
     const size_t b0 = s0.count * kDim * sizeof(float);
-    if (batch_off || !pageable(s0) || b0 > c.stage_bytes) {
+    const bool files = is_file(s0);
+    if (batch_off || !(files || pageable(s0)) || b0 > c.stage_bytes) {
       arena_copy(c, *imgs[k].first, s0);
       after(k++);
       continue;
     }
-    // pack images [k, e) into one slot
+    // pack images [k, e) of the same kind into one slot
     size_t e = k + 1, used = b0;
     while (e < imgs.size()) {
       const Source& se = *imgs[e].second;
       const size_t be = align_up(se.count * kDim * sizeof(float), 256);
-      if (!pageable(se) || align_up(used, 256) + be > c.stage_bytes) break;
+      if ((files ? !is_file(se) : !pageable(se)) || align_up(used, 256) + be > c.stage_bytes) break;
       used = align_up(used, 256) + be;
       ++e;
     }
+    // files: headers checked and opened in order before any read
+    std::vector<int> fds;
+    struct FdsGuard {
+      std::vector<int>& v;
+      ~FdsGuard() {
+        for (int fd : v) close(fd);
+      }
+    } fds_guard{fds};
+    if (files)
+      for (size_t j = k; j < e; ++j) fds.push_back(open_feature_file(imgs[j].second->path, imgs[j].second->count));
     int si;
     char* slot = next_slot(c, &si);
     std::vector<size_t> off(e - k);
@@ -800,19 +836,28 @@ void arena_copy_many(Ctx& c, const std::vector<std::pair<ArenaImage*, const Sour
       off[j - k] = o;
       o += imgs[j].second->count * kDim * sizeof(float);
     }
-    constexpr size_t kPart = 256u << 10;
+    // tasks: 256 KiB of a pageable array, or kFeatBlock records of a file
+    const size_t kPart = files ? kFeatBlock * kDim * sizeof(float) : (256u << 10);
     std::vector<std::pair<size_t, size_t>> parts;  // (image in batch, byte offset)
     for (size_t j = k; j < e; ++j) {
       const size_t bj = imgs[j].second->count * kDim * sizeof(float);
       for (size_t a = 0; a < bj; a += kPart) parts.emplace_back(j - k, a);
     }
     HostPool& pool = host_pool(c);
+    std::atomic<bool> short_read{false};
     pool.run(static_cast<int>(parts.size()), [&](int q) {
       const auto [j, a] = parts[q];
       const Source& src = *imgs[k + j].second;
       const size_t bj = src.count * kDim * sizeof(float);
-      stream_copy(slot + off[j] + a, reinterpret_cast<const char*>(src.desc) + a, std::min(kPart, bj - a));
+      if (files) {
+        const uint64_t r0 = a / (kDim * sizeof(float)), m = std::min<uint64_t>(kFeatBlock, src.count - r0);
+        if (!read_feature_block(fds[j], r0, m, reinterpret_cast<float*>(slot + off[j] + a))) short_read.store(true);
+        _mm_sfence();
+      } else {
+        stream_copy(slot + off[j] + a, reinterpret_cast<const char*>(src.desc) + a, std::min(kPart, bj - a));
+      }
     });
+    if (short_read.load()) fail(BMG_TRUNCATED_FILE, "unexpected end of file while reading descriptor");
     for (size_t j = k; j < e; ++j) {
       BMG_CUDA(cudaMemcpyAsync(imgs[j].first->d, slot + off[j - k], imgs[j].second->count * kDim * sizeof(float),
                                cudaMemcpyHostToDevice, c.s_copy));
