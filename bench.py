@@ -897,8 +897,12 @@ def main():
             line["retrieval"] = {"unavailable": str(e)}
     if rank == 0 and world > 1:
         gi, go, gm = gpu_flat
-        line["parity"] = {"status": "gathered result digest (compare with the N=1 line's digest_gpu)",
+        line["parity"] = {"status": "gathered result digest (compare with the N=1 line's result_digest)",
                           "digest_gpu": digest(gi, go, gm), "pairs": int(len(gi)), "matches": int(len(gm))}
+    if rank == 0:
+        # digest of the whole result (every pair), comparable across N
+        gi, go, gm = gpu_flat
+        line["result_digest"] = {"digest": digest(gi, go, gm), "pairs": int(len(gi)), "matches": int(len(gm))}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
