@@ -384,6 +384,23 @@ struct RowSlot {
     done = nullptr;
   }
 };
+// One VLAD batch in flight (bmg_encode_vlad alternates two): device
+// buffers and mapped host tables, kept by the context across calls
+// (grow-only, like the row slots).
+struct VladSlot {
+  DevBuf desc, assign, fix, fixcnt, acc, members, member_off, dmeta;
+  HostMapped meta, out;
+  cudaEvent_t done = nullptr;
+  std::vector<uint64_t> imgs;  // caller indices of the batch
+  void release() {
+    for (DevBuf* b : {&desc, &assign, &fix, &fixcnt, &acc, &members, &member_off, &dmeta}) b->release();
+    meta.release();
+    out.release();
+    if (done) cudaEventDestroy(done);
+    done = nullptr;
+    imgs.clear();
+  }
+};
 }  // namespace
 }  // namespace bmg
 
@@ -404,6 +421,7 @@ struct bmg_context {
   cudaEvent_t ev_copied = nullptr;
   uint64_t exec_serial = 0;        // execute_plan calls so far (re-projection epochs)
   bmg::RowSlot slot[2];
+  bmg::VladSlot vlad[2];
   int cur = 0;
   bmg::RowSlot& S() { return slot[cur]; }
   bool mean_chain_only = false;  // test hook: the literal sequential chain
@@ -1536,6 +1554,7 @@ int bmg_destroy(bmg_context* c) {
     for (DevBuf* b : {&c->planes_t, &c->planes, &c->plane_norm, &c->tc_b, &c->tc_fexp, &c->d_tmp_desc, &c->d_tmp_codes, &c->d_rp})
       b->release();
     for (RowSlot& sl : c->slot) sl.release();
+    for (VladSlot& v : c->vlad) v.release();
     c->res_ranges.release();
     c->res_log.release();
     c->d_res.release();
@@ -2356,32 +2375,25 @@ size_t vlad_batch_bytes() {  // BMG_VLAD_BATCH_BYTES: test hook (multi-batch pat
   if (const char* e = std::getenv("BMG_VLAD_BATCH_BYTES")) return std::max<size_t>(std::strtoull(e, nullptr, 10), 1);
   return size_t(256) << 20;
 }
-struct VladSlot {
-  DevBuf desc, assign, fix, fixcnt, acc, members, member_off, dmeta;
-  HostMapped meta, out;
-  cudaEvent_t done = nullptr;
-  std::vector<uint64_t> imgs;  // caller indices of the batch
-};
 }  // namespace
 }  // namespace bmg
 
 int bmg_encode_vlad(bmg_context* c, const float* centroids, int k_words, const bmg_feature_view* images,
                     uint64_t n_images, float* values_out, uint8_t* degenerate_out) {
   using namespace bmg;
-  VladSlot vs[2];
+  // the two batch slots persist in the context (no per-call allocation);
+  // on any exit their last batches are waited for
   auto cleanup = [&] {
-    for (VladSlot& v : vs) {
+    if (!c) return;
+    for (VladSlot& v : c->vlad) {
       if (v.done) cudaEventSynchronize(v.done);
-      for (DevBuf* b : {&v.desc, &v.assign, &v.fix, &v.fixcnt, &v.acc, &v.members, &v.member_off, &v.dmeta})
-        b->release();
-      v.meta.release();
-      v.out.release();
-      if (v.done) cudaEventDestroy(v.done);
-      v.done = nullptr;
+      v.imgs.clear();
     }
   };
   const int rc = guarded([&] {
     if (!c) fail(BMG_INVALID_ARGUMENT, "null argument");
+    VladSlot* vs = c->vlad;
+    for (int k = 0; k < 2; ++k) vs[k].imgs.clear();
     if (k_words < 1) fail(BMG_INVALID_ARGUMENT, "codebook has no words");  // retrieval.cpp:161
     if (k_words > kVladMaxWords)
       fail(BMG_UNSUPPORTED, "codebooks of more than " + std::to_string(kVladMaxWords) +
@@ -2406,7 +2418,8 @@ int bmg_encode_vlad(bmg_context* c, const float* centroids, int k_words, const b
       }
       v.imgs.clear();
     };
-    for (VladSlot& v : vs) BMG_CUDA(cudaEventCreateWithFlags(&v.done, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k)
+      if (!vs[k].done) BMG_CUDA(cudaEventCreateWithFlags(&vs[k].done, cudaEventDisableTiming));
     int si = 0;
     const size_t batch_bytes = vlad_batch_bytes();
     for (uint64_t i0 = 0; i0 < n_images;) {
