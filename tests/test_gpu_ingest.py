@@ -86,3 +86,38 @@ def test_pageable_staging_equals_pinned(reference, tmp_path):
     b = bm.execute_plan(plan, page, bm.DeviceArena(cap, hf))
     for x, y in zip(multigpu.result_flat(a), multigpu.result_flat(b)):
         assert np.array_equal(x, y)
+
+
+def test_mixed_pinned_pageable_unaligned_and_oversized_sources(reference, tmp_path):
+    """The staging packs consecutive pageable images into one pinned slot per
+    fork-join and sends pinned ones straight to the copy engine: a plan whose
+    images alternate between the two, with pageable arrays at odd (4-byte,
+    not 16-byte) addresses, odd counts and one image larger than a staging
+    slot (16 MiB), gives the pinned-only result."""
+    import torch
+    imgs, _, plan, _ = scene(reference, tmp_path, n=12, ppi=3001, band=4)
+    big = np.concatenate([imgs[5]] * 12)  # ~36k descriptors: 18 MB > one slot
+    big = big[: (16 << 20) // 512 + 777]
+    imgs = [big if i == 5 else d for i, d in enumerate(imgs)]
+    hf = bm.make_hash_functions(bm.seed_for(42, "matching"))
+    pinned = {}
+    for i, d in enumerate(imgs):
+        t = torch.empty(d.shape, dtype=torch.float32, pin_memory=True)
+        t.numpy()[...] = d
+        pinned[i] = bm.FeatureSet(i, t.numpy())
+    mixed = {}
+    for i, d in enumerate(imgs):
+        if i % 3 == 1:
+            mixed[i] = pinned[i]
+        else:
+            buf = np.empty(d.size + 1, np.float32)  # one float of offset: 4-byte aligned source
+            view = buf[1:].reshape(d.shape)
+            view[...] = d
+            assert view.ctypes.data % 16 != 0
+            mixed[i] = bm.FeatureSet(i, view)
+    cap = engine.arena_units_for(pinned, plan.size_gpu)
+    a = bm.execute_plan(plan, pinned, bm.DeviceArena(cap, hf))
+    b = bm.execute_plan(plan, mixed, bm.DeviceArena(cap, hf))
+    for x, y in zip(multigpu.result_flat(a), multigpu.result_flat(b)):
+        assert np.array_equal(x, y)
+    assert a.metrics.uploads == b.metrics.uploads
