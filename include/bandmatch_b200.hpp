@@ -16,6 +16,7 @@
 //                opts, graph)              |                              arena, opts, graph)
 //     engine.cpp:411-527                   |   (call sites: bandmatch_cli.cpp:234, :278)
 //   encode_vlad(fs, cb) per image          | bandmatch_b200::encode_vlad_batch(ctx, feats, cb)
+//   train_codebook(pool, k, iters, seed)    | bandmatch_b200::train_codebook(ctx, pool, k, iters, seed)
 //     retrieval.cpp:160-205                |
 //   select_pairs(feats, cb, top_n, hnsw,   | bandmatch_b200::select_pairs(ctx, feats, cb, top_n,
 //                seed) retrieval.cpp:386   |                              hnsw, seed)
@@ -418,6 +419,27 @@ inline std::vector<bandmatch::VladVector> encode_vlad_batch(Context& ctx,
     out[i].degenerate = deg[i] != 0;
   }
   return out;
+}
+
+// train_codebook (retrieval.hpp:34-36, retrieval.cpp:56-158) on the device:
+// the reference's seeding and Lloyd iterations, bit-exact centroids and SSE
+// history; errors as the reference (InvalidArgument, TooFewDescriptors).
+inline bandmatch::Codebook train_codebook(Context& ctx, const std::vector<bandmatch::Descriptor>& descriptors,
+                                          int k_words, int max_iters, std::uint64_t seed,
+                                          std::vector<double>* sse_history = nullptr) {
+  static_assert(sizeof(bandmatch::Descriptor) == bandmatch::kDescriptorDim * sizeof(float),
+                "Descriptor must be float[128]");
+  const std::size_t dim = static_cast<std::size_t>(std::max(k_words, 1)) * bandmatch::kDescriptorDim;
+  std::vector<float> cent(dim);
+  std::vector<double> sse(static_cast<std::size_t>(std::max(max_iters, 1)));
+  int n_sse = 0;
+  check(bmg_train_codebook(ctx.get(), descriptors.empty() ? nullptr : descriptors[0].v.data(),
+                           descriptors.size(), k_words, max_iters, seed, cent.data(), sse.data(), &n_sse));
+  if (sse_history) sse_history->assign(sse.begin(), sse.begin() + n_sse);
+  bandmatch::Codebook cb;
+  cb.k_words = k_words;
+  cb.centroids = std::move(cent);
+  return cb;
 }
 
 // select_pairs (retrieval.cpp:386-415) with its per-image encode_vlad loop

@@ -106,7 +106,13 @@ int main() {
     std::vector<Descriptor> pool;
     for (const FeatureSet& fs : fv)
       for (std::size_t i = 0; i < fs.size(); i += 7) pool.push_back(fs.descriptors[i]);
-    const Codebook cb = train_codebook(pool, 16, 8, 11);
+    std::vector<double> rsse, gsse;
+    const Codebook cb = train_codebook(pool, 16, 8, 11, &rsse);
+    const Codebook gcb = bandmatch_b200::train_codebook(ctx, pool, 16, 8, 11, &gsse);
+    report(gcb.k_words == cb.k_words && gcb.centroids.size() == cb.centroids.size() &&
+               std::memcmp(gcb.centroids.data(), cb.centroids.data(), cb.centroids.size() * sizeof(float)) == 0 &&
+               rsse == gsse,
+           "train_codebook on the device equals the reference (centroids and SSE history), bit for bit");
     const std::vector<VladVector> gv = bandmatch_b200::encode_vlad_batch(ctx, fv, cb);
     bool eq = gv.size() == fv.size();
     for (std::size_t i = 0; eq && i < fv.size(); ++i) {
