@@ -304,6 +304,13 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def sm_max_mhz():
+    try:
+        return float(json.loads(PEAKS.read_text())["sm_max_mhz"])
+    except Exception:  # noqa: BLE001
+        return 1965.0  # B200 boost clock (B200_PROFILING.md)
+
+
 def ncu_traffic(avg_ctas_per_launch):
     """DRAM bytes of one match launch from the committed `ncu --set full`
     capture, scaled by CTA count (one CTA = 1,024 queries of one pair) from
@@ -314,6 +321,17 @@ def ncu_traffic(avg_ctas_per_launch):
         g = m["metrics"]["launch__grid_size"]
         grid = float(str(g[0] if isinstance(g, (list, tuple)) else g).split()[0].replace(",", ""))
         return m["dram_bytes_per_launch"] / grid * avg_ctas_per_launch
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def ncu_inst_per_cta():
+    """Warp instructions per match CTA (1,024 queries of one pair) from the
+    committed `ncu --set full` capture: the issue-slot roofline's work."""
+    try:
+        m = json.loads(NCU_SUMMARY.read_text())["match_kernel"]["metrics"]
+        num = lambda v: float(str(v[0] if isinstance(v, (list, tuple)) else v).split()[0].replace(",", ""))
+        return num(m["smsp__inst_executed.sum"]) / num(m["launch__grid_size"])
     except Exception:  # noqa: BLE001
         return None
 
@@ -830,6 +848,22 @@ def main():
     popc_per_launch = queries_per_launch * cand_q * 2 * fw
     gather_per_launch = queries_per_launch * cand_q * (8 * fw + 4)
 
+    def issue_roofline():
+        # the binding resource of K4 (ncu: issue-bound, ALU pipe ~64%): warp
+        # instructions per launch (committed ncu capture, per CTA x this
+        # run's CTAs per launch) / launch time, against 4 issue slots per SM
+        # per cycle at the sampled SM clock
+        ipc = ncu_inst_per_cta()
+        mhz = clocks.summary().get("sm_mhz") or sm_max_mhz()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        if not ipc or not mhz or avg_launch_s <= 0:
+            return None
+        achieved = ipc * step_ctas * args.steps / max(match_n, 1) / avg_launch_s
+        peak = 4.0 * sms * float(mhz) * 1e6
+        return {"achieved": achieved, "peak": peak, "unit": "warp inst/s", "frac": achieved / peak,
+                "note": "warp instructions per CTA from profiles/ncu_summary.json (ncu smsp__inst_executed) x CTAs "
+                        "per launch / launch time, vs 4 issue slots per SM per cycle at the sampled SM clock"}
+
     line = None
     if rank == 0:
         line = {
@@ -870,6 +904,7 @@ def main():
                          "frac": (popc_per_launch / avg_launch_s / micro["popc32_per_s"]
                                   if micro.get("popc32_per_s") and avg_launch_s > 0 else None),
                          "note": "32-bit POPC per candidate = 4 at 128 bits; peak: profiles/r2_microbench.json"},
+                "issue": issue_roofline(),
                 "l2_gather": {"achieved": gather_per_launch / avg_launch_s / 1e9 if avg_launch_s > 0 else 0.0,
                               "peak": micro.get("gather16_l2_gbs"), "unit": "GB/s",
                               "frac": (gather_per_launch / avg_launch_s / 1e9 / micro["gather16_l2_gbs"]
