@@ -4,7 +4,7 @@ hashmatch.cpp:311-332), native libbmg vs the compiled reference, on the
 host of the GPU box.  Files live in a scratch dir (page cache warm after the
 first pass: the numbers are the parsing / copy cost, not the disk's).
 
-usage: python tools/io_bench.py [n_files] [ppi] [out.json]"""
+usage: python tests/probes/io_bench.py [n_files] [ppi] [out.json]"""
 import json
 import os
 import sys
@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 import paper_2505_22089_b200 as bm  # noqa: E402

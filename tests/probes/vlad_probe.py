@@ -1,9 +1,9 @@
 """Timing probe: bmg_encode_vlad on N synthetic 8,192-descriptor images
 (pinned and pageable) vs the reference encode_vlad on the host cores.
-usage: python tools/vlad_probe.py [n_images] [cpu_images]"""
+usage: python tests/probes/vlad_probe.py [n_images] [cpu_images]"""
 import json, os, sys, time
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", ".."))
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
-sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "tests"))
 import numpy as np
 import torch
 import paper_2505_22089_b200 as bm
