@@ -71,8 +71,10 @@ bool in_circumcircle(const Pt& a, const Pt& b, const Pt& c, const Pt& d) {
 #endif
 constexpr double kMaxSpread = BMG_SAO_MAX_SPREAD;
 
-// distance of the closest pair of the first n points (grid of ~n cells; the
-// input has no duplicates here)
+// distance of the closest pair of the first n points: a flat grid of ~n
+// cells (points bucketed by a counting sort), each point against the points
+// of the rings of cells around it, widening until a ring lies beyond the
+// best distance found (the input has no duplicates here)
 double closest_pair(const std::vector<Pt>& p, int n) {
   double lo_x = p[0].x, hi_x = p[0].x, lo_y = p[0].y, hi_y = p[0].y;
   for (int i = 0; i < n; ++i) {
@@ -85,32 +87,56 @@ double closest_pair(const std::vector<Pt>& p, int n) {
   if (!(w > 0.0)) return 0.0;
   const int g = std::max(1, static_cast<int>(std::sqrt(static_cast<double>(n))));
   const double cell = w / g * (1.0 + 1e-9);
-  std::unordered_map<int64_t, std::vector<int>> grid;
-  auto key = [&](int64_t cx, int64_t cy) { return cx * 1000003 + cy; };
-  for (int i = 0; i < n; ++i)
-    grid[key(static_cast<int64_t>((p[i].x - lo_x) / cell), static_cast<int64_t>((p[i].y - lo_y) / cell))].push_back(i);
-  double best = std::numeric_limits<double>::infinity();
-  // exact closest pair: points in the same or neighbouring cells, widening
-  // the search ring until a ring beyond the best distance is reached
+  auto cxy = [&](const Pt& q, int& cx, int& cy) {
+    cx = std::min(g - 1, std::max(0, static_cast<int>((q.x - lo_x) / cell)));
+    cy = std::min(g - 1, std::max(0, static_cast<int>((q.y - lo_y) / cell)));
+  };
+  std::vector<int> start(static_cast<size_t>(g) * g + 1, 0), order(n), cell_of(n);
   for (int i = 0; i < n; ++i) {
-    const int64_t cx = static_cast<int64_t>((p[i].x - lo_x) / cell), cy = static_cast<int64_t>((p[i].y - lo_y) / cell);
-    for (int64_t rr = 1;; ++rr) {
-      for (int64_t dx = -rr; dx <= rr; ++dx)
-        for (int64_t dy = -rr; dy <= rr; ++dy) {
-          if (std::max(std::abs(dx), std::abs(dy)) != rr && rr > 1) continue;
-          const auto it = grid.find(key(cx + dx, cy + dy));
-          if (it == grid.end()) continue;
-          for (int j : it->second)
-            if (j != i) {
-              const double ddx = p[i].x - p[j].x, ddy = p[i].y - p[j].y;
-              best = std::min(best, std::sqrt(ddx * ddx + ddy * ddy));
-            }
+    int cx, cy;
+    cxy(p[i], cx, cy);
+    cell_of[i] = cy * g + cx;
+    ++start[cell_of[i] + 1];
+  }
+  for (size_t c = 1; c < start.size(); ++c) start[c] += start[c - 1];
+  {
+    std::vector<int> pos(start.begin(), start.end() - 1);
+    for (int i = 0; i < n; ++i) order[pos[cell_of[i]]++] = i;
+  }
+  double best2 = std::numeric_limits<double>::infinity();  // squared
+  for (int i = 0; i < n; ++i) {
+    int cx, cy;
+    cxy(p[i], cx, cy);
+    for (int rr = 1;; ++rr) {
+      for (int dy = -rr; dy <= rr; ++dy) {
+        const int y = cy + dy;
+        if (y < 0 || y >= g) continue;
+        for (int dx = -rr; dx <= rr; ++dx) {
+          if (rr > 1 && std::max(std::abs(dx), std::abs(dy)) != rr) continue;
+          const int x = cx + dx;
+          if (x < 0 || x >= g) continue;
+          const int c = y * g + x;
+          for (int k = start[c]; k < start[c + 1]; ++k) {
+            const int j = order[k];
+            if (j == i) continue;
+            const double ddx = p[i].x - p[j].x, ddy = p[i].y - p[j].y;
+            best2 = std::min(best2, ddx * ddx + ddy * ddy);
+          }
         }
-      if (best <= (rr - 1) * cell || rr > g + 1) break;
+      }
+      // every cell within rr of p's has been seen: an unseen point is more
+      // than rr cells' width away
+      if (best2 <= (rr * cell) * (rr * cell) || rr > g + 1) break;
     }
   }
-  return best;
+  return std::sqrt(best2);
 }
+
+// neighbour lists of the points (CSR): v's are nbr[off[v] .. off[v+1])
+struct Adjacency {
+  std::vector<int> off, nbr;
+  bool empty() const { return off.empty(); }
+};
 
 // Bowyer-Watson with adjacency.  Triangle t has vertices v[0..2] in the
 // reference's order and nb[k] = the triangle across edge (v[k], v[k+1]).
@@ -120,7 +146,7 @@ class Triangulation {
 
   // adjacency of the input points (empty when no triangle of real points
   // survives), verify.cpp:47-107
-  std::vector<std::vector<int>> run() {
+  Adjacency run() {
     if (n_ < 3) return {};
     double lo_x = pts_[0].x, hi_x = pts_[0].x, lo_y = pts_[0].y, hi_y = pts_[0].y;
     for (const Pt& p : pts_) {
@@ -136,6 +162,19 @@ class Triangulation {
     pts_.push_back({cx + 2.0 * r, cy - r});
     pts_.push_back({cx, cy + 2.0 * r});
     add_tri(n_, n_ + 1, n_ + 2);
+    // point location starts from a triangle created near the point (a
+    // coarse grid of the last triangle made in each cell): the insertion
+    // order is the matches' order, spatially random, and a walk from the
+    // previous insertion would cross O(sqrt n) triangles.  Only the walk's
+    // start changes, not the triangle it finds.
+    grid_n_ = std::max(1, static_cast<int>(std::sqrt(static_cast<double>(n_) / 2.0)));
+    grid_x0_ = lo_x;
+    grid_y0_ = lo_y;
+    grid_sx_ = grid_n_ / std::max(hi_x - lo_x, 1e-300);
+    grid_sy_ = grid_n_ / std::max(hi_y - lo_y, 1e-300);
+    grid_.assign(static_cast<size_t>(grid_n_) * grid_n_, -1);
+    vert_tri_.assign(n_ + 3, -1);
+    vert_tri_[n_] = vert_tri_[n_ + 1] = vert_tri_[n_ + 2] = 0;
     // ill-conditioned input (the closest pair more than kMaxSpread times
     // smaller than the extent): the in-circle decisions near the super
     // triangle are dominated by rounding, the bad set need not be a connected
@@ -143,26 +182,46 @@ class Triangulation {
     exact_ = closest_pair(pts_, n_) * kMaxSpread < extent;
     for (int i = 0; i < n_; ++i) insert(i);
 
-    std::vector<std::vector<int>> adj(n_);
+    // the edge graph of the triangles of real points, as sorted, unique
+    // neighbour lists (CSR)
+    Adjacency adj;
+    adj.off.assign(n_ + 1, 0);
     bool any_real = false;
-    auto add = [&](int a, int b, int c) {
-      if (a >= n_ || b >= n_ || c >= n_) return;
-      any_real = true;
-      adj[a].push_back(b);
-      adj[a].push_back(c);
-      adj[b].push_back(a);
-      adj[b].push_back(c);
-      adj[c].push_back(a);
-      adj[c].push_back(b);
+    auto each = [&](auto&& f) {
+      for (const Tri& t : tris_)
+        if (t.alive && t.v[0] < n_ && t.v[1] < n_ && t.v[2] < n_) f(t.v[0], t.v[1], t.v[2]);
+      for (const V3& t : soup_)
+        if (t.a < n_ && t.b < n_ && t.c < n_) f(t.a, t.b, t.c);
     };
-    for (const Tri& t : tris_)
-      if (t.alive) add(t.v[0], t.v[1], t.v[2]);
-    for (const V3& t : soup_) add(t.a, t.b, t.c);
+    each([&](int a, int b, int c) {
+      any_real = true;
+      adj.off[a + 1] += 2;
+      adj.off[b + 1] += 2;
+      adj.off[c + 1] += 2;
+    });
     if (!any_real) return {};
-    for (auto& l : adj) {
-      std::sort(l.begin(), l.end());
-      l.erase(std::unique(l.begin(), l.end()), l.end());
+    for (int v = 0; v < n_; ++v) adj.off[v + 1] += adj.off[v];
+    adj.nbr.resize(adj.off[n_]);
+    std::vector<int> fill(adj.off.begin(), adj.off.end() - 1);
+    each([&](int a, int b, int c) {
+      adj.nbr[fill[a]++] = b;
+      adj.nbr[fill[a]++] = c;
+      adj.nbr[fill[b]++] = a;
+      adj.nbr[fill[b]++] = c;
+      adj.nbr[fill[c]++] = a;
+      adj.nbr[fill[c]++] = b;
+    });
+    int w = 0;
+    for (int v = 0; v < n_; ++v) {
+      int* b = adj.nbr.data() + adj.off[v];
+      int* e = adj.nbr.data() + adj.off[v + 1];
+      std::sort(b, e);
+      e = std::unique(b, e);
+      adj.off[v] = w;
+      for (int* q = b; q < e; ++q) adj.nbr[w++] = *q;
     }
+    adj.off[n_] = w;
+    adj.nbr.resize(w);
     return adj;
   }
 
@@ -178,7 +237,9 @@ class Triangulation {
   int add_tri(int a, int b, int c) {
     if (orient2d(pts_[a], pts_[b], pts_[c]) < 0.0) std::swap(b, c);
     tris_.push_back(Tri{{a, b, c}, {-1, -1, -1}, true, -1});
-    return static_cast<int>(tris_.size()) - 1;
+    const int t = static_cast<int>(tris_.size()) - 1;
+    if (!vert_tri_.empty()) vert_tri_[a] = vert_tri_[b] = vert_tri_[c] = t;
+    return t;
   }
 
   bool bad(int t, int i) {
@@ -188,9 +249,41 @@ class Triangulation {
 
   // a live triangle containing point i (or -1): walk from the last created
   // triangle, crossing an edge that has the point strictly on its outer side
+  int cell_of(const Pt& p) const {
+    const double top = grid_n_ - 1;
+    double fx = (p.x - grid_x0_) * grid_sx_, fy = (p.y - grid_y0_) * grid_sy_;
+    fx = fx >= 0.0 ? std::min(fx, top) : 0.0;  // also NaN -> 0
+    fy = fy >= 0.0 ? std::min(fy, top) : 0.0;
+    return static_cast<int>(fy) * grid_n_ + static_cast<int>(fx);
+  }
+
+  // a live triangle to start the walk for point p: one incident to an
+  // already inserted vertex in p's cell or the nearest non-empty ring of
+  // cells around it (every inserted vertex keeps a live incident triangle:
+  // a cavity's vertices all lie on its boundary and get new triangles)
+  int walk_start(const Pt& p) const {
+    if (grid_.empty()) return last_;
+    const int c = cell_of(p), cx = c % grid_n_, cy = c / grid_n_;
+    for (int rr = 0; rr < grid_n_; ++rr) {
+      for (int dy = -rr; dy <= rr; ++dy) {
+        const int y = cy + dy;
+        if (y < 0 || y >= grid_n_) continue;
+        for (int dx = -rr; dx <= rr; ++dx) {
+          if (std::max(std::abs(dx), std::abs(dy)) != rr) continue;
+          const int x = cx + dx;
+          if (x < 0 || x >= grid_n_) continue;
+          const int v = grid_[y * grid_n_ + x];
+          if (v >= 0 && vert_tri_[v] >= 0 && tris_[vert_tri_[v]].alive) return vert_tri_[v];
+        }
+      }
+      if (rr >= 3) break;  // sparse early insertions: the last triangle made
+    }
+    return last_;
+  }
+
   int locate(int i) {
-    int t = last_;
     const Pt& p = pts_[i];
+    int t = walk_start(p);
     for (int steps = 0; steps < 4 * static_cast<int>(tris_.size()) + 16; ++steps) {
       const Tri& T = tris_[t];
       // the triangle's own winding (make_ccw leaves collinear triples as given)
@@ -319,17 +412,19 @@ class Triangulation {
           }
         } else {
           const int other = a == i ? b : a;  // the edge (other, i)
-          const auto it = spoke_.find(other);
-          if (it == spoke_.end()) {
-            spoke_.emplace(other, std::make_pair(t, k));
+          size_t f = 0;
+          while (f < spoke_.size() && spoke_[f].v != other) ++f;
+          if (f == spoke_.size()) {
+            spoke_.push_back({other, t, k});
           } else {
-            T.nb[k] = it->second.first;
-            tris_[it->second.first].nb[it->second.second] = t;
+            T.nb[k] = spoke_[f].t;
+            tris_[spoke_[f].t].nb[spoke_[f].k] = t;
           }
         }
       }
       last_ = t;
     }
+    if (!grid_.empty()) grid_[cell_of(pts_[i])] = i;
     return true;
   }
 
@@ -343,7 +438,14 @@ class Triangulation {
   std::vector<uint64_t> keys_;
   bool exact_ = false;
   std::vector<EdgeRec> edges_;
-  std::unordered_map<int, std::pair<int, int>> spoke_;
+  struct Spoke {
+    int v, t, k;  // edge (v, new point) of triangle t, its index k
+  };
+  std::vector<Spoke> spoke_;  // the cavity's new spokes (a handful per insertion)
+  std::vector<int> grid_;     // per cell: the last vertex inserted there
+  std::vector<int> vert_tri_; // per vertex: a live incident triangle
+  int grid_n_ = 0;
+  double grid_x0_ = 0, grid_y0_ = 0, grid_sx_ = 0, grid_sy_ = 0;
   int n_;
   std::vector<Pt> pts_;
   std::vector<Tri> tris_;
@@ -384,7 +486,7 @@ std::vector<std::vector<int>> delaunay_knn(const std::vector<Pt>& pts, int k, bo
     for (int i = 0; i + 1 < n; ++i)
       if (pts[order[i]].x == pts[order[i + 1]].x && pts[order[i]].y == pts[order[i + 1]].y) dup = true;
   }
-  std::vector<std::vector<int>> adj;
+  Adjacency adj;
   if (!dup) adj = Triangulation(pts).run();
   if (adj.empty()) {
     *fallback = true;
@@ -399,22 +501,24 @@ std::vector<std::vector<int>> delaunay_knn(const std::vector<Pt>& pts, int k, bo
     }
     return out;
   }
-  std::vector<int> visited(n, -1);
+  std::vector<int> visited(n, -1), frontier, ring;
   for (int i = 0; i < n; ++i) {
     std::vector<int>& res = out[i];
     visited[i] = i;
-    std::vector<int> frontier = {i};
+    frontier.assign(1, i);
     while (static_cast<int>(res.size()) < k && !frontier.empty()) {
-      std::vector<int> ring;
+      ring.clear();
       for (int u : frontier)
-        for (int v : adj[u])
+        for (int e = adj.off[u]; e < adj.off[u + 1]; ++e) {
+          const int v = adj.nbr[e];
           if (visited[v] != i) {
             visited[v] = i;
             ring.push_back(v);
           }
+        }
       by_distance(pts[i], pts, ring);
       res.insert(res.end(), ring.begin(), ring.end());
-      frontier = std::move(ring);
+      frontier.swap(ring);
     }
     if (static_cast<int>(res.size()) > k) res.resize(k);
     if (static_cast<int>(res.size()) < k) {
@@ -462,14 +566,30 @@ int cyclic_edit(const std::vector<int>& a, const std::vector<int>& b) {
   if (b.empty()) return static_cast<int>(a.size());
   if (a.empty()) return static_cast<int>(b.size());
   const size_t na = a.size(), nb = b.size();
-  std::vector<int> prev(nb + 1), cur(nb + 1);
+  // rows of the DP on the stack for the usual ring sizes (n_neighbors = 6);
+  // b doubled so a rotation is a window (no modulo in the inner loop)
+  constexpr size_t kSmall = 32;
+  int prev_s[kSmall + 1], cur_s[kSmall + 1], bb_s[2 * kSmall];
+  std::vector<int> prev_v, cur_v, bb_v;
+  int *prev = prev_s, *cur = cur_s, *bb = bb_s;
+  if (nb > kSmall) {
+    prev_v.resize(nb + 1);
+    cur_v.resize(nb + 1);
+    bb_v.resize(2 * nb);
+    prev = prev_v.data();
+    cur = cur_v.data();
+    bb = bb_v.data();
+  }
+  for (size_t j = 0; j < nb; ++j) bb[j] = bb[j + nb] = b[j];
   int best = std::numeric_limits<int>::max();
   for (size_t rot = 0; rot < nb; ++rot) {
+    const int* br = bb + rot;
     for (size_t j = 0; j <= nb; ++j) prev[j] = static_cast<int>(j);
     for (size_t i = 1; i <= na; ++i) {
       cur[0] = static_cast<int>(i);
+      const int ai = a[i - 1];
       for (size_t j = 1; j <= nb; ++j) {
-        const int sub = prev[j - 1] + (a[i - 1] == b[(rot + j - 1) % nb] ? 0 : 1);
+        const int sub = prev[j - 1] + (ai == br[j - 1] ? 0 : 1);
         cur[j] = std::min({prev[j] + 1, cur[j - 1] + 1, sub});
       }
       std::swap(prev, cur);
