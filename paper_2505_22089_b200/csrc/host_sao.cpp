@@ -161,6 +161,7 @@ class Triangulation {
     pts_.push_back({cx - 2.0 * r, cy - r});
     pts_.push_back({cx + 2.0 * r, cy - r});
     pts_.push_back({cx, cy + 2.0 * r});
+    tris_.reserve(static_cast<size_t>(8) * n_ + 16);
     add_tri(n_, n_ + 1, n_ + 2);
     // point location starts from a triangle created near the point (a
     // coarse grid of the last triangle made in each cell): the insertion
