@@ -25,7 +25,7 @@
 // DeviceBackend hooks (engine.hpp:98-104), so its counters, CapacityExceeded
 // and NotResident behave exactly as in the reference.  With
 // opts.verify.enabled the initial matches are verified on host threads with
-// the reference's sao_filter + ransac_fundamental, as VerifyPool does
+// sao_filter (libbmg's native SAO, bit-equal) + the reference's ransac_fundamental, as VerifyPool does
 // (engine.cpp:326-377), WHILE the GPU matches later rows: each block row's
 // pairs arrive through the executor's on_pair hand-off as soon as that row's
 // matches are in host memory and go into a bounded queue (backpressure as in
@@ -139,6 +139,37 @@ inline bandmatch::PairMatches match_pair(Context& ctx, const bandmatch::FeatureS
   return pm;
 }
 
+// sao_filter (verify.hpp:53-54, verify.cpp:303-341) on libbmg's native SAO
+// (bmg_sao_filter: the reference's triangulation and rings, adjacency-driven
+// instead of the all-triangle Bowyer-Watson), the reference's outcome type.
+inline bandmatch::SaoOutcome sao_filter(const bandmatch::PairMatches& in,
+                                        const std::vector<bandmatch::Keypoint>& query_kps,
+                                        const std::vector<bandmatch::Keypoint>& train_kps,
+                                        const bandmatch::SaoParams& params) {
+  static_assert(sizeof(bandmatch::Keypoint) == 4 * sizeof(float), "Keypoint must be float[4]");
+  const std::size_t m = in.matches.size();
+  std::vector<std::int32_t> flat(2 * std::max<std::size_t>(m, 1));
+  for (std::size_t i = 0; i < m; ++i) {
+    flat[2 * i] = static_cast<std::int32_t>(in.matches[i].first);
+    flat[2 * i + 1] = static_cast<std::int32_t>(in.matches[i].second);
+  }
+  std::vector<std::uint8_t> keep(std::max<std::size_t>(m, 1));
+  bandmatch::SaoOutcome out;
+  out.scores.assign(m, 0.0);
+  std::uint32_t flags = 0;
+  check(bmg_sao_filter(flat.data(), m, query_kps.empty() ? nullptr : &query_kps[0].x, query_kps.size(),
+                       train_kps.empty() ? nullptr : &train_kps[0].x, train_kps.size(), params.n_neighbors,
+                       params.score_threshold, keep.data(), out.scores.data(), &flags));
+  out.passthrough = (flags & BMG_SAO_PASSTHROUGH) != 0;
+  out.delaunay_fallback = (flags & BMG_SAO_DELAUNAY_FALLBACK) != 0;
+  out.kept.query_image = in.query_image;
+  out.kept.train_image = in.train_image;
+  out.kept.stage = in.stage;
+  for (std::size_t i = 0; i < m; ++i)
+    if (keep[i]) out.kept.matches.push_back(in.matches[i]);
+  return out;
+}
+
 namespace detail {
 
 struct Hooks {
@@ -237,7 +268,7 @@ class Verifier {
     oc.pair = IdPair(in.query_image, in.train_image);
     oc.initial = in.matches.size();
     try {
-      const SaoOutcome sao = sao_filter(in, qf.keypoints, tf.keypoints, opts_.verify.sao);
+      const SaoOutcome sao = bandmatch_b200::sao_filter(in, qf.keypoints, tf.keypoints, opts_.verify.sao);
       oc.after_sao = sao.kept.matches.size();
       oc.sao_passthrough = sao.passthrough;
       oc.delaunay_fallback = sao.delaunay_fallback;

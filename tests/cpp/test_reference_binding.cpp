@@ -78,6 +78,25 @@ int main() {
   for (const IdPair& p : g.pairs()) processed &= marked.pair_state(p) == PairState::kProcessed;
   report(processed, "view graph pairs marked processed");
 
+  // sao_filter (verify.cpp:303-341) on libbmg's native SAO, every matched
+  // pair, against the reference's own
+  {
+    bool eq = true;
+    std::size_t n_checked = 0;
+    for (const PairMatches& pm : ref.matches) {
+      const FeatureSet& qf = feats.at(pm.query_image);
+      const FeatureSet& tf = feats.at(pm.train_image);
+      const SaoParams sp;
+      const SaoOutcome r = sao_filter(pm, qf.keypoints, tf.keypoints, sp);
+      const SaoOutcome gq = bandmatch_b200::sao_filter(pm, qf.keypoints, tf.keypoints, sp);
+      eq &= r.kept.matches == gq.kept.matches && r.scores == gq.scores && r.passthrough == gq.passthrough &&
+            r.delaunay_fallback == gq.delaunay_fallback && r.kept.query_image == gq.kept.query_image &&
+            r.kept.train_image == gq.kept.train_image && r.kept.stage == gq.kept.stage;
+      ++n_checked;
+    }
+    report(eq && n_checked > 0, "sao_filter on the native SAO equals the reference's, every matched pair");
+  }
+
   // compute_codes / match_pair through the binding
   std::array<float, kDescriptorDim> mean{};
   for (int c = 0; c < kDescriptorDim; ++c) mean[c] = 0.001f * static_cast<float>(c % 7);
