@@ -1896,16 +1896,28 @@ __global__ void __launch_bounds__(NT, (KM == 8 ? BMG_MATCH_MINB : 1)) match_kern
       // key below the last pull (it may be missing from the lists; a dropped
       // copy of a listed key also counts): then the query reruns on the
       // exact path below.
+      // the pulls are warp-uniform: lane r < 8 takes pull r through a
+      // 3-level select on its lane bits (7 SEL) instead of a compare and
+      // select per pull
+      uint32_t mv[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
+        mv[r] = kEmpty;
         if (r < K) {
           m = __reduce_min_sync(kFull, kl[0]);
-          lst = lane == r ? m : lst;
+          mv[r] = m;
           const bool pop = kl[0] == m;
 #pragma unroll
           for (int i = 0; i + 1 < kLaneKeys; ++i) kl[i] = pop ? kl[i + 1] : kl[i];
           kl[kLaneKeys - 1] = pop ? kEmpty : kl[kLaneKeys - 1];
         }
+      }
+      {
+        const bool b0 = (lane & 1) != 0, b1 = (lane & 2) != 0, b2 = (lane & 4) != 0;
+        const uint32_t x0 = b0 ? mv[1] : mv[0], x1 = b0 ? mv[3] : mv[2];
+        const uint32_t x2 = b0 ? mv[5] : mv[4], x3 = b0 ? mv[7] : mv[6];
+        const uint32_t y0 = b1 ? x1 : x0, y1 = b1 ? x3 : x2;
+        lst = lane < 8 ? (b2 ? y1 : y0) : kEmpty;
       }
       exact = __any_sync(kFull, dmin < m) || (a.test_flags & kTestForceExactWalk) != 0;
     }
