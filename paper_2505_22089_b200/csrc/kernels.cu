@@ -1579,6 +1579,7 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
   const uint32_t cend_s = lane < L ? cend : kEmpty;  // past the tables: never <= k
   const uint32_t sbase = (uint32_t)lane * T.ns + lo;
   const uint32_t sentinel = T.ns - kSentinel;  // all-pad chunk of table 0
+  const uint32_t kmul = 1u << ib;
   for (uint32_t pg = 0; pg < n_chunks; pg += 32) {
     // lane j describes chunk pg + j: table = #tables ending at or before it
     // (binary search over the nondecreasing chunk ends, one shuffle a step)
@@ -1613,7 +1614,16 @@ __device__ __forceinline__ void walk_union(const ImgDev& T, int L, uint32_t lo, 
       uint32_t jn;
       uint64_t cn[FWP];
       fetch(4 * (int)(r + kWalkDepth) + grp, jn, cn);
-      round((hamming<FWP>(qc, cr[0]) << ib) | jr[0]);
+      {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int x = 0; x < FWP; ++x) {
+          const uint64_t d = qc[x] ^ cr[0][x];
+          acc = __popc((uint32_t)d) * kmul + acc;
+          acc = __popc((uint32_t)(d >> 32)) * kmul + acc;
+        }
+        round(acc | jr[0]);
+      }
 #pragma unroll
       for (int d = 0; d + 1 < kWalkDepth; ++d) {
         jr[d] = jr[d + 1];
@@ -1863,15 +1873,18 @@ __global__ void __launch_bounds__(NT, (KM == 8 ? BMG_MATCH_MINB : 1)) match_kern
     if constexpr (KM == 8) {
       // Each lane keeps its kLaneKeys smallest keys sorted in kl[]; dmin is
       // the smallest key that fell off the list.
-      uint32_t kl[kLaneKeys], dmin = kEmpty;
+      uint32_t kl[kLaneKeys];
 #pragma unroll
       for (int i = 0; i < kLaneKeys; ++i) kl[i] = kEmpty;
       walk_union<FWP>(T, L, lo, sz, ib, qc, [&](uint32_t key) {
-        dmin = min(dmin, max(kl[kLaneKeys - 1], key));
 #pragma unroll
         for (int i = kLaneKeys - 1; i > 0; --i) kl[i] = max(kl[i - 1], min(kl[i], key));
         kl[0] = min(kl[0], key);
       });
+      // a lane that dropped a key x kept 4 keys <= x; if x is below the last
+      // pull, all 4 are pulled too, so the lane ends empty: a full lane that
+      // ends empty reruns the query exactly (a superset of the harmful drops)
+      const bool full = kl[kLaneKeys - 1] != kEmpty;
       uint32_t m = kEmpty;
       // Copies of one key that landed in one lane sit next to each other:
       // squeeze them out so a lane's list is a prefix of its distinct keys.
@@ -1919,7 +1932,7 @@ __global__ void __launch_bounds__(NT, (KM == 8 ? BMG_MATCH_MINB : 1)) match_kern
         const uint32_t y0 = b1 ? x1 : x0, y1 = b1 ? x3 : x2;
         lst = lane < 8 ? (b2 ? y1 : y0) : kEmpty;
       }
-      exact = __any_sync(kFull, dmin < m) || (a.test_flags & kTestForceExactWalk) != 0;
+      exact = __any_sync(kFull, full && kl[0] == kEmpty) || (a.test_flags & kTestForceExactWalk) != 0;
     }
     if (exact) {
       // ---- exact path: keys below the current K-th key are pulled out in
