@@ -592,6 +592,26 @@ def retrieval_leg(bm, m, feats, cores, cpu=True, cpu_images=32):
         out["cpu_baseline"] = {"value": k / dt, "unit": "images/s", "cores": cores, "kind": "reference",
                                "sample": f"first {k} images"}
         out["parity"] = "equal" if eq else "DIFFERENT"
+    # train_codebook (retrieval.cpp:56-158) on a training pool drawn from the
+    # images (every 100th descriptor), k_words 64, up to 10 Lloyd iterations:
+    # the device against the reference's single-threaded loops
+    pool_tc = np.ascontiguousarray(np.concatenate([im[::100] for im in imgs]), np.float32)
+    bm.train_codebook(pool_tc[:4096], 64, 2, 3, matcher=m)  # warm
+    t = time.perf_counter()
+    hist = []
+    cb_gpu = bm.train_codebook(pool_tc, 64, 10, 3, sse_history=hist, matcher=m)
+    t_gpu = time.perf_counter() - t
+    tc = {"pool": int(len(pool_tc)), "k_words": 64, "max_iters": 10, "iterations": len(hist),
+          "gpu_ms": t_gpu * 1e3}
+    if cpu:
+        t = time.perf_counter()
+        cent_ref, sse_ref = _reference().train_codebook(pool_tc, 64, 10, 3)
+        tc["reference_ms"] = (time.perf_counter() - t) * 1e3
+        tc["reference_threads"] = 1
+        tc["parity"] = ("equal" if np.array_equal(np.asarray(cb_gpu.centroids, np.float32).view(np.uint32),
+                                                  cent_ref.view(np.uint32))
+                        and np.array_equal(np.asarray(hist), sse_ref) else "DIFFERENT")
+    out["train_codebook"] = tc
     return out
 
 
