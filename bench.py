@@ -311,9 +311,14 @@ def sm_max_mhz():
         return 1965.0  # B200 boost clock (B200_PROFILING.md)
 
 
+# queries per match CTA (csrc/bmg_internal.h BMG_MATCH_QUERIES): scales the
+# committed ncu capture's per-CTA figures to this run's launches
+MATCH_QUERIES_PER_CTA = 2048
+
+
 def ncu_traffic(avg_ctas_per_launch):
     """DRAM bytes of one match launch from the committed `ncu --set full`
-    capture, scaled by CTA count (one CTA = 1,024 queries of one pair) from
+    capture, scaled by CTA count (one CTA = 2,048 queries of one pair) from
     the captured launch to this run's average launch (ncu: cold L2,
     serialised)."""
     try:
@@ -849,7 +854,7 @@ def main():
             for blk in row.blocks:
                 for a_, b_ in blk.pairs:
                     pair_bytes += feats[a_].descriptors.nbytes + feats[b_].descriptors.nbytes
-                    step_ctas += -(-len(feats[a_].descriptors) // 1024)
+                    step_ctas += -(-len(feats[a_].descriptors) // MATCH_QUERIES_PER_CTA)
     per_launch_bytes = pair_bytes * args.steps / max(match_n, 1)
     avg_launch_s = match_ms * 1e-3 / max(match_n, 1)
     peak, peak_src = peaks()

@@ -164,7 +164,7 @@ constexpr int kPlaneChunk = 180;  // planes per codes CTA: 15 warps x 12 (grid.y
 #endif
 constexpr int kMatchThreads = BMG_MATCH_THREADS;  // one query per warp at a time
 #ifndef BMG_MATCH_QUERIES
-#define BMG_MATCH_QUERIES 1024
+#define BMG_MATCH_QUERIES 2048
 #endif
 constexpr int kMatchQueries = BMG_MATCH_QUERIES;  // queries per match CTA
 // queries per CTA of the match kernel launch_match picks for (fwp, k)
