@@ -887,7 +887,9 @@ def main():
         peak = 4.0 * sms * float(mhz) * 1e6
         return {"achieved": achieved, "peak": peak, "unit": "warp inst/s", "frac": achieved / peak,
                 "note": "warp instructions per CTA from profiles/ncu_summary.json (ncu smsp__inst_executed) x CTAs "
-                        "per launch / launch time, vs 4 issue slots per SM per cycle at the sampled SM clock"}
+                        "per launch / launch time, vs 4 issue slots per SM per cycle at the sampled SM clock; the "
+                        "capture is of strip500 (8,192 descriptors): configs with other descriptor counts run "
+                        "more or fewer instructions per CTA, so their figure is only indicative"}
 
     line = None
     if rank == 0:
