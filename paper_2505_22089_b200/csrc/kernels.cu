@@ -1503,15 +1503,17 @@ __global__ void tables_scatter_kernel(HashDev h, const ImgDev* __restrict__ imgs
 //      lane (32 per page) and fetched per round with one shuffle; loads run
 //      two rounds ahead;
 //   2. per candidate: 128-bit Hamming via POPC and the unique key
-//      (hamming << idx_bits | train_idx).  Each lane keeps its kLaneKeys (4)
-//      smallest keys (branch-free sorted insert); the warp then pulls the K smallest
-//      out of the lanes' lists with the single-instruction warp min (REDUX).
-//      Equal keys are the same train index reached from several tables and
-//      are taken once -- the reference's last_seen dedup + stable counting
-//      sort by (hamming, idx) (:160-200).  Each lane also keeps the
-//      smallest key that fell off its list; if one lies below the last
-//      pull, the query reruns on the exact path (sorted list over lanes
-//      0..KM-1, REDUX-driven insertion);
+//      (hamming << idx_bits | train_idx; the shift folded into IMADs).  Each
+//      lane keeps its kLaneKeys (4) smallest keys (branch-free sorted
+//      insert); the warp then pulls the K smallest out of the lanes' lists
+//      with the single-instruction warp min (REDUX), lanes 0..7 taking the
+//      pulls by a select on their lane bits.  Equal keys are the same train
+//      index reached from several tables and are taken once -- the
+//      reference's last_seen dedup + stable counting sort by (hamming, idx)
+//      (:160-200).  A lane that dropped a key below the K-th pull kept 4
+//      smaller keys, all of which the pulls take: a full lane that ends the
+//      pulls empty sends the query to the exact path (sorted list over lanes
+//      0..KM-1, REDUX-driven insertion; ~0.17% of queries);
 //   3. re-rank (:196-208): lanes 4c..4c+3 hold candidate c; FP32 squared
 //      distances (packed FFMA2) with a certified relative error <= 1e-5
 //      decide the (dist, idx) argmin and the ratio test; uncertified queries
@@ -1871,8 +1873,7 @@ __global__ void __launch_bounds__(NT, (KM == 8 ? BMG_MATCH_MINB : 1)) match_kern
     uint32_t lst = kEmpty;
     bool exact = KM != 8;
     if constexpr (KM == 8) {
-      // Each lane keeps its kLaneKeys smallest keys sorted in kl[]; dmin is
-      // the smallest key that fell off the list.
+      // Each lane keeps its kLaneKeys smallest keys sorted in kl[].
       uint32_t kl[kLaneKeys];
 #pragma unroll
       for (int i = 0; i < kLaneKeys; ++i) kl[i] = kEmpty;
